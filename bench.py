@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: simulated cells/s on BASELINE config 1 (the headline workload).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): TI 500x500 3-facies (channels + levee
+lenses, synth.config1_ti), SG 1000x1000, T=64, OV=16, J=2, K=5 top-k random
+pick, unconditional, 100 realizations per GPU (weak scaling: rank r simulates
+realizations r*100 .. r*100+99 with seeds mix64(master, index + 1)).
+
+A step = one batched simulation of those 100 realizations.
+  value : cells/s with the TI pyramid resident in HBM and realizations left in
+          HBM (ccw_simulate_device); per-step CUDA events on the library's
+          stream, L2 flushed (256 MiB write) before every timed step.
+  e2e   : the same metric through the public C-ABI call with host buffers:
+          ccw_ti_create from host bytes (H2D + pyramid) + ccw_simulate into
+          pinned host memory (D2H of every realization), wall clock per step.
+Rank 0 prints one JSON line.  --impl reference times the reference's own CPU
+implementation (oracle/_ref: the unmodified reference headers) on the host
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated cells/s"
+UNIT = "cells/s"
+REAL_PER_GPU = 100
+MASTER = 20240441
+WORKLOAD = ("config1: TI 500x500 3-facies, SG 1000x1000, T64 OV16 J2 K5 random top-k pick, "
+            f"{REAL_PER_GPU} realizations per GPU")
+
+
+def cfg1():
+    from paper_2404_00441_b200 import ccwsim as cs
+    return cs.SimConfig(sg_height=1000, sg_width=1000, template_size=64, overlap=16, dwt_level=2,
+                        candidates=5, n_realizations=REAL_PER_GPU, master_seed=MASTER)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ccf_traffic.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path))
+        except Exception:
+            return None
+    return None
+
+
+def cpu_reference_rate(ti, nf, cfg, n_real, workers):
+    """cells/s of the compiled reference (oracle/_ref) on n_real realizations."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    impl, kind = (pyoracle.reference(), "reference") if pyoracle.reference_available() else \
+        (pyoracle.restatement(), "port")
+    c = pyoracle.Cfg(sg_height=cfg.sg_height, sg_width=cfg.sg_width,
+                     template_size=cfg.template_size, overlap=cfg.overlap,
+                     dwt_level=cfg.dwt_level, candidates=cfg.candidates,
+                     n_realizations=n_real, master_seed=cfg.master_seed)
+    t0 = time.perf_counter()
+    impl.simulate_ensemble(ti, nf, c, None, workers=workers)
+    dt = time.perf_counter() - t0
+    return n_real * cfg.sg_height * cfg.sg_width / dt, dt, kind
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2404_00441_b200 import synth
+    ti = synth.config1_ti()
+    cfg = cfg1()
+    cores = os.cpu_count() or 1
+    sample = max(cores, 4)  # one realization per host thread per step
+    for _ in range(args.warmup):
+        cpu_reference_rate(ti, 3, cfg, min(sample, 4), cores)
+    rates, times = [], []
+    kind = "reference"
+    for _ in range(args.steps):
+        r, dt, kind = cpu_reference_rate(ti, 3, cfg, sample, cores)
+        rates.append(r)
+        times.append(dt)
+    value = statistics.median(rates)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_realizations_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"{sample} config-1 realizations per step, "
+                                       f"simulate_ensemble(workers={cores})"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2404_00441_b200 import _abi, ccwsim as cs, synth
+
+    lib = _abi.lib()
+    dev = cs.Device(local)
+    stream = torch.cuda.ExternalStream(dev.stream_ptr, device=torch.device("cuda", local))
+    ti_a = synth.config1_ti()
+    nf = 3
+    cfg = cfg1()
+    grid = cs.CategoricalGrid(500, 500, nf, ti_a)
+    tih = cs.TrainingImage(grid, cfg.dwt_level, "indicator", dev)
+    base = rank * REAL_PER_GPU
+    seeds = np.array([cs.mix64(MASTER, base + r + 1) for r in range(REAL_PER_GPU)], np.uint64)
+    c = cfg.to_c()
+    sg = cfg.sg_height * cfg.sg_width
+    d_out = torch.empty(REAL_PER_GPU * sg, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    diags = (_abi.DiagC * REAL_PER_GPU)()
+
+    def step_device():
+        dev.check(lib.ccw_simulate_device(dev.handle, tih.handle, C.byref(c),
+                                          seeds.ctypes.data_as(_abi.U64P), REAL_PER_GPU, None, 0,
+                                          C.c_void_p(d_out.data_ptr()), diags))
+
+    # warm-up
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    # device-resident timed region
+    sampler = ClockSampler(local)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the events
+            evs[k][0].record(stream)
+        step_device()
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    timing = dev.last_timing()
+    launches_per_step = int(timing["launches"])
+    cells = world * REAL_PER_GPU * sg * args.steps
+    value = cells / (total_ms * 1e-3)
+
+    # profiling pass (separate from the timed region): per-launch CCF time
+    dev.set_profiling(True)
+    step_device()
+    prof = dev.last_timing()
+    dev.set_profiling(False)
+    ccf_avg_ms = prof["ccf_ms"] / max(prof["ccf_launches"], 1)
+    flop_per_launch = prof["ccf_flop"] / max(prof["ccf_launches"], 1)
+    peak = dev.measure_fp32_peak()
+    achieved = flop_per_launch / (ccf_avg_ms * 1e-3) / 1e12
+    traffic = load_traffic()
+
+    # end-to-end through the public API with host buffers
+    h_out = torch.empty(REAL_PER_GPU * sg, dtype=torch.uint8).pin_memory()
+    ti_host = np.ascontiguousarray(ti_a)
+
+    def step_e2e():
+        h = C.c_void_p()
+        dev.check(lib.ccw_ti_create(dev.handle, ti_host.ctypes.data_as(_abi.U8P), 500, 500, nf,
+                                    cfg.dwt_level, 0, C.byref(h)))
+        dev.check(lib.ccw_simulate(dev.handle, h, C.byref(c), seeds.ctypes.data_as(_abi.U64P),
+                                   REAL_PER_GPU, None, 0,
+                                   C.cast(C.c_void_p(h_out.data_ptr()), _abi.U8P), diags, None))
+        lib.ccw_ti_destroy(h)
+
+    step_e2e()
+    e2e_times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_e2e()
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = cells / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cores = os.cpu_count() or 1
+        n = max(cores, 4)
+        rate, dt, kind = cpu_reference_rate(ti_a, nf, cfg, n, cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{n} config-1 realizations, simulate_ensemble(workers={cores}), "
+                         f"{dt:.1f} s wall"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32(exact-int)+f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "realizations_per_gpu": REAL_PER_GPU,
+                       "parallelism": f"realization shards x{world}",
+                       "l2": "flushed before each timed step (256 MiB write, outside events)",
+                       "timing": "per-step CUDA events on the library stream, max over ranks"},
+            "roofline": {"bound": "fp32", "kernel": "ccf_direct_kernel",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None,
+                         "peak_source": "in-run FFMA microbenchmark (MEASURED_PEAKS.json has no "
+                                        "FP32 figure)",
+                         "flop_per_launch": flop_per_launch, "avg_launch_ms": ccf_avg_ms,
+                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "ccf_share_of_step": prof["ccf_ms"] / prof["total_ms"] if prof["total_ms"] else None,
+                         "select_share_of_step": prof["select_ms"] / prof["total_ms"] if prof["total_ms"] else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(ti_host.nbytes + seeds.nbytes),
+                    "d2h_bytes_per_step": int(REAL_PER_GPU * sg)},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

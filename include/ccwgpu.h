@@ -1,0 +1,222 @@
+/*
+ * ccwgpu.h -- C-ABI of the B200-native CCWSIM hot path (libccwgpu.so).
+ *
+ * This is the drop-in boundary.  The reference (/root/reference/proj) is a
+ * header-only C++20 library with no FFI layer; its public entry points for
+ * the hot path are the inline functions listed beside each declaration.  A
+ * maintainer binds the reference-facing C++ API to these symbols through the
+ * shim in include/ccwsim_gpu.hpp; Python binds them with
+ * ctypes (paper_2404_00441_b200/_abi.py).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross the ABI.
+ *  - Every function returns a ccw_status.  0 = ok; 1-7 mirror the reference
+ *    exception classes (errors.hpp:9-72); >= 100 are CUDA errors.  The message
+ *    (same text as the reference's exception where one exists) is available
+ *    from ccw_last_error(ctx) -- or ccw_last_error(NULL) for failures that
+ *    happen before a context exists.
+ *  - Host buffers are caller-owned and sized from the arguments.  Device
+ *    memory is owned by the context and the TI handle.
+ *  - A context binds one GPU and one CUDA stream and is not thread-safe; use
+ *    one context per host thread (one per GPU / rank).
+ *  - All computation runs on the GPU.  There is no CPU fallback: if the
+ *    device cannot be initialised every call returns CCW_ERR_CUDA.
+ */
+#ifndef CCWGPU_H
+#define CCWGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CCW_API __attribute__((visibility("default")))
+#else
+#define CCW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int ccw_status;
+enum {
+    CCW_OK = 0,
+    CCW_ERR_BOUNDS = 1,     /* ccwsim::BoundsError      (errors.hpp:15) */
+    CCW_ERR_DIMENSION = 2,  /* ccwsim::DimensionError   (errors.hpp:21) */
+    CCW_ERR_STRUCTURE = 3,  /* ccwsim::StructureError   (errors.hpp:27) */
+    CCW_ERR_CONFIG = 4,     /* ccwsim::ConfigError      (errors.hpp:33) */
+    CCW_ERR_EMPTY = 5,      /* ccwsim::EmptyInputError  (errors.hpp:38) */
+    CCW_ERR_IO = 6,         /* ccwsim::IoError          (errors.hpp:50) */
+    CCW_ERR_GENERIC = 7,    /* ccwsim::Error            (errors.hpp:9)  */
+    CCW_ERR_CUDA = 100
+};
+
+/* OrShape (simulator.hpp:87) and Corner (simulator.hpp:95) enum orders. */
+enum { CCW_OR_NONE = 0, CCW_OR_VERTICAL = 1, CCW_OR_HORIZONTAL = 2, CCW_OR_L = 3 };
+enum { CCW_TOP_LEFT = 0, CCW_TOP_RIGHT = 1, CCW_BOTTOM_LEFT = 2, CCW_BOTTOM_RIGHT = 3 };
+
+/* ccwsim::SimConfig (simulator.hpp:28-40) minus hard_data, which is passed
+ * separately as (row, col, facies) int32 triples. */
+typedef struct ccw_sim_config {
+    int32_t sg_height;
+    int32_t sg_width;
+    int32_t template_size;  /* T  */
+    int32_t overlap;        /* OV */
+    int32_t dwt_level;      /* J  */
+    int32_t candidates;     /* K  */
+    int32_t n_realizations;
+    int32_t scoring;        /* 0 raw, 1 normalized       (matcher.hpp:18)    */
+    int32_t facies_mode;    /* 0 indicator, 1 raw_codes  (simulator.hpp:25) */
+    int32_t min_cut;        /* 0 off, 1 on                                   */
+    uint64_t master_seed;
+} ccw_sim_config;
+
+/* ccwsim::SimDiagnostics (simulator.hpp:376-392). */
+typedef struct ccw_diag {
+    uint64_t seed;
+    int32_t origin;
+    int32_t column_major;
+    int32_t work_height;
+    int32_t work_width;
+    int32_t placement_count;
+    int32_t hard_data_count;
+    int32_t pre_overwrite_mismatches;
+    int32_t _pad;
+    double wall_seconds;  /* host wall time of the whole batched call */
+} ccw_diag;
+
+/* ccwsim::SimTrace (simulator.hpp:395-403), flattened per realization:
+ * arrays of `capacity` entries; `pasted` (capacity*T*T) may be NULL. */
+typedef struct ccw_trace {
+    int32_t capacity;
+    int32_t count;
+    int32_t* top;
+    int32_t* left;
+    int32_t* shape;
+    int32_t* ti_row;
+    int32_t* ti_col;
+    uint8_t* pasted;
+} ccw_trace;
+
+/* Per-call device timing, filled when profiling is enabled on the context. */
+typedef struct ccw_timing {
+    double total_ms;        /* device time of the last ccw_simulate*, CUDA events */
+    double ccf_ms;          /* summed device time of the CCF screen launches      */
+    double select_ms;       /* summed device time of the select+paste launches    */
+    int64_t ccf_launches;
+    int64_t launches;       /* every kernel this library launched in the call     */
+    double ccf_flop;        /* algorithmic FLOP of the CCF screen (2*ch*npos*mask) */
+    double ccf_flop_ref;    /* same count with the reference's F channels          */
+    int64_t waves;
+    int64_t jobs;
+} ccw_timing;
+
+typedef struct ccw_ctx ccw_ctx;
+typedef struct ccw_ti ccw_ti;
+
+/* ---------------------------------------------------------- context ---- */
+CCW_API ccw_status ccw_ctx_create(int device, ccw_ctx** out);
+CCW_API void ccw_ctx_destroy(ccw_ctx* ctx);
+CCW_API const char* ccw_last_error(const ccw_ctx* ctx);
+/* The cudaStream_t the context launches on (for event timing by callers). */
+CCW_API void* ccw_ctx_stream(ccw_ctx* ctx);
+CCW_API ccw_status ccw_ctx_set_profiling(ccw_ctx* ctx, int enabled);
+CCW_API ccw_status ccw_ctx_last_timing(ccw_ctx* ctx, ccw_timing* out);
+/* Selects the CCF screen kernel: 0 = auto, 1 = fp32 CUDA-core direct. */
+CCW_API ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant);
+
+/* FP32 FFMA peak of this GPU (TFLOP/s), measured with an in-library
+ * microbenchmark: the roofline denominator of the CUDA-core CCF screen. */
+CCW_API ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops);
+
+/* ---------------------------------------------------------- rng -------- */
+/* rng.hpp:11-16 */
+CCW_API uint64_t ccw_mix64(uint64_t seed, uint64_t index);
+
+/* ------------------------------------------------------ training image - */
+/* Uploads a TI (h*w codes in [0, num_facies)) and builds its level-J
+ * wavelet pyramid on the device once: replaces the per-realization
+ * to_indicator_planes + dwt2(...).apex of simulate_one (simulator.hpp:429-435,
+ * grid.hpp:245-263, wavelet.hpp:147-171).  facies_mode as in ccw_sim_config.
+ * ccw_ti_create_device takes a device pointer instead of a host pointer. */
+CCW_API ccw_status ccw_ti_create(ccw_ctx* ctx, const uint8_t* cells, int h, int w, int num_facies,
+                         int levels, int facies_mode, ccw_ti** out);
+CCW_API ccw_status ccw_ti_create_device(ccw_ctx* ctx, const uint8_t* d_cells, int h, int w,
+                                int num_facies, int levels, int facies_mode, ccw_ti** out);
+CCW_API void ccw_ti_destroy(ccw_ti* ti);
+/* Copies the device apex (channels x (h>>J) x (w>>J) doubles) to the host. */
+CCW_API ccw_status ccw_ti_apex(ccw_ti* ti, double* out);
+
+/* ------------------------------------------------------- simulation ---- */
+/* Batched simulate_one (simulator.hpp:418-519) for n_real explicit seeds;
+ * realization r of the output (n_real * sg_height * sg_width codes) is
+ * bit-identical to ccwsim::simulate_one(ti, cfg, seeds[r]).  hd may be NULL.
+ * diag (n_real entries) and traces (n_real entries) may be NULL.  The TI
+ * handle's levels / facies_mode must match cfg. */
+CCW_API ccw_status ccw_simulate(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                        const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                        uint8_t* out, ccw_diag* diag, ccw_trace* traces);
+/* Same, writing realizations to device memory (d_out, n_real*sg cells). */
+CCW_API ccw_status ccw_simulate_device(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                               const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                               uint8_t* d_out, ccw_diag* diag);
+/* simulate_ensemble (simulator.hpp:523-566): seeds mix64(master, r+1), all
+ * cfg->n_realizations in one batched call (the reference's `workers` knob is
+ * meaningless here and is ignored by the C++ shim, which the reference's
+ * worker-count-invariance contract allows). */
+CCW_API ccw_status ccw_simulate_ensemble(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                                 const int32_t* hd, int n_hd, uint8_t* out, ccw_diag* diag);
+
+/* ------------------------------------------- drop-in fp64 operators ---- */
+/* dwt2_single (wavelet.hpp:69-106): in h*w -> four (h/2)*(w/2) planes. */
+CCW_API ccw_status ccw_dwt2_single_f64(ccw_ctx* ctx, const double* in, int h, int w, double* a,
+                               double* dh, double* dv, double* dd);
+/* idwt2_single (wavelet.hpp:108-143). */
+CCW_API ccw_status ccw_idwt2_single_f64(ccw_ctx* ctx, const double* a, const double* dh,
+                                const double* dv, const double* dd, int hh, int hw, double* out);
+/* dwt2 (wavelet.hpp:147-171).  details packed per level j=1..J as H,V,D
+ * planes of (h>>j)*(w>>j) doubles; may be NULL. */
+CCW_API ccw_status ccw_dwt2_f64(ccw_ctx* ctx, const double* in, int h, int w, int levels, double* apex,
+                        double* details);
+/* idwt2 (wavelet.hpp:174-191), same packing. */
+CCW_API ccw_status ccw_idwt2_f64(ccw_ctx* ctx, const double* apex, const double* details, int h, int w,
+                         int levels, double* out);
+/* ccw_score_map_channels (matcher.hpp:147-173); ccw_score_map
+ * (matcher.hpp:132-141) is nch = 1, scoring = 0.  ti: nch planes of
+ * ti_h*ti_w; tmpl: nch planes of t_h*t_w; mask t_h*t_w in {0,1};
+ * out (ti_h-t_h+1)*(ti_w-t_w+1).  Bit-identical to the reference. */
+CCW_API ccw_status ccw_score_map_f64(ccw_ctx* ctx, const double* ti, const double* tmpl, int nch,
+                             int ti_h, int ti_w, int t_h, int t_w, const double* mask,
+                             int scoring, double* out);
+/* top_k (matcher.hpp:177-204).  rows/cols/vals hold k entries; n_out gets
+ * min(k, h*w). */
+CCW_API ccw_status ccw_top_k_f64(ccw_ctx* ctx, const double* scores, int h, int w, int k, int32_t* rows,
+                         int32_t* cols, double* vals, int* n_out);
+/* select_conditional (matcher.hpp:222-241): hd = n_hd (row, col, facies)
+ * template-local triples; ti = ti_h*ti_w codes. */
+CCW_API ccw_status ccw_select_conditional(ccw_ctx* ctx, const int32_t* rows, const int32_t* cols,
+                                  int n_cands, const int32_t* hd, int n_hd, const uint8_t* ti,
+                                  int ti_h, int ti_w, int levels, int* pick, int* mismatches);
+/* min_cut_stitch (simulator.hpp:328-374) on t*t patches. */
+CCW_API ccw_status ccw_min_cut_stitch(ccw_ctx* ctx, const uint8_t* existing, const uint8_t* incoming,
+                              int t, int shape, int vertical_on_left, int horizontal_on_top,
+                              int overlap, uint8_t* out);
+
+/* -------------------------------------------------- host-side helpers -- */
+/* SimConfig::validate / validate_against (simulator.hpp:46-84) incl.
+ * validate_hard_data (grid.hpp:151-170); ti_h/ti_w <= 0 skips the TI part. */
+CCW_API ccw_status ccw_validate_config(const ccw_sim_config* cfg, int ti_h, int ti_w, int num_facies,
+                               const int32_t* hd, int n_hd, char* msg, size_t msg_len);
+/* plan_raster_path (simulator.hpp:148-190) given its two rng draws:
+ * origin = bounded(rng, 4), column_major = (bounded(rng, 2) == 1).  The
+ * caller owns the generator (the C++ shim passes its std::mt19937_64). */
+CCW_API ccw_status ccw_plan_raster_path(const ccw_sim_config* cfg, int origin, int column_major,
+                                int* work_h, int* work_w, int32_t* tops, int32_t* lefts,
+                                int32_t* shapes, int capacity, int* count, char* msg,
+                                size_t msg_len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CCWGPU_H */

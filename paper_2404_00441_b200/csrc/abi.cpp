@@ -1,0 +1,542 @@
+// abi.cpp -- the extern "C" boundary of libccwgpu.so plus the host-side
+// logic that stays on the CPU by nature: configuration validation, the raster
+// plan and the mt19937_64 draw schedule.  Messages match the reference's
+// exception texts (tests match substrings such as "overlap" / "template").
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <utility>
+
+#include "internal.hpp"
+
+using ccwgpu::Fail;
+
+namespace {
+
+thread_local std::string g_err;  // errors raised before a context exists
+
+std::string fmt(const char* f, ...) __attribute__((format(printf, 1, 2)));
+std::string fmt(const char* f, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+template <typename F>
+ccw_status guarded(ccw_ctx* ctx, F&& f) {
+    try {
+        if (ctx) CCW_CUDA(cudaSetDevice(ctx->device));
+        f();
+        return CCW_OK;
+    } catch (const Fail& e) {
+        (ctx ? ctx->err : g_err) = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        (ctx ? ctx->err : g_err) = e.what();
+        return CCW_ERR_GENERIC;
+    }
+}
+
+void copy_msg(char* msg, size_t len, const std::string& s) {
+    if (msg && len) {
+        std::snprintf(msg, len, "%s", s.c_str());
+    }
+}
+
+}  // namespace
+
+namespace ccwgpu {
+
+// simulator.hpp:46-69
+void validate_config(const ccw_sim_config& c) {
+    if (c.sg_height < 1 || c.sg_width < 1)
+        throw Fail(CCW_ERR_CONFIG, "sg_size: dimensions must be positive");
+    if (c.dwt_level < 1) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be >= 1");
+    if (c.dwt_level > 10) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be <= 10");
+    if (c.template_size < 2) throw Fail(CCW_ERR_CONFIG, "template: must be >= 2");
+    if (c.overlap < 1 || c.overlap >= c.template_size)
+        throw Fail(CCW_ERR_CONFIG, "overlap: must be in [1, template)");
+    const int b = 1 << c.dwt_level;
+    if (c.template_size % b != 0)
+        throw Fail(CCW_ERR_CONFIG, fmt("template: %d not divisible by 2^dwt_level = %d",
+                                       c.template_size, b));
+    if (c.overlap % b != 0)
+        throw Fail(CCW_ERR_CONFIG,
+                   fmt("overlap: %d not divisible by 2^dwt_level = %d", c.overlap, b));
+    if (c.candidates < 1) throw Fail(CCW_ERR_CONFIG, "candidates: must be >= 1");
+    if (c.n_realizations < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+    if (c.template_size > c.sg_height || c.template_size > c.sg_width)
+        throw Fail(CCW_ERR_CONFIG, fmt("template: %d exceeds simulation grid %dx%d",
+                                       c.template_size, c.sg_height, c.sg_width));
+    if (c.scoring != 0 && c.scoring != 1) throw Fail(CCW_ERR_CONFIG, "scoring: must be raw or normalized");
+    if (c.facies_mode != 0 && c.facies_mode != 1)
+        throw Fail(CCW_ERR_CONFIG, "facies_mode: must be indicator or raw-codes");
+}
+
+// grid.hpp:151-170
+static void validate_hard_data(const int32_t* hd, int n_hd, int h, int w, int nf) {
+    std::vector<int> seen;
+    if (n_hd > 0) seen.assign(static_cast<size_t>(h) * w, -1);
+    for (int i = 0; i < n_hd; ++i) {
+        const int r = hd[3 * i], c = hd[3 * i + 1], f = hd[3 * i + 2];
+        if (r < 0 || r >= h || c < 0 || c >= w)
+            throw Fail(CCW_ERR_BOUNDS,
+                       fmt("hard datum %d at (%d, %d) outside %dx%d grid", i, r, c, h, w));
+        if (f < 0 || f >= nf)
+            throw Fail(CCW_ERR_BOUNDS,
+                       fmt("hard datum %d has facies %d outside [0, %d)", i, f, nf));
+        int& s = seen[static_cast<size_t>(r) * w + c];
+        if (s >= 0)
+            throw Fail(CCW_ERR_STRUCTURE,
+                       fmt("duplicate hard data at (%d, %d): entries %d and %d", r, c, s, i));
+        s = i;
+    }
+}
+
+// simulator.hpp:72-84
+void validate_against(const ccw_sim_config& c, int ti_h, int ti_w, int nf, const int32_t* hd,
+                      int n_hd) {
+    validate_config(c);
+    if (c.template_size > ti_h || c.template_size > ti_w)
+        throw Fail(CCW_ERR_CONFIG, fmt("template: %d exceeds training image %dx%d",
+                                       c.template_size, ti_h, ti_w));
+    const int b = 1 << c.dwt_level;
+    if (ti_h % b != 0 || ti_w % b != 0)
+        throw Fail(CCW_ERR_CONFIG,
+                   fmt("training image %dx%d not divisible by 2^dwt_level = %d", ti_h, ti_w, b));
+    if (hd) validate_hard_data(hd, n_hd, c.sg_height, c.sg_width, nf);
+}
+
+uint64_t bounded(std::mt19937_64& rng, uint64_t n) {
+    const uint64_t threshold = (0 - n) % n;
+    for (;;) {
+        const uint64_t r = rng();
+        if (r >= threshold) return r % n;
+    }
+}
+
+static int padded_extent(int sg, int t, int stride) {  // simulator.hpp:125-131
+    if (sg == t) return t;
+    const int steps = (sg - t + stride - 1) / stride;
+    return t + steps * stride;
+}
+
+Plan make_plan(const ccw_sim_config& c, std::mt19937_64& rng) {
+    validate_config(c);
+    const int origin = static_cast<int>(bounded(rng, 4));
+    const bool column_major = bounded(rng, 2) == 1;
+    return make_plan_from(c, origin, column_major);
+}
+
+Plan make_plan_from(const ccw_sim_config& c, int origin, bool column_major) {
+    validate_config(c);
+    const int t = c.template_size, stride = t - c.overlap;
+    Plan p;
+    p.origin = origin;
+    p.column_major = column_major;
+    p.work_h = padded_extent(c.sg_height, t, stride);
+    p.work_w = padded_extent(c.sg_width, t, stride);
+    const bool rows_asc = p.origin == CCW_TOP_LEFT || p.origin == CCW_TOP_RIGHT;
+    const bool cols_asc = p.origin == CCW_TOP_LEFT || p.origin == CCW_BOTTOM_LEFT;
+    std::vector<int> rp, cp;
+    for (int q = 0; q + t <= p.work_h; q += stride) rp.push_back(q);
+    for (int q = 0; q + t <= p.work_w; q += stride) cp.push_back(q);
+    if (!rows_asc) std::reverse(rp.begin(), rp.end());
+    if (!cols_asc) std::reverse(cp.begin(), cp.end());
+    const std::vector<int>& outer = p.column_major ? cp : rp;
+    const std::vector<int>& inner = p.column_major ? rp : cp;
+    p.n_outer = static_cast<int>(outer.size());
+    p.n_inner = static_cast<int>(inner.size());
+    const size_t n = outer.size() * inner.size();
+    p.tops.reserve(n);
+    p.lefts.reserve(n);
+    p.shapes.reserve(n);
+    for (int o = 0; o < p.n_outer; ++o)
+        for (int i = 0; i < p.n_inner; ++i) {
+            p.tops.push_back(p.column_major ? inner[i] : outer[o]);
+            p.lefts.push_back(p.column_major ? outer[o] : inner[i]);
+            int sh;
+            if (o == 0 && i == 0)
+                sh = CCW_OR_NONE;
+            else if (o == 0)
+                sh = p.column_major ? CCW_OR_HORIZONTAL : CCW_OR_VERTICAL;
+            else if (i == 0)
+                sh = p.column_major ? CCW_OR_VERTICAL : CCW_OR_HORIZONTAL;
+            else
+                sh = CCW_OR_L;
+            p.shapes.push_back(sh);
+            p.outer_idx.push_back(o);
+            p.inner_idx.push_back(i);
+        }
+    return p;
+}
+
+}  // namespace ccwgpu
+
+// ================================================================ C-ABI ===
+
+extern "C" {
+
+ccw_status ccw_ctx_create(int device, ccw_ctx** out) {
+    if (!out) {
+        g_err = "ccw_ctx_create: null output pointer";
+        return CCW_ERR_GENERIC;
+    }
+    *out = nullptr;
+    auto* ctx = new ccw_ctx();
+    ctx->device = device;
+    ccw_status st = guarded(nullptr, [&] {
+        int n = 0;
+        CCW_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n)
+            throw Fail(CCW_ERR_CUDA, fmt("device %d not present (%d visible)", device, n));
+        CCW_CUDA(cudaSetDevice(device));
+        CCW_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    });
+    if (st != CCW_OK) {
+        delete ctx;
+        return st;
+    }
+    *out = ctx;
+    return CCW_OK;
+}
+
+void ccw_ctx_destroy(ccw_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (ccwgpu::DevBuf* b : {&ctx->jobs, &ctx->work, &ctx->hd, &ctx->wts, &ctx->tm64,
+                              &ctx->scores, &ctx->chosen, &ctx->pasted, &ctx->mism, &ctx->out,
+                              &ctx->ops_a, &ctx->ops_b, &ctx->ops_c, &ctx->ops_d, &ctx->ops_e})
+        b->release();
+    ctx->h_stage.release();
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* ccw_last_error(const ccw_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+void* ccw_ctx_stream(ccw_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+ccw_status ccw_ctx_set_profiling(ccw_ctx* ctx, int enabled) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    ctx->profiling = enabled != 0;
+    return CCW_OK;
+}
+
+ccw_status ccw_ctx_last_timing(ccw_ctx* ctx, ccw_timing* out) {
+    if (!ctx || !out) return CCW_ERR_GENERIC;
+    *out = ctx->timing;
+    return CCW_OK;
+}
+
+ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (variant < 0 || variant > 1)
+            throw Fail(CCW_ERR_CONFIG, fmt("ccf variant %d unknown", variant));
+        ctx->ccf_variant = variant;
+    });
+}
+
+ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops) {
+    if (!ctx || !tflops) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] { *tflops = ccwgpu::measure_ffma_peak(ctx); });
+}
+
+uint64_t ccw_mix64(uint64_t seed, uint64_t index) {  // rng.hpp:11-16
+    uint64_t z = seed + index * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device_ptr, int h,
+                                 int w, int nf, int levels, int mode, ccw_ti** out) {
+    if (!ctx || !out) return CCW_ERR_GENERIC;
+    *out = nullptr;
+    auto* ti = new ccw_ti();
+    ccw_status st = guarded(ctx, [&] {
+        if (h <= 0 || w <= 0) throw Fail(CCW_ERR_DIMENSION, "grid dimensions must be positive");
+        if (nf <= 0) throw Fail(CCW_ERR_DIMENSION, "num_facies must be positive");
+        if (nf > 255) throw Fail(CCW_ERR_DIMENSION, "num_facies must be <= 255 (uint8 codes)");
+        if (levels < 1) throw Fail(CCW_ERR_DIMENSION, "decomposition level must be >= 1");
+        if (levels > 10 || h % (1 << levels) != 0 || w % (1 << levels) != 0)
+            throw Fail(CCW_ERR_CONFIG,
+                       fmt("training image %dx%d not divisible by 2^dwt_level = %d", h, w,
+                           1 << std::min(levels, 30)));
+        if (mode != 0 && mode != 1) throw Fail(CCW_ERR_CONFIG, "facies_mode: unknown");
+        if (!device_ptr) {
+            // grid.hpp:36-40 code-range check (the device path trusts its caller)
+            for (size_t i = 0; i < static_cast<size_t>(h) * w; ++i)
+                if (cells[i] >= nf)
+                    throw Fail(CCW_ERR_BOUNDS, fmt("cell %zu holds code %d outside [0, %d)", i,
+                                                   static_cast<int>(cells[i]), nf));
+        }
+        ti->ctx = ctx;
+        ti->device = ctx->device;
+        ti->h = h;
+        ti->w = w;
+        ti->F = nf;
+        ti->J = levels;
+        ti->mode = mode;
+        ti->hc = h >> levels;
+        ti->wc = w >> levels;
+        ti->nch = mode == 0 ? nf : 1;
+        ti->nscr = mode == 0 ? nf - 1 : 1;
+        const size_t n = static_cast<size_t>(h) * w;
+        const size_t nc = static_cast<size_t>(ti->hc) * ti->wc;
+        CCW_CUDA(cudaMalloc(&ti->d_codes, n));
+        CCW_CUDA(cudaMalloc(&ti->d_ti64, sizeof(double) * nc * ti->nch));
+        CCW_CUDA(cudaMalloc(&ti->d_scr, sizeof(float) * nc * std::max(ti->nscr, 1)));
+        CCW_CUDA(cudaMemcpyAsync(ti->d_codes, cells, n,
+                                 device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        ccwgpu::build_pyramid(ti, ctx->stream);
+    });
+    if (st != CCW_OK) {
+        ccw_ti_destroy(ti);
+        return st;
+    }
+    *out = ti;
+    return CCW_OK;
+}
+
+ccw_status ccw_ti_create(ccw_ctx* ctx, const uint8_t* cells, int h, int w, int nf, int levels,
+                         int mode, ccw_ti** out) {
+    return ti_create_impl(ctx, cells, false, h, w, nf, levels, mode, out);
+}
+
+ccw_status ccw_ti_create_device(ccw_ctx* ctx, const uint8_t* d_cells, int h, int w, int nf,
+                                int levels, int mode, ccw_ti** out) {
+    return ti_create_impl(ctx, d_cells, true, h, w, nf, levels, mode, out);
+}
+
+void ccw_ti_destroy(ccw_ti* ti) {
+    if (!ti) return;
+    // cudaFree synchronises the device; the owning context may already be gone.
+    cudaSetDevice(ti->device);
+    if (ti->d_codes) cudaFree(ti->d_codes);
+    if (ti->d_ti64) cudaFree(ti->d_ti64);
+    if (ti->d_scr) cudaFree(ti->d_scr);
+    delete ti;
+}
+
+ccw_status ccw_ti_apex(ccw_ti* ti, double* out) {
+    if (!ti) return CCW_ERR_GENERIC;
+    return guarded(ti->ctx, [&] {
+        CCW_CUDA(cudaMemcpyAsync(out, ti->d_ti64,
+                                 sizeof(double) * ti->nch * static_cast<size_t>(ti->hc) * ti->wc,
+                                 cudaMemcpyDeviceToHost, ti->ctx->stream));
+        CCW_CUDA(cudaStreamSynchronize(ti->ctx->stream));
+    });
+}
+
+static void check_ti_cfg(ccw_ti* ti, const ccw_sim_config* cfg, const int32_t* hd, int n_hd) {
+    if (!cfg) throw Fail(CCW_ERR_GENERIC, "null config");
+    ccwgpu::validate_against(*cfg, ti->h, ti->w, ti->F, hd, n_hd);
+    if (cfg->dwt_level != ti->J)
+        throw Fail(CCW_ERR_CONFIG, fmt("dwt_level: %d does not match the TI pyramid level %d",
+                                       cfg->dwt_level, ti->J));
+    if (cfg->facies_mode != ti->mode)
+        throw Fail(CCW_ERR_CONFIG, "facies_mode: does not match the TI pyramid");
+}
+
+ccw_status ccw_simulate(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                        const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                        uint8_t* out, ccw_diag* diag, ccw_trace* traces) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti_cfg(ti, cfg, hd, n_hd);
+        if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+        ccwgpu::run_simulation(ctx, ti, *cfg, seeds, n_real, hd, n_hd, nullptr, out, diag,
+                               traces);
+    });
+}
+
+ccw_status ccw_simulate_device(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                               const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                               uint8_t* d_out, ccw_diag* diag) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti_cfg(ti, cfg, hd, n_hd);
+        if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+        ccwgpu::run_simulation(ctx, ti, *cfg, seeds, n_real, hd, n_hd, d_out, nullptr, diag,
+                               nullptr);
+    });
+}
+
+ccw_status ccw_simulate_ensemble(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                                 const int32_t* hd, int n_hd, uint8_t* out, ccw_diag* diag) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti_cfg(ti, cfg, hd, n_hd);
+        std::vector<uint64_t> seeds(static_cast<size_t>(cfg->n_realizations));
+        for (int r = 0; r < cfg->n_realizations; ++r)
+            seeds[r] = ccw_mix64(cfg->master_seed, static_cast<uint64_t>(r) + 1);
+        ccwgpu::run_simulation(ctx, ti, *cfg, seeds.data(), cfg->n_realizations, hd, n_hd,
+                               nullptr, out, diag, nullptr);
+    });
+}
+
+ccw_status ccw_dwt2_single_f64(ccw_ctx* ctx, const double* in, int h, int w, double* a,
+                               double* dh, double* dv, double* dd) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (h <= 0 || w <= 0) throw Fail(CCW_ERR_DIMENSION, "plane dimensions must be positive");
+        if (h % 2 != 0 || w % 2 != 0)
+            throw Fail(CCW_ERR_DIMENSION,
+                       fmt("dwt2_single requires even dimensions, got %dx%d", h, w));
+        ccwgpu::op_dwt2_single(ctx, in, h, w, a, dh, dv, dd);
+    });
+}
+
+ccw_status ccw_idwt2_single_f64(ccw_ctx* ctx, const double* a, const double* dh,
+                                const double* dv, const double* dd, int hh, int hw,
+                                double* out) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (hh <= 0 || hw <= 0) throw Fail(CCW_ERR_DIMENSION, "plane dimensions must be positive");
+        ccwgpu::op_idwt2_single(ctx, a, dh, dv, dd, hh, hw, out);
+    });
+}
+
+ccw_status ccw_dwt2_f64(ccw_ctx* ctx, const double* in, int h, int w, int levels, double* apex,
+                        double* details) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (h <= 0 || w <= 0) throw Fail(CCW_ERR_DIMENSION, "plane dimensions must be positive");
+        if (levels < 1) throw Fail(CCW_ERR_DIMENSION, "decomposition level must be >= 1");
+        if (levels > 30 || h % (1 << levels) != 0 || w % (1 << levels) != 0)
+            throw Fail(CCW_ERR_DIMENSION,
+                       fmt("plane %dx%d not divisible by 2^%d", h, w, levels));
+        ccwgpu::op_dwt2(ctx, in, h, w, levels, apex, details);
+    });
+}
+
+ccw_status ccw_idwt2_f64(ccw_ctx* ctx, const double* apex, const double* details, int h, int w,
+                         int levels, double* out) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (levels < 1 || levels > 30 || h <= 0 || w <= 0 || (h >> levels) < 1 ||
+            (w >> levels) < 1 || h % (1 << levels) != 0 || w % (1 << levels) != 0)
+            throw Fail(CCW_ERR_STRUCTURE, "pyramid level count inconsistent");
+        if (!details) throw Fail(CCW_ERR_STRUCTURE, "pyramid level count inconsistent");
+        ccwgpu::op_idwt2(ctx, apex, details, h, w, levels, out);
+    });
+}
+
+ccw_status ccw_score_map_f64(ccw_ctx* ctx, const double* ti, const double* tmpl, int nch,
+                             int ti_h, int ti_w, int t_h, int t_w, const double* mask,
+                             int scoring, double* out) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (nch < 1) throw Fail(CCW_ERR_STRUCTURE, "channel counts disagree");
+        // matcher.hpp:102-123
+        if (t_h > ti_h || t_w > ti_w)
+            throw Fail(CCW_ERR_DIMENSION,
+                       fmt("template %dx%d larger than TI coefficients %dx%d", t_h, t_w, ti_h, ti_w));
+        for (int f = 0; f < nch; ++f)
+            for (int i = 0; i < t_h * t_w; ++i) {
+                const double m = mask[i];
+                if (m != 0.0 && m != 1.0) throw Fail(CCW_ERR_STRUCTURE, "mask values must be 0 or 1");
+                if (m == 0.0 && tmpl[static_cast<size_t>(f) * t_h * t_w + i] != 0.0)
+                    throw Fail(CCW_ERR_STRUCTURE,
+                               "template carries nonzero values outside the mask");
+            }
+        ccwgpu::op_score_map(ctx, ti, tmpl, nch, ti_h, ti_w, t_h, t_w, mask, scoring, out);
+    });
+}
+
+ccw_status ccw_top_k_f64(ccw_ctx* ctx, const double* scores, int h, int w, int k, int32_t* rows,
+                         int32_t* cols, double* vals, int* n_out) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (h <= 0 || w <= 0 || !scores) throw Fail(CCW_ERR_EMPTY, "top_k on empty score map");
+        if (k < 1) throw Fail(CCW_ERR_CONFIG, "candidate count must be >= 1");
+        ccwgpu::op_top_k(ctx, scores, h, w, k, rows, cols, vals, n_out);
+    });
+}
+
+ccw_status ccw_select_conditional(ccw_ctx* ctx, const int32_t* rows, const int32_t* cols,
+                                  int n_cands, const int32_t* hd, int n_hd, const uint8_t* ti,
+                                  int ti_h, int ti_w, int levels, int* pick, int* mismatches) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (n_cands < 1) throw Fail(CCW_ERR_EMPTY, "select_conditional on empty candidate set");
+        // CategoricalGrid::at bounds (grid.hpp:69-75)
+        for (int i = 0; i < n_cands; ++i)
+            for (int d = 0; d < n_hd; ++d) {
+                const int r = (rows[i] << levels) + hd[3 * d];
+                const int c = (cols[i] << levels) + hd[3 * d + 1];
+                if (r < 0 || r >= ti_h || c < 0 || c >= ti_w)
+                    throw Fail(CCW_ERR_BOUNDS, fmt("cell (%d, %d) outside %dx%d grid", r, c,
+                                                   ti_h, ti_w));
+            }
+        ccwgpu::op_select_conditional(ctx, rows, cols, n_cands, hd, n_hd, ti, ti_h, ti_w, levels,
+                                      pick, mismatches);
+    });
+}
+
+ccw_status ccw_min_cut_stitch(ccw_ctx* ctx, const uint8_t* existing, const uint8_t* incoming,
+                              int t, int shape, int vleft, int htop, int overlap, uint8_t* out) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (t <= 0) throw Fail(CCW_ERR_DIMENSION, "crop size must be positive");
+        if (shape < 0 || shape > 3) throw Fail(CCW_ERR_STRUCTURE, "unknown overlap shape");
+        if (shape != CCW_OR_NONE && (overlap < 1 || overlap >= t))
+            throw Fail(CCW_ERR_STRUCTURE, "overlap band width out of range");
+        ccwgpu::op_min_cut_stitch(ctx, existing, incoming, t, shape, vleft, htop, overlap, out);
+    });
+}
+
+ccw_status ccw_validate_config(const ccw_sim_config* cfg, int ti_h, int ti_w, int nf,
+                               const int32_t* hd, int n_hd, char* msg, size_t msg_len) {
+    try {
+        if (!cfg) throw Fail(CCW_ERR_GENERIC, "null config");
+        if (ti_h <= 0 || ti_w <= 0) {
+            ccwgpu::validate_config(*cfg);
+        } else {
+            ccwgpu::validate_against(*cfg, ti_h, ti_w, nf, hd, n_hd);
+        }
+        copy_msg(msg, msg_len, "");
+        return CCW_OK;
+    } catch (const Fail& e) {
+        copy_msg(msg, msg_len, e.what());
+        g_err = e.what();
+        return e.code;
+    }
+}
+
+ccw_status ccw_plan_raster_path(const ccw_sim_config* cfg, int origin, int column_major,
+                                int* work_h, int* work_w, int32_t* tops, int32_t* lefts,
+                                int32_t* shapes, int capacity, int* count, char* msg,
+                                size_t msg_len) {
+    try {
+        if (!cfg) throw Fail(CCW_ERR_GENERIC, "null config");
+        if (origin < 0 || origin > 3) throw Fail(CCW_ERR_CONFIG, "origin: must be in [0, 4)");
+        const ccwgpu::Plan p = ccwgpu::make_plan_from(*cfg, origin, column_major != 0);
+        *work_h = p.work_h;
+        *work_w = p.work_w;
+        *count = static_cast<int>(p.tops.size());
+        for (int i = 0; i < *count && i < capacity; ++i) {
+            tops[i] = p.tops[i];
+            lefts[i] = p.lefts[i];
+            shapes[i] = p.shapes[i];
+        }
+        copy_msg(msg, msg_len, "");
+        return CCW_OK;
+    } catch (const Fail& e) {
+        copy_msg(msg, msg_len, e.what());
+        g_err = e.what();
+        return e.code;
+    }
+}
+
+}  // extern "C"

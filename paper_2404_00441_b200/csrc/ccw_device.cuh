@@ -1,0 +1,143 @@
+// ccw_device.cuh -- device-side building blocks shared by the kernels.
+//
+// Exactness contract: everything that reproduces a reference
+// double uses explicit round-to-nearest intrinsics (__dmul_rn / __dadd_rn /
+// __ddiv_rn / __dsqrt_rn), so nvcc can never contract it into an FMA, and
+// follows the reference's operation order literally.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ccwgpu {
+
+constexpr double kInvSqrt2 = 0.70710678118654752440084436210485;  // wavelet.hpp:17
+constexpr int kMaxLevels = 12;
+constexpr uint8_t kNoDatum = 255;
+
+enum OrShape : int { kNone = 0, kVertical = 1, kHorizontal = 2, kL = 3 };  // simulator.hpp:87
+
+// One placement of one realization, as scheduled on the device.
+struct Job {
+    int32_t real;    // realization index within the call
+    int32_t place;   // placement index in the reference raster order
+    int32_t top;     // fine-grid footprint origin in the work grid
+    int32_t left;
+    int32_t shape;   // OrShape
+    int32_t vleft;   // vertical strip on the left (plan.vertical_on_left())
+    int32_t htop;    // horizontal strip on top (plan.horizontal_on_top())
+    int32_t pick;    // unconditional: precomputed bounded(rng, K') draw; -1 = conditional
+    int32_t fr;      // first placement: precomputed block-aligned TI origin
+    int32_t fc;
+};
+
+// Parameters shared by every job of one simulate call.
+struct SimParams {
+    // training image
+    const uint8_t* ti;       // h*w codes
+    const double* ti64;      // nch planes hc*wc: reference-order apex values
+    const float* tiscr;      // nscr planes hc*wc: exact block-sum screen planes
+    int ti_h, ti_w, hc, wc;
+    int F, J, mode;          // mode 0 indicator, 1 raw_codes
+    int nch, nscr;
+    // geometry
+    int T, OV, Tc, OVc, B;   // B = 2^J
+    int out_h, out_w, npos;  // score-map extent
+    int K;                   // min(candidates, npos)
+    int scoring;             // 0 raw, 1 normalized
+    int min_cut;
+    // simulation grid
+    uint8_t* work;           // n_real planes of wh*ww
+    int wh, ww;
+    const uint8_t* hd;       // wh*ww plane, kNoDatum = none; may be null
+    // per-job scratch (indexed by job slot within a launch chunk)
+    int32_t* wts;            // nscr*Tc*Tc integer screen weights
+    double* tm64;            // nch*Tc*Tc reference-order OR apex values
+    int32_t* scores;         // npos screen scores
+    // outputs
+    int32_t* chosen;         // per job (global job id): fr, fc
+    uint8_t* pasted;         // optional trace of pasted patches (global job id * T*T)
+};
+
+// Row-major run of the coarse overlap mask in template row s: [t0, t1).
+// Every simulator mask (strip or L, simulator.hpp:194-215) has at most one
+// maximal run per row, so mask_runs (matcher.hpp:44-61) reduces to this.
+__device__ __forceinline__ void mask_row_run(int shape, int vleft, int htop, int Tc, int OVc,
+                                             int s, int& t0, int& t1) {
+    const bool vert = shape == kVertical || shape == kL;
+    const bool horz = shape == kHorizontal || shape == kL;
+    const bool in_h = horz && (htop ? s < OVc : s >= Tc - OVc);
+    if (in_h) {
+        t0 = 0;
+        t1 = Tc;
+    } else if (vert) {
+        t0 = vleft ? 0 : Tc - OVc;
+        t1 = t0 + OVc;
+    } else {
+        t0 = 0;
+        t1 = 0;
+    }
+}
+
+// Level-J Haar apex of one 2^J x 2^J block in the reference's exact order.
+// The reference transforms whole planes level by level (wavelet.hpp:163-168);
+// by locality each apex value depends only on its block, through the tree
+//   a = s*((s*A00 + s*A01) + (s*A10 + s*A11))      (wavelet.hpp:29, :99)
+// over the four level-(j-1) quadrant values.  Visiting the leaves in Morton
+// order and folding every completed quartet reproduces that tree exactly.
+// leaf(code) is the indicator (mode 0, facies f) or the raw code (mode 1).
+__device__ __forceinline__ double haar_apex_block(const uint8_t* cells, int ld, int J, int mode,
+                                                  int f) {
+    double st[kMaxLevels][4];
+    int cnt[kMaxLevels];
+    for (int l = 0; l < J; ++l) cnt[l] = 0;
+    const int n = 1 << (2 * J);
+    for (int k = 0; k < n; ++k) {
+        int r = 0, c = 0;
+        for (int b = 0; b < J; ++b) {
+            c |= ((k >> (2 * b)) & 1) << b;
+            r |= ((k >> (2 * b + 1)) & 1) << b;
+        }
+        const int code = cells[r * ld + c];
+        double x = mode == 0 ? (code == f ? 1.0 : 0.0) : (double)code;
+        int l = 0;
+        st[0][cnt[0]++] = x;
+        while (cnt[l] == 4) {
+            const double lo0 = __dadd_rn(__dmul_rn(kInvSqrt2, st[l][0]), __dmul_rn(kInvSqrt2, st[l][1]));
+            const double lo1 = __dadd_rn(__dmul_rn(kInvSqrt2, st[l][2]), __dmul_rn(kInvSqrt2, st[l][3]));
+            const double a = __dmul_rn(kInvSqrt2, __dadd_rn(lo0, lo1));
+            cnt[l] = 0;
+            ++l;
+            if (l == J) return a;
+            st[l][cnt[l]++] = a;
+        }
+    }
+    return 0.0;  // unreachable for J >= 1
+}
+
+// Exact-integer block statistic used by the screen: the count of facies f
+// (mode 0) or the sum of codes (mode 1) over one 2^J x 2^J block.
+__device__ __forceinline__ int block_stat(const uint8_t* cells, int ld, int B, int mode, int f) {
+    int acc = 0;
+    for (int r = 0; r < B; ++r)
+        for (int c = 0; c < B; ++c) {
+            const int code = cells[r * ld + c];
+            acc += mode == 0 ? (code == f) : code;
+        }
+    return acc;
+}
+
+// Block-wide reductions for blockDim.x a multiple of 32 (<= 1024).
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    T r = red[0];
+    for (int i = 1; i < nw; ++i) r = op(r, red[i]);
+    return r;
+}
+
+}  // namespace ccwgpu

@@ -1,0 +1,987 @@
+// sim.cu -- the batched, wavefront-scheduled CCWSIM simulation on sm_100a.
+//
+// One ccw_simulate call runs every realization in lock-step.  Placements of
+// all realizations are grouped into waves by the key (d+1)*o + i of their
+// raster coordinates (o outer, i inner; d = how many stride steps a footprint
+// reaches), which orders every pair of overlapping footprints exactly as the
+// reference's raster loop does (simulator.hpp:447-496) while letting the
+// placements of one wave run concurrently.  Per wave:
+//
+//   or_prep        overlap region -> exact-integer screen weights and the
+//                  reference-order fp64 OR apex (simulator.hpp:455-460)
+//   ccf_direct     exact-integer CCF screen over every TI window, fp32 FFMA
+//                  on CUDA cores (matcher.hpp:64-81 up to a per-job constant)
+//   select_paste   exact K-th-largest threshold, fp64 reference-order
+//                  rescoring of the tie group, top-K ordering
+//                  (matcher.hpp:177-204), unconditional / conditional pick
+//                  (matcher.hpp:207-241), optional min-cut stitch
+//                  (simulator.hpp:286-374) and the paste (simulator.hpp:483-493)
+//
+// and once per call a finalize kernel applies the hard-data overwrite and
+// crops the work grid (simulator.hpp:506-515).
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstring>
+
+#include "ccw_device.cuh"
+#include "internal.hpp"
+
+namespace ccwgpu {
+
+// ------------------------------------------------------------ pyramid ----
+
+// TI pyramid, once per TI: reference-order apex per channel (wavelet.hpp:147-171
+// applied to to_indicator_planes / to_real_plane, simulator.hpp:429-435) and the
+// exact-integer screen planes (block counts of facies 0..F-2, or code sums).
+__global__ void pyramid_kernel(const uint8_t* __restrict__ codes, int w, int hc, int wc, int J,
+                               int mode, int nscr, double* __restrict__ ti64,
+                               float* __restrict__ scr) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ch = blockIdx.y;
+    if (cell >= hc * wc) return;
+    const int i = cell / wc, j = cell - i * wc;
+    const int B = 1 << J;
+    const uint8_t* base = codes + static_cast<size_t>(i * B) * w + j * B;
+    ti64[static_cast<size_t>(ch) * hc * wc + cell] = haar_apex_block(base, w, J, mode, ch);
+    if (ch < nscr)
+        scr[static_cast<size_t>(ch) * hc * wc + cell] = static_cast<float>(block_stat(base, w, B, mode, ch));
+}
+
+void build_pyramid(ccw_ti* ti, cudaStream_t s) {
+    const int n = ti->hc * ti->wc;
+    dim3 grid((n + 127) / 128, ti->nch);
+    pyramid_kernel<<<grid, 128, 0, s>>>(ti->d_codes, ti->w, ti->hc, ti->wc, ti->J, ti->mode,
+                                        ti->nscr, ti->d_ti64, ti->d_scr);
+    CCW_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ or_prep ----
+
+// Screen weights: indicator mode uses F-1 channels with w_f = n_f - n_{F-1}
+// (n = OR block counts).  Because every fine cell holds exactly one facies,
+//   S = sum_f sum_mask N_f * n_f = sum_{f<F-1} sum_mask N_f * w_f + B * sum_mask n_{F-1}
+// and the last term is the same for every TI window, so ranking by the F-1
+// channel sum is ranking by S.  Raw-codes mode uses the code sums directly.
+__global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    const int slot = blockIdx.x;
+    const Job jb = jobs[job0 + slot];
+    const int Tc = P.Tc, B = P.B;
+    const uint8_t* grid = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
+    int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
+    double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+    for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
+        const int s = c / Tc, t = c - s * Tc;
+        int t0, t1;
+        mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+        const bool in = t >= t0 && t < t1;
+        const uint8_t* base = grid + static_cast<size_t>(jb.top + s * B) * P.ww + jb.left + t * B;
+        if (P.mode == 0) {
+            const int last = in ? block_stat(base, P.ww, B, 0, P.F - 1) : 0;
+            for (int f = 0; f < P.nscr; ++f)
+                wts[f * Tc * Tc + c] = in ? block_stat(base, P.ww, B, 0, f) - last : 0;
+        } else {
+            wts[c] = in ? block_stat(base, P.ww, B, 1, 0) : 0;
+        }
+        for (int ch = 0; ch < P.nch; ++ch)
+            tm[ch * Tc * Tc + c] = in ? haar_apex_block(base, P.ww, P.J, P.mode, ch) : 0.0;
+    }
+}
+
+// --------------------------------------------------------- CCF screen ----
+
+constexpr int CCF_TX = 16;  // output rows per CTA
+constexpr int CCF_TY = 64;  // output columns per CTA
+constexpr int CCF_RY = 8;   // consecutive outputs per thread
+constexpr int CCF_THREADS = CCF_TX * CCF_TY / CCF_RY;
+
+struct Rect {
+    int s0, t0, h, w;
+};
+
+// The strip / L overlap masks are the union of at most two disjoint
+// rectangles: the horizontal strip (full width) and the rest of the vertical
+// strip.  (Any summation order is exact for the integer screen.)
+__device__ __forceinline__ int mask_rects(const Job& jb, int Tc, int OVc, Rect* r) {
+    const bool vert = jb.shape == kVertical || jb.shape == kL;
+    const bool horz = jb.shape == kHorizontal || jb.shape == kL;
+    int n = 0;
+    if (horz) r[n++] = {jb.htop ? 0 : Tc - OVc, 0, OVc, Tc};
+    if (vert) {
+        const int c0 = jb.vleft ? 0 : Tc - OVc;
+        if (horz)
+            r[n++] = {jb.htop ? OVc : 0, c0, Tc - OVc, OVc};
+        else
+            r[n++] = {0, c0, Tc, OVc};
+    }
+    return n;
+}
+
+__host__ __device__ constexpr int ccf_sw(int Tc) { return ((CCF_TY + Tc + 4) + 3) & ~3; }
+__host__ __device__ constexpr int ccf_wp(int Tc) { return (Tc + 3) & ~3; }
+
+size_t ccf_smem_bytes(int Tc, int nscr) {
+    const int SH = CCF_TX + Tc - 1, SW = ccf_sw(Tc), WP = ccf_wp(Tc);
+    return sizeof(float) * (static_cast<size_t>(nscr) * SH * SW + static_cast<size_t>(nscr) * 2 * Tc * WP);
+}
+
+// Direct correlation of the job's integer weights with the TI screen planes,
+// fp32 on CUDA cores.  Every operand is a small integer and every partial sum
+// is bounded by mask * B^2 < 2^24 (checked on the host), so FFMA is exact.
+// Tiling: one CTA = 16 x 64 outputs of one job; thread = 1 x 8 outputs with a
+// sliding 11-register TI window per 4-wide weight chunk.
+__global__ void __launch_bounds__(CCF_THREADS) ccf_direct_kernel(SimParams P,
+                                                                 const Job* __restrict__ jobs,
+                                                                 int job0) {
+    extern __shared__ __align__(16) float ccf_sm[];
+    const int slot = blockIdx.z;
+    const Job jb = jobs[job0 + slot];
+    const int Tc = P.Tc, hc = P.hc, wc = P.wc, nscr = P.nscr;
+    const int SH = CCF_TX + Tc - 1, SW = ccf_sw(Tc), WP = ccf_wp(Tc);
+    float* tile = ccf_sm;
+    float* wpk = ccf_sm + nscr * SH * SW;
+    Rect rc[2];
+    const int nr = mask_rects(jb, Tc, P.OVc, rc);
+    const int x0 = blockIdx.y * CCF_TX, y0 = blockIdx.x * CCF_TY;
+
+    const int tn = nscr * SH * SW;
+    for (int e = threadIdx.x; e < tn; e += CCF_THREADS) {
+        const int f = e / (SH * SW);
+        const int rem = e - f * SH * SW;
+        const int r = rem / SW, c = rem - r * SW;
+        const int gx = x0 + r, gy = y0 + c;
+        tile[e] = (gx < hc && gy < wc) ? P.tiscr[static_cast<size_t>(f) * hc * wc + gx * wc + gy] : 0.f;
+    }
+    const int32_t* wg = P.wts + static_cast<size_t>(slot) * nscr * Tc * Tc;
+    const int wn = nscr * 2 * Tc * WP;
+    for (int e = threadIdx.x; e < wn; e += CCF_THREADS) {
+        const int f = e / (2 * Tc * WP);
+        const int k = (e / (Tc * WP)) & 1;
+        const int i = (e / WP) % Tc;
+        const int j = e % WP;
+        float v = 0.f;
+        if (k < nr && i < rc[k].h && j < rc[k].w)
+            v = static_cast<float>(wg[f * Tc * Tc + (rc[k].s0 + i) * Tc + rc[k].t0 + j]);
+        wpk[e] = v;
+    }
+    __syncthreads();
+
+    const int tr = threadIdx.x >> 3, tcg = (threadIdx.x & 7) * CCF_RY;
+    float acc[CCF_RY];
+#pragma unroll
+    for (int b = 0; b < CCF_RY; ++b) acc[b] = 0.f;
+    for (int f = 0; f < nscr; ++f) {
+        for (int k = 0; k < nr; ++k) {
+            const Rect R = rc[k];
+            const float* tb = tile + f * SH * SW + (tr + R.s0) * SW + tcg + R.t0;
+            const float* wb = wpk + (f * 2 + k) * Tc * WP;
+            for (int i = 0; i < R.h; ++i) {
+                const float* trow = tb + i * SW;
+                const float* wrow = wb + i * WP;
+                for (int j = 0; j < R.w; j += 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(wrow + j);
+                    float v[CCF_RY + 3];
+#pragma unroll
+                    for (int q = 0; q < CCF_RY + 3; ++q) v[q] = trow[j + q];
+#pragma unroll
+                    for (int b = 0; b < CCF_RY; ++b) {
+                        acc[b] = fmaf(v[b], w4.x, acc[b]);
+                        acc[b] = fmaf(v[b + 1], w4.y, acc[b]);
+                        acc[b] = fmaf(v[b + 2], w4.z, acc[b]);
+                        acc[b] = fmaf(v[b + 3], w4.w, acc[b]);
+                    }
+                }
+            }
+        }
+    }
+    const int x = x0 + tr;
+    if (x < P.out_h) {
+        int32_t* out = P.scores + static_cast<size_t>(slot) * P.npos + static_cast<size_t>(x) * P.out_w;
+#pragma unroll
+        for (int b = 0; b < CCF_RY; ++b) {
+            const int y = y0 + tcg + b;
+            if (y < P.out_w) out[y] = __float2int_rn(acc[b]);
+        }
+    }
+}
+
+// ------------------------------------------------------- select+paste ----
+
+constexpr int SEL_T = 256;
+constexpr int GCAP = 1024;
+constexpr int KMAX = 8192;
+
+struct SelLayout {
+    size_t hist, misc, redd, redi, gkey, gidx, tkey, tidx, exist, outp, from, dp, seam, total;
+};
+
+__host__ __device__ inline SelLayout sel_layout(int K, int T, int OV) {
+    SelLayout L{};
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = (o + bytes + 15) & ~static_cast<size_t>(15);
+        return at;
+    };
+    L.hist = take(256 * 4);
+    L.misc = take(16 * 4);
+    L.redd = take(32 * 8);
+    L.redi = take(64 * 4);
+    L.gkey = take(static_cast<size_t>(GCAP + SEL_T + K) * 8);
+    L.gidx = take(static_cast<size_t>(GCAP + SEL_T + K) * 4);
+    L.tkey = take(static_cast<size_t>(K) * 8);
+    L.tidx = take(static_cast<size_t>(K) * 4);
+    L.exist = take(static_cast<size_t>(T) * T);
+    L.outp = take(static_cast<size_t>(T) * T);
+    L.from = take(static_cast<size_t>(T) * OV * 2);
+    L.dp = take(static_cast<size_t>(2) * OV * 4);
+    L.seam = take(static_cast<size_t>(T) * 4);
+    L.total = o;
+    return L;
+}
+
+// Exact K-th largest value (with multiplicity) of n int32 scores: block-wide
+// radix select over the offset range, 8 bits per pass, warp-aggregated
+// shared-memory histograms.
+__device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, int* hist,
+                                 int* misc, int* redi) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        const int v = sc[p];
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    lo = block_reduce(lo, [](int a, int b) { return min(a, b); }, redi);
+    hi = block_reduce(hi, [](int a, int b) { return max(a, b); }, redi);
+    const uint32_t range = static_cast<uint32_t>(hi) - static_cast<uint32_t>(lo);
+    if (range == 0) return lo;
+    const int nbits = 32 - __clz(range);
+    const int passes = (nbits + 7) / 8;
+    uint32_t prefix = 0;
+    int krem = K;
+    for (int ps = passes - 1; ps >= 0; --ps) {
+        const int shift = ps * 8;
+        for (int e = threadIdx.x; e < 256; e += blockDim.x) hist[e] = 0;
+        __syncthreads();
+        for (int base = 0; base < n; base += blockDim.x) {
+            const int p = base + threadIdx.x;
+            bool match = false;
+            int dg = 0;
+            if (p < n) {
+                const uint32_t u = static_cast<uint32_t>(sc[p]) - static_cast<uint32_t>(lo);
+                match = (static_cast<uint64_t>(u) >> (shift + 8)) ==
+                        (static_cast<uint64_t>(prefix) >> (shift + 8));
+                dg = (u >> shift) & 255;
+            }
+            const unsigned mm = __ballot_sync(0xffffffffu, match);
+            if (match) {
+                const unsigned grp = __match_any_sync(mm, dg);
+                if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&hist[dg], __popc(grp));
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int cum = 0, d = 255;
+            for (; d > 0; --d) {
+                if (cum + hist[d] >= krem) break;
+                cum += hist[d];
+            }
+            misc[0] = d;
+            misc[1] = krem - cum;
+        }
+        __syncthreads();
+        prefix |= static_cast<uint32_t>(misc[0]) << shift;
+        krem = misc[1];
+        __syncthreads();
+    }
+    return static_cast<int>(static_cast<uint32_t>(lo) + prefix);
+}
+
+// fp64 rescoring of one window in the reference's exact order:
+//   acc = 0; for f: for run (row-major): sum = 0; sum += ti*or over the run;
+//   acc += sum          (matcher.hpp:64-81, 158-161)
+// and, for normalized scoring, the masked squares (matcher.hpp:84-100,
+// 163-171) and acc / sqrt(norm).
+__device__ double rescore(const SimParams& P, const Job& jb, const double* __restrict__ tm,
+                          int pos) {
+    const int x = pos / P.out_w, y = pos - x * P.out_w;
+    const int Tc = P.Tc;
+    double acc = 0.0;
+    for (int ch = 0; ch < P.nch; ++ch) {
+        const double* tip = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc;
+        const double* tmp = tm + ch * Tc * Tc;
+        for (int s = 0; s < Tc; ++s) {
+            int t0, t1;
+            mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+            if (t1 <= t0) continue;
+            const double* a = tip + static_cast<size_t>(x + s) * P.wc + y;
+            const double* b = tmp + s * Tc;
+            double sum = 0.0;
+            for (int t = t0; t < t1; ++t) sum = __dadd_rn(sum, __dmul_rn(a[t], b[t]));
+            acc = __dadd_rn(acc, sum);
+        }
+    }
+    if (P.scoring != 1) return acc;
+    double nrm = 0.0;
+    for (int ch = 0; ch < P.nch; ++ch) {
+        const double* tip = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc;
+        for (int s = 0; s < Tc; ++s) {
+            int t0, t1;
+            mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+            if (t1 <= t0) continue;
+            const double* a = tip + static_cast<size_t>(x + s) * P.wc + y;
+            double sum = 0.0;
+            for (int t = t0; t < t1; ++t) sum = __dadd_rn(sum, __dmul_rn(a[t], a[t]));
+            nrm = __dadd_rn(nrm, sum);
+        }
+    }
+    return nrm > 0.0 ? __ddiv_rn(acc, __dsqrt_rn(nrm)) : 0.0;
+}
+
+// Reference ranking: higher score first, earlier row-major location on ties
+// (matcher.hpp:189-198 -- the result is a prefix of the stable sort).
+__device__ __forceinline__ bool better(double ka, int ia, double kb, int ib) {
+    return ka > kb || (ka == kb && ia < ib);
+}
+
+// Monotone min-cost seam (simulator.hpp:286-320) with the reference tie rules;
+// dp rows in shared memory, one thread per band column, thread 0 backtracks.
+template <typename CostF>
+__device__ void seam_dp(int layers, int width, CostF cost, int16_t* from, int* dp, int* seam) {
+    for (int j = threadIdx.x; j < width; j += blockDim.x) dp[j] = cost(0, j);
+    __syncthreads();
+    for (int l = 1; l < layers; ++l) {
+        const int* prev = dp + ((l - 1) & 1) * width;
+        int* cur = dp + (l & 1) * width;
+        for (int j = threadIdx.x; j < width; j += blockDim.x) {
+            int best = prev[j], arg = j;
+            if (j > 0 && prev[j - 1] < best) {
+                best = prev[j - 1];
+                arg = j - 1;
+            }
+            if (j + 1 < width && prev[j + 1] < best) {
+                best = prev[j + 1];
+                arg = j + 1;
+            }
+            if (j > 0 && prev[j - 1] == best && j - 1 < arg) arg = j - 1;
+            cur[j] = cost(l, j) + best;
+            from[l * width + j] = static_cast<int16_t>(arg);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int* last = dp + ((layers - 1) & 1) * width;
+        int end = 0;
+        for (int j = 1; j < width; ++j)
+            if (last[j] < last[end]) end = j;
+        seam[layers - 1] = end;
+        for (int l = layers - 1; l > 0; --l) seam[l - 1] = from[l * width + seam[l]];
+    }
+    __syncthreads();
+}
+
+// min_cut_stitch (simulator.hpp:328-374) on T x T patches in shared memory:
+// `outp` holds the incoming patch on entry and the stitched patch on exit.
+__device__ void min_cut_device(const uint8_t* exist, uint8_t* outp, int T, int OV, int shape,
+                               int vleft, int htop, int16_t* from, int* dp, int* seam) {
+    if (shape == kNone) return;
+    if (shape == kVertical || shape == kL) {
+        const int c0 = vleft ? 0 : T - OV;
+        seam_dp(T, OV,
+                [&](int r, int j) { return exist[r * T + c0 + j] != outp[r * T + c0 + j] ? 1 : 0; },
+                from, dp, seam);
+        for (int e = threadIdx.x; e < T * OV; e += blockDim.x) {
+            const int r = e / OV, j = e - r * OV;
+            const bool keep = vleft ? j < seam[r] : j > seam[r];
+            if (keep) outp[r * T + c0 + j] = exist[r * T + c0 + j];
+        }
+        __syncthreads();
+    }
+    if (shape == kHorizontal || shape == kL) {
+        const int r0 = htop ? 0 : T - OV;
+        seam_dp(T, OV,
+                [&](int c, int j) { return exist[(r0 + j) * T + c] != outp[(r0 + j) * T + c] ? 1 : 0; },
+                from, dp, seam);
+        for (int e = threadIdx.x; e < T * OV; e += blockDim.x) {
+            const int c = e / OV, j = e - c * OV;
+            const bool keep = htop ? j < seam[c] : j > seam[c];
+            if (keep) outp[(r0 + j) * T + c] = exist[(r0 + j) * T + c];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
+                                                             const Job* __restrict__ jobs,
+                                                             int job0, int use_screen) {
+    extern __shared__ __align__(16) unsigned char sel_sm[];
+    const SelLayout L = sel_layout(P.K, P.T, P.OV);
+    int* hist = reinterpret_cast<int*>(sel_sm + L.hist);
+    int* misc = reinterpret_cast<int*>(sel_sm + L.misc);
+    double* redd = reinterpret_cast<double*>(sel_sm + L.redd);
+    int* redi = reinterpret_cast<int*>(sel_sm + L.redi);
+    double* gkey = reinterpret_cast<double*>(sel_sm + L.gkey);
+    int* gidx = reinterpret_cast<int*>(sel_sm + L.gidx);
+    double* tkey = reinterpret_cast<double*>(sel_sm + L.tkey);
+    int* tidx = reinterpret_cast<int*>(sel_sm + L.tidx);
+    uint8_t* exist = sel_sm + L.exist;
+    uint8_t* outp = sel_sm + L.outp;
+    int16_t* from = reinterpret_cast<int16_t*>(sel_sm + L.from);
+    int* dp = reinterpret_cast<int*>(sel_sm + L.dp);
+    int* seam = reinterpret_cast<int*>(sel_sm + L.seam);
+
+    const int gj = job0 + blockIdx.x;
+    const Job jb = jobs[gj];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int fr, fc;
+    if (jb.shape == kNone) {
+        fr = jb.fr;
+        fc = jb.fc;
+    } else {
+        const int32_t* sc = P.scores + static_cast<size_t>(blockIdx.x) * P.npos;
+        const double* tm = P.tm64 + static_cast<size_t>(blockIdx.x) * P.nch * P.Tc * P.Tc;
+        const int K = P.K;
+        // 1. exact screen threshold: every window whose integer score reaches
+        //    the K-th largest can appear in the reference's top-K.
+        const bool all = !use_screen;
+        const int thr = all ? 0 : radix_kth_largest(sc, P.npos, K, hist, misc, redi);
+        // 2. gather the tie group in row-major chunks, rescore in fp64, keep the
+        //    running top-K by (fp64 desc, index asc).
+        int ntop = 0, cnt = 0;
+        for (int base = 0; base < P.npos; base += SEL_T) {
+            const int p = base + tid;
+            const bool q = p < P.npos && (all || sc[p] >= thr);
+            const unsigned bal = __ballot_sync(0xffffffffu, q);
+            if (lane == 0) redi[wid] = __popc(bal);
+            __syncthreads();
+            int off = 0, tot = 0;
+            for (int w = 0; w < SEL_T / 32; ++w) {
+                if (w < wid) off += redi[w];
+                tot += redi[w];
+            }
+            if (q) gidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
+            cnt += tot;
+            __syncthreads();
+            const bool last = base + SEL_T >= P.npos;
+            if (cnt + SEL_T > GCAP || (last && cnt > 0)) {
+                for (int e = tid; e < cnt; e += SEL_T) gkey[e] = rescore(P, jb, tm, gidx[e]);
+                for (int e = tid; e < ntop; e += SEL_T) {
+                    gkey[cnt + e] = tkey[e];
+                    gidx[cnt + e] = tidx[e];
+                }
+                __syncthreads();
+                const int n = cnt + ntop;
+                const int keep = min(K, n);
+                for (int round = 0; round < keep; ++round) {
+                    double bk = 0.0;
+                    int bi = INT_MAX, bp = -1;
+                    for (int e = tid; e < n; e += SEL_T) {
+                        const int ix = gidx[e];
+                        if (ix >= 0 && (bp < 0 || better(gkey[e], ix, bk, bi))) {
+                            bk = gkey[e];
+                            bi = ix;
+                            bp = e;
+                        }
+                    }
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                        if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
+                            bk = ok;
+                            bi = oi;
+                            bp = op;
+                        }
+                    }
+                    if (lane == 0) {
+                        redd[wid] = bk;
+                        redi[wid] = bi;
+                        redi[32 + wid] = bp;
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        for (int w = 1; w < SEL_T / 32; ++w) {
+                            if (redi[32 + w] >= 0 &&
+                                (bp < 0 || better(redd[w], redi[w], bk, bi))) {
+                                bk = redd[w];
+                                bi = redi[w];
+                                bp = redi[32 + w];
+                            }
+                        }
+                        tkey[round] = bk;
+                        tidx[round] = bi;
+                        gidx[bp] = -1;
+                    }
+                    __syncthreads();
+                }
+                ntop = keep;
+                cnt = 0;
+                __syncthreads();
+            }
+        }
+        // 3. choose (matcher.hpp:207-241)
+        int pick = jb.pick;
+        if (pick < 0) {
+            int best = 0, best_mis = INT_MAX;
+            pick = -1;
+            for (int c = 0; c < ntop; ++c) {
+                const int pos = tidx[c];
+                const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
+                int mis = 0;
+                for (int e = tid; e < P.T * P.T; e += SEL_T) {
+                    const int r = e / P.T, cc = e - r * P.T;
+                    const uint8_t hv = P.hd[static_cast<size_t>(jb.top + r) * P.ww + jb.left + cc];
+                    if (hv != kNoDatum && P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != hv)
+                        ++mis;
+                }
+                mis = block_reduce(mis, [](int a, int b) { return a + b; }, redi);
+                if (mis == 0) {
+                    pick = c;
+                    break;
+                }
+                if (mis < best_mis) {
+                    best = c;
+                    best_mis = mis;
+                }
+            }
+            if (pick < 0) pick = best;
+        }
+        const int pos = tidx[pick];
+        fr = (pos / P.out_w) << P.J;
+        fc = (pos % P.out_w) << P.J;
+        __syncthreads();
+    }
+
+    // 4. crop + optional stitch + paste (simulator.hpp:483-493)
+    const int T = P.T;
+    uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
+    uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
+    if (P.min_cut && jb.shape != kNone) {
+        for (int e = tid; e < T * T; e += SEL_T) {
+            const int r = e / T, c = e - r * T;
+            exist[e] = g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c];
+            outp[e] = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+        }
+        __syncthreads();
+        min_cut_device(exist, outp, T, P.OV, jb.shape, jb.vleft, jb.htop, from, dp, seam);
+        for (int e = tid; e < T * T; e += SEL_T) {
+            const int r = e / T, c = e - r * T;
+            g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = outp[e];
+            if (trace) trace[e] = outp[e];
+        }
+    } else {
+        for (int e = tid; e < T * T; e += SEL_T) {
+            const int r = e / T, c = e - r * T;
+            const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+            g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
+            if (trace) trace[e] = v;
+        }
+    }
+    if (tid == 0) {
+        P.chosen[2 * gj] = fr;
+        P.chosen[2 * gj + 1] = fc;
+    }
+}
+
+// ----------------------------------------------------------- finalize ----
+
+__global__ void hd_scatter_kernel(const int32_t* __restrict__ hd, int n_hd, uint8_t* plane, int ww) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_hd) plane[static_cast<size_t>(hd[3 * i]) * ww + hd[3 * i + 1]] = static_cast<uint8_t>(hd[3 * i + 2]);
+}
+
+// Hard-data overwrite with pre-overwrite mismatch count, then the crop to
+// the simulation grid (simulator.hpp:506-515).
+__global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww,
+                                const uint8_t* __restrict__ hd, int sg_h, int sg_w,
+                                uint8_t* __restrict__ out, int* mism) {
+    const size_t n = static_cast<size_t>(sg_h) * sg_w;
+    const int r = blockIdx.y;
+    const uint8_t* g = work + static_cast<size_t>(r) * wh * ww;
+    int local = 0;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(e / sg_w), x = static_cast<int>(e - static_cast<size_t>(y) * sg_w);
+        uint8_t v = g[static_cast<size_t>(y) * ww + x];
+        if (hd) {
+            const uint8_t h = hd[static_cast<size_t>(y) * ww + x];
+            if (h != kNoDatum) {
+                local += v != h;
+                v = h;
+            }
+        }
+        out[static_cast<size_t>(r) * n + e] = v;
+    }
+    if (hd) {
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
+    }
+}
+
+// min_cut_stitch as a stand-alone operator (the drop-in API surface).
+__global__ void __launch_bounds__(256) min_cut_op_kernel(const uint8_t* __restrict__ ex,
+                                                         const uint8_t* __restrict__ inc, int T,
+                                                         int OV, int shape, int vleft, int htop,
+                                                         uint8_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char mc_sm[];
+    const SelLayout L = sel_layout(1, T, OV);
+    uint8_t* exist = mc_sm + L.exist;
+    uint8_t* outp = mc_sm + L.outp;
+    int16_t* from = reinterpret_cast<int16_t*>(mc_sm + L.from);
+    int* dp = reinterpret_cast<int*>(mc_sm + L.dp);
+    int* seam = reinterpret_cast<int*>(mc_sm + L.seam);
+    for (int e = threadIdx.x; e < T * T; e += blockDim.x) {
+        exist[e] = ex[e];
+        outp[e] = inc[e];
+    }
+    __syncthreads();
+    min_cut_device(exist, outp, T, OV, shape, vleft, htop, from, dp, seam);
+    for (int e = threadIdx.x; e < T * T; e += blockDim.x) out[e] = outp[e];
+}
+
+void op_min_cut_stitch(ccw_ctx* ctx, const uint8_t* existing, const uint8_t* incoming, int t,
+                       int shape, int vleft, int htop, int overlap, uint8_t* out) {
+    const size_t n = static_cast<size_t>(t) * t;
+    const int ov = std::max(overlap, 1);
+    uint8_t* d = ctx->ops_a.as<uint8_t>(3 * n);
+    CCW_CUDA(cudaMemcpyAsync(d, existing, n, cudaMemcpyHostToDevice, ctx->stream));
+    CCW_CUDA(cudaMemcpyAsync(d + n, incoming, n, cudaMemcpyHostToDevice, ctx->stream));
+    const size_t smem = sel_layout(1, t, ov).total;
+    if (smem > 227 * 1024) throw Fail(CCW_ERR_DIMENSION, "patch too large for the stitch kernel");
+    CCW_CUDA(cudaFuncSetAttribute(min_cut_op_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    min_cut_op_kernel<<<1, 256, smem, ctx->stream>>>(d, d + n, t, ov, shape, vleft, htop, d + 2 * n);
+    CCW_CUDA(cudaGetLastError());
+    CCW_CUDA(cudaMemcpyAsync(out, d + 2 * n, n, cudaMemcpyDeviceToHost, ctx->stream));
+    CCW_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ------------------------------------------------------- host driver -----
+
+namespace {
+
+struct EventTimer {
+    ccw_ctx* ctx;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ccf, sel;
+    size_t next = 0;
+    cudaEvent_t get() {
+        if (next == ctx->ev_pool.size()) {
+            cudaEvent_t e;
+            CCW_CUDA(cudaEventCreate(&e));
+            ctx->ev_pool.push_back(e);
+        }
+        return ctx->ev_pool[next++];
+    }
+};
+
+double pair_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    double t = 0;
+    for (auto& p : v) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        t += ms;
+    }
+    return t;
+}
+
+}  // namespace
+
+void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
+                    int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out,
+                    ccw_diag* diag, ccw_trace* traces) {
+    const auto wall0 = std::chrono::steady_clock::now();
+    cudaStream_t st = ctx->stream;
+    const int T = cfg.template_size, OV = cfg.overlap, J = cfg.dwt_level, B = 1 << J;
+    const int stride = T - OV;
+    const int Tc = T >> J, OVc = OV >> J;
+    const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1;
+    const int npos = out_h * out_w;
+    const int Kp = std::min(cfg.candidates, npos);
+    if (Kp > KMAX)
+        throw Fail(CCW_ERR_CONFIG, "candidates: more than 8192 effective candidates unsupported");
+    const int reach = (T + stride - 1) / stride - 1;  // footprints overlap up to `reach` steps
+    const int keymul = reach + 1;
+
+    // ---- host schedule: plans, hard-data lattice, mt19937_64 draw schedule
+    std::vector<Plan> plans;
+    plans.reserve(n_real);
+    std::vector<std::mt19937_64> rngs;
+    rngs.reserve(n_real);
+    for (int r = 0; r < n_real; ++r) {
+        rngs.emplace_back(seeds[r]);
+        plans.push_back(make_plan(cfg, rngs.back()));
+    }
+    const int wh = plans[0].work_h, ww = plans[0].work_w;
+    const int nlr = (wh - T) / stride + 1, nlc = (ww - T) / stride + 1;
+    std::vector<uint8_t> lattice_hd;
+    if (hd && n_hd > 0) {
+        lattice_hd.assign(static_cast<size_t>(nlr) * nlc, 0);
+        for (int i = 0; i < n_hd; ++i) {
+            const int r = hd[3 * i], c = hd[3 * i + 1];
+            const int qr0 = std::max(0, (r - T + 1 + stride - 1) / stride);
+            const int qc0 = std::max(0, (c - T + 1 + stride - 1) / stride);
+            for (int qr = qr0; qr <= std::min(nlr - 1, r / stride); ++qr)
+                for (int qc = qc0; qc <= std::min(nlc - 1, c / stride); ++qc)
+                    if (r >= qr * stride && r < qr * stride + T && c >= qc * stride &&
+                        c < qc * stride + T)
+                        lattice_hd[static_cast<size_t>(qr) * nlc + qc] = 1;
+        }
+    }
+    int max_key = 0;
+    for (const Plan& p : plans) max_key = std::max(max_key, keymul * (p.n_outer - 1) + p.n_inner - 1);
+    std::vector<std::vector<Job>> waves(max_key + 1);
+    size_t total_jobs = 0;
+    for (int r = 0; r < n_real; ++r) {
+        const Plan& p = plans[r];
+        std::mt19937_64& rng = rngs[r];
+        const int cnt = static_cast<int>(p.tops.size());
+        for (int k = 0; k < cnt; ++k) {
+            Job jb{};
+            jb.real = r;
+            jb.place = k;
+            jb.top = p.tops[k];
+            jb.left = p.lefts[k];
+            jb.shape = p.shapes[k];
+            jb.vleft = p.vertical_on_left();
+            jb.htop = p.horizontal_on_top();
+            jb.pick = 0;
+            if (jb.shape == kNone) {  // simulator.hpp:450-453
+                jb.fr = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->h - T) / B + 1))) * B;
+                jb.fc = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->w - T) / B + 1))) * B;
+            } else {
+                const bool cond = !lattice_hd.empty() &&
+                                  lattice_hd[static_cast<size_t>(jb.top / stride) * nlc + jb.left / stride];
+                jb.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
+            }
+            waves[keymul * p.outer_idx[k] + p.inner_idx[k]].push_back(jb);
+            ++total_jobs;
+        }
+    }
+    std::vector<Job> flat;
+    flat.reserve(total_jobs);
+    std::vector<size_t> wave_off;
+    for (auto& w : waves) {
+        wave_off.push_back(flat.size());
+        flat.insert(flat.end(), w.begin(), w.end());
+    }
+    wave_off.push_back(flat.size());
+
+    // ---- exactness guard for the fp32 screen
+    const double maxw = ti->mode == 0 ? B : static_cast<double>(ti->F - 1) * B;
+    const double mask_cells = static_cast<double>(Tc) * OVc + static_cast<double>(Tc - OVc) * OVc;
+    const bool use_screen = cfg.scoring == 0 && ti->nscr > 0;
+    if (use_screen && mask_cells * maxw * maxw * std::max(1, ti->nscr) >= 16777216.0)
+        throw Fail(CCW_ERR_CONFIG, "configuration exceeds the exact fp32 screen range (mask*B^2 >= 2^24)");
+
+    // ---- device buffers
+    Job* d_jobs = ctx->jobs.as<Job>(flat.size());
+    CCW_CUDA(cudaMemcpyAsync(d_jobs, flat.data(), sizeof(Job) * flat.size(), cudaMemcpyHostToDevice, st));
+    const size_t plane = static_cast<size_t>(wh) * ww;
+    uint8_t* d_work = ctx->work.as<uint8_t>(plane * n_real);
+    CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
+    uint8_t* d_hd = nullptr;
+    if (hd && n_hd > 0) {
+        d_hd = ctx->hd.as<uint8_t>(plane);
+        CCW_CUDA(cudaMemsetAsync(d_hd, kNoDatum, plane, st));
+        int32_t* d_hdl = reinterpret_cast<int32_t*>(ctx->ops_e.get(sizeof(int32_t) * 3 * n_hd));
+        CCW_CUDA(cudaMemcpyAsync(d_hdl, hd, sizeof(int32_t) * 3 * n_hd, cudaMemcpyHostToDevice, st));
+        hd_scatter_kernel<<<(n_hd + 255) / 256, 256, 0, st>>>(d_hdl, n_hd, d_hd, ww);
+        CCW_CUDA(cudaGetLastError());
+    }
+    const size_t score_budget = static_cast<size_t>(512) << 20;
+    const size_t maxj = std::max<size_t>(1, std::min<size_t>(flat.size(), score_budget / (sizeof(int32_t) * npos)));
+    int32_t* d_scores = ctx->scores.as<int32_t>(maxj * npos);
+    int32_t* d_wts = ctx->wts.as<int32_t>(maxj * std::max(ti->nscr, 1) * Tc * Tc);
+    double* d_tm = ctx->tm64.as<double>(maxj * ti->nch * Tc * Tc);
+    int32_t* d_chosen = ctx->chosen.as<int32_t>(2 * flat.size());
+    const bool want_pasted = traces != nullptr;
+    for (int r = 0; traces && r < n_real; ++r) (void)r;
+    uint8_t* d_pasted = want_pasted ? ctx->pasted.as<uint8_t>(flat.size() * T * T) : nullptr;
+    int* d_mism = ctx->mism.as<int>(n_real);
+    CCW_CUDA(cudaMemsetAsync(d_mism, 0, sizeof(int) * n_real, st));
+
+    SimParams P{};
+    P.ti = ti->d_codes;
+    P.ti64 = ti->d_ti64;
+    P.tiscr = ti->d_scr;
+    P.ti_h = ti->h;
+    P.ti_w = ti->w;
+    P.hc = ti->hc;
+    P.wc = ti->wc;
+    P.F = ti->F;
+    P.J = J;
+    P.mode = ti->mode;
+    P.nch = ti->nch;
+    P.nscr = ti->nscr;
+    P.T = T;
+    P.OV = OV;
+    P.Tc = Tc;
+    P.OVc = OVc;
+    P.B = B;
+    P.out_h = out_h;
+    P.out_w = out_w;
+    P.npos = npos;
+    P.K = Kp;
+    P.scoring = cfg.scoring;
+    P.min_cut = cfg.min_cut;
+    P.work = d_work;
+    P.wh = wh;
+    P.ww = ww;
+    P.hd = d_hd;
+    P.wts = d_wts;
+    P.tm64 = d_tm;
+    P.scores = d_scores;
+    P.chosen = d_chosen;
+    P.pasted = d_pasted;
+
+    const size_t ccf_smem = ccf_smem_bytes(Tc, ti->nscr);
+    const size_t sel_smem = sel_layout(Kp, T, OV).total;
+    if (ccf_smem > 227 * 1024 || sel_smem > 227 * 1024)
+        throw Fail(CCW_ERR_CONFIG, "configuration exceeds the per-CTA shared-memory budget");
+    CCW_CUDA(cudaFuncSetAttribute(ccf_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ccf_smem)));
+    CCW_CUDA(cudaFuncSetAttribute(select_paste_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sel_smem)));
+
+    EventTimer tm{ctx, {}, {}, 0};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (ctx->profiling) {
+        ev0 = tm.get();
+        ev1 = tm.get();
+        CCW_CUDA(cudaEventRecord(ev0, st));
+    }
+    int64_t launches = 0, ccf_launches = 0;
+    double ccf_flop = 0, ccf_flop_ref = 0;
+    const dim3 ccf_grid_xy((out_w + CCF_TY - 1) / CCF_TY, (out_h + CCF_TX - 1) / CCF_TX);
+    for (size_t w = 0; w + 1 < wave_off.size(); ++w) {
+        for (size_t j0 = wave_off[w]; j0 < wave_off[w + 1]; j0 += maxj) {
+            const int nj = static_cast<int>(std::min(maxj, wave_off[w + 1] - j0));
+            const bool first_wave = flat[j0].shape == kNone;
+            if (!first_wave) {
+                or_prep_kernel<<<nj, 128, 0, st>>>(P, d_jobs, static_cast<int>(j0));
+                ++launches;
+                if (use_screen) {
+                    cudaEvent_t a = nullptr, b = nullptr;
+                    if (ctx->profiling) {
+                        a = tm.get();
+                        b = tm.get();
+                        CCW_CUDA(cudaEventRecord(a, st));
+                    }
+                    dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
+                    ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, st>>>(P, d_jobs, static_cast<int>(j0));
+                    ++launches;
+                    ++ccf_launches;
+                    if (ctx->profiling) {
+                        CCW_CUDA(cudaEventRecord(b, st));
+                        tm.ccf.push_back({a, b});
+                    }
+                    for (int q = 0; q < nj; ++q) {
+                        const int sh = flat[j0 + q].shape;
+                        const double m = sh == kL ? mask_cells : static_cast<double>(Tc) * OVc;
+                        ccf_flop += 2.0 * ti->nscr * npos * m;
+                        ccf_flop_ref += 2.0 * ti->nch * npos * m;
+                    }
+                }
+            }
+            cudaEvent_t a = nullptr, b = nullptr;
+            if (ctx->profiling) {
+                a = tm.get();
+                b = tm.get();
+                CCW_CUDA(cudaEventRecord(a, st));
+            }
+            select_paste_kernel<<<nj, SEL_T, sel_smem, st>>>(P, d_jobs, static_cast<int>(j0),
+                                                            use_screen ? 1 : 0);
+            ++launches;
+            if (ctx->profiling) {
+                CCW_CUDA(cudaEventRecord(b, st));
+                tm.sel.push_back({a, b});
+            }
+        }
+    }
+    CCW_CUDA(cudaGetLastError());
+
+    // ---- finalize
+    uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
+    {
+        const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
+        const int bx = static_cast<int>(std::min<size_t>((n + 255) / 256, 1024));
+        finalize_kernel<<<dim3(bx, n_real), 256, 0, st>>>(d_work, wh, ww, d_hd, cfg.sg_height,
+                                                          cfg.sg_width, fin, d_mism);
+        ++launches;
+        CCW_CUDA(cudaGetLastError());
+    }
+    if (ctx->profiling) CCW_CUDA(cudaEventRecord(ev1, st));
+    if (h_out)
+        CCW_CUDA(cudaMemcpyAsync(h_out, fin, static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real,
+                                 cudaMemcpyDeviceToHost, st));
+    std::vector<int> mism(n_real, 0);
+    CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> chosen;
+    std::vector<uint8_t> pasted;
+    if (traces) {
+        chosen.resize(2 * flat.size());
+        CCW_CUDA(cudaMemcpyAsync(chosen.data(), d_chosen, sizeof(int32_t) * chosen.size(),
+                                 cudaMemcpyDeviceToHost, st));
+        pasted.resize(flat.size() * T * T);
+        CCW_CUDA(cudaMemcpyAsync(pasted.data(), d_pasted, pasted.size(), cudaMemcpyDeviceToHost, st));
+    }
+    CCW_CUDA(cudaStreamSynchronize(st));
+
+    if (ctx->profiling) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        ctx->timing.total_ms = ms;
+        ctx->timing.ccf_ms = pair_ms(tm.ccf);
+        ctx->timing.select_ms = pair_ms(tm.sel);
+    } else {
+        ctx->timing.total_ms = ctx->timing.ccf_ms = ctx->timing.select_ms = 0;
+    }
+    ctx->timing.ccf_launches = ccf_launches;
+    ctx->timing.launches = launches + (d_hd ? 1 : 0) + 0;
+    ctx->timing.ccf_flop = ccf_flop;
+    ctx->timing.ccf_flop_ref = ccf_flop_ref;
+    ctx->timing.waves = static_cast<int64_t>(wave_off.size() - 1);
+    ctx->timing.jobs = static_cast<int64_t>(flat.size());
+
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    for (int r = 0; r < n_real; ++r) {
+        if (diag) {
+            ccw_diag& d = diag[r];
+            d.seed = seeds[r];
+            d.origin = plans[r].origin;
+            d.column_major = plans[r].column_major;
+            d.work_height = wh;
+            d.work_width = ww;
+            d.placement_count = static_cast<int>(plans[r].tops.size());
+            d.hard_data_count = hd ? n_hd : 0;
+            d.pre_overwrite_mismatches = mism[r];
+            d._pad = 0;
+            d.wall_seconds = wall;
+        }
+        if (traces) {
+            ccw_trace& tr = traces[r];
+            tr.count = 0;
+            (void)tr;
+        }
+    }
+    if (traces) {
+        // flat is wave-ordered; rebuild each realization's raster-ordered trace
+        for (size_t g = 0; g < flat.size(); ++g) {
+            const Job& jb = flat[g];
+            ccw_trace& tr = traces[jb.real];
+            if (jb.place >= tr.capacity) continue;
+            tr.top[jb.place] = jb.top;
+            tr.left[jb.place] = jb.left;
+            tr.shape[jb.place] = jb.shape;
+            tr.ti_row[jb.place] = chosen[2 * g];
+            tr.ti_col[jb.place] = chosen[2 * g + 1];
+            if (tr.pasted)
+                std::memcpy(tr.pasted + static_cast<size_t>(jb.place) * T * T, pasted.data() + g * T * T,
+                            static_cast<size_t>(T) * T);
+        }
+        for (int r = 0; r < n_real; ++r)
+            traces[r].count = std::min(traces[r].capacity, static_cast<int>(plans[r].tops.size()));
+    }
+}
+
+}  // namespace ccwgpu

@@ -1,0 +1,188 @@
+"""Parity of the CUDA simulation path (libccwgpu.so) with the reference:
+bit-identical realizations, diagnostics and provenance traces against the
+reference's own outputs (tests/golden) and against the oracle restatement on a
+seeded corpus; size-independent properties at the BASELINE configs' sizes."""
+import numpy as np
+import pytest
+
+import pyoracle
+from _golden import load, sim_cases
+from paper_2404_00441_b200 import ccwsim as cs
+
+pytestmark = pytest.mark.gpu
+
+
+def to_cfg(d, hd=None):
+    names = {0: "raw", 1: "normalized"}
+    modes = {0: "indicator", 1: "raw_codes"}
+    cfg = cs.SimConfig(sg_height=d["sg_height"], sg_width=d["sg_width"],
+                       template_size=d["template_size"], overlap=d["overlap"],
+                       dwt_level=d["dwt_level"], candidates=d["candidates"],
+                       n_realizations=d.get("n_realizations", 1),
+                       master_seed=d.get("master_seed", 0), scoring=names[d.get("scoring", 0)],
+                       facies_mode=modes[d.get("facies_mode", 0)],
+                       min_cut=bool(d.get("min_cut", 0)))
+    if hd:
+        cfg.hard_data = cs.HardDataSet([cs.HardDatum(*p) for p in hd])
+    return cfg
+
+
+@pytest.mark.parametrize("case", sim_cases(), ids=lambda c: c["name"])
+def test_golden_realizations_bit_exact(case):
+    ti = cs.CategoricalGrid(case["ti"].shape[0], case["ti"].shape[1], case["nf"], case["ti"])
+    cfg = to_cfg(case["cfg"], case["hd"])
+    traces = [cs.SimTrace() for _ in case["seeds"]]
+    res = cs.simulate_batch(ti, cfg, case["seeds"], traces)
+    for i, r in enumerate(res):
+        assert np.array_equal(r.realization.cells, case["real"][i])
+        assert r.diagnostics.pre_overwrite_mismatches == case["mism"][i]
+        assert r.diagnostics.origin == case["origin"][i]
+        assert int(r.diagnostics.column_major) == case["colmajor"][i]
+        assert [e.ti_row for e in traces[i].events] == case["ti_row"][i].tolist()
+        assert [e.ti_col for e in traces[i].events] == case["ti_col"][i].tolist()
+
+
+def test_golden_ensemble():
+    z = load("ensemble_channel64.npz")
+    ti = cs.CategoricalGrid(64, 64, 2, z["ti"])
+    cfg = cs.SimConfig(64, 64, 16, 4, 2, 4, n_realizations=6, master_seed=int(z["master"]))
+    res = cs.simulate_ensemble(ti, cfg, workers=4)
+    assert np.array_equal(np.stack([r.realization.cells for r in res]), z["real"])
+
+
+def random_case(rng, trial):
+    J = int(rng.integers(1, 4))
+    b = 1 << J
+    T = b * int(rng.integers(2, 7))
+    OV = b * int(rng.integers(1, T // b))
+    nf = int(rng.integers(1, 6))
+    H = b * int(rng.integers(T // b + 1, 128 // b + 1))
+    W = b * int(rng.integers(T // b + 1, 128 // b + 1))
+    if trial % 2:
+        ti = rng.integers(0, nf, (H, W)).astype(np.uint8)
+    else:  # blocky TI -> many exact score ties
+        ti = np.repeat(np.repeat(rng.integers(0, nf, (H // b, W // b)), b, 0), b, 1).astype(np.uint8)
+    sg_h, sg_w = int(rng.integers(T, 96)), int(rng.integers(T, 96))
+    d = dict(sg_height=sg_h, sg_width=sg_w, template_size=T, overlap=OV, dwt_level=J,
+             candidates=int(rng.integers(1, 12)), scoring=int(rng.integers(0, 2)) if trial % 4 == 0 else 0,
+             facies_mode=int(rng.integers(0, 2)), min_cut=int(rng.integers(0, 2)))
+    hd = None
+    if trial % 3 == 0:
+        cells = rng.choice(sg_h * sg_w, size=int(rng.integers(1, 30)), replace=False)
+        hd = [(int(c // sg_w), int(c % sg_w), int(rng.integers(0, nf))) for c in cells]
+    return ti, nf, d, hd
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_randomized_corpus_vs_oracle(oracle, block):
+    rng = np.random.default_rng(1000 + block)
+    for trial in range(12):
+        ti_a, nf, d, hd = random_case(rng, trial)
+        ti = cs.CategoricalGrid(ti_a.shape[0], ti_a.shape[1], nf, ti_a)
+        cfg = to_cfg(d, hd)
+        seeds = [int(s) for s in rng.integers(0, 2**63, 3)]
+        res = cs.simulate_batch(ti, cfg, seeds)
+        for s, r in zip(seeds, res):
+            o = oracle.simulate_one(ti_a, nf, pyoracle.Cfg(**d), hd, seed=s)
+            assert np.array_equal(r.realization.cells, o["realization"]), (block, trial, d)
+            assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+
+
+def test_large_k_and_conditioning(oracle):
+    # acceptance.cpp:383-436 shape: K=64 and dense hard data from a reference realization
+    ti_a = pyoracle.reference().make_channel_ti(256, 256, 2026) if pyoracle.reference_available() \
+        else load("sim_channel128_J3.npz")["ti"]
+    ti = cs.CategoricalGrid(ti_a.shape[0], ti_a.shape[1], 2, ti_a)
+    d = dict(sg_height=256, sg_width=256, template_size=32, overlap=8, dwt_level=2, candidates=64)
+    ref_real = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=777)["realization"]
+    rng = np.random.default_rng(606)
+    cells = rng.choice(256 * 256, size=1000, replace=False)
+    hd = [(int(c // 256), int(c % 256), int(ref_real[c // 256, c % 256])) for c in cells]
+    cfg = to_cfg(d, hd)
+    res = cs.simulate_batch(ti, cfg, [11, 12])
+    for s, r in zip([11, 12], res):
+        o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), hd, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"])
+        assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+        assert all(r.realization.cells[a, b] == f for a, b, f in hd)
+        assert r.diagnostics.pre_overwrite_mismatch_rate() < 0.10
+
+
+def test_provenance_and_replay():
+    # test_simulator.cpp:434-460, acceptance.cpp:349-381
+    z = load("sim_channel64_base.npz")
+    ti = cs.CategoricalGrid(64, 64, 2, z["ti"])
+    cfg = cs.SimConfig(52, 64, 16, 4, 2, 6)
+    tr = cs.SimTrace()
+    res = cs.simulate_one(ti, cfg, 2024, tr)
+    replay = np.zeros((res.diagnostics.work_height, res.diagnostics.work_width), np.uint8)
+    for ev in tr.events:
+        assert ev.ti_row % 4 == 0 and ev.ti_col % 4 == 0
+        assert np.array_equal(ev.pasted.cells, z["ti"][ev.ti_row:ev.ti_row + 16, ev.ti_col:ev.ti_col + 16])
+        replay[ev.placement.top:ev.placement.top + 16, ev.placement.left:ev.placement.left + 16] = ev.pasted.cells
+    assert np.array_equal(replay[:52, :64], res.realization.cells)
+
+
+def test_constant_ti_and_determinism():
+    # test_simulator.cpp:401-432
+    ti = cs.CategoricalGrid(32, 32, 2, fill=1)
+    cfg = cs.SimConfig(48, 48, 16, 4, 2, 4)
+    assert (cs.simulate_one(ti, cfg, 999).realization.cells == 1).all()
+    z = load("sim_channel64_base.npz")
+    ti = cs.CategoricalGrid(64, 64, 2, z["ti"])
+    cfg = cs.SimConfig(64, 64, 16, 4, 2, 4)
+    a = cs.simulate_one(ti, cfg, 31337)
+    b = cs.simulate_one(ti, cfg, 31337)
+    c = cs.simulate_one(ti, cfg, 31338)
+    assert a.realization == b.realization and a.realization != c.realization
+    assert a.diagnostics.seed == 31337 and a.diagnostics.placement_count > 0
+
+
+def test_batch_equals_single():
+    z = load("sim_channel64_base.npz")
+    ti = cs.CategoricalGrid(64, 64, 2, z["ti"])
+    cfg = cs.SimConfig(64, 64, 16, 4, 2, 4, min_cut=True)
+    seeds = [5, 6, 7, 8, 9]
+    batch = cs.simulate_batch(ti, cfg, seeds)
+    for s, r in zip(seeds, batch):
+        assert r.realization == cs.simulate_one(ti, cfg, s).realization
+
+
+@pytest.mark.slow
+def test_config1_full_size_bit_exact(oracle):
+    """BASELINE config 1 geometry (TI 500^2, 3 facies, SG 1000^2, T64, OV16,
+    J2, K5): two realizations bit-identical to the oracle."""
+    from paper_2404_00441_b200 import synth
+    ti_a = synth.config1_ti()
+    ti = cs.CategoricalGrid(500, 500, 3, ti_a)
+    cfg = cs.SimConfig(1000, 1000, 64, 16, 2, 5)
+    seeds = [cs.mix64(0, 1), cs.mix64(0, 2)]
+    res = cs.simulate_batch(ti, cfg, seeds)
+    for s, r in zip(seeds, res):
+        o = oracle.simulate_one(ti_a, 3, pyoracle.Cfg(**cfg_dict(cfg)), None, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"])
+
+
+@pytest.mark.slow
+def test_config2_full_size_bit_exact(oracle):
+    """BASELINE config 2 geometry (TI 2000^2, SG 4000^2, T96, OV24, J3, K1,
+    1% hard data): one realization bit-identical to the oracle."""
+    from paper_2404_00441_b200 import synth
+    ti_a = synth.config2_ti()
+    hd = synth.config2_hard_data(ti_a)
+    ti = cs.CategoricalGrid(2000, 2000, 2, ti_a)
+    cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1)
+    cfg.hard_data = hd
+    seed = cs.mix64(0, 1)
+    r = cs.simulate_one(ti, cfg, seed)
+    o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**cfg_dict(cfg)), hd, seed=seed)
+    assert np.array_equal(r.realization.cells, o["realization"])
+    assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+    assert (r.realization.cells[hd[:, 0], hd[:, 1]] == hd[:, 2]).all()
+
+
+def cfg_dict(cfg):
+    c = cfg.to_c()
+    return dict(sg_height=c.sg_height, sg_width=c.sg_width, template_size=c.template_size,
+                overlap=c.overlap, dwt_level=c.dwt_level, candidates=c.candidates,
+                scoring=c.scoring, facies_mode=c.facies_mode, min_cut=bool(c.min_cut))
