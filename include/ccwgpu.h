@@ -109,6 +109,10 @@ typedef struct ccw_timing {
     double ccf_flop_ref;    /* same count with the reference's F channels          */
     int64_t waves;
     int64_t jobs;
+    int64_t rescored;       /* windows rescored in fp64 (the exact-score tie groups)   */
+    int64_t screened_jobs;  /* placements that went through the CCF screen            */
+    int64_t ccf_variant;    /* 0 none (normalized / F=1), 1 fp32 direct, 2 tcgen05 int8 */
+    double ccf_mma_flop;    /* tensor-core MMA FLOP issued (full Tc x Tc window, padded K) */
 } ccw_timing;
 
 typedef struct ccw_ctx ccw_ctx;
@@ -122,7 +126,8 @@ CCW_API const char* ccw_last_error(const ccw_ctx* ctx);
 CCW_API void* ccw_ctx_stream(ccw_ctx* ctx);
 CCW_API ccw_status ccw_ctx_set_profiling(ccw_ctx* ctx, int enabled);
 CCW_API ccw_status ccw_ctx_last_timing(ccw_ctx* ctx, ccw_timing* out);
-/* Selects the CCF screen kernel: 0 = auto, 1 = fp32 CUDA-core direct. */
+/* Selects the CCF screen kernel: 0 = auto (tcgen05 int8 when the block
+ * counts fit int8, else fp32), 1 = fp32 CUDA-core direct, 2 = tcgen05 int8. */
 CCW_API ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant);
 
 /* FP32 FFMA peak of this GPU (TFLOP/s), measured with an in-library

@@ -40,7 +40,9 @@ class TraceC(C.Structure):
 class TimingC(C.Structure):
     _fields_ = [("total_ms", C.c_double), ("ccf_ms", C.c_double), ("select_ms", C.c_double),
                 ("ccf_launches", C.c_int64), ("launches", C.c_int64), ("ccf_flop", C.c_double),
-                ("ccf_flop_ref", C.c_double), ("waves", C.c_int64), ("jobs", C.c_int64)]
+                ("ccf_flop_ref", C.c_double), ("waves", C.c_int64), ("jobs", C.c_int64),
+                ("rescored", C.c_int64), ("screened_jobs", C.c_int64), ("ccf_variant", C.c_int64),
+                ("ccf_mma_flop", C.c_double)]
 
 
 P = C.c_void_p

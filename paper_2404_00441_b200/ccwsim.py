@@ -306,6 +306,10 @@ class Device:
         self.check(self._lib.ccw_ctx_last_timing(self.handle, C.byref(t)))
         return {k: getattr(t, k) for k, _ in _abi.TimingC._fields_}
 
+    def set_ccf_variant(self, variant: int) -> None:
+        """0 auto (tcgen05 int8 when it is exact), 1 fp32 CUDA-core, 2 tcgen05 int8."""
+        self.check(self._lib.ccw_ctx_set_ccf_variant(self.handle, int(variant)))
+
     def measure_fp32_peak(self) -> float:
         """FP32 FFMA peak of this GPU in TFLOP/s (in-library microbenchmark)."""
         v = C.c_double(0)

@@ -210,9 +210,10 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (ccwgpu::DevBuf* b : {&ctx->jobs, &ctx->work, &ctx->hd, &ctx->wts, &ctx->tm64,
-                              &ctx->scores, &ctx->chosen, &ctx->pasted, &ctx->mism, &ctx->out,
-                              &ctx->ops_a, &ctx->ops_b, &ctx->ops_c, &ctx->ops_d, &ctx->ops_e})
+    for (ccwgpu::DevBuf* b : {&ctx->jobs, &ctx->work, &ctx->hd, &ctx->wts, &ctx->wts8,
+                              &ctx->tm64, &ctx->scores, &ctx->summary, &ctx->chosen,
+                              &ctx->pasted, &ctx->mism, &ctx->out, &ctx->stats, &ctx->ops_a,
+                              &ctx->ops_b, &ctx->ops_c, &ctx->ops_d, &ctx->ops_e})
         b->release();
     ctx->h_stage.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -239,7 +240,7 @@ ccw_status ccw_ctx_last_timing(ccw_ctx* ctx, ccw_timing* out) {
 ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant) {
     if (!ctx) return CCW_ERR_GENERIC;
     return guarded(ctx, [&] {
-        if (variant < 0 || variant > 1)
+        if (variant < 0 || variant > 2)
             throw Fail(CCW_ERR_CONFIG, fmt("ccf variant %d unknown", variant));
         ctx->ccf_variant = variant;
     });
@@ -325,6 +326,7 @@ void ccw_ti_destroy(ccw_ti* ti) {
     if (ti->d_codes) cudaFree(ti->d_codes);
     if (ti->d_ti64) cudaFree(ti->d_ti64);
     if (ti->d_scr) cudaFree(ti->d_scr);
+    for (auto& kv : ti->im2col) cudaFree(kv.second);
     delete ti;
 }
 

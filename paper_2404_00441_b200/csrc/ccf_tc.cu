@@ -1,0 +1,335 @@
+// ccf_tc.cu -- the CCF screen as an int8 implicit GEMM on the 5th-generation
+// tensor cores (tcgen05.mma kind::i8, int32 accumulators in TMEM).
+//
+// For one wave of placements (jobs) the exact-integer screen is
+//
+//   S[job, pos] = sum_k W[job, k] * X[pos, k],   k = (channel, s, t) over the
+//                                                 Tc x Tc coarse template window
+//
+// with X the im2col of the TI block-count planes (built once per TI and Tc,
+// int8: counts <= 4^J <= 64) and W the per-job OR weights (int8 in [-4^J, 4^J],
+// zero off the overlap mask).  int8 x int8 -> int32 is exact, so S equals the
+// fp32 CUDA-core screen (ccf_direct_kernel) bit for bit.  Off-mask template
+// cells cost MMA work but no correctness (their weights are zero).
+//
+// Tile: M = 128 jobs x N = 256 positions, K in 128-byte stages, two-stage
+// TMA -> shared-memory (128B swizzle) ring feeding a single-thread MMA issuer;
+// the accumulator (128 lanes x 256 columns int32) lives in TMEM.  The epilogue
+// (4 warps, one TMEM lane per job) writes S and a per-(job, tile) summary of
+// the top-Q scores with multiplicity, from which the select kernel derives
+// the exact K-th largest score without rescanning every position.
+#include <cuda.h>
+
+#include <algorithm>
+#include <climits>
+#include <mutex>
+
+#include "ccw_device.cuh"
+#include "ccf_tc.hpp"
+#include "internal.hpp"
+
+namespace ccwgpu {
+
+namespace {
+
+constexpr int kM = 128;
+constexpr int kN = 256;
+constexpr int kKC = 128;  // bytes of K per stage (one 128B swizzle atom)
+constexpr int kStages = 2;
+constexpr int kABytes = kM * kKC;
+constexpr int kBBytes = kN * kKC;
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major operand in the canonical 128B-swizzle
+// layout TMA writes: 8-row x 128-byte swizzle atoms, SBO = 1024 bytes between
+// 8-row groups, LBO unused (1), version 1 (tcgen05), layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+// kind::i8 instruction descriptor: D s32, A s8, B s8, both K-major.
+__host__ __device__ constexpr uint32_t i8_idesc(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     bar)
+                 : "memory");
+}
+
+#define LDTM_X32(taddr, r)                                                                         \
+    asm volatile(                                                                                  \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"   \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"         \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),      \
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),  \
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),            \
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),            \
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
+        : "r"(taddr))
+
+__global__ void __launch_bounds__(kThreads, 1)
+    ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  TcArgs a) {
+    extern __shared__ __align__(1024) uint8_t tc_sm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_sm_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * kN, m0 = blockIdx.y * kM;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        mbar_init(smem_u32(tfull), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)));
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            for (int kc = 0; kc < a.nk; ++kc) {
+                const int s = kc % kStages;
+                if (kc >= kStages) mbar_wait(smem_u32(&empty[s]), ((kc / kStages) - 1) & 1);
+                const uint32_t bar = smem_u32(&full[s]);
+                mbar_expect_tx(bar, kStageBytes);
+                tma_load_2d(smem_u32(sm + s * kStageBytes), &tmA, kc * kKC, m0, bar);
+                tma_load_2d(smem_u32(sm + s * kStageBytes + kABytes), &tmB, kc * kKC, n0, bar);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // single-thread MMA issuer
+            constexpr uint32_t idesc = i8_idesc(kM, kN);
+            for (int kc = 0; kc < a.nk; ++kc) {
+                const int s = kc % kStages;
+                mbar_wait(smem_u32(&full[s]), (kc / kStages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t ad = sw128_desc(smem_u32(sm + s * kStageBytes));
+                const uint64_t bd = sw128_desc(smem_u32(sm + s * kStageBytes + kABytes));
+#pragma unroll
+                for (int k = 0; k < kKC / 32; ++k)  // K = 32 bytes per kind::i8 MMA
+                    mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+                mma_commit(smem_u32(&empty[s]));
+            }
+            mma_commit(smem_u32(tfull));
+        }
+    } else {  // epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
+        mbar_wait(smem_u32(tfull), 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int q = warp & 3;
+        const int job = m0 + q * 32 + lane;
+        const bool valid_job = job < a.nj;
+        int top[kTcQ];
+#pragma unroll
+        for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
+        int32_t* out = a.scores + static_cast<size_t>(valid_job ? job : 0) * a.sld;
+        for (int c = 0; c < kN / 32; ++c) {
+            uint32_t r[32];
+            LDTM_X32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int p0 = n0 + c * 32;
+            if (valid_job) {
+                if (p0 + 32 <= a.npos) {
+                    int4* dst = reinterpret_cast<int4*>(out + p0);
+#pragma unroll
+                    for (int v = 0; v < 8; ++v)
+                        dst[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                } else {
+                    for (int i = 0; i < 32; ++i)
+                        if (p0 + i < a.npos) out[p0 + i] = static_cast<int>(r[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    int v = static_cast<int>(r[i]);
+                    if (p0 + i < a.npos && v > top[kTcQ - 1]) {
+                        // insertion into the descending top-Q list (multiplicity kept)
+#pragma unroll
+                        for (int j = 0; j < kTcQ; ++j) {
+                            if (v > top[j]) {
+                                const int t = top[j];
+                                top[j] = v;
+                                v = t;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (valid_job) {
+            int* sm_out = a.summary + (static_cast<size_t>(job) * a.ntiles + blockIdx.x) * kTcQ;
+#pragma unroll
+            for (int i = 0; i < kTcQ; ++i) sm_out[i] = top[i];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// im2col of the TI screen planes: row = score-map position, column k =
+// (ch, s, t); values are exact small integers, stored as int8.
+__global__ void im2col_kernel(const float* __restrict__ scr, int nscr, int hc, int wc, int Tc,
+                              int out_w, int npos, int kpad, int8_t* __restrict__ X) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t total = static_cast<size_t>(npos) * kpad;
+    if (idx >= total) return;
+    const int p = static_cast<int>(idx / kpad), k = static_cast<int>(idx - static_cast<size_t>(p) * kpad);
+    const int x = p / out_w, y = p - x * out_w;
+    int8_t v = 0;
+    if (k < nscr * Tc * Tc) {
+        const int ch = k / (Tc * Tc), rem = k - ch * Tc * Tc;
+        const int s = rem / Tc, t = rem - s * Tc;
+        v = static_cast<int8_t>(__float2int_rn(scr[static_cast<size_t>(ch) * hc * wc +
+                                                   static_cast<size_t>(x + s) * wc + y + t]));
+    }
+    X[idx] = v;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw Fail(CCW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap make_map(void* base, uint64_t cols_bytes, uint64_t rows, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols_bytes, rows};
+    const cuuint64_t strides[1] = {cols_bytes};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kKC), box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Fail(CCW_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+}  // namespace
+
+size_t ccf_tc_smem_bytes() { return kStages * kStageBytes + 1024 + 256; }
+
+int tc_kpad(int nscr, int Tc) { return ((nscr * Tc * Tc + 15) / 16) * 16; }
+
+const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st) {
+    auto it = ti->im2col.find(Tc);
+    if (it != ti->im2col.end()) return it->second;
+    const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1;
+    const int npos = out_h * out_w;
+    const int kpad = tc_kpad(ti->nscr, Tc);
+    int8_t* X = nullptr;
+    CCW_CUDA(cudaMalloc(&X, static_cast<size_t>(npos) * kpad));
+    const size_t total = static_cast<size_t>(npos) * kpad;
+    im2col_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        ti->d_scr, ti->nscr, ti->hc, ti->wc, Tc, out_w, npos, kpad, X);
+    CCW_CUDA(cudaGetLastError());
+    ti->im2col[Tc] = X;
+    return X;
+}
+
+void launch_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int sld, int kpad, int nj,
+                   int32_t* scores, int32_t* summary, cudaStream_t st) {
+    const CUtensorMap ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
+    const CUtensorMap mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
+    TcArgs a;
+    a.nj = nj;
+    a.npos = npos;
+    a.sld = sld;
+    a.nk = (kpad + kKC - 1) / kKC;
+    a.ntiles = (npos + kN - 1) / kN;
+    a.scores = scores;
+    a.summary = summary;
+    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ccf_tc_smem_bytes())));
+    dim3 grid(a.ntiles, (nj + kM - 1) / kM);
+    ccf_tc_kernel<<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(ma, mb, a);
+    CCW_CUDA(cudaGetLastError());
+}
+
+int tc_tiles(int npos) { return (npos + kN - 1) / kN; }
+
+}  // namespace ccwgpu

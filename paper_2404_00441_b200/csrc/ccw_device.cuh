@@ -51,9 +51,15 @@ struct SimParams {
     int wh, ww;
     const uint8_t* hd;       // wh*ww plane, kNoDatum = none; may be null
     // per-job scratch (indexed by job slot within a launch chunk)
-    int32_t* wts;            // nscr*Tc*Tc integer screen weights
+    int32_t* wts;            // nscr*Tc*Tc integer screen weights (fp32 screen)
+    int8_t* wts8;            // kpad int8 screen weights per job (tcgen05 screen), may be null
+    int kpad;
+    int32_t* summary;        // per job: ntiles x kTcQ top scores (tcgen05 screen), may be null
+    int ntiles;
+    unsigned long long* stats;  // [0] windows rescored in fp64, [1] screened jobs
     double* tm64;            // nch*Tc*Tc reference-order OR apex values
-    int32_t* scores;         // npos screen scores
+    int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
+    int sld;
     // outputs
     int32_t* chosen;         // per job (global job id): fr, fc
     uint8_t* pasted;         // optional trace of pasted patches (global job id * T*T)

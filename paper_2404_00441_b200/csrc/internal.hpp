@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -83,8 +84,8 @@ struct ccw_ctx {
     int ccf_variant = 0;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf jobs, work, hd, wts, tm64, scores, chosen, pasted, mism, out, ops_a, ops_b,
-        ops_c, ops_d, ops_e;
+    ccwgpu::DevBuf jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+        stats, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
     std::vector<cudaEvent_t> ev_pool;
 };
@@ -97,6 +98,7 @@ struct ccw_ti {
     uint8_t* d_codes = nullptr;  // h*w
     double* d_ti64 = nullptr;    // nch*hc*wc
     float* d_scr = nullptr;      // nscr*hc*wc
+    std::map<int, int8_t*> im2col;  // per template size Tc: npos x kpad int8 (tcgen05 screen)
 };
 
 namespace ccwgpu {

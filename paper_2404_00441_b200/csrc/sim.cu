@@ -24,6 +24,7 @@
 #include <climits>
 #include <cstring>
 
+#include "ccf_tc.hpp"
 #include "ccw_device.cuh"
 #include "internal.hpp"
 
@@ -70,18 +71,27 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
     const uint8_t* grid = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
     int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
     double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+    if (P.wts8)  // zero the K padding of this job's int8 weight row
+        for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x)
+            P.wts8[static_cast<size_t>(slot) * P.kpad + k] = 0;
     for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
         const int s = c / Tc, t = c - s * Tc;
         int t0, t1;
         mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
         const bool in = t >= t0 && t < t1;
         const uint8_t* base = grid + static_cast<size_t>(jb.top + s * B) * P.ww + jb.left + t * B;
+        int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
         if (P.mode == 0) {
             const int last = in ? block_stat(base, P.ww, B, 0, P.F - 1) : 0;
-            for (int f = 0; f < P.nscr; ++f)
-                wts[f * Tc * Tc + c] = in ? block_stat(base, P.ww, B, 0, f) - last : 0;
+            for (int f = 0; f < P.nscr; ++f) {
+                const int v = in ? block_stat(base, P.ww, B, 0, f) - last : 0;
+                wts[f * Tc * Tc + c] = v;
+                if (w8) w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
+            }
         } else {
-            wts[c] = in ? block_stat(base, P.ww, B, 1, 0) : 0;
+            const int v = in ? block_stat(base, P.ww, B, 1, 0) : 0;
+            wts[c] = v;
+            if (w8) w8[c] = static_cast<int8_t>(v);
         }
         for (int ch = 0; ch < P.nch; ++ch)
             tm[ch * Tc * Tc + c] = in ? haar_apex_block(base, P.ww, P.J, P.mode, ch) : 0.0;
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(CCF_THREADS) ccf_direct_kernel(SimParams P,
     }
     const int x = x0 + tr;
     if (x < P.out_h) {
-        int32_t* out = P.scores + static_cast<size_t>(slot) * P.npos + static_cast<size_t>(x) * P.out_w;
+        int32_t* out = P.scores + static_cast<size_t>(slot) * P.sld + static_cast<size_t>(x) * P.out_w;
 #pragma unroll
         for (int b = 0; b < CCF_RY; ++b) {
             const int y = y0 + tcg + b;
@@ -210,12 +220,15 @@ __global__ void __launch_bounds__(CCF_THREADS) ccf_direct_kernel(SimParams P,
 constexpr int SEL_T = 256;
 constexpr int GCAP = 1024;
 constexpr int KMAX = 8192;
+constexpr int RSUM_CAP = 4096;  // (window, run) partial sums staged per rescoring group
 
 struct SelLayout {
-    size_t hist, misc, redd, redi, gkey, gidx, tkey, tidx, exist, outp, from, dp, seam, total;
+    size_t hist, misc, redd, redi, gkey, gidx, tkey, tidx, runs, tmpl, rsum, rnrm, exist, outp,
+        from, dp, seam, total;
 };
 
-__host__ __device__ inline SelLayout sel_layout(int K, int T, int OV) {
+__host__ __device__ inline SelLayout sel_layout(int K, int T, int OV, int nch = 1, int Tc = 1,
+                                                int normalized = 0) {
     SelLayout L{};
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -231,6 +244,10 @@ __host__ __device__ inline SelLayout sel_layout(int K, int T, int OV) {
     L.gidx = take(static_cast<size_t>(GCAP + SEL_T + K) * 4);
     L.tkey = take(static_cast<size_t>(K) * 8);
     L.tidx = take(static_cast<size_t>(K) * 4);
+    L.runs = take(static_cast<size_t>(nch) * Tc * 16);
+    L.tmpl = take(static_cast<size_t>(nch) * Tc * Tc * 8);
+    L.rsum = take(static_cast<size_t>(RSUM_CAP) * 8);
+    L.rnrm = take(normalized ? static_cast<size_t>(RSUM_CAP) * 8 : 0);
     L.exist = take(static_cast<size_t>(T) * T);
     L.outp = take(static_cast<size_t>(T) * T);
     L.from = take(static_cast<size_t>(T) * OV * 2);
@@ -240,14 +257,15 @@ __host__ __device__ inline SelLayout sel_layout(int K, int T, int OV) {
     return L;
 }
 
-// Exact K-th largest value (with multiplicity) of n int32 scores: block-wide
-// radix select over the offset range, 8 bits per pass, warp-aggregated
-// shared-memory histograms.
+// Exact K-th largest value (with multiplicity) of n int32 values, skipping
+// INT_MIN padding: block-wide radix select over the offset range, 8 bits per
+// pass, warp-aggregated shared-memory histograms.
 __device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, int* hist,
                                  int* misc, int* redi) {
     int lo = INT_MAX, hi = INT_MIN;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
         const int v = sc[p];
+        if (v == INT_MIN) continue;
         lo = min(lo, v);
         hi = max(hi, v);
     }
@@ -267,7 +285,7 @@ __device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, i
             const int p = base + threadIdx.x;
             bool match = false;
             int dg = 0;
-            if (p < n) {
+            if (p < n && sc[p] != INT_MIN) {
                 const uint32_t u = static_cast<uint32_t>(sc[p]) - static_cast<uint32_t>(lo);
                 match = (static_cast<uint64_t>(u) >> (shift + 8)) ==
                         (static_cast<uint64_t>(prefix) >> (shift + 8));
@@ -297,45 +315,55 @@ __device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, i
     return static_cast<int>(static_cast<uint32_t>(lo) + prefix);
 }
 
-// fp64 rescoring of one window in the reference's exact order:
+struct RunDesc {
+    int ch, s, t0, t1;
+};
+
+// fp64 rescoring of `cnt` windows in the reference's exact order
 //   acc = 0; for f: for run (row-major): sum = 0; sum += ti*or over the run;
 //   acc += sum          (matcher.hpp:64-81, 158-161)
-// and, for normalized scoring, the masked squares (matcher.hpp:84-100,
-// 163-171) and acc / sqrt(norm).
-__device__ double rescore(const SimParams& P, const Job& jb, const double* __restrict__ tm,
-                          int pos) {
-    const int x = pos / P.out_w, y = pos - x * P.out_w;
-    const int Tc = P.Tc;
-    double acc = 0.0;
-    for (int ch = 0; ch < P.nch; ++ch) {
-        const double* tip = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc;
-        const double* tmp = tm + ch * Tc * Tc;
-        for (int s = 0; s < Tc; ++s) {
-            int t0, t1;
-            mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
-            if (t1 <= t0) continue;
-            const double* a = tip + static_cast<size_t>(x + s) * P.wc + y;
-            const double* b = tmp + s * Tc;
-            double sum = 0.0;
-            for (int t = t0; t < t1; ++t) sum = __dadd_rn(sum, __dmul_rn(a[t], b[t]));
-            acc = __dadd_rn(acc, sum);
+// plus, for normalized scoring, the masked squares and acc / sqrt(norm)
+// (matcher.hpp:84-100, 163-171).  Parallel over (window, run) pairs: each
+// thread forms one run's sum (the reference's inner chain), then one thread
+// per window folds the run sums in order -- the same operations in the same
+// order as the reference, so the result is bit-identical.
+__device__ void rescore_group(const SimParams& P, const RunDesc* runs, int R,
+                              const double* tmpl, const int* gidx, double* gkey, int cnt,
+                              double* rsum, double* rnrm) {
+    const int EG = max(1, RSUM_CAP / R);
+    const bool norm = P.scoring == 1;
+    for (int e0 = 0; e0 < cnt; e0 += EG) {
+        const int ng = min(EG, cnt - e0);
+        for (int w = threadIdx.x; w < ng * R; w += blockDim.x) {
+            const int e = e0 + w / R, r = w - (w / R) * R;
+            const int pos = gidx[e];
+            const int x = pos / P.out_w, y = pos - x * P.out_w;
+            const RunDesc rd = runs[r];
+            const double* a = P.ti64 + static_cast<size_t>(rd.ch) * P.hc * P.wc +
+                              static_cast<size_t>(x + rd.s) * P.wc + y;
+            const double* b = tmpl + (rd.ch * P.Tc + rd.s) * P.Tc;
+            double sum = 0.0, nsum = 0.0;
+            for (int t = rd.t0; t < rd.t1; ++t) {
+                const double av = __ldg(a + t);
+                sum = __dadd_rn(sum, __dmul_rn(av, b[t]));
+                if (norm) nsum = __dadd_rn(nsum, __dmul_rn(av, av));
+            }
+            rsum[w] = sum;
+            if (norm) rnrm[w] = nsum;
         }
-    }
-    if (P.scoring != 1) return acc;
-    double nrm = 0.0;
-    for (int ch = 0; ch < P.nch; ++ch) {
-        const double* tip = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc;
-        for (int s = 0; s < Tc; ++s) {
-            int t0, t1;
-            mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
-            if (t1 <= t0) continue;
-            const double* a = tip + static_cast<size_t>(x + s) * P.wc + y;
-            double sum = 0.0;
-            for (int t = t0; t < t1; ++t) sum = __dadd_rn(sum, __dmul_rn(a[t], a[t]));
-            nrm = __dadd_rn(nrm, sum);
+        __syncthreads();
+        for (int e = threadIdx.x; e < ng; e += blockDim.x) {
+            double acc = 0.0;
+            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, rsum[e * R + r]);
+            if (norm) {
+                double n = 0.0;
+                for (int r = 0; r < R; ++r) n = __dadd_rn(n, rnrm[e * R + r]);
+                acc = n > 0.0 ? __ddiv_rn(acc, __dsqrt_rn(n)) : 0.0;
+            }
+            gkey[e0 + e] = acc;
         }
+        __syncthreads();
     }
-    return nrm > 0.0 ? __ddiv_rn(acc, __dsqrt_rn(nrm)) : 0.0;
 }
 
 // Reference ranking: higher score first, earlier row-major location on ties
@@ -411,11 +439,73 @@ __device__ void min_cut_device(const uint8_t* exist, uint8_t* outp, int T, int O
     }
 }
 
+// Rescore the gathered windows and merge them with the running top-K list
+// (K rounds of a block-wide argmax under the reference ranking).
+__device__ void flush_candidates(const SimParams& P, const RunDesc* runs, int R,
+                                 const double* tmpl, int* gidx, double* gkey, int& cnt,
+                                 double* tkey, int* tidx, int& ntop, int K, double* rsum,
+                                 double* rnrm, double* redd, int* redi) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+    rescore_group(P, runs, R, tmpl, gidx, gkey, cnt, rsum, rnrm);
+    for (int e = tid; e < ntop; e += SEL_T) {
+        gkey[cnt + e] = tkey[e];
+        gidx[cnt + e] = tidx[e];
+    }
+    __syncthreads();
+    const int n = cnt + ntop;
+    const int keep = min(K, n);
+    for (int round = 0; round < keep; ++round) {
+        double bk = 0.0;
+        int bi = INT_MAX, bp = -1;
+        for (int e = tid; e < n; e += SEL_T) {
+            const int ix = gidx[e];
+            if (ix >= 0 && (bp < 0 || better(gkey[e], ix, bk, bi))) {
+                bk = gkey[e];
+                bi = ix;
+                bp = e;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
+                bk = ok;
+                bi = oi;
+                bp = op;
+            }
+        }
+        if (lane == 0) {
+            redd[wid] = bk;
+            redi[wid] = bi;
+            redi[32 + wid] = bp;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < SEL_T / 32; ++w) {
+                if (redi[32 + w] >= 0 && (bp < 0 || better(redd[w], redi[w], bk, bi))) {
+                    bk = redd[w];
+                    bi = redi[w];
+                    bp = redi[32 + w];
+                }
+            }
+            tkey[round] = bk;
+            tidx[round] = bi;
+            gidx[bp] = -1;
+        }
+        __syncthreads();
+    }
+    ntop = keep;
+    cnt = 0;
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
                                                              const Job* __restrict__ jobs,
                                                              int job0, int use_screen) {
     extern __shared__ __align__(16) unsigned char sel_sm[];
-    const SelLayout L = sel_layout(P.K, P.T, P.OV);
+    const SelLayout L = sel_layout(P.K, P.T, P.OV, P.nch, P.Tc, P.scoring == 1);
     int* hist = reinterpret_cast<int*>(sel_sm + L.hist);
     int* misc = reinterpret_cast<int*>(sel_sm + L.misc);
     double* redd = reinterpret_cast<double*>(sel_sm + L.redd);
@@ -424,6 +514,10 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
     int* gidx = reinterpret_cast<int*>(sel_sm + L.gidx);
     double* tkey = reinterpret_cast<double*>(sel_sm + L.tkey);
     int* tidx = reinterpret_cast<int*>(sel_sm + L.tidx);
+    RunDesc* runs = reinterpret_cast<RunDesc*>(sel_sm + L.runs);
+    double* tmpl = reinterpret_cast<double*>(sel_sm + L.tmpl);
+    double* rsum = reinterpret_cast<double*>(sel_sm + L.rsum);
+    double* rnrm = reinterpret_cast<double*>(sel_sm + L.rnrm);
     uint8_t* exist = sel_sm + L.exist;
     uint8_t* outp = sel_sm + L.outp;
     int16_t* from = reinterpret_cast<int16_t*>(sel_sm + L.from);
@@ -438,87 +532,74 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         fr = jb.fr;
         fc = jb.fc;
     } else {
-        const int32_t* sc = P.scores + static_cast<size_t>(blockIdx.x) * P.npos;
-        const double* tm = P.tm64 + static_cast<size_t>(blockIdx.x) * P.nch * P.Tc * P.Tc;
+        const int Tc = P.Tc;
+        const int32_t* sc = P.scores + static_cast<size_t>(blockIdx.x) * P.sld;
+        const double* tm = P.tm64 + static_cast<size_t>(blockIdx.x) * P.nch * Tc * Tc;
         const int K = P.K;
+        // stage the job's fp64 template and its run list (matcher.hpp:44-61 order)
+        for (int e = tid; e < P.nch * Tc * Tc; e += SEL_T) tmpl[e] = tm[e];
+        int R = 0;
+        {
+            int rows = 0;
+            for (int s = 0; s < Tc; ++s) {
+                int t0, t1;
+                mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+                rows += t1 > t0;
+            }
+            R = rows * P.nch;
+            if (tid == 0) {
+                int r = 0;
+                for (int ch = 0; ch < P.nch; ++ch)
+                    for (int s = 0; s < Tc; ++s) {
+                        int t0, t1;
+                        mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+                        if (t1 > t0) runs[r++] = {ch, s, t0, t1};
+                    }
+            }
+        }
         // 1. exact screen threshold: every window whose integer score reaches
         //    the K-th largest can appear in the reference's top-K.
         const bool all = !use_screen;
-        const int thr = all ? 0 : radix_kth_largest(sc, P.npos, K, hist, misc, redi);
-        // 2. gather the tie group in row-major chunks, rescore in fp64, keep the
+        const int32_t* tsum =
+            P.summary ? P.summary + static_cast<size_t>(blockIdx.x) * P.ntiles * kTcQ : nullptr;
+        int thr = 0;
+        if (!all) {
+            if (tsum && K <= kTcQ)  // union of per-tile top-Q lists holds the global top-K
+                thr = radix_kth_largest(tsum, P.ntiles * kTcQ, K, hist, misc, redi);
+            else
+                thr = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
+        }
+        if (P.stats && tid == 0) atomicAdd(&P.stats[1], 1ull);
+        __syncthreads();
+        // 2. gather the tie group in row-major order, rescore in fp64, keep the
         //    running top-K by (fp64 desc, index asc).
+        const int span = tsum ? kTcTile : SEL_T;
+        const int nspans = (P.npos + span - 1) / span;
         int ntop = 0, cnt = 0;
-        for (int base = 0; base < P.npos; base += SEL_T) {
-            const int p = base + tid;
-            const bool q = p < P.npos && (all || sc[p] >= thr);
-            const unsigned bal = __ballot_sync(0xffffffffu, q);
-            if (lane == 0) redi[wid] = __popc(bal);
-            __syncthreads();
-            int off = 0, tot = 0;
-            for (int w = 0; w < SEL_T / 32; ++w) {
-                if (w < wid) off += redi[w];
-                tot += redi[w];
-            }
-            if (q) gidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
-            cnt += tot;
-            __syncthreads();
-            const bool last = base + SEL_T >= P.npos;
-            if (cnt + SEL_T > GCAP || (last && cnt > 0)) {
-                for (int e = tid; e < cnt; e += SEL_T) gkey[e] = rescore(P, jb, tm, gidx[e]);
-                for (int e = tid; e < ntop; e += SEL_T) {
-                    gkey[cnt + e] = tkey[e];
-                    gidx[cnt + e] = tidx[e];
-                }
+        for (int sp = 0; sp < nspans; ++sp) {
+            if (!all && tsum && tsum[static_cast<size_t>(sp) * kTcQ] < thr) continue;  // uniform
+            for (int sub = 0; sub < span; sub += SEL_T) {
+                const int p = sp * span + sub + tid;
+                const bool q = p < P.npos && (all || sc[p] >= thr);
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (lane == 0) redi[wid] = __popc(bal);
                 __syncthreads();
-                const int n = cnt + ntop;
-                const int keep = min(K, n);
-                for (int round = 0; round < keep; ++round) {
-                    double bk = 0.0;
-                    int bi = INT_MAX, bp = -1;
-                    for (int e = tid; e < n; e += SEL_T) {
-                        const int ix = gidx[e];
-                        if (ix >= 0 && (bp < 0 || better(gkey[e], ix, bk, bi))) {
-                            bk = gkey[e];
-                            bi = ix;
-                            bp = e;
-                        }
-                    }
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                        if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
-                            bk = ok;
-                            bi = oi;
-                            bp = op;
-                        }
-                    }
-                    if (lane == 0) {
-                        redd[wid] = bk;
-                        redi[wid] = bi;
-                        redi[32 + wid] = bp;
-                    }
-                    __syncthreads();
-                    if (tid == 0) {
-                        for (int w = 1; w < SEL_T / 32; ++w) {
-                            if (redi[32 + w] >= 0 &&
-                                (bp < 0 || better(redd[w], redi[w], bk, bi))) {
-                                bk = redd[w];
-                                bi = redi[w];
-                                bp = redi[32 + w];
-                            }
-                        }
-                        tkey[round] = bk;
-                        tidx[round] = bi;
-                        gidx[bp] = -1;
-                    }
-                    __syncthreads();
+                int off = 0, tot = 0;
+                for (int w = 0; w < SEL_T / 32; ++w) {
+                    if (w < wid) off += redi[w];
+                    tot += redi[w];
                 }
-                ntop = keep;
-                cnt = 0;
+                if (q) gidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
+                cnt += tot;
                 __syncthreads();
+                if (cnt + SEL_T > GCAP)
+                    flush_candidates(P, runs, R, tmpl, gidx, gkey, cnt, tkey, tidx, ntop, K, rsum,
+                                     rnrm, redd, redi);
             }
         }
+        if (cnt > 0)
+            flush_candidates(P, runs, R, tmpl, gidx, gkey, cnt, tkey, tidx, ntop, K, rsum, rnrm,
+                             redd, redi);
         // 3. choose (matcher.hpp:207-241)
         int pick = jb.pick;
         if (pick < 0) {
@@ -790,7 +871,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     const size_t score_budget = static_cast<size_t>(512) << 20;
     const size_t maxj = std::max<size_t>(1, std::min<size_t>(flat.size(), score_budget / (sizeof(int32_t) * npos)));
-    int32_t* d_scores = ctx->scores.as<int32_t>(maxj * npos);
+    const int sld = (npos + 3) & ~3;
+    int32_t* d_scores = ctx->scores.as<int32_t>(maxj * sld);
     int32_t* d_wts = ctx->wts.as<int32_t>(maxj * std::max(ti->nscr, 1) * Tc * Tc);
     double* d_tm = ctx->tm64.as<double>(maxj * ti->nch * Tc * Tc);
     int32_t* d_chosen = ctx->chosen.as<int32_t>(2 * flat.size());
@@ -831,11 +913,36 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.wts = d_wts;
     P.tm64 = d_tm;
     P.scores = d_scores;
+    P.sld = sld;
     P.chosen = d_chosen;
     P.pasted = d_pasted;
 
+    // screen variant: tcgen05 int8 implicit GEMM when every operand fits int8
+    const int maxv = ti->mode == 0 ? B * B : (ti->F - 1) * B * B;
+    const bool tc_ok = use_screen && maxv <= 127;
+    if (ctx->ccf_variant == 2 && use_screen && !tc_ok)
+        throw Fail(CCW_ERR_CONFIG, "tcgen05 int8 screen needs block statistics <= 127");
+    const bool use_tc = tc_ok && ctx->ccf_variant != 1;
+    const int kpad = tc_kpad(ti->nscr, Tc);
+    const int ntiles = tc_tiles(npos);
+    const int8_t* d_x = nullptr;
+    int8_t* d_w8 = nullptr;
+    int32_t* d_summary = nullptr;
+    if (use_tc) {
+        d_x = ti_im2col(ti, Tc, st);
+        d_w8 = ctx->wts8.as<int8_t>(maxj * kpad);
+        d_summary = ctx->summary.as<int32_t>(maxj * ntiles * kTcQ);
+    }
+    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(4);
+    CCW_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), st));
+    P.wts8 = d_w8;
+    P.kpad = kpad;
+    P.summary = d_summary;
+    P.ntiles = ntiles;
+    P.stats = d_stats;
+
     const size_t ccf_smem = ccf_smem_bytes(Tc, ti->nscr);
-    const size_t sel_smem = sel_layout(Kp, T, OV).total;
+    const size_t sel_smem = sel_layout(Kp, T, OV, ti->nch, Tc, cfg.scoring == 1).total;
     if (ccf_smem > 227 * 1024 || sel_smem > 227 * 1024)
         throw Fail(CCW_ERR_CONFIG, "configuration exceeds the per-CTA shared-memory budget");
     CCW_CUDA(cudaFuncSetAttribute(ccf_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -851,7 +958,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaEventRecord(ev0, st));
     }
     int64_t launches = 0, ccf_launches = 0;
-    double ccf_flop = 0, ccf_flop_ref = 0;
+    double ccf_flop = 0, ccf_flop_ref = 0, ccf_mma_flop = 0;
     const dim3 ccf_grid_xy((out_w + CCF_TY - 1) / CCF_TY, (out_h + CCF_TX - 1) / CCF_TX);
     for (size_t w = 0; w + 1 < wave_off.size(); ++w) {
         for (size_t j0 = wave_off[w]; j0 < wave_off[w + 1]; j0 += maxj) {
@@ -867,14 +974,21 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         b = tm.get();
                         CCW_CUDA(cudaEventRecord(a, st));
                     }
-                    dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
-                    ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, st>>>(P, d_jobs, static_cast<int>(j0));
+                    if (use_tc) {
+                        launch_ccf_tc(d_w8, static_cast<int>(maxj), d_x, npos, sld, kpad, nj, d_scores,
+                                      d_summary, st);
+                    } else {
+                        dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
+                        ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, st>>>(P, d_jobs,
+                                                                               static_cast<int>(j0));
+                    }
                     ++launches;
                     ++ccf_launches;
                     if (ctx->profiling) {
                         CCW_CUDA(cudaEventRecord(b, st));
                         tm.ccf.push_back({a, b});
                     }
+                    ccf_mma_flop += 2.0 * kpad * static_cast<double>(npos) * nj;
                     for (int q = 0; q < nj; ++q) {
                         const int sh = flat[j0 + q].shape;
                         const double m = sh == kL ? mask_cells : static_cast<double>(Tc) * OVc;
@@ -914,6 +1028,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (h_out)
         CCW_CUDA(cudaMemcpyAsync(h_out, fin, static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real,
                                  cudaMemcpyDeviceToHost, st));
+    unsigned long long stats[4] = {0, 0, 0, 0};
+    CCW_CUDA(cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
     std::vector<int> mism(n_real, 0);
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
     std::vector<int32_t> chosen;
@@ -942,6 +1058,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.ccf_flop_ref = ccf_flop_ref;
     ctx->timing.waves = static_cast<int64_t>(wave_off.size() - 1);
     ctx->timing.jobs = static_cast<int64_t>(flat.size());
+    ctx->timing.rescored = static_cast<int64_t>(stats[0]);
+    ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
+    ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
+    ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     for (int r = 0; r < n_real; ++r) {
