@@ -100,7 +100,7 @@ typedef struct ccw_trace {
 
 /* Per-call device timing, filled when profiling is enabled on the context. */
 typedef struct ccw_timing {
-    double total_ms;        /* device time of the last ccw_simulate*, CUDA events */
+    double total_ms;        /* device time of the last ccw_simulate* (always filled)  */
     double ccf_ms;          /* summed device time of the CCF screen launches      */
     double select_ms;       /* summed device time of the select+paste launches    */
     int64_t ccf_launches;
@@ -113,6 +113,7 @@ typedef struct ccw_timing {
     int64_t screened_jobs;  /* placements that went through the CCF screen            */
     int64_t ccf_variant;    /* 0 none (normalized / F=1), 1 fp32 direct, 2 tcgen05 int8 */
     double ccf_mma_flop;    /* tensor-core MMA FLOP issued (full Tc x Tc window, padded K) */
+    int64_t groups;         /* realization groups run concurrently on separate streams */
 } ccw_timing;
 
 typedef struct ccw_ctx ccw_ctx;

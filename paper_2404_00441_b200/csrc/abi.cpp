@@ -212,11 +212,12 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (ccwgpu::DevBuf* b : {&ctx->jobs, &ctx->work, &ctx->hd, &ctx->wts, &ctx->wts8,
                               &ctx->tm64, &ctx->scores, &ctx->summary, &ctx->chosen,
-                              &ctx->pasted, &ctx->mism, &ctx->out, &ctx->stats, &ctx->ops_a,
+                              &ctx->pasted, &ctx->mism, &ctx->out, &ctx->stats, &ctx->src, &ctx->ops_a,
                               &ctx->ops_b, &ctx->ops_c, &ctx->ops_d, &ctx->ops_e})
         b->release();
     ctx->h_stage.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -39,7 +39,8 @@ constexpr int kStages = 2;
 constexpr int kABytes = kM * kKC;
 constexpr int kBBytes = kN * kKC;
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, 128 columns each
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -121,6 +122,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
           "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
         : "r"(taddr))
 
+template <int Q>
 __global__ void __launch_bounds__(kThreads, 1)
     ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   TcArgs a) {
@@ -182,21 +184,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mma_commit(smem_u32(tfull));
         }
-    } else {  // epilogue: warps 2..5 -> TMEM lane quarters 2,3,0,1
+    } else {  // epilogue: warps 2..9; lane quarter = warp % 4, column half = (warp - 2) / 4
         mbar_wait(smem_u32(tfull), 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int job = m0 + q * 32 + lane;
         const bool valid_job = job < a.nj;
-        int top[kTcQ];
+        int top[Q];
 #pragma unroll
-        for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
+        for (int i = 0; i < Q; ++i) top[i] = INT_MIN;
         int32_t* out = a.scores + static_cast<size_t>(valid_job ? job : 0) * a.sld;
-        for (int c = 0; c < kN / 32; ++c) {
+        const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * (kN / 2);
+        for (int c = 0; c < kN / 64; ++c) {
             uint32_t r[32];
-            LDTM_X32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
+            LDTM_X32(trow + c * 32, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int p0 = n0 + c * 32;
+            const int p0 = n0 + half * (kN / 2) + c * 32;
             if (valid_job) {
                 if (p0 + 32 <= a.npos) {
                     int4* dst = reinterpret_cast<int4*>(out + p0);
@@ -210,10 +214,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     int v = static_cast<int>(r[i]);
-                    if (p0 + i < a.npos && v > top[kTcQ - 1]) {
+                    if (p0 + i < a.npos && v > top[Q - 1]) {
                         // insertion into the descending top-Q list (multiplicity kept)
 #pragma unroll
-                        for (int j = 0; j < kTcQ; ++j) {
+                        for (int j = 0; j < Q; ++j) {
                             if (v > top[j]) {
                                 const int t = top[j];
                                 top[j] = v;
@@ -225,9 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (valid_job) {
-            int* sm_out = a.summary + (static_cast<size_t>(job) * a.ntiles + blockIdx.x) * kTcQ;
+            int* sm_out = a.summary + (static_cast<size_t>(job) * a.ntiles + 2 * blockIdx.x + half) * kTcQ;
 #pragma unroll
-            for (int i = 0; i < kTcQ; ++i) sm_out[i] = top[i];
+            for (int i = 0; i < kTcQ; ++i) sm_out[i] = i < Q ? top[i < Q ? i : 0] : INT_MIN;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -312,7 +316,7 @@ const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st) {
 }
 
 void launch_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int sld, int kpad, int nj,
-                   int32_t* scores, int32_t* summary, cudaStream_t st) {
+                   int K, int32_t* scores, int32_t* summary, cudaStream_t st) {
     const CUtensorMap ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
     const CUtensorMap mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
     TcArgs a;
@@ -320,16 +324,28 @@ void launch_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
     a.npos = npos;
     a.sld = sld;
     a.nk = (kpad + kKC - 1) / kKC;
-    a.ntiles = (npos + kN - 1) / kN;
+    a.ntiles = tc_tiles(npos);
     a.scores = scores;
     a.summary = summary;
-    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(ccf_tc_smem_bytes())));
-    dim3 grid(a.ntiles, (nj + kM - 1) / kM);
-    ccf_tc_kernel<<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(ma, mb, a);
+    dim3 grid((npos + kN - 1) / kN, (nj + kM - 1) / kM);
+    auto go = [&](auto kern) {
+        CCW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ccf_tc_smem_bytes())));
+        kern<<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(ma, mb, a);
+    };
+    // summary depth: the smallest supported Q >= K (deeper lists cost epilogue
+    // instructions; K > kTcQ uses the full score rows only)
+    if (K <= 1)
+        go(ccf_tc_kernel<1>);
+    else if (K <= 2)
+        go(ccf_tc_kernel<2>);
+    else if (K <= 4)
+        go(ccf_tc_kernel<4>);
+    else
+        go(ccf_tc_kernel<8>);
     CCW_CUDA(cudaGetLastError());
 }
 
-int tc_tiles(int npos) { return (npos + kN - 1) / kN; }
+int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // summaries per half tile
 
 }  // namespace ccwgpu

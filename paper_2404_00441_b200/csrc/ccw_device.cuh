@@ -50,6 +50,9 @@ struct SimParams {
     uint8_t* work;           // n_real planes of wh*ww
     int wh, ww;
     const uint8_t* hd;       // wh*ww plane, kNoDatum = none; may be null
+    int32_t* src;            // n_real planes of (wh/B)*(ww/B): TI coarse index each work block
+                             // was pasted from (null with min-cut, whose blocks mix sources)
+    int swc;                 // ww / B
     // per-job scratch (indexed by job slot within a launch chunk)
     int32_t* wts;            // nscr*Tc*Tc integer screen weights (fp32 screen)
     int8_t* wts8;            // kpad int8 screen weights per job (tcgen05 screen), may be null

@@ -85,9 +85,10 @@ struct ccw_ctx {
     ccw_timing timing{};
     // scratch
     ccwgpu::DevBuf jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
-        stats, ops_a, ops_b, ops_c, ops_d, ops_e;
+        stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
     std::vector<cudaEvent_t> ev_pool;
+    std::vector<cudaStream_t> gstreams;  // realization-group streams
 };
 
 struct ccw_ti {

@@ -21,6 +21,8 @@
 // crops the work grid (simulator.hpp:506-515).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 
@@ -64,6 +66,40 @@ void build_pyramid(ccw_ti* ti, cudaStream_t s) {
 //   S = sum_f sum_mask N_f * n_f = sum_{f<F-1} sum_mask N_f * w_f + B * sum_mask n_{F-1}
 // and the last term is the same for every TI window, so ranking by the F-1
 // channel sum is ranking by S.  Raw-codes mode uses the code sums directly.
+// Fast path (no min-cut): every work block is a verbatim block-aligned TI
+// block (pastes are block aligned, simulator.hpp:452-453, 480-483), so the OR's
+// counts and reference-order apex values are gathers from the TI pyramid at
+// the recorded source block -- identical values, no recomputation.
+__global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    const int slot = blockIdx.x;
+    const Job jb = jobs[job0 + slot];
+    const int Tc = P.Tc, B = P.B, nc = P.hc * P.wc;
+    const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc;
+    int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
+    double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+    int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
+    if (w8)
+        for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x) w8[k] = 0;
+    for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
+        const int s = c / Tc, t = c - s * Tc;
+        int t0, t1;
+        mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+        const bool in = t >= t0 && t < t1;
+        const int sb = in ? src[static_cast<size_t>(jb.top / B + s) * P.swc + jb.left / B + t] : 0;
+        int last = B * B;
+        if (P.mode == 0)
+            for (int f = 0; f < P.nscr; ++f) last -= static_cast<int>(P.tiscr[static_cast<size_t>(f) * nc + sb]);
+        for (int f = 0; f < P.nscr; ++f) {
+            const int n = static_cast<int>(P.tiscr[static_cast<size_t>(f) * nc + sb]);
+            const int v = in ? (P.mode == 0 ? n - last : n) : 0;
+            wts[f * Tc * Tc + c] = v;
+            if (w8) w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
+        }
+        for (int ch = 0; ch < P.nch; ++ch)
+            tm[ch * Tc * Tc + c] = in ? P.ti64[static_cast<size_t>(ch) * nc + sb] : 0.0;
+    }
+}
+
 __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
     const int slot = blockIdx.x;
     const Job jb = jobs[job0 + slot];
@@ -580,7 +616,7 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
             if (!all && tsum && tsum[static_cast<size_t>(sp) * kTcQ] < thr) continue;  // uniform
             for (int sub = 0; sub < span; sub += SEL_T) {
                 const int p = sp * span + sub + tid;
-                const bool q = p < P.npos && (all || sc[p] >= thr);
+                const bool q = sub + tid < span && p < P.npos && (all || sc[p] >= thr);
                 const unsigned bal = __ballot_sync(0xffffffffu, q);
                 if (lane == 0) redi[wid] = __popc(bal);
                 __syncthreads();
@@ -658,9 +694,361 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
             if (trace) trace[e] = v;
         }
     }
+    if (P.src) {
+        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc;
+        for (int e = tid; e < P.Tc * P.Tc; e += SEL_T) {
+            const int a = e / P.Tc, b = e - a * P.Tc;
+            sm[static_cast<size_t>(jb.top / P.B + a) * P.swc + jb.left / P.B + b] =
+                (fr / P.B + a) * P.wc + fc / P.B + b;
+        }
+    }
     if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
+    }
+}
+
+// ----------------------------------------------------- warp-per-job select --
+//
+// The common case (raw scoring, K <= kTcQ, tcgen05 summaries, no min-cut):
+// one warp per placement, no block-wide barriers.  Same contract as
+// select_paste_kernel: exact threshold from the per-tile top-Q summaries,
+// fp64 reference-order rescoring of the windows at or above it, reference
+// ranking, pick, paste.
+constexpr int WS_WARPS = 4;
+constexpr int WS_CB = 96;     // candidate buffer (flushed at WS_CB - 32)
+constexpr int WS_RS = 256;    // (window, run) partial sums per rescoring batch
+
+constexpr int WS_MAXTC = 64;   // template rows tabulated per warp
+
+constexpr int WS_PB = 2048;  // staged fp64 TI values (windows x mask cells) per batch
+
+struct WarpSel {
+    short4 rows[WS_MAXTC];  // (s, t0, t1, cell offset) of the mask rows, row-major
+    int cidx[WS_CB + kTcQ];
+    double ckey[WS_CB + kTcQ];
+    int tidx[kTcQ];
+    double tkey[kTcQ];
+    double rsum[WS_RS];
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Rescore the buffered windows (one lane per (window, run) pair forms the
+// run's sum, one lane per window folds the run sums in row-major order --
+// the reference's operations in the reference's order) and merge them into
+// the running top-K by the reference ranking.
+__device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm, int R,
+                                           WarpSel& W, int& cnt, int& ntop, int K, int lane,
+                                           unsigned long long* tacc) {
+    const long long c0 = clock64();
+    if (P.stats && lane == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+    const int rows = R / P.nch;
+    const int EB = max(1, WS_RS / R);
+    for (int e0 = 0; e0 < cnt; e0 += EB) {
+        const int ng = min(EB, cnt - e0);
+        // run sums: sum += ti*or left to right (matcher.hpp:72-76)
+        int e = 0, r = lane;
+        while (r >= R) {
+            r -= R;
+            ++e;
+        }
+        for (int w = lane; w < ng * R; w += 32) {
+            const int pos = W.cidx[e0 + e];
+            const int x = pos / P.out_w, y = pos - x * P.out_w;
+            const int ch = r / rows;
+            const short4 rw = W.rows[r - ch * rows];
+            const double* a = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
+                              static_cast<size_t>(x + rw.x) * P.wc + y;
+            const double* b = tm + (ch * P.Tc + rw.x) * P.Tc;
+            double sum = 0.0;
+#pragma unroll 8
+            for (int t = rw.y; t < rw.z; ++t) sum = __dadd_rn(sum, __dmul_rn(__ldg(a + t), __ldg(b + t)));
+            W.rsum[w] = sum;
+            r += 32;
+            while (r >= R) {
+                r -= R;
+                ++e;
+            }
+        }
+        __syncwarp();
+        // fold: acc += sum over runs in row-major order (matcher.hpp:77, 160-161)
+        for (int e = lane; e < ng; e += 32) {
+            double acc = 0.0;
+            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, W.rsum[e * R + r]);
+            W.ckey[e0 + e] = acc;
+        }
+        __syncwarp();
+    }
+    const long long c1 = clock64();
+    for (int e = lane; e < ntop; e += 32) {
+        W.ckey[cnt + e] = W.tkey[e];
+        W.cidx[cnt + e] = W.tidx[e];
+    }
+    __syncwarp();
+    const int n = cnt + ntop;
+    const int keep = min(K, n);
+    if (n <= 32) {
+        // one pass: every entry's rank under the reference ordering
+        const double mk = lane < n ? W.ckey[lane] : 0.0;
+        const int mi = lane < n ? W.cidx[lane] : INT_MAX;
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const double ok = __shfl_sync(0xffffffffu, mk, j);
+            const int oi = __shfl_sync(0xffffffffu, mi, j);
+            rank += better(ok, oi, mk, mi);
+        }
+        __syncwarp();
+        if (lane < n && rank < keep) {
+            W.tkey[rank] = mk;
+            W.tidx[rank] = mi;
+        }
+    } else {
+        for (int round = 0; round < keep; ++round) {
+            double bk = 0.0;
+            int bi = INT_MAX, bp = -1;
+            for (int e = lane; e < n; e += 32) {
+                const int ix = W.cidx[e];
+                if (ix >= 0 && (bp < 0 || better(W.ckey[e], ix, bk, bi))) {
+                    bk = W.ckey[e];
+                    bi = ix;
+                    bp = e;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
+                    bk = ok;
+                    bi = oi;
+                    bp = op;
+                }
+            }
+            if (lane == 0) {
+                W.tkey[round] = bk;
+                W.tidx[round] = bi;
+                W.cidx[bp] = -1;
+            }
+            __syncwarp();
+        }
+    }
+    ntop = keep;
+    cnt = 0;
+    __syncwarp();
+    if (tacc && lane == 0) {
+        atomicAdd(&tacc[0], static_cast<unsigned long long>(c1 - c0));
+        atomicAdd(&tacc[1], static_cast<unsigned long long>(clock64() - c1));
+    }
+}
+
+__global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
+    SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
+    extern __shared__ __align__(16) unsigned char ws_raw[];
+    WarpSel* smem_ws = reinterpret_cast<WarpSel*>(ws_raw);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * WS_WARPS + wid;
+    if (slot >= nj) return;
+    WarpSel& W = smem_ws[wid];
+    const int gj = job0 + slot;
+    const Job jb = jobs[gj];
+    const int Tc = P.Tc;
+    int fr, fc;
+    unsigned long long* tacc = P.stats ? P.stats + 8 : nullptr;  // phase clocks
+    long long clk0 = clock64(), clk1 = 0, clk2 = 0, clk3 = 0;
+    if (jb.shape == kNone) {
+        fr = jb.fr;
+        fc = jb.fc;
+    } else {
+        const int K = P.K;
+        const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+        const double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+        const int32_t* tsum = P.summary + static_cast<size_t>(slot) * P.ntiles * kTcQ;
+        // 1. exact K-th largest screen score from the per-tile top-Q lists
+        int top[kTcQ];
+#pragma unroll
+        for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
+        const int nv = P.ntiles * kTcQ;
+        for (int e0 = 0; e0 < nv; e0 += 32 * 8) {
+            int vb[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int e = e0 + i * 32 + lane;
+                vb[i] = e < nv ? tsum[e] : INT_MIN;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                int v = vb[i];
+                if (v > top[kTcQ - 1]) {
+#pragma unroll
+                    for (int j = 0; j < kTcQ; ++j)
+                        if (v > top[j]) {
+                            const int t = top[j];
+                            top[j] = v;
+                            v = t;
+                        }
+                }
+            }
+        }
+        int ptr = 0, acc = 0, thr = INT_MIN;
+        for (int round = 0; round < kTcQ + 1; ++round) {
+            int head = INT_MIN;
+#pragma unroll
+            for (int i = 0; i < kTcQ; ++i)
+                if (i == ptr) head = top[i];
+            int m = head;
+            for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < kTcQ; ++i)
+                if (i >= ptr && top[i] == m) ++c;
+            ptr += c;
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            acc += c;
+            if (acc >= K || m == INT_MIN) {
+                thr = m;
+                break;
+            }
+        }
+        if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+        clk1 = clock64();
+        int R = 0;
+        for (int s0 = 0; s0 < Tc; s0 += 32) {
+            const int s = s0 + lane;
+            int t0 = 0, t1 = 0;
+            if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+            const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
+            if (t1 > t0) W.rows[R + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
+            R += __popc(m);
+        }
+        __syncwarp();
+        R *= P.nch;
+        // 2. gather every window at or above the threshold, row-major.  Tile
+        //    heads are tested 32 at a time; a qualifying tile is read with one
+        //    vector load per lane (8 consecutive scores).
+        int cnt = 0, ntop = 0;
+        for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
+            const int tt = t0 + lane;
+            const bool hit = tt < P.ntiles && tsum[static_cast<size_t>(tt) * kTcQ] >= thr;
+            unsigned tiles = __ballot_sync(0xffffffffu, hit);
+            while (tiles) {
+                const int t = t0 + __ffs(tiles) - 1;
+                tiles &= tiles - 1;
+                const int p0 = t * kTcTile + lane * 4;  // kTcTile = 128 = 32 lanes x 4
+                int v[4];
+                if (p0 + 4 <= P.npos) {
+                    const int4 a = *reinterpret_cast<const int4*>(sc + p0);
+                    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[i] = p0 + i < P.npos ? sc[p0 + i] : INT_MIN;
+                }
+                // at most 32 appends per step, flushed before the buffer can overflow
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool q = v[i] >= thr;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (!bal) continue;
+                    if (cnt + 32 > WS_CB) warp_flush(P, tm, R, W, cnt, ntop, K, lane, tacc);
+                    if (q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = p0 + i;
+                    cnt += __popc(bal);
+                    __syncwarp();
+                }
+            }
+        }
+        if (cnt > 0) warp_flush(P, tm, R, W, cnt, ntop, K, lane, tacc);
+        clk2 = clock64();
+        // 3. choose (matcher.hpp:207-241)
+        int pick = jb.pick;
+        if (pick < 0) {
+            int best = 0, best_mis = INT_MAX;
+            for (int c = 0; c < ntop; ++c) {
+                const int pos = W.tidx[c];
+                const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
+                int mis = 0;
+                for (int r = 0; r < P.T; ++r)
+                    for (int cc = lane; cc < P.T; cc += 32) {
+                        const uint8_t hv = P.hd[static_cast<size_t>(jb.top + r) * P.ww + jb.left + cc];
+                        if (hv != kNoDatum && P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != hv)
+                            ++mis;
+                    }
+                for (int o = 16; o > 0; o >>= 1) mis += __shfl_xor_sync(0xffffffffu, mis, o);
+                if (mis == 0) {
+                    pick = c;
+                    break;
+                }
+                if (mis < best_mis) {
+                    best = c;
+                    best_mis = mis;
+                }
+            }
+            if (pick < 0) pick = best;
+        }
+        const int pos = W.tidx[pick];
+        fr = (pos / P.out_w) << P.J;
+        fc = (pos % P.out_w) << P.J;
+        clk3 = clock64();
+    }
+    // 4. paste (simulator.hpp:483-493) + source-block map
+    const int T = P.T;
+    uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
+    uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
+    const int wpr = T >> 2;  // 32-bit words per row
+    const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= 32 && (32 % wpr) == 0;
+    if (vec4) {
+        // lane -> (row phase, word); 8 independent loads in flight per lane
+        const int rpi = 32 / wpr, rsub = lane / wpr, cw = lane - rsub * wpr;
+        const uint8_t* srcp = P.ti + static_cast<size_t>(fr) * P.ti_w + fc + 4 * cw;
+        uint8_t* dstp = g + static_cast<size_t>(jb.top) * P.ww + jb.left + 4 * cw;
+        for (int r0 = rsub; r0 < T; r0 += rpi * 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = r0 + i * rpi;
+                if (r < T) v[i] = *reinterpret_cast<const uint32_t*>(srcp + static_cast<size_t>(r) * P.ti_w);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = r0 + i * rpi;
+                if (r < T) {
+                    *reinterpret_cast<uint32_t*>(dstp + static_cast<size_t>(r) * P.ww) = v[i];
+                    if (trace) *reinterpret_cast<uint32_t*>(trace + r * T + 4 * cw) = v[i];
+                }
+            }
+        }
+    } else {
+        for (int r = 0; r < T; ++r)
+            for (int c = lane; c < T; c += 32) {
+                const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+                g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
+                if (trace) trace[r * T + c] = v;
+            }
+    }
+    if (P.src) {
+        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc +
+                      static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
+        const int s0 = (fr / P.B) * P.wc + fc / P.B;
+        for (int a = 0; a < Tc; ++a)
+            for (int b = lane; b < Tc; b += 32) sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
+    }
+    if (lane == 0) {
+        P.chosen[2 * gj] = fr;
+        P.chosen[2 * gj + 1] = fc;
+        if (tacc && clk1) {
+            const long long clk4 = clock64();
+            atomicAdd(&tacc[2], static_cast<unsigned long long>(clk1 - clk0));
+            atomicAdd(&tacc[3], static_cast<unsigned long long>(clk2 - clk1));
+            atomicAdd(&tacc[4], static_cast<unsigned long long>(clk3 - clk2));
+            atomicAdd(&tacc[5], static_cast<unsigned long long>(clk4 - clk3));
+        }
     }
 }
 
@@ -810,11 +1198,18 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     int max_key = 0;
     for (const Plan& p : plans) max_key = std::max(max_key, keymul * (p.n_outer - 1) + p.n_inner - 1);
-    std::vector<std::vector<Job>> waves(max_key + 1);
+
+    // Realizations are split into G independent groups, each on its own
+    // stream, so one group's latency-bound select overlaps another group's
+    // tensor-core screen.  Within a group, waves run in order.
+    int G = std::max(1, std::min(n_real, 4));
+    if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
+    std::vector<std::vector<std::vector<Job>>> gw(G, std::vector<std::vector<Job>>(max_key + 1));
     size_t total_jobs = 0;
     for (int r = 0; r < n_real; ++r) {
         const Plan& p = plans[r];
         std::mt19937_64& rng = rngs[r];
+        const int g = static_cast<int>(static_cast<int64_t>(r) * G / n_real);
         const int cnt = static_cast<int>(p.tops.size());
         for (int k = 0; k < cnt; ++k) {
             Job jb{};
@@ -834,18 +1229,22 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   lattice_hd[static_cast<size_t>(jb.top / stride) * nlc + jb.left / stride];
                 jb.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
             }
-            waves[keymul * p.outer_idx[k] + p.inner_idx[k]].push_back(jb);
+            gw[g][keymul * p.outer_idx[k] + p.inner_idx[k]].push_back(jb);
             ++total_jobs;
         }
     }
     std::vector<Job> flat;
     flat.reserve(total_jobs);
-    std::vector<size_t> wave_off;
-    for (auto& w : waves) {
-        wave_off.push_back(flat.size());
-        flat.insert(flat.end(), w.begin(), w.end());
+    std::vector<std::vector<size_t>> wave_off(G);  // per group, absolute offsets into flat
+    size_t max_wave = 1;
+    for (int g = 0; g < G; ++g) {
+        for (auto& w : gw[g]) {
+            wave_off[g].push_back(flat.size());
+            flat.insert(flat.end(), w.begin(), w.end());
+            max_wave = std::max(max_wave, w.size());
+        }
+        wave_off[g].push_back(flat.size());
     }
-    wave_off.push_back(flat.size());
 
     // ---- exactness guard for the fp32 screen
     const double maxw = ti->mode == 0 ? B : static_cast<double>(ti->F - 1) * B;
@@ -869,16 +1268,14 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         hd_scatter_kernel<<<(n_hd + 255) / 256, 256, 0, st>>>(d_hdl, n_hd, d_hd, ww);
         CCW_CUDA(cudaGetLastError());
     }
-    const size_t score_budget = static_cast<size_t>(512) << 20;
-    const size_t maxj = std::max<size_t>(1, std::min<size_t>(flat.size(), score_budget / (sizeof(int32_t) * npos)));
     const int sld = (npos + 3) & ~3;
-    int32_t* d_scores = ctx->scores.as<int32_t>(maxj * sld);
-    int32_t* d_wts = ctx->wts.as<int32_t>(maxj * std::max(ti->nscr, 1) * Tc * Tc);
-    double* d_tm = ctx->tm64.as<double>(maxj * ti->nch * Tc * Tc);
+    const size_t score_budget = (static_cast<size_t>(512) << 20) / G;
+    const size_t maxj = std::max<size_t>(1, std::min<size_t>(max_wave, score_budget / (sizeof(int32_t) * sld)));
+    int32_t* d_scores = ctx->scores.as<int32_t>(G * maxj * sld);
+    int32_t* d_wts = ctx->wts.as<int32_t>(G * maxj * std::max(ti->nscr, 1) * Tc * Tc);
+    double* d_tm = ctx->tm64.as<double>(G * maxj * ti->nch * Tc * Tc);
     int32_t* d_chosen = ctx->chosen.as<int32_t>(2 * flat.size());
-    const bool want_pasted = traces != nullptr;
-    for (int r = 0; traces && r < n_real; ++r) (void)r;
-    uint8_t* d_pasted = want_pasted ? ctx->pasted.as<uint8_t>(flat.size() * T * T) : nullptr;
+    uint8_t* d_pasted = traces ? ctx->pasted.as<uint8_t>(flat.size() * T * T) : nullptr;
     int* d_mism = ctx->mism.as<int>(n_real);
     CCW_CUDA(cudaMemsetAsync(d_mism, 0, sizeof(int) * n_real, st));
 
@@ -910,9 +1307,6 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.wh = wh;
     P.ww = ww;
     P.hd = d_hd;
-    P.wts = d_wts;
-    P.tm64 = d_tm;
-    P.scores = d_scores;
     P.sld = sld;
     P.chosen = d_chosen;
     P.pasted = d_pasted;
@@ -930,16 +1324,32 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     int32_t* d_summary = nullptr;
     if (use_tc) {
         d_x = ti_im2col(ti, Tc, st);
-        d_w8 = ctx->wts8.as<int8_t>(maxj * kpad);
-        d_summary = ctx->summary.as<int32_t>(maxj * ntiles * kTcQ);
+        d_w8 = ctx->wts8.as<int8_t>(G * maxj * kpad);
+        d_summary = ctx->summary.as<int32_t>(G * maxj * ntiles * kTcQ);
     }
-    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(4);
-    CCW_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), st));
-    P.wts8 = d_w8;
+    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(16);
+    CCW_CUDA(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
+    // source-block map (fast or_prep), valid whenever pastes are verbatim TI blocks
+    const int swc = ww / B;
+    int32_t* d_src = nullptr;
+    if (!cfg.min_cut) {
+        d_src = ctx->src.as<int32_t>(static_cast<size_t>(n_real) * (wh / B) * swc);
+    }
+    P.src = d_src;
+    P.swc = swc;
+    const bool warp_select = use_tc && Kp <= kTcQ && !cfg.min_cut && cfg.scoring == 0 &&
+                             ti->nch * Tc <= WS_RS && Tc <= WS_MAXTC;
     P.kpad = kpad;
-    P.summary = d_summary;
     P.ntiles = ntiles;
     P.stats = d_stats;
+    std::vector<SimParams> GP(G, P);
+    for (int g = 0; g < G; ++g) {
+        GP[g].scores = d_scores + g * maxj * sld;
+        GP[g].wts = d_wts + g * maxj * std::max(ti->nscr, 1) * Tc * Tc;
+        GP[g].tm64 = d_tm + g * maxj * ti->nch * Tc * Tc;
+        GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
+        GP[g].summary = d_summary ? d_summary + g * maxj * ntiles * kTcQ : nullptr;
+    }
 
     const size_t ccf_smem = ccf_smem_bytes(Tc, ti->nscr);
     const size_t sel_smem = sel_layout(Kp, T, OV, ti->nch, Tc, cfg.scoring == 1).total;
@@ -949,70 +1359,93 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   static_cast<int>(ccf_smem)));
     CCW_CUDA(cudaFuncSetAttribute(select_paste_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sel_smem)));
+    CCW_CUDA(cudaFuncSetAttribute(select_paste_warp_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(WarpSel) * WS_WARPS)));
 
-    EventTimer tm{ctx, {}, {}, 0};
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (ctx->profiling) {
-        ev0 = tm.get();
-        ev1 = tm.get();
-        CCW_CUDA(cudaEventRecord(ev0, st));
+    // group streams, forked from / joined back to the context stream
+    while (static_cast<int>(ctx->gstreams.size()) < G) {
+        cudaStream_t s2;
+        CCW_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        ctx->gstreams.push_back(s2);
     }
+    EventTimer tm{ctx, {}, {}, 0};
+    cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
+    CCW_CUDA(cudaEventRecord(ev0, st));
+    for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
     int64_t launches = 0, ccf_launches = 0;
     double ccf_flop = 0, ccf_flop_ref = 0, ccf_mma_flop = 0;
     const dim3 ccf_grid_xy((out_w + CCF_TY - 1) / CCF_TY, (out_h + CCF_TX - 1) / CCF_TX);
-    for (size_t w = 0; w + 1 < wave_off.size(); ++w) {
-        for (size_t j0 = wave_off[w]; j0 < wave_off[w + 1]; j0 += maxj) {
-            const int nj = static_cast<int>(std::min(maxj, wave_off[w + 1] - j0));
-            const bool first_wave = flat[j0].shape == kNone;
-            if (!first_wave) {
-                or_prep_kernel<<<nj, 128, 0, st>>>(P, d_jobs, static_cast<int>(j0));
-                ++launches;
-                if (use_screen) {
-                    cudaEvent_t a = nullptr, b = nullptr;
-                    if (ctx->profiling) {
-                        a = tm.get();
-                        b = tm.get();
-                        CCW_CUDA(cudaEventRecord(a, st));
-                    }
-                    if (use_tc) {
-                        launch_ccf_tc(d_w8, static_cast<int>(maxj), d_x, npos, sld, kpad, nj, d_scores,
-                                      d_summary, st);
-                    } else {
-                        dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
-                        ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, st>>>(P, d_jobs,
-                                                                               static_cast<int>(j0));
-                    }
+    for (int w = 0; w <= max_key; ++w) {
+        for (int g = 0; g < G; ++g) {
+            cudaStream_t gs = ctx->gstreams[g];
+            const SimParams& Q = GP[g];
+            for (size_t j0 = wave_off[g][w]; j0 < wave_off[g][w + 1]; j0 += maxj) {
+                const int nj = static_cast<int>(std::min(maxj, wave_off[g][w + 1] - j0));
+                const bool first_wave = flat[j0].shape == kNone;
+                if (!first_wave) {
+                    if (d_src)
+                        or_prep_src_kernel<<<nj, 128, 0, gs>>>(Q, d_jobs, static_cast<int>(j0));
+                    else
+                        or_prep_kernel<<<nj, 128, 0, gs>>>(Q, d_jobs, static_cast<int>(j0));
                     ++launches;
-                    ++ccf_launches;
-                    if (ctx->profiling) {
-                        CCW_CUDA(cudaEventRecord(b, st));
-                        tm.ccf.push_back({a, b});
-                    }
-                    ccf_mma_flop += 2.0 * kpad * static_cast<double>(npos) * nj;
-                    for (int q = 0; q < nj; ++q) {
-                        const int sh = flat[j0 + q].shape;
-                        const double m = sh == kL ? mask_cells : static_cast<double>(Tc) * OVc;
-                        ccf_flop += 2.0 * ti->nscr * npos * m;
-                        ccf_flop_ref += 2.0 * ti->nch * npos * m;
+                    if (use_screen) {
+                        cudaEvent_t a = nullptr, b = nullptr;
+                        if (ctx->profiling) {
+                            a = tm.get();
+                            b = tm.get();
+                            CCW_CUDA(cudaEventRecord(a, gs));
+                        }
+                        if (use_tc) {
+                            launch_ccf_tc(Q.wts8, static_cast<int>(maxj), d_x, npos, sld, kpad, nj,
+                                          Kp, Q.scores, Q.summary, gs);
+                        } else {
+                            dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
+                            ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, gs>>>(
+                                Q, d_jobs, static_cast<int>(j0));
+                        }
+                        ++launches;
+                        ++ccf_launches;
+                        if (ctx->profiling) {
+                            CCW_CUDA(cudaEventRecord(b, gs));
+                            tm.ccf.push_back({a, b});
+                        }
+                        ccf_mma_flop += 2.0 * kpad * static_cast<double>(npos) * nj;
+                        for (int q = 0; q < nj; ++q) {
+                            const int sh = flat[j0 + q].shape;
+                            const double m = sh == kL ? mask_cells : static_cast<double>(Tc) * OVc;
+                            ccf_flop += 2.0 * ti->nscr * npos * m;
+                            ccf_flop_ref += 2.0 * ti->nch * npos * m;
+                        }
                     }
                 }
-            }
-            cudaEvent_t a = nullptr, b = nullptr;
-            if (ctx->profiling) {
-                a = tm.get();
-                b = tm.get();
-                CCW_CUDA(cudaEventRecord(a, st));
-            }
-            select_paste_kernel<<<nj, SEL_T, sel_smem, st>>>(P, d_jobs, static_cast<int>(j0),
-                                                            use_screen ? 1 : 0);
-            ++launches;
-            if (ctx->profiling) {
-                CCW_CUDA(cudaEventRecord(b, st));
-                tm.sel.push_back({a, b});
+                cudaEvent_t a = nullptr, b = nullptr;
+                if (ctx->profiling) {
+                    a = tm.get();
+                    b = tm.get();
+                    CCW_CUDA(cudaEventRecord(a, gs));
+                }
+                if (warp_select || (first_wave && !cfg.min_cut))
+                    select_paste_warp_kernel<<<(nj + WS_WARPS - 1) / WS_WARPS, WS_WARPS * 32,
+                                               sizeof(WarpSel) * WS_WARPS, gs>>>(
+                        Q, d_jobs, static_cast<int>(j0), nj);
+                else
+                    select_paste_kernel<<<nj, SEL_T, sel_smem, gs>>>(Q, d_jobs, static_cast<int>(j0),
+                                                                     use_screen ? 1 : 0);
+                ++launches;
+                if (ctx->profiling) {
+                    CCW_CUDA(cudaEventRecord(b, gs));
+                    tm.sel.push_back({a, b});
+                }
             }
         }
     }
     CCW_CUDA(cudaGetLastError());
+    for (int g = 0; g < G; ++g) {
+        cudaEvent_t e = tm.get();
+        CCW_CUDA(cudaEventRecord(e, ctx->gstreams[g]));
+        CCW_CUDA(cudaStreamWaitEvent(st, e, 0));
+    }
 
     // ---- finalize
     uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
@@ -1024,11 +1457,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         ++launches;
         CCW_CUDA(cudaGetLastError());
     }
-    if (ctx->profiling) CCW_CUDA(cudaEventRecord(ev1, st));
+    CCW_CUDA(cudaEventRecord(ev1, st));
     if (h_out)
         CCW_CUDA(cudaMemcpyAsync(h_out, fin, static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real,
                                  cudaMemcpyDeviceToHost, st));
-    unsigned long long stats[4] = {0, 0, 0, 0};
+    unsigned long long stats[16] = {0};
     CCW_CUDA(cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
     std::vector<int> mism(n_real, 0);
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
@@ -1043,22 +1476,24 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     CCW_CUDA(cudaStreamSynchronize(st));
 
-    if (ctx->profiling) {
+    {
         float ms = 0;
         cudaEventElapsedTime(&ms, ev0, ev1);
         ctx->timing.total_ms = ms;
-        ctx->timing.ccf_ms = pair_ms(tm.ccf);
-        ctx->timing.select_ms = pair_ms(tm.sel);
-    } else {
-        ctx->timing.total_ms = ctx->timing.ccf_ms = ctx->timing.select_ms = 0;
+        ctx->timing.ccf_ms = ctx->profiling ? pair_ms(tm.ccf) : 0.0;
+        ctx->timing.select_ms = ctx->profiling ? pair_ms(tm.sel) : 0.0;
     }
     ctx->timing.ccf_launches = ccf_launches;
     ctx->timing.launches = launches + (d_hd ? 1 : 0) + 0;
     ctx->timing.ccf_flop = ccf_flop;
     ctx->timing.ccf_flop_ref = ccf_flop_ref;
-    ctx->timing.waves = static_cast<int64_t>(wave_off.size() - 1);
+    ctx->timing.waves = static_cast<int64_t>(max_key + 1);
+    ctx->timing.groups = G;
     ctx->timing.jobs = static_cast<int64_t>(flat.size());
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
+    if (getenv("CCW_PHASES"))
+        fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu\n",
+                stats[8], stats[9], stats[10], stats[11], stats[12], stats[13]);
     ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
     ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
