@@ -35,7 +35,7 @@ namespace {
 constexpr int kM = 128;
 constexpr int kN = 256;
 constexpr int kKC = 128;  // bytes of K per stage (one 128B swizzle atom)
-constexpr int kStages = 2;
+constexpr int kStages = 4;
 constexpr int kABytes = kM * kKC;
 constexpr int kBBytes = kN * kKC;
 constexpr int kStageBytes = kABytes + kBBytes;
@@ -122,6 +122,134 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
           "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
         : "r"(taddr))
 
+// One (job tile, position tile) of accumulators, drained from TMEM: exact
+// scores (optional), the per-half-tile top-Q summary, and -- in list mode --
+// the (score, position) pairs reaching the Q-th score.
+template <int Q>
+__device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int m0, int n0,
+                                            int warp, int lane) {
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int job = m0 + q * 32 + lane;
+    const bool valid_job = job < a.nj;
+    int top[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) top[i] = INT_MIN;
+    int32_t* out = a.scores ? a.scores + static_cast<size_t>(valid_job ? job : 0) * a.sld : nullptr;
+    const uint32_t trow = tbuf + (static_cast<uint32_t>(q * 32) << 16) + half * (kN / 2);
+    const int pbase = n0 + half * (kN / 2);
+    const int ntile = (n0 / kN) * 2 + half;
+    for (int c = 0; c < kN / 64; ++c) {
+        uint32_t r[32];
+        LDTM_X32(trow + c * 32, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int p0 = pbase + c * 32;
+        if (valid_job) {
+            if (!out) {
+                // list mode: no score rows
+            } else if (p0 + 32 <= a.npos) {
+                int4* dst = reinterpret_cast<int4*>(out + p0);
+#pragma unroll
+                for (int v = 0; v < 8; ++v)
+                    dst[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+            } else {
+                for (int i = 0; i < 32; ++i)
+                    if (p0 + i < a.npos) out[p0 + i] = static_cast<int>(r[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                int v = static_cast<int>(r[i]);
+                if (p0 + i < a.npos && v > top[Q - 1]) {
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        if (v > top[j]) {
+                            const int t = top[j];
+                            top[j] = v;
+                            v = t;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    int2* sm_out = a.summary + (static_cast<size_t>(valid_job ? job : 0) * a.ntiles + ntile) * kTcQ;
+    if (out) {
+        if (valid_job)
+#pragma unroll
+            for (int i = 0; i < kTcQ; ++i) sm_out[i] = make_int2(i < Q ? top[i < Q ? i : 0] : INT_MIN, -1);
+        return;
+    }
+    // list mode, pass 2: pairs reaching the Q-th score, in position order
+    const int L = top[Q - 1];
+    int lv[Q], lp[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        lv[i] = INT_MIN;
+        lp[i] = -1;
+    }
+    int n = 0;
+    for (int c = 0; c < kN / 64; ++c) {
+        uint32_t r[32];
+        LDTM_X32(trow + c * 32, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int p0 = pbase + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int v = static_cast<int>(r[i]);
+            if (valid_job && p0 + i < a.npos && v >= L) {
+#pragma unroll
+                for (int j = 0; j < Q; ++j)
+                    if (j == n) {
+                        lv[j] = v;
+                        lp[j] = p0 + i;
+                    }
+                ++n;
+            }
+        }
+    }
+    const bool ovf = n > Q;
+    if (__any_sync(0xffffffffu, ovf)) {  // rare: ties overflow the list -> exact scores of the half tile
+        int32_t* o2 = a.ovf + static_cast<size_t>(valid_job ? job : 0) * a.sld;
+        for (int c = 0; c < kN / 64; ++c) {
+            uint32_t r[32];
+            LDTM_X32(trow + c * 32, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int p0 = pbase + c * 32;
+            if (valid_job && ovf)
+                for (int i = 0; i < 32; ++i)
+                    if (p0 + i < a.npos) o2[p0 + i] = static_cast<int>(r[i]);
+        }
+    }
+    if (!ovf) {  // order by (score desc, position asc): entry 0 = tile max
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+#pragma unroll
+            for (int j = Q - 1; j >= i; --j)
+                if (lv[j] > lv[j - 1] ||
+                    (lv[j] == lv[j - 1] && lp[j] >= 0 && (lp[j - 1] < 0 || lp[j] < lp[j - 1]))) {
+                    const int tv = lv[j], tp = lp[j];
+                    lv[j] = lv[j - 1];
+                    lp[j] = lp[j - 1];
+                    lv[j - 1] = tv;
+                    lp[j - 1] = tp;
+                }
+    }
+    if (valid_job) {
+#pragma unroll
+        for (int i = 0; i < kTcQ; ++i) {
+            int2 e = make_int2(INT_MIN, -1);
+            if (i < Q)
+                e = ovf ? make_int2(top[i < Q ? i : 0], -2) : make_int2(lv[i < Q ? i : 0], lp[i < Q ? i : 0]);
+            sm_out[i] = e;
+        }
+    }
+}
+
+// Persistent implicit GEMM: one CTA per SM loops over (job tile, position
+// tile) pairs; warp 0 streams K stages through a 4-deep TMA ring, warp 1
+// issues the MMAs into one of two TMEM accumulators, warps 2..9 drain the
+// other accumulator -- the epilogue of tile i overlaps the loads and MMAs of
+// tile i+1.
 template <int Q>
 __global__ void __launch_bounds__(kThreads, 1)
     ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -131,24 +259,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
     uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* tfull = empty + kStages;   // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;        // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * kN, m0 = blockIdx.y * kM;
+    const int n_mt = (a.nj + kM - 1) / kM, n_nt = (a.npos + kN - 1) / kN;
+    const int ntot = n_mt * n_nt;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
             mbar_init(smem_u32(&empty[s]), 1);
         }
-        mbar_init(smem_u32(tfull), 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_u32(&tfull[b]), 1);
+            mbar_init(smem_u32(&tempty[b]), kEpiWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)));
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)));
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -158,86 +291,60 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer
-            for (int kc = 0; kc < a.nk; ++kc) {
-                const int s = kc % kStages;
-                if (kc >= kStages) mbar_wait(smem_u32(&empty[s]), ((kc / kStages) - 1) & 1);
-                const uint32_t bar = smem_u32(&full[s]);
-                mbar_expect_tx(bar, kStageBytes);
-                tma_load_2d(smem_u32(sm + s * kStageBytes), &tmA, kc * kKC, m0, bar);
-                tma_load_2d(smem_u32(sm + s * kStageBytes + kABytes), &tmB, kc * kKC, n0, bar);
+        if (lane == 0) {  // TMA producer: K stages of every tile, one ring
+            int it = 0;
+            for (int t = blockIdx.x; t < ntot; t += gridDim.x) {
+                const int m0 = (t % n_mt) * kM, n0 = (t / n_mt) * kN;
+                for (int kc = 0; kc < a.nk; ++kc, ++it) {
+                    const int s = it % kStages;
+                    if (it >= kStages) mbar_wait(smem_u32(&empty[s]), ((it / kStages) - 1) & 1);
+                    const uint32_t bar = smem_u32(&full[s]);
+                    mbar_expect_tx(bar, kStageBytes);
+                    tma_load_2d(smem_u32(sm + s * kStageBytes), &tmA, kc * kKC, m0, bar);
+                    tma_load_2d(smem_u32(sm + s * kStageBytes + kABytes), &tmB, kc * kKC, n0, bar);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // single-thread MMA issuer
             constexpr uint32_t idesc = i8_idesc(kM, kN);
-            for (int kc = 0; kc < a.nk; ++kc) {
-                const int s = kc % kStages;
-                mbar_wait(smem_u32(&full[s]), (kc / kStages) & 1);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntot; t += gridDim.x, ++lt) {
+                const int b = lt & 1;
+                if (lt >= 2) mbar_wait(smem_u32(&tempty[b]), ((lt >> 1) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t ad = sw128_desc(smem_u32(sm + s * kStageBytes));
-                const uint64_t bd = sw128_desc(smem_u32(sm + s * kStageBytes + kABytes));
+                const uint32_t acc = tmem + b * kN;
+                for (int kc = 0; kc < a.nk; ++kc, ++it) {
+                    const int s = it % kStages;
+                    mbar_wait(smem_u32(&full[s]), (it / kStages) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t ad = sw128_desc(smem_u32(sm + s * kStageBytes));
+                    const uint64_t bd = sw128_desc(smem_u32(sm + s * kStageBytes + kABytes));
 #pragma unroll
-                for (int k = 0; k < kKC / 32; ++k)  // K = 32 bytes per kind::i8 MMA
-                    mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
-                mma_commit(smem_u32(&empty[s]));
-            }
-            mma_commit(smem_u32(tfull));
-        }
-    } else {  // epilogue: warps 2..9; lane quarter = warp % 4, column half = (warp - 2) / 4
-        mbar_wait(smem_u32(tfull), 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int q = warp & 3;
-        const int half = (warp - 2) >> 2;
-        const int job = m0 + q * 32 + lane;
-        const bool valid_job = job < a.nj;
-        int top[Q];
-#pragma unroll
-        for (int i = 0; i < Q; ++i) top[i] = INT_MIN;
-        int32_t* out = a.scores + static_cast<size_t>(valid_job ? job : 0) * a.sld;
-        const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * (kN / 2);
-        for (int c = 0; c < kN / 64; ++c) {
-            uint32_t r[32];
-            LDTM_X32(trow + c * 32, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int p0 = n0 + half * (kN / 2) + c * 32;
-            if (valid_job) {
-                if (p0 + 32 <= a.npos) {
-                    int4* dst = reinterpret_cast<int4*>(out + p0);
-#pragma unroll
-                    for (int v = 0; v < 8; ++v)
-                        dst[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-                } else {
-                    for (int i = 0; i < 32; ++i)
-                        if (p0 + i < a.npos) out[p0 + i] = static_cast<int>(r[i]);
+                    for (int k = 0; k < kKC / 32; ++k)  // K = 32 bytes per kind::i8 MMA
+                        mma_i8(acc, ad + 2 * k, bd + 2 * k, idesc, (kc | k) != 0);
+                    mma_commit(smem_u32(&empty[s]));
                 }
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    int v = static_cast<int>(r[i]);
-                    if (p0 + i < a.npos && v > top[Q - 1]) {
-                        // insertion into the descending top-Q list (multiplicity kept)
-#pragma unroll
-                        for (int j = 0; j < Q; ++j) {
-                            if (v > top[j]) {
-                                const int t = top[j];
-                                top[j] = v;
-                                v = t;
-                            }
-                        }
-                    }
-                }
+                mma_commit(smem_u32(&tfull[b]));
             }
         }
-        if (valid_job) {
-            int* sm_out = a.summary + (static_cast<size_t>(job) * a.ntiles + 2 * blockIdx.x + half) * kTcQ;
-#pragma unroll
-            for (int i = 0; i < kTcQ; ++i) sm_out[i] = i < Q ? top[i < Q ? i : 0] : INT_MIN;
+    } else {  // epilogue warps 2..9
+        int lt = 0;
+        for (int t = blockIdx.x; t < ntot; t += gridDim.x, ++lt) {
+            const int b = lt & 1;
+            mbar_wait(smem_u32(&tfull[b]), (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int m0 = (t % n_mt) * kM, n0 = (t / n_mt) * kN;
+            tc_epilogue<Q>(a, tmem + b * kN, m0, n0, warp, lane);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // im2col of the TI screen planes: row = score-map position, column k =
@@ -297,6 +404,16 @@ CUtensorMap make_map(void* base, uint64_t cols_bytes, uint64_t rows, uint32_t bo
 
 size_t ccf_tc_smem_bytes() { return kStages * kStageBytes + 1024 + 256; }
 
+int tc_num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return sms;
+}
+
 int tc_kpad(int nscr, int Tc) { return ((nscr * Tc * Tc + 15) / 16) * 16; }
 
 const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st) {
@@ -315,10 +432,26 @@ const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st) {
     return X;
 }
 
-void launch_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int sld, int kpad, int nj,
-                   int K, int32_t* scores, int32_t* summary, cudaStream_t st) {
-    const CUtensorMap ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
-    const CUtensorMap mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
+TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad, int K) {
+    TcPlan pl;
+    pl.ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
+    pl.mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
+    pl.q = tc_qdepth(K);
+    auto attr = [&](auto kern) {
+        CCW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ccf_tc_smem_bytes())));
+    };
+    if (pl.q == 4)
+        attr(ccf_tc_kernel<4>);
+    else if (pl.q == 6)
+        attr(ccf_tc_kernel<6>);
+    else
+        attr(ccf_tc_kernel<8>);
+    return pl;
+}
+
+void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
+                   int32_t* ovf, int2* summary, cudaStream_t st) {
     TcArgs a;
     a.nj = nj;
     a.npos = npos;
@@ -326,25 +459,20 @@ void launch_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
     a.nk = (kpad + kKC - 1) / kKC;
     a.ntiles = tc_tiles(npos);
     a.scores = scores;
+    a.ovf = ovf;
     a.summary = summary;
-    dim3 grid((npos + kN - 1) / kN, (nj + kM - 1) / kM);
-    auto go = [&](auto kern) {
-        CCW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(ccf_tc_smem_bytes())));
-        kern<<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(ma, mb, a);
-    };
-    // summary depth: the smallest supported Q >= K (deeper lists cost epilogue
-    // instructions; K > kTcQ uses the full score rows only)
-    if (K <= 1)
-        go(ccf_tc_kernel<1>);
-    else if (K <= 2)
-        go(ccf_tc_kernel<2>);
-    else if (K <= 4)
-        go(ccf_tc_kernel<4>);
+    const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
+    dim3 grid(std::min(ntot, tc_num_sms()));
+    if (pl.q == 4)
+        ccf_tc_kernel<4><<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(pl.ma, pl.mb, a);
+    else if (pl.q == 6)
+        ccf_tc_kernel<6><<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(pl.ma, pl.mb, a);
     else
-        go(ccf_tc_kernel<8>);
-    CCW_CUDA(cudaGetLastError());
+        ccf_tc_kernel<8><<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(pl.ma, pl.mb, a);
 }
+
+// summary depth: K plus headroom (keeps tie overflow rare), from {4, 6, 8}
+int tc_qdepth(int K) { return K + 3 <= 4 ? 4 : (K + 3 <= 6 ? 6 : 8); }
 
 int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // summaries per half tile
 

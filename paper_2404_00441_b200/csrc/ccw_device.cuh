@@ -56,12 +56,15 @@ struct SimParams {
     // per-job scratch (indexed by job slot within a launch chunk)
     int32_t* wts;            // nscr*Tc*Tc integer screen weights (fp32 screen)
     int8_t* wts8;            // kpad int8 screen weights per job (tcgen05 screen), may be null
+    const int8_t* im2col;    // npos x kpad int8 TI windows (tcgen05 screen), may be null
     int kpad;
-    int32_t* summary;        // per job: ntiles x kTcQ top scores (tcgen05 screen), may be null
+    int2* summary;           // per job: ntiles x kTcQ top (score, position) (tcgen05), may be null
+    int qdepth;              // summary slots actually filled (overflow check)
     int ntiles;
     unsigned long long* stats;  // [0] windows rescored in fp64, [1] screened jobs
     double* tm64;            // nch*Tc*Tc reference-order OR apex values
     int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
+    int32_t* ovf;            // same layout, only tie-overflowing tiles written (warp path)
     int sld;
     // outputs
     int32_t* chosen;         // per job (global job id): fr, fc

@@ -297,10 +297,10 @@ __host__ __device__ inline SelLayout sel_layout(int K, int T, int OV, int nch = 
 // INT_MIN padding: block-wide radix select over the offset range, 8 bits per
 // pass, warp-aggregated shared-memory histograms.
 __device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, int* hist,
-                                 int* misc, int* redi) {
+                                 int* misc, int* redi, int stride = 1) {
     int lo = INT_MAX, hi = INT_MIN;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
-        const int v = sc[p];
+        const int v = sc[static_cast<size_t>(p) * stride];
         if (v == INT_MIN) continue;
         lo = min(lo, v);
         hi = max(hi, v);
@@ -321,8 +321,8 @@ __device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, i
             const int p = base + threadIdx.x;
             bool match = false;
             int dg = 0;
-            if (p < n && sc[p] != INT_MIN) {
-                const uint32_t u = static_cast<uint32_t>(sc[p]) - static_cast<uint32_t>(lo);
+            if (p < n && sc[static_cast<size_t>(p) * stride] != INT_MIN) {
+                const uint32_t u = static_cast<uint32_t>(sc[static_cast<size_t>(p) * stride]) - static_cast<uint32_t>(lo);
                 match = (static_cast<uint64_t>(u) >> (shift + 8)) ==
                         (static_cast<uint64_t>(prefix) >> (shift + 8));
                 dg = (u >> shift) & 255;
@@ -596,12 +596,13 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         // 1. exact screen threshold: every window whose integer score reaches
         //    the K-th largest can appear in the reference's top-K.
         const bool all = !use_screen;
-        const int32_t* tsum =
+        const int2* tsum =
             P.summary ? P.summary + static_cast<size_t>(blockIdx.x) * P.ntiles * kTcQ : nullptr;
         int thr = 0;
         if (!all) {
-            if (tsum && K <= kTcQ)  // union of per-tile top-Q lists holds the global top-K
-                thr = radix_kth_largest(tsum, P.ntiles * kTcQ, K, hist, misc, redi);
+            if (tsum && K <= P.qdepth)  // union of per-tile top-Q lists holds the global top-K
+                thr = radix_kth_largest(reinterpret_cast<const int32_t*>(tsum), P.ntiles * kTcQ, K,
+                                        hist, misc, redi, 2);
             else
                 thr = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
         }
@@ -613,7 +614,7 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         const int nspans = (P.npos + span - 1) / span;
         int ntop = 0, cnt = 0;
         for (int sp = 0; sp < nspans; ++sp) {
-            if (!all && tsum && tsum[static_cast<size_t>(sp) * kTcQ] < thr) continue;  // uniform
+            if (!all && tsum && tsum[static_cast<size_t>(sp) * kTcQ].x < thr) continue;  // uniform
             for (int sub = 0; sub < span; sub += SEL_T) {
                 const int p = sp * span + sub + tid;
                 const bool q = sub + tid < span && p < P.npos && (all || sc[p] >= thr);
@@ -869,9 +870,9 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
         fc = jb.fc;
     } else {
         const int K = P.K;
-        const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+        const int32_t* sc = P.scores ? P.scores + static_cast<size_t>(slot) * P.sld : nullptr;
         const double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
-        const int32_t* tsum = P.summary + static_cast<size_t>(slot) * P.ntiles * kTcQ;
+        const int2* tsum = P.summary + static_cast<size_t>(slot) * P.ntiles * kTcQ;
         // 1. exact K-th largest screen score from the per-tile top-Q lists
         int top[kTcQ];
 #pragma unroll
@@ -882,7 +883,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int e = e0 + i * 32 + lane;
-                vb[i] = e < nv ? tsum[e] : INT_MIN;
+                vb[i] = e < nv ? tsum[e].x : INT_MIN;
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -937,19 +938,33 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
         int cnt = 0, ntop = 0;
         for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
             const int tt = t0 + lane;
-            const bool hit = tt < P.ntiles && tsum[static_cast<size_t>(tt) * kTcQ] >= thr;
+            const bool hit = tt < P.ntiles && tsum[static_cast<size_t>(tt) * kTcQ].x >= thr;
             unsigned tiles = __ballot_sync(0xffffffffu, hit);
             while (tiles) {
                 const int t = t0 + __ffs(tiles) - 1;
                 tiles &= tiles - 1;
+                const int2* tl = tsum + static_cast<size_t>(t) * kTcQ;
+                if (!P.scores && tl[0].y != -2) {
+                    // the tile's (score, position) list holds every window >= thr
+                    const int2 cv = lane < P.qdepth ? tl[lane] : make_int2(INT_MIN, 0);
+                    const bool q = cv.x >= thr;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (cnt + 32 > WS_CB) warp_flush(P, tm, R, W, cnt, ntop, K, lane, tacc);
+                    if (q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = cv.y;
+                    cnt += __popc(bal);
+                    __syncwarp();
+                    continue;
+                }
                 const int p0 = t * kTcTile + lane * 4;  // kTcTile = 128 = 32 lanes x 4
                 int v[4];
+                const int32_t* src_sc = P.scores ? sc : P.ovf + static_cast<size_t>(slot) * P.sld;
+                if (!P.scores && P.stats && lane == 0) atomicAdd(&P.stats[2], 1ull);
                 if (p0 + 4 <= P.npos) {
-                    const int4 a = *reinterpret_cast<const int4*>(sc + p0);
+                    const int4 a = *reinterpret_cast<const int4*>(src_sc + p0);
                     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) v[i] = p0 + i < P.npos ? sc[p0 + i] : INT_MIN;
+                    for (int i = 0; i < 4; ++i) v[i] = p0 + i < P.npos ? src_sc[p0 + i] : INT_MIN;
                 }
                 // at most 32 appends per step, flushed before the buffer can overflow
 #pragma unroll
@@ -1202,7 +1217,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // Realizations are split into G independent groups, each on its own
     // stream, so one group's latency-bound select overlaps another group's
     // tensor-core screen.  Within a group, waves run in order.
-    int G = std::max(1, std::min(n_real, 4));
+    int G = std::max(1, std::min(n_real, 2));
     if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
     std::vector<std::vector<std::vector<Job>>> gw(G, std::vector<std::vector<Job>>(max_key + 1));
     size_t total_jobs = 0;
@@ -1268,7 +1283,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         hd_scatter_kernel<<<(n_hd + 255) / 256, 256, 0, st>>>(d_hdl, n_hd, d_hd, ww);
         CCW_CUDA(cudaGetLastError());
     }
-    const int sld = (npos + 3) & ~3;
+    const int sld = (npos + 3) & ~3;  // (score rows exist only for the block-select path)
     const size_t score_budget = (static_cast<size_t>(512) << 20) / G;
     const size_t maxj = std::max<size_t>(1, std::min<size_t>(max_wave, score_budget / (sizeof(int32_t) * sld)));
     int32_t* d_scores = ctx->scores.as<int32_t>(G * maxj * sld);
@@ -1321,11 +1336,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const int ntiles = tc_tiles(npos);
     const int8_t* d_x = nullptr;
     int8_t* d_w8 = nullptr;
-    int32_t* d_summary = nullptr;
+    int2* d_summary = nullptr;
     if (use_tc) {
         d_x = ti_im2col(ti, Tc, st);
         d_w8 = ctx->wts8.as<int8_t>(G * maxj * kpad);
-        d_summary = ctx->summary.as<int32_t>(G * maxj * ntiles * kTcQ);
+        d_summary = ctx->summary.as<int2>(G * maxj * ntiles * kTcQ);
     }
     unsigned long long* d_stats = ctx->stats.as<unsigned long long>(16);
     CCW_CUDA(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
@@ -1341,10 +1356,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                              ti->nch * Tc <= WS_RS && Tc <= WS_MAXTC;
     P.kpad = kpad;
     P.ntiles = ntiles;
+    P.qdepth = tc_qdepth(Kp);
     P.stats = d_stats;
+    P.im2col = d_x;
+    // list mode: the screen keeps per-tile (score, position) lists instead of score rows
+    const bool list_mode = warp_select && getenv("CCW_TCLISTS");  // measured slower (r1)
     std::vector<SimParams> GP(G, P);
     for (int g = 0; g < G; ++g) {
-        GP[g].scores = d_scores + g * maxj * sld;
+        // the warp select recomputes the few tiles it needs: no score rows
+        GP[g].scores = list_mode ? nullptr : d_scores + g * maxj * sld;
+        GP[g].ovf = list_mode ? d_scores + g * maxj * sld : nullptr;
         GP[g].wts = d_wts + g * maxj * std::max(ti->nscr, 1) * Tc * Tc;
         GP[g].tm64 = d_tm + g * maxj * ti->nch * Tc * Tc;
         GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
@@ -1363,6 +1384,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(WarpSel) * WS_WARPS)));
 
+    std::vector<TcPlan> tcplans;
+    if (use_tc)
+        for (int g = 0; g < G; ++g)
+            tcplans.push_back(plan_ccf_tc(GP[g].wts8, static_cast<int>(maxj), d_x, npos, kpad, Kp));
     // group streams, forked from / joined back to the context stream
     while (static_cast<int>(ctx->gstreams.size()) < G) {
         cudaStream_t s2;
@@ -1397,8 +1422,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                             CCW_CUDA(cudaEventRecord(a, gs));
                         }
                         if (use_tc) {
-                            launch_ccf_tc(Q.wts8, static_cast<int>(maxj), d_x, npos, sld, kpad, nj,
-                                          Kp, Q.scores, Q.summary, gs);
+                            launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.ovf,
+                                          Q.summary, gs);
                         } else {
                             dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
                             ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, gs>>>(
@@ -1495,6 +1520,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu\n",
                 stats[8], stats[9], stats[10], stats[11], stats[12], stats[13]);
     ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
+    ctx->timing.recomputed_tiles = static_cast<int64_t>(stats[2]);
     ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 
