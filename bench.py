@@ -243,10 +243,11 @@ def run_ours(args):
     dev.set_profiling(False)
     ccf_avg_ms = prof["ccf_ms"] / max(prof["ccf_launches"], 1)
     flop_per_launch = prof["ccf_flop"] / max(prof["ccf_launches"], 1)
-    peak = dev.measure_fp32_peak()
+    mma_per_launch = prof["ccf_mma_flop"] / max(prof["ccf_launches"], 1)
+    tensor = prof["ccf_variant"] == 2
+    peak = dev.measure_i8_peak() if tensor else dev.measure_fp32_peak()
     achieved = flop_per_launch / (ccf_avg_ms * 1e-3) / 1e12
     traffic = load_traffic()
-
     # end-to-end through the public API with host buffers
     h_out = torch.empty(REAL_PER_GPU * sg, dtype=torch.uint8).pin_memory()
     ti_host = np.ascontiguousarray(ti_a)
@@ -295,15 +296,23 @@ def run_ours(args):
                        "parallelism": f"realization shards x{world}",
                        "l2": "flushed before each timed step (256 MiB write, outside events)",
                        "timing": "per-step CUDA events on the library stream, max over ranks"},
-            "roofline": {"bound": "fp32", "kernel": "ccf_direct_kernel",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "roofline": {"bound": "tensor" if tensor else "fp32",
+                         "kernel": "ccf_tc_kernel (tcgen05 kind::i8)" if tensor else "ccf_direct_kernel",
+                         "achieved": achieved, "peak": peak,
+                         "unit": "TOPS" if tensor else "TFLOP/s",
                          "frac": achieved / peak if peak else None,
-                         "peak_source": "in-run FFMA microbenchmark (MEASURED_PEAKS.json has no "
-                                        "FP32 figure)",
-                         "flop_per_launch": flop_per_launch, "avg_launch_ms": ccf_avg_ms,
+                         "peak_source": ("in-run tcgen05 kind::i8 probe, same MMA shape (MEASURED_PEAKS.json "
+                                         "has only bf16)") if tensor else
+                                        "in-run FFMA probe (MEASURED_PEAKS.json has no FP32 figure)",
+                         "algorithmic_ops_per_launch": flop_per_launch,
+                         "algorithmic_ops_note": "2 x (F-1) screen channels x positions x mask cells per placement "
+                                                 "(the reference's F-channel count is x F/(F-1))",
+                         "mma_ops_issued_per_launch": mma_per_launch,
+                         "avg_launch_ms": ccf_avg_ms,
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
-                         "ccf_share_of_step": prof["ccf_ms"] / prof["total_ms"] if prof["total_ms"] else None,
-                         "select_share_of_step": prof["select_ms"] / prof["total_ms"] if prof["total_ms"] else None},
+                         "step_ms_profiled": prof["total_ms"],
+                         "ccf_ms_per_step": prof["ccf_ms"], "select_ms_per_step": prof["select_ms"],
+                         "fp64_windows_rescored": prof["rescored"]},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(ti_host.nbytes + seeds.nbytes),

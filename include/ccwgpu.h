@@ -115,6 +115,7 @@ typedef struct ccw_timing {
     double ccf_mma_flop;    /* tensor-core MMA FLOP issued (full Tc x Tc window, padded K) */
     int64_t groups;         /* realization groups run concurrently on separate streams */
     int64_t recomputed_tiles; /* summary tiles re-scored because ties overflowed the list */
+    double host_prep_ms;    /* host schedule build (plans + mt19937_64 draws) before launch */
 } ccw_timing;
 
 typedef struct ccw_ctx ccw_ctx;
@@ -135,6 +136,9 @@ CCW_API ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant);
 /* FP32 FFMA peak of this GPU (TFLOP/s), measured with an in-library
  * microbenchmark: the roofline denominator of the CUDA-core CCF screen. */
 CCW_API ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops);
+/* Dense int8 tensor-core rate (TOPS) of the CCF screen's tcgen05 MMA shape
+ * (kind::i8, M=128, N=256, cta_group::1), measured with an in-library probe. */
+CCW_API ccw_status ccw_measure_i8_peak(ccw_ctx* ctx, double* tops);
 
 /* ---------------------------------------------------------- rng -------- */
 /* rng.hpp:11-16 */

@@ -43,7 +43,7 @@ class TimingC(C.Structure):
                 ("ccf_flop_ref", C.c_double), ("waves", C.c_int64), ("jobs", C.c_int64),
                 ("rescored", C.c_int64), ("screened_jobs", C.c_int64), ("ccf_variant", C.c_int64),
                 ("ccf_mma_flop", C.c_double), ("groups", C.c_int64),
-                ("recomputed_tiles", C.c_int64)]
+                ("recomputed_tiles", C.c_int64), ("host_prep_ms", C.c_double)]
 
 
 P = C.c_void_p
@@ -63,6 +63,7 @@ SIGNATURES = {
     "ccw_ctx_last_timing": (C.c_int, [P, C.POINTER(TimingC)]),
     "ccw_ctx_set_ccf_variant": (C.c_int, [P, C.c_int]),
     "ccw_measure_fp32_peak": (C.c_int, [P, F64P]),
+    "ccw_measure_i8_peak": (C.c_int, [P, F64P]),
     "ccw_mix64": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ccw_ti_create": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
     "ccw_ti_create_device": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -316,6 +316,12 @@ class Device:
         self.check(self._lib.ccw_measure_fp32_peak(self.handle, C.byref(v)))
         return v.value
 
+    def measure_i8_peak(self) -> float:
+        """Dense int8 tcgen05 rate (TOPS) of the screen's MMA shape."""
+        v = C.c_double(0)
+        self.check(self._lib.ccw_measure_i8_peak(self.handle, C.byref(v)))
+        return v.value
+
     def close(self) -> None:
         if self.handle:
             self._lib.ccw_ctx_destroy(self.handle)

@@ -9,6 +9,7 @@
 #include <map>
 #include <utility>
 
+#include "ccf_tc.hpp"
 #include "internal.hpp"
 
 using ccwgpu::Fail;
@@ -250,6 +251,11 @@ ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant) {
 ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops) {
     if (!ctx || !tflops) return CCW_ERR_GENERIC;
     return guarded(ctx, [&] { *tflops = ccwgpu::measure_ffma_peak(ctx); });
+}
+
+ccw_status ccw_measure_i8_peak(ccw_ctx* ctx, double* tops) {
+    if (!ctx || !tops) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] { *tops = ccwgpu::measure_i8_peak(ctx->stream); });
 }
 
 uint64_t ccw_mix64(uint64_t seed, uint64_t index) {  // rng.hpp:11-16

@@ -347,6 +347,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// Tensor-core peak probe: back-to-back kind::i8 MMAs of the screen's shape
+// (M=128, N=256, K=32, cta_group::1) on shared-memory operands, one CTA per SM.
+__global__ void __launch_bounds__(128, 1) i8_peak_kernel(int iters) {
+    extern __shared__ __align__(1024) uint8_t pk_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pk_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kABytes + kBBytes);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < (kABytes + kBBytes) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u;
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(bar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        constexpr uint32_t idesc = i8_idesc(kM, kN);
+        const uint64_t ad = sw128_desc(smem_u32(sm)), bd = sw128_desc(smem_u32(sm + kABytes));
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+        mma_commit(smem_u32(bar));
+        mbar_wait(smem_u32(bar), 0);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
 // im2col of the TI screen planes: row = score-map position, column k =
 // (ch, s, t); values are exact small integers, stored as int8.
 __global__ void im2col_kernel(const float* __restrict__ scr, int nscr, int hc, int wc, int Tc,
@@ -430,6 +468,31 @@ const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st) {
     CCW_CUDA(cudaGetLastError());
     ti->im2col[Tc] = X;
     return X;
+}
+
+double measure_i8_peak(cudaStream_t st) {
+    const int sms = tc_num_sms();
+    const size_t smem = kABytes + kBBytes + 1024 + 64;
+    CCW_CUDA(cudaFuncSetAttribute(i8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    cudaEvent_t a, b;
+    CCW_CUDA(cudaEventCreate(&a));
+    CCW_CUDA(cudaEventCreate(&b));
+    const int iters = 4096;
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+        CCW_CUDA(cudaEventRecord(a, st));
+        i8_peak_kernel<<<sms, 128, smem, st>>>(iters);
+        CCW_CUDA(cudaEventRecord(b, st));
+        CCW_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        CCW_CUDA(cudaEventElapsedTime(&ms, a, b));
+        const double ops = 2.0 * kM * kN * 32.0 * 4.0 * iters * sms;
+        if (rep > 0) best = std::max(best, ops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return best;
 }
 
 TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad, int K) {

@@ -32,6 +32,9 @@ int tc_tiles(int npos);
 int tc_qdepth(int K);
 // im2col of the TI screen planes for template size Tc (cached on the TI).
 const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st);
+// Measured dense int8 tcgen05 rate of the screen's MMA shape (TOPS).
+double measure_i8_peak(cudaStream_t st);
+
 // TMA descriptors + kernel choice, built once per simulate call and group.
 struct TcPlan {
     CUtensorMap ma, mb;

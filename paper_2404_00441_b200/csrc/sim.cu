@@ -20,7 +20,11 @@
 // and once per call a finalize kernel applies the hard-data overwrite and
 // crops the work grid (simulator.hpp:506-515).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <climits>
@@ -1186,17 +1190,22 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const int reach = (T + stride - 1) / stride - 1;  // footprints overlap up to `reach` steps
     const int keymul = reach + 1;
 
-    // ---- host schedule: plans, hard-data lattice, mt19937_64 draw schedule
-    std::vector<Plan> plans;
-    plans.reserve(n_real);
-    std::vector<std::mt19937_64> rngs;
-    rngs.reserve(n_real);
-    for (int r = 0; r < n_real; ++r) {
-        rngs.emplace_back(seeds[r]);
-        plans.push_back(make_plan(cfg, rngs.back()));
+    // ---- host schedule: plans, hard-data lattice, mt19937_64 draw schedule.
+    // Every realization's draws are independent (seeded per realization), so
+    // the schedule is built in parallel host threads, then counting-sorted by
+    // (group, wave) straight into pinned staging memory for one upload.
+    std::vector<Plan> plans(n_real);
+    std::vector<std::vector<Job>> rjobs(n_real);
+    std::vector<std::vector<int>> rkeys(n_real);
+    int wh = 0, ww = 0, nlr = 0, nlc = 0;
+    {
+        std::mt19937_64 r0(seeds[0]);
+        const Plan p0 = make_plan(cfg, r0);  // geometry (identical for every plan)
+        wh = p0.work_h;
+        ww = p0.work_w;
+        nlr = (wh - T) / stride + 1;
+        nlc = (ww - T) / stride + 1;
     }
-    const int wh = plans[0].work_h, ww = plans[0].work_w;
-    const int nlr = (wh - T) / stride + 1, nlc = (ww - T) / stride + 1;
     std::vector<uint8_t> lattice_hd;
     if (hd && n_hd > 0) {
         lattice_hd.assign(static_cast<size_t>(nlr) * nlc, 0);
@@ -1211,23 +1220,17 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         lattice_hd[static_cast<size_t>(qr) * nlc + qc] = 1;
         }
     }
-    int max_key = 0;
-    for (const Plan& p : plans) max_key = std::max(max_key, keymul * (p.n_outer - 1) + p.n_inner - 1);
-
-    // Realizations are split into G independent groups, each on its own
-    // stream, so one group's latency-bound select overlaps another group's
-    // tensor-core screen.  Within a group, waves run in order.
-    int G = std::max(1, std::min(n_real, 2));
-    if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
-    std::vector<std::vector<std::vector<Job>>> gw(G, std::vector<std::vector<Job>>(max_key + 1));
-    size_t total_jobs = 0;
-    for (int r = 0; r < n_real; ++r) {
+    auto build_one = [&](int r) {
+        std::mt19937_64 rng(seeds[r]);
+        plans[r] = make_plan(cfg, rng);
         const Plan& p = plans[r];
-        std::mt19937_64& rng = rngs[r];
-        const int g = static_cast<int>(static_cast<int64_t>(r) * G / n_real);
         const int cnt = static_cast<int>(p.tops.size());
+        std::vector<Job>& jv = rjobs[r];
+        std::vector<int>& kv = rkeys[r];
+        jv.resize(cnt);
+        kv.resize(cnt);
         for (int k = 0; k < cnt; ++k) {
-            Job jb{};
+            Job& jb = jv[k];
             jb.real = r;
             jb.place = k;
             jb.top = p.tops[k];
@@ -1236,6 +1239,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             jb.vleft = p.vertical_on_left();
             jb.htop = p.horizontal_on_top();
             jb.pick = 0;
+            jb.fr = jb.fc = 0;
             if (jb.shape == kNone) {  // simulator.hpp:450-453
                 jb.fr = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->h - T) / B + 1))) * B;
                 jb.fc = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->w - T) / B + 1))) * B;
@@ -1244,22 +1248,70 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   lattice_hd[static_cast<size_t>(jb.top / stride) * nlc + jb.left / stride];
                 jb.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
             }
-            gw[g][keymul * p.outer_idx[k] + p.inner_idx[k]].push_back(jb);
-            ++total_jobs;
+            kv[k] = keymul * p.outer_idx[k] + p.inner_idx[k];
+        }
+    };
+    {
+        const int nthr = std::max(1, std::min<int>(n_real / 4, std::min<int>(16, static_cast<int>(std::thread::hardware_concurrency()))));
+        if (nthr <= 1) {
+            for (int r = 0; r < n_real; ++r) build_one(r);
+        } else {
+            std::vector<std::thread> pool;
+            std::atomic<int> next{0};
+            std::exception_ptr err;
+            std::mutex mu;
+            for (int t = 0; t < nthr; ++t)
+                pool.emplace_back([&] {
+                    for (;;) {
+                        const int r = next.fetch_add(1);
+                        if (r >= n_real) return;
+                        try {
+                            build_one(r);
+                        } catch (...) {
+                            std::lock_guard<std::mutex> lk(mu);
+                            if (!err) err = std::current_exception();
+                            return;
+                        }
+                    }
+                });
+            for (auto& th : pool) th.join();
+            if (err) std::rethrow_exception(err);
         }
     }
-    std::vector<Job> flat;
-    flat.reserve(total_jobs);
+    int max_key = 0;
+    for (const Plan& p : plans) max_key = std::max(max_key, keymul * (p.n_outer - 1) + p.n_inner - 1);
+
+    // Realizations are split into G independent groups, each on its own
+    // stream, so one group's latency-bound select overlaps another group's
+    // tensor-core screen.  Within a group, waves run in order.
+    int G = std::max(1, std::min(n_real, 2));
+    if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
+    const int nkeys = max_key + 1;
+    std::vector<size_t> bucket(static_cast<size_t>(G) * nkeys + 1, 0);
+    size_t total_jobs = 0;
+    for (int r = 0; r < n_real; ++r) {
+        const int g = static_cast<int>(static_cast<int64_t>(r) * G / n_real);
+        for (int k : rkeys[r]) ++bucket[static_cast<size_t>(g) * nkeys + k + 1];
+        total_jobs += rkeys[r].size();
+    }
+    for (size_t i = 1; i < bucket.size(); ++i) bucket[i] += bucket[i - 1];
     std::vector<std::vector<size_t>> wave_off(G);  // per group, absolute offsets into flat
     size_t max_wave = 1;
     for (int g = 0; g < G; ++g) {
-        for (auto& w : gw[g]) {
-            wave_off[g].push_back(flat.size());
-            flat.insert(flat.end(), w.begin(), w.end());
-            max_wave = std::max(max_wave, w.size());
-        }
-        wave_off[g].push_back(flat.size());
+        for (int k = 0; k <= nkeys; ++k) wave_off[g].push_back(bucket[static_cast<size_t>(g) * nkeys + std::min(k, nkeys)]);
+        for (int k = 0; k < nkeys; ++k) max_wave = std::max(max_wave, wave_off[g][k + 1] - wave_off[g][k]);
     }
+    Job* flat = static_cast<Job*>(ctx->h_stage.get(sizeof(Job) * total_jobs));
+    {
+        std::vector<size_t> fill(bucket.begin(), bucket.end() - 1);
+        for (int r = 0; r < n_real; ++r) {  // realization order within each wave
+            const int g = static_cast<int>(static_cast<int64_t>(r) * G / n_real);
+            const std::vector<Job>& jv = rjobs[r];
+            for (size_t k = 0; k < jv.size(); ++k) flat[fill[static_cast<size_t>(g) * nkeys + rkeys[r][k]]++] = jv[k];
+        }
+    }
+    const double host_prep_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
 
     // ---- exactness guard for the fp32 screen
     const double maxw = ti->mode == 0 ? B : static_cast<double>(ti->F - 1) * B;
@@ -1269,8 +1321,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         throw Fail(CCW_ERR_CONFIG, "configuration exceeds the exact fp32 screen range (mask*B^2 >= 2^24)");
 
     // ---- device buffers
-    Job* d_jobs = ctx->jobs.as<Job>(flat.size());
-    CCW_CUDA(cudaMemcpyAsync(d_jobs, flat.data(), sizeof(Job) * flat.size(), cudaMemcpyHostToDevice, st));
+    Job* d_jobs = ctx->jobs.as<Job>(total_jobs);
+    CCW_CUDA(cudaMemcpyAsync(d_jobs, flat, sizeof(Job) * total_jobs, cudaMemcpyHostToDevice, st));
     const size_t plane = static_cast<size_t>(wh) * ww;
     uint8_t* d_work = ctx->work.as<uint8_t>(plane * n_real);
     CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
@@ -1289,8 +1341,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     int32_t* d_scores = ctx->scores.as<int32_t>(G * maxj * sld);
     int32_t* d_wts = ctx->wts.as<int32_t>(G * maxj * std::max(ti->nscr, 1) * Tc * Tc);
     double* d_tm = ctx->tm64.as<double>(G * maxj * ti->nch * Tc * Tc);
-    int32_t* d_chosen = ctx->chosen.as<int32_t>(2 * flat.size());
-    uint8_t* d_pasted = traces ? ctx->pasted.as<uint8_t>(flat.size() * T * T) : nullptr;
+    int32_t* d_chosen = ctx->chosen.as<int32_t>(2 * total_jobs);
+    uint8_t* d_pasted = traces ? ctx->pasted.as<uint8_t>(total_jobs * T * T) : nullptr;
     int* d_mism = ctx->mism.as<int>(n_real);
     CCW_CUDA(cudaMemsetAsync(d_mism, 0, sizeof(int) * n_real, st));
 
@@ -1493,10 +1545,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     std::vector<int32_t> chosen;
     std::vector<uint8_t> pasted;
     if (traces) {
-        chosen.resize(2 * flat.size());
+        chosen.resize(2 * total_jobs);
         CCW_CUDA(cudaMemcpyAsync(chosen.data(), d_chosen, sizeof(int32_t) * chosen.size(),
                                  cudaMemcpyDeviceToHost, st));
-        pasted.resize(flat.size() * T * T);
+        pasted.resize(total_jobs * T * T);
         CCW_CUDA(cudaMemcpyAsync(pasted.data(), d_pasted, pasted.size(), cudaMemcpyDeviceToHost, st));
     }
     CCW_CUDA(cudaStreamSynchronize(st));
@@ -1514,7 +1566,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.ccf_flop_ref = ccf_flop_ref;
     ctx->timing.waves = static_cast<int64_t>(max_key + 1);
     ctx->timing.groups = G;
-    ctx->timing.jobs = static_cast<int64_t>(flat.size());
+    ctx->timing.host_prep_ms = host_prep_ms;
+    ctx->timing.jobs = static_cast<int64_t>(total_jobs);
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu\n",
@@ -1547,7 +1600,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     if (traces) {
         // flat is wave-ordered; rebuild each realization's raster-ordered trace
-        for (size_t g = 0; g < flat.size(); ++g) {
+        for (size_t g = 0; g < total_jobs; ++g) {
             const Job& jb = flat[g];
             ccw_trace& tr = traces[jb.real];
             if (jb.place >= tr.capacity) continue;
