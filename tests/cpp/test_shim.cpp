@@ -75,7 +75,8 @@ static void test_wavelet() {
     for (double v : c.approx.values()) CHECK(std::abs(v - 6.5) < 1e-12);
     CHECK_THROWS_AS(dwt2_single(RealPlane(3, 4)), DimensionError);
     CHECK_THROWS_AS(dwt2(RealPlane(12, 16), 3), DimensionError);
-    for (double v : dwt2(RealPlane(8, 8, 1.5), 3).apex.values()) CHECK(std::abs(v - 12.0) < 1e-12);
+    const WaveletPyramid cp = dwt2(RealPlane(8, 8, 1.5), 3);
+    for (double v : cp.apex.values()) CHECK(std::abs(v - 12.0) < 1e-12);
     // bit-exact vs the oracle + perfect reconstruction (test_wavelet.cpp:191-204)
     std::mt19937_64 rng(25);
     for (int trial = 0; trial < 30; ++trial) {
@@ -205,7 +206,8 @@ static void test_simulator() {
     // constant TI -> constant realization; same seed identical (test_simulator.cpp:401-421)
     cfg = base_config();
     cfg.sg_height = cfg.sg_width = 48;
-    for (int v : simulate_one(CategoricalGrid(32, 32, 2, 1), cfg, 999).realization.cells()) CHECK(v == 1);
+    const SimResult cres = simulate_one(CategoricalGrid(32, 32, 2, 1), cfg, 999);
+    for (int v : cres.realization.cells()) CHECK(v == 1);
     std::mt19937_64 rng(3);
     const CategoricalGrid ti = random_grid(64, 64, 3, rng);
     CHECK(simulate_one(ti, base_config(), 31337).realization == simulate_one(ti, base_config(), 31337).realization);
