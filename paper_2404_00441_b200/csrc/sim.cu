@@ -751,54 +751,81 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // run's sum, one lane per window folds the run sums in row-major order --
 // the reference's operations in the reference's order) and merge them into
 // the running top-K by the reference ranking.
+template <int NWJ>
+__device__ __forceinline__ void job_sync() {
+    if constexpr (NWJ == 1)
+        job_sync<NWJ>();
+    else
+        __syncthreads();
+}
+
+// NWJ warps serve one job: control flow is replicated in every warp (same
+// data, same decisions, only warp 0 writes shared state), the parallel loops
+// run over all 32*NWJ threads.
+template <int NWJ>
 __device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm, int R,
                                            WarpSel& W, int& cnt, int& ntop, int K, int lane,
                                            unsigned long long* tacc) {
+    constexpr int JT = 32 * NWJ;
+    const int jt = NWJ == 1 ? lane : static_cast<int>(threadIdx.x);
+    const bool writer = NWJ == 1 || threadIdx.x < 32;
     const long long c0 = clock64();
-    if (P.stats && lane == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+    if (P.stats && jt == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
     const int rows = R / P.nch;
     const int EB = max(1, WS_RS / R);
     for (int e0 = 0; e0 < cnt; e0 += EB) {
         const int ng = min(EB, cnt - e0);
         // run sums: sum += ti*or left to right (matcher.hpp:72-76)
-        int e = 0, r = lane;
+        int e = 0, r = jt;
         while (r >= R) {
             r -= R;
             ++e;
         }
-        for (int w = lane; w < ng * R; w += 32) {
+        for (int w = jt; w < ng * R; w += JT) {
             const int pos = W.cidx[e0 + e];
             const int x = pos / P.out_w, y = pos - x * P.out_w;
             const int ch = r / rows;
             const short4 rw = W.rows[r - ch * rows];
             const double* a = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
-                              static_cast<size_t>(x + rw.x) * P.wc + y;
-            const double* b = tm + (ch * P.Tc + rw.x) * P.Tc;
+                              static_cast<size_t>(x + rw.x) * P.wc + y + rw.y;
+            const double* b = tm + (ch * P.Tc + rw.x) * P.Tc + rw.y;
+            const int len = rw.z - rw.y;
             double sum = 0.0;
-#pragma unroll 8
-            for (int t = rw.y; t < rw.z; ++t) sum = __dadd_rn(sum, __dmul_rn(__ldg(a + t), __ldg(b + t)));
+            for (int t0 = 0; t0 < len; t0 += 16) {
+                // all operands of (up to) 16 cells in flight at once, then the
+                // reference's sequential chain
+                double av[16], bv[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    av[i] = t0 + i < len ? __ldg(a + t0 + i) : 0.0;
+                    bv[i] = t0 + i < len ? __ldg(b + t0 + i) : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (t0 + i < len) sum = __dadd_rn(sum, __dmul_rn(av[i], bv[i]));
+            }
             W.rsum[w] = sum;
-            r += 32;
+            r += JT;
             while (r >= R) {
                 r -= R;
                 ++e;
             }
         }
-        __syncwarp();
+        job_sync<NWJ>();
         // fold: acc += sum over runs in row-major order (matcher.hpp:77, 160-161)
-        for (int e = lane; e < ng; e += 32) {
+        for (int e = jt; e < ng; e += JT) {
             double acc = 0.0;
             for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, W.rsum[e * R + r]);
             W.ckey[e0 + e] = acc;
         }
-        __syncwarp();
+        job_sync<NWJ>();
     }
     const long long c1 = clock64();
-    for (int e = lane; e < ntop; e += 32) {
+    for (int e = jt; e < ntop; e += JT) {
         W.ckey[cnt + e] = W.tkey[e];
         W.cidx[cnt + e] = W.tidx[e];
     }
-    __syncwarp();
+    job_sync<NWJ>();
     const int n = cnt + ntop;
     const int keep = min(K, n);
     if (n <= 32) {
@@ -811,8 +838,8 @@ __device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm,
             const int oi = __shfl_sync(0xffffffffu, mi, j);
             rank += better(ok, oi, mk, mi);
         }
-        __syncwarp();
-        if (lane < n && rank < keep) {
+        job_sync<NWJ>();
+        if (writer && lane < n && rank < keep) {
             W.tkey[rank] = mk;
             W.tidx[rank] = mi;
         }
@@ -838,31 +865,36 @@ __device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm,
                     bp = op;
                 }
             }
-            if (lane == 0) {
+            job_sync<NWJ>();  // every warp has read this round's entries
+            if (writer && lane == 0) {
                 W.tkey[round] = bk;
                 W.tidx[round] = bi;
                 W.cidx[bp] = -1;
             }
-            __syncwarp();
+            job_sync<NWJ>();
         }
     }
     ntop = keep;
     cnt = 0;
-    __syncwarp();
-    if (tacc && lane == 0) {
+    job_sync<NWJ>();
+    if (tacc && jt == 0) {
         atomicAdd(&tacc[0], static_cast<unsigned long long>(c1 - c0));
         atomicAdd(&tacc[1], static_cast<unsigned long long>(clock64() - c1));
     }
 }
 
-__global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
-    SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
+template <int NWJ>
+__global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
+    select_paste_warp_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
     extern __shared__ __align__(16) unsigned char ws_raw[];
     WarpSel* smem_ws = reinterpret_cast<WarpSel*>(ws_raw);
+    constexpr int JT = 32 * NWJ;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = blockIdx.x * WS_WARPS + wid;
+    const int jt = NWJ == 1 ? lane : static_cast<int>(threadIdx.x);
+    const bool writer = NWJ == 1 || wid == 0;
+    const int slot = NWJ == 1 ? blockIdx.x * WS_WARPS + wid : blockIdx.x;
     if (slot >= nj) return;
-    WarpSel& W = smem_ws[wid];
+    WarpSel& W = smem_ws[NWJ == 1 ? wid : 0];
     const int gj = job0 + slot;
     const Job jb = jobs[gj];
     const int Tc = P.Tc;
@@ -882,15 +914,15 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
 #pragma unroll
         for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
         const int nv = P.ntiles * kTcQ;
-        for (int e0 = 0; e0 < nv; e0 += 32 * 8) {
-            int vb[8];
+        for (int e0 = 0; e0 < nv; e0 += 32 * 24) {
+            int vb[24];  // the job's summaries in one round trip (<= 768 per batch)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 24; ++i) {
                 const int e = e0 + i * 32 + lane;
                 vb[i] = e < nv ? tsum[e].x : INT_MIN;
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 24; ++i) {
                 int v = vb[i];
                 if (v > top[kTcQ - 1]) {
 #pragma unroll
@@ -923,7 +955,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
                 break;
             }
         }
-        if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+        if (P.stats && jt == 0) atomicAdd(&P.stats[1], 1ull);
         clk1 = clock64();
         int R = 0;
         for (int s0 = 0; s0 < Tc; s0 += 32) {
@@ -931,10 +963,10 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
             int t0 = 0, t1 = 0;
             if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
             const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
-            if (t1 > t0) W.rows[R + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
+            if (writer && t1 > t0) W.rows[R + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
             R += __popc(m);
         }
-        __syncwarp();
+        job_sync<NWJ>();
         R *= P.nch;
         // 2. gather every window at or above the threshold, row-major.  Tile
         //    heads are tested 32 at a time; a qualifying tile is read with one
@@ -953,16 +985,16 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
                     const int2 cv = lane < P.qdepth ? tl[lane] : make_int2(INT_MIN, 0);
                     const bool q = cv.x >= thr;
                     const unsigned bal = __ballot_sync(0xffffffffu, q);
-                    if (cnt + 32 > WS_CB) warp_flush(P, tm, R, W, cnt, ntop, K, lane, tacc);
-                    if (q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = cv.y;
+                    if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
+                    if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = cv.y;
                     cnt += __popc(bal);
-                    __syncwarp();
+                    job_sync<NWJ>();
                     continue;
                 }
                 const int p0 = t * kTcTile + lane * 4;  // kTcTile = 128 = 32 lanes x 4
                 int v[4];
                 const int32_t* src_sc = P.scores ? sc : P.ovf + static_cast<size_t>(slot) * P.sld;
-                if (!P.scores && P.stats && lane == 0) atomicAdd(&P.stats[2], 1ull);
+                if (!P.scores && P.stats && jt == 0) atomicAdd(&P.stats[2], 1ull);
                 if (p0 + 4 <= P.npos) {
                     const int4 a = *reinterpret_cast<const int4*>(src_sc + p0);
                     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
@@ -976,14 +1008,14 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
                     const bool q = v[i] >= thr;
                     const unsigned bal = __ballot_sync(0xffffffffu, q);
                     if (!bal) continue;
-                    if (cnt + 32 > WS_CB) warp_flush(P, tm, R, W, cnt, ntop, K, lane, tacc);
-                    if (q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = p0 + i;
+                    if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
+                    if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = p0 + i;
                     cnt += __popc(bal);
-                    __syncwarp();
+                    job_sync<NWJ>();
                 }
             }
         }
-        if (cnt > 0) warp_flush(P, tm, R, W, cnt, ntop, K, lane, tacc);
+        if (cnt > 0) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
         clk2 = clock64();
         // 3. choose (matcher.hpp:207-241)
         int pick = jb.pick;
@@ -1021,21 +1053,21 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
     uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
     uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
     const int wpr = T >> 2;  // 32-bit words per row
-    const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= 32 && (32 % wpr) == 0;
+    const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= JT && (JT % wpr) == 0;
     if (vec4) {
-        // lane -> (row phase, word); 8 independent loads in flight per lane
-        const int rpi = 32 / wpr, rsub = lane / wpr, cw = lane - rsub * wpr;
+        // thread -> (row phase, word); every row it copies loaded in one round trip
+        const int rpi = JT / wpr, rsub = jt / wpr, cw = jt - rsub * wpr;
         const uint8_t* srcp = P.ti + static_cast<size_t>(fr) * P.ti_w + fc + 4 * cw;
         uint8_t* dstp = g + static_cast<size_t>(jb.top) * P.ww + jb.left + 4 * cw;
-        for (int r0 = rsub; r0 < T; r0 += rpi * 8) {
-            uint32_t v[8];
+        for (int r0 = rsub; r0 < T; r0 += rpi * 32) {
+            uint32_t v[32];  // every row this lane copies, loaded in one round trip
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 32; ++i) {
                 const int r = r0 + i * rpi;
                 if (r < T) v[i] = *reinterpret_cast<const uint32_t*>(srcp + static_cast<size_t>(r) * P.ti_w);
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 32; ++i) {
                 const int r = r0 + i * rpi;
                 if (r < T) {
                     *reinterpret_cast<uint32_t*>(dstp + static_cast<size_t>(r) * P.ww) = v[i];
@@ -1045,7 +1077,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
         }
     } else {
         for (int r = 0; r < T; ++r)
-            for (int c = lane; c < T; c += 32) {
+            for (int c = jt; c < T; c += JT) {
                 const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
                 g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
                 if (trace) trace[r * T + c] = v;
@@ -1056,9 +1088,9 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 4) select_paste_warp_kernel(
                       static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
         const int s0 = (fr / P.B) * P.wc + fc / P.B;
         for (int a = 0; a < Tc; ++a)
-            for (int b = lane; b < Tc; b += 32) sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
+            for (int b = jt; b < Tc; b += JT) sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
     }
-    if (lane == 0) {
+    if (jt == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
         if (tacc && clk1) {
@@ -1432,7 +1464,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   static_cast<int>(ccf_smem)));
     CCW_CUDA(cudaFuncSetAttribute(select_paste_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sel_smem)));
-    CCW_CUDA(cudaFuncSetAttribute(select_paste_warp_kernel,
+    int selw = 2;  // warps per placement in the select kernel (measured best, r1)
+    if (const char* e = getenv("CCW_SELW")) selw = atoi(e) <= 1 ? 1 : (atoi(e) == 2 ? 2 : 4);
+    CCW_CUDA(cudaFuncSetAttribute(select_paste_warp_kernel<1>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(WarpSel) * WS_WARPS)));
 
@@ -1502,10 +1536,18 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     b = tm.get();
                     CCW_CUDA(cudaEventRecord(a, gs));
                 }
-                if (warp_select || (first_wave && !cfg.min_cut))
-                    select_paste_warp_kernel<<<(nj + WS_WARPS - 1) / WS_WARPS, WS_WARPS * 32,
-                                               sizeof(WarpSel) * WS_WARPS, gs>>>(
-                        Q, d_jobs, static_cast<int>(j0), nj);
+                if (warp_select || (first_wave && !cfg.min_cut)) {
+                    if (selw == 1)
+                        select_paste_warp_kernel<1><<<(nj + WS_WARPS - 1) / WS_WARPS, WS_WARPS * 32,
+                                                      sizeof(WarpSel) * WS_WARPS, gs>>>(
+                            Q, d_jobs, static_cast<int>(j0), nj);
+                    else if (selw == 2)
+                        select_paste_warp_kernel<2><<<nj, 64, sizeof(WarpSel), gs>>>(
+                            Q, d_jobs, static_cast<int>(j0), nj);
+                    else
+                        select_paste_warp_kernel<4><<<nj, 128, sizeof(WarpSel), gs>>>(
+                            Q, d_jobs, static_cast<int>(j0), nj);
+                }
                 else
                     select_paste_kernel<<<nj, SEL_T, sel_smem, gs>>>(Q, d_jobs, static_cast<int>(j0),
                                                                      use_screen ? 1 : 0);
