@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mt = (a.nj + kM - 1) / kM, n_nt = (a.npos + kN - 1) / kN;
+    pdl_trigger();
     const int ntot = n_mt * n_nt;
 
     if (warp == 0 && lane == 0) {
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // the weights (or_prep) and the previous wave's outputs are complete
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer: K stages of every tile, one ring
@@ -527,11 +529,11 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
     dim3 grid(std::min(ntot, tc_num_sms()));
     if (pl.q == 4)
-        ccf_tc_kernel<4><<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(pl.ma, pl.mb, a);
+        launch_pdl(ccf_tc_kernel<4>, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
     else if (pl.q == 6)
-        ccf_tc_kernel<6><<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(pl.ma, pl.mb, a);
+        launch_pdl(ccf_tc_kernel<6>, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
     else
-        ccf_tc_kernel<8><<<grid, kThreads, ccf_tc_smem_bytes(), st>>>(pl.ma, pl.mb, a);
+        launch_pdl(ccf_tc_kernel<8>, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
 }
 
 // summary depth: K plus headroom (keeps tie overflow rare), from {4, 6, 8}

@@ -139,6 +139,13 @@ __device__ __forceinline__ int block_stat(const uint8_t* cells, int ld, int B, i
     return acc;
 }
 
+// Programmatic dependent launch (PDL): a kernel lets its stream successor
+// start launching early, and waits for its predecessor's completion (and
+// memory) before reading what the predecessor wrote.  Both are no-ops for a
+// kernel launched without the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Block-wide reductions for blockDim.x a multiple of 32 (<= 1024).
 template <typename T, typename Op>
 __device__ __forceinline__ T block_reduce(T v, Op op, T* red) {

@@ -8,6 +8,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/ccwgpu.h"
@@ -27,6 +28,25 @@ struct Fail : std::runtime_error {
             throw ::ccwgpu::Fail(CCW_ERR_CUDA, std::string(#expr) + ": " +                 \
                                                    cudaGetErrorString(e_));                \
     } while (0)
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its stream predecessor drains; it must pdl_wait() before reading the
+// predecessor's output.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CCW_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // Grow-only device buffer owned by a context.
 struct DevBuf {

@@ -75,8 +75,10 @@ void build_pyramid(ccw_ti* ti, cudaStream_t s) {
 // counts and reference-order apex values are gathers from the TI pyramid at
 // the recorded source block -- identical values, no recomputation.
 __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    pdl_trigger();
     const int slot = blockIdx.x;
     const Job jb = jobs[job0 + slot];
+    pdl_wait();
     const int Tc = P.Tc, B = P.B, nc = P.hc * P.wc;
     const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc;
     int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
@@ -105,8 +107,10 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
 }
 
 __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    pdl_trigger();
     const int slot = blockIdx.x;
     const Job jb = jobs[job0 + slot];
+    pdl_wait();
     const int Tc = P.Tc, B = P.B;
     const uint8_t* grid = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
     int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
@@ -184,8 +188,10 @@ __global__ void __launch_bounds__(CCF_THREADS) ccf_direct_kernel(SimParams P,
                                                                  const Job* __restrict__ jobs,
                                                                  int job0) {
     extern __shared__ __align__(16) float ccf_sm[];
+    pdl_trigger();
     const int slot = blockIdx.z;
     const Job jb = jobs[job0 + slot];
+    pdl_wait();
     const int Tc = P.Tc, hc = P.hc, wc = P.wc, nscr = P.nscr;
     const int SH = CCF_TX + Tc - 1, SW = ccf_sw(Tc), WP = ccf_wp(Tc);
     float* tile = ccf_sm;
@@ -564,9 +570,11 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
     int* dp = reinterpret_cast<int*>(sel_sm + L.dp);
     int* seam = reinterpret_cast<int*>(sel_sm + L.seam);
 
+    pdl_trigger();
     const int gj = job0 + blockIdx.x;
     const Job jb = jobs[gj];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_wait();
     int fr, fc;
     if (jb.shape == kNone) {
         fr = jb.fr;
@@ -893,6 +901,8 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
     const int jt = NWJ == 1 ? lane : static_cast<int>(threadIdx.x);
     const bool writer = NWJ == 1 || wid == 0;
     const int slot = NWJ == 1 ? blockIdx.x * WS_WARPS + wid : blockIdx.x;
+    pdl_trigger();
+    pdl_wait();
     if (slot >= nj) return;
     WarpSel& W = smem_ws[NWJ == 1 ? wid : 0];
     const int gj = job0 + slot;
@@ -1115,6 +1125,7 @@ __global__ void hd_scatter_kernel(const int32_t* __restrict__ hd, int n_hd, uint
 __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww,
                                 const uint8_t* __restrict__ hd, int sg_h, int sg_w,
                                 uint8_t* __restrict__ out, int* mism) {
+    pdl_wait();
     const size_t n = static_cast<size_t>(sg_h) * sg_w;
     const int r = blockIdx.y;
     const uint8_t* g = work + static_cast<size_t>(r) * wh * ww;
@@ -1496,9 +1507,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 const bool first_wave = flat[j0].shape == kNone;
                 if (!first_wave) {
                     if (d_src)
-                        or_prep_src_kernel<<<nj, 128, 0, gs>>>(Q, d_jobs, static_cast<int>(j0));
+                        launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
+                                   static_cast<const Job*>(d_jobs), static_cast<int>(j0));
                     else
-                        or_prep_kernel<<<nj, 128, 0, gs>>>(Q, d_jobs, static_cast<int>(j0));
+                        launch_pdl(or_prep_kernel, dim3(nj), dim3(128), 0, gs, Q,
+                                   static_cast<const Job*>(d_jobs), static_cast<int>(j0));
                     ++launches;
                     if (use_screen) {
                         cudaEvent_t a = nullptr, b = nullptr;
@@ -1511,9 +1524,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                             launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.ovf,
                                           Q.summary, gs);
                         } else {
-                            dim3 grid(ccf_grid_xy.x, ccf_grid_xy.y, nj);
-                            ccf_direct_kernel<<<grid, CCF_THREADS, ccf_smem, gs>>>(
-                                Q, d_jobs, static_cast<int>(j0));
+                            launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, ccf_grid_xy.y, nj),
+                                       dim3(CCF_THREADS), ccf_smem, gs, Q,
+                                       static_cast<const Job*>(d_jobs), static_cast<int>(j0));
                         }
                         ++launches;
                         ++ccf_launches;
@@ -1537,20 +1550,22 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     CCW_CUDA(cudaEventRecord(a, gs));
                 }
                 if (warp_select || (first_wave && !cfg.min_cut)) {
+                    const Job* dj = d_jobs;
                     if (selw == 1)
-                        select_paste_warp_kernel<1><<<(nj + WS_WARPS - 1) / WS_WARPS, WS_WARPS * 32,
-                                                      sizeof(WarpSel) * WS_WARPS, gs>>>(
-                            Q, d_jobs, static_cast<int>(j0), nj);
+                        launch_pdl(select_paste_warp_kernel<1>, dim3((nj + WS_WARPS - 1) / WS_WARPS),
+                                   dim3(WS_WARPS * 32), sizeof(WarpSel) * WS_WARPS, gs, Q, dj,
+                                   static_cast<int>(j0), nj);
                     else if (selw == 2)
-                        select_paste_warp_kernel<2><<<nj, 64, sizeof(WarpSel), gs>>>(
-                            Q, d_jobs, static_cast<int>(j0), nj);
+                        launch_pdl(select_paste_warp_kernel<2>, dim3(nj), dim3(64), sizeof(WarpSel), gs,
+                                   Q, dj, static_cast<int>(j0), nj);
                     else
-                        select_paste_warp_kernel<4><<<nj, 128, sizeof(WarpSel), gs>>>(
-                            Q, d_jobs, static_cast<int>(j0), nj);
+                        launch_pdl(select_paste_warp_kernel<4>, dim3(nj), dim3(128), sizeof(WarpSel), gs,
+                                   Q, dj, static_cast<int>(j0), nj);
                 }
                 else
-                    select_paste_kernel<<<nj, SEL_T, sel_smem, gs>>>(Q, d_jobs, static_cast<int>(j0),
-                                                                     use_screen ? 1 : 0);
+                    launch_pdl(select_paste_kernel, dim3(nj), dim3(SEL_T), sel_smem, gs, Q,
+                               static_cast<const Job*>(d_jobs), static_cast<int>(j0),
+                               use_screen ? 1 : 0);
                 ++launches;
                 if (ctx->profiling) {
                     CCW_CUDA(cudaEventRecord(b, gs));
