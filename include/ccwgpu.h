@@ -116,6 +116,7 @@ typedef struct ccw_timing {
     int64_t groups;         /* realization groups run concurrently on separate streams */
     int64_t recomputed_tiles; /* summary tiles re-scored because ties overflowed the list */
     double host_prep_ms;    /* host schedule build (plans + mt19937_64 draws) before launch */
+    int64_t bulk_jobs;      /* placements whose tie group went to the bulk (CTA-wide) rescoring */
 } ccw_timing;
 
 typedef struct ccw_ctx ccw_ctx;

@@ -43,7 +43,8 @@ class TimingC(C.Structure):
                 ("ccf_flop_ref", C.c_double), ("waves", C.c_int64), ("jobs", C.c_int64),
                 ("rescored", C.c_int64), ("screened_jobs", C.c_int64), ("ccf_variant", C.c_int64),
                 ("ccf_mma_flop", C.c_double), ("groups", C.c_int64),
-                ("recomputed_tiles", C.c_int64), ("host_prep_ms", C.c_double)]
+                ("recomputed_tiles", C.c_int64), ("host_prep_ms", C.c_double),
+                ("bulk_jobs", C.c_int64)]
 
 
 P = C.c_void_p

@@ -29,6 +29,7 @@ struct TcArgs {
 size_t ccf_tc_smem_bytes();
 int tc_kpad(int nscr, int Tc);
 int tc_tiles(int npos);
+int tc_num_sms();
 int tc_qdepth(int K);
 // im2col of the TI screen planes for template size Tc (cached on the TI).
 const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st);

@@ -50,6 +50,9 @@ struct SimParams {
     uint8_t* work;           // n_real planes of wh*ww
     int wh, ww;
     const uint8_t* hd;       // wh*ww plane, kNoDatum = none; may be null
+    const int32_t* hd_off;   // per stride-lattice cell: CSR offsets into hd_ent (null without hard data)
+    const uint32_t* hd_ent;  // (footprint cell r*T+c) << 8 | facies
+    int lat_nlc, stride;     // lattice columns, placement stride T - OV
     int32_t* src;            // n_real planes of (wh/B)*(ww/B): TI coarse index each work block
                              // was pasted from (null with min-cut, whose blocks mix sources)
     int swc;                 // ww / B
@@ -66,6 +69,12 @@ struct SimParams {
     int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
     int32_t* ovf;            // same layout, only tie-overflowing tiles written (warp path)
     int sld;
+    int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
+    int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
+    int bulk_min;            // estimated tie-group size above which a placement is deferred
+    int* bulk_sync;          // per job slot: [next position block, finished CTAs]
+    double* bulk_keys;       // per job slot x CTA: that CTA's top-K keys
+    int* bulk_idx;           //   ... and positions
     // outputs
     int32_t* chosen;         // per job (global job id): fr, fc
     uint8_t* pasted;         // optional trace of pasted patches (global job id * T*T)

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <map>
+#include <tuple>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -104,7 +105,7 @@ struct ccw_ctx {
     int ccf_variant = 0;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
     std::vector<cudaEvent_t> ev_pool;
@@ -120,6 +121,9 @@ struct ccw_ti {
     double* d_ti64 = nullptr;    // nch*hc*wc
     float* d_scr = nullptr;      // nscr*hc*wc
     std::map<int, int8_t*> im2col;  // per template size Tc: npos x kpad int8 (tcgen05 screen)
+    // launch plan memory: geometries whose last call deferred no placement to
+    // the bulk tie select skip its per-wave launch (re-enabled on demand)
+    std::map<std::tuple<int, int, int, int>, bool> bulk_off;
 };
 
 namespace ccwgpu {

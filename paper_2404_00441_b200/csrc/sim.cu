@@ -654,15 +654,16 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         if (pick < 0) {
             int best = 0, best_mis = INT_MAX;
             pick = -1;
+            const int cell = (jb.top / P.stride) * P.lat_nlc + jb.left / P.stride;
+            const int e0 = P.hd_off[cell], e1 = P.hd_off[cell + 1];
             for (int c = 0; c < ntop; ++c) {
                 const int pos = tidx[c];
                 const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
                 int mis = 0;
-                for (int e = tid; e < P.T * P.T; e += SEL_T) {
-                    const int r = e / P.T, cc = e - r * P.T;
-                    const uint8_t hv = P.hd[static_cast<size_t>(jb.top + r) * P.ww + jb.left + cc];
-                    if (hv != kNoDatum && P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != hv)
-                        ++mis;
+                for (int e = e0 + tid; e < e1; e += SEL_T) {
+                    const uint32_t u = P.hd_ent[e];
+                    const int rc = static_cast<int>(u >> 8), r = rc / P.T, cc = rc - r * P.T;
+                    mis += P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != (u & 255u);
                 }
                 mis = block_reduce(mis, [](int a, int b) { return a + b; }, redi);
                 if (mis == 0) {
@@ -734,8 +735,6 @@ constexpr int WS_RS = 256;    // (window, run) partial sums per rescoring batch
 
 constexpr int WS_MAXTC = 64;   // template rows tabulated per warp
 
-constexpr int WS_PB = 2048;  // staged fp64 TI values (windows x mask cells) per batch
-
 struct WarpSel {
     short4 rows[WS_MAXTC];  // (s, t0, t1, cell offset) of the mask rows, row-major
     int cidx[WS_CB + kTcQ];
@@ -762,7 +761,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 template <int NWJ>
 __device__ __forceinline__ void job_sync() {
     if constexpr (NWJ == 1)
-        job_sync<NWJ>();
+        __syncwarp();
     else
         __syncthreads();
 }
@@ -891,6 +890,104 @@ __device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm,
     }
 }
 
+// Conditional / unconditional choice among the ranked top-K (matcher.hpp:207-241):
+// the host-drawn index, or the first zero-mismatch candidate against the hard
+// data, else the fewest mismatches.  Warp-level; every warp of a job may run
+// it redundantly (identical inputs, identical result).
+__device__ __forceinline__ int choose_pick(const SimParams& P, const Job& jb, const int* tidx, int ntop,
+                                        int lane) {
+    int pick = jb.pick;
+    if (pick < 0) {
+        int best = 0, best_mis = INT_MAX;
+        const int cell = (jb.top / P.stride) * P.lat_nlc + jb.left / P.stride;
+        const int e0 = P.hd_off[cell], e1 = P.hd_off[cell + 1];
+        for (int c = 0; c < ntop; ++c) {
+            const int pos = tidx[c];
+            const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
+            int mis = 0;
+            for (int e = e0 + lane; e < e1; e += 32) {
+                const uint32_t u = P.hd_ent[e];
+                const int rc = static_cast<int>(u >> 8), r = rc / P.T, cc = rc - r * P.T;
+                mis += P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != (u & 255u);
+            }
+            for (int o = 16; o > 0; o >>= 1) mis += __shfl_xor_sync(0xffffffffu, mis, o);
+            if (mis == 0) {
+                pick = c;
+                break;
+            }
+            if (mis < best_mis) {
+                best = c;
+                best_mis = mis;
+            }
+        }
+        if (pick < 0) pick = best;
+    }
+    return tidx[pick];
+}
+
+// Paste the chosen TI crop (simulator.hpp:483-493), record the trace and the
+// source-block map; JT threads cooperate (jt = 0..JT-1).
+template <int JT>
+__device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int gj, int fr, int fc,
+                                          int jt) {
+    const int Tc = P.Tc;
+    const int T = P.T;
+    uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
+    uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
+    const int wpr = T >> 2;  // 32-bit words per row
+    const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= JT && (JT % wpr) == 0;
+    if (vec4) {
+        // thread -> (row phase, word); every row it copies loaded in one round trip
+        const int rpi = JT / wpr, rsub = jt / wpr, cw = jt - rsub * wpr;
+        const uint8_t* srcp = P.ti + static_cast<size_t>(fr) * P.ti_w + fc + 4 * cw;
+        uint8_t* dstp = g + static_cast<size_t>(jb.top) * P.ww + jb.left + 4 * cw;
+        for (int r0 = rsub; r0 < T; r0 += rpi * 32) {
+            uint32_t v[32];  // every row this lane copies, loaded in one round trip
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int r = r0 + i * rpi;
+                if (r < T) v[i] = *reinterpret_cast<const uint32_t*>(srcp + static_cast<size_t>(r) * P.ti_w);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int r = r0 + i * rpi;
+                if (r < T) {
+                    *reinterpret_cast<uint32_t*>(dstp + static_cast<size_t>(r) * P.ww) = v[i];
+                    if (trace) *reinterpret_cast<uint32_t*>(trace + r * T + 4 * cw) = v[i];
+                }
+            }
+        }
+    } else {
+        // unaligned rows: byte copies, 16 loads in flight per thread
+        constexpr int BB = 16;
+        for (int e0 = 0; e0 < T * T; e0 += JT * BB) {
+            uint8_t v[BB];
+#pragma unroll
+            for (int i = 0; i < BB; ++i) {
+                const int e = e0 + i * JT + jt;
+                const int r = e / T, c = e - r * T;
+                if (e < T * T) v[i] = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+            }
+#pragma unroll
+            for (int i = 0; i < BB; ++i) {
+                const int e = e0 + i * JT + jt;
+                const int r = e / T, c = e - r * T;
+                if (e < T * T) {
+                    g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v[i];
+                    if (trace) trace[e] = v[i];
+                }
+            }
+        }
+    }
+    if (P.src) {
+        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc +
+                      static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
+        const int s0 = (fr / P.B) * P.wc + fc / P.B;
+        for (int a = 0; a < Tc; ++a)
+            for (int b = jt; b < Tc; b += JT) sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
+    }
+}
+
 template <int NWJ>
 __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
     select_paste_warp_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
@@ -978,6 +1075,28 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
         }
         job_sync<NWJ>();
         R *= P.nch;
+        if (P.bulk_min > 0) {
+            // Large tie groups (binary TIs, small K) would take many small
+            // flushes here; hand them to select_bulk_kernel, which rescores
+            // thread-per-window out of shared-memory TI tiles.
+            int est = 0;
+            for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
+                const int tt = t0 + lane;
+                if (tt < P.ntiles && tsum[static_cast<size_t>(tt) * kTcQ].x >= thr) {
+                    int c = 0;
+                    for (int i = 0; i < P.qdepth; ++i) c += tsum[static_cast<size_t>(tt) * kTcQ + i].x >= thr;
+                    est += c == P.qdepth ? 32 : c;  // a saturated list hides more ties
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) est += __shfl_xor_sync(0xffffffffu, est, o);
+            const bool big = est > P.bulk_min;
+            if (P.defer) {
+                if (jt == 0) P.defer[slot] = big ? thr : INT_MIN;
+                if (big) return;  // uniform across the job's warps
+            } else if (big && P.stats && jt == 0) {
+                atomicAdd(&P.stats[4], 1ull);  // would have deferred: re-enable the bulk launches
+            }
+        }
         // 2. gather every window at or above the threshold, row-major.  Tile
         //    heads are tested 32 at a time; a qualifying tile is read with one
         //    vector load per lane (8 consecutive scores).
@@ -1028,78 +1147,13 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
         if (cnt > 0) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
         clk2 = clock64();
         // 3. choose (matcher.hpp:207-241)
-        int pick = jb.pick;
-        if (pick < 0) {
-            int best = 0, best_mis = INT_MAX;
-            for (int c = 0; c < ntop; ++c) {
-                const int pos = W.tidx[c];
-                const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
-                int mis = 0;
-                for (int r = 0; r < P.T; ++r)
-                    for (int cc = lane; cc < P.T; cc += 32) {
-                        const uint8_t hv = P.hd[static_cast<size_t>(jb.top + r) * P.ww + jb.left + cc];
-                        if (hv != kNoDatum && P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != hv)
-                            ++mis;
-                    }
-                for (int o = 16; o > 0; o >>= 1) mis += __shfl_xor_sync(0xffffffffu, mis, o);
-                if (mis == 0) {
-                    pick = c;
-                    break;
-                }
-                if (mis < best_mis) {
-                    best = c;
-                    best_mis = mis;
-                }
-            }
-            if (pick < 0) pick = best;
-        }
-        const int pos = W.tidx[pick];
+        const int pos = choose_pick(P, jb, W.tidx, ntop, lane);
         fr = (pos / P.out_w) << P.J;
         fc = (pos % P.out_w) << P.J;
         clk3 = clock64();
     }
     // 4. paste (simulator.hpp:483-493) + source-block map
-    const int T = P.T;
-    uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
-    uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
-    const int wpr = T >> 2;  // 32-bit words per row
-    const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= JT && (JT % wpr) == 0;
-    if (vec4) {
-        // thread -> (row phase, word); every row it copies loaded in one round trip
-        const int rpi = JT / wpr, rsub = jt / wpr, cw = jt - rsub * wpr;
-        const uint8_t* srcp = P.ti + static_cast<size_t>(fr) * P.ti_w + fc + 4 * cw;
-        uint8_t* dstp = g + static_cast<size_t>(jb.top) * P.ww + jb.left + 4 * cw;
-        for (int r0 = rsub; r0 < T; r0 += rpi * 32) {
-            uint32_t v[32];  // every row this lane copies, loaded in one round trip
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int r = r0 + i * rpi;
-                if (r < T) v[i] = *reinterpret_cast<const uint32_t*>(srcp + static_cast<size_t>(r) * P.ti_w);
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int r = r0 + i * rpi;
-                if (r < T) {
-                    *reinterpret_cast<uint32_t*>(dstp + static_cast<size_t>(r) * P.ww) = v[i];
-                    if (trace) *reinterpret_cast<uint32_t*>(trace + r * T + 4 * cw) = v[i];
-                }
-            }
-        }
-    } else {
-        for (int r = 0; r < T; ++r)
-            for (int c = jt; c < T; c += JT) {
-                const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
-                g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
-                if (trace) trace[r * T + c] = v;
-            }
-    }
-    if (P.src) {
-        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc +
-                      static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
-        const int s0 = (fr / P.B) * P.wc + fc / P.B;
-        for (int a = 0; a < Tc; ++a)
-            for (int b = jt; b < Tc; b += JT) sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
-    }
+    paste_job<JT>(P, jb, gj, fr, fc, jt);
     if (jt == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
@@ -1110,6 +1164,347 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
             atomicAdd(&tacc[4], static_cast<unsigned long long>(clk3 - clk2));
             atomicAdd(&tacc[5], static_cast<unsigned long long>(clk4 - clk3));
         }
+    }
+}
+
+// ------------------------------------------------------- bulk tie select --
+//
+// Placements whose exact-screen tie group is large (a binary TI with K = 1
+// can tie thousands of windows at the maximum) are deferred here by the warp
+// select.  S CTAs serve each deferred placement: they take position blocks of
+// bulk_bx x bulk_by windows from a per-placement counter; a block holding a
+// window at or above the threshold stages the TI apex tile it reads into
+// shared memory (cp.async) and every thread rescores whole windows in the
+// reference's operation order (matcher.hpp:72-77, 160-161), BK_W independent
+// windows interleaved to hide the dependent fp64 chain.  Each CTA publishes
+// its top-K; the last CTA to finish merges them by the reference ranking
+// (matcher.hpp:189-198), chooses and pastes like the warp select.
+constexpr int BK_T = 256;
+constexpr int BK_W = 4;
+constexpr int BK_V = 8;      // positions per thread per scan pass
+constexpr int BK_SMAX = 8;   // CTAs per placement (upper bound)
+
+struct BulkLayout {
+    size_t stage, tm, rows, cand, misc, total;
+    int sh, sw;
+};
+
+__host__ __device__ inline BulkLayout bulk_layout(int nch, int Tc, int bx, int by) {
+    BulkLayout L{};
+    L.sh = bx + Tc - 1;
+    L.sw = (by + Tc - 1) | 1;  // odd row stride spreads rows over the banks
+    size_t o = 0;
+    L.stage = o;
+    o += static_cast<size_t>(nch) * L.sh * L.sw * sizeof(double);
+    // the per-thread top-K lists reuse the stage area at the end
+    o = std::max(o, static_cast<size_t>(BK_T) * kTcQ * (sizeof(double) + sizeof(int)));
+    L.tm = o;
+    o += static_cast<size_t>(nch) * Tc * Tc * sizeof(double);
+    L.rows = o;
+    o += static_cast<size_t>(Tc) * sizeof(short4);
+    L.cand = o;
+    o += (static_cast<size_t>(bx) * by + BK_T) * sizeof(int);
+    o = (o + 15) & ~static_cast<size_t>(15);
+    L.misc = o;
+    o += 320 + static_cast<size_t>(BK_SMAX) * kTcQ * (sizeof(double) + sizeof(int));
+    L.total = o;
+    return L;
+}
+
+__global__ void __launch_bounds__(BK_T, 1)
+    select_bulk_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj, int S) {
+    extern __shared__ __align__(16) unsigned char bk_sm[];
+    pdl_trigger();
+    pdl_wait();
+    const int slot = blockIdx.y, part = blockIdx.x;
+    if (slot >= nj) return;
+    const int thr = P.defer[slot];
+    if (thr == INT_MIN) return;  // handled by the warp select
+    const int gj = job0 + slot;
+    const Job jb = jobs[gj];
+    const int Tc = P.Tc, nch = P.nch, K = P.K;
+    const int bx = P.bulk_bx, by = P.bulk_by;
+    const BulkLayout L = bulk_layout(nch, Tc, bx, by);
+    double* stg = reinterpret_cast<double*>(bk_sm + L.stage);
+    double* tmS = reinterpret_cast<double*>(bk_sm + L.tm);
+    short4* rows = reinterpret_cast<short4*>(bk_sm + L.rows);
+    int* cand = reinterpret_cast<int*>(bk_sm + L.cand);
+    unsigned char* misc = bk_sm + L.misc;
+    int* wcnt = reinterpret_cast<int*>(misc);               // [8]
+    double* rk = reinterpret_cast<double*>(misc + 64);     // [8]
+    int* ri = reinterpret_cast<int*>(misc + 128);          // [8]
+    int* rp = reinterpret_cast<int*>(misc + 160);          // [8]
+    double* tkey = reinterpret_cast<double*>(misc + 192);  // [kTcQ]
+    int* tidx = reinterpret_cast<int*>(misc + 256);        // [kTcQ]
+    int* shv = reinterpret_cast<int*>(misc + 288);         // [4] broadcast scalars
+    double* mk = reinterpret_cast<double*>(misc + 320);    // [BK_SMAX * kTcQ] merge keys
+    int* mi = reinterpret_cast<int*>(misc + 320 + 8 * BK_SMAX * kTcQ);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+    const int2* tsum = P.summary + static_cast<size_t>(slot) * P.ntiles * kTcQ;
+    const double* tm = P.tm64 + static_cast<size_t>(slot) * nch * Tc * Tc;
+    long long clk_stage = 0, clk_comp = 0;
+    const long long clk_start = clock64();
+    for (int e = tid; e < nch * Tc * Tc; e += BK_T) tmS[e] = tm[e];
+    int nrows = 0;
+    for (int s0 = 0; s0 < Tc; s0 += 32) {
+        const int s = s0 + lane;
+        int t0 = 0, t1 = 0;
+        if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+        const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
+        if (wid == 0 && t1 > t0) rows[nrows + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
+        nrows += __popc(m);
+    }
+    double tk[kTcQ];
+    int tix[kTcQ];
+#pragma unroll
+    for (int j = 0; j < kTcQ; ++j) {
+        tk[j] = -INFINITY;
+        tix[j] = INT_MAX;
+    }
+    unsigned long long rescored = 0;
+    const int nbx = (P.out_h + bx - 1) / bx, nby = (P.out_w + by - 1) / by;
+    int* next = P.bulk_sync + 2 * slot;  // [0] next block, [1] finished CTAs
+    for (;;) {
+        __syncthreads();  // previous block's stage / candidates consumed
+        if (tid == 0) shv[0] = atomicAdd(next, 1);
+        __syncthreads();
+        const int kb = shv[0];
+        if (kb >= nbx * nby) break;
+        const int xb = (kb / nby) * bx, yb = (kb % nby) * by;
+        const int bxa = min(bx, P.out_h - xb), bya = min(by, P.out_w - yb);
+        // skip blocks whose tiles all stay below the threshold
+        const int tf = (xb * P.out_w + yb) / kTcTile;
+        const int tl = ((xb + bxa - 1) * P.out_w + yb + bya - 1) / kTcTile;
+        bool any = false;
+        for (int t = tf + tid; t <= tl; t += BK_T) any |= tsum[static_cast<size_t>(t) * kTcQ].x >= thr;
+        if (!__syncthreads_or(any)) continue;
+        // windows of the block at or above the threshold (block-local index)
+        const long long c_st = clock64();
+        int cnt = 0;
+        const int nb = bxa * bya;
+        for (int e0 = 0; e0 < nb; e0 += BK_T * BK_V) {
+            int v[BK_V];
+#pragma unroll
+            for (int i = 0; i < BK_V; ++i) {
+                const int e = e0 + tid * BK_V + i;
+                v[i] = INT_MIN;
+                if (e < nb) {
+                    const int lx = e / bya, ly = e - lx * bya;
+                    v[i] = sc[(xb + lx) * P.out_w + yb + ly];
+                }
+            }
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < BK_V; ++i) c += v[i] >= thr;
+            int incl = c;  // warp inclusive scan
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wcnt[wid] = incl;
+            __syncthreads();
+            int off = incl - c, tot = 0;
+#pragma unroll
+            for (int w = 0; w < BK_T / 32; ++w) {
+                off += w < wid ? wcnt[w] : 0;
+                tot += wcnt[w];
+            }
+            off += cnt;
+#pragma unroll
+            for (int i = 0; i < BK_V; ++i)
+                if (v[i] >= thr) cand[off++] = e0 + tid * BK_V + i;
+            cnt += tot;
+            __syncthreads();
+        }
+        if (cnt == 0) continue;
+        rescored += cnt;
+        // stage the apex tile the block's windows read
+        const int sha = bxa + Tc - 1, swa = bya + Tc - 1;
+        for (int ch = 0; ch < nch; ++ch) {
+            const double* src = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
+                                static_cast<size_t>(xb) * P.wc + yb;
+            double* dst = stg + static_cast<size_t>(ch) * L.sh * L.sw;
+            for (int e = tid; e < sha * swa; e += BK_T) {
+                const int r = e / swa, c = e - r * swa;
+                cp_async8(dst + r * L.sw + c, src + static_cast<size_t>(r) * P.wc + c);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        const long long c_cp = clock64();
+        clk_stage += c_cp - c_st;
+        for (int i0 = tid; i0 < cnt; i0 += BK_T * BK_W) {
+            int base[BK_W], pidx[BK_W];
+            bool ok[BK_W];
+#pragma unroll
+            for (int k = 0; k < BK_W; ++k) {
+                const int i = i0 + k * BK_T;
+                ok[k] = i < cnt;
+                const int e = cand[ok[k] ? i : i0];
+                const int lx = e / bya, ly = e - lx * bya;
+                base[k] = lx * L.sw + ly;
+                pidx[k] = (xb + lx) * P.out_w + yb + ly;
+            }
+            double acc[BK_W];
+#pragma unroll
+            for (int k = 0; k < BK_W; ++k) acc[k] = 0.0;
+            for (int ch = 0; ch < nch; ++ch) {
+                const double* sp = stg + static_cast<size_t>(ch) * L.sh * L.sw;
+                const double* tp = tmS + ch * Tc * Tc;
+                for (int r = 0; r < nrows; ++r) {
+                    const short4 rw = rows[r];
+                    const double* a = sp + rw.x * L.sw + rw.y;
+                    const double* b = tp + rw.x * Tc + rw.y;
+                    const int len = rw.z - rw.y;
+                    double sum[BK_W];
+#pragma unroll
+                    for (int k = 0; k < BK_W; ++k) sum[k] = 0.0;
+                    // sum += ti*or left to right (matcher.hpp:72-76)
+#pragma unroll 4
+                    for (int t = 0; t < len; ++t) {
+                        const double bv = b[t];
+#pragma unroll
+                        for (int k = 0; k < BK_W; ++k) sum[k] = __dadd_rn(sum[k], __dmul_rn(a[base[k] + t], bv));
+                    }
+#pragma unroll
+                    for (int k = 0; k < BK_W; ++k) acc[k] = __dadd_rn(acc[k], sum[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < BK_W; ++k) {
+                if (!ok[k]) continue;
+                double ck = acc[k];
+                int ci = pidx[k];
+#pragma unroll
+                for (int j = 0; j < kTcQ; ++j)
+                    if (j < K && better(ck, ci, tk[j], tix[j])) {
+                        const double t0 = tk[j];
+                        const int t1 = tix[j];
+                        tk[j] = ck;
+                        tix[j] = ci;
+                        ck = t0;
+                        ci = t1;
+                    }
+            }
+        }
+        clk_comp += clock64() - c_cp;
+    }
+    // this CTA's top-K: K rounds of a block-wide arg-best over the per-thread lists
+    double* lk = stg;
+    int* li = reinterpret_cast<int*>(stg + BK_T * kTcQ);
+#pragma unroll
+    for (int j = 0; j < kTcQ; ++j) {
+        lk[j * BK_T + tid] = tk[j];
+        li[j * BK_T + tid] = tix[j];
+    }
+    int head = 0;
+    for (int round = 0; round < K; ++round) {
+        double bk = head < K ? lk[head * BK_T + tid] : -INFINITY;
+        int bi = head < K ? li[head * BK_T + tid] : INT_MAX;
+        int bt = tid;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ok2 = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+            if (better(ok2, oi, bk, bi)) {
+                bk = ok2;
+                bi = oi;
+                bt = ot;
+            }
+        }
+        if (lane == 0) {
+            rk[wid] = bk;
+            ri[wid] = bi;
+            rp[wid] = bt;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < BK_T / 32; ++w)
+                if (better(rk[w], ri[w], bk, bi)) {
+                    bk = rk[w];
+                    bi = ri[w];
+                    bt = rp[w];
+                }
+            tkey[round] = bk;
+            tidx[round] = bi;
+            shv[1] = bt;
+        }
+        __syncthreads();
+        if (tid == shv[1]) ++head;
+    }
+    if (tid == 0) {
+        double* gk = P.bulk_keys + (static_cast<size_t>(slot) * BK_SMAX + part) * kTcQ;
+        int* gi = P.bulk_idx + (static_cast<size_t>(slot) * BK_SMAX + part) * kTcQ;
+        for (int j = 0; j < K; ++j) {
+            gk[j] = tkey[j];
+            gi[j] = tidx[j];
+        }
+        if (P.stats) {
+            atomicAdd(&P.stats[14], static_cast<unsigned long long>(clk_stage));
+            atomicAdd(&P.stats[15], static_cast<unsigned long long>(clk_comp));
+            atomicAdd(&P.stats[7], static_cast<unsigned long long>(clock64() - clk_start));
+            if (rescored) atomicAdd(&P.stats[0], rescored);
+        }
+        __threadfence();
+        shv[2] = atomicAdd(next + 1, 1);
+    }
+    __syncthreads();
+    if (shv[2] != S - 1) return;  // not the last CTA of this placement
+    // last CTA: merge the S lists (reference ranking), choose, paste
+    __threadfence();
+    const int nm = S * K;
+    for (int e = tid; e < nm; e += BK_T) {
+        const int p = e / K, j = e - p * K;
+        mk[e] = __ldcg(P.bulk_keys + (static_cast<size_t>(slot) * BK_SMAX + p) * kTcQ + j);
+        mi[e] = __ldcg(P.bulk_idx + (static_cast<size_t>(slot) * BK_SMAX + p) * kTcQ + j);
+    }
+    __syncthreads();
+    int ntop = 0;
+    if (wid == 0) {
+        for (int round = 0; round < K; ++round) {
+            double bk = -INFINITY;
+            int bi = INT_MAX, bp = -1;
+            for (int e = lane; e < nm; e += 32)
+                if (mi[e] != INT_MAX && better(mk[e], mi[e], bk, bi)) {
+                    bk = mk[e];
+                    bi = mi[e];
+                    bp = e;
+                }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ok2 = __shfl_xor_sync(0xffffffffu, bk, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (better(ok2, oi, bk, bi)) {
+                    bk = ok2;
+                    bi = oi;
+                    bp = op;
+                }
+            }
+            if (bp < 0) break;
+            if (lane == 0) {
+                tkey[round] = bk;
+                tidx[round] = bi;
+                mi[bp] = INT_MAX;
+            }
+            __syncwarp();
+            ntop = round + 1;
+        }
+        const int pos = choose_pick(P, jb, tidx, ntop, lane);
+        if (lane == 0) {
+            shv[3] = pos;
+            next[0] = 0;  // reset the placement's counters for the next launch
+            next[1] = 0;
+            if (P.stats) atomicAdd(&P.stats[3], 1ull);
+        }
+    }
+    __syncthreads();
+    const int pos = shv[3];
+    const int fr = (pos / P.out_w) << P.J, fc = (pos % P.out_w) << P.J;
+    paste_job<BK_T>(P, jb, gj, fr, fc, tid);
+    if (tid == 0) {
+        P.chosen[2 * gj] = fr;
+        P.chosen[2 * gj + 1] = fc;
     }
 }
 
@@ -1249,19 +1644,37 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         nlr = (wh - T) / stride + 1;
         nlc = (ww - T) / stride + 1;
     }
+    // hard data per lattice cell (placements sit on the stride lattice for
+    // every raster path): CSR lists of (cell in footprint, facies), so the
+    // conditional choice reads only the cells that hold data
     std::vector<uint8_t> lattice_hd;
+    std::vector<int32_t> hd_off;
+    std::vector<uint32_t> hd_ent;
     if (hd && n_hd > 0) {
-        lattice_hd.assign(static_cast<size_t>(nlr) * nlc, 0);
-        for (int i = 0; i < n_hd; ++i) {
+        const size_t ncell = static_cast<size_t>(nlr) * nlc;
+        lattice_hd.assign(ncell, 0);
+        hd_off.assign(ncell + 1, 0);
+        auto each_cell = [&](int i, auto&& fn) {
             const int r = hd[3 * i], c = hd[3 * i + 1];
             const int qr0 = std::max(0, (r - T + 1 + stride - 1) / stride);
             const int qc0 = std::max(0, (c - T + 1 + stride - 1) / stride);
             for (int qr = qr0; qr <= std::min(nlr - 1, r / stride); ++qr)
                 for (int qc = qc0; qc <= std::min(nlc - 1, c / stride); ++qc)
-                    if (r >= qr * stride && r < qr * stride + T && c >= qc * stride &&
-                        c < qc * stride + T)
-                        lattice_hd[static_cast<size_t>(qr) * nlc + qc] = 1;
+                    if (r >= qr * stride && r < qr * stride + T && c >= qc * stride && c < qc * stride + T)
+                        fn(static_cast<size_t>(qr) * nlc + qc, r - qr * stride, c - qc * stride, hd[3 * i + 2]);
+        };
+        for (int i = 0; i < n_hd; ++i)
+            each_cell(i, [&](size_t q, int, int, int) { ++hd_off[q + 1]; });
+        for (size_t q = 0; q < ncell; ++q) {
+            lattice_hd[q] = hd_off[q + 1] > 0;
+            hd_off[q + 1] += hd_off[q];
         }
+        hd_ent.resize(hd_off[ncell]);
+        std::vector<int32_t> fill(hd_off.begin(), hd_off.end() - 1);
+        for (int i = 0; i < n_hd; ++i)
+            each_cell(i, [&](size_t q, int lr, int lc, int v) {
+                hd_ent[fill[q]++] = (static_cast<uint32_t>(lr * T + lc) << 8) | static_cast<uint32_t>(v);
+            });
     }
     auto build_one = [&](int r) {
         std::mt19937_64 rng(seeds[r]);
@@ -1370,6 +1783,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     uint8_t* d_work = ctx->work.as<uint8_t>(plane * n_real);
     CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
     uint8_t* d_hd = nullptr;
+    const int32_t* P_hd_off = nullptr;
+    const uint32_t* P_hd_ent = nullptr;
     if (hd && n_hd > 0) {
         d_hd = ctx->hd.as<uint8_t>(plane);
         CCW_CUDA(cudaMemsetAsync(d_hd, kNoDatum, plane, st));
@@ -1377,6 +1792,14 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaMemcpyAsync(d_hdl, hd, sizeof(int32_t) * 3 * n_hd, cudaMemcpyHostToDevice, st));
         hd_scatter_kernel<<<(n_hd + 255) / 256, 256, 0, st>>>(d_hdl, n_hd, d_hd, ww);
         CCW_CUDA(cudaGetLastError());
+        int32_t* d_off = ctx->hdoff.as<int32_t>(hd_off.size());
+        uint32_t* d_ent = ctx->hdent.as<uint32_t>(std::max<size_t>(1, hd_ent.size()));
+        CCW_CUDA(cudaMemcpyAsync(d_off, hd_off.data(), sizeof(int32_t) * hd_off.size(), cudaMemcpyHostToDevice, st));
+        if (!hd_ent.empty())
+            CCW_CUDA(cudaMemcpyAsync(d_ent, hd_ent.data(), sizeof(uint32_t) * hd_ent.size(),
+                                     cudaMemcpyHostToDevice, st));
+        P_hd_off = d_off;
+        P_hd_ent = d_ent;
     }
     const int sld = (npos + 3) & ~3;  // (score rows exist only for the block-select path)
     const size_t score_budget = (static_cast<size_t>(512) << 20) / G;
@@ -1417,6 +1840,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.wh = wh;
     P.ww = ww;
     P.hd = d_hd;
+    P.hd_off = P_hd_off;
+    P.hd_ent = P_hd_ent;
+    P.lat_nlc = nlc;
+    P.stride = stride;
     P.sld = sld;
     P.chosen = d_chosen;
     P.pasted = d_pasted;
@@ -1456,6 +1883,39 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.im2col = d_x;
     // list mode: the screen keeps per-tile (score, position) lists instead of score rows
     const bool list_mode = warp_select && getenv("CCW_TCLISTS");  // measured slower (r1)
+    // bulk tie select: largest window block whose apex tile fits the shared-memory budget
+    size_t bulk_smem = 0;
+    if (warp_select && !list_mode && !getenv("CCW_NOBULK")) {
+        constexpr size_t kBudget = 200 * 1024;
+        for (int by = std::min(out_w, 256); by >= 8 && !bulk_smem; by /= 2) {
+            int bx = std::min(out_h, 64);
+            while (bx > 1 && bulk_layout(ti->nch, Tc, bx, by).total > kBudget) --bx;
+            if (bulk_layout(ti->nch, Tc, bx, by).total <= kBudget && (bx >= 4 || bx == out_h)) {
+                P.bulk_bx = bx;
+                P.bulk_by = by;
+                bulk_smem = bulk_layout(ti->nch, Tc, bx, by).total;
+            }
+        }
+    }
+    const auto bulk_key = std::make_tuple(Tc, OVc, Kp, T);
+    const bool bulk_launch = bulk_smem && !ti->bulk_off.count(bulk_key);
+    int* d_defer = bulk_launch ? ctx->defer.as<int>(G * maxj) : nullptr;
+    int bulk_S = 1;
+    if (bulk_launch) {
+        // CTAs per deferred placement: enough to cover the SMs when a wave
+        // chunk defers a third of its placements
+        bulk_S = std::max(1, std::min(BK_SMAX, 3 * tc_num_sms() / std::max<int>(1, static_cast<int>(std::min<size_t>(maxj, max_wave)))));
+        int* d_bsync = ctx->bulk_sync.as<int>(2 * G * maxj);
+        CCW_CUDA(cudaMemsetAsync(d_bsync, 0, sizeof(int) * 2 * G * maxj, st));
+        P.bulk_sync = d_bsync;
+        P.bulk_keys = ctx->bulk_keys.as<double>(G * maxj * BK_SMAX * kTcQ);
+        P.bulk_idx = ctx->bulk_idx.as<int>(G * maxj * BK_SMAX * kTcQ);
+    }
+    P.bulk_min = bulk_smem ? 2 * WS_CB : 0;
+    if (const char* e = getenv("CCW_BULK_EST")) P.bulk_min = atoi(e);
+    if (bulk_smem)
+        CCW_CUDA(cudaFuncSetAttribute(select_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(bulk_smem)));
     std::vector<SimParams> GP(G, P);
     for (int g = 0; g < G; ++g) {
         // the warp select recomputes the few tiles it needs: no score rows
@@ -1465,6 +1925,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         GP[g].tm64 = d_tm + g * maxj * ti->nch * Tc * Tc;
         GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
         GP[g].summary = d_summary ? d_summary + g * maxj * ntiles * kTcQ : nullptr;
+        GP[g].defer = d_defer ? d_defer + g * maxj : nullptr;
+        if (d_defer) {
+            GP[g].bulk_sync = P.bulk_sync + 2 * g * maxj;
+            GP[g].bulk_keys = P.bulk_keys + g * maxj * BK_SMAX * kTcQ;
+            GP[g].bulk_idx = P.bulk_idx + g * maxj * BK_SMAX * kTcQ;
+        }
     }
 
     const size_t ccf_smem = ccf_smem_bytes(Tc, ti->nscr);
@@ -1561,6 +2027,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     else
                         launch_pdl(select_paste_warp_kernel<4>, dim3(nj), dim3(128), sizeof(WarpSel), gs,
                                    Q, dj, static_cast<int>(j0), nj);
+                    if (Q.defer && !first_wave) {
+                        launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, Q, dj,
+                                   static_cast<int>(j0), nj, bulk_S);
+                        ++launches;
+                    }
                 }
                 else
                     launch_pdl(select_paste_kernel, dim3(nj), dim3(SEL_T), sel_smem, gs, Q,
@@ -1627,10 +2098,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.jobs = static_cast<int64_t>(total_jobs);
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
     if (getenv("CCW_PHASES"))
-        fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu\n",
-                stats[8], stats[9], stats[10], stats[11], stats[12], stats[13]);
+        fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu"
+                " | bulk total %llu stage %llu compute %llu\n",
+                stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[7], stats[14], stats[15]);
     ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
     ctx->timing.recomputed_tiles = static_cast<int64_t>(stats[2]);
+    ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
+    if (bulk_launch && stats[3] == 0)
+        ti->bulk_off[bulk_key] = true;
+    else if (!bulk_launch && stats[4] > 0)
+        ti->bulk_off.erase(bulk_key);
     ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 

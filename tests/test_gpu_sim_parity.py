@@ -107,6 +107,30 @@ def test_large_k_and_conditioning(oracle):
         assert all(r.realization.cells[a, b] == f for a, b, f in hd)
 
 
+@pytest.mark.parametrize("k", [1, 2, 5])
+def test_large_tie_groups_bulk_path(oracle, k):
+    """Binary TI at J=3 (BASELINE config 2 regime): the exact screen ties
+    hundreds to thousands of windows at the K-th score, which the warp select
+    hands to the bulk rescoring kernel.  Bit-exact against the oracle, with
+    and without hard data."""
+    from paper_2404_00441_b200 import synth
+    ti_a = synth.channel_ti(640, 640, 77, scale=6.0)
+    ti = cs.CategoricalGrid(640, 640, 2, ti_a)
+    d = dict(sg_height=600, sg_width=700, template_size=96, overlap=24, dwt_level=3, candidates=k)
+    dev = cs.default_device()
+    seeds = [cs.mix64(5, k), cs.mix64(6, k)]
+    ref0 = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=seeds[0])["realization"]
+    hd = synth.hard_data_from(ref0, 0.01, 9 + k)
+    for cond in (None, [tuple(int(v) for v in row) for row in hd]):
+        cfg = to_cfg(d, cond)
+        res = cs.simulate_batch(ti, cfg, seeds)
+        assert dev.last_timing()["bulk_jobs"] > 0
+        for s, r in zip(seeds, res):
+            o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), cond, seed=s)
+            assert np.array_equal(r.realization.cells, o["realization"]), (k, cond is None)
+            assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+
+
 def test_provenance_and_replay():
     # test_simulator.cpp:434-460, acceptance.cpp:349-381
     z = load("sim_channel64_base.npz")
