@@ -6,6 +6,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <atomic>
 #include <map>
 #include <utility>
 
@@ -177,6 +179,48 @@ Plan make_plan_from(const ccw_sim_config& c, int origin, bool column_major) {
     return p;
 }
 
+namespace {
+struct DevCache {
+    std::mutex mu;
+    std::map<void*, std::pair<int, size_t>> live;                   // ptr -> (device, bytes)
+    std::multimap<std::pair<int, size_t>, void*> idle;              // (device, bytes) -> ptr
+};
+DevCache& dev_cache() {
+    static DevCache* c = new DevCache();  // intentionally leaked: outlives static destructors
+    return *c;
+}
+}  // namespace
+
+void* cache_alloc(int device, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 1);
+    DevCache& c = dev_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.idle.find({device, bytes});
+        if (it != c.idle.end()) {
+            void* p = it->second;
+            c.idle.erase(it);
+            c.live[p] = {device, bytes};
+            return p;
+        }
+    }
+    void* p = nullptr;
+    CCW_CUDA(cudaMalloc(&p, bytes));
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.live[p] = {device, bytes};
+    return p;
+}
+
+void cache_free(void* p) {
+    if (!p) return;
+    DevCache& c = dev_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.live.find(p);
+    if (it == c.live.end()) return;
+    c.idle.emplace(it->second, p);
+    c.live.erase(it);
+}
+
 }  // namespace ccwgpu
 
 // ================================================================ C-ABI ===
@@ -300,9 +344,32 @@ static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device
         ti->nscr = mode == 0 ? nf - 1 : 1;
         const size_t n = static_cast<size_t>(h) * w;
         const size_t nc = static_cast<size_t>(ti->hc) * ti->wc;
-        CCW_CUDA(cudaMalloc(&ti->d_codes, n));
-        CCW_CUDA(cudaMalloc(&ti->d_ti64, sizeof(double) * nc * ti->nch));
-        CCW_CUDA(cudaMalloc(&ti->d_scr, sizeof(float) * nc * std::max(ti->nscr, 1)));
+        ti->d_codes = static_cast<uint8_t*>(ccwgpu::cache_alloc(ti->device, n));
+        ti->d_ti64 = static_cast<double*>(ccwgpu::cache_alloc(ti->device, sizeof(double) * nc * ti->nch));
+        ti->d_scr = static_cast<float*>(ccwgpu::cache_alloc(ti->device, sizeof(float) * nc * std::max(ti->nscr, 1)));
+        // content key: host cells hashed with the shape; device cells get a unique id
+        uint64_t key = 0x9E3779B97F4A7C15ull ^ (static_cast<uint64_t>(h) << 40) ^
+                       (static_cast<uint64_t>(w) << 16) ^ (static_cast<uint64_t>(nf) << 8) ^
+                       (static_cast<uint64_t>(levels) << 4) ^ static_cast<uint64_t>(mode);
+        if (!device_ptr) {
+            // four independent multiply-rotate lanes, folded at the end
+            uint64_t a[4] = {key, key + 1, key + 2, key + 3};
+            constexpr uint64_t kM = 0x9FB21C651E98DF25ull;
+            size_t i = 0;
+            for (; i + 32 <= n; i += 32)
+                for (int l = 0; l < 4; ++l) {
+                    uint64_t v;
+                    std::memcpy(&v, cells + i + 8 * l, 8);
+                    a[l] = ((a[l] ^ v) * kM);
+                    a[l] ^= a[l] >> 29;
+                }
+            for (; i < n; ++i) a[0] = (a[0] ^ cells[i]) * kM;
+            key = ccwgpu::mix_key(a[0] ^ ccwgpu::mix_key(a[1] ^ ccwgpu::mix_key(a[2] ^ ccwgpu::mix_key(a[3]))));
+        } else {
+            static std::atomic<uint64_t> next_id{1};
+            key = ccwgpu::mix_key(key ^ (next_id.fetch_add(1) << 1 | 1));
+        }
+        ti->key = key;
         CCW_CUDA(cudaMemcpyAsync(ti->d_codes, cells, n,
                                  device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                  ctx->stream));
@@ -328,12 +395,14 @@ ccw_status ccw_ti_create_device(ccw_ctx* ctx, const uint8_t* d_cells, int h, int
 
 void ccw_ti_destroy(ccw_ti* ti) {
     if (!ti) return;
-    // cudaFree synchronises the device; the owning context may already be gone.
+    // The owning context may already be gone: drain the device, then hand
+    // the buffers back to the process-wide cache.
     cudaSetDevice(ti->device);
-    if (ti->d_codes) cudaFree(ti->d_codes);
-    if (ti->d_ti64) cudaFree(ti->d_ti64);
-    if (ti->d_scr) cudaFree(ti->d_scr);
-    for (auto& kv : ti->im2col) cudaFree(kv.second);
+    cudaDeviceSynchronize();
+    ccwgpu::cache_free(ti->d_codes);
+    ccwgpu::cache_free(ti->d_ti64);
+    ccwgpu::cache_free(ti->d_scr);
+    for (auto& kv : ti->im2col) ccwgpu::cache_free(kv.second);
     delete ti;
 }
 

@@ -462,8 +462,7 @@ const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st) {
     const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1;
     const int npos = out_h * out_w;
     const int kpad = tc_kpad(ti->nscr, Tc);
-    int8_t* X = nullptr;
-    CCW_CUDA(cudaMalloc(&X, static_cast<size_t>(npos) * kpad));
+    int8_t* X = static_cast<int8_t*>(cache_alloc(ti->device, static_cast<size_t>(npos) * kpad));
     const size_t total = static_cast<size_t>(npos) * kpad;
     im2col_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
         ti->d_scr, ti->nscr, ti->hc, ti->wc, Tc, out_w, npos, kpad, X);

@@ -4,7 +4,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <exception>
+#include <functional>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <tuple>
 #include <random>
 #include <stdexcept>
@@ -95,6 +102,104 @@ struct HostBuf {
     }
 };
 
+// 64-bit finalizer (splitmix64 style) for content keys.
+inline uint64_t mix_key(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Process-wide caching device allocator (exact-size reuse, per device):
+// training-image buffers come and go with every ccw_ti; returning them to
+// the driver (cudaFree) would unmap memory and stall on every destroy.
+void* cache_alloc(int device, size_t bytes);
+void cache_free(void* p);
+
+// Persistent host worker pool (one per context): run(n, fn) calls fn(i) for
+// every i in [0, n) on the workers and the calling thread, then rethrows the
+// first exception.  Keeps thread start-up out of every simulate call.
+class HostPool {
+public:
+    HostPool() = default;
+    HostPool(const HostPool&) = delete;
+    HostPool& operator=(const HostPool&) = delete;
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : thr_) t.join();
+    }
+    template <class F>
+    void run(int n, F&& fn) {
+        if (n <= 0) return;
+        const int want = std::min(n / 2, max_workers());
+        if (want <= 0) {
+            for (int i = 0; i < n; ++i) fn(i);
+            return;
+        }
+        while (static_cast<int>(thr_.size()) < want) thr_.emplace_back([this, g = gen_] { worker(g); });
+        std::function<void(int)> job(std::forward<F>(fn));
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &job;
+            n_ = n;
+            next_.store(0);
+            busy_ = static_cast<int>(thr_.size());
+            err_ = nullptr;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return busy_ == 0; });
+        job_ = nullptr;
+        if (err_) std::rethrow_exception(err_);
+    }
+
+private:
+    static int max_workers() {
+        const int hw = static_cast<int>(std::thread::hardware_concurrency());
+        return std::max(0, std::min(hw, 16) - 1);
+    }
+    void work() {
+        for (;;) {
+            const int i = next_.fetch_add(1);
+            if (i >= n_) return;
+            try {
+                (*job_)(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!err_) err_ = std::current_exception();
+                next_.store(n_);
+            }
+        }
+    }
+    void worker(uint64_t seen) {
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--busy_ == 0) done_.notify_all();
+        }
+    }
+    std::vector<std::thread> thr_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    std::function<void(int)>* job_ = nullptr;
+    int n_ = 0, busy_ = 0;
+    std::atomic<int> next_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    std::exception_ptr err_;
+};
+
 }  // namespace ccwgpu
 
 struct ccw_ctx {
@@ -108,8 +213,13 @@ struct ccw_ctx {
     ccwgpu::DevBuf defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
+    ccwgpu::HostPool pool;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<cudaStream_t> gstreams;  // realization-group streams
+    // launch plan memory: (TI content key, Tc, OVc, K, T) whose last call
+    // deferred no placement to the bulk tie select skip its per-wave launch
+    // (re-enabled when the warp select reports a would-be deferral)
+    std::map<std::tuple<uint64_t, int, int, int, int>, bool> bulk_off;
 };
 
 struct ccw_ti {
@@ -121,9 +231,7 @@ struct ccw_ti {
     double* d_ti64 = nullptr;    // nch*hc*wc
     float* d_scr = nullptr;      // nscr*hc*wc
     std::map<int, int8_t*> im2col;  // per template size Tc: npos x kpad int8 (tcgen05 screen)
-    // launch plan memory: geometries whose last call deferred no placement to
-    // the bulk tie select skip its per-wave launch (re-enabled on demand)
-    std::map<std::tuple<int, int, int, int>, bool> bulk_off;
+    uint64_t key = 0;  // content key (hash of cells + shape) for per-context plan memory
 };
 
 namespace ccwgpu {

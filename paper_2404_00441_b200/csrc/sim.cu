@@ -1628,17 +1628,29 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const int reach = (T + stride - 1) / stride - 1;  // footprints overlap up to `reach` steps
     const int keymul = reach + 1;
 
-    // ---- host schedule: plans, hard-data lattice, mt19937_64 draw schedule.
-    // Every realization's draws are independent (seeded per realization), so
-    // the schedule is built in parallel host threads, then counting-sorted by
-    // (group, wave) straight into pinned staging memory for one upload.
-    std::vector<Plan> plans(n_real);
-    std::vector<std::vector<Job>> rjobs(n_real);
-    std::vector<std::vector<int>> rkeys(n_real);
+    // ---- host schedule: raster paths, hard-data lattice, mt19937_64 draws.
+    // A raster path (simulator.hpp:148-190) is one of 8 variants (origin x
+    // major order); each realization draws its variant, then its per-placement
+    // draws.  Jobs are written straight into pinned staging memory in
+    // (group, wave, realization, placement) order.
+    std::vector<Plan> variants(8);
+    std::vector<char> have(8, 0);
+    std::vector<int> vid(n_real);
+    std::vector<std::mt19937_64> rngs(n_real);
+    for (int r = 0; r < n_real; ++r) {
+        rngs[r].seed(seeds[r]);
+        const int origin = static_cast<int>(bounded(rngs[r], 4));
+        const bool cm = bounded(rngs[r], 2) == 1;
+        const int v = origin * 2 + (cm ? 1 : 0);
+        if (!have[v]) {
+            variants[v] = make_plan_from(cfg, origin, cm);
+            have[v] = 1;
+        }
+        vid[r] = v;
+    }
     int wh = 0, ww = 0, nlr = 0, nlc = 0;
     {
-        std::mt19937_64 r0(seeds[0]);
-        const Plan p0 = make_plan(cfg, r0);  // geometry (identical for every plan)
+        const Plan& p0 = variants[vid[0]];  // geometry (identical for every variant)
         wh = p0.work_h;
         ww = p0.work_w;
         nlr = (wh - T) / stride + 1;
@@ -1676,17 +1688,59 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 hd_ent[fill[q]++] = (static_cast<uint32_t>(lr * T + lc) << 8) | static_cast<uint32_t>(v);
             });
     }
+    int max_key = 0;
+    for (int v = 0; v < 8; ++v)
+        if (have[v]) max_key = std::max(max_key, keymul * (variants[v].n_outer - 1) + variants[v].n_inner - 1);
+    const int nkeys = max_key + 1;
+    // per-variant wave histograms
+    std::vector<std::vector<int>> vhist(8);
+    for (int v = 0; v < 8; ++v)
+        if (have[v]) {
+            vhist[v].assign(nkeys, 0);
+            const Plan& p = variants[v];
+            for (size_t k = 0; k < p.tops.size(); ++k) ++vhist[v][keymul * p.outer_idx[k] + p.inner_idx[k]];
+        }
+
+    // Realizations are split into G independent groups, each on its own
+    // stream, so one group's latency-bound select overlaps another group's
+    // tensor-core screen.  Within a group, waves run in order.
+    int G = std::max(1, std::min(n_real, 2));
+    if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
+    auto group_of = [&](int r) { return static_cast<int>(static_cast<int64_t>(r) * G / n_real); };
+    std::vector<size_t> bucket(static_cast<size_t>(G) * nkeys + 1, 0);
+    size_t total_jobs = 0;
+    for (int r = 0; r < n_real; ++r) {
+        const size_t g = group_of(r);
+        for (int k = 0; k < nkeys; ++k) bucket[g * nkeys + k + 1] += vhist[vid[r]][k];
+        total_jobs += variants[vid[r]].tops.size();
+    }
+    for (size_t i = 1; i < bucket.size(); ++i) bucket[i] += bucket[i - 1];
+    std::vector<std::vector<size_t>> wave_off(G);  // per group, absolute offsets into flat
+    size_t max_wave = 1;
+    for (int g = 0; g < G; ++g) {
+        for (int k = 0; k <= nkeys; ++k) wave_off[g].push_back(bucket[static_cast<size_t>(g) * nkeys + std::min(k, nkeys)]);
+        for (int k = 0; k < nkeys; ++k) max_wave = std::max(max_wave, wave_off[g][k + 1] - wave_off[g][k]);
+    }
+    // each realization's first slot in every wave bucket
+    std::vector<size_t> roff(static_cast<size_t>(n_real) * nkeys);
+    {
+        std::vector<size_t> fill(bucket.begin(), bucket.end() - 1);
+        for (int r = 0; r < n_real; ++r) {
+            const size_t g = group_of(r);
+            for (int k = 0; k < nkeys; ++k) {
+                roff[static_cast<size_t>(r) * nkeys + k] = fill[g * nkeys + k];
+                fill[g * nkeys + k] += vhist[vid[r]][k];
+            }
+        }
+    }
+    Job* flat = static_cast<Job*>(ctx->h_stage.get(sizeof(Job) * total_jobs));
     auto build_one = [&](int r) {
-        std::mt19937_64 rng(seeds[r]);
-        plans[r] = make_plan(cfg, rng);
-        const Plan& p = plans[r];
+        std::mt19937_64& rng = rngs[r];
+        const Plan& p = variants[vid[r]];
+        size_t* off = roff.data() + static_cast<size_t>(r) * nkeys;
         const int cnt = static_cast<int>(p.tops.size());
-        std::vector<Job>& jv = rjobs[r];
-        std::vector<int>& kv = rkeys[r];
-        jv.resize(cnt);
-        kv.resize(cnt);
         for (int k = 0; k < cnt; ++k) {
-            Job& jb = jv[k];
+            Job jb;
             jb.real = r;
             jb.place = k;
             jb.top = p.tops[k];
@@ -1704,68 +1758,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   lattice_hd[static_cast<size_t>(jb.top / stride) * nlc + jb.left / stride];
                 jb.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
             }
-            kv[k] = keymul * p.outer_idx[k] + p.inner_idx[k];
+            flat[off[keymul * p.outer_idx[k] + p.inner_idx[k]]++] = jb;
         }
     };
-    {
-        const int nthr = std::max(1, std::min<int>(n_real / 4, std::min<int>(16, static_cast<int>(std::thread::hardware_concurrency()))));
-        if (nthr <= 1) {
-            for (int r = 0; r < n_real; ++r) build_one(r);
-        } else {
-            std::vector<std::thread> pool;
-            std::atomic<int> next{0};
-            std::exception_ptr err;
-            std::mutex mu;
-            for (int t = 0; t < nthr; ++t)
-                pool.emplace_back([&] {
-                    for (;;) {
-                        const int r = next.fetch_add(1);
-                        if (r >= n_real) return;
-                        try {
-                            build_one(r);
-                        } catch (...) {
-                            std::lock_guard<std::mutex> lk(mu);
-                            if (!err) err = std::current_exception();
-                            return;
-                        }
-                    }
-                });
-            for (auto& th : pool) th.join();
-            if (err) std::rethrow_exception(err);
-        }
-    }
-    int max_key = 0;
-    for (const Plan& p : plans) max_key = std::max(max_key, keymul * (p.n_outer - 1) + p.n_inner - 1);
-
-    // Realizations are split into G independent groups, each on its own
-    // stream, so one group's latency-bound select overlaps another group's
-    // tensor-core screen.  Within a group, waves run in order.
-    int G = std::max(1, std::min(n_real, 2));
-    if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
-    const int nkeys = max_key + 1;
-    std::vector<size_t> bucket(static_cast<size_t>(G) * nkeys + 1, 0);
-    size_t total_jobs = 0;
-    for (int r = 0; r < n_real; ++r) {
-        const int g = static_cast<int>(static_cast<int64_t>(r) * G / n_real);
-        for (int k : rkeys[r]) ++bucket[static_cast<size_t>(g) * nkeys + k + 1];
-        total_jobs += rkeys[r].size();
-    }
-    for (size_t i = 1; i < bucket.size(); ++i) bucket[i] += bucket[i - 1];
-    std::vector<std::vector<size_t>> wave_off(G);  // per group, absolute offsets into flat
-    size_t max_wave = 1;
-    for (int g = 0; g < G; ++g) {
-        for (int k = 0; k <= nkeys; ++k) wave_off[g].push_back(bucket[static_cast<size_t>(g) * nkeys + std::min(k, nkeys)]);
-        for (int k = 0; k < nkeys; ++k) max_wave = std::max(max_wave, wave_off[g][k + 1] - wave_off[g][k]);
-    }
-    Job* flat = static_cast<Job*>(ctx->h_stage.get(sizeof(Job) * total_jobs));
-    {
-        std::vector<size_t> fill(bucket.begin(), bucket.end() - 1);
-        for (int r = 0; r < n_real; ++r) {  // realization order within each wave
-            const int g = static_cast<int>(static_cast<int64_t>(r) * G / n_real);
-            const std::vector<Job>& jv = rjobs[r];
-            for (size_t k = 0; k < jv.size(); ++k) flat[fill[static_cast<size_t>(g) * nkeys + rkeys[r][k]]++] = jv[k];
-        }
-    }
+    ctx->pool.run(n_real, build_one);
     const double host_prep_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
 
@@ -1897,8 +1893,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             }
         }
     }
-    const auto bulk_key = std::make_tuple(Tc, OVc, Kp, T);
-    const bool bulk_launch = bulk_smem && !ti->bulk_off.count(bulk_key);
+    const auto bulk_key = std::make_tuple(ti->key, Tc, OVc, Kp, T);
+    const bool bulk_launch = bulk_smem && !ctx->bulk_off.count(bulk_key);
     int* d_defer = bulk_launch ? ctx->defer.as<int>(G * maxj) : nullptr;
     int bulk_S = 1;
     if (bulk_launch) {
@@ -2105,9 +2101,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.recomputed_tiles = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
     if (bulk_launch && stats[3] == 0)
-        ti->bulk_off[bulk_key] = true;
+        ctx->bulk_off[bulk_key] = true;
     else if (!bulk_launch && stats[4] > 0)
-        ti->bulk_off.erase(bulk_key);
+        ctx->bulk_off.erase(bulk_key);
     ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 
@@ -2116,11 +2112,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         if (diag) {
             ccw_diag& d = diag[r];
             d.seed = seeds[r];
-            d.origin = plans[r].origin;
-            d.column_major = plans[r].column_major;
+            d.origin = variants[vid[r]].origin;
+            d.column_major = variants[vid[r]].column_major;
             d.work_height = wh;
             d.work_width = ww;
-            d.placement_count = static_cast<int>(plans[r].tops.size());
+            d.placement_count = static_cast<int>(variants[vid[r]].tops.size());
             d.hard_data_count = hd ? n_hd : 0;
             d.pre_overwrite_mismatches = mism[r];
             d._pad = 0;
@@ -2148,7 +2144,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                             static_cast<size_t>(T) * T);
         }
         for (int r = 0; r < n_real; ++r)
-            traces[r].count = std::min(traces[r].capacity, static_cast<int>(plans[r].tops.size()));
+            traces[r].count = std::min(traces[r].capacity, static_cast<int>(variants[vid[r]].tops.size()));
     }
 }
 
