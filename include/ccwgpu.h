@@ -114,7 +114,7 @@ typedef struct ccw_timing {
     int64_t ccf_variant;    /* 0 none (normalized / F=1), 1 fp32 direct, 2 tcgen05 int8 */
     double ccf_mma_flop;    /* tensor-core MMA FLOP issued (full Tc x Tc window, padded K) */
     int64_t groups;         /* realization groups run concurrently on separate streams */
-    int64_t recomputed_tiles; /* summary tiles re-scored because ties overflowed the list */
+    int64_t list_overflows; /* placements with more than 256 windows at or above the tile bound */
     double host_prep_ms;    /* host schedule build (plans + mt19937_64 draws) before launch */
     int64_t bulk_jobs;      /* placements whose tie group went to the bulk (CTA-wide) rescoring */
 } ccw_timing;

@@ -43,7 +43,7 @@ class TimingC(C.Structure):
                 ("ccf_flop_ref", C.c_double), ("waves", C.c_int64), ("jobs", C.c_int64),
                 ("rescored", C.c_int64), ("screened_jobs", C.c_int64), ("ccf_variant", C.c_int64),
                 ("ccf_mma_flop", C.c_double), ("groups", C.c_int64),
-                ("recomputed_tiles", C.c_int64), ("host_prep_ms", C.c_double),
+                ("list_overflows", C.c_int64), ("host_prep_ms", C.c_double),
                 ("bulk_jobs", C.c_int64)]
 
 
@@ -101,11 +101,12 @@ def lib():
     """Load libccwgpu.so (built in-tree by ``__graft_entry__.build()``)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("CCW_LIB_VARIANT") or LIB_PATH  # build-variant experiments
+        if not os.path.exists(path):
             raise ImportError(
-                f"{LIB_PATH} is missing: build the CUDA extension first "
+                f"{path} is missing: build the CUDA extension first "
                 "(python -c 'import __graft_entry__ as g; g.build()')")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res

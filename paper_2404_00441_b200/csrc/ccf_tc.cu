@@ -12,12 +12,13 @@
 // fp32 CUDA-core screen (ccf_direct_kernel) bit for bit.  Off-mask template
 // cells cost MMA work but no correctness (their weights are zero).
 //
-// Tile: M = 128 jobs x N = 256 positions, K in 128-byte stages, two-stage
-// TMA -> shared-memory (128B swizzle) ring feeding a single-thread MMA issuer;
-// the accumulator (128 lanes x 256 columns int32) lives in TMEM.  The epilogue
-// (4 warps, one TMEM lane per job) writes S and a per-(job, tile) summary of
-// the top-Q scores with multiplicity, from which the select kernel derives
-// the exact K-th largest score without rescanning every position.
+// Tile: M = 128 jobs x N = 256 positions, K in 128-byte stages, a TMA ->
+// shared-memory (128B swizzle) ring feeding a single-thread MMA issuer; the
+// accumulator (128 lanes x 256 columns int32) lives in TMEM.  The epilogue
+// (8 warps, one TMEM lane per job) transposes each 32 x 32 block through
+// shared memory so the score rows are written with row-contiguous stores,
+// and keeps the maximum of every 128-position tile, from which the select
+// kernel bounds the K-th largest score without rescanning every position.
 #include <cuda.h>
 
 #include <algorithm>
@@ -35,7 +36,14 @@ namespace {
 constexpr int kM = 128;
 constexpr int kN = 256;
 constexpr int kKC = 128;  // bytes of K per stage (one 128B swizzle atom)
-constexpr int kStages = 4;
+#ifndef CCW_TC_STAGES
+#define CCW_TC_STAGES 4
+#endif
+#ifndef CCW_TC_ACC
+#define CCW_TC_ACC 2
+#endif
+constexpr int kStages = CCW_TC_STAGES;
+constexpr int kAcc = CCW_TC_ACC;  // TMEM accumulators (kAcc x 256 columns)
 constexpr int kABytes = kM * kKC;
 constexpr int kBBytes = kN * kKC;
 constexpr int kStageBytes = kABytes + kBBytes;
@@ -122,127 +130,56 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
           "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
         : "r"(taddr))
 
-// One (job tile, position tile) of accumulators, drained from TMEM: exact
-// scores (optional), the per-half-tile top-Q summary, and -- in list mode --
-// the (score, position) pairs reaching the Q-th score.
-template <int Q>
+// One (job tile, half position tile) of accumulators, drained from TMEM:
+// the exact scores and the tile maximum.  stage = this warp's 4 KB of shared
+// memory (32 rows x 128 B, 16-byte chunks swizzled by row) for the transpose.
 __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int m0, int n0,
-                                            int warp, int lane) {
+                                            int warp, int lane, uint32_t stage) {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int job = m0 + q * 32 + lane;
-    const bool valid_job = job < a.nj;
-    int top[Q];
-#pragma unroll
-    for (int i = 0; i < Q; ++i) top[i] = INT_MIN;
-    int32_t* out = a.scores ? a.scores + static_cast<size_t>(valid_job ? job : 0) * a.sld : nullptr;
     const uint32_t trow = tbuf + (static_cast<uint32_t>(q * 32) << 16) + half * (kN / 2);
     const int pbase = n0 + half * (kN / 2);
     const int ntile = (n0 / kN) * 2 + half;
+    int mx = INT_MIN;
+    // store phase: lane -> (row r0 + 4 i, 16-byte chunk lane & 7)
+    const int srow = lane >> 3, schunk = lane & 7;
     for (int c = 0; c < kN / 64; ++c) {
         uint32_t r[32];
         LDTM_X32(trow + c * 32, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int p0 = pbase + c * 32;
-        if (valid_job) {
-            if (!out) {
-                // list mode: no score rows
-            } else if (p0 + 32 <= a.npos) {
-                int4* dst = reinterpret_cast<int4*>(out + p0);
+        const int lim = a.npos - p0;  // valid columns of this chunk
 #pragma unroll
-                for (int v = 0; v < 8; ++v)
-                    dst[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-            } else {
-                for (int i = 0; i < 32; ++i)
-                    if (p0 + i < a.npos) out[p0 + i] = static_cast<int>(r[i]);
-            }
+        for (int i = 0; i < 32; ++i)
+            if (i < lim) mx = max(mx, static_cast<int>(r[i]));
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                int v = static_cast<int>(r[i]);
-                if (p0 + i < a.npos && v > top[Q - 1]) {
-#pragma unroll
-                    for (int j = 0; j < Q; ++j) {
-                        if (v > top[j]) {
-                            const int t = top[j];
-                            top[j] = v;
-                            v = t;
-                        }
-                    }
-                }
-            }
+        for (int v = 0; v < 8; ++v) {
+            const uint32_t addr = stage + lane * 128 + ((v ^ (lane & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(r[4 * v]),
+                         "r"(r[4 * v + 1]), "r"(r[4 * v + 2]), "r"(r[4 * v + 3])
+                         : "memory");
         }
-    }
-    int2* sm_out = a.summary + (static_cast<size_t>(valid_job ? job : 0) * a.ntiles + ntile) * kTcQ;
-    if (out) {
-        if (valid_job)
+        __syncwarp();
+        const int pos = p0 + schunk * 4;
 #pragma unroll
-            for (int i = 0; i < kTcQ; ++i) sm_out[i] = make_int2(i < Q ? top[i < Q ? i : 0] : INT_MIN, -1);
-        return;
-    }
-    // list mode, pass 2: pairs reaching the Q-th score, in position order
-    const int L = top[Q - 1];
-    int lv[Q], lp[Q];
-#pragma unroll
-    for (int i = 0; i < Q; ++i) {
-        lv[i] = INT_MIN;
-        lp[i] = -1;
-    }
-    int n = 0;
-    for (int c = 0; c < kN / 64; ++c) {
-        uint32_t r[32];
-        LDTM_X32(trow + c * 32, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int p0 = pbase + c * 32;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int v = static_cast<int>(r[i]);
-            if (valid_job && p0 + i < a.npos && v >= L) {
-#pragma unroll
-                for (int j = 0; j < Q; ++j)
-                    if (j == n) {
-                        lv[j] = v;
-                        lp[j] = p0 + i;
-                    }
-                ++n;
-            }
+        for (int i = 0; i < 8; ++i) {
+            const int row = 4 * i + srow;
+            const uint32_t addr = stage + row * 128 + ((schunk ^ (row & 7)) << 4);
+            int4 v;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(addr)
+                         : "memory");
+            const int jr = m0 + q * 32 + row;
+            // rows are padded to sld (a multiple of 4) >= npos: a chunk that
+            // starts inside the row is stored whole
+            if (jr < a.nj && pos < a.npos)
+                *reinterpret_cast<int4*>(a.scores + static_cast<size_t>(jr) * a.sld + pos) = v;
         }
+        __syncwarp();
     }
-    const bool ovf = n > Q;
-    if (__any_sync(0xffffffffu, ovf)) {  // rare: ties overflow the list -> exact scores of the half tile
-        int32_t* o2 = a.ovf + static_cast<size_t>(valid_job ? job : 0) * a.sld;
-        for (int c = 0; c < kN / 64; ++c) {
-            uint32_t r[32];
-            LDTM_X32(trow + c * 32, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int p0 = pbase + c * 32;
-            if (valid_job && ovf)
-                for (int i = 0; i < 32; ++i)
-                    if (p0 + i < a.npos) o2[p0 + i] = static_cast<int>(r[i]);
-        }
-    }
-    if (!ovf) {  // order by (score desc, position asc): entry 0 = tile max
-#pragma unroll
-        for (int i = 1; i < Q; ++i)
-#pragma unroll
-            for (int j = Q - 1; j >= i; --j)
-                if (lv[j] > lv[j - 1] ||
-                    (lv[j] == lv[j - 1] && lp[j] >= 0 && (lp[j - 1] < 0 || lp[j] < lp[j - 1]))) {
-                    const int tv = lv[j], tp = lp[j];
-                    lv[j] = lv[j - 1];
-                    lp[j] = lp[j - 1];
-                    lv[j - 1] = tv;
-                    lp[j - 1] = tp;
-                }
-    }
-    if (valid_job) {
-#pragma unroll
-        for (int i = 0; i < kTcQ; ++i) {
-            int2 e = make_int2(INT_MIN, -1);
-            if (i < Q)
-                e = ovf ? make_int2(top[i < Q ? i : 0], -2) : make_int2(lv[i < Q ? i : 0], lp[i < Q ? i : 0]);
-            sm_out[i] = e;
-        }
-    }
+    if (job < a.nj) a.tmax[static_cast<size_t>(job) * a.ntiles + ntile] = mx;
 }
 
 // Persistent implicit GEMM: one CTA per SM loops over (job tile, position
@@ -250,7 +187,6 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
 // issues the MMAs into one of two TMEM accumulators, warps 2..9 drain the
 // other accumulator -- the epilogue of tile i overlaps the loads and MMAs of
 // tile i+1.
-template <int Q>
 __global__ void __launch_bounds__(kThreads, 1)
     ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   TcArgs a) {
@@ -262,9 +198,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + kStages;   // [2] accumulator ready
     uint64_t* tempty = tfull + 2;        // [2] accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const uint32_t epi_stage = smem_u32(sm + kStages * kStageBytes + 256);  // 4 KB per epilogue warp
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mt = (a.nj + kM - 1) / kM, n_nt = (a.npos + kN - 1) / kN;
+    const long long pc0 = clock64();
+    auto probe = [&](int k) {
+        if (a.probe) atomicAdd(&a.probe[k], static_cast<unsigned long long>(clock64() - pc0));
+    };
     pdl_trigger();
     const int ntot = n_mt * n_nt;
 
@@ -282,15 +223,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)));
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(tmem_slot)), "n"(kAcc * kN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) probe(0);
     pdl_wait();  // the weights (or_prep) and the previous wave's outputs are complete
+    if (threadIdx.x == 0) probe(1);
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer: K stages of every tile, one ring
@@ -312,13 +255,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc = i8_idesc(kM, kN);
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < ntot; t += gridDim.x, ++lt) {
-                const int b = lt & 1;
-                if (lt >= 2) mbar_wait(smem_u32(&tempty[b]), ((lt >> 1) - 1) & 1);
+                const int b = lt % kAcc;
+                if (lt >= kAcc) mbar_wait(smem_u32(&tempty[b]), ((lt / kAcc) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t acc = tmem + b * kN;
                 for (int kc = 0; kc < a.nk; ++kc, ++it) {
                     const int s = it % kStages;
                     mbar_wait(smem_u32(&full[s]), (it / kStages) & 1);
+                    if (it == 0) probe(2);
+                    if (it == a.nk - 1) probe(3);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint64_t ad = sw128_desc(smem_u32(sm + s * kStageBytes));
                     const uint64_t bd = sw128_desc(smem_u32(sm + s * kStageBytes + kABytes));
@@ -333,11 +278,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {  // epilogue warps 2..9
         int lt = 0;
         for (int t = blockIdx.x; t < ntot; t += gridDim.x, ++lt) {
-            const int b = lt & 1;
-            mbar_wait(smem_u32(&tfull[b]), (lt >> 1) & 1);
+            const int b = lt % kAcc;
+            mbar_wait(smem_u32(&tfull[b]), (lt / kAcc) & 1);
+            if (lt == 0 && warp == 2 && lane == 0) probe(4);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int m0 = (t % n_mt) * kM, n0 = (t / n_mt) * kN;
-            tc_epilogue<Q>(a, tmem + b * kN, m0, n0, warp, lane);
+            tc_epilogue(a, tmem + b * kN, m0, n0, warp, lane, epi_stage + (warp - 2) * 4096);
+            if (lt == 0 && lane == 0) probe(5);  // summed over the 8 epilogue warps
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
@@ -345,8 +292,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) {
+        probe(6);
+        if (a.probe) atomicAdd(&a.probe[7], 1ull);
+    }
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAcc * kN));
 }
 
 // Tensor-core peak probe: back-to-back kind::i8 MMAs of the screen's shape
@@ -442,7 +393,7 @@ CUtensorMap make_map(void* base, uint64_t cols_bytes, uint64_t rows, uint32_t bo
 
 }  // namespace
 
-size_t ccf_tc_smem_bytes() { return kStages * kStageBytes + 1024 + 256; }
+size_t ccf_tc_smem_bytes() { return kStages * kStageBytes + 1024 + 256 + kEpiWarps * 4096; }
 
 int tc_num_sms() {
     static int sms = 0;
@@ -453,6 +404,8 @@ int tc_num_sms() {
     }
     return sms;
 }
+
+unsigned long long* tc_probe_buffer = nullptr;
 
 int tc_kpad(int nscr, int Tc) { return ((nscr * Tc * Tc + 15) / 16) * 16; }
 
@@ -496,26 +449,17 @@ double measure_i8_peak(cudaStream_t st) {
     return best;
 }
 
-TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad, int K) {
+TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad) {
     TcPlan pl;
     pl.ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
     pl.mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
-    pl.q = tc_qdepth(K);
-    auto attr = [&](auto kern) {
-        CCW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(ccf_tc_smem_bytes())));
-    };
-    if (pl.q == 4)
-        attr(ccf_tc_kernel<4>);
-    else if (pl.q == 6)
-        attr(ccf_tc_kernel<6>);
-    else
-        attr(ccf_tc_kernel<8>);
+    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ccf_tc_smem_bytes())));
     return pl;
 }
 
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* ovf, int2* summary, cudaStream_t st) {
+                   int32_t* tmax, cudaStream_t st) {
     TcArgs a;
     a.nj = nj;
     a.npos = npos;
@@ -523,21 +467,13 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     a.nk = (kpad + kKC - 1) / kKC;
     a.ntiles = tc_tiles(npos);
     a.scores = scores;
-    a.ovf = ovf;
-    a.summary = summary;
+    a.tmax = tmax;
+    a.probe = tc_probe_buffer;
     const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
     dim3 grid(std::min(ntot, tc_num_sms()));
-    if (pl.q == 4)
-        launch_pdl(ccf_tc_kernel<4>, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
-    else if (pl.q == 6)
-        launch_pdl(ccf_tc_kernel<6>, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
-    else
-        launch_pdl(ccf_tc_kernel<8>, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
+    launch_pdl(ccf_tc_kernel, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
 }
 
-// summary depth: K plus headroom (keeps tie overflow rare), from {4, 6, 8}
-int tc_qdepth(int K) { return K + 3 <= 4 ? 4 : (K + 3 <= 6 ? 6 : 8); }
-
-int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // summaries per half tile
+int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // tile maxima per score row
 
 }  // namespace ccwgpu

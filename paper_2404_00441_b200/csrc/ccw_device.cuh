@@ -61,13 +61,11 @@ struct SimParams {
     int8_t* wts8;            // kpad int8 screen weights per job (tcgen05 screen), may be null
     const int8_t* im2col;    // npos x kpad int8 TI windows (tcgen05 screen), may be null
     int kpad;
-    int2* summary;           // per job: ntiles x kTcQ top (score, position) (tcgen05), may be null
-    int qdepth;              // summary slots actually filled (overflow check)
+    int32_t* tmax;           // per job: ntiles tile maxima of the screen (tcgen05), may be null
     int ntiles;
     unsigned long long* stats;  // [0] windows rescored in fp64, [1] screened jobs
     double* tm64;            // nch*Tc*Tc reference-order OR apex values
     int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
-    int32_t* ovf;            // same layout, only tie-overflowing tiles written (warp path)
     int sld;
     int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)

@@ -608,25 +608,18 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         // 1. exact screen threshold: every window whose integer score reaches
         //    the K-th largest can appear in the reference's top-K.
         const bool all = !use_screen;
-        const int2* tsum =
-            P.summary ? P.summary + static_cast<size_t>(blockIdx.x) * P.ntiles * kTcQ : nullptr;
+        const int32_t* tmx = P.tmax ? P.tmax + static_cast<size_t>(blockIdx.x) * P.ntiles : nullptr;
         int thr = 0;
-        if (!all) {
-            if (tsum && K <= P.qdepth)  // union of per-tile top-Q lists holds the global top-K
-                thr = radix_kth_largest(reinterpret_cast<const int32_t*>(tsum), P.ntiles * kTcQ, K,
-                                        hist, misc, redi, 2);
-            else
-                thr = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
-        }
+        if (!all) thr = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
         if (P.stats && tid == 0) atomicAdd(&P.stats[1], 1ull);
         __syncthreads();
         // 2. gather the tie group in row-major order, rescore in fp64, keep the
         //    running top-K by (fp64 desc, index asc).
-        const int span = tsum ? kTcTile : SEL_T;
+        const int span = tmx ? kTcTile : SEL_T;
         const int nspans = (P.npos + span - 1) / span;
         int ntop = 0, cnt = 0;
         for (int sp = 0; sp < nspans; ++sp) {
-            if (!all && tsum && tsum[static_cast<size_t>(sp) * kTcQ].x < thr) continue;  // uniform
+            if (!all && tmx && tmx[sp] < thr) continue;  // uniform
             for (int sub = 0; sub < span; sub += SEL_T) {
                 const int p = sp * span + sub + tid;
                 const bool q = sub + tid < span && p < P.npos && (all || sc[p] >= thr);
@@ -735,8 +728,12 @@ constexpr int WS_RS = 256;    // (window, run) partial sums per rescoring batch
 
 constexpr int WS_MAXTC = 64;   // template rows tabulated per warp
 
+constexpr int WS_LC = 256;   // (score, position) list of windows >= M_K
+
 struct WarpSel {
     short4 rows[WS_MAXTC];  // (s, t0, t1, cell offset) of the mask rows, row-major
+    int lv[WS_LC];
+    int lp[WS_LC];
     int cidx[WS_CB + kTcQ];
     double ckey[WS_CB + kTcQ];
     int tidx[kTcQ];
@@ -890,6 +887,29 @@ __device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm,
     }
 }
 
+// K-th largest (with multiplicity) of the union of the lanes' sorted top
+// lists (INT_MIN padded): rounds of warp max over the lanes' heads.
+__device__ __forceinline__ int warp_kth(const int (&top)[kTcQ], int K, int lane) {
+    int ptr = 0, acc = 0;
+    for (int round = 0; round < kTcQ + 1; ++round) {
+        int head = INT_MIN;
+#pragma unroll
+        for (int i = 0; i < kTcQ; ++i)
+            if (i == ptr) head = top[i];
+        int m = head;
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < kTcQ; ++i)
+            if (i >= ptr && top[i] == m) ++c;
+        ptr += c;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        acc += c;
+        if (acc >= K || m == INT_MIN) return m;
+    }
+    return INT_MIN;
+}
+
 // Conditional / unconditional choice among the ranked top-K (matcher.hpp:207-241):
 // the host-drawn index, or the first zero-mismatch candidate against the hard
 // data, else the fewest mismatches.  Warp-level; every warp of a job may run
@@ -1015,21 +1035,22 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
         const int K = P.K;
         const int32_t* sc = P.scores ? P.scores + static_cast<size_t>(slot) * P.sld : nullptr;
         const double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
-        const int2* tsum = P.summary + static_cast<size_t>(slot) * P.ntiles * kTcQ;
-        // 1. exact K-th largest screen score from the per-tile top-Q lists
+        const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
+        // 1. M_K = K-th largest tile maximum (with multiplicity): a lower bound
+        //    of the K-th largest screen score S_K (the K best tiles each hold
+        //    a window scoring at least M_K).
         int top[kTcQ];
 #pragma unroll
         for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
-        const int nv = P.ntiles * kTcQ;
-        for (int e0 = 0; e0 < nv; e0 += 32 * 24) {
-            int vb[24];  // the job's summaries in one round trip (<= 768 per batch)
+        for (int e0 = 0; e0 < P.ntiles; e0 += 32 * 16) {
+            int vb[16];  // up to 512 tile maxima per round trip
 #pragma unroll
-            for (int i = 0; i < 24; ++i) {
+            for (int i = 0; i < 16; ++i) {
                 const int e = e0 + i * 32 + lane;
-                vb[i] = e < nv ? tsum[e].x : INT_MIN;
+                vb[i] = e < P.ntiles ? tmx[e] : INT_MIN;
             }
 #pragma unroll
-            for (int i = 0; i < 24; ++i) {
+            for (int i = 0; i < 16; ++i) {
                 int v = vb[i];
                 if (v > top[kTcQ - 1]) {
 #pragma unroll
@@ -1042,26 +1063,7 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
                 }
             }
         }
-        int ptr = 0, acc = 0, thr = INT_MIN;
-        for (int round = 0; round < kTcQ + 1; ++round) {
-            int head = INT_MIN;
-#pragma unroll
-            for (int i = 0; i < kTcQ; ++i)
-                if (i == ptr) head = top[i];
-            int m = head;
-            for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-            int c = 0;
-#pragma unroll
-            for (int i = 0; i < kTcQ; ++i)
-                if (i >= ptr && top[i] == m) ++c;
-            ptr += c;
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-            acc += c;
-            if (acc >= K || m == INT_MIN) {
-                thr = m;
-                break;
-            }
-        }
+        const int mk = warp_kth(top, K, lane);
         if (P.stats && jt == 0) atomicAdd(&P.stats[1], 1ull);
         clk1 = clock64();
         int R = 0;
@@ -1075,72 +1077,119 @@ __global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
         }
         job_sync<NWJ>();
         R *= P.nch;
-        if (P.bulk_min > 0) {
-            // Large tie groups (binary TIs, small K) would take many small
-            // flushes here; hand them to select_bulk_kernel, which rescores
-            // thread-per-window out of shared-memory TI tiles.
-            int est = 0;
-            for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
-                const int tt = t0 + lane;
-                if (tt < P.ntiles && tsum[static_cast<size_t>(tt) * kTcQ].x >= thr) {
-                    int c = 0;
-                    for (int i = 0; i < P.qdepth; ++i) c += tsum[static_cast<size_t>(tt) * kTcQ + i].x >= thr;
-                    est += c == P.qdepth ? 32 : c;  // a saturated list hides more ties
+        // 2. every window scoring >= M_K, from the tiles whose maximum reaches
+        //    it, into a (score, position) list; four tiles per round trip
+        int nl = 0;
+        bool over = false;
+        for (int t0 = 0; t0 < P.ntiles && !over; t0 += 32) {
+            const int tt = t0 + lane;
+            unsigned tiles = __ballot_sync(0xffffffffu, tt < P.ntiles && tmx[tt] >= mk);
+            while (tiles && !over) {
+                int tl[4], v[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    tl[u] = -1;
+                    if (tiles) {
+                        tl[u] = t0 + __ffs(tiles) - 1;
+                        tiles &= tiles - 1;
+                    }
                 }
-            }
-            for (int o = 16; o > 0; o >>= 1) est += __shfl_xor_sync(0xffffffffu, est, o);
-            const bool big = est > P.bulk_min;
-            if (P.defer) {
-                if (jt == 0) P.defer[slot] = big ? thr : INT_MIN;
-                if (big) return;  // uniform across the job's warps
-            } else if (big && P.stats && jt == 0) {
-                atomicAdd(&P.stats[4], 1ull);  // would have deferred: re-enable the bulk launches
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p0 = tl[u] * kTcTile + lane * 4;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
+                    if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
+                        const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
+                        v[u][0] = a4.x;
+                        v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
+                        v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
+                        v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool q = v[u][i] != INT_MIN && v[u][i] >= mk;  // scores are never INT_MIN
+                        const unsigned bal = __ballot_sync(0xffffffffu, q);
+                        if (!bal) continue;
+                        if (nl + __popc(bal) > WS_LC) {
+                            over = true;
+                            continue;
+                        }
+                        if (writer && q) {
+                            const int o = nl + __popc(bal & ((1u << lane) - 1));
+                            W.lv[o] = v[u][i];
+                            W.lp[o] = tl[u] * kTcTile + lane * 4 + i;
+                        }
+                        nl += __popc(bal);
+                    }
             }
         }
-        // 2. gather every window at or above the threshold, row-major.  Tile
-        //    heads are tested 32 at a time; a qualifying tile is read with one
-        //    vector load per lane (8 consecutive scores).
+        job_sync<NWJ>();
+        int thr = mk;  // overflow: rescore everything >= M_K (a superset: still exact)
+        if (over && P.stats && jt == 0) atomicAdd(&P.stats[2], 1ull);
+        if (!over) {
+            // exact S_K from the list (K rounds of warp max with multiplicity)
+            int cur = INT_MAX, acc = 0;
+            for (int round = 0; round < K; ++round) {
+                int m = INT_MIN;
+                for (int e = lane; e < nl; e += 32)
+                    if (W.lv[e] < cur) m = max(m, W.lv[e]);
+                for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+                int c = 0;
+                for (int e = lane; e < nl; e += 32) c += W.lv[e] == m;
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                acc += c;
+                thr = m;
+                if (acc >= K || m == INT_MIN) break;
+                cur = m;
+            }
+        } else if (P.defer) {
+            // a large tie group: the bulk kernel rescores every window >= M_K
+            // (INT_MIN marks "not deferred"; scores never reach it, so INT_MIN + 1 filters alike)
+            if (jt == 0) P.defer[slot] = max(mk, INT_MIN + 1);
+            return;  // uniform across the job's warps
+        }
+        if (P.defer && jt == 0) P.defer[slot] = INT_MIN;
+        // 3. candidates (>= S_K) -> fp64 rescoring in the reference's order
         int cnt = 0, ntop = 0;
-        for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
-            const int tt = t0 + lane;
-            const bool hit = tt < P.ntiles && tsum[static_cast<size_t>(tt) * kTcQ].x >= thr;
-            unsigned tiles = __ballot_sync(0xffffffffu, hit);
-            while (tiles) {
-                const int t = t0 + __ffs(tiles) - 1;
-                tiles &= tiles - 1;
-                const int2* tl = tsum + static_cast<size_t>(t) * kTcQ;
-                if (!P.scores && tl[0].y != -2) {
-                    // the tile's (score, position) list holds every window >= thr
-                    const int2 cv = lane < P.qdepth ? tl[lane] : make_int2(INT_MIN, 0);
-                    const bool q = cv.x >= thr;
-                    const unsigned bal = __ballot_sync(0xffffffffu, q);
-                    if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
-                    if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = cv.y;
-                    cnt += __popc(bal);
-                    job_sync<NWJ>();
-                    continue;
-                }
-                const int p0 = t * kTcTile + lane * 4;  // kTcTile = 128 = 32 lanes x 4
-                int v[4];
-                const int32_t* src_sc = P.scores ? sc : P.ovf + static_cast<size_t>(slot) * P.sld;
-                if (!P.scores && P.stats && jt == 0) atomicAdd(&P.stats[2], 1ull);
-                if (p0 + 4 <= P.npos) {
-                    const int4 a = *reinterpret_cast<const int4*>(src_sc + p0);
-                    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-                } else {
+        if (!over) {
+            for (int e0 = 0; e0 < nl; e0 += 32) {
+                const int e = e0 + lane;
+                const bool q = e < nl && W.lv[e] >= thr;
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (!bal) continue;
+                if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
+                const int pe = q ? W.lp[e] : 0;
+                job_sync<NWJ>();
+                if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = pe;
+                cnt += __popc(bal);
+                job_sync<NWJ>();
+            }
+        } else {
+            // no bulk kernel: stream the tiles again with threshold M_K
+            for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
+                const int tt = t0 + lane;
+                unsigned tiles = __ballot_sync(0xffffffffu, tt < P.ntiles && tmx[tt] >= thr);
+                while (tiles) {
+                    const int t = t0 + __ffs(tiles) - 1;
+                    tiles &= tiles - 1;
+                    const int p0 = t * kTcTile + lane * 4;
+                    int v[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) v[i] = p0 + i < P.npos ? src_sc[p0 + i] : INT_MIN;
-                }
-                // at most 32 appends per step, flushed before the buffer can overflow
+                    for (int i = 0; i < 4; ++i) v[i] = p0 + i < P.npos ? sc[p0 + i] : INT_MIN;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const bool q = v[i] >= thr;
-                    const unsigned bal = __ballot_sync(0xffffffffu, q);
-                    if (!bal) continue;
-                    if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
-                    if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = p0 + i;
-                    cnt += __popc(bal);
-                    job_sync<NWJ>();
+                    for (int i = 0; i < 4; ++i) {
+                        const bool q = v[i] != INT_MIN && v[i] >= thr;
+                        const unsigned bal = __ballot_sync(0xffffffffu, q);
+                        if (!bal) continue;
+                        if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
+                        if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = p0 + i;
+                        cnt += __popc(bal);
+                        job_sync<NWJ>();
+                    }
                 }
             }
         }
@@ -1241,7 +1290,7 @@ __global__ void __launch_bounds__(BK_T, 1)
     int* mi = reinterpret_cast<int*>(misc + 320 + 8 * BK_SMAX * kTcQ);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
-    const int2* tsum = P.summary + static_cast<size_t>(slot) * P.ntiles * kTcQ;
+    const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
     const double* tm = P.tm64 + static_cast<size_t>(slot) * nch * Tc * Tc;
     long long clk_stage = 0, clk_comp = 0;
     const long long clk_start = clock64();
@@ -1277,7 +1326,7 @@ __global__ void __launch_bounds__(BK_T, 1)
         const int tf = (xb * P.out_w + yb) / kTcTile;
         const int tl = ((xb + bxa - 1) * P.out_w + yb + bya - 1) / kTcTile;
         bool any = false;
-        for (int t = tf + tid; t <= tl; t += BK_T) any |= tsum[static_cast<size_t>(t) * kTcQ].x >= thr;
+        for (int t = tf + tid; t <= tl; t += BK_T) any |= tmx[t] >= thr;
         if (!__syncthreads_or(any)) continue;
         // windows of the block at or above the threshold (block-local index)
         const long long c_st = clock64();
@@ -1854,11 +1903,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const int ntiles = tc_tiles(npos);
     const int8_t* d_x = nullptr;
     int8_t* d_w8 = nullptr;
-    int2* d_summary = nullptr;
+    int32_t* d_tmax = nullptr;
     if (use_tc) {
         d_x = ti_im2col(ti, Tc, st);
         d_w8 = ctx->wts8.as<int8_t>(G * maxj * kpad);
-        d_summary = ctx->summary.as<int2>(G * maxj * ntiles * kTcQ);
+        d_tmax = ctx->summary.as<int32_t>(G * maxj * ntiles);
     }
     unsigned long long* d_stats = ctx->stats.as<unsigned long long>(16);
     CCW_CUDA(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
@@ -1874,14 +1923,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                              ti->nch * Tc <= WS_RS && Tc <= WS_MAXTC;
     P.kpad = kpad;
     P.ntiles = ntiles;
-    P.qdepth = tc_qdepth(Kp);
     P.stats = d_stats;
     P.im2col = d_x;
     // list mode: the screen keeps per-tile (score, position) lists instead of score rows
-    const bool list_mode = warp_select && getenv("CCW_TCLISTS");  // measured slower (r1)
     // bulk tie select: largest window block whose apex tile fits the shared-memory budget
     size_t bulk_smem = 0;
-    if (warp_select && !list_mode && !getenv("CCW_NOBULK")) {
+    if (warp_select && !getenv("CCW_NOBULK")) {
         constexpr size_t kBudget = 200 * 1024;
         for (int by = std::min(out_w, 256); by >= 8 && !bulk_smem; by /= 2) {
             int bx = std::min(out_h, 64);
@@ -1914,13 +1961,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                       static_cast<int>(bulk_smem)));
     std::vector<SimParams> GP(G, P);
     for (int g = 0; g < G; ++g) {
-        // the warp select recomputes the few tiles it needs: no score rows
-        GP[g].scores = list_mode ? nullptr : d_scores + g * maxj * sld;
-        GP[g].ovf = list_mode ? d_scores + g * maxj * sld : nullptr;
+        GP[g].scores = d_scores + g * maxj * sld;
         GP[g].wts = d_wts + g * maxj * std::max(ti->nscr, 1) * Tc * Tc;
         GP[g].tm64 = d_tm + g * maxj * ti->nch * Tc * Tc;
         GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
-        GP[g].summary = d_summary ? d_summary + g * maxj * ntiles * kTcQ : nullptr;
+        GP[g].tmax = d_tmax ? d_tmax + g * maxj * ntiles : nullptr;
         GP[g].defer = d_defer ? d_defer + g * maxj : nullptr;
         if (d_defer) {
             GP[g].bulk_sync = P.bulk_sync + 2 * g * maxj;
@@ -1943,16 +1988,28 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(WarpSel) * WS_WARPS)));
 
+    unsigned long long* d_probe = nullptr;
+    if (getenv("CCW_TC_PROBE")) {
+        d_probe = reinterpret_cast<unsigned long long*>(ctx->ops_d.get(8 * sizeof(unsigned long long)));
+        CCW_CUDA(cudaMemsetAsync(d_probe, 0, 8 * sizeof(unsigned long long), st));
+    }
+    tc_probe_buffer = d_probe;
     std::vector<TcPlan> tcplans;
     if (use_tc)
         for (int g = 0; g < G; ++g)
-            tcplans.push_back(plan_ccf_tc(GP[g].wts8, static_cast<int>(maxj), d_x, npos, kpad, Kp));
+            tcplans.push_back(plan_ccf_tc(GP[g].wts8, static_cast<int>(maxj), d_x, npos, kpad));
     // group streams, forked from / joined back to the context stream
     while (static_cast<int>(ctx->gstreams.size()) < G) {
         cudaStream_t s2;
         CCW_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
         ctx->gstreams.push_back(s2);
     }
+    // timing experiments only (results are wrong when set): skip a kernel class
+    const char* skip_env = getenv("CCW_DEBUG_SKIP");
+    const std::string skip = skip_env ? skip_env : "";
+    const bool skip_prep = skip.find("prep") != std::string::npos;
+    const bool skip_ccf = skip.find("ccf") != std::string::npos;
+    const bool skip_sel = skip.find("sel") != std::string::npos;
     EventTimer tm{ctx, {}, {}, 0};
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
@@ -1968,7 +2025,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 const int nj = static_cast<int>(std::min(maxj, wave_off[g][w + 1] - j0));
                 const bool first_wave = flat[j0].shape == kNone;
                 if (!first_wave) {
-                    if (d_src)
+                    if (skip_prep) {
+                    } else if (d_src)
                         launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
                                    static_cast<const Job*>(d_jobs), static_cast<int>(j0));
                     else
@@ -1982,9 +2040,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                             b = tm.get();
                             CCW_CUDA(cudaEventRecord(a, gs));
                         }
-                        if (use_tc) {
-                            launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.ovf,
-                                          Q.summary, gs);
+                        if (skip_ccf) {
+                        } else if (use_tc) {
+                            launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.tmax, gs);
                         } else {
                             launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, ccf_grid_xy.y, nj),
                                        dim3(CCF_THREADS), ccf_smem, gs, Q,
@@ -2011,7 +2069,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     b = tm.get();
                     CCW_CUDA(cudaEventRecord(a, gs));
                 }
-                if (warp_select || (first_wave && !cfg.min_cut)) {
+                if (skip_sel && !first_wave) {
+                } else if (warp_select || (first_wave && !cfg.min_cut)) {
                     const Job* dj = d_jobs;
                     if (selw == 1)
                         launch_pdl(select_paste_warp_kernel<1>, dim3((nj + WS_WARPS - 1) / WS_WARPS),
@@ -2093,12 +2152,21 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.host_prep_ms = host_prep_ms;
     ctx->timing.jobs = static_cast<int64_t>(total_jobs);
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
+    if (d_probe) {
+        unsigned long long pr[8];
+        CCW_CUDA(cudaMemcpy(pr, d_probe, sizeof(pr), cudaMemcpyDeviceToHost));
+        const double n = static_cast<double>(std::max(1ull, pr[7]));
+        fprintf(stderr, "ccf probe (mean cycles from CTA start over %llu CTAs): setup %.0f pdl_wait %.0f first_stage %.0f "
+                "last_stage %.0f acc_ready %.0f epilogue_done %.0f end %.0f\n", pr[7], pr[0] / n, pr[1] / n,
+                pr[2] / n, pr[3] / n, pr[4] / n, pr[5] / (8 * n), pr[6] / n);
+        tc_probe_buffer = nullptr;
+    }
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu"
                 " | bulk total %llu stage %llu compute %llu\n",
                 stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[7], stats[14], stats[15]);
     ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
-    ctx->timing.recomputed_tiles = static_cast<int64_t>(stats[2]);
+    ctx->timing.list_overflows = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
     if (bulk_launch && stats[3] == 0)
         ctx->bulk_off[bulk_key] = true;

@@ -131,6 +131,25 @@ def test_large_tie_groups_bulk_path(oracle, k):
             assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+@pytest.mark.parametrize("k", [4, 8])
+def test_k_above_tile_count_with_ties(oracle, k):
+    """Fewer 128-position tiles than K and a blocky TI (every window ties):
+    the tile-maximum bound degenerates, the candidate list overflows and the
+    placement goes to the bulk path with an all-positions threshold."""
+    rng = np.random.default_rng(77 + k)
+    ti_a = np.repeat(np.repeat(rng.integers(0, 3, (17, 21)), 4, 0), 4, 1).astype(np.uint8)
+    ti = cs.CategoricalGrid(68, 84, 3, ti_a)
+    for mode in (0, 1):
+        d = dict(sg_height=38, sg_width=94, template_size=12, overlap=4, dwt_level=2, candidates=k,
+                 facies_mode=mode)
+        cfg = to_cfg(d)
+        seeds = [3 + k, 4 + k]
+        res = cs.simulate_batch(ti, cfg, seeds)
+        for s, r in zip(seeds, res):
+            o = oracle.simulate_one(ti_a, 3, pyoracle.Cfg(**d), None, seed=s)
+            assert np.array_equal(r.realization.cells, o["realization"]), (k, mode)
+
+
 def test_provenance_and_replay():
     # test_simulator.cpp:434-460, acceptance.cpp:349-381
     z = load("sim_channel64_base.npz")
