@@ -37,7 +37,7 @@ constexpr int kM = 128;
 constexpr int kN = 256;
 constexpr int kKC = 128;  // bytes of K per stage (one 128B swizzle atom)
 #ifndef CCW_TC_STAGES
-#define CCW_TC_STAGES 4
+#define CCW_TC_STAGES 3
 #endif
 #ifndef CCW_TC_ACC
 #define CCW_TC_ACC 2
@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) probe(0);
+    tl_mark(a.tl, 2);
     pdl_wait();  // the weights (or_prep) and the previous wave's outputs are complete
+    tl_mark(a.tl, 0);
     if (threadIdx.x == 0) probe(1);
 
     if (warp == 0) {
@@ -292,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    tl_mark(a.tl, 1);
     if (threadIdx.x == 0) {
         probe(6);
         if (a.probe) atomicAdd(&a.probe[7], 1ull);
@@ -459,7 +462,7 @@ TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
 }
 
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* tmax, cudaStream_t st) {
+                   int32_t* tmax, cudaStream_t st, unsigned long long* tl) {
     TcArgs a;
     a.nj = nj;
     a.npos = npos;
@@ -469,6 +472,7 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     a.scores = scores;
     a.tmax = tmax;
     a.probe = tc_probe_buffer;
+    a.tl = tl;
     const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
     dim3 grid(std::min(ntot, tc_num_sms()));
     launch_pdl(ccf_tc_kernel, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);

@@ -22,6 +22,7 @@ struct TcArgs {
     int32_t* scores;   // [nj][sld] exact screen scores
     int32_t* tmax;     // [nj][ntiles] maximum score of each tile
     unsigned long long* probe;  // debug phase clocks (null unless CCW_TC_PROBE)
+    unsigned long long* tl;     // debug timeline slot (null unless CCW_TIMELINE)
 };
 
 size_t ccf_tc_smem_bytes();
@@ -40,6 +41,6 @@ struct TcPlan {
 };
 TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad);
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* tmax, cudaStream_t st);
+                   int32_t* tmax, cudaStream_t st, unsigned long long* tl = nullptr);
 
 }  // namespace ccwgpu

@@ -68,8 +68,11 @@ struct SimParams {
     int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
     int sld;
     int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
+    unsigned long long* tl;  // debug timeline slot of this launch (null unless CCW_TIMELINE)
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
-    int bulk_min;            // estimated tie-group size above which a placement is deferred
+    int* cand;               // fast select: candidate positions per job slot (SC_LC each)
+    int* ncand;              //   count, -1 = stream windows >= cthr, -2 = deferred to the bulk kernel
+    int* cthr;               //   streaming threshold (list overflow without the bulk kernel)
     int* bulk_sync;          // per job slot: [next position block, finished CTAs]
     double* bulk_keys;       // per job slot x CTA: that CTA's top-K keys
     int* bulk_idx;           //   ... and positions
@@ -152,6 +155,25 @@ __device__ __forceinline__ int block_stat(const uint8_t* cells, int ld, int B, i
 // kernel launched without the programmatic-serialization attribute.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Debug timeline (CCW_TIMELINE): per launch [first CTA past its dependency
+// wait, last CTA end, first CTA resident] in globaltimer ns.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int k) {
+    if (tl && threadIdx.x == 0) {
+        const unsigned long long t = gtimer();
+        if (k == 1) {
+            atomicMax(&tl[1], t);
+        } else {
+            atomicMin(&tl[k], t);
+            if (k == 0) atomicMax(&tl[3], t);  // last CTA past its wait
+        }
+    }
+}
 
 // Block-wide reductions for blockDim.x a multiple of 32 (<= 1024).
 template <typename T, typename Op>

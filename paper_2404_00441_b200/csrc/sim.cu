@@ -20,6 +20,7 @@
 // and once per call a finalize kernel applies the hard-data overwrite and
 // crops the work grid (simulator.hpp:506-515).
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <exception>
@@ -78,7 +79,9 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
     pdl_trigger();
     const int slot = blockIdx.x;
     const Job jb = jobs[job0 + slot];
+    tl_mark(P.tl, 2);
     pdl_wait();
+    tl_mark(P.tl, 0);
     const int Tc = P.Tc, B = P.B, nc = P.hc * P.wc;
     const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc;
     int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
@@ -104,6 +107,7 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
         for (int ch = 0; ch < P.nch; ++ch)
             tm[ch * Tc * Tc + c] = in ? P.ti64[static_cast<size_t>(ch) * nc + sb] : 0.0;
     }
+    tl_mark(P.tl, 1);
 }
 
 __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
@@ -678,7 +682,7 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
 
     // 4. crop + optional stitch + paste (simulator.hpp:483-493)
     const int T = P.T;
-    uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
+    uint8_t* g = P.work ? P.work + static_cast<size_t>(jb.real) * P.wh * P.ww : nullptr;
     uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
     if (P.min_cut && jb.shape != kNone) {
         for (int e = tid; e < T * T; e += SEL_T) {
@@ -693,11 +697,11 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
             g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = outp[e];
             if (trace) trace[e] = outp[e];
         }
-    } else {
+    } else if (P.work || trace) {  // (no work grid: the source-block map is the realization)
         for (int e = tid; e < T * T; e += SEL_T) {
             const int r = e / T, c = e - r * T;
             const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
-            g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
+            if (P.work) g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
             if (trace) trace[e] = v;
         }
     }
@@ -715,31 +719,26 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
     }
 }
 
-// ----------------------------------------------------- warp-per-job select --
+// ------------------------------------------------ two-stage fast select --
 //
-// The common case (raw scoring, K <= kTcQ, tcgen05 summaries, no min-cut):
-// one warp per placement, no block-wide barriers.  Same contract as
-// select_paste_kernel: exact threshold from the per-tile top-Q summaries,
-// fp64 reference-order rescoring of the windows at or above it, reference
-// ranking, pick, paste.
-constexpr int WS_WARPS = 4;
-constexpr int WS_CB = 96;     // candidate buffer (flushed at WS_CB - 32)
-constexpr int WS_RS = 256;    // (window, run) partial sums per rescoring batch
-
-constexpr int WS_MAXTC = 64;   // template rows tabulated per warp
-
-constexpr int WS_LC = 256;   // (score, position) list of windows >= M_K
-
-struct WarpSel {
-    short4 rows[WS_MAXTC];  // (s, t0, t1, cell offset) of the mask rows, row-major
-    int lv[WS_LC];
-    int lp[WS_LC];
-    int cidx[WS_CB + kTcQ];
-    double ckey[WS_CB + kTcQ];
-    int tidx[kTcQ];
-    double tkey[kTcQ];
-    double rsum[WS_RS];
-};
+// The common case (raw scoring, K <= kTcQ, tcgen05 screen, no min-cut) runs
+// as two kernels per wave:
+//   select_scan_kernel  one warp per placement: the tile-maximum bound M_K,
+//                       the (score, position) list of windows >= M_K, the
+//                       exact K-th score S_K, the candidate positions;
+//   select_pick_kernel  one CTA per placement: every (candidate, mask run)
+//                       partial sum in parallel, the per-window fold in the
+//                       reference's order, the reference ranking, the pick
+//                       and the source-block map.
+// Placements whose list overflows go to select_bulk_kernel (or, without it,
+// are streamed by select_pick_kernel at threshold M_K).
+constexpr int SC_WARPS = 4;    // placements per scan CTA
+constexpr int SC_LC = 256;     // list / candidate capacity per placement
+constexpr int SC_TB = 8;       // qualifying tiles read per round trip
+constexpr int PK_T = 256;      // threads per placement in select_pick_kernel
+constexpr int PK_TMC = 1024;   // fp64 template values staged in shared memory (when they fit)
+constexpr int PK_RS = 2048;    // (window, run) partial sums per rescoring batch
+constexpr int PK_MAXTC = 64;   // template rows tabulated
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
@@ -749,142 +748,6 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// Rescore the buffered windows (one lane per (window, run) pair forms the
-// run's sum, one lane per window folds the run sums in row-major order --
-// the reference's operations in the reference's order) and merge them into
-// the running top-K by the reference ranking.
-template <int NWJ>
-__device__ __forceinline__ void job_sync() {
-    if constexpr (NWJ == 1)
-        __syncwarp();
-    else
-        __syncthreads();
-}
-
-// NWJ warps serve one job: control flow is replicated in every warp (same
-// data, same decisions, only warp 0 writes shared state), the parallel loops
-// run over all 32*NWJ threads.
-template <int NWJ>
-__device__ __forceinline__ void warp_flush(const SimParams& P, const double* tm, int R,
-                                           WarpSel& W, int& cnt, int& ntop, int K, int lane,
-                                           unsigned long long* tacc) {
-    constexpr int JT = 32 * NWJ;
-    const int jt = NWJ == 1 ? lane : static_cast<int>(threadIdx.x);
-    const bool writer = NWJ == 1 || threadIdx.x < 32;
-    const long long c0 = clock64();
-    if (P.stats && jt == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
-    const int rows = R / P.nch;
-    const int EB = max(1, WS_RS / R);
-    for (int e0 = 0; e0 < cnt; e0 += EB) {
-        const int ng = min(EB, cnt - e0);
-        // run sums: sum += ti*or left to right (matcher.hpp:72-76)
-        int e = 0, r = jt;
-        while (r >= R) {
-            r -= R;
-            ++e;
-        }
-        for (int w = jt; w < ng * R; w += JT) {
-            const int pos = W.cidx[e0 + e];
-            const int x = pos / P.out_w, y = pos - x * P.out_w;
-            const int ch = r / rows;
-            const short4 rw = W.rows[r - ch * rows];
-            const double* a = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
-                              static_cast<size_t>(x + rw.x) * P.wc + y + rw.y;
-            const double* b = tm + (ch * P.Tc + rw.x) * P.Tc + rw.y;
-            const int len = rw.z - rw.y;
-            double sum = 0.0;
-            for (int t0 = 0; t0 < len; t0 += 16) {
-                // all operands of (up to) 16 cells in flight at once, then the
-                // reference's sequential chain
-                double av[16], bv[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    av[i] = t0 + i < len ? __ldg(a + t0 + i) : 0.0;
-                    bv[i] = t0 + i < len ? __ldg(b + t0 + i) : 0.0;
-                }
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (t0 + i < len) sum = __dadd_rn(sum, __dmul_rn(av[i], bv[i]));
-            }
-            W.rsum[w] = sum;
-            r += JT;
-            while (r >= R) {
-                r -= R;
-                ++e;
-            }
-        }
-        job_sync<NWJ>();
-        // fold: acc += sum over runs in row-major order (matcher.hpp:77, 160-161)
-        for (int e = jt; e < ng; e += JT) {
-            double acc = 0.0;
-            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, W.rsum[e * R + r]);
-            W.ckey[e0 + e] = acc;
-        }
-        job_sync<NWJ>();
-    }
-    const long long c1 = clock64();
-    for (int e = jt; e < ntop; e += JT) {
-        W.ckey[cnt + e] = W.tkey[e];
-        W.cidx[cnt + e] = W.tidx[e];
-    }
-    job_sync<NWJ>();
-    const int n = cnt + ntop;
-    const int keep = min(K, n);
-    if (n <= 32) {
-        // one pass: every entry's rank under the reference ordering
-        const double mk = lane < n ? W.ckey[lane] : 0.0;
-        const int mi = lane < n ? W.cidx[lane] : INT_MAX;
-        int rank = 0;
-        for (int j = 0; j < n; ++j) {
-            const double ok = __shfl_sync(0xffffffffu, mk, j);
-            const int oi = __shfl_sync(0xffffffffu, mi, j);
-            rank += better(ok, oi, mk, mi);
-        }
-        job_sync<NWJ>();
-        if (writer && lane < n && rank < keep) {
-            W.tkey[rank] = mk;
-            W.tidx[rank] = mi;
-        }
-    } else {
-        for (int round = 0; round < keep; ++round) {
-            double bk = 0.0;
-            int bi = INT_MAX, bp = -1;
-            for (int e = lane; e < n; e += 32) {
-                const int ix = W.cidx[e];
-                if (ix >= 0 && (bp < 0 || better(W.ckey[e], ix, bk, bi))) {
-                    bk = W.ckey[e];
-                    bi = ix;
-                    bp = e;
-                }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
-                    bk = ok;
-                    bi = oi;
-                    bp = op;
-                }
-            }
-            job_sync<NWJ>();  // every warp has read this round's entries
-            if (writer && lane == 0) {
-                W.tkey[round] = bk;
-                W.tidx[round] = bi;
-                W.cidx[bp] = -1;
-            }
-            job_sync<NWJ>();
-        }
-    }
-    ntop = keep;
-    cnt = 0;
-    job_sync<NWJ>();
-    if (tacc && jt == 0) {
-        atomicAdd(&tacc[0], static_cast<unsigned long long>(c1 - c0));
-        atomicAdd(&tacc[1], static_cast<unsigned long long>(clock64() - c1));
-    }
 }
 
 // K-th largest (with multiplicity) of the union of the lanes' sorted top
@@ -952,15 +815,18 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
                                           int jt) {
     const int Tc = P.Tc;
     const int T = P.T;
-    uint8_t* g = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
     uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
+    // Without a work grid (source-block map mode) the realization is rebuilt
+    // from the map at finalize: only the map (and a requested trace) is written.
+    uint8_t* g = P.work ? P.work + static_cast<size_t>(jb.real) * P.wh * P.ww : nullptr;
     const int wpr = T >> 2;  // 32-bit words per row
     const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= JT && (JT % wpr) == 0;
-    if (vec4) {
+    if (!g && !trace) {
+    } else if (vec4) {
         // thread -> (row phase, word); every row it copies loaded in one round trip
         const int rpi = JT / wpr, rsub = jt / wpr, cw = jt - rsub * wpr;
         const uint8_t* srcp = P.ti + static_cast<size_t>(fr) * P.ti_w + fc + 4 * cw;
-        uint8_t* dstp = g + static_cast<size_t>(jb.top) * P.ww + jb.left + 4 * cw;
+        uint8_t* dstp = g ? g + static_cast<size_t>(jb.top) * P.ww + jb.left + 4 * cw : nullptr;
         for (int r0 = rsub; r0 < T; r0 += rpi * 32) {
             uint32_t v[32];  // every row this lane copies, loaded in one round trip
 #pragma unroll
@@ -972,7 +838,7 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
             for (int i = 0; i < 32; ++i) {
                 const int r = r0 + i * rpi;
                 if (r < T) {
-                    *reinterpret_cast<uint32_t*>(dstp + static_cast<size_t>(r) * P.ww) = v[i];
+                    if (g) *reinterpret_cast<uint32_t*>(dstp + static_cast<size_t>(r) * P.ww) = v[i];
                     if (trace) *reinterpret_cast<uint32_t*>(trace + r * T + 4 * cw) = v[i];
                 }
             }
@@ -993,7 +859,7 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
                 const int e = e0 + i * JT + jt;
                 const int r = e / T, c = e - r * T;
                 if (e < T * T) {
-                    g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v[i];
+                    if (g) g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v[i];
                     if (trace) trace[e] = v[i];
                 }
             }
@@ -1008,212 +874,741 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
     }
 }
 
-template <int NWJ>
-__global__ void __launch_bounds__(NWJ == 1 ? WS_WARPS * 32 : NWJ * 32, 1)
-    select_paste_warp_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
-    extern __shared__ __align__(16) unsigned char ws_raw[];
-    WarpSel* smem_ws = reinterpret_cast<WarpSel*>(ws_raw);
-    constexpr int JT = 32 * NWJ;
+struct ScanWarp {
+    int lv[SC_LC];
+    int lp[SC_LC];
+};
+
+// Warp-level scan of one placement (every lane of the warp calls it): the
+// tile-maximum bound M_K, the (score, position) list of windows >= M_K, the
+// exact K-th score S_K and the candidate positions (>= S_K) into out[].
+// Returns the candidate count, or -1 when the list overflowed (then every
+// window >= mk_out must be rescored -- a superset, still exact).
+__device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& W, int* out, int& mk_out,
+                                        long long* sclk) {
+    const int lane = threadIdx.x & 31;
+    const int K = P.K;
+    const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+    const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
+    // 1. M_K = K-th largest tile maximum (with multiplicity): a lower bound of
+    //    the K-th largest screen score S_K (the K best tiles each hold a
+    //    window scoring at least M_K).  Tile maxima stay in registers.
+    constexpr int kTM = 16;  // tile maxima per lane (512 tiles per placement)
+    const bool regs = P.ntiles <= 32 * kTM;  // else: stream the maxima (sorted per-lane top lists)
+    int tv[kTM];
+#pragma unroll
+    for (int i = 0; i < kTM; ++i) {
+        const int e = i * 32 + lane;
+        tv[i] = regs && e < P.ntiles ? tmx[e] : INT_MIN;
+    }
+    int mk = INT_MIN;
+    if (!regs) {
+        int top[kTcQ];
+#pragma unroll
+        for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
+        for (int e = lane; e < P.ntiles; e += 32) {
+            int v = tmx[e];
+            if (v > top[kTcQ - 1]) {
+#pragma unroll
+                for (int j = 0; j < kTcQ; ++j)
+                    if (v > top[j]) {
+                        const int t = top[j];
+                        top[j] = v;
+                        v = t;
+                    }
+            }
+        }
+        mk = warp_kth(top, K, lane);
+    } else {
+        int cur = INT_MAX, acc = 0;
+        for (int round = 0; round < K; ++round) {
+            int m = INT_MIN;
+#pragma unroll
+            for (int i = 0; i < kTM; ++i)
+                if (tv[i] < cur) m = max(m, tv[i]);
+            m = __reduce_max_sync(0xffffffffu, m);
+            int c = 0;
+#pragma unroll
+            for (int i = 0; i < kTM; ++i) c += tv[i] == m;
+            acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+            mk = m;
+            if (acc >= K || m == INT_MIN) break;
+            cur = m;
+        }
+    }
+    sclk[1] = clock64();
+    // 2. every window scoring >= M_K, from the tiles whose maximum reaches it,
+    //    into a (score, position) list; SC_TB tiles per round trip
+    int nl = 0;
+    bool over = false;
+#pragma unroll 1
+    for (int i0 = 0; i0 * 32 < P.ntiles && !over; ++i0) {
+        const int t0 = i0 * 32;
+        int mine = INT_MIN;
+        if (regs) {
+#pragma unroll
+            for (int i = 0; i < kTM; ++i)
+                if (i == i0) mine = tv[i];
+        } else if (t0 + lane < P.ntiles) {
+            mine = tmx[t0 + lane];
+        }
+        unsigned tiles = __ballot_sync(0xffffffffu, mine != INT_MIN && mine >= mk);
+        while (tiles && !over) {
+            int tl[SC_TB], v[SC_TB][4];
+#pragma unroll
+            for (int u = 0; u < SC_TB; ++u) {
+                tl[u] = -1;
+                if (tiles) {
+                    tl[u] = t0 + __ffs(tiles) - 1;
+                    tiles &= tiles - 1;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SC_TB; ++u) {
+                const int p0 = tl[u] * kTcTile + lane * 4;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
+                if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
+                    const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
+                    v[u][0] = a4.x;
+                    v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
+                    v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
+                    v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SC_TB; ++u)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool q = v[u][i] != INT_MIN && v[u][i] >= mk;  // scores are never INT_MIN
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (!bal) continue;
+                    if (nl + __popc(bal) > SC_LC) {
+                        over = true;
+                        continue;
+                    }
+                    if (q) {
+                        const int o = nl + __popc(bal & ((1u << lane) - 1));
+                        W.lv[o] = v[u][i];
+                        W.lp[o] = tl[u] * kTcTile + lane * 4 + i;
+                    }
+                    nl += __popc(bal);
+                }
+        }
+    }
+    __syncwarp();
+    sclk[2] = clock64();
+#ifdef CCW_DBG_STATS
+    if (P.stats) {
+        int nq = 0;
+        for (int t0 = 0; t0 < P.ntiles; t0 += 32)
+            nq += __popc(__ballot_sync(0xffffffffu, t0 + lane < P.ntiles && tmx[t0 + lane] >= mk));
+        if (lane == 0) {
+            atomicAdd(&P.stats[5], static_cast<unsigned long long>(nq));
+            atomicAdd(&P.stats[6], static_cast<unsigned long long>(nl));
+        }
+    }
+#endif
+    if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+    mk_out = mk;
+    if (over) {
+        if (lane == 0 && P.stats) atomicAdd(&P.stats[2], 1ull);
+        return -1;
+    }
+    // 3. exact S_K from the list (rounds of warp max with multiplicity)
+    int lvr[SC_LC / 32];
+#pragma unroll
+    for (int j2 = 0; j2 < SC_LC / 32; ++j2) {
+        const int e = j2 * 32 + lane;
+        lvr[j2] = e < nl ? W.lv[e] : INT_MIN;
+    }
+    int thr = mk, cur = INT_MAX, acc = 0;
+    for (int round = 0; round < K; ++round) {
+        int m = INT_MIN;
+#pragma unroll
+        for (int j2 = 0; j2 < SC_LC / 32; ++j2)
+            if (lvr[j2] < cur) m = max(m, lvr[j2]);
+        m = __reduce_max_sync(0xffffffffu, m);
+        int c = 0;
+#pragma unroll
+        for (int j2 = 0; j2 < SC_LC / 32; ++j2) c += lvr[j2] == m;
+        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+        thr = m;
+        if (acc >= K || m == INT_MIN) break;
+        cur = m;
+    }
+    sclk[3] = clock64();
+    // 4. the candidates: every listed window >= S_K
+    int* cd = out;
+    int cnt = 0;
+    for (int e0 = 0; e0 < nl; e0 += 32) {
+        const int e = e0 + lane;
+        const bool q = e < nl && W.lv[e] >= thr;
+        const unsigned bal = __ballot_sync(0xffffffffu, q);
+        if (q) cd[cnt + __popc(bal & ((1u << lane) - 1))] = W.lp[e];
+        cnt += __popc(bal);
+    }
+    return cnt;
+}
+
+// ncand[slot]: >= 0 candidates in cand[slot * SC_LC ..], -1 stream every window
+// >= cthr[slot] (no bulk kernel), -2 deferred to select_bulk_kernel.
+__global__ void __launch_bounds__(SC_WARPS * 32)
+    select_scan_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
+    __shared__ ScanWarp sw[SC_WARPS];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int jt = NWJ == 1 ? lane : static_cast<int>(threadIdx.x);
-    const bool writer = NWJ == 1 || wid == 0;
-    const int slot = NWJ == 1 ? blockIdx.x * WS_WARPS + wid : blockIdx.x;
+    const int slot = blockIdx.x * SC_WARPS + wid;
     pdl_trigger();
+    tl_mark(P.tl, 2);
     pdl_wait();
+    tl_mark(P.tl, 0);
     if (slot >= nj) return;
-    WarpSel& W = smem_ws[NWJ == 1 ? wid : 0];
+    long long sclk[5];
+    sclk[0] = clock64();
+    int mk = INT_MIN;
+    const int cnt = scan_job(P, slot, sw[wid], P.cand + static_cast<size_t>(slot) * SC_LC, mk, sclk);
+    if (lane == 0) {
+        if (cnt < 0) {
+            if (P.defer) {
+                // a large tie group: the bulk kernel rescores every window >= M_K
+                // (INT_MIN marks "not deferred"; scores never reach it)
+                P.defer[slot] = max(mk, INT_MIN + 1);
+                P.ncand[slot] = -2;
+            } else {
+                P.cthr[slot] = mk;
+                P.ncand[slot] = -1;
+            }
+        } else {
+            if (P.defer) P.defer[slot] = INT_MIN;
+            P.ncand[slot] = cnt;
+        }
+        if (cnt >= 0 && P.stats && P.tl) {  // phase clocks with the debug timeline
+            sclk[4] = clock64();
+            for (int q = 0; q < 4; ++q) atomicAdd(&P.stats[8 + q], static_cast<unsigned long long>(sclk[q + 1] - sclk[q]));
+        }
+    }
+    tl_mark(P.tl, 1);
+}
+
+struct PickSmem {
+    double tm[PK_TMC];
+    double rsum[PK_RS];
+    double key[SC_LC + kTcQ];
+    int cidx[SC_LC + kTcQ];
+    short4 rows[PK_MAXTC];
+    double tkey[kTcQ];
+    int tidx[kTcQ];
+    double rk[PK_T / 32];
+    int ri[PK_T / 32], rp[PK_T / 32];
+    int wc[PK_T / 32];
+    int misc[4];
+};
+
+// Rescore S.cidx[0, cnt) (fp64, the reference's operations in the reference's
+// order: run sums left to right, matcher.hpp:72-76; runs folded row-major,
+// matcher.hpp:77, 160-161) and merge them with the running top-K (S.tkey /
+// S.tidx, ntop entries) by the reference ranking.
+__device__ __forceinline__ void pick_batch(const SimParams& P, PickSmem& S, const double* tmS, int R,
+                                           int cnt, int& ntop, int K) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int rows = R / P.nch;
+    const int EB = max(1, PK_RS / R);
+    if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+    for (int e0 = 0; e0 < cnt; e0 += EB) {
+        const int ng = min(EB, cnt - e0);
+        for (int w = tid; w < ng * R; w += PK_T) {
+            const int e = w / R, r = w - e * R;
+            const int pos = S.cidx[e0 + e];
+            const int x = pos / P.out_w, y = pos - x * P.out_w;
+            const int ch = r / rows;
+            const short4 rw = S.rows[r - ch * rows];
+            const double* a = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
+                              static_cast<size_t>(x + rw.x) * P.wc + y + rw.y;
+            const double* b = tmS + (ch * P.Tc + rw.x) * P.Tc + rw.y;
+            const int len = rw.z - rw.y;
+            double sum = 0.0;
+            for (int t0 = 0; t0 < len; t0 += 16) {
+                double av[16];  // the run's TI operands in one round trip
+#pragma unroll
+                for (int i = 0; i < 16; ++i) av[i] = t0 + i < len ? __ldg(a + t0 + i) : 0.0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (t0 + i < len) sum = __dadd_rn(sum, __dmul_rn(av[i], b[t0 + i]));
+            }
+            S.rsum[w] = sum;
+        }
+        __syncthreads();
+        for (int e = tid; e < ng; e += PK_T) {
+            double acc = 0.0;
+            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, S.rsum[e * R + r]);
+            S.key[e0 + e] = acc;
+        }
+        __syncthreads();
+    }
+    // merge: the batch plus the running top-K
+    for (int e = tid; e < ntop; e += PK_T) {
+        S.key[cnt + e] = S.tkey[e];
+        S.cidx[cnt + e] = S.tidx[e];
+    }
+    __syncthreads();
+    const int n = cnt + ntop;
+    const int keep = min(K, n);
+    if (n <= 32) {
+        if (wid == 0) {  // every entry's rank in one pass
+            const double mk = lane < n ? S.key[lane] : 0.0;
+            const int mi = lane < n ? S.cidx[lane] : INT_MAX;
+            int rank = 0;
+            for (int j = 0; j < n; ++j) {
+                const double ok = __shfl_sync(0xffffffffu, mk, j);
+                const int oi = __shfl_sync(0xffffffffu, mi, j);
+                rank += better(ok, oi, mk, mi);
+            }
+            if (lane < n && rank < keep) {
+                S.tkey[rank] = mk;
+                S.tidx[rank] = mi;
+            }
+        }
+    } else {
+        for (int round = 0; round < keep; ++round) {
+            double bk = 0.0;
+            int bi = INT_MAX, bp = -1;
+            for (int e = tid; e < n; e += PK_T) {
+                const int ix = S.cidx[e];
+                if (ix >= 0 && (bp < 0 || better(S.key[e], ix, bk, bi))) {
+                    bk = S.key[e];
+                    bi = ix;
+                    bp = e;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
+                    bk = ok;
+                    bi = oi;
+                    bp = op;
+                }
+            }
+            if (lane == 0) {
+                S.rk[wid] = bk;
+                S.ri[wid] = bi;
+                S.rp[wid] = bp;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < PK_T / 32; ++w)
+                    if (S.rp[w] >= 0 && (bp < 0 || better(S.rk[w], S.ri[w], bk, bi))) {
+                        bk = S.rk[w];
+                        bi = S.ri[w];
+                        bp = S.rp[w];
+                    }
+                S.tkey[round] = bk;
+                S.tidx[round] = bi;
+                S.cidx[bp] = -1;
+            }
+            __syncthreads();
+        }
+    }
+    ntop = keep;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(PK_T, 3)
+    select_pick_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
+    __shared__ PickSmem S;
+    const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_trigger();
+    tl_mark(P.tl, 2);
+    pdl_wait();
+    tl_mark(P.tl, 0);
+    if (slot >= nj) return;
     const int gj = job0 + slot;
     const Job jb = jobs[gj];
     const int Tc = P.Tc;
+    long long pclk0 = clock64(), pclk1 = 0, pclk2 = 0;
     int fr, fc;
-    unsigned long long* tacc = P.stats ? P.stats + 8 : nullptr;  // phase clocks
-    long long clk0 = clock64(), clk1 = 0, clk2 = 0, clk3 = 0;
     if (jb.shape == kNone) {
         fr = jb.fr;
         fc = jb.fc;
     } else {
+        const int n = P.ncand[slot];
+        if (n == -2) return;  // select_bulk_kernel
         const int K = P.K;
-        const int32_t* sc = P.scores ? P.scores + static_cast<size_t>(slot) * P.sld : nullptr;
-        const double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
-        const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
-        // 1. M_K = K-th largest tile maximum (with multiplicity): a lower bound
-        //    of the K-th largest screen score S_K (the K best tiles each hold
-        //    a window scoring at least M_K).
-        int top[kTcQ];
-#pragma unroll
-        for (int i = 0; i < kTcQ; ++i) top[i] = INT_MIN;
-        for (int e0 = 0; e0 < P.ntiles; e0 += 32 * 16) {
-            int vb[16];  // up to 512 tile maxima per round trip
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int e = e0 + i * 32 + lane;
-                vb[i] = e < P.ntiles ? tmx[e] : INT_MIN;
-            }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                int v = vb[i];
-                if (v > top[kTcQ - 1]) {
-#pragma unroll
-                    for (int j = 0; j < kTcQ; ++j)
-                        if (v > top[j]) {
-                            const int t = top[j];
-                            top[j] = v;
-                            v = t;
-                        }
-                }
-            }
+        // stage the fp64 template (matcher.hpp:44-61 order) and the mask rows
+        const double* tmg = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+        const int ntm = P.nch * Tc * Tc;
+        const double* tmS = tmg;
+        if (ntm <= PK_TMC) {
+            for (int e = tid; e < ntm; e += PK_T) cp_async8(&S.tm[e], tmg + e);
+            tmS = S.tm;
         }
-        const int mk = warp_kth(top, K, lane);
-        if (P.stats && jt == 0) atomicAdd(&P.stats[1], 1ull);
-        clk1 = clock64();
-        int R = 0;
+        int nr = 0;
         for (int s0 = 0; s0 < Tc; s0 += 32) {
             const int s = s0 + lane;
             int t0 = 0, t1 = 0;
             if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
             const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
-            if (writer && t1 > t0) W.rows[R + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
-            R += __popc(m);
+            if (wid == 0 && t1 > t0) S.rows[nr + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
+            nr += __popc(m);
         }
-        job_sync<NWJ>();
-        R *= P.nch;
-        // 2. every window scoring >= M_K, from the tiles whose maximum reaches
-        //    it, into a (score, position) list; four tiles per round trip
-        int nl = 0;
-        bool over = false;
-        for (int t0 = 0; t0 < P.ntiles && !over; t0 += 32) {
-            const int tt = t0 + lane;
-            unsigned tiles = __ballot_sync(0xffffffffu, tt < P.ntiles && tmx[tt] >= mk);
-            while (tiles && !over) {
-                int tl[4], v[4][4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    tl[u] = -1;
-                    if (tiles) {
-                        tl[u] = t0 + __ffs(tiles) - 1;
-                        tiles &= tiles - 1;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int p0 = tl[u] * kTcTile + lane * 4;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
-                    if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
-                        const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
-                        v[u][0] = a4.x;
-                        v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
-                        v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
-                        v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const bool q = v[u][i] != INT_MIN && v[u][i] >= mk;  // scores are never INT_MIN
-                        const unsigned bal = __ballot_sync(0xffffffffu, q);
-                        if (!bal) continue;
-                        if (nl + __popc(bal) > WS_LC) {
-                            over = true;
-                            continue;
-                        }
-                        if (writer && q) {
-                            const int o = nl + __popc(bal & ((1u << lane) - 1));
-                            W.lv[o] = v[u][i];
-                            W.lp[o] = tl[u] * kTcTile + lane * 4 + i;
-                        }
-                        nl += __popc(bal);
-                    }
-            }
-        }
-        job_sync<NWJ>();
-        int thr = mk;  // overflow: rescore everything >= M_K (a superset: still exact)
-        if (over && P.stats && jt == 0) atomicAdd(&P.stats[2], 1ull);
-        if (!over) {
-            // exact S_K from the list (K rounds of warp max with multiplicity)
-            int cur = INT_MAX, acc = 0;
-            for (int round = 0; round < K; ++round) {
-                int m = INT_MIN;
-                for (int e = lane; e < nl; e += 32)
-                    if (W.lv[e] < cur) m = max(m, W.lv[e]);
-                for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-                int c = 0;
-                for (int e = lane; e < nl; e += 32) c += W.lv[e] == m;
-                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-                acc += c;
-                thr = m;
-                if (acc >= K || m == INT_MIN) break;
-                cur = m;
-            }
-        } else if (P.defer) {
-            // a large tie group: the bulk kernel rescores every window >= M_K
-            // (INT_MIN marks "not deferred"; scores never reach it, so INT_MIN + 1 filters alike)
-            if (jt == 0) P.defer[slot] = max(mk, INT_MIN + 1);
-            return;  // uniform across the job's warps
-        }
-        if (P.defer && jt == 0) P.defer[slot] = INT_MIN;
-        // 3. candidates (>= S_K) -> fp64 rescoring in the reference's order
-        int cnt = 0, ntop = 0;
-        if (!over) {
-            for (int e0 = 0; e0 < nl; e0 += 32) {
-                const int e = e0 + lane;
-                const bool q = e < nl && W.lv[e] >= thr;
-                const unsigned bal = __ballot_sync(0xffffffffu, q);
-                if (!bal) continue;
-                if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
-                const int pe = q ? W.lp[e] : 0;
-                job_sync<NWJ>();
-                if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = pe;
-                cnt += __popc(bal);
-                job_sync<NWJ>();
-            }
+        const int R = nr * P.nch;
+        int ntop = 0;
+        if (n >= 0) {
+            const int* cd = P.cand + static_cast<size_t>(slot) * SC_LC;
+            for (int e = tid; e < n; e += PK_T) S.cidx[e] = cd[e];
+            cp_async_wait_all();
+            __syncthreads();
+            pclk1 = clock64();
+            pick_batch(P, S, tmS, R, n, ntop, K);
+            pclk2 = clock64();
         } else {
-            // no bulk kernel: stream the tiles again with threshold M_K
-            for (int t0 = 0; t0 < P.ntiles; t0 += 32) {
-                const int tt = t0 + lane;
-                unsigned tiles = __ballot_sync(0xffffffffu, tt < P.ntiles && tmx[tt] >= thr);
-                while (tiles) {
-                    const int t = t0 + __ffs(tiles) - 1;
-                    tiles &= tiles - 1;
-                    const int p0 = t * kTcTile + lane * 4;
-                    int v[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) v[i] = p0 + i < P.npos ? sc[p0 + i] : INT_MIN;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const bool q = v[i] != INT_MIN && v[i] >= thr;
-                        const unsigned bal = __ballot_sync(0xffffffffu, q);
-                        if (!bal) continue;
-                        if (cnt + 32 > WS_CB) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
-                        if (writer && q) W.cidx[cnt + __popc(bal & ((1u << lane) - 1))] = p0 + i;
-                        cnt += __popc(bal);
-                        job_sync<NWJ>();
-                    }
+            // list overflow without the bulk kernel: every window >= M_K, in batches
+            const int thr = P.cthr[slot];
+            const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+            const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
+            cp_async_wait_all();
+            int cnt = 0;
+            for (int t = 0; t < P.ntiles; ++t) {
+                if (tmx[t] < thr) continue;  // uniform
+                const int p = t * kTcTile + tid;
+                const bool q = tid < kTcTile && p < P.npos && sc[p] >= thr;
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (lane == 0) S.wc[wid] = __popc(bal);
+                __syncthreads();
+                int off = 0, tot = 0;
+                for (int w = 0; w < PK_T / 32; ++w) {
+                    off += w < wid ? S.wc[w] : 0;
+                    tot += S.wc[w];
                 }
+                if (cnt + tot > SC_LC) {
+                    pick_batch(P, S, tmS, R, cnt, ntop, K);
+                    cnt = 0;
+                }
+                if (q) S.cidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
+                cnt += tot;
+                __syncthreads();
             }
+            if (cnt > 0) pick_batch(P, S, tmS, R, cnt, ntop, K);
         }
-        if (cnt > 0) warp_flush<NWJ>(P, tm, R, W, cnt, ntop, K, lane, tacc);
-        clk2 = clock64();
-        // 3. choose (matcher.hpp:207-241)
-        const int pos = choose_pick(P, jb, W.tidx, ntop, lane);
+        // choose (matcher.hpp:207-241)
+        if (wid == 0) {
+            const int pos = choose_pick(P, jb, S.tidx, ntop, lane);
+            if (lane == 0) S.misc[0] = pos;
+        }
+        __syncthreads();
+        const int pos = S.misc[0];
         fr = (pos / P.out_w) << P.J;
         fc = (pos % P.out_w) << P.J;
-        clk3 = clock64();
     }
-    // 4. paste (simulator.hpp:483-493) + source-block map
-    paste_job<JT>(P, jb, gj, fr, fc, jt);
-    if (jt == 0) {
+    // source-block map (+ optional trace), simulator.hpp:483-493
+    paste_job<PK_T>(P, jb, gj, fr, fc, tid);
+    if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
-        if (tacc && clk1) {
-            const long long clk4 = clock64();
-            atomicAdd(&tacc[2], static_cast<unsigned long long>(clk1 - clk0));
-            atomicAdd(&tacc[3], static_cast<unsigned long long>(clk2 - clk1));
-            atomicAdd(&tacc[4], static_cast<unsigned long long>(clk3 - clk2));
-            atomicAdd(&tacc[5], static_cast<unsigned long long>(clk4 - clk3));
+        if (P.tl && P.stats && pclk2) {
+            atomicAdd(&P.stats[12], static_cast<unsigned long long>(pclk1 - pclk0));
+            atomicAdd(&P.stats[13], static_cast<unsigned long long>(pclk2 - pclk1));
+            atomicAdd(&P.stats[4], static_cast<unsigned long long>(clock64() - pclk2));
         }
     }
+    tl_mark(P.tl, 1);
+}
+
+// ---------------------------------------------------- fused fast select --
+//
+// One 128-thread CTA per placement: warp 0 scans (scan_job) while warps 1-3
+// stage the fp64 template, the mask rows and the rescoring work items; then
+// every (candidate, run group) item is rescored by one thread -- a run group
+// is up to FS_G cells of consecutive mask rows of one channel with the same
+// column run, whose operands are loaded in one round trip and whose run sums
+// are formed left to right (matcher.hpp:72-76); per-window folds in
+// row-major run order (matcher.hpp:77, 160-161); reference ranking; pick;
+// source-block map.
+constexpr int FS_T = 128;
+constexpr int FS_G = 16;       // cells per rescoring item
+constexpr int FS_MAXG = 512;   // run groups per placement
+constexpr int FS_RS = 1536;    // (window, run) partial sums per batch
+
+struct FastSmem {
+    double tm[PK_TMC];
+    double rsum[FS_RS];
+    double key[SC_LC + kTcQ];
+    int cidx[SC_LC + kTcQ];
+    ScanWarp sw;
+    int4 grp[FS_MAXG];      // (channel, first row-table index, rows, t0 << 8 | len)
+    short4 rows[PK_MAXTC];  // mask rows (s, t0, t1, -)
+    double tkey[kTcQ];
+    int tidx[kTcQ];
+    double rk[FS_T / 32];
+    int ri[FS_T / 32], rp[FS_T / 32], wc[FS_T / 32];
+    int misc[8];
+};
+
+// Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
+__device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, const double* tmS, int nr,
+                                           int ngrp, int cnt, int& ntop, int K) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int R = nr * P.nch;
+    const int EB = max(1, FS_RS / R);
+    const size_t plane = static_cast<size_t>(P.hc) * P.wc;
+    if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+    for (int e0 = 0; e0 < cnt; e0 += EB) {
+        const int ng = min(EB, cnt - e0);
+        for (int it = tid; it < ng * ngrp; it += FS_T) {
+            const int e = it / ngrp, g = it - e * ngrp;
+            const int4 G = S.grp[g];
+            const int ch = G.x, k0 = G.y, nk = G.z, t0 = G.w >> 8, len = G.w & 255;
+            const int pos = S.cidx[e0 + e];
+            const int x = pos / P.out_w, y = pos - x * P.out_w;
+            const double* base = P.ti64 + ch * plane + static_cast<size_t>(x) * P.wc + y + t0;
+            const double* tb = tmS + ch * P.Tc * P.Tc + t0;
+            double* rs = S.rsum + e * R + ch * nr + k0;
+            if (len > FS_G) {  // one long run (nk == 1), FS_G operands per round trip
+                const int s = S.rows[k0].x;
+                const double* a = base + static_cast<size_t>(s) * P.wc;
+                const double* b = tb + s * P.Tc;
+                double sum = 0.0;
+                for (int c0 = 0; c0 < len; c0 += FS_G) {
+                    double av[FS_G];
+#pragma unroll
+                    for (int c = 0; c < FS_G; ++c) av[c] = c0 + c < len ? __ldg(a + c0 + c) : 0.0;
+#pragma unroll
+                    for (int c = 0; c < FS_G; ++c)
+                        if (c0 + c < len) sum = __dadd_rn(sum, __dmul_rn(av[c], b[c0 + c]));
+                }
+                rs[0] = sum;
+                continue;
+            }
+            double av[FS_G];
+            {
+                int kk = 0, t = 0;
+#pragma unroll
+                for (int c = 0; c < FS_G; ++c) {
+                    av[c] = kk < nk ? __ldg(base + static_cast<size_t>(S.rows[k0 + kk].x) * P.wc + t) : 0.0;
+                    if (++t == len) {
+                        t = 0;
+                        ++kk;
+                    }
+                }
+            }
+            double sum = 0.0;
+            int kk = 0, t = 0;
+#pragma unroll
+            for (int c = 0; c < FS_G; ++c) {
+                if (kk < nk) {
+                    sum = __dadd_rn(sum, __dmul_rn(av[c], tb[S.rows[k0 + kk].x * P.Tc + t]));
+                    if (++t == len) {
+                        rs[kk] = sum;
+                        sum = 0.0;
+                        t = 0;
+                        ++kk;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < ng; e += FS_T) {
+            double acc = 0.0;
+            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, S.rsum[e * R + r]);
+            S.key[e0 + e] = acc;
+        }
+        __syncthreads();
+    }
+    // merge: the batch plus the running top-K (reference ranking)
+    for (int e = tid; e < ntop; e += FS_T) {
+        S.key[cnt + e] = S.tkey[e];
+        S.cidx[cnt + e] = S.tidx[e];
+    }
+    __syncthreads();
+    const int n = cnt + ntop;
+    const int keep = min(K, n);
+    if (n <= 32) {
+        if (wid == 0) {
+            const double mk = lane < n ? S.key[lane] : 0.0;
+            const int mi = lane < n ? S.cidx[lane] : INT_MAX;
+            int rank = 0;
+            for (int j = 0; j < n; ++j) {
+                const double ok = __shfl_sync(0xffffffffu, mk, j);
+                const int oi = __shfl_sync(0xffffffffu, mi, j);
+                rank += better(ok, oi, mk, mi);
+            }
+            if (lane < n && rank < keep) {
+                S.tkey[rank] = mk;
+                S.tidx[rank] = mi;
+            }
+        }
+    } else {
+        for (int round = 0; round < keep; ++round) {
+            double bk = 0.0;
+            int bi = INT_MAX, bp = -1;
+            for (int e = tid; e < n; e += FS_T) {
+                const int ix = S.cidx[e];
+                if (ix >= 0 && (bp < 0 || better(S.key[e], ix, bk, bi))) {
+                    bk = S.key[e];
+                    bi = ix;
+                    bp = e;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
+                    bk = ok;
+                    bi = oi;
+                    bp = op;
+                }
+            }
+            if (lane == 0) {
+                S.rk[wid] = bk;
+                S.ri[wid] = bi;
+                S.rp[wid] = bp;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < FS_T / 32; ++w)
+                    if (S.rp[w] >= 0 && (bp < 0 || better(S.rk[w], S.ri[w], bk, bi))) {
+                        bk = S.rk[w];
+                        bi = S.ri[w];
+                        bp = S.rp[w];
+                    }
+                S.tkey[round] = bk;
+                S.tidx[round] = bi;
+                S.cidx[bp] = -1;
+            }
+            __syncthreads();
+        }
+    }
+    ntop = keep;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(FS_T, 4)
+    select_fast_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
+    __shared__ FastSmem S;
+    const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_trigger();
+    tl_mark(P.tl, 2);
+    pdl_wait();
+    tl_mark(P.tl, 0);
+    if (slot >= nj) return;
+    const int gj = job0 + slot;
+    const Job jb = jobs[gj];
+    const int Tc = P.Tc;
+    int fr, fc;
+    if (jb.shape == kNone) {
+        fr = jb.fr;
+        fc = jb.fc;
+    } else {
+        const int K = P.K;
+        const double* tmg = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+        const int ntm = P.nch * Tc * Tc;
+        const double* tmS = ntm <= PK_TMC ? S.tm : tmg;
+        int mk = INT_MIN;
+        if (wid == 0) {
+            long long sclk[5];
+            sclk[0] = clock64();
+            const int n = scan_job(P, slot, S.sw, S.cidx, mk, sclk);
+            if (lane == 0) {
+                S.misc[0] = n;
+                S.misc[1] = mk;
+            }
+        } else {
+            // stage the template (matcher.hpp:44-61 order), the mask rows and the run groups
+            if (ntm <= PK_TMC)
+                for (int e = tid - 32; e < ntm; e += FS_T - 32) cp_async8(&S.tm[e], tmg + e);
+            if (wid == 1) {
+                int nr = 0;
+                for (int s0 = 0; s0 < Tc; s0 += 32) {
+                    const int s = s0 + lane;
+                    int t0 = 0, t1 = 0;
+                    if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+                    const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
+                    if (t1 > t0) S.rows[nr + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
+                    nr += __popc(m);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    int ng = 0;
+                    for (int ch = 0; ch < P.nch; ++ch) {
+                        int k = 0;
+                        while (k < nr) {
+                            const int t0 = S.rows[k].y, len = S.rows[k].z - S.rows[k].y;
+                            int nk = 1;
+                            while (k + nk < nr && S.rows[k + nk].y == t0 && S.rows[k + nk].z - t0 == len &&
+                                   (nk + 1) * len <= FS_G)
+                                ++nk;
+                            if (len > FS_G) {  // a long run stays one item (one sequential sum)
+                                if (ng < FS_MAXG) S.grp[ng++] = make_int4(ch, k, 1, (t0 << 8) | len);
+                                nk = 1;
+                            } else if (ng < FS_MAXG) {
+                                S.grp[ng++] = make_int4(ch, k, nk, (t0 << 8) | len);
+                            }
+                            k += nk;
+                        }
+                    }
+                    S.misc[2] = nr;
+                    S.misc[3] = ng;
+                }
+            }
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        const int n = S.misc[0], nr = S.misc[2], ngrp = S.misc[3];
+        mk = S.misc[1];
+        int ntop = 0;
+        if (n < 0 && P.defer) {  // a large tie group: the bulk kernel rescores every window >= M_K
+            if (tid == 0) P.defer[slot] = max(mk, INT_MIN + 1);  // (INT_MIN marks "not deferred")
+            return;
+        }
+        if (P.defer && tid == 0) P.defer[slot] = INT_MIN;
+        if (n >= 0) {
+            fast_batch(P, S, tmS, nr, ngrp, n, ntop, K);
+        } else {
+            // list overflow without the bulk kernel: every window >= M_K, in batches
+            const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+            const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
+            int cnt = 0;
+            for (int t = 0; t < P.ntiles; ++t) {
+                if (tmx[t] < mk) continue;  // uniform
+                const int p = t * kTcTile + tid;  // FS_T == kTcTile
+                const bool q = p < P.npos && sc[p] >= mk;
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (lane == 0) S.wc[wid] = __popc(bal);
+                __syncthreads();
+                int off = 0, tot = 0;
+                for (int w = 0; w < FS_T / 32; ++w) {
+                    off += w < wid ? S.wc[w] : 0;
+                    tot += S.wc[w];
+                }
+                __syncthreads();
+                if (cnt + tot > SC_LC) {
+                    fast_batch(P, S, tmS, nr, ngrp, cnt, ntop, K);
+                    cnt = 0;
+                }
+                if (q) S.cidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
+                cnt += tot;
+                __syncthreads();
+            }
+            if (cnt > 0) fast_batch(P, S, tmS, nr, ngrp, cnt, ntop, K);
+        }
+        // choose (matcher.hpp:207-241)
+        if (wid == 0) {
+            const int pos = choose_pick(P, jb, S.tidx, ntop, lane);
+            if (lane == 0) S.misc[4] = pos;
+        }
+        __syncthreads();
+        const int pos = S.misc[4];
+        fr = (pos / P.out_w) << P.J;
+        fc = (pos % P.out_w) << P.J;
+    }
+    paste_job<FS_T>(P, jb, gj, fr, fc, tid);
+    if (tid == 0) {
+        P.chosen[2 * gj] = fr;
+        P.chosen[2 * gj + 1] = fc;
+    }
+    tl_mark(P.tl, 1);
 }
 
 // ------------------------------------------------------- bulk tie select --
@@ -1566,18 +1961,31 @@ __global__ void hd_scatter_kernel(const int32_t* __restrict__ hd, int n_hd, uint
 
 // Hard-data overwrite with pre-overwrite mismatch count, then the crop to
 // the simulation grid (simulator.hpp:506-515).
+// Without a work grid the cell is read from the TI through the source-block
+// map (every work block is a verbatim copy of the TI block it was last pasted
+// from).
 __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww,
+                                const int32_t* __restrict__ src, int B, int J, int swc,
+                                const uint8_t* __restrict__ ti, int ti_w, int wc,
                                 const uint8_t* __restrict__ hd, int sg_h, int sg_w,
                                 uint8_t* __restrict__ out, int* mism) {
     pdl_wait();
     const size_t n = static_cast<size_t>(sg_h) * sg_w;
     const int r = blockIdx.y;
-    const uint8_t* g = work + static_cast<size_t>(r) * wh * ww;
+    const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
+    const int32_t* sm = src ? src + static_cast<size_t>(r) * (wh >> J) * swc : nullptr;
     int local = 0;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int y = static_cast<int>(e / sg_w), x = static_cast<int>(e - static_cast<size_t>(y) * sg_w);
-        uint8_t v = g[static_cast<size_t>(y) * ww + x];
+        uint8_t v;
+        if (g) {
+            v = g[static_cast<size_t>(y) * ww + x];
+        } else {
+            const int b = sm[static_cast<size_t>(y >> J) * swc + (x >> J)];
+            const int by = b / wc, bx = b - by * wc;
+            v = ti[static_cast<size_t>((by << J) + (y & (B - 1))) * ti_w + (bx << J) + (x & (B - 1))];
+        }
         if (hd) {
             const uint8_t h = hd[static_cast<size_t>(y) * ww + x];
             if (h != kNoDatum) {
@@ -1825,8 +2233,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     Job* d_jobs = ctx->jobs.as<Job>(total_jobs);
     CCW_CUDA(cudaMemcpyAsync(d_jobs, flat, sizeof(Job) * total_jobs, cudaMemcpyHostToDevice, st));
     const size_t plane = static_cast<size_t>(wh) * ww;
-    uint8_t* d_work = ctx->work.as<uint8_t>(plane * n_real);
-    CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
+    // the work grid exists only with min-cut (seams read the grid); otherwise
+    // the source-block map is the realization until finalize
+    uint8_t* d_work = nullptr;
+    if (cfg.min_cut) {
+        d_work = ctx->work.as<uint8_t>(plane * n_real);
+        CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
+    }
     uint8_t* d_hd = nullptr;
     const int32_t* P_hd_off = nullptr;
     const uint32_t* P_hd_ent = nullptr;
@@ -1920,12 +2333,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.src = d_src;
     P.swc = swc;
     const bool warp_select = use_tc && Kp <= kTcQ && !cfg.min_cut && cfg.scoring == 0 &&
-                             ti->nch * Tc <= WS_RS && Tc <= WS_MAXTC;
+                             ti->nch * Tc <= FS_MAXG && Tc <= PK_MAXTC;
     P.kpad = kpad;
     P.ntiles = ntiles;
     P.stats = d_stats;
     P.im2col = d_x;
-    // list mode: the screen keeps per-tile (score, position) lists instead of score rows
     // bulk tie select: largest window block whose apex tile fits the shared-memory budget
     size_t bulk_smem = 0;
     if (warp_select && !getenv("CCW_NOBULK")) {
@@ -1954,8 +2366,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.bulk_keys = ctx->bulk_keys.as<double>(G * maxj * BK_SMAX * kTcQ);
         P.bulk_idx = ctx->bulk_idx.as<int>(G * maxj * BK_SMAX * kTcQ);
     }
-    P.bulk_min = bulk_smem ? 2 * WS_CB : 0;
-    if (const char* e = getenv("CCW_BULK_EST")) P.bulk_min = atoi(e);
+    const bool split_select = getenv("CCW_SPLIT_SELECT") != nullptr;  // scan + pick kernels (r1 A/B)
+    if (warp_select) {
+        P.cand = ctx->cand.as<int>(G * maxj * SC_LC);
+        P.ncand = ctx->ncand.as<int>(G * maxj);
+        P.cthr = ctx->cthr.as<int>(G * maxj);
+    }
     if (bulk_smem)
         CCW_CUDA(cudaFuncSetAttribute(select_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(bulk_smem)));
@@ -1967,6 +2383,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
         GP[g].tmax = d_tmax ? d_tmax + g * maxj * ntiles : nullptr;
         GP[g].defer = d_defer ? d_defer + g * maxj : nullptr;
+        if (warp_select) {
+            GP[g].cand = P.cand + g * maxj * SC_LC;
+            GP[g].ncand = P.ncand + g * maxj;
+            GP[g].cthr = P.cthr + g * maxj;
+        }
         if (d_defer) {
             GP[g].bulk_sync = P.bulk_sync + 2 * g * maxj;
             GP[g].bulk_keys = P.bulk_keys + g * maxj * BK_SMAX * kTcQ;
@@ -1982,11 +2403,6 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   static_cast<int>(ccf_smem)));
     CCW_CUDA(cudaFuncSetAttribute(select_paste_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sel_smem)));
-    int selw = 2;  // warps per placement in the select kernel (measured best, r1)
-    if (const char* e = getenv("CCW_SELW")) selw = atoi(e) <= 1 ? 1 : (atoi(e) == 2 ? 2 : 4);
-    CCW_CUDA(cudaFuncSetAttribute(select_paste_warp_kernel<1>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(WarpSel) * WS_WARPS)));
 
     unsigned long long* d_probe = nullptr;
     if (getenv("CCW_TC_PROBE")) {
@@ -2014,17 +2430,39 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
+    // debug timeline: [resident, past-wait, end] per launch
+    const bool want_tl = getenv("CCW_TIMELINE") != nullptr;
+    std::vector<std::array<int, 3>> tl_tag;  // (wave, group, kind 0 prep / 1 ccf / 2 select)
+    unsigned long long* d_tl = nullptr;
+    const size_t tl_cap = static_cast<size_t>(max_key + 1) * G * 4 * 8;
+    if (want_tl) {
+        d_tl = reinterpret_cast<unsigned long long*>(ctx->ops_c.get(tl_cap * 4 * sizeof(unsigned long long)));
+        std::vector<unsigned long long> init(tl_cap * 4);
+        for (size_t i = 0; i < tl_cap; ++i) {
+            init[4 * i] = ~0ull;
+            init[4 * i + 1] = 0;
+            init[4 * i + 2] = ~0ull;
+            init[4 * i + 3] = 0;
+        }
+        CCW_CUDA(cudaMemcpy(d_tl, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    }
+    auto tl_next = [&](int w, int g, int kind) -> unsigned long long* {
+        if (!d_tl || tl_tag.size() >= tl_cap) return nullptr;
+        tl_tag.push_back({w, g, kind});
+        return d_tl + 4 * (tl_tag.size() - 1);
+    };
     int64_t launches = 0, ccf_launches = 0;
     double ccf_flop = 0, ccf_flop_ref = 0, ccf_mma_flop = 0;
     const dim3 ccf_grid_xy((out_w + CCF_TY - 1) / CCF_TY, (out_h + CCF_TX - 1) / CCF_TX);
     for (int w = 0; w <= max_key; ++w) {
         for (int g = 0; g < G; ++g) {
             cudaStream_t gs = ctx->gstreams[g];
-            const SimParams& Q = GP[g];
+            SimParams Q = GP[g];
             for (size_t j0 = wave_off[g][w]; j0 < wave_off[g][w + 1]; j0 += maxj) {
                 const int nj = static_cast<int>(std::min(maxj, wave_off[g][w + 1] - j0));
                 const bool first_wave = flat[j0].shape == kNone;
                 if (!first_wave) {
+                    Q.tl = tl_next(w, g, 0);
                     if (skip_prep) {
                     } else if (d_src)
                         launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
@@ -2042,7 +2480,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         }
                         if (skip_ccf) {
                         } else if (use_tc) {
-                            launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.tmax, gs);
+                            launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.tmax, gs,
+                                          tl_next(w, g, 1));
                         } else {
                             launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, ccf_grid_xy.y, nj),
                                        dim3(CCF_THREADS), ccf_smem, gs, Q,
@@ -2069,20 +2508,25 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     b = tm.get();
                     CCW_CUDA(cudaEventRecord(a, gs));
                 }
+                Q.tl = tl_next(w, g, 2);
                 if (skip_sel && !first_wave) {
                 } else if (warp_select || (first_wave && !cfg.min_cut)) {
                     const Job* dj = d_jobs;
-                    if (selw == 1)
-                        launch_pdl(select_paste_warp_kernel<1>, dim3((nj + WS_WARPS - 1) / WS_WARPS),
-                                   dim3(WS_WARPS * 32), sizeof(WarpSel) * WS_WARPS, gs, Q, dj,
+                    if (!split_select) {
+                        launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
                                    static_cast<int>(j0), nj);
-                    else if (selw == 2)
-                        launch_pdl(select_paste_warp_kernel<2>, dim3(nj), dim3(64), sizeof(WarpSel), gs,
-                                   Q, dj, static_cast<int>(j0), nj);
-                    else
-                        launch_pdl(select_paste_warp_kernel<4>, dim3(nj), dim3(128), sizeof(WarpSel), gs,
-                                   Q, dj, static_cast<int>(j0), nj);
+                    } else {
+                        if (!first_wave) {
+                            launch_pdl(select_scan_kernel, dim3((nj + SC_WARPS - 1) / SC_WARPS),
+                                       dim3(SC_WARPS * 32), 0, gs, Q, dj, static_cast<int>(j0), nj);
+                            ++launches;
+                            Q.tl = tl_next(w, g, 3);
+                        }
+                        launch_pdl(select_pick_kernel, dim3(nj), dim3(PK_T), 0, gs, Q, dj,
+                                   static_cast<int>(j0), nj);
+                    }
                     if (Q.defer && !first_wave) {
+                        Q.tl = nullptr;
                         launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, Q, dj,
                                    static_cast<int>(j0), nj, bulk_S);
                         ++launches;
@@ -2112,7 +2556,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     {
         const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
         const int bx = static_cast<int>(std::min<size_t>((n + 255) / 256, 1024));
-        finalize_kernel<<<dim3(bx, n_real), 256, 0, st>>>(d_work, wh, ww, d_hd, cfg.sg_height,
+        finalize_kernel<<<dim3(bx, n_real), 256, 0, st>>>(d_work, wh, ww, d_src, B, J, swc, ti->d_codes,
+                                                          ti->w, ti->wc, d_hd, cfg.sg_height,
                                                           cfg.sg_width, fin, d_mism);
         ++launches;
         CCW_CUDA(cudaGetLastError());
@@ -2152,6 +2597,19 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.host_prep_ms = host_prep_ms;
     ctx->timing.jobs = static_cast<int64_t>(total_jobs);
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
+    if (d_tl) {
+        std::vector<unsigned long long> h(tl_tag.size() * 4);
+        CCW_CUDA(cudaMemcpy(h.data(), d_tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull;
+        for (size_t i = 0; i < tl_tag.size(); ++i) t0 = std::min(t0, h[4 * i + 2]);
+        fprintf(stderr, "timeline (us from first resident CTA): wave group kind resident start end last_start\n");
+        for (size_t i = 0; i < tl_tag.size(); ++i) {
+            if (h[4 * i + 1] == 0) continue;
+            fprintf(stderr, "TL %d %d %d %.2f %.2f %.2f %.2f\n", tl_tag[i][0], tl_tag[i][1], tl_tag[i][2],
+                    (h[4 * i + 2] - t0) * 1e-3, (h[4 * i] - t0) * 1e-3, (h[4 * i + 1] - t0) * 1e-3,
+                    (h[4 * i + 3] - t0) * 1e-3);
+        }
+    }
     if (d_probe) {
         unsigned long long pr[8];
         CCW_CUDA(cudaMemcpy(pr, d_probe, sizeof(pr), cudaMemcpyDeviceToHost));
@@ -2162,15 +2620,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         tc_probe_buffer = nullptr;
     }
     if (getenv("CCW_PHASES"))
-        fprintf(stderr, "phase clocks: rescore %llu merge %llu thr %llu gather %llu choose %llu paste %llu"
-                " | bulk total %llu stage %llu compute %llu\n",
-                stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[7], stats[14], stats[15]);
+        fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] pick[stage %llu batch %llu choose+map %llu]"
+                " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
+                stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[4], stats[7], stats[14],
+                stats[15], stats[5], stats[6]);
     ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
     ctx->timing.list_overflows = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
     if (bulk_launch && stats[3] == 0)
         ctx->bulk_off[bulk_key] = true;
-    else if (!bulk_launch && stats[4] > 0)
+    else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back
         ctx->bulk_off.erase(bulk_key);
     ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
