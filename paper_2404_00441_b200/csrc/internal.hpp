@@ -132,19 +132,23 @@ public:
         for (auto& t : thr_) t.join();
     }
     template <class F>
-    void run(int n, F&& fn) {
+    void run(int n, F&& fn, int max_threads = 1 << 30) {
         if (n <= 0) return;
-        const int want = std::min(n / 2, max_workers());
+        const int want = std::min({n / 2, max_workers(), max_threads - 1});
         if (want <= 0) {
             for (int i = 0; i < n; ++i) fn(i);
             return;
         }
-        while (static_cast<int>(thr_.size()) < want) thr_.emplace_back([this, g = gen_] { worker(g); });
+        while (static_cast<int>(thr_.size()) < want) {
+            const int idx = static_cast<int>(thr_.size());
+            thr_.emplace_back([this, idx, g = gen_] { worker(idx, g); });
+        }
         std::function<void(int)> job(std::forward<F>(fn));
         {
             std::lock_guard<std::mutex> lk(mu_);
             job_ = &job;
             n_ = n;
+            active_ = want;  // workers [0, want) join; the rest check in and wait
             next_.store(0);
             busy_ = static_cast<int>(thr_.size());
             err_ = nullptr;
@@ -176,15 +180,17 @@ private:
             }
         }
     }
-    void worker(uint64_t seen) {
+    void worker(int idx, uint64_t seen) {
         for (;;) {
+            bool join = false;
             {
                 std::unique_lock<std::mutex> lk(mu_);
                 cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
                 if (stop_) return;
                 seen = gen_;
+                join = idx < active_;
             }
-            work();
+            if (join) work();
             std::lock_guard<std::mutex> lk(mu_);
             if (--busy_ == 0) done_.notify_all();
         }
@@ -193,7 +199,7 @@ private:
     std::mutex mu_;
     std::condition_variable cv_, done_;
     std::function<void(int)>* job_ = nullptr;
-    int n_ = 0, busy_ = 0;
+    int n_ = 0, busy_ = 0, active_ = 0;
     std::atomic<int> next_{0};
     uint64_t gen_ = 0;
     bool stop_ = false;
@@ -210,12 +216,14 @@ struct ccw_ctx {
     int ccf_variant = 0;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf defer, cand, ncand, cthr, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf bandstage, defer, cand, ncand, cthr, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
+    ccwgpu::HostBuf h_bands;  // pinned staging of progressively copied result bands
     ccwgpu::HostPool pool;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<cudaStream_t> gstreams;  // realization-group streams
+    cudaStream_t copy_stream = nullptr;  // progressive device->host copies of final bands
     // launch plan memory: (TI content key, Tc, OVc, K, T) whose last call
     // deferred no placement to the bulk tie select skip its per-wave launch
     // (re-enabled when the warp select reports a would-be deferral)

@@ -1496,6 +1496,7 @@ __global__ void __launch_bounds__(FS_T, 4)
     const int gj = job0 + slot;
     const Job jb = jobs[gj];
     const int Tc = P.Tc;
+    long long fclk[5] = {clock64(), 0, 0, 0, 0};
     int fr, fc;
     if (jb.shape == kNone) {
         fr = jb.fr;
@@ -1513,6 +1514,11 @@ __global__ void __launch_bounds__(FS_T, 4)
             if (lane == 0) {
                 S.misc[0] = n;
                 S.misc[1] = mk;
+                if (P.stats && P.tl && n >= 0) {
+                    sclk[4] = clock64();
+                    for (int q = 0; q < 4; ++q)
+                        atomicAdd(&P.stats[8 + q], static_cast<unsigned long long>(sclk[q + 1] - sclk[q]));
+                }
             }
         } else {
             // stage the template (matcher.hpp:44-61 order), the mask rows and the run groups
@@ -1555,6 +1561,7 @@ __global__ void __launch_bounds__(FS_T, 4)
             cp_async_wait_all();
         }
         __syncthreads();
+        fclk[1] = clock64();
         const int n = S.misc[0], nr = S.misc[2], ngrp = S.misc[3];
         mk = S.misc[1];
         int ntop = 0;
@@ -1593,12 +1600,14 @@ __global__ void __launch_bounds__(FS_T, 4)
             }
             if (cnt > 0) fast_batch(P, S, tmS, nr, ngrp, cnt, ntop, K);
         }
+        fclk[2] = clock64();
         // choose (matcher.hpp:207-241)
         if (wid == 0) {
             const int pos = choose_pick(P, jb, S.tidx, ntop, lane);
             if (lane == 0) S.misc[4] = pos;
         }
         __syncthreads();
+        fclk[3] = clock64();
         const int pos = S.misc[4];
         fr = (pos / P.out_w) << P.J;
         fc = (pos % P.out_w) << P.J;
@@ -1607,6 +1616,12 @@ __global__ void __launch_bounds__(FS_T, 4)
     if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
+        if (P.stats && P.tl && fclk[3]) {
+            fclk[4] = clock64();
+            atomicAdd(&P.stats[12], static_cast<unsigned long long>(fclk[1] - fclk[0]));
+            atomicAdd(&P.stats[13], static_cast<unsigned long long>(fclk[2] - fclk[1]));
+            atomicAdd(&P.stats[4], static_cast<unsigned long long>(fclk[4] - fclk[2]));
+        }
     }
     tl_mark(P.tl, 1);
 }
@@ -1994,6 +2009,58 @@ __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww
             }
         }
         out[static_cast<size_t>(r) * n + e] = v;
+    }
+    if (hd) {
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
+    }
+}
+
+// Progressive finalize: band descriptors (realization, axis, lo, hi) in
+// output coordinates -- axis 0: rows [lo, hi) x every column; axis 1: every
+// row x columns [lo, hi).  A band is final once every placement covering it
+// is done (run_simulation's checkpoints), so it is rebuilt -- in place for
+// row bands, packed at boff[band] in a staging buffer for column bands -- and
+// copied to the host while later waves still compute.
+__global__ void finalize_band_kernel(const int4* __restrict__ bands, const size_t* __restrict__ boff,
+                                     const uint8_t* __restrict__ work,
+                                     int wh, int ww, const int32_t* __restrict__ src, int B, int J,
+                                     int swc, const uint8_t* __restrict__ ti, int ti_w, int wc,
+                                     const uint8_t* __restrict__ hd, int sg_h, int sg_w,
+                                     uint8_t* __restrict__ out, uint8_t* __restrict__ stage, int* mism) {
+    pdl_wait();
+    const int4 bd = bands[blockIdx.y];
+    const size_t pk = boff[blockIdx.y];
+    const int r = bd.x;
+    const int rows = bd.y == 0 ? bd.w - bd.z : sg_h;
+    const int cols = bd.y == 0 ? sg_w : bd.w - bd.z;
+    const int y0 = bd.y == 0 ? bd.z : 0, x0 = bd.y == 0 ? 0 : bd.z;
+    const size_t n = static_cast<size_t>(rows) * cols;
+    const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
+    const int32_t* sm = src ? src + static_cast<size_t>(r) * (wh >> J) * swc : nullptr;
+    int local = 0;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int y = y0 + static_cast<int>(e / cols), x = x0 + static_cast<int>(e % cols);
+        uint8_t v;
+        if (g) {
+            v = g[static_cast<size_t>(y) * ww + x];
+        } else {
+            const int b = sm[static_cast<size_t>(y >> J) * swc + (x >> J)];
+            const int by = b / wc, bx = b - by * wc;
+            v = ti[static_cast<size_t>((by << J) + (y & (B - 1))) * ti_w + (bx << J) + (x & (B - 1))];
+        }
+        if (hd) {
+            const uint8_t h = hd[static_cast<size_t>(y) * ww + x];
+            if (h != kNoDatum) {
+                local += v != h;
+                v = h;
+            }
+        }
+        if (pk == ~static_cast<size_t>(0))
+            out[(static_cast<size_t>(r) * sg_h + y) * sg_w + x] = v;  // in place (row band)
+        else
+            stage[pk + e] = v;  // packed, the band's cells row-major (column band)
     }
     if (hd) {
         for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -2415,6 +2482,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         for (int g = 0; g < G; ++g)
             tcplans.push_back(plan_ccf_tc(GP[g].wts8, static_cast<int>(maxj), d_x, npos, kpad));
     // group streams, forked from / joined back to the context stream
+    if (!ctx->copy_stream) CCW_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     while (static_cast<int>(ctx->gstreams.size()) < G) {
         cudaStream_t s2;
         CCW_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
@@ -2430,6 +2498,57 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
+    // ---- progressive output (host results): bands of every realization that
+    // no remaining placement covers are finalized and copied back at a few
+    // checkpoint waves, overlapping the copy with the remaining waves
+    uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
+    const bool stream_out = h_out && !getenv("CCW_NO_STREAM_OUT");
+    std::vector<int4> bands;                                   // all checkpoints, in launch order
+    std::vector<std::vector<std::pair<int, std::pair<size_t, size_t>>>> band_at(G);  // per group: (wave, [off, off+n))
+    if (stream_out) {
+        int nck = 6;
+        if (const char* e = getenv("CCW_STREAM_BANDS")) nck = std::max(1, atoi(e));
+        const int delta = std::max(1, (max_key + 1 + nck - 1) / nck);
+        std::vector<int> done(n_real, 0);  // raster-outer extent already emitted
+        for (int w = 0; w <= max_key; ++w) {
+            if ((w + 1) % delta != 0 && w != max_key) continue;
+            for (int g = 0; g < G; ++g) {
+                const size_t off = bands.size();
+                for (int r = 0; r < n_real; ++r) {
+                    if (group_of(r) != g) continue;
+                    const Plan& p = variants[vid[r]];
+                    // column-major raster paths free whole columns, which would be strided copies
+                    // (slow DMA): those realizations are emitted whole at the last wave
+                    if (p.column_major && w != max_key) continue;
+                    const int axis = 0;
+                    const bool asc = p.column_major || p.origin == CCW_TOP_LEFT || p.origin == CCW_TOP_RIGHT;
+                    const int extent = wh, sg_ext = cfg.sg_height;
+                    int O = w >= p.n_inner - 1 ? (w - (p.n_inner - 1)) / keymul : -1;
+                    O = std::min(O, p.n_outer - 1);
+                    const int U = (w == max_key || O == p.n_outer - 1) ? extent : (O + 1) * stride;
+                    if (U <= done[r]) continue;
+                    int lo = asc ? done[r] : extent - U, hi = asc ? U : extent - done[r];
+                    done[r] = U;
+                    lo = std::max(lo, 0);
+                    hi = std::min(hi, sg_ext);
+                    if (hi > lo) bands.push_back(make_int4(r, axis, lo, hi));
+                }
+                if (bands.size() > off) band_at[g].push_back({w, {off, bands.size()}});
+            }
+        }
+    }
+    int4* d_bands = nullptr;
+    size_t* d_boff = nullptr;
+    std::vector<size_t> boff(bands.size() + 1, 0);  // packed staging offsets (launch order)
+    if (!bands.empty()) {
+        for (size_t q = 0; q < bands.size(); ++q) boff[q] = ~static_cast<size_t>(0);  // all in place
+        d_bands = reinterpret_cast<int4*>(ctx->ops_b.get(sizeof(int4) * bands.size() + sizeof(size_t) * boff.size()));
+        d_boff = reinterpret_cast<size_t*>(d_bands + bands.size());
+        CCW_CUDA(cudaMemcpyAsync(d_bands, bands.data(), sizeof(int4) * bands.size(), cudaMemcpyHostToDevice, st));
+        CCW_CUDA(cudaMemcpyAsync(d_boff, boff.data(), sizeof(size_t) * boff.size(), cudaMemcpyHostToDevice, st));
+    }
+    std::vector<size_t> band_next(G, 0);
+
     // debug timeline: [resident, past-wait, end] per launch
     const bool want_tl = getenv("CCW_TIMELINE") != nullptr;
     std::vector<std::array<int, 3>> tl_tag;  // (wave, group, kind 0 prep / 1 ccf / 2 select)
@@ -2542,6 +2661,39 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     tm.sel.push_back({a, b});
                 }
             }
+            if (band_next[g] < band_at[g].size() && band_at[g][band_next[g]].first == w) {
+                const auto rng = band_at[g][band_next[g]++].second;
+                const int nb = static_cast<int>(rng.second - rng.first);
+                launch_pdl(finalize_band_kernel, dim3(32, nb), dim3(256), 0, gs,
+                           static_cast<const int4*>(d_bands + rng.first), static_cast<const size_t*>(d_boff + rng.first),
+                           static_cast<const uint8_t*>(d_work),
+                           wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
+                           static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
+                           static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, static_cast<uint8_t*>(nullptr), d_mism);
+                ++launches;
+                // copies on their own stream (the group's next wave does not wait),
+                // straight into the caller's buffer; adjacent ranges merged
+                cudaEvent_t be = tm.get();
+                CCW_CUDA(cudaEventRecord(be, gs));
+                CCW_CUDA(cudaStreamWaitEvent(ctx->copy_stream, be, 0));
+                const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
+                size_t o0 = 0, o1 = 0;
+                auto flush = [&] {
+                    if (o1 > o0)
+                        CCW_CUDA(cudaMemcpyAsync(h_out + o0, fin + o0, o1 - o0, cudaMemcpyDeviceToHost,
+                                                 ctx->copy_stream));
+                    o0 = o1 = 0;
+                };
+                for (size_t q = rng.first; q < rng.second; ++q) {
+                    const int4 bd = bands[q];
+                    const size_t a0 = static_cast<size_t>(bd.x) * n + static_cast<size_t>(bd.z) * cfg.sg_width;
+                    const size_t a1 = static_cast<size_t>(bd.x) * n + static_cast<size_t>(bd.w) * cfg.sg_width;
+                    if (a0 != o1) flush();
+                    if (o1 == 0) o0 = a0;
+                    o1 = a1;
+                }
+                flush();
+            }
         }
     }
     CCW_CUDA(cudaGetLastError());
@@ -2550,10 +2702,14 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaEventRecord(e, ctx->gstreams[g]));
         CCW_CUDA(cudaStreamWaitEvent(st, e, 0));
     }
+    if (stream_out) {
+        cudaEvent_t e = tm.get();
+        CCW_CUDA(cudaEventRecord(e, ctx->copy_stream));
+        CCW_CUDA(cudaStreamWaitEvent(st, e, 0));
+    }
 
-    // ---- finalize
-    uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
-    {
+    // ---- finalize (device results, or host results without streaming)
+    if (!stream_out) {
         const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
         const int bx = static_cast<int>(std::min<size_t>((n + 255) / 256, 1024));
         finalize_kernel<<<dim3(bx, n_real), 256, 0, st>>>(d_work, wh, ww, d_src, B, J, swc, ti->d_codes,
@@ -2563,7 +2719,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaGetLastError());
     }
     CCW_CUDA(cudaEventRecord(ev1, st));
-    if (h_out)
+    if (h_out && !stream_out)
         CCW_CUDA(cudaMemcpyAsync(h_out, fin, static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real,
                                  cudaMemcpyDeviceToHost, st));
     unsigned long long stats[16] = {0};
@@ -2620,7 +2776,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         tc_probe_buffer = nullptr;
     }
     if (getenv("CCW_PHASES"))
-        fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] pick[stage %llu batch %llu choose+map %llu]"
+        fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast|pick[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
                 stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[4], stats[7], stats[14],
                 stats[15], stats[5], stats[6]);
