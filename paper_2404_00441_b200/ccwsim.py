@@ -53,6 +53,20 @@ class IoError(Error):
     pass
 
 
+class ParseError(Error):
+    """errors.hpp:57-73: a malformed input file; carries the path and the
+    1-based line number (0 when unknown)."""
+
+    def __init__(self, path: str, line, msg: Optional[str] = None):
+        if msg is None:  # (path, msg)
+            line, msg = 0, line
+            super().__init__(f"{path}: {msg}")
+        else:
+            super().__init__(f"{path}:{line}: {msg}")
+        self.path = path
+        self.line = line
+
+
 class DeviceError(Error):
     """CUDA failure inside libccwgpu.so (status >= 100)."""
 
