@@ -70,6 +70,9 @@ struct SimParams {
     int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
     unsigned long long* tl;  // debug timeline slot of this launch (null unless CCW_TIMELINE)
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
+    int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)
+    const int32_t* nnmap;    // normalized screen: [8 mask variants][npos] sum over mask and
+                             // channels of squared TI block counts (null otherwise)
     int* cand;               // fast select: candidate positions per job slot (SC_LC each)
     int* ncand;              //   count, -1 = stream windows >= cthr, -2 = deferred to the bulk kernel
     int* cthr;               //   streaming threshold (list overflow without the bulk kernel)

@@ -216,7 +216,7 @@ struct ccw_ctx {
     int ccf_variant = 0;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf bandstage, defer, cand, ncand, cthr, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf bandstage, cjob, defer, cand, ncand, cthr, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
     ccwgpu::HostBuf h_bands;  // pinned staging of progressively copied result bands
@@ -239,6 +239,7 @@ struct ccw_ti {
     double* d_ti64 = nullptr;    // nch*hc*wc
     float* d_scr = nullptr;      // nscr*hc*wc
     std::map<int, int8_t*> im2col;  // per template size Tc: npos x kpad int8 (tcgen05 screen)
+    std::map<std::pair<int, int>, int32_t*> nnmap;  // per (Tc, OVc): normalized-screen norms
     uint64_t key = 0;  // content key (hash of cells + shape) for per-context plan memory
 };
 

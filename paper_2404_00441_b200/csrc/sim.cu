@@ -66,6 +66,21 @@ void build_pyramid(ccw_ti* ti, cudaStream_t s) {
 
 // ------------------------------------------------------------ or_prep ----
 
+// Normalized screen: C_job = B^2 * sum over the mask of the OR's last-facies
+// block count, so the screen S' (F-1 channels) plus C_job is the full
+// count score S (indicator mode; 0 in raw-codes mode).
+__device__ __forceinline__ void store_cjob(const SimParams& P, int slot, int csum) {
+    __shared__ int red[32];
+    for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = csum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        P.cjob[slot] = P.mode == 0 ? P.B * P.B * t : 0;
+    }
+}
+
 // Screen weights: indicator mode uses F-1 channels with w_f = n_f - n_{F-1}
 // (n = OR block counts).  Because every fine cell holds exactly one facies,
 //   S = sum_f sum_mask N_f * n_f = sum_{f<F-1} sum_mask N_f * w_f + B * sum_mask n_{F-1}
@@ -89,6 +104,7 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
     int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
     if (w8)
         for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x) w8[k] = 0;
+    int csum = 0;
     for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
         const int s = c / Tc, t = c - s * Tc;
         int t0, t1;
@@ -98,6 +114,7 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
         int last = B * B;
         if (P.mode == 0)
             for (int f = 0; f < P.nscr; ++f) last -= static_cast<int>(P.tiscr[static_cast<size_t>(f) * nc + sb]);
+        if (in) csum += last;
         for (int f = 0; f < P.nscr; ++f) {
             const int n = static_cast<int>(P.tiscr[static_cast<size_t>(f) * nc + sb]);
             const int v = in ? (P.mode == 0 ? n - last : n) : 0;
@@ -107,6 +124,7 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
         for (int ch = 0; ch < P.nch; ++ch)
             tm[ch * Tc * Tc + c] = in ? P.ti64[static_cast<size_t>(ch) * nc + sb] : 0.0;
     }
+    if (P.cjob) store_cjob(P, slot, csum);
     tl_mark(P.tl, 1);
 }
 
@@ -122,6 +140,7 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
     if (P.wts8)  // zero the K padding of this job's int8 weight row
         for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x)
             P.wts8[static_cast<size_t>(slot) * P.kpad + k] = 0;
+    int csum = 0;
     for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
         const int s = c / Tc, t = c - s * Tc;
         int t0, t1;
@@ -131,6 +150,7 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
         int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
         if (P.mode == 0) {
             const int last = in ? block_stat(base, P.ww, B, 0, P.F - 1) : 0;
+            csum += last;
             for (int f = 0; f < P.nscr; ++f) {
                 const int v = in ? block_stat(base, P.ww, B, 0, f) - last : 0;
                 wts[f * Tc * Tc + c] = v;
@@ -144,6 +164,7 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
         for (int ch = 0; ch < P.nch; ++ch)
             tm[ch * Tc * Tc + c] = in ? haar_apex_block(base, P.ww, P.J, P.mode, ch) : 0.0;
     }
+    if (P.cjob) store_cjob(P, slot, csum);
 }
 
 // --------------------------------------------------------- CCF screen ----
@@ -310,7 +331,8 @@ __host__ __device__ inline SelLayout sel_layout(int K, int T, int OV, int nch = 
 // Exact K-th largest value (with multiplicity) of n int32 values, skipping
 // INT_MIN padding: block-wide radix select over the offset range, 8 bits per
 // pass, warp-aggregated shared-memory histograms.
-__device__ int radix_kth_largest(const int32_t* __restrict__ sc, int n, int K, int* hist,
+// (No __restrict__: the normalized screen rewrites its input in the same kernel.)
+__device__ int radix_kth_largest(const int32_t* sc, int n, int K, int* hist,
                                  int* misc, int* redi, int stride = 1) {
     int lo = INT_MAX, hi = INT_MIN;
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
@@ -551,6 +573,49 @@ __device__ void flush_candidates(const SimParams& P, const RunDesc* runs, int R,
     __syncthreads();
 }
 
+// Normalized screen.  Mask variant of a placement:
+// L (vleft, htop) 0-3, vertical strip 4 + vleft, horizontal strip 6 + htop.
+__host__ __device__ inline int mask_variant(int shape, int vleft, int htop) {
+    return shape == kL ? (vleft ? 2 : 0) + (htop ? 1 : 0)
+                       : (shape == kVertical ? 4 + (vleft ? 1 : 0) : 6 + (htop ? 1 : 0));
+}
+
+// NN[v][p] = sum over mask variant v's cells and over every channel of the
+// squared TI block count: the reference's normalization sum_f sum_mask ti_f^2
+// (matcher.hpp:84-100, 163-171) times 4^J, exact in integers.
+__global__ void nn_map_kernel(const float* __restrict__ scr, int nscr, int mode, int B, int hc, int wc,
+                              int Tc, int OVc, int out_w, int npos, int32_t* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y;
+    if (p >= npos) return;
+    const int shape = v < 4 ? kL : (v < 6 ? kVertical : kHorizontal);
+    const int vleft = v < 4 ? (v >> 1) : (v < 6 ? v - 4 : 0);
+    const int htop = v < 4 ? (v & 1) : (v < 6 ? 0 : v - 6);
+    const int x = p / out_w, y = p - x * out_w;
+    const size_t nc = static_cast<size_t>(hc) * wc;
+    int acc = 0;
+    for (int s = 0; s < Tc; ++s) {
+        int t0, t1;
+        mask_row_run(shape, vleft, htop, Tc, OVc, s, t0, t1);
+        for (int t = t0; t < t1; ++t) {
+            const size_t idx = static_cast<size_t>(x + s) * wc + y + t;
+            if (mode == 0) {
+                int rest = B * B;  // the last facies' count
+                for (int f = 0; f < nscr; ++f) {
+                    const int n = static_cast<int>(scr[f * nc + idx]);
+                    acc += n * n;
+                    rest -= n;
+                }
+                acc += rest * rest;
+            } else {
+                const int n = static_cast<int>(scr[idx]);
+                acc += n * n;
+            }
+        }
+    }
+    out[static_cast<size_t>(v) * npos + p] = acc;
+}
+
 __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
                                                              const Job* __restrict__ jobs,
                                                              int job0, int use_screen) {
@@ -614,7 +679,27 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         const bool all = !use_screen;
         const int32_t* tmx = P.tmax ? P.tmax + static_cast<size_t>(blockIdx.x) * P.ntiles : nullptr;
         int thr = 0;
-        if (!all) thr = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
+        if (use_screen == 2) {
+            // normalized: R = S / sqrt(NN) with S = S' + C_job and NN exact
+            // integers; keys = R rounded down to float32 (monotone as int32
+            // for R >= 0).  Every window the reference's fp64 score (relative
+            // error << 1e-9) can rank in the top-K has R >= R_K (1 - 1e-9),
+            // hence key >= the threshold below: a superset, rescored exactly.
+            int32_t* scw = P.scores + static_cast<size_t>(blockIdx.x) * P.sld;
+            const int32_t* nn = P.nnmap + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * P.npos;
+            const int cj = P.cjob[blockIdx.x];
+            for (int p = tid; p < P.npos; p += SEL_T) {
+                const int n = nn[p];
+                const double R = n > 0 ? static_cast<double>(scw[p] + cj) / sqrt(static_cast<double>(n)) : 0.0;
+                scw[p] = __float_as_int(__double2float_rd(R));
+            }
+            __syncthreads();
+            const int kk = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
+            thr = __float_as_int(__double2float_rd(static_cast<double>(__int_as_float(kk)) * (1.0 - 1e-9)));
+            tmx = nullptr;  // the tile maxima bound S', not the keys
+        } else if (!all) {
+            thr = radix_kth_largest(sc, P.npos, K, hist, misc, redi);
+        }
         if (P.stats && tid == 0) atomicAdd(&P.stats[1], 1ull);
         __syncthreads();
         // 2. gather the tie group in row-major order, rescore in fp64, keep the
@@ -2136,6 +2221,20 @@ double pair_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
 
 }  // namespace
 
+// NN maps of a TI for template Tc / overlap OVc (8 mask variants), cached on the TI.
+const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
+    const auto key = std::make_pair(Tc, OVc);
+    auto it = ti->nnmap.find(key);
+    if (it != ti->nnmap.end()) return it->second;
+    const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1, npos = out_h * out_w;
+    int32_t* m = static_cast<int32_t*>(cache_alloc(ti->device, sizeof(int32_t) * 8 * static_cast<size_t>(npos)));
+    nn_map_kernel<<<dim3((npos + 255) / 256, 8), 256, 0, st>>>(ti->d_scr, ti->nscr, ti->mode, 1 << ti->J, ti->hc,
+                                                             ti->wc, Tc, OVc, out_w, npos, m);
+    CCW_CUDA(cudaGetLastError());
+    ti->nnmap[key] = m;
+    return m;
+}
+
 void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
                     int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out,
                     ccw_diag* diag, ccw_trace* traces) {
@@ -2293,6 +2392,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const double maxw = ti->mode == 0 ? B : static_cast<double>(ti->F - 1) * B;
     const double mask_cells = static_cast<double>(Tc) * OVc + static_cast<double>(Tc - OVc) * OVc;
     const bool use_screen = cfg.scoring == 0 && ti->nscr > 0;
+    // normalized scoring: screened on the int8 tensor-core GEMM when it applies
+    // (otherwise every window is rescored in fp64)
+    bool norm_screen = cfg.scoring == 1 && ti->nscr > 0 && !getenv("CCW_NO_NORM_SCREEN") &&
+                       mask_cells * ti->nch * maxw * maxw * maxw * maxw < 2147483647.0;
     if (use_screen && mask_cells * maxw * maxw * std::max(1, ti->nscr) >= 16777216.0)
         throw Fail(CCW_ERR_CONFIG, "configuration exceeds the exact fp32 screen range (mask*B^2 >= 2^24)");
 
@@ -2375,10 +2478,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
 
     // screen variant: tcgen05 int8 implicit GEMM when every operand fits int8
     const int maxv = ti->mode == 0 ? B * B : (ti->F - 1) * B * B;
-    const bool tc_ok = use_screen && maxv <= 127;
+    const bool tc_ok = (use_screen || norm_screen) && maxv <= 127;
     if (ctx->ccf_variant == 2 && use_screen && !tc_ok)
         throw Fail(CCW_ERR_CONFIG, "tcgen05 int8 screen needs block statistics <= 127");
     const bool use_tc = tc_ok && ctx->ccf_variant != 1;
+    norm_screen = norm_screen && use_tc;  // the normalized screen rides on the int8 GEMM only
+    const bool any_screen = use_screen || norm_screen;
     const int kpad = tc_kpad(ti->nscr, Tc);
     const int ntiles = tc_tiles(npos);
     const int8_t* d_x = nullptr;
@@ -2388,6 +2493,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         d_x = ti_im2col(ti, Tc, st);
         d_w8 = ctx->wts8.as<int8_t>(G * maxj * kpad);
         d_tmax = ctx->summary.as<int32_t>(G * maxj * ntiles);
+    }
+    int32_t* d_cjob = nullptr;
+    if (norm_screen) {
+        P.nnmap = ti_nnmap(ti, Tc, OVc, st);
+        d_cjob = ctx->cjob.as<int32_t>(G * maxj);
     }
     unsigned long long* d_stats = ctx->stats.as<unsigned long long>(16);
     CCW_CUDA(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
@@ -2449,6 +2559,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         GP[g].tm64 = d_tm + g * maxj * ti->nch * Tc * Tc;
         GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
         GP[g].tmax = d_tmax ? d_tmax + g * maxj * ntiles : nullptr;
+        GP[g].cjob = d_cjob ? d_cjob + g * maxj : nullptr;
         GP[g].defer = d_defer ? d_defer + g * maxj : nullptr;
         if (warp_select) {
             GP[g].cand = P.cand + g * maxj * SC_LC;
@@ -2590,7 +2701,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         launch_pdl(or_prep_kernel, dim3(nj), dim3(128), 0, gs, Q,
                                    static_cast<const Job*>(d_jobs), static_cast<int>(j0));
                     ++launches;
-                    if (use_screen) {
+                    if (any_screen) {
                         cudaEvent_t a = nullptr, b = nullptr;
                         if (ctx->profiling) {
                             a = tm.get();
@@ -2654,7 +2765,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 else
                     launch_pdl(select_paste_kernel, dim3(nj), dim3(SEL_T), sel_smem, gs, Q,
                                static_cast<const Job*>(d_jobs), static_cast<int>(j0),
-                               use_screen ? 1 : 0);
+                               use_screen ? 1 : (norm_screen ? 2 : 0));
                 ++launches;
                 if (ctx->profiling) {
                     CCW_CUDA(cudaEventRecord(b, gs));
@@ -2787,7 +2898,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         ctx->bulk_off[bulk_key] = true;
     else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back
         ctx->bulk_off.erase(bulk_key);
-    ctx->timing.ccf_variant = use_screen ? (use_tc ? 2 : 1) : 0;
+    ctx->timing.ccf_variant = any_screen ? (use_tc ? 2 : 1) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();

@@ -150,6 +150,35 @@ def test_k_above_tile_count_with_ties(oracle, k):
             assert np.array_equal(r.realization.cells, o["realization"]), (k, mode)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("k", [1, 5])
+def test_normalized_screen(oracle, mode, k):
+    """Normalized scoring through the int8 screen (S = S' + C_job over the
+    exact norm map): bit-exact against the oracle on a channel TI and on a
+    blocky, tie-heavy TI, with hard data."""
+    from paper_2404_00441_b200 import synth
+    rng = np.random.default_rng(900 + 10 * mode + k)
+    tis = [synth.channel_levee_ti(192, 160, 31),
+           np.repeat(np.repeat(rng.integers(0, 3, (48, 40)), 4, 0), 4, 1).astype(np.uint8)]
+    dev = cs.default_device()
+    for ti_a in tis:
+        nf = 3
+        ti = cs.CategoricalGrid(ti_a.shape[0], ti_a.shape[1], nf, ti_a)
+        d = dict(sg_height=150, sg_width=170, template_size=32, overlap=8, dwt_level=2, candidates=k,
+                 scoring=1, facies_mode=mode)
+        seeds = [cs.mix64(17, k), cs.mix64(18, k)]
+        ref0 = oracle.simulate_one(ti_a, nf, pyoracle.Cfg(**d), None, seed=seeds[0])["realization"]
+        cells = rng.choice(150 * 170, size=40, replace=False)
+        hd = [(int(c // 170), int(c % 170), int(ref0[c // 170, c % 170])) for c in cells]
+        for cond in (None, hd):
+            res = cs.simulate_batch(ti, to_cfg(d, cond), seeds)
+            assert dev.last_timing()["ccf_variant"] == 2  # screened
+            for s_, r in zip(seeds, res):
+                o = oracle.simulate_one(ti_a, nf, pyoracle.Cfg(**d), cond, seed=s_)
+                assert np.array_equal(r.realization.cells, o["realization"]), (mode, k, cond is None)
+                assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+
+
 def test_provenance_and_replay():
     # test_simulator.cpp:434-460, acceptance.cpp:349-381
     z = load("sim_channel64_base.npz")
