@@ -179,6 +179,37 @@ def test_normalized_screen(oracle, mode, k):
                 assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+@pytest.mark.parametrize("case", ["long_runs", "many_tiles", "k8", "long_runs_hd"])
+def test_fast_select_geometries(oracle, case):
+    """Fast-select corners against the oracle: mask rows longer than one
+    rescoring item (Tc = 32), score rows with more than 512 tiles (the scan
+    streams the tile maxima), K = 8 (the register top-K limit), hard data."""
+    from paper_2404_00441_b200 import synth
+    if case in ("long_runs", "long_runs_hd"):
+        ti_a, nf = synth.channel_levee_ti(192, 192, 5), 3
+        d = dict(sg_height=160, sg_width=176, template_size=64, overlap=16, dwt_level=1, candidates=3)
+    elif case == "many_tiles":
+        ti_a, nf = synth.channel_ti(600, 600, 11), 2
+        d = dict(sg_height=64, sg_width=72, template_size=16, overlap=4, dwt_level=1, candidates=5)
+    else:
+        ti_a, nf = synth.channel_levee_ti(256, 256, 6), 3
+        d = dict(sg_height=200, sg_width=200, template_size=32, overlap=8, dwt_level=2, candidates=8)
+    ti = cs.CategoricalGrid(ti_a.shape[0], ti_a.shape[1], nf, ti_a)
+    seeds = [cs.mix64(23, 1), cs.mix64(23, 2)]
+    hd = None
+    if case == "long_runs_hd":
+        ref0 = oracle.simulate_one(ti_a, nf, pyoracle.Cfg(**d), None, seed=seeds[0])["realization"]
+        rng = np.random.default_rng(5)
+        cells = rng.choice(d["sg_height"] * d["sg_width"], size=120, replace=False)
+        hd = [(int(c // d["sg_width"]), int(c % d["sg_width"]),
+               int(ref0[c // d["sg_width"], c % d["sg_width"]])) for c in cells]
+    res = cs.simulate_batch(ti, to_cfg(d, hd), seeds)
+    for s_, r in zip(seeds, res):
+        o = oracle.simulate_one(ti_a, nf, pyoracle.Cfg(**d), hd, seed=s_)
+        assert np.array_equal(r.realization.cells, o["realization"]), case
+        assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+
+
 def test_provenance_and_replay():
     # test_simulator.cpp:434-460, acceptance.cpp:349-381
     z = load("sim_channel64_base.npz")
