@@ -835,6 +835,5 @@ def simulate_ensemble(ti: CategoricalGrid, cfg: SimConfig, workers: int = 1,
     ordered by r.  All realizations run in one batched device call, so
     ``workers`` has no effect (the reference guarantees worker-count-invariant
     output, so this is observably identical)."""
-    cfg.validate_against(ti)
     seeds = [mix64(cfg.master_seed, r + 1) for r in range(cfg.n_realizations)]
-    return simulate_batch(ti, cfg, seeds, None, device)
+    return simulate_batch(ti, cfg, seeds, None, device)  # (validates)

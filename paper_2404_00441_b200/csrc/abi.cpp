@@ -83,8 +83,10 @@ void validate_config(const ccw_sim_config& c) {
 
 // grid.hpp:151-170
 static void validate_hard_data(const int32_t* hd, int n_hd, int h, int w, int nf) {
-    std::vector<int> seen;
-    if (n_hd > 0) seen.assign(static_cast<size_t>(h) * w, -1);
+    // one bit per cell (a 4000^2 grid is 2 MB); the earlier entry of a
+    // duplicate is looked up only when reporting it
+    std::vector<uint64_t> seen;
+    if (n_hd > 0) seen.assign((static_cast<size_t>(h) * w + 63) / 64, 0);
     for (int i = 0; i < n_hd; ++i) {
         const int r = hd[3 * i], c = hd[3 * i + 1], f = hd[3 * i + 2];
         if (r < 0 || r >= h || c < 0 || c >= w)
@@ -93,11 +95,16 @@ static void validate_hard_data(const int32_t* hd, int n_hd, int h, int w, int nf
         if (f < 0 || f >= nf)
             throw Fail(CCW_ERR_BOUNDS,
                        fmt("hard datum %d has facies %d outside [0, %d)", i, f, nf));
-        int& s = seen[static_cast<size_t>(r) * w + c];
-        if (s >= 0)
+        const size_t cell = static_cast<size_t>(r) * w + c;
+        uint64_t& word = seen[cell >> 6];
+        const uint64_t bit = 1ull << (cell & 63);
+        if (word & bit) {
+            int s = 0;
+            while (hd[3 * s] != r || hd[3 * s + 1] != c) ++s;
             throw Fail(CCW_ERR_STRUCTURE,
                        fmt("duplicate hard data at (%d, %d): entries %d and %d", r, c, s, i));
-        s = i;
+        }
+        word |= bit;
     }
 }
 

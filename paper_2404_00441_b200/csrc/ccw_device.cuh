@@ -73,9 +73,6 @@ struct SimParams {
     int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)
     const int32_t* nnmap;    // normalized screen: [8 mask variants][npos] sum over mask and
                              // channels of squared TI block counts (null otherwise)
-    int* cand;               // fast select: candidate positions per job slot (SC_LC each)
-    int* ncand;              //   count, -1 = stream windows >= cthr, -2 = deferred to the bulk kernel
-    int* cthr;               //   streaming threshold (list overflow without the bulk kernel)
     int* bulk_sync;          // per job slot: [next position block, finished CTAs]
     double* bulk_keys;       // per job slot x CTA: that CTA's top-K keys
     int* bulk_idx;           //   ... and positions

@@ -216,10 +216,10 @@ struct ccw_ctx {
     int ccf_variant = 0;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf bandstage, cjob, defer, cand, ncand, cthr, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf cjob, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
-    ccwgpu::HostBuf h_bands;  // pinned staging of progressively copied result bands
+    ccwgpu::HostBuf h_out_stage;  // pinned landing zone when the caller's result buffer is pageable
     ccwgpu::HostPool pool;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<cudaStream_t> gstreams;  // realization-group streams

@@ -804,25 +804,16 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
     }
 }
 
-// ------------------------------------------------ two-stage fast select --
+// ------------------------------------------------------------ fast select --
 //
-// The common case (raw scoring, K <= kTcQ, tcgen05 screen, no min-cut) runs
-// as two kernels per wave:
-//   select_scan_kernel  one warp per placement: the tile-maximum bound M_K,
-//                       the (score, position) list of windows >= M_K, the
-//                       exact K-th score S_K, the candidate positions;
-//   select_pick_kernel  one CTA per placement: every (candidate, mask run)
-//                       partial sum in parallel, the per-window fold in the
-//                       reference's order, the reference ranking, the pick
-//                       and the source-block map.
-// Placements whose list overflows go to select_bulk_kernel (or, without it,
-// are streamed by select_pick_kernel at threshold M_K).
-constexpr int SC_WARPS = 4;    // placements per scan CTA
+// The common case (raw scoring, K <= kTcQ, tcgen05 screen, no min-cut): the
+// tile-maximum bound M_K, the (score, position) list of windows >= M_K, the
+// exact K-th score S_K, fp64 rescoring of the candidates, ranking, pick --
+// select_fast_kernel below; placements whose list overflows go to
+// select_bulk_kernel.
 constexpr int SC_LC = 256;     // list / candidate capacity per placement
 constexpr int SC_TB = 8;       // qualifying tiles read per round trip
-constexpr int PK_T = 256;      // threads per placement in select_pick_kernel
 constexpr int PK_TMC = 1024;   // fp64 template values staged in shared memory (when they fit)
-constexpr int PK_RS = 2048;    // (window, run) partial sums per rescoring batch
 constexpr int PK_MAXTC = 64;   // template rows tabulated
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -1134,270 +1125,6 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
         cnt += __popc(bal);
     }
     return cnt;
-}
-
-// ncand[slot]: >= 0 candidates in cand[slot * SC_LC ..], -1 stream every window
-// >= cthr[slot] (no bulk kernel), -2 deferred to select_bulk_kernel.
-__global__ void __launch_bounds__(SC_WARPS * 32)
-    select_scan_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
-    __shared__ ScanWarp sw[SC_WARPS];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = blockIdx.x * SC_WARPS + wid;
-    pdl_trigger();
-    tl_mark(P.tl, 2);
-    pdl_wait();
-    tl_mark(P.tl, 0);
-    if (slot >= nj) return;
-    long long sclk[5];
-    sclk[0] = clock64();
-    int mk = INT_MIN;
-    const int cnt = scan_job(P, slot, sw[wid], P.cand + static_cast<size_t>(slot) * SC_LC, mk, sclk);
-    if (lane == 0) {
-        if (cnt < 0) {
-            if (P.defer) {
-                // a large tie group: the bulk kernel rescores every window >= M_K
-                // (INT_MIN marks "not deferred"; scores never reach it)
-                P.defer[slot] = max(mk, INT_MIN + 1);
-                P.ncand[slot] = -2;
-            } else {
-                P.cthr[slot] = mk;
-                P.ncand[slot] = -1;
-            }
-        } else {
-            if (P.defer) P.defer[slot] = INT_MIN;
-            P.ncand[slot] = cnt;
-        }
-        if (cnt >= 0 && P.stats && P.tl) {  // phase clocks with the debug timeline
-            sclk[4] = clock64();
-            for (int q = 0; q < 4; ++q) atomicAdd(&P.stats[8 + q], static_cast<unsigned long long>(sclk[q + 1] - sclk[q]));
-        }
-    }
-    tl_mark(P.tl, 1);
-}
-
-struct PickSmem {
-    double tm[PK_TMC];
-    double rsum[PK_RS];
-    double key[SC_LC + kTcQ];
-    int cidx[SC_LC + kTcQ];
-    short4 rows[PK_MAXTC];
-    double tkey[kTcQ];
-    int tidx[kTcQ];
-    double rk[PK_T / 32];
-    int ri[PK_T / 32], rp[PK_T / 32];
-    int wc[PK_T / 32];
-    int misc[4];
-};
-
-// Rescore S.cidx[0, cnt) (fp64, the reference's operations in the reference's
-// order: run sums left to right, matcher.hpp:72-76; runs folded row-major,
-// matcher.hpp:77, 160-161) and merge them with the running top-K (S.tkey /
-// S.tidx, ntop entries) by the reference ranking.
-__device__ __forceinline__ void pick_batch(const SimParams& P, PickSmem& S, const double* tmS, int R,
-                                           int cnt, int& ntop, int K) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int rows = R / P.nch;
-    const int EB = max(1, PK_RS / R);
-    if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
-    for (int e0 = 0; e0 < cnt; e0 += EB) {
-        const int ng = min(EB, cnt - e0);
-        for (int w = tid; w < ng * R; w += PK_T) {
-            const int e = w / R, r = w - e * R;
-            const int pos = S.cidx[e0 + e];
-            const int x = pos / P.out_w, y = pos - x * P.out_w;
-            const int ch = r / rows;
-            const short4 rw = S.rows[r - ch * rows];
-            const double* a = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
-                              static_cast<size_t>(x + rw.x) * P.wc + y + rw.y;
-            const double* b = tmS + (ch * P.Tc + rw.x) * P.Tc + rw.y;
-            const int len = rw.z - rw.y;
-            double sum = 0.0;
-            for (int t0 = 0; t0 < len; t0 += 16) {
-                double av[16];  // the run's TI operands in one round trip
-#pragma unroll
-                for (int i = 0; i < 16; ++i) av[i] = t0 + i < len ? __ldg(a + t0 + i) : 0.0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (t0 + i < len) sum = __dadd_rn(sum, __dmul_rn(av[i], b[t0 + i]));
-            }
-            S.rsum[w] = sum;
-        }
-        __syncthreads();
-        for (int e = tid; e < ng; e += PK_T) {
-            double acc = 0.0;
-            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, S.rsum[e * R + r]);
-            S.key[e0 + e] = acc;
-        }
-        __syncthreads();
-    }
-    // merge: the batch plus the running top-K
-    for (int e = tid; e < ntop; e += PK_T) {
-        S.key[cnt + e] = S.tkey[e];
-        S.cidx[cnt + e] = S.tidx[e];
-    }
-    __syncthreads();
-    const int n = cnt + ntop;
-    const int keep = min(K, n);
-    if (n <= 32) {
-        if (wid == 0) {  // every entry's rank in one pass
-            const double mk = lane < n ? S.key[lane] : 0.0;
-            const int mi = lane < n ? S.cidx[lane] : INT_MAX;
-            int rank = 0;
-            for (int j = 0; j < n; ++j) {
-                const double ok = __shfl_sync(0xffffffffu, mk, j);
-                const int oi = __shfl_sync(0xffffffffu, mi, j);
-                rank += better(ok, oi, mk, mi);
-            }
-            if (lane < n && rank < keep) {
-                S.tkey[rank] = mk;
-                S.tidx[rank] = mi;
-            }
-        }
-    } else {
-        for (int round = 0; round < keep; ++round) {
-            double bk = 0.0;
-            int bi = INT_MAX, bp = -1;
-            for (int e = tid; e < n; e += PK_T) {
-                const int ix = S.cidx[e];
-                if (ix >= 0 && (bp < 0 || better(S.key[e], ix, bk, bi))) {
-                    bk = S.key[e];
-                    bi = ix;
-                    bp = e;
-                }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
-                    bk = ok;
-                    bi = oi;
-                    bp = op;
-                }
-            }
-            if (lane == 0) {
-                S.rk[wid] = bk;
-                S.ri[wid] = bi;
-                S.rp[wid] = bp;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                for (int w = 1; w < PK_T / 32; ++w)
-                    if (S.rp[w] >= 0 && (bp < 0 || better(S.rk[w], S.ri[w], bk, bi))) {
-                        bk = S.rk[w];
-                        bi = S.ri[w];
-                        bp = S.rp[w];
-                    }
-                S.tkey[round] = bk;
-                S.tidx[round] = bi;
-                S.cidx[bp] = -1;
-            }
-            __syncthreads();
-        }
-    }
-    ntop = keep;
-    __syncthreads();
-}
-
-__global__ void __launch_bounds__(PK_T, 3)
-    select_pick_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
-    __shared__ PickSmem S;
-    const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    pdl_trigger();
-    tl_mark(P.tl, 2);
-    pdl_wait();
-    tl_mark(P.tl, 0);
-    if (slot >= nj) return;
-    const int gj = job0 + slot;
-    const Job jb = jobs[gj];
-    const int Tc = P.Tc;
-    long long pclk0 = clock64(), pclk1 = 0, pclk2 = 0;
-    int fr, fc;
-    if (jb.shape == kNone) {
-        fr = jb.fr;
-        fc = jb.fc;
-    } else {
-        const int n = P.ncand[slot];
-        if (n == -2) return;  // select_bulk_kernel
-        const int K = P.K;
-        // stage the fp64 template (matcher.hpp:44-61 order) and the mask rows
-        const double* tmg = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
-        const int ntm = P.nch * Tc * Tc;
-        const double* tmS = tmg;
-        if (ntm <= PK_TMC) {
-            for (int e = tid; e < ntm; e += PK_T) cp_async8(&S.tm[e], tmg + e);
-            tmS = S.tm;
-        }
-        int nr = 0;
-        for (int s0 = 0; s0 < Tc; s0 += 32) {
-            const int s = s0 + lane;
-            int t0 = 0, t1 = 0;
-            if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
-            const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
-            if (wid == 0 && t1 > t0) S.rows[nr + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
-            nr += __popc(m);
-        }
-        const int R = nr * P.nch;
-        int ntop = 0;
-        if (n >= 0) {
-            const int* cd = P.cand + static_cast<size_t>(slot) * SC_LC;
-            for (int e = tid; e < n; e += PK_T) S.cidx[e] = cd[e];
-            cp_async_wait_all();
-            __syncthreads();
-            pclk1 = clock64();
-            pick_batch(P, S, tmS, R, n, ntop, K);
-            pclk2 = clock64();
-        } else {
-            // list overflow without the bulk kernel: every window >= M_K, in batches
-            const int thr = P.cthr[slot];
-            const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
-            const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
-            cp_async_wait_all();
-            int cnt = 0;
-            for (int t = 0; t < P.ntiles; ++t) {
-                if (tmx[t] < thr) continue;  // uniform
-                const int p = t * kTcTile + tid;
-                const bool q = tid < kTcTile && p < P.npos && sc[p] >= thr;
-                const unsigned bal = __ballot_sync(0xffffffffu, q);
-                if (lane == 0) S.wc[wid] = __popc(bal);
-                __syncthreads();
-                int off = 0, tot = 0;
-                for (int w = 0; w < PK_T / 32; ++w) {
-                    off += w < wid ? S.wc[w] : 0;
-                    tot += S.wc[w];
-                }
-                if (cnt + tot > SC_LC) {
-                    pick_batch(P, S, tmS, R, cnt, ntop, K);
-                    cnt = 0;
-                }
-                if (q) S.cidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
-                cnt += tot;
-                __syncthreads();
-            }
-            if (cnt > 0) pick_batch(P, S, tmS, R, cnt, ntop, K);
-        }
-        // choose (matcher.hpp:207-241)
-        if (wid == 0) {
-            const int pos = choose_pick(P, jb, S.tidx, ntop, lane);
-            if (lane == 0) S.misc[0] = pos;
-        }
-        __syncthreads();
-        const int pos = S.misc[0];
-        fr = (pos / P.out_w) << P.J;
-        fc = (pos % P.out_w) << P.J;
-    }
-    // source-block map (+ optional trace), simulator.hpp:483-493
-    paste_job<PK_T>(P, jb, gj, fr, fc, tid);
-    if (tid == 0) {
-        P.chosen[2 * gj] = fr;
-        P.chosen[2 * gj + 1] = fc;
-        if (P.tl && P.stats && pclk2) {
-            atomicAdd(&P.stats[12], static_cast<unsigned long long>(pclk1 - pclk0));
-            atomicAdd(&P.stats[13], static_cast<unsigned long long>(pclk2 - pclk1));
-            atomicAdd(&P.stats[4], static_cast<unsigned long long>(clock64() - pclk2));
-        }
-    }
-    tl_mark(P.tl, 1);
 }
 
 // ---------------------------------------------------- fused fast select --
@@ -1759,7 +1486,9 @@ __global__ void __launch_bounds__(BK_T, 1)
     select_bulk_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj, int S) {
     extern __shared__ __align__(16) unsigned char bk_sm[];
     pdl_trigger();
+    tl_mark(P.tl, 2);
     pdl_wait();
+    tl_mark(P.tl, 0);
     const int slot = blockIdx.y, part = blockIdx.x;
     if (slot >= nj) return;
     const int thr = P.defer[slot];
@@ -2050,6 +1779,7 @@ __global__ void __launch_bounds__(BK_T, 1)
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
     }
+    tl_mark(P.tl, 1);
 }
 
 // ----------------------------------------------------------- finalize ----
@@ -2104,18 +1834,17 @@ __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww
 // Progressive finalize: band descriptors (realization, axis, lo, hi) in
 // output coordinates -- axis 0: rows [lo, hi) x every column; axis 1: every
 // row x columns [lo, hi).  A band is final once every placement covering it
-// is done (run_simulation's checkpoints), so it is rebuilt -- in place for
-// row bands, packed at boff[band] in a staging buffer for column bands -- and
-// copied to the host while later waves still compute.
-__global__ void finalize_band_kernel(const int4* __restrict__ bands, const size_t* __restrict__ boff,
-                                     const uint8_t* __restrict__ work,
+// is done (run_simulation's checkpoints), so it is rebuilt and copied to the
+// host while later waves still compute.
+__global__ void finalize_band_kernel(const int4* __restrict__ bands, const uint8_t* __restrict__ work,
                                      int wh, int ww, const int32_t* __restrict__ src, int B, int J,
                                      int swc, const uint8_t* __restrict__ ti, int ti_w, int wc,
                                      const uint8_t* __restrict__ hd, int sg_h, int sg_w,
-                                     uint8_t* __restrict__ out, uint8_t* __restrict__ stage, int* mism) {
+                                     uint8_t* __restrict__ out, int* mism, unsigned long long* tl) {
+    tl_mark(tl, 2);
     pdl_wait();
+    tl_mark(tl, 0);
     const int4 bd = bands[blockIdx.y];
-    const size_t pk = boff[blockIdx.y];
     const int r = bd.x;
     const int rows = bd.y == 0 ? bd.w - bd.z : sg_h;
     const int cols = bd.y == 0 ? sg_w : bd.w - bd.z;
@@ -2142,15 +1871,13 @@ __global__ void finalize_band_kernel(const int4* __restrict__ bands, const size_
                 v = h;
             }
         }
-        if (pk == ~static_cast<size_t>(0))
-            out[(static_cast<size_t>(r) * sg_h + y) * sg_w + x] = v;  // in place (row band)
-        else
-            stage[pk + e] = v;  // packed, the band's cells row-major (column band)
+        out[(static_cast<size_t>(r) * sg_h + y) * sg_w + x] = v;
     }
     if (hd) {
         for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
         if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
     }
+    tl_mark(tl, 1);
 }
 
 // min_cut_stitch as a stand-alone operator (the drop-in API surface).
@@ -2543,12 +2270,6 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.bulk_keys = ctx->bulk_keys.as<double>(G * maxj * BK_SMAX * kTcQ);
         P.bulk_idx = ctx->bulk_idx.as<int>(G * maxj * BK_SMAX * kTcQ);
     }
-    const bool split_select = getenv("CCW_SPLIT_SELECT") != nullptr;  // scan + pick kernels (r1 A/B)
-    if (warp_select) {
-        P.cand = ctx->cand.as<int>(G * maxj * SC_LC);
-        P.ncand = ctx->ncand.as<int>(G * maxj);
-        P.cthr = ctx->cthr.as<int>(G * maxj);
-    }
     if (bulk_smem)
         CCW_CUDA(cudaFuncSetAttribute(select_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(bulk_smem)));
@@ -2561,11 +2282,6 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         GP[g].tmax = d_tmax ? d_tmax + g * maxj * ntiles : nullptr;
         GP[g].cjob = d_cjob ? d_cjob + g * maxj : nullptr;
         GP[g].defer = d_defer ? d_defer + g * maxj : nullptr;
-        if (warp_select) {
-            GP[g].cand = P.cand + g * maxj * SC_LC;
-            GP[g].ncand = P.ncand + g * maxj;
-            GP[g].cthr = P.cthr + g * maxj;
-        }
         if (d_defer) {
             GP[g].bulk_sync = P.bulk_sync + 2 * g * maxj;
             GP[g].bulk_keys = P.bulk_keys + g * maxj * BK_SMAX * kTcQ;
@@ -2613,6 +2329,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // no remaining placement covers are finalized and copied back at a few
     // checkpoint waves, overlapping the copy with the remaining waves
     uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
+    const size_t out_bytes = static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real;
+    // device->host copies need page-locked memory to run asynchronously: a
+    // pageable destination gets a pinned staging buffer, copied out at the end
+    uint8_t* h_dst = h_out;
+    if (h_out) {
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, h_out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (!pinned) h_dst = static_cast<uint8_t*>(ctx->h_out_stage.get(out_bytes));
+    }
     const bool stream_out = h_out && !getenv("CCW_NO_STREAM_OUT");
     std::vector<int4> bands;                                   // all checkpoints, in launch order
     std::vector<std::vector<std::pair<int, std::pair<size_t, size_t>>>> band_at(G);  // per group: (wave, [off, off+n))
@@ -2649,14 +2375,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         }
     }
     int4* d_bands = nullptr;
-    size_t* d_boff = nullptr;
-    std::vector<size_t> boff(bands.size() + 1, 0);  // packed staging offsets (launch order)
     if (!bands.empty()) {
-        for (size_t q = 0; q < bands.size(); ++q) boff[q] = ~static_cast<size_t>(0);  // all in place
-        d_bands = reinterpret_cast<int4*>(ctx->ops_b.get(sizeof(int4) * bands.size() + sizeof(size_t) * boff.size()));
-        d_boff = reinterpret_cast<size_t*>(d_bands + bands.size());
+        d_bands = reinterpret_cast<int4*>(ctx->ops_b.get(sizeof(int4) * bands.size()));
         CCW_CUDA(cudaMemcpyAsync(d_bands, bands.data(), sizeof(int4) * bands.size(), cudaMemcpyHostToDevice, st));
-        CCW_CUDA(cudaMemcpyAsync(d_boff, boff.data(), sizeof(size_t) * boff.size(), cudaMemcpyHostToDevice, st));
     }
     std::vector<size_t> band_next(G, 0);
 
@@ -2742,21 +2463,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 if (skip_sel && !first_wave) {
                 } else if (warp_select || (first_wave && !cfg.min_cut)) {
                     const Job* dj = d_jobs;
-                    if (!split_select) {
-                        launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
-                                   static_cast<int>(j0), nj);
-                    } else {
-                        if (!first_wave) {
-                            launch_pdl(select_scan_kernel, dim3((nj + SC_WARPS - 1) / SC_WARPS),
-                                       dim3(SC_WARPS * 32), 0, gs, Q, dj, static_cast<int>(j0), nj);
-                            ++launches;
-                            Q.tl = tl_next(w, g, 3);
-                        }
-                        launch_pdl(select_pick_kernel, dim3(nj), dim3(PK_T), 0, gs, Q, dj,
-                                   static_cast<int>(j0), nj);
-                    }
+                    launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
+                               static_cast<int>(j0), nj);
                     if (Q.defer && !first_wave) {
-                        Q.tl = nullptr;
+                        Q.tl = tl_next(w, g, 5);
                         launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, Q, dj,
                                    static_cast<int>(j0), nj, bulk_S);
                         ++launches;
@@ -2775,12 +2485,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             if (band_next[g] < band_at[g].size() && band_at[g][band_next[g]].first == w) {
                 const auto rng = band_at[g][band_next[g]++].second;
                 const int nb = static_cast<int>(rng.second - rng.first);
-                launch_pdl(finalize_band_kernel, dim3(32, nb), dim3(256), 0, gs,
-                           static_cast<const int4*>(d_bands + rng.first), static_cast<const size_t*>(d_boff + rng.first),
-                           static_cast<const uint8_t*>(d_work),
+                size_t most = 1;  // cells of the largest band: enough CTAs to cover it
+                for (size_t q = rng.first; q < rng.second; ++q)
+                    most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
+                                              (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
+                const int bxb = static_cast<int>(std::min<size_t>((most + 255) / 256, 1024));
+                launch_pdl(finalize_band_kernel, dim3(bxb, nb), dim3(256), 0, gs,
+                           static_cast<const int4*>(d_bands + rng.first), static_cast<const uint8_t*>(d_work),
                            wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
                            static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
-                           static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, static_cast<uint8_t*>(nullptr), d_mism);
+                           static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, d_mism, tl_next(w, g, 4));
                 ++launches;
                 // copies on their own stream (the group's next wave does not wait),
                 // straight into the caller's buffer; adjacent ranges merged
@@ -2791,7 +2505,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 size_t o0 = 0, o1 = 0;
                 auto flush = [&] {
                     if (o1 > o0)
-                        CCW_CUDA(cudaMemcpyAsync(h_out + o0, fin + o0, o1 - o0, cudaMemcpyDeviceToHost,
+                        CCW_CUDA(cudaMemcpyAsync(h_dst + o0, fin + o0, o1 - o0, cudaMemcpyDeviceToHost,
                                                  ctx->copy_stream));
                     o0 = o1 = 0;
                 };
@@ -2831,8 +2545,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     CCW_CUDA(cudaEventRecord(ev1, st));
     if (h_out && !stream_out)
-        CCW_CUDA(cudaMemcpyAsync(h_out, fin, static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real,
-                                 cudaMemcpyDeviceToHost, st));
+        CCW_CUDA(cudaMemcpyAsync(h_dst, fin, out_bytes, cudaMemcpyDeviceToHost, st));
     unsigned long long stats[16] = {0};
     CCW_CUDA(cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
     std::vector<int> mism(n_real, 0);
@@ -2847,6 +2560,14 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaMemcpyAsync(pasted.data(), d_pasted, pasted.size(), cudaMemcpyDeviceToHost, st));
     }
     CCW_CUDA(cudaStreamSynchronize(st));
+    if (h_out && h_dst != h_out) {  // pinned staging -> the caller's pageable buffer, in parallel
+        constexpr size_t kChunk = 4u << 20;
+        const int nchunk = static_cast<int>((out_bytes + kChunk - 1) / kChunk);
+        ctx->pool.run(nchunk, [&](int i) {
+            const size_t o = static_cast<size_t>(i) * kChunk;
+            std::memcpy(h_out + o, h_dst + o, std::min(kChunk, out_bytes - o));
+        });
+    }
 
     {
         float ms = 0;
@@ -2887,7 +2608,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         tc_probe_buffer = nullptr;
     }
     if (getenv("CCW_PHASES"))
-        fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast|pick[scan+stage %llu batch %llu choose+map %llu]"
+        fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
                 stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[4], stats[7], stats[14],
                 stats[15], stats[5], stats[6]);
