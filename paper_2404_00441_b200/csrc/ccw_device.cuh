@@ -29,6 +29,9 @@ struct Job {
     int32_t pick;    // unconditional: precomputed bounded(rng, K') draw; -1 = conditional
     int32_t fr;      // first placement: precomputed block-aligned TI origin
     int32_t fc;
+    int32_t dep0;    // fused OR prep: flat index of a next-wave placement that reads this
+    int32_t dep1;    //   one's paste ((o, i+1) and (o+1, i-1)), -1 = none
+    int32_t ndep;    //   previous-wave placements this one reads ((o, i-1), (o-1, i+1))
 };
 
 // Parameters shared by every job of one simulate call.
@@ -68,6 +71,13 @@ struct SimParams {
     int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
     int sld;
     int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
+    // fused OR prep: the select of wave w prepares the placements of wave w+1
+    // once both of their wave-w dependencies have pasted (null: separate launch)
+    int* depcnt;             // per next-wave slot: dependencies that have pasted
+    int next_j0;             // flat index of the next wave's first job (this group)
+    int8_t* n_wts8;          // next wave's prep outputs (the other parity buffers)
+    double* n_tm64;
+    int32_t* n_cjob;
     unsigned long long* tl;  // debug timeline slot of this launch (null unless CCW_TIMELINE)
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
     int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)

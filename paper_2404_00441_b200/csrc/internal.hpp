@@ -216,7 +216,7 @@ struct ccw_ctx {
     int ccf_variant = 0;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf cjob, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, ops_a, ops_b, ops_c, ops_d, ops_e;
     ccwgpu::HostBuf h_stage;
     ccwgpu::HostBuf h_out_stage;  // pinned landing zone when the caller's result buffer is pageable

@@ -69,15 +69,16 @@ void build_pyramid(ccw_ti* ti, cudaStream_t s) {
 // Normalized screen: C_job = B^2 * sum over the mask of the OR's last-facies
 // block count, so the screen S' (F-1 channels) plus C_job is the full
 // count score S (indicator mode; 0 in raw-codes mode).
-__device__ __forceinline__ void store_cjob(const SimParams& P, int slot, int csum) {
+__device__ __forceinline__ void store_cjob(int32_t* cjob, int mode, int B, int slot, int csum) {
     __shared__ int red[32];
     for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    __syncthreads();  // (red may be in use by an earlier call)
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = csum;
     __syncthreads();
     if (threadIdx.x == 0) {
         int t = 0;
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
-        P.cjob[slot] = P.mode == 0 ? P.B * P.B * t : 0;
+        cjob[slot] = mode == 0 ? B * B * t : 0;
     }
 }
 
@@ -90,18 +91,17 @@ __device__ __forceinline__ void store_cjob(const SimParams& P, int slot, int csu
 // block (pastes are block aligned, simulator.hpp:452-453, 480-483), so the OR's
 // counts and reference-order apex values are gathers from the TI pyramid at
 // the recorded source block -- identical values, no recomputation.
-__global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
-    pdl_trigger();
-    const int slot = blockIdx.x;
-    const Job jb = jobs[job0 + slot];
-    tl_mark(P.tl, 2);
-    pdl_wait();
-    tl_mark(P.tl, 0);
+// One placement's OR preparation from the source-block map (every thread of
+// the calling CTA takes part; the CTA size is free).  Outputs go to the given
+// per-slot bases: the int8 screen weights (w8base, or the int32 weights of the
+// fp32 screen when w8base is null), the fp64 template and C_job.
+__device__ __forceinline__ void prep_src_job(const SimParams& P, const Job& jb, int slot, int8_t* w8base,
+                                             double* tmbase, int32_t* cjobbase) {
     const int Tc = P.Tc, B = P.B, nc = P.hc * P.wc;
     const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc;
-    int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
-    double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
-    int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
+    int32_t* wts = w8base ? nullptr : P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
+    double* tm = tmbase + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+    int8_t* w8 = w8base ? w8base + static_cast<size_t>(slot) * P.kpad : nullptr;
     if (w8)
         for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x) w8[k] = 0;
     int csum = 0;
@@ -118,13 +118,25 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
         for (int f = 0; f < P.nscr; ++f) {
             const int n = static_cast<int>(P.tiscr[static_cast<size_t>(f) * nc + sb]);
             const int v = in ? (P.mode == 0 ? n - last : n) : 0;
-            wts[f * Tc * Tc + c] = v;
-            if (w8) w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
+            if (w8)
+                w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
+            else
+                wts[f * Tc * Tc + c] = v;
         }
         for (int ch = 0; ch < P.nch; ++ch)
             tm[ch * Tc * Tc + c] = in ? P.ti64[static_cast<size_t>(ch) * nc + sb] : 0.0;
     }
-    if (P.cjob) store_cjob(P, slot, csum);
+    if (cjobbase) store_cjob(cjobbase, P.mode, P.B, slot, csum);
+}
+
+__global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    pdl_trigger();
+    const int slot = blockIdx.x;
+    const Job jb = jobs[job0 + slot];
+    tl_mark(P.tl, 2);
+    pdl_wait();
+    tl_mark(P.tl, 0);
+    prep_src_job(P, jb, slot, P.wts8, P.tm64, P.cjob);
     tl_mark(P.tl, 1);
 }
 
@@ -164,7 +176,7 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
         for (int ch = 0; ch < P.nch; ++ch)
             tm[ch * Tc * Tc + c] = in ? haar_apex_block(base, P.ww, P.J, P.mode, ch) : 0.0;
     }
-    if (P.cjob) store_cjob(P, slot, csum);
+    if (P.cjob) store_cjob(P.cjob, P.mode, P.B, slot, csum);
 }
 
 // --------------------------------------------------------- CCF screen ----
@@ -1127,6 +1139,34 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
     return cnt;
 }
 
+// Fused OR prep (select epilogue): after this placement's source-block map
+// is written, count it against each next-wave placement that reads it; the
+// CTA that completes a dependent's count prepares that dependent (its OR
+// weights, template and C_job) into the next wave's buffers.  Every thread
+// of the CTA calls this (it synchronizes).
+__device__ __forceinline__ void prep_dependents(const SimParams& P, const Job* __restrict__ jobs,
+                                                const Job& jb, int* flag) {
+    if (!P.depcnt) return;
+    __syncthreads();  // this CTA's map writes are issued
+    for (int q = 0; q < 2; ++q) {
+        const int d = q == 0 ? jb.dep0 : jb.dep1;  // uniform
+        if (d < 0) continue;
+        if (threadIdx.x == 0) {
+            __threadfence();  // release the map writes before counting
+            const int need = jobs[d].ndep;
+            const int old = atomicAdd(&P.depcnt[d - P.next_j0], 1);
+            *flag = old == need - 1;
+            if (*flag) {
+                P.depcnt[d - P.next_j0] = 0;  // reset for the next use of this slot
+                __threadfence();              // acquire the other dependency's writes
+            }
+        }
+        __syncthreads();
+        if (*flag) prep_src_job(P, jobs[d], d - P.next_j0, P.n_wts8, P.n_tm64, P.n_cjob);
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------- fused fast select --
 //
 // One 128-thread CTA per placement: warp 0 scans (scan_job) while warps 1-3
@@ -1425,6 +1465,7 @@ __global__ void __launch_bounds__(FS_T, 4)
         fc = (pos % P.out_w) << P.J;
     }
     paste_job<FS_T>(P, jb, gj, fr, fc, tid);
+    prep_dependents(P, jobs, jb, &S.misc[5]);
     if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
@@ -1775,6 +1816,7 @@ __global__ void __launch_bounds__(BK_T, 1)
     const int pos = shv[3];
     const int fr = (pos / P.out_w) << P.J, fc = (pos % P.out_w) << P.J;
     paste_job<BK_T>(P, jb, gj, fr, fc, tid);
+    prep_dependents(P, jobs, jb, shv + 4);  // (misc + 304: free)
     if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
@@ -2089,8 +2131,21 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         const Plan& p = variants[vid[r]];
         size_t* off = roff.data() + static_cast<size_t>(r) * nkeys;
         const int cnt = static_cast<int>(p.tops.size());
+        // flat index of every placement (in placement order within each wave bucket)
+        std::vector<int32_t> fi(cnt);
+        {
+            std::vector<size_t> o2(off, off + nkeys);
+            for (int k = 0; k < cnt; ++k) fi[k] = static_cast<int32_t>(o2[keymul * p.outer_idx[k] + p.inner_idx[k]]++);
+        }
+        const int ni = p.n_inner, no = p.n_outer;
         for (int k = 0; k < cnt; ++k) {
             Job jb;
+            {  // raster neighbours (k = o * n_inner + i): next-wave readers, previous-wave writers
+                const int o = p.outer_idx[k], i = p.inner_idx[k];
+                jb.dep0 = i + 1 < ni ? fi[k + 1] : -1;
+                jb.dep1 = (o + 1 < no && i >= 1) ? fi[k + ni - 1] : -1;
+                jb.ndep = (i >= 1 ? 1 : 0) + (o >= 1 && i + 1 < ni ? 1 : 0);
+            }
             jb.real = r;
             jb.place = k;
             jb.top = p.tops[k];
@@ -2161,7 +2216,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const size_t maxj = std::max<size_t>(1, std::min<size_t>(max_wave, score_budget / (sizeof(int32_t) * sld)));
     int32_t* d_scores = ctx->scores.as<int32_t>(G * maxj * sld);
     int32_t* d_wts = ctx->wts.as<int32_t>(G * maxj * std::max(ti->nscr, 1) * Tc * Tc);
-    double* d_tm = ctx->tm64.as<double>(G * maxj * ti->nch * Tc * Tc);
+    // prep outputs (template, screen weights) have two parity halves: with the
+    // fused OR prep, wave w's select writes wave w+1's half while wave w reads its own
+    double* d_tm = ctx->tm64.as<double>(2 * G * maxj * ti->nch * Tc * Tc);
     int32_t* d_chosen = ctx->chosen.as<int32_t>(2 * total_jobs);
     uint8_t* d_pasted = traces ? ctx->pasted.as<uint8_t>(total_jobs * T * T) : nullptr;
     int* d_mism = ctx->mism.as<int>(n_real);
@@ -2218,7 +2275,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     int32_t* d_tmax = nullptr;
     if (use_tc) {
         d_x = ti_im2col(ti, Tc, st);
-        d_w8 = ctx->wts8.as<int8_t>(G * maxj * kpad);
+        d_w8 = ctx->wts8.as<int8_t>(2 * G * maxj * kpad);
         d_tmax = ctx->summary.as<int32_t>(G * maxj * ntiles);
     }
     int32_t* d_cjob = nullptr;
@@ -2289,6 +2346,36 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         }
     }
 
+    // fused OR prep (opt-in, CCW_FUSE_PREP=1): applies with the fast select,
+    // one-step wavefront neighbours (keymul 2) and waves that fit one launch
+    // (the slot of a dependent is its index in the next wave).  Measured r1:
+    // slower (config 1 5.2 -> 5.5 ms, config 2 39 -> 45 ms) -- the completing
+    // CTA's preps lengthen the select's critical path by more than the
+    // separate, fully parallel prep kernel costs.
+    const bool fuse_prep = warp_select && keymul == 2 && max_wave <= maxj && d_src &&
+                           getenv("CCW_FUSE_PREP") != nullptr;
+    int* d_depcnt = nullptr;
+    if (fuse_prep) {
+        d_depcnt = ctx->depcnt.as<int>(G * maxj);
+        CCW_CUDA(cudaMemsetAsync(d_depcnt, 0, sizeof(int) * G * maxj, st));
+    }
+    // per (group, parity) parameter sets
+    std::vector<std::array<SimParams, 2>> GPP(G);
+    const size_t tm_half = G * maxj * ti->nch * Tc * Tc, w8_half = G * maxj * kpad;
+    for (int g = 0; g < G; ++g)
+        for (int par = 0; par < 2; ++par) {
+            SimParams& Q = GPP[g][par];
+            Q = GP[g];
+            Q.tm64 = GP[g].tm64 + par * tm_half;
+            Q.wts8 = GP[g].wts8 ? GP[g].wts8 + par * w8_half : nullptr;
+            if (fuse_prep) {
+                Q.depcnt = d_depcnt + g * maxj;
+                Q.n_tm64 = GP[g].tm64 + (1 - par) * tm_half;
+                Q.n_wts8 = GP[g].wts8 ? GP[g].wts8 + (1 - par) * w8_half : nullptr;
+                Q.n_cjob = nullptr;  // (raw scoring only)
+            }
+        }
+
     const size_t ccf_smem = ccf_smem_bytes(Tc, ti->nscr);
     const size_t sel_smem = sel_layout(Kp, T, OV, ti->nch, Tc, cfg.scoring == 1).total;
     if (ccf_smem > 227 * 1024 || sel_smem > 227 * 1024)
@@ -2304,10 +2391,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaMemsetAsync(d_probe, 0, 8 * sizeof(unsigned long long), st));
     }
     tc_probe_buffer = d_probe;
-    std::vector<TcPlan> tcplans;
+    std::vector<std::array<TcPlan, 2>> tcplans(G);
     if (use_tc)
         for (int g = 0; g < G; ++g)
-            tcplans.push_back(plan_ccf_tc(GP[g].wts8, static_cast<int>(maxj), d_x, npos, kpad));
+            for (int par = 0; par < 2; ++par)
+                tcplans[g][par] = plan_ccf_tc(GPP[g][par].wts8, static_cast<int>(maxj), d_x, npos, kpad);
     // group streams, forked from / joined back to the context stream
     if (!ctx->copy_stream) CCW_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     while (static_cast<int>(ctx->gstreams.size()) < G) {
@@ -2408,20 +2496,23 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     for (int w = 0; w <= max_key; ++w) {
         for (int g = 0; g < G; ++g) {
             cudaStream_t gs = ctx->gstreams[g];
-            SimParams Q = GP[g];
+            const int par = fuse_prep ? (w & 1) : 0;
+            SimParams Q = GPP[g][par];
+            Q.next_j0 = static_cast<int>(wave_off[g][std::min(w + 1, nkeys)]);
             for (size_t j0 = wave_off[g][w]; j0 < wave_off[g][w + 1]; j0 += maxj) {
                 const int nj = static_cast<int>(std::min(maxj, wave_off[g][w + 1] - j0));
                 const bool first_wave = flat[j0].shape == kNone;
                 if (!first_wave) {
                     Q.tl = tl_next(w, g, 0);
-                    if (skip_prep) {
-                    } else if (d_src)
-                        launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
-                                   static_cast<const Job*>(d_jobs), static_cast<int>(j0));
-                    else
-                        launch_pdl(or_prep_kernel, dim3(nj), dim3(128), 0, gs, Q,
-                                   static_cast<const Job*>(d_jobs), static_cast<int>(j0));
-                    ++launches;
+                    if (!skip_prep && !fuse_prep) {  // (fused: prepared by the previous wave's select)
+                        if (d_src)
+                            launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
+                                       static_cast<const Job*>(d_jobs), static_cast<int>(j0));
+                        else
+                            launch_pdl(or_prep_kernel, dim3(nj), dim3(128), 0, gs, Q,
+                                       static_cast<const Job*>(d_jobs), static_cast<int>(j0));
+                        ++launches;
+                    }
                     if (any_screen) {
                         cudaEvent_t a = nullptr, b = nullptr;
                         if (ctx->profiling) {
@@ -2431,7 +2522,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         }
                         if (skip_ccf) {
                         } else if (use_tc) {
-                            launch_ccf_tc(tcplans[g], npos, sld, kpad, nj, Q.scores, Q.tmax, gs,
+                            launch_ccf_tc(tcplans[g][par], npos, sld, kpad, nj, Q.scores, Q.tmax, gs,
                                           tl_next(w, g, 1));
                         } else {
                             launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, ccf_grid_xy.y, nj),
