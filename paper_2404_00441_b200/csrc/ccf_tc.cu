@@ -187,7 +187,10 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
 // issues the MMAs into one of two TMEM accumulators, warps 2..9 drain the
 // other accumulator -- the epilogue of tile i overlaps the loads and MMAs of
 // tile i+1.
-__global__ void __launch_bounds__(kThreads, 1)
+#ifndef CCW_TC_MINB
+#define CCW_TC_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
     ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   TcArgs a) {
     extern __shared__ __align__(1024) uint8_t tc_sm_raw[];

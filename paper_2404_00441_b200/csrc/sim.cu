@@ -825,7 +825,10 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
 // select_bulk_kernel.
 constexpr int SC_LC = 256;     // list / candidate capacity per placement
 constexpr int SC_TB = 8;       // qualifying tiles read per round trip
-constexpr int PK_TMC = 1024;   // fp64 template values staged in shared memory (when they fit)
+#ifndef CCW_PK_TMC
+#define CCW_PK_TMC 1024
+#endif
+constexpr int PK_TMC = CCW_PK_TMC;   // fp64 template values staged in shared memory (when they fit)
 constexpr int PK_MAXTC = 64;   // template rows tabulated
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -965,6 +968,7 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
 struct ScanWarp {
     int lv[SC_LC];
     int lp[SC_LC];
+    int tq[SC_TB];  // queued qualifying tiles
 };
 
 // Warp-level scan of one placement (every lane of the warp calls it): the
@@ -1026,9 +1030,49 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
     }
     sclk[1] = clock64();
     // 2. every window scoring >= M_K, from the tiles whose maximum reaches it,
-    //    into a (score, position) list; SC_TB tiles per round trip
-    int nl = 0;
+    //    into a (score, position) list.  Qualifying tiles are queued across the
+    //    32-tile groups and loaded SC_TB per round trip.
+    int nl = 0, ntl = 0;
     bool over = false;
+    auto flush_tiles = [&]() {
+        __syncwarp();
+        int tl[SC_TB], v[SC_TB][4];
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u) tl[u] = u < ntl ? W.tq[u] : -1;
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u) {
+            const int p0 = tl[u] * kTcTile + lane * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
+            if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
+                const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
+                v[u][0] = a4.x;
+                v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
+                v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
+                v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const bool q = v[u][i] != INT_MIN && v[u][i] >= mk;  // scores are never INT_MIN
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (!bal) continue;
+                if (nl + __popc(bal) > SC_LC) {
+                    over = true;
+                    continue;
+                }
+                if (q) {
+                    const int o = nl + __popc(bal & ((1u << lane) - 1));
+                    W.lv[o] = v[u][i];
+                    W.lp[o] = tl[u] * kTcTile + lane * 4 + i;
+                }
+                nl += __popc(bal);
+            }
+        ntl = 0;
+        __syncwarp();
+    };
 #pragma unroll 1
     for (int i0 = 0; i0 * 32 < P.ntiles && !over; ++i0) {
         const int t0 = i0 * 32;
@@ -1042,48 +1086,12 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
         }
         unsigned tiles = __ballot_sync(0xffffffffu, mine != INT_MIN && mine >= mk);
         while (tiles && !over) {
-            int tl[SC_TB], v[SC_TB][4];
-#pragma unroll
-            for (int u = 0; u < SC_TB; ++u) {
-                tl[u] = -1;
-                if (tiles) {
-                    tl[u] = t0 + __ffs(tiles) - 1;
-                    tiles &= tiles - 1;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < SC_TB; ++u) {
-                const int p0 = tl[u] * kTcTile + lane * 4;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
-                if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
-                    const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
-                    v[u][0] = a4.x;
-                    v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
-                    v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
-                    v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < SC_TB; ++u)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const bool q = v[u][i] != INT_MIN && v[u][i] >= mk;  // scores are never INT_MIN
-                    const unsigned bal = __ballot_sync(0xffffffffu, q);
-                    if (!bal) continue;
-                    if (nl + __popc(bal) > SC_LC) {
-                        over = true;
-                        continue;
-                    }
-                    if (q) {
-                        const int o = nl + __popc(bal & ((1u << lane) - 1));
-                        W.lv[o] = v[u][i];
-                        W.lp[o] = tl[u] * kTcTile + lane * 4 + i;
-                    }
-                    nl += __popc(bal);
-                }
+            if (lane == 0) W.tq[ntl] = t0 + __ffs(tiles) - 1;
+            tiles &= tiles - 1;
+            if (++ntl == SC_TB) flush_tiles();
         }
     }
+    if (ntl > 0 && !over) flush_tiles();
     __syncwarp();
     sclk[2] = clock64();
 #ifdef CCW_DBG_STATS
@@ -1179,8 +1187,14 @@ __device__ __forceinline__ void prep_dependents(const SimParams& P, const Job* _
 // source-block map.
 constexpr int FS_T = 128;
 constexpr int FS_G = 16;       // cells per rescoring item
-constexpr int FS_MAXG = 512;   // run groups per placement
-constexpr int FS_RS = 1536;    // (window, run) partial sums per batch
+#ifndef CCW_FS_MAXG
+#define CCW_FS_MAXG 512
+#endif
+constexpr int FS_MAXG = CCW_FS_MAXG;   // run groups per placement
+#ifndef CCW_FS_RS
+#define CCW_FS_RS 1536
+#endif
+constexpr int FS_RS = CCW_FS_RS;    // (window, run) partial sums per batch
 
 struct FastSmem {
     double tm[PK_TMC];
@@ -1261,8 +1275,18 @@ __device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, cons
         }
         __syncthreads();
         for (int e = tid; e < ng; e += FS_T) {
+            // the fold is one sequential chain; its operands load 8 at a time
+            const double* rp = S.rsum + e * R;
             double acc = 0.0;
-            for (int r = 0; r < R; ++r) acc = __dadd_rn(acc, S.rsum[e * R + r]);
+            int r = 0;
+            for (; r + 8 <= R; r += 8) {
+                double x[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x[i] = rp[r + i];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc = __dadd_rn(acc, x[i]);
+            }
+            for (; r < R; ++r) acc = __dadd_rn(acc, rp[r]);
             S.key[e0 + e] = acc;
         }
         __syncthreads();
@@ -1336,7 +1360,10 @@ __device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, cons
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(FS_T, 4)
+#ifndef CCW_FS_MINB
+#define CCW_FS_MINB 4
+#endif
+__global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     select_fast_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
     __shared__ FastSmem S;
     const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
