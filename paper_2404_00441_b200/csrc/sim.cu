@@ -2461,20 +2461,27 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         int nck = 6;
         if (const char* e = getenv("CCW_STREAM_BANDS")) nck = std::max(1, atoi(e));
         const int delta = std::max(1, (max_key + 1 + nck - 1) / nck);
+        // column-major raster paths free whole columns: strided copies, slower
+        // per byte -- emitted whole at the last wave (CCW_STREAM_COLS=1: every
+        // other checkpoint; measured slower end to end, r1)
+        const char* ce = getenv("CCW_STREAM_COLS");
+        const bool stream_cols = ce && atoi(ce) != 0;  // measured slower (r1): off by default
         std::vector<int> done(n_real, 0);  // raster-outer extent already emitted
+        int ck = 0;
         for (int w = 0; w <= max_key; ++w) {
             if ((w + 1) % delta != 0 && w != max_key) continue;
+            const bool col_ck = w == max_key || (stream_cols && (ck & 1));
+            ++ck;
             for (int g = 0; g < G; ++g) {
                 const size_t off = bands.size();
                 for (int r = 0; r < n_real; ++r) {
                     if (group_of(r) != g) continue;
                     const Plan& p = variants[vid[r]];
-                    // column-major raster paths free whole columns, which would be strided copies
-                    // (slow DMA): those realizations are emitted whole at the last wave
-                    if (p.column_major && w != max_key) continue;
-                    const int axis = 0;
-                    const bool asc = p.column_major || p.origin == CCW_TOP_LEFT || p.origin == CCW_TOP_RIGHT;
-                    const int extent = wh, sg_ext = cfg.sg_height;
+                    if (p.column_major && !col_ck) continue;
+                    const int axis = p.column_major ? 1 : 0;
+                    const bool asc = axis == 0 ? (p.origin == CCW_TOP_LEFT || p.origin == CCW_TOP_RIGHT)
+                                               : (p.origin == CCW_TOP_LEFT || p.origin == CCW_BOTTOM_LEFT);
+                    const int extent = axis == 0 ? wh : ww, sg_ext = axis == 0 ? cfg.sg_height : cfg.sg_width;
                     int O = w >= p.n_inner - 1 ? (w - (p.n_inner - 1)) / keymul : -1;
                     O = std::min(O, p.n_outer - 1);
                     const int U = (w == max_key || O == p.n_outer - 1) ? extent : (O + 1) * stride;
@@ -2629,8 +2636,18 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 };
                 for (size_t q = rng.first; q < rng.second; ++q) {
                     const int4 bd = bands[q];
-                    const size_t a0 = static_cast<size_t>(bd.x) * n + static_cast<size_t>(bd.z) * cfg.sg_width;
-                    const size_t a1 = static_cast<size_t>(bd.x) * n + static_cast<size_t>(bd.w) * cfg.sg_width;
+                    const size_t base = static_cast<size_t>(bd.x) * n;
+                    const bool full = (bd.y == 0 && bd.z == 0 && bd.w == cfg.sg_height) ||
+                                      (bd.y == 1 && bd.z == 0 && bd.w == cfg.sg_width);
+                    if (bd.y == 1 && !full) {  // a column band: one strided copy
+                        flush();
+                        CCW_CUDA(cudaMemcpy2DAsync(h_dst + base + bd.z, cfg.sg_width, fin + base + bd.z,
+                                                   cfg.sg_width, bd.w - bd.z, cfg.sg_height,
+                                                   cudaMemcpyDeviceToHost, ctx->copy_stream));
+                        continue;
+                    }
+                    const size_t a0 = full ? base : base + static_cast<size_t>(bd.z) * cfg.sg_width;
+                    const size_t a1 = full ? base + n : base + static_cast<size_t>(bd.w) * cfg.sg_width;
                     if (a0 != o1) flush();
                     if (o1 == 0) o0 = a0;
                     o1 = a1;
