@@ -956,12 +956,14 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
             }
         }
     }
-    if (P.src) {
+    if (P.src) {  // Tc x Tc map entries spread over every thread
         int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc +
                       static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
         const int s0 = (fr / P.B) * P.wc + fc / P.B;
-        for (int a = 0; a < Tc; ++a)
-            for (int b = jt; b < Tc; b += JT) sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
+        for (int e = jt; e < Tc * Tc; e += JT) {
+            const int a = e / Tc, b = e - a * Tc;
+            sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
+        }
     }
 }
 
@@ -1501,6 +1503,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             atomicAdd(&P.stats[12], static_cast<unsigned long long>(fclk[1] - fclk[0]));
             atomicAdd(&P.stats[13], static_cast<unsigned long long>(fclk[2] - fclk[1]));
             atomicAdd(&P.stats[4], static_cast<unsigned long long>(fclk[4] - fclk[2]));
+            atomicAdd(&P.stats[5], static_cast<unsigned long long>(fclk[3] - fclk[2]));  // choose
         }
     }
     tl_mark(P.tl, 1);
