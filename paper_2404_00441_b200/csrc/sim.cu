@@ -979,7 +979,7 @@ struct ScanWarp {
 // Returns the candidate count, or -1 when the list overflowed (then every
 // window >= mk_out must be rescored -- a superset, still exact).
 __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& W, int* out, int& mk_out,
-                                        long long* sclk) {
+                                        long long* sclk, int* out_s = nullptr) {
     const int lane = threadIdx.x & 31;
     const int K = P.K;
     const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
@@ -1143,7 +1143,11 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
         const int e = e0 + lane;
         const bool q = e < nl && W.lv[e] >= thr;
         const unsigned bal = __ballot_sync(0xffffffffu, q);
-        if (q) cd[cnt + __popc(bal & ((1u << lane) - 1))] = W.lp[e];
+        if (q) {
+            const int o = cnt + __popc(bal & ((1u << lane) - 1));
+            cd[o] = W.lp[e];
+            if (out_s) out_s[o] = W.lv[e];
+        }
         cnt += __popc(bal);
     }
     return cnt;
@@ -1203,6 +1207,9 @@ struct FastSmem {
     double rsum[FS_RS];
     double key[SC_LC + kTcQ];
     int cidx[SC_LC + kTcQ];
+    int cs[SC_LC];          // the candidates' screen scores
+    int tie[32];            // candidates sharing their screen score (positions)
+    int tslot[32];          // candidate -> its entry in tie[] (or -1)
     ScanWarp sw;
     int4 grp[FS_MAXG];      // (channel, first row-table index, rows, t0 << 8 | len)
     short4 rows[PK_MAXTC];  // mask rows (s, t0, t1, -)
@@ -1214,9 +1221,10 @@ struct FastSmem {
 };
 
 // Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
-__device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, const double* tmS, int nr,
-                                           int ngrp, int cnt, int& ntop, int K) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+// fp64 keys of the windows cidx[0, cnt) (reference order, see fast_batch).
+__device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, const double* tmS, int nr,
+                                             int ngrp, const int* cidx, int cnt, double* keys) {
+    const int tid = threadIdx.x;
     const int R = nr * P.nch;
     const int EB = max(1, FS_RS / R);
     const size_t plane = static_cast<size_t>(P.hc) * P.wc;
@@ -1227,7 +1235,7 @@ __device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, cons
             const int e = it / ngrp, g = it - e * ngrp;
             const int4 G = S.grp[g];
             const int ch = G.x, k0 = G.y, nk = G.z, t0 = G.w >> 8, len = G.w & 255;
-            const int pos = S.cidx[e0 + e];
+            const int pos = cidx[e0 + e];
             const int x = pos / P.out_w, y = pos - x * P.out_w;
             const double* base = P.ti64 + ch * plane + static_cast<size_t>(x) * P.wc + y + t0;
             const double* tb = tmS + ch * P.Tc * P.Tc + t0;
@@ -1289,10 +1297,17 @@ __device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, cons
                 for (int i = 0; i < 8; ++i) acc = __dadd_rn(acc, x[i]);
             }
             for (; r < R; ++r) acc = __dadd_rn(acc, rp[r]);
-            S.key[e0 + e] = acc;
+            keys[e0 + e] = acc;
         }
         __syncthreads();
     }
+}
+
+// Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
+__device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, const double* tmS, int nr,
+                                           int ngrp, int cnt, int& ntop, int K) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    rescore_keys(P, S, tmS, nr, ngrp, S.cidx, cnt, S.key);
     // merge: the batch plus the running top-K (reference ranking)
     for (int e = tid; e < ntop; e += FS_T) {
         S.key[cnt + e] = S.tkey[e];
@@ -1391,7 +1406,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         if (wid == 0) {
             long long sclk[5];
             sclk[0] = clock64();
-            const int n = scan_job(P, slot, S.sw, S.cidx, mk, sclk);
+            const int n = scan_job(P, slot, S.sw, S.cidx, mk, sclk, S.cs);
             if (lane == 0) {
                 S.misc[0] = n;
                 S.misc[1] = mk;
@@ -1451,7 +1466,42 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             return;
         }
         if (P.defer && tid == 0) P.defer[slot] = INT_MIN;
-        if (n >= 0) {
+        if (n >= 0 && n <= 32) {
+            // Windows with different screen scores never swap in fp64 (§3 of
+            // DESIGN.md): only candidates that share their score are rescored;
+            // the ranking is (S desc, fp64 desc within equal S, index asc).
+            if (wid == 0) {
+                const int sv = lane < n ? S.cs[lane] : INT_MIN;
+                const unsigned grp = __match_any_sync(0xffffffffu, sv);
+                const bool tie = lane < n && __popc(grp) > 1;
+                const unsigned tb = __ballot_sync(0xffffffffu, tie);
+                const int o = __popc(tb & ((1u << lane) - 1));
+                if (tie) S.tie[o] = S.cidx[lane];
+                if (lane < n) S.tslot[lane] = tie ? o : -1;
+                if (lane == 0) S.misc[6] = __popc(tb);
+            }
+            __syncthreads();
+            const int nt = S.misc[6];
+            if (nt > 0) rescore_keys(P, S, tmS, nr, ngrp, S.tie, nt, S.key);
+            if (wid == 0) {
+                const int si = lane < n ? S.cs[lane] : INT_MIN;
+                const int ii = lane < n ? S.cidx[lane] : INT_MAX;
+                const double ki = lane < n && S.tslot[lane] >= 0 ? S.key[S.tslot[lane]] : 0.0;
+                int rank = 0;
+                for (int j = 0; j < n; ++j) {
+                    const int sj = __shfl_sync(0xffffffffu, si, j);
+                    const int ij = __shfl_sync(0xffffffffu, ii, j);
+                    const double kj = __shfl_sync(0xffffffffu, ki, j);
+                    rank += sj > si || (sj == si && better(kj, ij, ki, ii));
+                }
+                if (lane < n && rank < K) {
+                    S.tidx[rank] = ii;
+                    S.tkey[rank] = ki;
+                }
+            }
+            ntop = min(K, n);
+            __syncthreads();
+        } else if (n >= 0) {
             fast_batch(P, S, tmS, nr, ngrp, n, ntop, K);
         } else {
             // list overflow without the bulk kernel: every window >= M_K, in batches
