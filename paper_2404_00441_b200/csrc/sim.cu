@@ -2668,17 +2668,18 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
                                               (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
                 const int bxb = static_cast<int>(std::min<size_t>((most + 255) / 256, 1024));
-                launch_pdl(finalize_band_kernel, dim3(bxb, nb), dim3(256), 0, gs,
+                // final bands are never written again: rebuild and copy them on the copy
+                // stream, off the group's critical path
+                cudaEvent_t be = tm.get();
+                CCW_CUDA(cudaEventRecord(be, gs));
+                CCW_CUDA(cudaStreamWaitEvent(ctx->copy_stream, be, 0));
+                launch_pdl(finalize_band_kernel, dim3(bxb, nb), dim3(256), 0, ctx->copy_stream,
                            static_cast<const int4*>(d_bands + rng.first), static_cast<const uint8_t*>(d_work),
                            wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
                            static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
                            static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, d_mism, tl_next(w, g, 4));
                 ++launches;
-                // copies on their own stream (the group's next wave does not wait),
-                // straight into the caller's buffer; adjacent ranges merged
-                cudaEvent_t be = tm.get();
-                CCW_CUDA(cudaEventRecord(be, gs));
-                CCW_CUDA(cudaStreamWaitEvent(ctx->copy_stream, be, 0));
+                // copies straight into the caller's buffer; adjacent ranges merged
                 const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
                 size_t o0 = 0, o1 = 0;
                 auto flush = [&] {
