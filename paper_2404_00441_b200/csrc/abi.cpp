@@ -270,7 +270,7 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
     ctx->h_stage.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
-    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (cudaStream_t s : ctx->copy_streams) cudaStreamDestroy(s);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -223,7 +223,7 @@ struct ccw_ctx {
     ccwgpu::HostPool pool;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<cudaStream_t> gstreams;  // realization-group streams
-    cudaStream_t copy_stream = nullptr;  // progressive device->host copies of final bands
+    std::vector<cudaStream_t> copy_streams;  // per group: progressive device->host copies of final bands
     // launch plan memory: (TI content key, Tc, OVc, K, T) whose last call
     // deferred no placement to the bulk tie select skip its per-wave launch
     // (re-enabled when the warp select reports a would-be deferral)

@@ -1968,7 +1968,7 @@ __global__ void finalize_band_kernel(const int4* __restrict__ bands, const uint8
     tl_mark(tl, 0);
     const int4 bd = bands[blockIdx.y];
     const int r = bd.x;
-    const int rows = bd.y == 0 ? bd.w - bd.z : sg_h;
+    const int rows = bd.y == 0 ? bd.w - bd.z : sg_h;  // (axis 2: a column band, copied whole later)
     const int cols = bd.y == 0 ? sg_w : bd.w - bd.z;
     const int y0 = bd.y == 0 ? bd.z : 0, x0 = bd.y == 0 ? 0 : bd.z;
     const size_t n = static_cast<size_t>(rows) * cols;
@@ -2477,7 +2477,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             for (int par = 0; par < 2; ++par)
                 tcplans[g][par] = plan_ccf_tc(GPP[g][par].wts8, static_cast<int>(maxj), d_x, npos, kpad);
     // group streams, forked from / joined back to the context stream
-    if (!ctx->copy_stream) CCW_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    while (static_cast<int>(ctx->copy_streams.size()) < G) {  // one per group: final copies overlap
+        cudaStream_t s3;
+        CCW_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+        ctx->copy_streams.push_back(s3);
+    }
     while (static_cast<int>(ctx->gstreams.size()) < G) {
         cudaStream_t s2;
         CCW_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
@@ -2511,7 +2515,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     std::vector<int4> bands;                                   // all checkpoints, in launch order
     std::vector<std::vector<std::pair<int, std::pair<size_t, size_t>>>> band_at(G);  // per group: (wave, [off, off+n))
     if (stream_out) {
-        int nck = 6;
+        int nck = 4;
         if (const char* e = getenv("CCW_STREAM_BANDS")) nck = std::max(1, atoi(e));
         const int delta = std::max(1, (max_key + 1 + nck - 1) / nck);
         // column-major raster paths free whole columns: strided copies, slower
@@ -2530,20 +2534,25 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 for (int r = 0; r < n_real; ++r) {
                     if (group_of(r) != g) continue;
                     const Plan& p = variants[vid[r]];
-                    if (p.column_major && !col_ck) continue;
-                    const int axis = p.column_major ? 1 : 0;
+                    // column bands: strided copies at col_ck checkpoints (CCW_STREAM_COLS,
+                    // axis 1), or finalized on the device at every checkpoint and the whole
+                    // realization copied at the last wave (axis 2: the final band, possibly
+                    // empty, carries the copy)
+                    if (p.column_major && stream_cols && !col_ck) continue;
+                    const int axis = !p.column_major ? 0 : (stream_cols ? 1 : 2);
                     const bool asc = axis == 0 ? (p.origin == CCW_TOP_LEFT || p.origin == CCW_TOP_RIGHT)
                                                : (p.origin == CCW_TOP_LEFT || p.origin == CCW_BOTTOM_LEFT);
                     const int extent = axis == 0 ? wh : ww, sg_ext = axis == 0 ? cfg.sg_height : cfg.sg_width;
                     int O = w >= p.n_inner - 1 ? (w - (p.n_inner - 1)) / keymul : -1;
                     O = std::min(O, p.n_outer - 1);
                     const int U = (w == max_key || O == p.n_outer - 1) ? extent : (O + 1) * stride;
-                    if (U <= done[r]) continue;
+                    const bool carry = axis == 2 && w == max_key;
+                    if (U <= done[r] && !carry) continue;
                     int lo = asc ? done[r] : extent - U, hi = asc ? U : extent - done[r];
-                    done[r] = U;
+                    done[r] = std::max(done[r], U);
                     lo = std::max(lo, 0);
                     hi = std::min(hi, sg_ext);
-                    if (hi > lo) bands.push_back(make_int4(r, axis, lo, hi));
+                    if (hi > lo || carry) bands.push_back(make_int4(r, axis, lo, std::max(lo, hi)));
                 }
                 if (bands.size() > off) band_at[g].push_back({w, {off, bands.size()}});
             }
@@ -2555,6 +2564,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaMemcpyAsync(d_bands, bands.data(), sizeof(int4) * bands.size(), cudaMemcpyHostToDevice, st));
     }
     std::vector<size_t> band_next(G, 0);
+    struct CopyMark {
+        int w, g;
+        cudaEvent_t ev;
+    };
+    std::vector<CopyMark> copy_marks;
 
     // debug timeline: [resident, past-wait, end] per launch
     const bool want_tl = getenv("CCW_TIMELINE") != nullptr;
@@ -2672,8 +2686,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 // stream, off the group's critical path
                 cudaEvent_t be = tm.get();
                 CCW_CUDA(cudaEventRecord(be, gs));
-                CCW_CUDA(cudaStreamWaitEvent(ctx->copy_stream, be, 0));
-                launch_pdl(finalize_band_kernel, dim3(bxb, nb), dim3(256), 0, ctx->copy_stream,
+                CCW_CUDA(cudaStreamWaitEvent(ctx->copy_streams[g], be, 0));
+                launch_pdl(finalize_band_kernel, dim3(bxb, nb), dim3(256), 0, ctx->copy_streams[g],
                            static_cast<const int4*>(d_bands + rng.first), static_cast<const uint8_t*>(d_work),
                            wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
                            static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
@@ -2685,19 +2699,20 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 auto flush = [&] {
                     if (o1 > o0)
                         CCW_CUDA(cudaMemcpyAsync(h_dst + o0, fin + o0, o1 - o0, cudaMemcpyDeviceToHost,
-                                                 ctx->copy_stream));
+                                                 ctx->copy_streams[g]));
                     o0 = o1 = 0;
                 };
                 for (size_t q = rng.first; q < rng.second; ++q) {
                     const int4 bd = bands[q];
                     const size_t base = static_cast<size_t>(bd.x) * n;
+                    if (bd.y == 2 && w != max_key) continue;  // device-only column band
                     const bool full = (bd.y == 0 && bd.z == 0 && bd.w == cfg.sg_height) ||
-                                      (bd.y == 1 && bd.z == 0 && bd.w == cfg.sg_width);
+                                      (bd.y == 1 && bd.z == 0 && bd.w == cfg.sg_width) || bd.y == 2;
                     if (bd.y == 1 && !full) {  // a column band: one strided copy
                         flush();
                         CCW_CUDA(cudaMemcpy2DAsync(h_dst + base + bd.z, cfg.sg_width, fin + base + bd.z,
                                                    cfg.sg_width, bd.w - bd.z, cfg.sg_height,
-                                                   cudaMemcpyDeviceToHost, ctx->copy_stream));
+                                                   cudaMemcpyDeviceToHost, ctx->copy_streams[g]));
                         continue;
                     }
                     const size_t a0 = full ? base : base + static_cast<size_t>(bd.z) * cfg.sg_width;
@@ -2707,6 +2722,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     o1 = a1;
                 }
                 flush();
+                if (want_tl) {  // debug: copy-stream progress per checkpoint
+                    cudaEvent_t ce = tm.get();
+                    CCW_CUDA(cudaEventRecord(ce, ctx->copy_streams[g]));
+                    copy_marks.push_back({w, g, ce});
+                }
             }
         }
     }
@@ -2716,11 +2736,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaEventRecord(e, ctx->gstreams[g]));
         CCW_CUDA(cudaStreamWaitEvent(st, e, 0));
     }
-    if (stream_out) {
-        cudaEvent_t e = tm.get();
-        CCW_CUDA(cudaEventRecord(e, ctx->copy_stream));
-        CCW_CUDA(cudaStreamWaitEvent(st, e, 0));
-    }
+    if (stream_out)
+        for (int g = 0; g < G; ++g) {
+            cudaEvent_t e = tm.get();
+            CCW_CUDA(cudaEventRecord(e, ctx->copy_streams[g]));
+            CCW_CUDA(cudaStreamWaitEvent(st, e, 0));
+        }
 
     // ---- finalize (device results, or host results without streaming)
     if (!stream_out) {
@@ -2774,6 +2795,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.host_prep_ms = host_prep_ms;
     ctx->timing.jobs = static_cast<int64_t>(total_jobs);
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
+    for (const CopyMark& cm : copy_marks) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev0, cm.ev);
+        fprintf(stderr, "copy stream: wave %d group %d bands copied at %.3f ms\n", cm.w, cm.g, ms);
+    }
     if (d_tl) {
         std::vector<unsigned long long> h(tl_tag.size() * 4);
         CCW_CUDA(cudaMemcpy(h.data(), d_tl, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
