@@ -1,0 +1,148 @@
+// prep.cu -- per-TI and per-wave preparation: the TI pyramid (reference-order
+// apex values and exact block-count screen planes), the overlap-region prep
+// of every placement (screen weights, fp64 template) and the normalized
+// screen's norm maps.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+#include "sim_kernels.cuh"
+
+namespace ccwgpu {
+
+// ------------------------------------------------------------ pyramid ----
+
+// TI pyramid, once per TI: reference-order apex per channel (wavelet.hpp:147-171
+// applied to to_indicator_planes / to_real_plane, simulator.hpp:429-435) and the
+// exact-integer screen planes (block counts of facies 0..F-2, or code sums).
+__global__ void pyramid_kernel(const uint8_t* __restrict__ codes, int w, int hc, int wc, int J,
+                               int mode, int nscr, double* __restrict__ ti64,
+                               float* __restrict__ scr) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ch = blockIdx.y;
+    if (cell >= hc * wc) return;
+    const int i = cell / wc, j = cell - i * wc;
+    const int B = 1 << J;
+    const uint8_t* base = codes + static_cast<size_t>(i * B) * w + j * B;
+    ti64[static_cast<size_t>(ch) * hc * wc + cell] = haar_apex_block(base, w, J, mode, ch);
+    if (ch < nscr)
+        scr[static_cast<size_t>(ch) * hc * wc + cell] = static_cast<float>(block_stat(base, w, B, mode, ch));
+}
+
+void build_pyramid(ccw_ti* ti, cudaStream_t s) {
+    const int n = ti->hc * ti->wc;
+    dim3 grid((n + 127) / 128, ti->nch);
+    pyramid_kernel<<<grid, 128, 0, s>>>(ti->d_codes, ti->w, ti->hc, ti->wc, ti->J, ti->mode,
+                                        ti->nscr, ti->d_ti64, ti->d_scr);
+    CCW_CUDA(cudaGetLastError());
+}
+
+__global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    pdl_trigger();
+    const int slot = blockIdx.x;
+    const Job jb = jobs[job0 + slot];
+    tl_mark(P.tl, 2);
+    pdl_wait();
+    tl_mark(P.tl, 0);
+    prep_src_job(P, jb, slot, P.wts8, P.tm64, P.cjob);
+    tl_mark(P.tl, 1);
+}
+
+__global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
+    pdl_trigger();
+    const int slot = blockIdx.x;
+    const Job jb = jobs[job0 + slot];
+    pdl_wait();
+    const int Tc = P.Tc, B = P.B;
+    const uint8_t* grid = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
+    int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
+    double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+    if (P.wts8)  // zero the K padding of this job's int8 weight row
+        for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x)
+            P.wts8[static_cast<size_t>(slot) * P.kpad + k] = 0;
+    int csum = 0;
+    for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
+        const int s = c / Tc, t = c - s * Tc;
+        int t0, t1;
+        mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+        const bool in = t >= t0 && t < t1;
+        const uint8_t* base = grid + static_cast<size_t>(jb.top + s * B) * P.ww + jb.left + t * B;
+        int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
+        if (P.mode == 0) {
+            const int last = in ? block_stat(base, P.ww, B, 0, P.F - 1) : 0;
+            csum += last;
+            for (int f = 0; f < P.nscr; ++f) {
+                const int v = in ? block_stat(base, P.ww, B, 0, f) - last : 0;
+                wts[f * Tc * Tc + c] = v;
+                if (w8) w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
+            }
+        } else {
+            const int v = in ? block_stat(base, P.ww, B, 1, 0) : 0;
+            wts[c] = v;
+            if (w8) w8[c] = static_cast<int8_t>(v);
+        }
+        for (int ch = 0; ch < P.nch; ++ch)
+            tm[ch * Tc * Tc + c] = in ? haar_apex_block(base, P.ww, P.J, P.mode, ch) : 0.0;
+    }
+    if (P.cjob) store_cjob(P.cjob, P.mode, P.B, slot, csum);
+}
+
+// NN[v][p] = sum over mask variant v's cells and over every channel of the
+// squared TI block count: the reference's normalization sum_f sum_mask ti_f^2
+// (matcher.hpp:84-100, 163-171) times 4^J, exact in integers.
+__global__ void nn_map_kernel(const float* __restrict__ scr, int nscr, int mode, int B, int hc, int wc,
+                              int Tc, int OVc, int out_w, int npos, int32_t* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y;
+    if (p >= npos) return;
+    const int shape = v < 4 ? kL : (v < 6 ? kVertical : kHorizontal);
+    const int vleft = v < 4 ? (v >> 1) : (v < 6 ? v - 4 : 0);
+    const int htop = v < 4 ? (v & 1) : (v < 6 ? 0 : v - 6);
+    const int x = p / out_w, y = p - x * out_w;
+    const size_t nc = static_cast<size_t>(hc) * wc;
+    int acc = 0;
+    for (int s = 0; s < Tc; ++s) {
+        int t0, t1;
+        mask_row_run(shape, vleft, htop, Tc, OVc, s, t0, t1);
+        for (int t = t0; t < t1; ++t) {
+            const size_t idx = static_cast<size_t>(x + s) * wc + y + t;
+            if (mode == 0) {
+                int rest = B * B;  // the last facies' count
+                for (int f = 0; f < nscr; ++f) {
+                    const int n = static_cast<int>(scr[f * nc + idx]);
+                    acc += n * n;
+                    rest -= n;
+                }
+                acc += rest * rest;
+            } else {
+                const int n = static_cast<int>(scr[idx]);
+                acc += n * n;
+            }
+        }
+    }
+    out[static_cast<size_t>(v) * npos + p] = acc;
+}
+
+// NN maps of a TI for template Tc / overlap OVc (8 mask variants), cached on the TI.
+const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
+    const auto key = std::make_pair(Tc, OVc);
+    auto it = ti->nnmap.find(key);
+    if (it != ti->nnmap.end()) return it->second;
+    const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1, npos = out_h * out_w;
+    int32_t* m = static_cast<int32_t*>(cache_alloc(ti->device, sizeof(int32_t) * 8 * static_cast<size_t>(npos)));
+    nn_map_kernel<<<dim3((npos + 255) / 256, 8), 256, 0, st>>>(ti->d_scr, ti->nscr, ti->mode, 1 << ti->J, ti->hc,
+                                                             ti->wc, Tc, OVc, out_w, npos, m);
+    CCW_CUDA(cudaGetLastError());
+    ti->nnmap[key] = m;
+    return m;
+}
+
+}  // namespace ccwgpu
