@@ -44,42 +44,93 @@ __global__ void hd_scatter_kernel(const int32_t* __restrict__ hd, int n_hd, uint
     if (i < n_hd) plane[static_cast<size_t>(hd[3 * i]) * ww + hd[3 * i + 1]] = static_cast<uint8_t>(hd[3 * i + 2]);
 }
 
-// Hard-data overwrite with pre-overwrite mismatch count, then the crop to
-// the simulation grid (simulator.hpp:506-515).
-// Without a work grid the cell is read from the TI through the source-block
-// map (every work block is a verbatim copy of the TI block it was last pasted
-// from).
+// Rebuild (and hard-data overwrite) the output cells of rows [y0, y1) x columns
+// [x0, x1) of realization r.  With the source-block map, one thread per
+// coarse block: one map entry, then the B x B TI patch (BT = B for 2/4/8; 0 =
+// one thread per cell, for min-cut's work grid or large blocks).
+template <int BT>
+__device__ __forceinline__ void finalize_region(int r, int y0, int y1, int x0, int x1,
+                                                const uint8_t* __restrict__ work, int wh, int ww,
+                                                const int32_t* __restrict__ src, int B, int J, int swc,
+                                                const uint8_t* __restrict__ ti, int ti_w, int wc,
+                                                const uint8_t* __restrict__ hd, int sg_h, int sg_w,
+                                                uint8_t* __restrict__ out, int& local) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    uint8_t* o = out + static_cast<size_t>(r) * sg_h * sg_w;
+    const uint8_t* hp = hd;
+    if constexpr (BT == 0) {
+        const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
+        const int32_t* sm = src ? src + static_cast<size_t>(r) * (wh >> J) * swc : nullptr;
+        const int cols = x1 - x0;
+        const size_t n = static_cast<size_t>(y1 - y0) * cols;
+        for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
+            const int y = y0 + static_cast<int>(e / cols), x = x0 + static_cast<int>(e % cols);
+            uint8_t v;
+            if (g) {
+                v = g[static_cast<size_t>(y) * ww + x];
+            } else {
+                const int b = sm[static_cast<size_t>(y >> J) * swc + (x >> J)];
+                const int by = b / wc, bx = b - by * wc;
+                v = ti[static_cast<size_t>((by << J) + (y & (B - 1))) * ti_w + (bx << J) + (x & (B - 1))];
+            }
+            if (hp) {
+                const uint8_t h = hp[static_cast<size_t>(y) * ww + x];
+                if (h != kNoDatum) {
+                    local += v != h;
+                    v = h;
+                }
+            }
+            o[static_cast<size_t>(y) * sg_w + x] = v;
+        }
+    } else {
+        const int32_t* sm = src + static_cast<size_t>(r) * (wh >> J) * swc;
+        const int by0 = y0 / BT, by1 = (y1 + BT - 1) / BT, bx0 = x0 / BT, bx1 = (x1 + BT - 1) / BT;
+        const int nbw = bx1 - bx0;
+        const size_t nb = static_cast<size_t>(by1 - by0) * nbw;
+        for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nb; e += stride) {
+            const int cby = by0 + static_cast<int>(e / nbw), cbx = bx0 + static_cast<int>(e % nbw);
+            const int b = sm[static_cast<size_t>(cby) * swc + cbx];
+            const int tby = b / wc, tbx = b - tby * wc;
+            const uint8_t* tp = ti + static_cast<size_t>(tby * BT) * ti_w + tbx * BT;
+            uint8_t v[BT][BT];
+#pragma unroll
+            for (int i = 0; i < BT; ++i)
+#pragma unroll
+                for (int j = 0; j < BT; ++j) v[i][j] = tp[static_cast<size_t>(i) * ti_w + j];
+#pragma unroll
+            for (int i = 0; i < BT; ++i) {
+                const int y = cby * BT + i;
+                if (y < y0 || y >= y1) continue;
+#pragma unroll
+                for (int j = 0; j < BT; ++j) {
+                    const int x = cbx * BT + j;
+                    if (x < x0 || x >= x1) continue;
+                    uint8_t w = v[i][j];
+                    if (hp) {
+                        const uint8_t h = hp[static_cast<size_t>(y) * ww + x];
+                        if (h != kNoDatum) {
+                            local += w != h;
+                            w = h;
+                        }
+                    }
+                    o[static_cast<size_t>(y) * sg_w + x] = w;
+                }
+            }
+        }
+    }
+}
+
+template <int BT>
 __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww,
                                 const int32_t* __restrict__ src, int B, int J, int swc,
                                 const uint8_t* __restrict__ ti, int ti_w, int wc,
                                 const uint8_t* __restrict__ hd, int sg_h, int sg_w,
                                 uint8_t* __restrict__ out, int* mism) {
     pdl_wait();
-    const size_t n = static_cast<size_t>(sg_h) * sg_w;
     const int r = blockIdx.y;
-    const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
-    const int32_t* sm = src ? src + static_cast<size_t>(r) * (wh >> J) * swc : nullptr;
     int local = 0;
-    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int y = static_cast<int>(e / sg_w), x = static_cast<int>(e - static_cast<size_t>(y) * sg_w);
-        uint8_t v;
-        if (g) {
-            v = g[static_cast<size_t>(y) * ww + x];
-        } else {
-            const int b = sm[static_cast<size_t>(y >> J) * swc + (x >> J)];
-            const int by = b / wc, bx = b - by * wc;
-            v = ti[static_cast<size_t>((by << J) + (y & (B - 1))) * ti_w + (bx << J) + (x & (B - 1))];
-        }
-        if (hd) {
-            const uint8_t h = hd[static_cast<size_t>(y) * ww + x];
-            if (h != kNoDatum) {
-                local += v != h;
-                v = h;
-            }
-        }
-        out[static_cast<size_t>(r) * n + e] = v;
-    }
+    finalize_region<BT>(r, 0, sg_h, 0, sg_w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w, out,
+                        local);
     if (hd) {
         for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
         if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
@@ -87,10 +138,11 @@ __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww
 }
 
 // Progressive finalize: band descriptors (realization, axis, lo, hi) in
-// output coordinates -- axis 0: rows [lo, hi) x every column; axis 1: every
-// row x columns [lo, hi).  A band is final once every placement covering it
-// is done (run_simulation's checkpoints), so it is rebuilt and copied to the
-// host while later waves still compute.
+// output coordinates -- axis 0: rows [lo, hi) x every column; axis 1 / 2:
+// every row x columns [lo, hi).  A band is final once every placement
+// covering it is done (run_simulation's checkpoints), so it is rebuilt and
+// copied to the host while later waves still compute.
+template <int BT>
 __global__ void finalize_band_kernel(const int4* __restrict__ bands, const uint8_t* __restrict__ work,
                                      int wh, int ww, const int32_t* __restrict__ src, int B, int J,
                                      int swc, const uint8_t* __restrict__ ti, int ti_w, int wc,
@@ -101,33 +153,13 @@ __global__ void finalize_band_kernel(const int4* __restrict__ bands, const uint8
     tl_mark(tl, 0);
     const int4 bd = bands[blockIdx.y];
     const int r = bd.x;
-    const int rows = bd.y == 0 ? bd.w - bd.z : sg_h;  // (axis 2: a column band, copied whole later)
-    const int cols = bd.y == 0 ? sg_w : bd.w - bd.z;
-    const int y0 = bd.y == 0 ? bd.z : 0, x0 = bd.y == 0 ? 0 : bd.z;
-    const size_t n = static_cast<size_t>(rows) * cols;
-    const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
-    const int32_t* sm = src ? src + static_cast<size_t>(r) * (wh >> J) * swc : nullptr;
     int local = 0;
-    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int y = y0 + static_cast<int>(e / cols), x = x0 + static_cast<int>(e % cols);
-        uint8_t v;
-        if (g) {
-            v = g[static_cast<size_t>(y) * ww + x];
-        } else {
-            const int b = sm[static_cast<size_t>(y >> J) * swc + (x >> J)];
-            const int by = b / wc, bx = b - by * wc;
-            v = ti[static_cast<size_t>((by << J) + (y & (B - 1))) * ti_w + (bx << J) + (x & (B - 1))];
-        }
-        if (hd) {
-            const uint8_t h = hd[static_cast<size_t>(y) * ww + x];
-            if (h != kNoDatum) {
-                local += v != h;
-                v = h;
-            }
-        }
-        out[(static_cast<size_t>(r) * sg_h + y) * sg_w + x] = v;
-    }
+    if (bd.y == 0)
+        finalize_region<BT>(r, bd.z, bd.w, 0, sg_w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w,
+                            out, local);
+    else
+        finalize_region<BT>(r, 0, sg_h, bd.z, bd.w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w,
+                            out, local);
     if (hd) {
         for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
         if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
@@ -578,6 +610,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
+    // finalize granularity: one thread per coarse block (B = 2, 4, 8) with the map
+    const int fin_bt = d_src && (B == 2 || B == 4 || B == 8) ? B : 0;
+    const size_t fin_cells = fin_bt ? static_cast<size_t>(B) * B : 1;
     // ---- progressive output (host results): bands of every realization that
     // no remaining placement covers are finalized and copied back at a few
     // checkpoint waves, overlapping the copy with the remaining waves
@@ -762,17 +797,24 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 for (size_t q = rng.first; q < rng.second; ++q)
                     most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
                                               (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
-                const int bxb = static_cast<int>(std::min<size_t>((most + 255) / 256, 1024));
+                const int bxb = static_cast<int>(std::min<size_t>((most / fin_cells + 255) / 256 + 1, 1024));
                 // final bands are never written again: rebuild and copy them on the copy
                 // stream, off the group's critical path
                 cudaEvent_t be = tm.get();
                 CCW_CUDA(cudaEventRecord(be, gs));
                 CCW_CUDA(cudaStreamWaitEvent(ctx->copy_streams[g], be, 0));
-                launch_pdl(finalize_band_kernel, dim3(bxb, nb), dim3(256), 0, ctx->copy_streams[g],
-                           static_cast<const int4*>(d_bands + rng.first), static_cast<const uint8_t*>(d_work),
-                           wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
-                           static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
-                           static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, d_mism, tl_next(w, g, 4));
+                auto band = [&](auto kern) {
+                    launch_pdl(kern, dim3(bxb, nb), dim3(256), 0, ctx->copy_streams[g],
+                               static_cast<const int4*>(d_bands + rng.first), static_cast<const uint8_t*>(d_work),
+                               wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
+                               static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
+                               static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, d_mism,
+                               tl_next(w, g, 4));
+                };
+                if (fin_bt == 2) band(finalize_band_kernel<2>);
+                else if (fin_bt == 4) band(finalize_band_kernel<4>);
+                else if (fin_bt == 8) band(finalize_band_kernel<8>);
+                else band(finalize_band_kernel<0>);
                 ++launches;
                 // copies straight into the caller's buffer; adjacent ranges merged
                 const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
@@ -826,11 +868,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
 
     // ---- finalize (device results, or host results without streaming)
     if (!stream_out) {
-        const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
+        const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width / fin_cells + 1;
         const int bx = static_cast<int>(std::min<size_t>((n + 255) / 256, 1024));
-        finalize_kernel<<<dim3(bx, n_real), 256, 0, st>>>(d_work, wh, ww, d_src, B, J, swc, ti->d_codes,
-                                                          ti->w, ti->wc, d_hd, cfg.sg_height,
-                                                          cfg.sg_width, fin, d_mism);
+        auto full = [&](auto kern) {
+            kern<<<dim3(bx, n_real), 256, 0, st>>>(d_work, wh, ww, d_src, B, J, swc, ti->d_codes, ti->w, ti->wc,
+                                                 d_hd, cfg.sg_height, cfg.sg_width, fin, d_mism);
+        };
+        if (fin_bt == 2) full(finalize_kernel<2>);
+        else if (fin_bt == 4) full(finalize_kernel<4>);
+        else if (fin_bt == 8) full(finalize_kernel<8>);
+        else full(finalize_kernel<0>);
         ++launches;
         CCW_CUDA(cudaGetLastError());
     }
