@@ -222,17 +222,17 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     std::vector<char> have(8, 0);
     std::vector<int> vid(n_real);
     std::vector<std::mt19937_64> rngs(n_real);
-    for (int r = 0; r < n_real; ++r) {
+    ctx->pool.run(n_real, [&](int r) {  // seeding + the two plan draws, in parallel
         rngs[r].seed(seeds[r]);
         const int origin = static_cast<int>(bounded(rngs[r], 4));
         const bool cm = bounded(rngs[r], 2) == 1;
-        const int v = origin * 2 + (cm ? 1 : 0);
-        if (!have[v]) {
-            variants[v] = make_plan_from(cfg, origin, cm);
-            have[v] = 1;
+        vid[r] = origin * 2 + (cm ? 1 : 0);
+    });
+    for (int r = 0; r < n_real; ++r)
+        if (!have[vid[r]]) {
+            variants[vid[r]] = make_plan_from(cfg, vid[r] / 2, (vid[r] & 1) != 0);
+            have[vid[r]] = 1;
         }
-        vid[r] = v;
-    }
     int wh = 0, ww = 0, nlr = 0, nlc = 0;
     {
         const Plan& p0 = variants[vid[0]];  // geometry (identical for every variant)
