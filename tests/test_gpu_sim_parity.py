@@ -210,6 +210,48 @@ def test_fast_select_geometries(oracle, case):
         assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+def fast_case(rng, trial):
+    """Fast-select geometries (raw scoring, K <= 8, no min-cut), mid-size."""
+    J = int(rng.integers(1, 4))
+    b = 1 << J
+    T = b * int(rng.integers(3, 9))
+    OV = b * int(rng.integers(1, max(2, (T // b) // 2 + 1)))
+    nf = int(rng.integers(2, 5))
+    H = b * int(rng.integers(max(T // b + 4, 24), 72))
+    W = b * int(rng.integers(max(T // b + 4, 24), 72))
+    if trial % 3 == 0:
+        ti = np.repeat(np.repeat(rng.integers(0, nf, (H // b, W // b)), b, 0), b, 1).astype(np.uint8)
+    else:
+        ti = rng.integers(0, nf, (H, W)).astype(np.uint8)
+        ti = np.where(rng.random((H, W)) < 0.7, np.roll(ti, 1, axis=1), ti).astype(np.uint8)
+    sg_h, sg_w = int(rng.integers(T + 8, 3 * T + 40)), int(rng.integers(T + 8, 3 * T + 40))
+    d = dict(sg_height=sg_h, sg_width=sg_w, template_size=T, overlap=OV, dwt_level=J,
+             candidates=int(rng.integers(1, 9)), facies_mode=int(rng.integers(0, 2)))
+    hd = None
+    if trial % 2:
+        cells = rng.choice(sg_h * sg_w, size=int(rng.integers(5, 80)), replace=False)
+        hd = [(int(c // sg_w), int(c % sg_w), int(rng.integers(0, nf))) for c in cells]
+    return ti, nf, d, hd
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_fast_path_corpus_vs_oracle(oracle, block):
+    """Randomized fast-select configurations (equal-score ranking, tile
+    queueing, bulk deferral, streamed result bands) against the oracle."""
+    rng = np.random.default_rng(5000 + block)
+    for trial in range(20):
+        ti_a, nf, d, hd = fast_case(rng, trial)
+        if nf > 2 and d["dwt_level"] == 3 and d["facies_mode"] == 1:
+            d["facies_mode"] = 0  # raw-code block sums above 127 leave the int8 screen (covered elsewhere)
+        ti = cs.CategoricalGrid(ti_a.shape[0], ti_a.shape[1], nf, ti_a)
+        seeds = [int(s) for s in rng.integers(0, 2**63, 4)]
+        res = cs.simulate_batch(ti, to_cfg(d, hd), seeds)
+        for s_, r in zip(seeds, res):
+            o = oracle.simulate_one(ti_a, nf, pyoracle.Cfg(**d), hd, seed=s_)
+            assert np.array_equal(r.realization.cells, o["realization"]), (block, trial, d)
+            assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+
+
 def test_provenance_and_replay():
     # test_simulator.cpp:434-460, acceptance.cpp:349-381
     z = load("sim_channel64_base.npz")
