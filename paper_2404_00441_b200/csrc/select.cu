@@ -1152,6 +1152,21 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             atomicAdd(&P.stats[13], static_cast<unsigned long long>(fclk[2] - fclk[1]));
             atomicAdd(&P.stats[4], static_cast<unsigned long long>(fclk[4] - fclk[2]));
             atomicAdd(&P.stats[5], static_cast<unsigned long long>(fclk[3] - fclk[2]));  // choose
+#ifdef CCW_DBG_TAIL
+            const bool had_tie = S.misc[6] > 0;
+            const unsigned long long tot = static_cast<unsigned long long>(fclk[4] - fclk[0]);
+            atomicAdd(&P.stats[had_tie ? 16 : 19], 1ull);
+            atomicAdd(&P.stats[had_tie ? 17 : 20], tot);
+            atomicMax(&P.stats[had_tie ? 18 : 21], tot);
+            atomicAdd(&P.stats[22 + (tot < 10000 ? 0 : tot < 20000 ? 1 : tot < 40000 ? 2 : tot < 80000 ? 3 : 4)], 1ull);
+            // where the long ones spend it: scan, batch, choose+map
+            if (tot >= 40000) {
+                atomicAdd(&P.stats[30], static_cast<unsigned long long>(S.misc[0]));  // candidates
+                atomicAdd(&P.stats[27], static_cast<unsigned long long>(fclk[1] - fclk[0]));
+                atomicAdd(&P.stats[28], static_cast<unsigned long long>(fclk[2] - fclk[1]));
+                atomicAdd(&P.stats[29], static_cast<unsigned long long>(fclk[4] - fclk[2]));
+            }
+#endif
         }
     }
     tl_mark(P.tl, 1);

@@ -476,8 +476,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.nnmap = ti_nnmap(ti, Tc, OVc, st);
         d_cjob = ctx->cjob.as<int32_t>(G * maxj);
     }
-    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(16);
-    CCW_CUDA(cudaMemsetAsync(d_stats, 0, 16 * sizeof(unsigned long long), st));
+    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(32);
+    CCW_CUDA(cudaMemsetAsync(d_stats, 0, 32 * sizeof(unsigned long long), st));
     // source-block map (fast or_prep), valid whenever pastes are verbatim TI blocks
     const int swc = ww / B;
     int32_t* d_src = nullptr;
@@ -884,7 +884,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     CCW_CUDA(cudaEventRecord(ev1, st));
     if (h_out && !stream_out)
         CCW_CUDA(cudaMemcpyAsync(h_dst, fin, out_bytes, cudaMemcpyDeviceToHost, st));
-    unsigned long long stats[16] = {0};
+    unsigned long long stats[32] = {0};
     CCW_CUDA(cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
     std::vector<int> mism(n_real, 0);
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
@@ -950,6 +950,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 pr[2] / n, pr[3] / n, pr[4] / n, pr[5] / (8 * n), pr[6] / n);
         tc_probe_buffer = nullptr;
     }
+    if (getenv("CCW_TAIL"))
+        fprintf(stderr, "select jobs: ties %llu avg %.0f max %llu cycles | no ties %llu avg %.0f max %llu cycles\n",
+                stats[16], stats[16] ? double(stats[17]) / stats[16] : 0.0, stats[18], stats[19],
+                stats[19] ? double(stats[20]) / stats[19] : 0.0, stats[21]);
+    if (getenv("CCW_TAIL"))
+        fprintf(stderr, "select cycles histogram <10k %llu <20k %llu <40k %llu <80k %llu >=80k %llu | long jobs: scan+stage %llu batch %llu choose+map %llu candidates %llu\n",
+                stats[22], stats[23], stats[24], stats[25], stats[26], stats[27], stats[28], stats[29], stats[30]);
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
