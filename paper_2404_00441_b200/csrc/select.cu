@@ -806,7 +806,7 @@ struct FastSmem {
     double key[SC_LC + kTcQ];
     int cidx[SC_LC + kTcQ];
     int cs[SC_LC];          // the candidates' screen scores
-    int tie[32];            // candidates sharing their screen score (positions)
+    int tie[SC_LC];         // candidates sharing their screen score (positions)
     int tslot[32];          // candidate -> its entry in tie[] (or -1)
     ScanWarp sw;
     int4 grp[FS_MAXG];      // (channel, first row-table index, rows, t0 << 8 | len)
@@ -1064,7 +1064,91 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             return;
         }
         if (P.defer && tid == 0) P.defer[slot] = INT_MIN;
-        if (n >= 0 && n <= 32) {
+        int picked = -1;  // the chosen position when settled without the ranked list
+        if (n >= 0 && jb.pick >= 0) {
+            // Unconditional pick (matcher.hpp:207-211): only the candidate at rank
+            // `pick` of (S desc, fp64 desc, index asc) matters, and windows with
+            // different S never swap in fp64 -- so only the equal-S group that
+            // holds rank `pick` can need fp64 keys, and none when it is a single window.
+            if (wid == 0) {
+                constexpr int kV = SC_LC / 32;
+                int v[kV];
+#pragma unroll
+                for (int j = 0; j < kV; ++j) {
+                    const int e = j * 32 + lane;
+                    v[j] = e < n ? S.cs[e] : INT_MIN;
+                }
+                int cur = INT_MAX, acc = 0, sp = INT_MIN, above = 0;
+                for (int round = 0; round <= jb.pick && round < n; ++round) {
+                    int m = INT_MIN;
+#pragma unroll
+                    for (int j = 0; j < kV; ++j)
+                        if (v[j] < cur) m = max(m, v[j]);
+                    m = __reduce_max_sync(0xffffffffu, m);
+                    int c = 0;
+#pragma unroll
+                    for (int j = 0; j < kV; ++j) c += v[j] == m;
+                    c = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+                    sp = m;
+                    above = acc;
+                    if (acc + c > jb.pick) break;
+                    acc += c;
+                    cur = m;
+                }
+                int g = 0;
+#pragma unroll
+                for (int j = 0; j < kV; ++j) {
+                    const int e = j * 32 + lane;
+                    const bool q = e < n && v[j] == sp;
+                    const unsigned bal = __ballot_sync(0xffffffffu, q);
+                    if (q) S.tie[g + __popc(bal & ((1u << lane) - 1))] = S.cidx[e];
+                    g += __popc(bal);
+                }
+                if (lane == 0) {
+                    S.misc[6] = g;
+                    S.misc[5] = jb.pick - above;  // rank inside the group
+                }
+            }
+            __syncthreads();
+            const int g = S.misc[6], rk = S.misc[5];
+            if (g == 1) {
+                picked = S.tie[0];
+            } else {
+                rescore_keys(P, S, tmS, nr, ngrp, S.tie, g, S.key);
+                if (wid == 0) {  // the rk-th best of the group by (fp64 desc, index asc)
+                    for (int round = 0; round <= rk; ++round) {
+                        double bk = 0.0;
+                        int bi = INT_MAX, bp = -1;
+                        for (int e = lane; e < g; e += 32) {
+                            const int ix = S.tie[e];
+                            if (ix >= 0 && (bp < 0 || better(S.key[e], ix, bk, bi))) {
+                                bk = S.key[e];
+                                bi = ix;
+                                bp = e;
+                            }
+                        }
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                            if (op >= 0 && (bp < 0 || better(ok, oi, bk, bi))) {
+                                bk = ok;
+                                bi = oi;
+                                bp = op;
+                            }
+                        }
+                        if (round == rk) {
+                            if (lane == 0) S.misc[4] = bi;
+                        } else if (lane == 0) {
+                            S.tie[bp] = -1;
+                        }
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+                picked = S.misc[4];
+            }
+        } else if (n >= 0 && n <= 32) {
             // Windows with different screen scores never swap in fp64 (§3 of
             // DESIGN.md): only candidates that share their score are rescored;
             // the ranking is (S desc, fp64 desc within equal S, index asc).
@@ -1131,13 +1215,13 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         }
         fclk[2] = clock64();
         // choose (matcher.hpp:207-241)
-        if (wid == 0) {
+        if (picked < 0 && wid == 0) {
             const int pos = choose_pick(P, jb, S.tidx, ntop, lane);
             if (lane == 0) S.misc[4] = pos;
         }
         __syncthreads();
         fclk[3] = clock64();
-        const int pos = S.misc[4];
+        const int pos = picked >= 0 ? picked : S.misc[4];
         fr = (pos / P.out_w) << P.J;
         fc = (pos % P.out_w) << P.J;
     }
