@@ -144,10 +144,14 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
     int mx = INT_MIN;
     // store phase: lane -> (row r0 + 4 i, 16-byte chunk lane & 7)
     const int srow = lane >> 3, schunk = lane & 7;
+    uint32_t rr[2][32];  // two 32-column chunks per TMEM round trip
     for (int c = 0; c < kN / 64; ++c) {
-        uint32_t r[32];
-        LDTM_X32(trow + c * 32, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if ((c & 1) == 0) {
+            LDTM_X32(trow + c * 32, rr[0]);
+            LDTM_X32(trow + (c + 1) * 32, rr[1]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
+        uint32_t (&r)[32] = rr[c & 1];
         const int p0 = pbase + c * 32;
         const int lim = a.npos - p0;  // valid columns of this chunk
 #pragma unroll
@@ -235,23 +239,40 @@ __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) probe(0);
-    tl_mark(a.tl, 2);
-    pdl_wait();  // the weights (or_prep) and the previous wave's outputs are complete
-    tl_mark(a.tl, 0);
-    if (threadIdx.x == 0) probe(1);
+    // The dependency wait (griddepcontrol.wait) is per role: the producer's B
+    // operand (the TI im2col) does not depend on earlier kernels, so the first
+    // ring of B tiles is requested before it; the weights (A, written by
+    // or_prep) and the epilogue's stores (score rows the previous select read)
+    // wait.  The MMA warp touches no global memory.
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer: K stages of every tile, one ring
+            // prologue: the first ring's B tiles, before the dependency wait
+            int npre = 0;
+            for (int t = blockIdx.x; t < ntot && npre < kStages; t += gridDim.x) {
+                const int n0 = (t / n_mt) * kN;
+                for (int kc = 0; kc < a.nk && npre < kStages; ++kc, ++npre) {
+                    const uint32_t bar = smem_u32(&full[npre]);
+                    mbar_expect_tx(bar, kStageBytes);
+                    tma_load_2d(smem_u32(sm + npre * kStageBytes + kABytes), &tmB, kc * kKC, n0, bar);
+                }
+            }
+            tl_mark(a.tl, 2);
+            pdl_wait();  // the weights (or_prep) are complete
+            tl_mark(a.tl, 0);
+            probe(1);
             int it = 0;
             for (int t = blockIdx.x; t < ntot; t += gridDim.x) {
                 const int m0 = (t % n_mt) * kM, n0 = (t / n_mt) * kN;
                 for (int kc = 0; kc < a.nk; ++kc, ++it) {
                     const int s = it % kStages;
-                    if (it >= kStages) mbar_wait(smem_u32(&empty[s]), ((it / kStages) - 1) & 1);
                     const uint32_t bar = smem_u32(&full[s]);
-                    mbar_expect_tx(bar, kStageBytes);
+                    if (it >= npre) {
+                        if (it >= kStages) mbar_wait(smem_u32(&empty[s]), ((it / kStages) - 1) & 1);
+                        mbar_expect_tx(bar, kStageBytes);
+                        tma_load_2d(smem_u32(sm + s * kStageBytes + kABytes), &tmB, kc * kKC, n0, bar);
+                    }
                     tma_load_2d(smem_u32(sm + s * kStageBytes), &tmA, kc * kKC, m0, bar);
-                    tma_load_2d(smem_u32(sm + s * kStageBytes + kABytes), &tmB, kc * kKC, n0, bar);
                 }
             }
         }
@@ -281,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
             }
         }
     } else {  // epilogue warps 2..9
+        pdl_wait();  // the previous wave's select has read the score rows
         int lt = 0;
         for (int t = blockIdx.x; t < ntot; t += gridDim.x, ++lt) {
             const int b = lt % kAcc;

@@ -184,8 +184,14 @@ constexpr int FS_RS = CCW_FS_RS;    // (window, run) partial sums per batch
 // windows interleaved to hide the dependent fp64 chain.  Each CTA publishes
 // its top-K; the last CTA to finish merges them by the reference ranking
 // (matcher.hpp:189-198), chooses and pastes like the warp select.
-constexpr int BK_T = 256;
-constexpr int BK_W = 4;
+#ifndef CCW_BK_T
+#define CCW_BK_T 256
+#endif
+#ifndef CCW_BK_W
+#define CCW_BK_W 4
+#endif
+constexpr int BK_T = CCW_BK_T;
+constexpr int BK_W = CCW_BK_W;
 constexpr int BK_V = 8;      // positions per thread per scan pass
 constexpr int BK_SMAX = 8;   // CTAs per placement (upper bound)
 
