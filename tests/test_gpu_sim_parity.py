@@ -252,6 +252,28 @@ def test_fast_path_corpus_vs_oracle(oracle, block):
             assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+@pytest.mark.parametrize("F", [6, 8, 12])
+def test_many_facies_and_odd_templates(oracle, F):
+    """More facies (wider int8 screen K, raw-code block sums beyond int8 fall
+    back to the fp32 screen) and template sizes that are not multiples of 4
+    (the byte paste / map paths)."""
+    rng = np.random.default_rng(77 + F)
+    for J, T, OV in ((1, 14, 4), (1, 22, 6), (2, 20, 8)):
+        b = 1 << J
+        H, W = b * 60, b * 52
+        ti_a = np.repeat(np.repeat(rng.integers(0, F, (H // b, W // b)), b, 0), b, 1).astype(np.uint8)
+        ti_a = np.where(rng.random((H, W)) < 0.3, rng.integers(0, F, (H, W)), ti_a).astype(np.uint8)
+        ti = cs.CategoricalGrid(H, W, F, ti_a)
+        for mode in (0, 1):
+            d = dict(sg_height=90, sg_width=77, template_size=T, overlap=OV, dwt_level=J,
+                     candidates=int(rng.integers(1, 9)), facies_mode=mode)
+            seeds = [int(s) for s in rng.integers(0, 2**63, 3)]
+            res = cs.simulate_batch(ti, to_cfg(d), seeds)
+            for s_, r in zip(seeds, res):
+                o = oracle.simulate_one(ti_a, F, pyoracle.Cfg(**d), None, seed=s_)
+                assert np.array_equal(r.realization.cells, o["realization"]), (F, J, T, OV, mode)
+
+
 def test_provenance_and_replay():
     # test_simulator.cpp:434-460, acceptance.cpp:349-381
     z = load("sim_channel64_base.npz")
