@@ -144,14 +144,25 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
     int mx = INT_MIN;
     // store phase: lane -> (row r0 + 4 i, 16-byte chunk lane & 7)
     const int srow = lane >> 3, schunk = lane & 7;
-    uint32_t rr[2][32];  // two 32-column chunks per TMEM round trip
+#ifndef CCW_TC_LDTM1  // (measured r1: two chunks per wait is ~2% faster end to end)
+#define CCW_TC_LDTM2
+#endif
+#ifdef CCW_TC_LDTM2
+    uint32_t rr[2][32];  // two 32-column chunks per TMEM round trip (more registers)
+#endif
     for (int c = 0; c < kN / 64; ++c) {
+#ifdef CCW_TC_LDTM2
         if ((c & 1) == 0) {
             LDTM_X32(trow + c * 32, rr[0]);
             LDTM_X32(trow + (c + 1) * 32, rr[1]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
         uint32_t (&r)[32] = rr[c & 1];
+#else
+        uint32_t r[32];
+        LDTM_X32(trow + c * 32, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#endif
         const int p0 = pbase + c * 32;
         const int lim = a.npos - p0;  // valid columns of this chunk
 #pragma unroll
