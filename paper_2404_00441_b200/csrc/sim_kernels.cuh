@@ -47,11 +47,64 @@ __device__ __forceinline__ void prep_src_job(const SimParams& P, const Job& jb, 
     const int Tc = P.Tc, B = P.B, nc = P.hc * P.wc;
     const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc;
     int32_t* wts = w8base ? nullptr : P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
-    double* tm = tmbase + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+    double* tm = tmbase ? tmbase + static_cast<size_t>(slot) * P.nch * Tc * Tc : nullptr;
     int8_t* w8 = w8base ? w8base + static_cast<size_t>(slot) * P.kpad : nullptr;
     if (w8)
         for (int k = P.nscr * Tc * Tc + threadIdx.x; k < P.kpad; k += blockDim.x) w8[k] = 0;
     int csum = 0;
+    constexpr int kCh = 8, kCpt = 2;  // batched path: <= 8 channels, 2 cells per thread
+    if (P.nch <= kCh && P.nscr <= kCh) {
+        // every load of a thread's cells in flight at once: the map entries, then
+        // the screen planes and apex values at the source blocks
+        for (int c0 = threadIdx.x; c0 < Tc * Tc; c0 += kCpt * blockDim.x) {
+            int sb[kCpt];
+            bool in[kCpt];
+#pragma unroll
+            for (int u = 0; u < kCpt; ++u) {
+                const int c = c0 + u * blockDim.x;
+                const int s = c / Tc, t = c - s * Tc;
+                int t0 = 0, t1 = 0;
+                if (c < Tc * Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+                in[u] = c < Tc * Tc && t >= t0 && t < t1;
+                sb[u] = in[u] ? src[static_cast<size_t>(jb.top / B + s) * P.swc + jb.left / B + t] : 0;
+            }
+            float n[kCpt][kCh];
+            double a[kCpt][kCh];
+#pragma unroll
+            for (int u = 0; u < kCpt; ++u)
+#pragma unroll
+                for (int f = 0; f < kCh; ++f) {
+                    n[u][f] = f < P.nscr ? P.tiscr[static_cast<size_t>(f) * nc + sb[u]] : 0.f;
+                    a[u][f] = f < P.nch && in[u] ? P.ti64[static_cast<size_t>(f) * nc + sb[u]] : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < kCpt; ++u) {
+                const int c = c0 + u * blockDim.x;
+                if (c >= Tc * Tc) continue;
+                int last = B * B;
+                if (P.mode == 0)
+#pragma unroll
+                    for (int f = 0; f < kCh; ++f)
+                        if (f < P.nscr) last -= static_cast<int>(n[u][f]);
+                if (in[u]) csum += last;
+#pragma unroll
+                for (int f = 0; f < kCh; ++f) {
+                    if (f >= P.nscr) break;
+                    const int v = in[u] ? (P.mode == 0 ? static_cast<int>(n[u][f]) - last : static_cast<int>(n[u][f])) : 0;
+                    if (w8)
+                        w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
+                    else
+                        wts[f * Tc * Tc + c] = v;
+                }
+                if (tm)
+#pragma unroll
+                    for (int ch = 0; ch < kCh; ++ch)
+                        if (ch < P.nch) tm[ch * Tc * Tc + c] = a[u][ch];
+            }
+        }
+        if (cjobbase) store_cjob(cjobbase, P.mode, P.B, slot, csum);
+        return;
+    }
     for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
         const int s = c / Tc, t = c - s * Tc;
         int t0, t1;
