@@ -81,6 +81,7 @@ struct SimParams {
     unsigned long long* tl;  // debug timeline slot of this launch (null unless CCW_TIMELINE)
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
     int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)
+    const int4* mtab;        // fast select: mask rows and run groups per mask variant
     const int32_t* nnmap;    // normalized screen: [8 mask variants][npos] sum over mask and
                              // channels of squared TI block counts (null otherwise)
     int* bulk_sync;          // per job slot: [next position block, finished CTAs]
@@ -94,7 +95,7 @@ struct SimParams {
 // Row-major run of the coarse overlap mask in template row s: [t0, t1).
 // Every simulator mask (strip or L, simulator.hpp:194-215) has at most one
 // maximal run per row, so mask_runs (matcher.hpp:44-61) reduces to this.
-__device__ __forceinline__ void mask_row_run(int shape, int vleft, int htop, int Tc, int OVc,
+__host__ __device__ __forceinline__ void mask_row_run(int shape, int vleft, int htop, int Tc, int OVc,
                                              int s, int& t0, int& t1) {
     const bool vert = shape == kVertical || shape == kL;
     const bool horz = shape == kHorizontal || shape == kL;

@@ -456,6 +456,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
                  "l"(src)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -592,6 +597,74 @@ struct ScanWarp {
     int tq[SC_TB];  // queued qualifying tiles
 };
 
+constexpr int kTM = 16;  // tile maxima per lane in registers (512 tiles per placement)
+
+// K-th largest (with multiplicity) of the warp's register-held values.
+__device__ __forceinline__ int regs_kth(const int (&tv)[kTM], int K) {
+    int cur = INT_MAX, acc = 0, mk = INT_MIN;
+    for (int round = 0; round < K; ++round) {
+        int m = INT_MIN;
+#pragma unroll
+        for (int i = 0; i < kTM; ++i)
+            if (tv[i] < cur) m = max(m, tv[i]);
+        m = __reduce_max_sync(0xffffffffu, m);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < kTM; ++i) c += tv[i] == m;
+        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+        mk = m;
+        if (acc >= K || m == INT_MIN) break;
+        cur = m;
+    }
+    return mk;
+}
+
+// Steps 3-4 of the scan (one warp): the exact K-th score S_K of the list
+// W.lv[0, nl) and the candidate positions (>= S_K) into out[].
+__device__ __forceinline__ int scan_finish(const SimParams& P, const ScanWarp& W, int nl, int mk, int* out,
+                                           long long* sclk, int* out_s) {
+    const int lane = threadIdx.x & 31;
+    const int K = P.K;
+    // 3. exact S_K from the list (rounds of warp max with multiplicity)
+    int lvr[SC_LC / 32];
+#pragma unroll
+    for (int j2 = 0; j2 < SC_LC / 32; ++j2) {
+        const int e = j2 * 32 + lane;
+        lvr[j2] = e < nl ? W.lv[e] : INT_MIN;
+    }
+    int thr = mk, cur = INT_MAX, acc = 0;
+    for (int round = 0; round < K; ++round) {
+        int m = INT_MIN;
+#pragma unroll
+        for (int j2 = 0; j2 < SC_LC / 32; ++j2)
+            if (lvr[j2] < cur) m = max(m, lvr[j2]);
+        m = __reduce_max_sync(0xffffffffu, m);
+        int c = 0;
+#pragma unroll
+        for (int j2 = 0; j2 < SC_LC / 32; ++j2) c += lvr[j2] == m;
+        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+        thr = m;
+        if (acc >= K || m == INT_MIN) break;
+        cur = m;
+    }
+    sclk[3] = clock64();
+    // 4. the candidates: every listed window >= S_K
+    int* cd = out;
+    int cnt = 0;
+    for (int e0 = 0; e0 < nl; e0 += 32) {
+        const int e = e0 + lane;
+        const bool q = e < nl && W.lv[e] >= thr;
+        const unsigned bal = __ballot_sync(0xffffffffu, q);
+        if (q) {
+            const int o = cnt + __popc(bal & ((1u << lane) - 1));
+            cd[o] = W.lp[e];
+            if (out_s) out_s[o] = W.lv[e];
+        }
+        cnt += __popc(bal);
+    }
+    return cnt;
+}
+
 // Warp-level scan of one placement (every lane of the warp calls it): the
 // tile-maximum bound M_K, the (score, position) list of windows >= M_K, the
 // exact K-th score S_K and the candidate positions (>= S_K) into out[].
@@ -606,7 +679,6 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
     // 1. M_K = K-th largest tile maximum (with multiplicity): a lower bound of
     //    the K-th largest screen score S_K (the K best tiles each hold a
     //    window scoring at least M_K).  Tile maxima stay in registers.
-    constexpr int kTM = 16;  // tile maxima per lane (512 tiles per placement)
     const bool regs = P.ntiles <= 32 * kTM;  // else: stream the maxima (sorted per-lane top lists)
     int tv[kTM];
 #pragma unroll
@@ -633,21 +705,7 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
         }
         mk = warp_kth(top, K, lane);
     } else {
-        int cur = INT_MAX, acc = 0;
-        for (int round = 0; round < K; ++round) {
-            int m = INT_MIN;
-#pragma unroll
-            for (int i = 0; i < kTM; ++i)
-                if (tv[i] < cur) m = max(m, tv[i]);
-            m = __reduce_max_sync(0xffffffffu, m);
-            int c = 0;
-#pragma unroll
-            for (int i = 0; i < kTM; ++i) c += tv[i] == m;
-            acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
-            mk = m;
-            if (acc >= K || m == INT_MIN) break;
-            cur = m;
-        }
+        mk = regs_kth(tv, K);
     }
     sclk[1] = clock64();
     // 2. every window scoring >= M_K, from the tiles whose maximum reaches it,
@@ -732,44 +790,7 @@ __device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& 
         if (lane == 0 && P.stats) atomicAdd(&P.stats[2], 1ull);
         return -1;
     }
-    // 3. exact S_K from the list (rounds of warp max with multiplicity)
-    int lvr[SC_LC / 32];
-#pragma unroll
-    for (int j2 = 0; j2 < SC_LC / 32; ++j2) {
-        const int e = j2 * 32 + lane;
-        lvr[j2] = e < nl ? W.lv[e] : INT_MIN;
-    }
-    int thr = mk, cur = INT_MAX, acc = 0;
-    for (int round = 0; round < K; ++round) {
-        int m = INT_MIN;
-#pragma unroll
-        for (int j2 = 0; j2 < SC_LC / 32; ++j2)
-            if (lvr[j2] < cur) m = max(m, lvr[j2]);
-        m = __reduce_max_sync(0xffffffffu, m);
-        int c = 0;
-#pragma unroll
-        for (int j2 = 0; j2 < SC_LC / 32; ++j2) c += lvr[j2] == m;
-        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
-        thr = m;
-        if (acc >= K || m == INT_MIN) break;
-        cur = m;
-    }
-    sclk[3] = clock64();
-    // 4. the candidates: every listed window >= S_K
-    int* cd = out;
-    int cnt = 0;
-    for (int e0 = 0; e0 < nl; e0 += 32) {
-        const int e = e0 + lane;
-        const bool q = e < nl && W.lv[e] >= thr;
-        const unsigned bal = __ballot_sync(0xffffffffu, q);
-        if (q) {
-            const int o = cnt + __popc(bal & ((1u << lane) - 1));
-            cd[o] = W.lp[e];
-            if (out_s) out_s[o] = W.lv[e];
-        }
-        cnt += __popc(bal);
-    }
-    return cnt;
+    return scan_finish(P, W, nl, mk, out, sclk, out_s);
 }
 
 // Fused OR prep (select epilogue): after this placement's source-block map
@@ -810,13 +831,101 @@ struct FastSmem {
     int tslot[32];          // candidate -> its entry in tie[] (or -1)
     ScanWarp sw;
     int4 grp[FS_MAXG];      // (channel, first row-table index, rows, t0 << 8 | len)
-    short4 rows[PK_MAXTC];  // mask rows (s, t0, t1, -)
+    alignas(16) short4 rows[PK_MAXTC];  // mask rows (s, t0, t1, -)
     double tkey[kTcQ];
     int tidx[kTcQ];
     double rk[FS_T / 32];
     int ri[FS_T / 32], rp[FS_T / 32], wc[FS_T / 32];
     int misc[8];
+    int tqa[32 * kTM];      // cooperative scan: the tiles whose maximum reaches M_K
+    int nq, lcnt, lover;    // their count, the list length, list overflow
 };
+
+// Cooperative scan (ntiles <= 32 * kTM), step 1 on warp 0: M_K (as scan_job)
+// and the queue of tiles whose maximum reaches it, in tile order.
+__device__ __forceinline__ void coop_head(const SimParams& P, int slot, FastSmem& S) {
+    const int lane = threadIdx.x & 31;
+    const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
+    int tv[kTM];
+#pragma unroll
+    for (int i = 0; i < kTM; ++i) {
+        const int e = i * 32 + lane;
+        tv[i] = e < P.ntiles ? tmx[e] : INT_MIN;
+    }
+    const int mk = regs_kth(tv, P.K);
+    int nq = 0;
+#pragma unroll
+    for (int i = 0; i < kTM; ++i) {
+        const bool q = tv[i] != INT_MIN && tv[i] >= mk;
+        const unsigned bal = __ballot_sync(0xffffffffu, q);
+        if (q) S.tqa[nq + __popc(bal & ((1u << lane) - 1))] = i * 32 + lane;
+        nq += __popc(bal);
+    }
+    if (lane == 0) {
+        S.misc[1] = mk;
+        S.nq = nq;
+        S.lcnt = 0;
+        S.lover = 0;
+    }
+}
+
+// Step 2 on every warp: the windows >= M_K of the queued tiles (SC_TB tiles per
+// round trip per warp) appended to the shared (score, position) list.  The
+// list order is irrelevant: every later ranking is a total order on (S, fp64
+// key, index).  Overflow iff the list would exceed SC_LC, as in scan_job.
+__device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem& S) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
+    const int nq = S.nq, mk = S.misc[1];
+    for (int q0 = wid * SC_TB; q0 < nq; q0 += (FS_T / 32) * SC_TB) {
+        int tl[SC_TB], v[SC_TB][4];
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u) tl[u] = q0 + u < nq ? S.tqa[q0 + u] : -1;
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u) {
+            const int p0 = tl[u] * kTcTile + lane * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
+            if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
+                const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
+                v[u][0] = a4.x;
+                v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
+                v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
+                v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
+            }
+        }
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) c += v[u][i] != INT_MIN && v[u][i] >= mk;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&S.lcnt, tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base + tot > SC_LC) {
+            if (lane == 0) S.lover = 1;
+            continue;
+        }
+        int o = base + incl - c;
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (v[u][i] != INT_MIN && v[u][i] >= mk) {
+                    S.sw.lv[o] = v[u][i];
+                    S.sw.lp[o] = tl[u] * kTcTile + lane * 4 + i;
+                    ++o;
+                }
+    }
+}
 
 // Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
 // fp64 keys of the windows cidx[0, cnt) (reference order, see fast_batch).
@@ -827,6 +936,9 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
     const int EB = max(1, FS_RS / R);
     const size_t plane = static_cast<size_t>(P.hc) * P.wc;
     if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+#ifdef CCW_DBG_TAIL
+    long long c_items = 0, c_fold = 0, c0 = clock64();
+#endif
     for (int e0 = 0; e0 < cnt; e0 += EB) {
         const int ng = min(EB, cnt - e0);
         for (int it = tid; it < ng * ngrp; it += FS_T) {
@@ -882,6 +994,10 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
             }
         }
         __syncthreads();
+#ifdef CCW_DBG_TAIL
+        const long long c1 = clock64();
+        c_items += c1 - c0;
+#endif
         for (int e = tid; e < ng; e += FS_T) {
             // the fold is one sequential chain; its operands load 8 at a time
             const double* rp = S.rsum + e * R;
@@ -898,7 +1014,19 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
             keys[e0 + e] = acc;
         }
         __syncthreads();
+#ifdef CCW_DBG_TAIL
+        c0 = clock64();
+        c_fold += c0 - c1;
+#endif
     }
+#ifdef CCW_DBG_TAIL
+    if (P.stats && tid == 0 && cnt >= 64) {
+        atomicAdd(&P.stats[31], 1ull);
+        atomicAdd(&P.stats[14], static_cast<unsigned long long>(c_items));
+        atomicAdd(&P.stats[15], static_cast<unsigned long long>(c_fold));
+        atomicAdd(&P.stats[3], static_cast<unsigned long long>(cnt));
+    }
+#endif
 }
 
 // Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
@@ -975,6 +1103,9 @@ __device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, cons
     __syncthreads();
 }
 
+#ifndef CCW_COOP_SCAN
+#define CCW_COOP_SCAN 1
+#endif
 #ifndef CCW_FS_MINB
 #define CCW_FS_MINB 4
 #endif
@@ -1001,60 +1132,68 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         const int ntm = P.nch * Tc * Tc;
         const double* tmS = ntm <= PK_TMC ? S.tm : tmg;
         int mk = INT_MIN;
+        // the scan: warp 0 alone (scan_job), or with the list step spread over
+        // every warp when the tile maxima fit in registers
+        const bool coop = CCW_COOP_SCAN && P.ntiles <= 32 * kTM;
+        long long sclk[5];
         if (wid == 0) {
-            long long sclk[5];
             sclk[0] = clock64();
-            const int n = scan_job(P, slot, S.sw, S.cidx, mk, sclk, S.cs);
-            if (lane == 0) {
-                S.misc[0] = n;
-                S.misc[1] = mk;
-                if (P.stats && P.tl && n >= 0) {
-                    sclk[4] = clock64();
-                    for (int q = 0; q < 4; ++q)
-                        atomicAdd(&P.stats[8 + q], static_cast<unsigned long long>(sclk[q + 1] - sclk[q]));
+            if (coop) {
+                coop_head(P, slot, S);
+                sclk[1] = clock64();
+            } else {
+                const int n = scan_job(P, slot, S.sw, S.cidx, mk, sclk, S.cs);
+                if (lane == 0) {
+                    S.misc[0] = n;
+                    S.misc[1] = mk;
+                    if (P.stats && P.tl && n >= 0) {
+                        sclk[4] = clock64();
+                        for (int q = 0; q < 4; ++q)
+                            atomicAdd(&P.stats[8 + q], static_cast<unsigned long long>(sclk[q + 1] - sclk[q]));
+                    }
                 }
             }
         } else {
             // stage the template (matcher.hpp:44-61 order), the mask rows and the run groups
             if (ntm <= PK_TMC)
                 for (int e = tid - 32; e < ntm; e += FS_T - 32) cp_async8(&S.tm[e], tmg + e);
-            if (wid == 1) {
-                int nr = 0;
-                for (int s0 = 0; s0 < Tc; s0 += 32) {
-                    const int s = s0 + lane;
-                    int t0 = 0, t1 = 0;
-                    if (s < Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
-                    const unsigned m = __ballot_sync(0xffffffffu, t1 > t0);
-                    if (t1 > t0) S.rows[nr + __popc(m & ((1u << lane) - 1))] = make_short4(s, t0, t1, 0);
-                    nr += __popc(m);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    int ng = 0;
-                    for (int ch = 0; ch < P.nch; ++ch) {
-                        int k = 0;
-                        while (k < nr) {
-                            const int t0 = S.rows[k].y, len = S.rows[k].z - S.rows[k].y;
-                            int nk = 1;
-                            while (k + nk < nr && S.rows[k + nk].y == t0 && S.rows[k + nk].z - t0 == len &&
-                                   (nk + 1) * len <= FS_G)
-                                ++nk;
-                            if (len > FS_G) {  // a long run stays one item (one sequential sum)
-                                if (ng < FS_MAXG) S.grp[ng++] = make_int4(ch, k, 1, (t0 << 8) | len);
-                                nk = 1;
-                            } else if (ng < FS_MAXG) {
-                                S.grp[ng++] = make_int4(ch, k, nk, (t0 << 8) | len);
-                            }
-                            k += nk;
-                        }
-                    }
-                    S.misc[2] = nr;
-                    S.misc[3] = ng;
-                }
+            // the mask rows and run groups of this mask variant (host tables)
+            const int4* mt = P.mtab + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * MT_STRIDE;
+            const int4 info = __ldg(mt);
+            for (int e = tid - 32; e < MT_ROWS4 + info.y; e += FS_T - 32)
+                cp_async16(e < MT_ROWS4 ? reinterpret_cast<int4*>(S.rows) + e : &S.grp[e - MT_ROWS4], mt + 1 + e);
+            if (tid == 32) {
+                S.misc[2] = info.x;
+                S.misc[3] = info.y;
+                S.misc[7] = info.z;
             }
             cp_async_wait_all();
         }
         __syncthreads();
+        if (coop) {
+            coop_list(P, slot, S);
+            __syncthreads();
+            if (wid == 0) {
+                sclk[2] = clock64();
+                const int nl = S.lcnt, mk0 = S.misc[1];
+                if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+                int n = -1;
+                if (S.lover) {
+                    if (P.stats && lane == 0) atomicAdd(&P.stats[2], 1ull);
+                } else {
+                    n = scan_finish(P, S.sw, nl, mk0, S.cidx, sclk, S.cs);
+                }
+                if (lane == 0) {
+                    S.misc[0] = n;
+                    if (P.stats && P.tl && n >= 0) {
+                        sclk[4] = clock64();
+                        for (int q = 0; q < 4; ++q)
+                            atomicAdd(&P.stats[8 + q], static_cast<unsigned long long>(sclk[q + 1] - sclk[q]));
+                    }
+                }
+            }
+            __syncthreads();
+        }
         fclk[1] = clock64();
         const int n = S.misc[0], nr = S.misc[2], ngrp = S.misc[3];
         mk = S.misc[1];

@@ -195,6 +195,45 @@ double pair_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
     return t;
 }
 
+// Mask tables of the fast select (MT_STRIDE int4 per mask variant): the mask
+// rows of the placement and its rescoring run groups -- up to FS_G cells of
+// consecutive rows of one channel with the same column run (a run longer than
+// FS_G is a group of its own, summed sequentially).
+void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
+    tab.assign(static_cast<size_t>(8) * MT_STRIDE, make_int4(0, 0, 0, 0));
+    const int shapes[8][3] = {{kL, 0, 0}, {kL, 0, 1}, {kL, 1, 0}, {kL, 1, 1},
+                              {kVertical, 0, 0}, {kVertical, 1, 0}, {kHorizontal, 0, 0}, {kHorizontal, 0, 1}};
+    for (const auto& sh : shapes) {
+        const int v = mask_variant(sh[0], sh[1], sh[2]);
+        int4* mt = tab.data() + static_cast<size_t>(v) * MT_STRIDE;
+        short4* rows = reinterpret_cast<short4*>(mt + 1);
+        int4* grp = mt + 1 + MT_ROWS4;
+        int nr = 0, lng = 0;
+        for (int s = 0; s < Tc; ++s) {
+            int t0, t1;
+            mask_row_run(sh[0], sh[1], sh[2], Tc, OVc, s, t0, t1);
+            if (t1 > t0) {
+                rows[nr++] = make_short4(static_cast<short>(s), static_cast<short>(t0), static_cast<short>(t1), 0);
+                lng |= t1 - t0 > FS_G;
+            }
+        }
+        int ng = 0;
+        for (int ch = 0; ch < nch; ++ch) {
+            int k = 0;
+            while (k < nr) {
+                const int t0 = rows[k].y, len = rows[k].z - rows[k].y;
+                int nk = 1;
+                while (k + nk < nr && rows[k + nk].y == t0 && rows[k + nk].z - t0 == len && (nk + 1) * len <= FS_G)
+                    ++nk;
+                if (len > FS_G) nk = 1;
+                if (ng < FS_MAXG) grp[ng++] = make_int4(ch, k, nk, (t0 << 8) | len);
+                k += nk;
+            }
+        }
+        mt[0] = make_int4(nr, ng, lng, 0);
+    }
+}
+
 }  // namespace
 
 void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
@@ -488,6 +527,18 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.swc = swc;
     const bool warp_select = use_tc && Kp <= kTcQ && !cfg.min_cut && cfg.scoring == 0 &&
                              ti->nch * Tc <= FS_MAXG && Tc <= PK_MAXTC;
+    if (warp_select) {
+        const long long key = Tc | (static_cast<long long>(OVc) << 16) | (static_cast<long long>(ti->nch) << 32);
+        int4* d_mt = ctx->mtab.as<int4>(static_cast<size_t>(8) * MT_STRIDE);
+        if (ctx->mtab_key != key) {
+            std::vector<int4> tab;
+            build_mask_tables(Tc, OVc, ti->nch, tab);
+            CCW_CUDA(cudaMemcpyAsync(d_mt, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+            CCW_CUDA(cudaStreamSynchronize(st));  // tab is freed on return
+            ctx->mtab_key = key;
+        }
+        P.mtab = d_mt;
+    }
     P.kpad = kpad;
     P.ntiles = ntiles;
     P.stats = d_stats;
@@ -957,6 +1008,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (getenv("CCW_TAIL"))
         fprintf(stderr, "select cycles histogram <10k %llu <20k %llu <40k %llu <80k %llu >=80k %llu | long jobs: scan+stage %llu batch %llu choose+map %llu candidates %llu\n",
                 stats[22], stats[23], stats[24], stats[25], stats[26], stats[27], stats[28], stats[29], stats[30]);
+    if (getenv("CCW_TAIL"))
+        fprintf(stderr, "rescores of >= 64 windows: %llu, windows %llu, item cycles %llu, fold cycles %llu\n",
+                stats[31], stats[3], stats[14], stats[15]);
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",

@@ -220,6 +220,11 @@ constexpr int FS_G = 16;       // cells per rescoring item
 #define CCW_FS_MAXG 512
 #endif
 constexpr int FS_MAXG = CCW_FS_MAXG;   // run groups per placement
+// Per mask variant (mask_variant), built once on the host: int4 (rows, groups,
+// any run longer than FS_G, 0), the mask rows (short4 (s, t0, t1, 0), two per
+// int4) and the rescoring run groups (see select_fast_kernel).
+constexpr int MT_ROWS4 = PK_MAXTC / 2;
+constexpr int MT_STRIDE = 1 + MT_ROWS4 + FS_MAXG;
 #ifndef CCW_FS_RS
 #define CCW_FS_RS 1536
 #endif
