@@ -830,8 +830,7 @@ struct FastSmem {
     int tie[SC_LC];         // candidates sharing their screen score (positions)
     int tslot[32];          // candidate -> its entry in tie[] (or -1)
     ScanWarp sw;
-    int4 grp[FS_MAXG];      // (channel, first row-table index, rows, t0 << 8 | len)
-    alignas(16) short4 rows[PK_MAXTC];  // mask rows (s, t0, t1, -)
+    int4 grp[FS_MAXG];      // (channel, first row index | first row << 16, rows, t0 << 8 | len)
     double tkey[kTcQ];
     int tidx[kTcQ];
     double rk[FS_T / 32];
@@ -927,72 +926,82 @@ __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem
     }
 }
 
-// Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
+// The (window, run group) items of rescore_keys: every operand is loaded and
+// multiplied before the sequential sums (tb: the staged template in shared
+// memory, or the global one).
+template <typename TB>
+__device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, TB tb, int nr, int ngrp,
+                                              const int* cidx, int e0, int ng, int R) {
+    const size_t plane = static_cast<size_t>(P.hc) * P.wc;
+    for (int it = threadIdx.x; it < ng * ngrp; it += FS_T) {
+        const int e = it / ngrp, g = it - e * ngrp;
+        const int4 G = S.grp[g];  // rows s0 .. s0 + nk - 1, columns t0 .. t0 + len - 1
+        const int ch = G.x, k0 = G.y & 0xffff, s0 = G.y >> 16, nk = G.z, t0 = G.w >> 8, len = G.w & 255;
+        const int pos = cidx[e0 + e];
+        const int x = pos / P.out_w, y = pos - x * P.out_w;
+        const double* a0 = P.ti64 + ch * plane + static_cast<size_t>(x + s0) * P.wc + y + t0;
+        const int b0 = ch * P.Tc * P.Tc + s0 * P.Tc + t0;
+        double* rs = S.rsum + e * R + ch * nr + k0;
+        double pv[FS_G];
+        if (len > FS_G) {  // one long run (nk == 1), FS_G products per round trip
+            double sum = 0.0;
+            for (int c0 = 0; c0 < len; c0 += FS_G) {
+#pragma unroll
+                for (int c = 0; c < FS_G; ++c)
+                    pv[c] = c0 + c < len ? __dmul_rn(__ldg(a0 + c0 + c), tb[b0 + c0 + c]) : 0.0;
+#pragma unroll
+                for (int c = 0; c < FS_G; ++c)
+                    if (c0 + c < len) sum = __dadd_rn(sum, pv[c]);
+            }
+            rs[0] = sum;
+            continue;
+        }
+        {
+            int kk = 0, t = 0;
+#pragma unroll
+            for (int c = 0; c < FS_G; ++c) {
+                pv[c] = kk < nk ? __dmul_rn(__ldg(a0 + static_cast<size_t>(kk) * P.wc + t), tb[b0 + kk * P.Tc + t])
+                                : 0.0;
+                if (++t == len) {
+                    t = 0;
+                    ++kk;
+                }
+            }
+        }
+        double sum = 0.0;
+        int kk = 0, t = 0;
+#pragma unroll
+        for (int c = 0; c < FS_G; ++c) {
+            if (kk < nk) {
+                sum = __dadd_rn(sum, pv[c]);
+                if (++t == len) {
+                    rs[kk] = sum;
+                    sum = 0.0;
+                    t = 0;
+                    ++kk;
+                }
+            }
+        }
+    }
+}
+
 // fp64 keys of the windows cidx[0, cnt) (reference order, see fast_batch).
-__device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, const double* tmS, int nr,
+__device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, const double* tmg, int nr,
                                              int ngrp, const int* cidx, int cnt, double* keys) {
     const int tid = threadIdx.x;
     const int R = nr * P.nch;
     const int EB = max(1, FS_RS / R);
-    const size_t plane = static_cast<size_t>(P.hc) * P.wc;
+    const bool tm_smem = P.nch * P.Tc * P.Tc <= PK_TMC;
     if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
 #ifdef CCW_DBG_TAIL
     long long c_items = 0, c_fold = 0, c0 = clock64();
 #endif
     for (int e0 = 0; e0 < cnt; e0 += EB) {
         const int ng = min(EB, cnt - e0);
-        for (int it = tid; it < ng * ngrp; it += FS_T) {
-            const int e = it / ngrp, g = it - e * ngrp;
-            const int4 G = S.grp[g];
-            const int ch = G.x, k0 = G.y, nk = G.z, t0 = G.w >> 8, len = G.w & 255;
-            const int pos = cidx[e0 + e];
-            const int x = pos / P.out_w, y = pos - x * P.out_w;
-            const double* base = P.ti64 + ch * plane + static_cast<size_t>(x) * P.wc + y + t0;
-            const double* tb = tmS + ch * P.Tc * P.Tc + t0;
-            double* rs = S.rsum + e * R + ch * nr + k0;
-            if (len > FS_G) {  // one long run (nk == 1), FS_G operands per round trip
-                const int s = S.rows[k0].x;
-                const double* a = base + static_cast<size_t>(s) * P.wc;
-                const double* b = tb + s * P.Tc;
-                double sum = 0.0;
-                for (int c0 = 0; c0 < len; c0 += FS_G) {
-                    double av[FS_G];
-#pragma unroll
-                    for (int c = 0; c < FS_G; ++c) av[c] = c0 + c < len ? __ldg(a + c0 + c) : 0.0;
-#pragma unroll
-                    for (int c = 0; c < FS_G; ++c)
-                        if (c0 + c < len) sum = __dadd_rn(sum, __dmul_rn(av[c], b[c0 + c]));
-                }
-                rs[0] = sum;
-                continue;
-            }
-            double av[FS_G];
-            {
-                int kk = 0, t = 0;
-#pragma unroll
-                for (int c = 0; c < FS_G; ++c) {
-                    av[c] = kk < nk ? __ldg(base + static_cast<size_t>(S.rows[k0 + kk].x) * P.wc + t) : 0.0;
-                    if (++t == len) {
-                        t = 0;
-                        ++kk;
-                    }
-                }
-            }
-            double sum = 0.0;
-            int kk = 0, t = 0;
-#pragma unroll
-            for (int c = 0; c < FS_G; ++c) {
-                if (kk < nk) {
-                    sum = __dadd_rn(sum, __dmul_rn(av[c], tb[S.rows[k0 + kk].x * P.Tc + t]));
-                    if (++t == len) {
-                        rs[kk] = sum;
-                        sum = 0.0;
-                        t = 0;
-                        ++kk;
-                    }
-                }
-            }
-        }
+        if (tm_smem)
+            rescore_items(P, S, S.tm, nr, ngrp, cidx, e0, ng, R);
+        else
+            rescore_items(P, S, tmg, nr, ngrp, cidx, e0, ng, R);
         __syncthreads();
 #ifdef CCW_DBG_TAIL
         const long long c1 = clock64();
@@ -1030,10 +1039,10 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
 }
 
 // Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
-__device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, const double* tmS, int nr,
+__device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, const double* tmg, int nr,
                                            int ngrp, int cnt, int& ntop, int K) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    rescore_keys(P, S, tmS, nr, ngrp, S.cidx, cnt, S.key);
+    rescore_keys(P, S, tmg, nr, ngrp, S.cidx, cnt, S.key);
     // merge: the batch plus the running top-K (reference ranking)
     for (int e = tid; e < ntop; e += FS_T) {
         S.key[cnt + e] = S.tkey[e];
@@ -1130,7 +1139,6 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         const int K = P.K;
         const double* tmg = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
         const int ntm = P.nch * Tc * Tc;
-        const double* tmS = ntm <= PK_TMC ? S.tm : tmg;
         int mk = INT_MIN;
         // the scan: warp 0 alone (scan_job), or with the list step spread over
         // every warp when the tile maxima fit in registers
@@ -1157,11 +1165,10 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             // stage the template (matcher.hpp:44-61 order), the mask rows and the run groups
             if (ntm <= PK_TMC)
                 for (int e = tid - 32; e < ntm; e += FS_T - 32) cp_async8(&S.tm[e], tmg + e);
-            // the mask rows and run groups of this mask variant (host tables)
+            // the run groups of this mask variant (host tables)
             const int4* mt = P.mtab + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * MT_STRIDE;
             const int4 info = __ldg(mt);
-            for (int e = tid - 32; e < MT_ROWS4 + info.y; e += FS_T - 32)
-                cp_async16(e < MT_ROWS4 ? reinterpret_cast<int4*>(S.rows) + e : &S.grp[e - MT_ROWS4], mt + 1 + e);
+            for (int e = tid - 32; e < info.y; e += FS_T - 32) cp_async16(&S.grp[e], mt + 1 + MT_ROWS4 + e);
             if (tid == 32) {
                 S.misc[2] = info.x;
                 S.misc[3] = info.y;
@@ -1253,7 +1260,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             if (g == 1) {
                 picked = S.tie[0];
             } else {
-                rescore_keys(P, S, tmS, nr, ngrp, S.tie, g, S.key);
+                rescore_keys(P, S, tmg, nr, ngrp, S.tie, g, S.key);
                 if (wid == 0) {  // the rk-th best of the group by (fp64 desc, index asc)
                     for (int round = 0; round <= rk; ++round) {
                         double bk = 0.0;
@@ -1303,7 +1310,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             }
             __syncthreads();
             const int nt = S.misc[6];
-            if (nt > 0) rescore_keys(P, S, tmS, nr, ngrp, S.tie, nt, S.key);
+            if (nt > 0) rescore_keys(P, S, tmg, nr, ngrp, S.tie, nt, S.key);
             if (wid == 0) {
                 const int si = lane < n ? S.cs[lane] : INT_MIN;
                 const int ii = lane < n ? S.cidx[lane] : INT_MAX;
@@ -1323,7 +1330,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             ntop = min(K, n);
             __syncthreads();
         } else if (n >= 0) {
-            fast_batch(P, S, tmS, nr, ngrp, n, ntop, K);
+            fast_batch(P, S, tmg, nr, ngrp, n, ntop, K);
         } else {
             // list overflow without the bulk kernel: every window >= M_K, in batches
             const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
@@ -1343,14 +1350,14 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                 }
                 __syncthreads();
                 if (cnt + tot > SC_LC) {
-                    fast_batch(P, S, tmS, nr, ngrp, cnt, ntop, K);
+                    fast_batch(P, S, tmg, nr, ngrp, cnt, ntop, K);
                     cnt = 0;
                 }
                 if (q) S.cidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
                 cnt += tot;
                 __syncthreads();
             }
-            if (cnt > 0) fast_batch(P, S, tmS, nr, ngrp, cnt, ntop, K);
+            if (cnt > 0) fast_batch(P, S, tmg, nr, ngrp, cnt, ntop, K);
         }
         fclk[2] = clock64();
         // choose (matcher.hpp:207-241)

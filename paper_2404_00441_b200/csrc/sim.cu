@@ -198,7 +198,8 @@ double pair_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
 // Mask tables of the fast select (MT_STRIDE int4 per mask variant): the mask
 // rows of the placement and its rescoring run groups -- up to FS_G cells of
 // consecutive rows of one channel with the same column run (a run longer than
-// FS_G is a group of its own, summed sequentially).
+// FS_G is a group of its own, summed sequentially), as int4 (channel, first
+// row-table index | first row << 16, rows, t0 << 8 | run length).
 void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
     tab.assign(static_cast<size_t>(8) * MT_STRIDE, make_int4(0, 0, 0, 0));
     const int shapes[8][3] = {{kL, 0, 0}, {kL, 0, 1}, {kL, 1, 0}, {kL, 1, 1},
@@ -223,10 +224,11 @@ void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
             while (k < nr) {
                 const int t0 = rows[k].y, len = rows[k].z - rows[k].y;
                 int nk = 1;
-                while (k + nk < nr && rows[k + nk].y == t0 && rows[k + nk].z - t0 == len && (nk + 1) * len <= FS_G)
+                while (k + nk < nr && rows[k + nk].x == rows[k].x + nk && rows[k + nk].y == t0 &&
+                       rows[k + nk].z - t0 == len && (nk + 1) * len <= FS_G)
                     ++nk;
                 if (len > FS_G) nk = 1;
-                if (ng < FS_MAXG) grp[ng++] = make_int4(ch, k, nk, (t0 << 8) | len);
+                if (ng < FS_MAXG) grp[ng++] = make_int4(ch, k | (rows[k].x << 16), nk, (t0 << 8) | len);
                 k += nk;
             }
         }
