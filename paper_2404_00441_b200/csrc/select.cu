@@ -936,7 +936,7 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
     for (int it = threadIdx.x; it < ng * ngrp; it += FS_T) {
         const int e = it / ngrp, g = it - e * ngrp;
         const int4 G = S.grp[g];  // rows s0 .. s0 + nk - 1, columns t0 .. t0 + len - 1
-        const int ch = G.x, k0 = G.y & 0xffff, s0 = G.y >> 16, nk = G.z, t0 = G.w >> 8, len = G.w & 255;
+        const int ch = G.x, k0 = G.y & 0xffff, s0 = G.y >> 16, nk = G.z & 255, t0 = G.w >> 8, len = G.w & 255;
         const int pos = cidx[e0 + e];
         const int x = pos / P.out_w, y = pos - x * P.out_w;
         const double* a0 = P.ti64 + ch * plane + static_cast<size_t>(x + s0) * P.wc + y + t0;
@@ -956,30 +956,23 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
             rs[0] = sum;
             continue;
         }
-        {
-            int kk = 0, t = 0;
-#pragma unroll
-            for (int c = 0; c < FS_G; ++c) {
-                pv[c] = kk < nk ? __dmul_rn(__ldg(a0 + static_cast<size_t>(kk) * P.wc + t), tb[b0 + kk * P.Tc + t])
-                                : 0.0;
-                if (++t == len) {
-                    t = 0;
-                    ++kk;
-                }
-            }
-        }
-        double sum = 0.0;
-        int kk = 0, t = 0;
+        // Cells past nk * len read a clamped in-window address and are never
+        // stored, so no load needs a predicate and all FS_G are in flight at once.
+        const int inv = (4096 + len - 1) / len;  // c / len == (c * inv) >> 12 for c < 16
 #pragma unroll
         for (int c = 0; c < FS_G; ++c) {
-            if (kk < nk) {
-                sum = __dadd_rn(sum, pv[c]);
-                if (++t == len) {
-                    rs[kk] = sum;
-                    sum = 0.0;
-                    t = 0;
-                    ++kk;
-                }
+            const int kq = (c * inv) >> 12, t = c - kq * len, kk = min(kq, nk - 1);
+            pv[c] = __dmul_rn(__ldg(a0 + kk * P.wc + t), tb[b0 + kk * P.Tc + t]);
+        }
+        const int endm = G.z >> 8;  // cells that end a row
+        double sum = 0.0;
+        int kk = 0;
+#pragma unroll
+        for (int c = 0; c < FS_G; ++c) {
+            sum = __dadd_rn(sum, pv[c]);
+            if ((endm >> c) & 1) {
+                rs[kk++] = sum;
+                sum = 0.0;
             }
         }
     }

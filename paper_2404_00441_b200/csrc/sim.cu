@@ -199,7 +199,8 @@ double pair_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
 // rows of the placement and its rescoring run groups -- up to FS_G cells of
 // consecutive rows of one channel with the same column run (a run longer than
 // FS_G is a group of its own, summed sequentially), as int4 (channel, first
-// row-table index | first row << 16, rows, t0 << 8 | run length).
+// row-table index | first row << 16, rows | row-end cell mask << 8, t0 << 8 |
+// run length).
 void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
     tab.assign(static_cast<size_t>(8) * MT_STRIDE, make_int4(0, 0, 0, 0));
     const int shapes[8][3] = {{kL, 0, 0}, {kL, 0, 1}, {kL, 1, 0}, {kL, 1, 1},
@@ -228,7 +229,10 @@ void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
                        rows[k + nk].z - t0 == len && (nk + 1) * len <= FS_G)
                     ++nk;
                 if (len > FS_G) nk = 1;
-                if (ng < FS_MAXG) grp[ng++] = make_int4(ch, k | (rows[k].x << 16), nk, (t0 << 8) | len);
+                int endm = 0;  // cells that end a row (nk * len <= FS_G)
+                if (len <= FS_G)
+                    for (int q = 0; q < nk; ++q) endm |= 1 << (q * len + len - 1);
+                if (ng < FS_MAXG) grp[ng++] = make_int4(ch, k | (rows[k].x << 16), nk | (endm << 8), (t0 << 8) | len);
                 k += nk;
             }
         }
