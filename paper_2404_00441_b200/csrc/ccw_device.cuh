@@ -35,6 +35,18 @@ struct Job {
 };
 
 // Parameters shared by every job of one simulate call.
+// Shared rescoring (select_fast_kernel): a placement with a large equal-score
+// group posts it in chunks; the launch's CTAs that finish their own placement
+// claim and rescore chunks.  One board (+ per-slot counters) per launch.
+constexpr int HB_CAP = 1024;  // posts per board
+struct HelpBoard {
+    int nposts;
+    int pad[3];
+    int posts[HB_CAP];  // slot + 1 (0: being written)
+};
+// per slot of a board: int4 (next chunk, finished chunks, windows,
+// windows per chunk | mask variant << 16)
+
 struct SimParams {
     // training image
     const uint8_t* ti;       // h*w codes
@@ -84,6 +96,14 @@ struct SimParams {
     const int4* mtab;        // fast select: mask rows and run groups per mask variant
     const int32_t* nnmap;    // normalized screen: [8 mask variants][npos] sum over mask and
                              // channels of squared TI block counts (null otherwise)
+    HelpBoard* hb;           // shared rescoring board of this launch (null: off)
+    int4* hs;                //   ... its per-slot counters
+    HelpBoard* hb_reset;     // board of the next launch (reset by block 0)
+    int4* hs_reset;          //   ... its per-slot counters
+    int hs_n;                // slots per board
+    int* hpos;               // per job slot: SC_LC posted window positions
+    double* hkeys;           //   ... their fp64 keys
+    int help_min;            // smallest group that is shared
     int* bulk_sync;          // per job slot: [next position block, finished CTAs]
     double* bulk_keys;       // per job slot x CTA: that CTA's top-K keys
     int* bulk_idx;           //   ... and positions

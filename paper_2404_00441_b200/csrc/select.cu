@@ -979,16 +979,16 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
 }
 
 // fp64 keys of the windows cidx[0, cnt) (reference order, see fast_batch).
+// (tmg: the placement's template in global memory; staged in S.tm when it
+// fits, unless own_tm is false -- a chunk of another placement.)
 __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, const double* tmg, int nr,
-                                             int ngrp, const int* cidx, int cnt, double* keys) {
+                                             int ngrp, const int* cidx, int cnt, double* keys,
+                                             bool own_tm = true) {
     const int tid = threadIdx.x;
     const int R = nr * P.nch;
     const int EB = max(1, FS_RS / R);
-    const bool tm_smem = P.nch * P.Tc * P.Tc <= PK_TMC;
+    const bool tm_smem = own_tm && P.nch * P.Tc * P.Tc <= PK_TMC;
     if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
-#ifdef CCW_DBG_TAIL
-    long long c_items = 0, c_fold = 0, c0 = clock64();
-#endif
     for (int e0 = 0; e0 < cnt; e0 += EB) {
         const int ng = min(EB, cnt - e0);
         if (tm_smem)
@@ -996,10 +996,6 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
         else
             rescore_items(P, S, tmg, nr, ngrp, cidx, e0, ng, R);
         __syncthreads();
-#ifdef CCW_DBG_TAIL
-        const long long c1 = clock64();
-        c_items += c1 - c0;
-#endif
         for (int e = tid; e < ng; e += FS_T) {
             // the fold is one sequential chain; its operands load 8 at a time
             const double* rp = S.rsum + e * R;
@@ -1016,19 +1012,7 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
             keys[e0 + e] = acc;
         }
         __syncthreads();
-#ifdef CCW_DBG_TAIL
-        c0 = clock64();
-        c_fold += c0 - c1;
-#endif
     }
-#ifdef CCW_DBG_TAIL
-    if (P.stats && tid == 0 && cnt >= 64) {
-        atomicAdd(&P.stats[31], 1ull);
-        atomicAdd(&P.stats[14], static_cast<unsigned long long>(c_items));
-        atomicAdd(&P.stats[15], static_cast<unsigned long long>(c_fold));
-        atomicAdd(&P.stats[3], static_cast<unsigned long long>(cnt));
-    }
-#endif
 }
 
 // Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
@@ -1105,6 +1089,126 @@ __device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, cons
     __syncthreads();
 }
 
+
+// ---- shared rescoring (HelpBoard, ccw_device.cuh) ----
+
+// Rescore chunk c of slot's posted group (every thread calls; uses S.grp,
+// S.cs, S.rsum, S.key) and count it finished.
+__device__ __forceinline__ void hb_chunk(const SimParams& P, FastSmem& S, int slot, int c, int4 info) {
+    const int tid = threadIdx.x;
+    const int cw = info.w & 0xffff, var = info.w >> 16;
+    const int e0 = c * cw, n = min(cw, info.z - e0);
+    const int4* mt = P.mtab + static_cast<size_t>(var) * MT_STRIDE;
+    const int4 mi = __ldg(mt);
+    for (int e = tid; e < mi.y; e += FS_T) S.grp[e] = __ldg(mt + 1 + MT_ROWS4 + e);
+    for (int e = tid; e < n; e += FS_T) S.cs[e] = __ldcg(P.hpos + static_cast<size_t>(slot) * SC_LC + e0 + e);
+    __syncthreads();
+    const double* tmg = P.tm64 + static_cast<size_t>(slot) * P.nch * P.Tc * P.Tc;
+    rescore_keys(P, S, tmg, mi.x, mi.y, S.cs, n, S.key, false);
+    for (int e = tid; e < n; e += FS_T) P.hkeys[static_cast<size_t>(slot) * SC_LC + e0 + e] = S.key[e];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(&P.hs[slot].y, 1);
+#ifdef CCW_DBG_TAIL
+    if (tid == 0 && P.stats) {
+        atomicAdd(&P.stats[14], 1ull);
+        if (slot == static_cast<int>(blockIdx.x)) atomicAdd(&P.stats[15], 1ull);
+    }
+#endif
+}
+
+// Claim chunks of slot's posted group until none is left (every thread calls).
+__device__ __forceinline__ void hb_drain(const SimParams& P, FastSmem& S, int slot, int4 info) {
+    const int nchunk = (info.z + (info.w & 0xffff) - 1) / (info.w & 0xffff);
+    while (true) {
+        if (threadIdx.x == 0) {  // (a plain read first: most helpers arrive after the last claim)
+            const int seen = *reinterpret_cast<volatile int*>(&P.hs[slot].x);
+            S.misc[0] = seen >= nchunk ? seen : atomicAdd(&P.hs[slot].x, 1);
+        }
+        __syncthreads();
+        const int c = S.misc[0];
+        __syncthreads();
+        if (c >= nchunk) return;
+        hb_chunk(P, S, slot, c, info);
+    }
+}
+
+// Help with every group posted so far in this launch (every thread calls).
+__device__ __forceinline__ void hb_help(const SimParams& P, FastSmem& S) {
+    const int tid = threadIdx.x;
+    if (tid == 0) S.misc[1] = *reinterpret_cast<volatile int*>(&P.hb->nposts);
+    __syncthreads();
+    const int np = min(S.misc[1], HB_CAP);
+    for (int q = 0; q < np; ++q) {
+        __syncthreads();
+        if (tid == 0) {
+            volatile int* pp = &P.hb->posts[q];
+            int v;
+            while ((v = *pp) == 0) {  // (its poster is running and writes it next)
+            }
+            __threadfence();
+            const int slot = v - 1;
+            const int4 info = __ldcg(&P.hs[slot]);
+            S.misc[2] = slot;
+            S.misc[4] = info.z;
+            S.misc[5] = info.w;
+        }
+        __syncthreads();
+        const int slot = S.misc[2];
+        hb_drain(P, S, slot, make_int4(0, 0, S.misc[4], S.misc[5]));
+    }
+}
+
+// Rescore S.tie[0, g) of this placement with the launch's help: post the
+// group, rescore its chunks until none is left (helpers claim the others),
+// wait for the helpers' chunks, gather the keys into S.key.  Returns false
+// (nothing posted) when the board is full.  Every thread calls.
+__device__ __forceinline__ bool hb_rescore(const SimParams& P, FastSmem& S, int slot, int g, int ngrp,
+                                           int var) {
+    const int tid = threadIdx.x;
+    const int cw = max(1, FS_T / ngrp);  // windows per chunk: one round of items
+    const int nchunk = (g + cw - 1) / cw;
+    const int4 info = make_int4(0, 0, g, cw | var << 16);
+    for (int e = tid; e < g; e += FS_T) P.hpos[static_cast<size_t>(slot) * SC_LC + e] = S.tie[e];
+    if (tid == 0) {
+        P.hs[slot].z = info.z;
+        P.hs[slot].w = info.w;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const int q = atomicAdd(&P.hb->nposts, 1);
+        if (q < HB_CAP) atomicExch(&P.hb->posts[q], slot + 1);
+        S.misc[3] = q < HB_CAP;
+    }
+    __syncthreads();
+    if (!S.misc[3]) return false;
+#ifdef CCW_DBG_TAIL
+    const long long h0 = clock64();
+#endif
+    hb_drain(P, S, slot, info);
+#ifdef CCW_DBG_TAIL
+    const long long h1 = clock64();
+#endif
+    if (tid == 0) {
+        volatile int* done = &P.hs[slot].y;
+        while (*done < nchunk) {
+        }
+        __threadfence();
+#ifdef CCW_DBG_TAIL
+        if (P.stats) {
+            atomicAdd(&P.stats[31], 1ull);
+            atomicAdd(&P.stats[3], static_cast<unsigned long long>(h1 - h0));
+            atomicAdd(&P.stats[6], static_cast<unsigned long long>(clock64() - h1));
+        }
+#endif
+    }
+    __syncthreads();
+    for (int e = tid; e < g; e += FS_T) S.key[e] = __ldcg(P.hkeys + static_cast<size_t>(slot) * SC_LC + e);
+    __syncthreads();
+    return true;
+}
+
 #ifndef CCW_COOP_SCAN
 #define CCW_COOP_SCAN 1
 #endif
@@ -1119,6 +1223,11 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     tl_mark(P.tl, 2);
     pdl_wait();
     tl_mark(P.tl, 0);
+    if (P.hb_reset && slot == 0) {  // the next launch's board (the last launch that used it is complete)
+        for (int i = tid; i < HB_CAP; i += FS_T) P.hb_reset->posts[i] = 0;
+        for (int i = tid; i < P.hs_n; i += FS_T) P.hs_reset[i] = make_int4(0, 0, 0, 0);
+        if (tid == 0) P.hb_reset->nposts = 0;
+    }
     if (slot >= nj) return;
     const int gj = job0 + slot;
     const Job jb = jobs[gj];
@@ -1253,7 +1362,9 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             if (g == 1) {
                 picked = S.tie[0];
             } else {
-                rescore_keys(P, S, tmg, nr, ngrp, S.tie, g, S.key);
+                if (!(P.hb && g >= P.help_min &&
+                      hb_rescore(P, S, slot, g, ngrp, mask_variant(jb.shape, jb.vleft, jb.htop))))
+                    rescore_keys(P, S, tmg, nr, ngrp, S.tie, g, S.key);
                 if (wid == 0) {  // the rk-th best of the group by (fp64 desc, index asc)
                     for (int round = 0; round <= rk; ++round) {
                         double bk = 0.0;
@@ -1392,6 +1503,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
 #endif
         }
     }
+    if (P.hb) hb_help(P, S);  // rescore posted chunks of this launch's large groups
     tl_mark(P.tl, 1);
 }
 

@@ -609,6 +609,29 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         d_depcnt = ctx->depcnt.as<int>(G * maxj);
         CCW_CUDA(cudaMemsetAsync(d_depcnt, 0, sizeof(int) * G * maxj, st));
     }
+    // shared rescoring of large equal-score groups (select_fast_kernel): two
+    // boards per group, alternating between its select launches
+    HelpBoard* d_boards = nullptr;
+    int4* d_hslots = nullptr;
+    if (warp_select) {
+        int help_min = 32;
+        if (const char* e = getenv("CCW_HELP_MIN")) help_min = atoi(e);
+        if (help_min > 0) {
+            d_boards = ctx->hboards.as<HelpBoard>(2 * G);
+            CCW_CUDA(cudaMemsetAsync(d_boards, 0, sizeof(HelpBoard) * 2 * G, st));
+            d_hslots = ctx->hdone.as<int4>(2 * G * maxj);
+            CCW_CUDA(cudaMemsetAsync(d_hslots, 0, sizeof(int4) * 2 * G * maxj, st));
+            int* d_hpos = ctx->hpos.as<int>(G * maxj * SC_LC);
+            double* d_hkeys = ctx->hkeys.as<double>(G * maxj * SC_LC);
+            for (int g = 0; g < G; ++g) {
+                GP[g].hpos = d_hpos + g * maxj * SC_LC;
+                GP[g].hkeys = d_hkeys + g * maxj * SC_LC;
+                GP[g].hs_n = static_cast<int>(maxj);
+                GP[g].help_min = help_min;
+            }
+        }
+    }
+    std::vector<int> hb_par(G, 0);
     // per (group, parity) parameter sets
     std::vector<std::array<SimParams, 2>> GPP(G);
     const size_t tm_half = G * maxj * ti->nch * Tc * Tc, w8_half = G * maxj * kpad;
@@ -828,6 +851,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 if (skip_sel && !first_wave) {
                 } else if (warp_select || (first_wave && !cfg.min_cut)) {
                     const Job* dj = d_jobs;
+                    if (d_boards) {
+                        Q.hb = d_boards + 2 * g + hb_par[g];
+                        Q.hs = d_hslots + (2 * g + hb_par[g]) * maxj;
+                        Q.hb_reset = d_boards + 2 * g + (1 - hb_par[g]);
+                        Q.hs_reset = d_hslots + (2 * g + (1 - hb_par[g])) * maxj;
+                        hb_par[g] ^= 1;
+                    }
                     launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
                                static_cast<int>(j0), nj);
                     if (Q.defer && !first_wave) {
@@ -1015,8 +1045,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         fprintf(stderr, "select cycles histogram <10k %llu <20k %llu <40k %llu <80k %llu >=80k %llu | long jobs: scan+stage %llu batch %llu choose+map %llu candidates %llu\n",
                 stats[22], stats[23], stats[24], stats[25], stats[26], stats[27], stats[28], stats[29], stats[30]);
     if (getenv("CCW_TAIL"))
-        fprintf(stderr, "rescores of >= 64 windows: %llu, windows %llu, item cycles %llu, fold cycles %llu\n",
-                stats[31], stats[3], stats[14], stats[15]);
+        fprintf(stderr, "shared rescoring: posts %llu, chunks %llu (own %llu), owner help cycles %llu wait cycles %llu\n",
+                stats[31], stats[14], stats[15], stats[3], stats[6]);
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
