@@ -117,6 +117,7 @@ typedef struct ccw_timing {
     int64_t list_overflows; /* placements with more than 256 windows at or above the tile bound */
     double host_prep_ms;    /* host schedule build (plans + mt19937_64 draws) before launch */
     int64_t bulk_jobs;      /* placements whose tie group went to the bulk (CTA-wide) rescoring */
+    int64_t shared_groups;  /* equal-score groups rescored in chunks shared across the launch's CTAs */
 } ccw_timing;
 
 typedef struct ccw_ctx ccw_ctx;

@@ -35,6 +35,8 @@ struct Job {
 };
 
 // Parameters shared by every job of one simulate call.
+constexpr int kNumStats = 48;  // device counters per simulation call (SimParams::stats)
+
 // Shared rescoring (select_fast_kernel): a placement with a large equal-score
 // group posts it in chunks; the launch's CTAs that finish their own placement
 // claim and rescore chunks.  One board (+ per-slot counters) per launch.

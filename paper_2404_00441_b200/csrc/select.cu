@@ -1111,8 +1111,8 @@ __device__ __forceinline__ void hb_chunk(const SimParams& P, FastSmem& S, int sl
     if (tid == 0) atomicAdd(&P.hs[slot].y, 1);
 #ifdef CCW_DBG_TAIL
     if (tid == 0 && P.stats) {
-        atomicAdd(&P.stats[14], 1ull);
-        if (slot == static_cast<int>(blockIdx.x)) atomicAdd(&P.stats[15], 1ull);
+        atomicAdd(&P.stats[33], 1ull);
+        if (slot == static_cast<int>(blockIdx.x)) atomicAdd(&P.stats[34], 1ull);
     }
 #endif
 }
@@ -1195,11 +1195,11 @@ __device__ __forceinline__ bool hb_rescore(const SimParams& P, FastSmem& S, int 
         while (*done < nchunk) {
         }
         __threadfence();
+        if (P.stats) atomicAdd(&P.stats[32], 1ull);
 #ifdef CCW_DBG_TAIL
         if (P.stats) {
-            atomicAdd(&P.stats[31], 1ull);
-            atomicAdd(&P.stats[3], static_cast<unsigned long long>(h1 - h0));
-            atomicAdd(&P.stats[6], static_cast<unsigned long long>(clock64() - h1));
+            atomicAdd(&P.stats[35], static_cast<unsigned long long>(h1 - h0));
+            atomicAdd(&P.stats[36], static_cast<unsigned long long>(clock64() - h1));
         }
 #endif
     }

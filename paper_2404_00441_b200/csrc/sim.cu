@@ -521,8 +521,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.nnmap = ti_nnmap(ti, Tc, OVc, st);
         d_cjob = ctx->cjob.as<int32_t>(G * maxj);
     }
-    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(32);
-    CCW_CUDA(cudaMemsetAsync(d_stats, 0, 32 * sizeof(unsigned long long), st));
+    unsigned long long* d_stats = ctx->stats.as<unsigned long long>(kNumStats);
+    CCW_CUDA(cudaMemsetAsync(d_stats, 0, kNumStats * sizeof(unsigned long long), st));
     // source-block map (fast or_prep), valid whenever pastes are verbatim TI blocks
     const int swc = ww / B;
     int32_t* d_src = nullptr;
@@ -971,7 +971,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     CCW_CUDA(cudaEventRecord(ev1, st));
     if (h_out && !stream_out)
         CCW_CUDA(cudaMemcpyAsync(h_dst, fin, out_bytes, cudaMemcpyDeviceToHost, st));
-    unsigned long long stats[32] = {0};
+    unsigned long long stats[kNumStats] = {0};
     CCW_CUDA(cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
     std::vector<int> mism(n_real, 0);
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
@@ -1046,7 +1046,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 stats[22], stats[23], stats[24], stats[25], stats[26], stats[27], stats[28], stats[29], stats[30]);
     if (getenv("CCW_TAIL"))
         fprintf(stderr, "shared rescoring: posts %llu, chunks %llu (own %llu), owner help cycles %llu wait cycles %llu\n",
-                stats[31], stats[14], stats[15], stats[3], stats[6]);
+                stats[32], stats[33], stats[34], stats[35], stats[36]);
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
@@ -1055,6 +1055,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.screened_jobs = static_cast<int64_t>(stats[1]);
     ctx->timing.list_overflows = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
+    ctx->timing.shared_groups = static_cast<int64_t>(stats[32]);
     if (bulk_launch && stats[3] == 0)
         ctx->bulk_off[bulk_key] = true;
     else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back

@@ -131,6 +131,25 @@ def test_large_tie_groups_bulk_path(oracle, k):
             assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+@pytest.mark.parametrize("help_min", [2, 8])
+def test_shared_rescoring(oracle, help_min, monkeypatch):
+    """Equal-score groups of at least help_min windows are rescored in chunks
+    claimed by the launch's other CTAs (select.cu hb_rescore); a low
+    threshold makes most unconditional picks go that way.  Bit-exact."""
+    from paper_2404_00441_b200 import synth
+    monkeypatch.setenv("CCW_HELP_MIN", str(help_min))
+    ti_a = synth.channel_ti(200, 200, 31, scale=5.0)
+    ti = cs.CategoricalGrid(200, 200, 2, ti_a)
+    d = dict(sg_height=260, sg_width=230, template_size=32, overlap=8, dwt_level=2, candidates=5)
+    dev = cs.default_device()
+    seeds = [cs.mix64(9, i) for i in range(6)]
+    res = cs.simulate_batch(ti, to_cfg(d, None), seeds)
+    assert dev.last_timing()["shared_groups"] > 0
+    for s, r in zip(seeds, res):
+        o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"])
+
+
 @pytest.mark.parametrize("k", [4, 8])
 def test_k_above_tile_count_with_ties(oracle, k):
     """Fewer 128-position tiles than K and a blocky TI (every window ties):
