@@ -195,6 +195,29 @@ double pair_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
     return t;
 }
 
+// Raster-path variant (origin * 2 + column-major) of a realization: its
+// mt19937_64's first two outputs through bounded(4) and bounded(2)
+// (simulator.hpp:148-152).  Powers of two are never rejected by bounded()
+// (threshold (2^64 - n) mod n = 0), and outputs 0 and 1 read only state words
+// 0-2 and 156-157 of the seeded state, so the seeding recurrence stops at 157.
+int path_variant_of_seed(uint64_t seed) {
+    uint64_t x[158];
+    x[0] = seed;
+    for (int i = 1; i < 158; ++i) x[i] = 6364136223846793005ULL * (x[i - 1] ^ (x[i - 1] >> 62)) + i;
+    auto out = [&](int k) {
+        const uint64_t y = (x[k] & 0xFFFFFFFF80000000ULL) | (x[k + 1] & 0x7FFFFFFFULL);
+        uint64_t v = x[k + 156] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ULL : 0);
+        v ^= (v >> 29) & 0x5555555555555555ULL;
+        v ^= (v << 17) & 0x71D67FFFEDA60000ULL;
+        v ^= (v << 37) & 0xFFF7EEE000000000ULL;
+        v ^= v >> 43;
+        return v;
+    };
+    const int origin = static_cast<int>(out(0) % 4);
+    const int cm = static_cast<int>(out(1) % 2);
+    return origin * 2 + cm;
+}
+
 // Mask tables of the fast select (MT_STRIDE int4 per mask variant): the mask
 // rows of the placement and its rescoring run groups -- up to FS_G cells of
 // consecutive rows of one channel with the same column run (a run longer than
@@ -258,21 +281,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const int reach = (T + stride - 1) / stride - 1;  // footprints overlap up to `reach` steps
     const int keymul = reach + 1;
 
-    // ---- host schedule: raster paths, hard-data lattice, mt19937_64 draws.
-    // A raster path (simulator.hpp:148-190) is one of 8 variants (origin x
-    // major order); each realization draws its variant, then its per-placement
-    // draws.  Jobs are written straight into pinned staging memory in
+    // ---- host schedule: raster paths, hard-data lattice, wave layout.  A
+    // raster path (simulator.hpp:148-190) is one of 8 variants (origin x major
+    // order) drawn first by each realization's mt19937_64; the per-placement
+    // draws and the jobs themselves are made on the device (schedule.cu) in
     // (group, wave, realization, placement) order.
     std::vector<Plan> variants(8);
     std::vector<char> have(8, 0);
-    std::vector<int> vid(n_real);
-    std::vector<std::mt19937_64> rngs(n_real);
-    ctx->pool.run(n_real, [&](int r) {  // seeding + the two plan draws, in parallel
-        rngs[r].seed(seeds[r]);
-        const int origin = static_cast<int>(bounded(rngs[r], 4));
-        const bool cm = bounded(rngs[r], 2) == 1;
-        vid[r] = origin * 2 + (cm ? 1 : 0);
-    });
+    std::vector<int32_t> vid(n_real);
+    for (int r = 0; r < n_real; ++r) vid[r] = path_variant_of_seed(seeds[r]);
+    const double t_seed = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
     for (int r = 0; r < n_real; ++r)
         if (!have[vid[r]]) {
             variants[vid[r]] = make_plan_from(cfg, vid[r] / 2, (vid[r] & 1) != 0);
@@ -323,12 +341,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         if (have[v]) max_key = std::max(max_key, keymul * (variants[v].n_outer - 1) + variants[v].n_inner - 1);
     const int nkeys = max_key + 1;
     // per-variant wave histograms
-    std::vector<std::vector<int>> vhist(8);
+    std::vector<std::vector<int>> vhist(8), vhistL(8);  // placements (L-shaped ones) per wave
     for (int v = 0; v < 8; ++v)
         if (have[v]) {
             vhist[v].assign(nkeys, 0);
             const Plan& p = variants[v];
-            for (size_t k = 0; k < p.tops.size(); ++k) ++vhist[v][keymul * p.outer_idx[k] + p.inner_idx[k]];
+            vhistL[v].assign(nkeys, 0);
+            for (size_t k = 0; k < p.tops.size(); ++k) {
+                ++vhist[v][keymul * p.outer_idx[k] + p.inner_idx[k]];
+                if (p.shapes[k] == kL) ++vhistL[v][keymul * p.outer_idx[k] + p.inner_idx[k]];
+            }
         }
 
     // Realizations are split into G independent groups, each on its own
@@ -351,60 +373,21 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         for (int k = 0; k <= nkeys; ++k) wave_off[g].push_back(bucket[static_cast<size_t>(g) * nkeys + std::min(k, nkeys)]);
         for (int k = 0; k < nkeys; ++k) max_wave = std::max(max_wave, wave_off[g][k + 1] - wave_off[g][k]);
     }
-    // each realization's first slot in every wave bucket
-    std::vector<size_t> roff(static_cast<size_t>(n_real) * nkeys);
+    // each realization's first slot in every wave bucket (uploaded for the device schedule)
+    int32_t* roff = static_cast<int32_t*>(ctx->h_stage.get(sizeof(int32_t) * (static_cast<size_t>(n_real) * nkeys + n_real)));
+    int32_t* vid_stage = roff + static_cast<size_t>(n_real) * nkeys;
+    std::copy(vid.begin(), vid.end(), vid_stage);
     {
         std::vector<size_t> fill(bucket.begin(), bucket.end() - 1);
         for (int r = 0; r < n_real; ++r) {
             const size_t g = group_of(r);
             for (int k = 0; k < nkeys; ++k) {
-                roff[static_cast<size_t>(r) * nkeys + k] = fill[g * nkeys + k];
+                roff[static_cast<size_t>(r) * nkeys + k] = static_cast<int32_t>(fill[g * nkeys + k]);
                 fill[g * nkeys + k] += vhist[vid[r]][k];
             }
         }
     }
-    Job* flat = static_cast<Job*>(ctx->h_stage.get(sizeof(Job) * total_jobs));
-    auto build_one = [&](int r) {
-        std::mt19937_64& rng = rngs[r];
-        const Plan& p = variants[vid[r]];
-        size_t* off = roff.data() + static_cast<size_t>(r) * nkeys;
-        const int cnt = static_cast<int>(p.tops.size());
-        // flat index of every placement (in placement order within each wave bucket)
-        std::vector<int32_t> fi(cnt);
-        {
-            std::vector<size_t> o2(off, off + nkeys);
-            for (int k = 0; k < cnt; ++k) fi[k] = static_cast<int32_t>(o2[keymul * p.outer_idx[k] + p.inner_idx[k]]++);
-        }
-        const int ni = p.n_inner, no = p.n_outer;
-        for (int k = 0; k < cnt; ++k) {
-            Job jb;
-            {  // raster neighbours (k = o * n_inner + i): next-wave readers, previous-wave writers
-                const int o = p.outer_idx[k], i = p.inner_idx[k];
-                jb.dep0 = i + 1 < ni ? fi[k + 1] : -1;
-                jb.dep1 = (o + 1 < no && i >= 1) ? fi[k + ni - 1] : -1;
-                jb.ndep = (i >= 1 ? 1 : 0) + (o >= 1 && i + 1 < ni ? 1 : 0);
-            }
-            jb.real = r;
-            jb.place = k;
-            jb.top = p.tops[k];
-            jb.left = p.lefts[k];
-            jb.shape = p.shapes[k];
-            jb.vleft = p.vertical_on_left();
-            jb.htop = p.horizontal_on_top();
-            jb.pick = 0;
-            jb.fr = jb.fc = 0;
-            if (jb.shape == kNone) {  // simulator.hpp:450-453
-                jb.fr = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->h - T) / B + 1))) * B;
-                jb.fc = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->w - T) / B + 1))) * B;
-            } else {
-                const bool cond = !lattice_hd.empty() &&
-                                  lattice_hd[static_cast<size_t>(jb.top / stride) * nlc + jb.left / stride];
-                jb.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
-            }
-            flat[off[keymul * p.outer_idx[k] + p.inner_idx[k]]++] = jb;
-        }
-    };
-    ctx->pool.run(n_real, build_one);
+    const double t_sched = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
     const double host_prep_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
 
@@ -421,7 +404,43 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
 
     // ---- device buffers
     Job* d_jobs = ctx->jobs.as<Job>(total_jobs);
-    CCW_CUDA(cudaMemcpyAsync(d_jobs, flat, sizeof(Job) * total_jobs, cudaMemcpyHostToDevice, st));
+    {
+        const size_t nstage = static_cast<size_t>(n_real) * nkeys + n_real;
+        int32_t* d_roff = ctx->roff.as<int32_t>(nstage);
+        CCW_CUDA(cudaMemcpyAsync(d_roff, roff, sizeof(int32_t) * nstage, cudaMemcpyHostToDevice, st));
+        int* d_err = ctx->sched_err.as<int>(1);
+        CCW_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+        SchedParams SP{};
+        SP.seeds = static_cast<const uint64_t*>(ctx->seeds.get(sizeof(uint64_t) * n_real));
+        CCW_CUDA(cudaMemcpyAsync(const_cast<uint64_t*>(SP.seeds), seeds, sizeof(uint64_t) * n_real,
+                                 cudaMemcpyHostToDevice, st));
+        SP.vid = d_roff + static_cast<size_t>(n_real) * nkeys;
+        SP.roff = d_roff;
+        if (!lattice_hd.empty()) {
+            uint8_t* d_lat = ctx->lattice.as<uint8_t>(lattice_hd.size());
+            CCW_CUDA(cudaMemcpyAsync(d_lat, lattice_hd.data(), lattice_hd.size(), cudaMemcpyHostToDevice, st));
+            SP.lattice_hd = d_lat;
+        }
+        SP.err = d_err;
+        SP.n_real = n_real;
+        SP.nkeys = nkeys;
+        SP.keymul = keymul;
+        SP.nlr = nlr;
+        SP.nlc = nlc;
+        SP.stride = stride;
+        SP.B = B;
+        SP.Kp = Kp;
+        SP.nfr = static_cast<uint64_t>((ti->h - T) / B + 1);
+        SP.nfc = static_cast<uint64_t>((ti->w - T) / B + 1);
+        SP.thr_fr = (0 - SP.nfr) % SP.nfr;
+        SP.thr_fc = (0 - SP.nfc) % SP.nfc;
+        SP.thr_k = (0 - static_cast<uint64_t>(Kp)) % static_cast<uint64_t>(Kp);
+        SP.nout = 4 + nlr * nlc;  // the path, the first placement's two, one per other placement
+        SP.outs = ctx->sched_outs.as<uint64_t>(static_cast<size_t>(n_real) * SP.nout);
+        SP.replay = ctx->sched_replay.as<uint64_t>(static_cast<size_t>(n_real) * 313);
+        build_jobs_kernel<<<n_real, 32, 0, st>>>(SP, d_jobs);
+        CCW_CUDA(cudaGetLastError());
+    }
     const size_t plane = static_cast<size_t>(wh) * ww;
     // the work grid exists only with min-cut (seams read the grid); otherwise
     // the source-block map is the realization until finalize
@@ -690,6 +709,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
+    const bool host_t = getenv("CCW_HOSTT") != nullptr;
+    auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(); };
+    const double t_ev0 = host_t ? host_ms() : 0.0;
     // finalize granularity: one thread per coarse block (B = 2, 4, 8) with the map
     const int fin_bt = d_src && (B == 2 || B == 4 || B == 8) ? B : 0;
     const size_t fin_cells = fin_bt ? static_cast<size_t>(B) * B : 1;
@@ -798,7 +820,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             Q.next_j0 = static_cast<int>(wave_off[g][std::min(w + 1, nkeys)]);
             for (size_t j0 = wave_off[g][w]; j0 < wave_off[g][w + 1]; j0 += maxj) {
                 const int nj = static_cast<int>(std::min(maxj, wave_off[g][w + 1] - j0));
-                const bool first_wave = flat[j0].shape == kNone;
+                const bool first_wave = w == 0;  // (wave 0 is every realization's first placement)
                 if (!first_wave) {
                     Q.tl = tl_next(w, g, 0);
                     if (!skip_prep && !fuse_prep) {  // (fused: prepared by the previous wave's select)
@@ -833,9 +855,14 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                             tm.ccf.push_back({a, b});
                         }
                         ccf_mma_flop += 2.0 * kpad * static_cast<double>(npos) * nj;
-                        for (int q = 0; q < nj; ++q) {
-                            const int sh = flat[j0 + q].shape;
-                            const double m = sh == kL ? mask_cells : static_cast<double>(Tc) * OVc;
+                        if (j0 == wave_off[g][w]) {  // the whole wave's mask cells, at its first launch
+                            double nL = 0, nS = 0;
+                            for (int r = 0; r < n_real; ++r)
+                                if (group_of(r) == g) {
+                                    nL += vhistL[vid[r]][w];
+                                    nS += vhist[vid[r]][w] - vhistL[vid[r]][w];
+                                }
+                            const double m = nL * mask_cells + nS * static_cast<double>(Tc) * OVc;
                             ccf_flop += 2.0 * ti->nscr * npos * m;
                             ccf_flop_ref += 2.0 * ti->nch * npos * m;
                         }
@@ -968,6 +995,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         ++launches;
         CCW_CUDA(cudaGetLastError());
     }
+    if (host_t)
+        fprintf(stderr, "host ms: seed %.3f sched %.3f prep %.3f ev0 %.3f launched %.3f\n", t_seed, t_sched, host_prep_ms,
+                t_ev0, host_ms());
     CCW_CUDA(cudaEventRecord(ev1, st));
     if (h_out && !stream_out)
         CCW_CUDA(cudaMemcpyAsync(h_dst, fin, out_bytes, cudaMemcpyDeviceToHost, st));
@@ -977,14 +1007,20 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
     std::vector<int32_t> chosen;
     std::vector<uint8_t> pasted;
+    std::vector<Job> flat_jobs;
+    int sched_err = 0;
+    CCW_CUDA(cudaMemcpyAsync(&sched_err, ctx->sched_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (traces) {
         chosen.resize(2 * total_jobs);
         CCW_CUDA(cudaMemcpyAsync(chosen.data(), d_chosen, sizeof(int32_t) * chosen.size(),
                                  cudaMemcpyDeviceToHost, st));
+        flat_jobs.resize(total_jobs);
+        CCW_CUDA(cudaMemcpyAsync(flat_jobs.data(), d_jobs, sizeof(Job) * total_jobs, cudaMemcpyDeviceToHost, st));
         pasted.resize(total_jobs * T * T);
         CCW_CUDA(cudaMemcpyAsync(pasted.data(), d_pasted, pasted.size(), cudaMemcpyDeviceToHost, st));
     }
     CCW_CUDA(cudaStreamSynchronize(st));
+    if (sched_err) throw Fail(CCW_ERR_GENERIC, "internal: device schedule disagrees with the host path draws");
     if (h_out && h_dst != h_out) {  // pinned staging -> the caller's pageable buffer, in parallel
         constexpr size_t kChunk = 4u << 20;
         const int nchunk = static_cast<int>((out_bytes + kChunk - 1) / kChunk);
@@ -1087,7 +1123,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (traces) {
         // flat is wave-ordered; rebuild each realization's raster-ordered trace
         for (size_t g = 0; g < total_jobs; ++g) {
-            const Job& jb = flat[g];
+            const Job& jb = flat_jobs[g];
             ccw_trace& tr = traces[jb.real];
             if (jb.place >= tr.capacity) continue;
             tr.top[jb.place] = jb.top;

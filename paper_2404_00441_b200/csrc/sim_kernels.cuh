@@ -283,6 +283,24 @@ __host__ __device__ inline BulkLayout bulk_layout(int nch, int Tc, int bx, int b
 // ---------------------------------------------------------- kernels -----
 
 // prep.cu
+// Device schedule (schedule.cu): one thread per realization replays its
+// mt19937_64 draws and writes its jobs at their wave-ordered slots.
+enum { kTopLeft = 0, kTopRight = 1, kBottomLeft = 2, kBottomRight = 3 };  // simulator.hpp:97-104
+struct SchedParams {
+    const uint64_t* seeds;
+    const int32_t* vid;        // host's path variant per realization (origin * 2 + column-major), checked
+    const int32_t* roff;       // [n_real][nkeys] first flat slot of each realization in each wave
+    const uint8_t* lattice_hd; // stride-lattice cells holding hard data (null: none)
+    int* err;                  // set when the device draws disagree with vid
+    uint64_t* outs;            // [n_real][nout] tempered generator outputs (scratch)
+    uint64_t* replay;          // [n_real][313] generator state for the sequential replay (scratch)
+    int n_real, nkeys, keymul, nout;
+    int nlr, nlc, stride, B, Kp;
+    uint64_t nfr, nfc;         // first placement: block-aligned TI origins per axis
+    uint64_t thr_fr, thr_fc, thr_k;  // bounded() rejection thresholds (2^64 - n) mod n
+};
+__global__ void build_jobs_kernel(SchedParams S, Job* __restrict__ jobs);
+
 __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0);
 __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0);
 const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
