@@ -435,6 +435,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         SP.thr_fr = (0 - SP.nfr) % SP.nfr;
         SP.thr_fc = (0 - SP.nfc) % SP.nfc;
         SP.thr_k = (0 - static_cast<uint64_t>(Kp)) % static_cast<uint64_t>(Kp);
+        if (getenv("CCW_SCHED_REPLAY")) SP.thr_k = ~0ull;  // tests: every pick "rejected" -> sequential replay
         SP.nout = 4 + nlr * nlc;  // the path, the first placement's two, one per other placement
         SP.outs = ctx->sched_outs.as<uint64_t>(static_cast<size_t>(n_real) * SP.nout);
         SP.replay = ctx->sched_replay.as<uint64_t>(static_cast<size_t>(n_real) * 313);

@@ -131,6 +131,27 @@ def test_large_tie_groups_bulk_path(oracle, k):
             assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+@pytest.mark.parametrize("hard", [False, True])
+def test_device_schedule_replay(oracle, hard, monkeypatch):
+    """The job schedule is drawn on the device (schedule.cu); a draw rejected
+    by bounded() sends the realization to a sequential replay.  Forcing that
+    path for every realization must give the same realizations."""
+    from paper_2404_00441_b200 import synth
+    monkeypatch.setenv("CCW_SCHED_REPLAY", "1")
+    ti_a = synth.channel_ti(160, 160, 41, scale=5.0)
+    ti = cs.CategoricalGrid(160, 160, 2, ti_a)
+    d = dict(sg_height=150, sg_width=170, template_size=24, overlap=8, dwt_level=2, candidates=3)
+    seeds = [cs.mix64(13, i) for i in range(3)]
+    hd = None
+    if hard:
+        ref = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=seeds[0])["realization"]
+        hd = [tuple(int(v) for v in row) for row in synth.hard_data_from(ref, 0.01, 3)]
+    res = cs.simulate_batch(ti, to_cfg(d, hd), seeds)
+    for s, r in zip(seeds, res):
+        o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), hd, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"])
+
+
 @pytest.mark.parametrize("help_min", [2, 8])
 def test_shared_rescoring(oracle, help_min, monkeypatch):
     """Equal-score groups of at least help_min windows are rescored in chunks
