@@ -106,6 +106,7 @@ struct SimParams {
     int* hpos;               // per job slot: SC_LC posted window positions
     double* hkeys;           //   ... their fp64 keys
     int help_min;            // smallest group that is shared
+    unsigned long long* jdump;  // debug (CCW_DBG_TAIL builds, CCW_TAIL_DUMP): per job t0, t1, t_end, n | g << 32
     int* bulk_sync;          // per job slot: [next position block, finished CTAs]
     double* bulk_keys;       // per job slot x CTA: that CTA's top-K keys
     int* bulk_idx;           //   ... and positions

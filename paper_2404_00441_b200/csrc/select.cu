@@ -15,6 +15,16 @@
 
 #include "sim_kernels.cuh"
 
+// Rarely executed select paths (fp64 rescoring, batches, shared rescoring,
+// the streaming scan).  Measured r1: out of line (-DCCW_COLD_CALLS) they cost
+// more in calls and generic shared-memory accesses than they save in
+// instruction fetch (config 1: 2.27 -> 2.48 ms), so they stay inlined.
+#ifdef CCW_COLD_CALLS
+#define CCW_COLD __noinline__
+#else
+#define CCW_COLD __forceinline__
+#endif
+
 namespace ccwgpu {
 
 // Exact K-th largest value (with multiplicity) of n int32 values, skipping
@@ -526,8 +536,7 @@ __device__ __forceinline__ int choose_pick(const SimParams& P, const Job& jb, co
 // Paste the chosen TI crop (simulator.hpp:483-493), record the trace and the
 // source-block map; JT threads cooperate (jt = 0..JT-1).
 template <int JT>
-__device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int gj, int fr, int fc,
-                                          int jt) {
+__device__ __forceinline__ void paste_copy(const SimParams& P, const Job& jb, int gj, int fr, int fc, int jt) {
     const int Tc = P.Tc;
     const int T = P.T;
     uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
@@ -536,8 +545,7 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
     uint8_t* g = P.work ? P.work + static_cast<size_t>(jb.real) * P.wh * P.ww : nullptr;
     const int wpr = T >> 2;  // 32-bit words per row
     const bool vec4 = ((fc | jb.left | P.ti_w | P.ww | T) & 3) == 0 && wpr <= JT && (JT % wpr) == 0;
-    if (!g && !trace) {
-    } else if (vec4) {
+    if (vec4) {
         // thread -> (row phase, word); every row it copies loaded in one round trip
         const int rpi = JT / wpr, rsub = jt / wpr, cw = jt - rsub * wpr;
         const uint8_t* srcp = P.ti + static_cast<size_t>(fr) * P.ti_w + fc + 4 * cw;
@@ -580,6 +588,15 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
             }
         }
     }
+}
+
+template <int JT>
+__device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int gj, int fr, int fc,
+                                          int jt) {
+    const int Tc = P.Tc;
+    // Without a work grid (source-block map mode) the realization is rebuilt
+    // from the map at finalize: only the map (and a requested trace) is written.
+    if (P.work || P.pasted) paste_copy<JT>(P, jb, gj, fr, fc, jt);
     if (P.src) {  // Tc x Tc map entries spread over every thread
         int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc +
                       static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
@@ -670,7 +687,7 @@ __device__ __forceinline__ int scan_finish(const SimParams& P, const ScanWarp& W
 // exact K-th score S_K and the candidate positions (>= S_K) into out[].
 // Returns the candidate count, or -1 when the list overflowed (then every
 // window >= mk_out must be rescored -- a superset, still exact).
-__device__ __forceinline__ int scan_job(const SimParams& P, int slot, ScanWarp& W, int* out, int& mk_out,
+__device__ CCW_COLD int scan_job(const SimParams& P, int slot, ScanWarp& W, int* out, int& mk_out,
                                         long long* sclk, int* out_s = nullptr) {
     const int lane = threadIdx.x & 31;
     const int K = P.K;
@@ -934,6 +951,9 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
                                               const int* cidx, int e0, int ng, int R) {
     const size_t plane = static_cast<size_t>(P.hc) * P.wc;
     for (int it = threadIdx.x; it < ng * ngrp; it += FS_T) {
+#ifdef CCW_DBG_TAIL
+        long long z0 = clock64();
+#endif
         const int e = it / ngrp, g = it - e * ngrp;
         const int4 G = S.grp[g];  // rows s0 .. s0 + nk - 1, columns t0 .. t0 + len - 1
         const int ch = G.x, k0 = G.y & 0xffff, s0 = G.y >> 16, nk = G.z & 255, t0 = G.w >> 8, len = G.w & 255;
@@ -962,8 +982,18 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
 #pragma unroll
         for (int c = 0; c < FS_G; ++c) {
             const int kq = (c * inv) >> 12, t = c - kq * len, kk = min(kq, nk - 1);
+#ifdef CCW_DBG_NOTI  // timing experiment only: no TI reads (wrong results)
+            pv[c] = __dmul_rn(tb[(b0 + kk * P.Tc + t + 7) & 255], tb[b0 + kk * P.Tc + t]);
+#else
             pv[c] = __dmul_rn(__ldg(a0 + kk * P.wc + t), tb[b0 + kk * P.Tc + t]);
+#endif
         }
+#ifdef CCW_DBG_TAIL
+        double chk = 0;
+        for (int c = 0; c < FS_G; ++c) chk += pv[c];
+        long long z1 = clock64();
+        if (chk == 12345.678) z1 = 0;  // (keeps the products computed before z1)
+#endif
         const int endm = G.z >> 8;  // cells that end a row
         double sum = 0.0;
         int kk = 0;
@@ -975,13 +1005,21 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
                 sum = 0.0;
             }
         }
+#ifdef CCW_DBG_TAIL
+        if (threadIdx.x == 0 && P.stats && ng < 8) {
+            const long long z2 = clock64();
+            atomicAdd(&P.stats[41], static_cast<unsigned long long>(z1 - z0));
+            atomicAdd(&P.stats[42], static_cast<unsigned long long>(z2 - z1));
+            atomicAdd(&P.stats[43], 1ull);
+        }
+#endif
     }
 }
 
 // fp64 keys of the windows cidx[0, cnt) (reference order, see fast_batch).
 // (tmg: the placement's template in global memory; staged in S.tm when it
 // fits, unless own_tm is false -- a chunk of another placement.)
-__device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, const double* tmg, int nr,
+__device__ CCW_COLD void rescore_keys(const SimParams& P, FastSmem& S, const double* tmg, int nr,
                                              int ngrp, const int* cidx, int cnt, double* keys,
                                              bool own_tm = true) {
     const int tid = threadIdx.x;
@@ -989,13 +1027,19 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
     const int EB = max(1, FS_RS / R);
     const bool tm_smem = own_tm && P.nch * P.Tc * P.Tc <= PK_TMC;
     if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+#ifdef CCW_DBG_TAIL
+    long long r0 = clock64();
+#endif
     for (int e0 = 0; e0 < cnt; e0 += EB) {
         const int ng = min(EB, cnt - e0);
-        if (tm_smem)
-            rescore_items(P, S, S.tm, nr, ngrp, cidx, e0, ng, R);
-        else
-            rescore_items(P, S, tmg, nr, ngrp, cidx, e0, ng, R);
+        rescore_items(P, S, tm_smem ? static_cast<const double*>(S.tm) : tmg, nr, ngrp, cidx, e0, ng, R);
         __syncthreads();
+#ifdef CCW_DBG_TAIL
+        if (tid == 0 && P.stats && cnt < 8) {
+            atomicAdd(&P.stats[40], static_cast<unsigned long long>(clock64() - r0));
+            r0 = clock64();
+        }
+#endif
         for (int e = tid; e < ng; e += FS_T) {
             // the fold is one sequential chain; its operands load 8 at a time
             const double* rp = S.rsum + e * R;
@@ -1016,7 +1060,7 @@ __device__ __forceinline__ void rescore_keys(const SimParams& P, FastSmem& S, co
 }
 
 // Rescore S.cidx[0, cnt) and merge with the running top-K (ntop entries).
-__device__ __forceinline__ void fast_batch(const SimParams& P, FastSmem& S, const double* tmg, int nr,
+__device__ CCW_COLD void fast_batch(const SimParams& P, FastSmem& S, const double* tmg, int nr,
                                            int ngrp, int cnt, int& ntop, int K) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     rescore_keys(P, S, tmg, nr, ngrp, S.cidx, cnt, S.key);
@@ -1134,7 +1178,7 @@ __device__ __forceinline__ void hb_drain(const SimParams& P, FastSmem& S, int sl
 }
 
 // Help with every group posted so far in this launch (every thread calls).
-__device__ __forceinline__ void hb_help(const SimParams& P, FastSmem& S) {
+__device__ CCW_COLD void hb_help(const SimParams& P, FastSmem& S) {
     const int tid = threadIdx.x;
     if (tid == 0) S.misc[1] = *reinterpret_cast<volatile int*>(&P.hb->nposts);
     __syncthreads();
@@ -1163,7 +1207,7 @@ __device__ __forceinline__ void hb_help(const SimParams& P, FastSmem& S) {
 // group, rescore its chunks until none is left (helpers claim the others),
 // wait for the helpers' chunks, gather the keys into S.key.  Returns false
 // (nothing posted) when the board is full.  Every thread calls.
-__device__ __forceinline__ bool hb_rescore(const SimParams& P, FastSmem& S, int slot, int g, int ngrp,
+__device__ CCW_COLD bool hb_rescore(const SimParams& P, FastSmem& S, int slot, int g, int ngrp,
                                            int var) {
     const int tid = threadIdx.x;
     const int cw = max(1, FS_T / ngrp);  // windows per chunk: one round of items
@@ -1216,7 +1260,7 @@ __device__ __forceinline__ bool hb_rescore(const SimParams& P, FastSmem& S, int 
 #define CCW_FS_MINB 4
 #endif
 __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
-    select_fast_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
+    select_fast_kernel(const __grid_constant__ SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
     __shared__ FastSmem S;
     const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     pdl_trigger();
@@ -1233,6 +1277,10 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     const Job jb = jobs[gj];
     const int Tc = P.Tc;
     long long fclk[5] = {clock64(), 0, 0, 0, 0};
+#ifdef CCW_DBG_TAIL
+    const unsigned long long dbg_t0 = gtimer();
+    int dbg_n = -2, dbg_g = 0;
+#endif
     int fr, fc;
     if (jb.shape == kNone) {
         fr = jb.fr;
@@ -1305,6 +1353,9 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         }
         fclk[1] = clock64();
         const int n = S.misc[0], nr = S.misc[2], ngrp = S.misc[3];
+#ifdef CCW_DBG_TAIL
+        dbg_n = n;
+#endif
         mk = S.misc[1];
         int ntop = 0;
         if (n < 0 && P.defer) {  // a large tie group: the bulk kernel rescores every window >= M_K
@@ -1359,12 +1410,25 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             }
             __syncthreads();
             const int g = S.misc[6], rk = S.misc[5];
+#ifdef CCW_DBG_TAIL
+            dbg_g = g;
+#endif
             if (g == 1) {
                 picked = S.tie[0];
             } else {
+#ifdef CCW_DBG_TAIL
+                const long long q0 = clock64();
+#endif
                 if (!(P.hb && g >= P.help_min &&
                       hb_rescore(P, S, slot, g, ngrp, mask_variant(jb.shape, jb.vleft, jb.htop))))
                     rescore_keys(P, S, tmg, nr, ngrp, S.tie, g, S.key);
+#ifdef CCW_DBG_TAIL
+                if (tid == 0 && P.stats && g < 8) {
+                    atomicAdd(&P.stats[37], 1ull);
+                    atomicAdd(&P.stats[38], static_cast<unsigned long long>(clock64() - q0));
+                    atomicAdd(&P.stats[39], static_cast<unsigned long long>(q0 - fclk[1]));
+                }
+#endif
                 if (wid == 0) {  // the rk-th best of the group by (fp64 desc, index asc)
                     for (int round = 0; round <= rk; ++round) {
                         double bk = 0.0;
@@ -1503,7 +1567,20 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
 #endif
         }
     }
+#ifdef CCW_DBG_TAIL
+    const unsigned long long dbg_t1 = gtimer();
+#endif
     if (P.hb) hb_help(P, S);  // rescore posted chunks of this launch's large groups
+#ifdef CCW_DBG_TAIL
+    if (P.jdump && tid == 0) {
+        unsigned long long* d = P.jdump + 4 * static_cast<size_t>(gj);
+        d[0] = dbg_t0;
+        d[1] = dbg_t1;
+        d[2] = gtimer();
+        d[3] = static_cast<unsigned long long>(static_cast<unsigned>(dbg_n)) |
+               (static_cast<unsigned long long>(dbg_g) << 32);
+    }
+#endif
     tl_mark(P.tl, 1);
 }
 

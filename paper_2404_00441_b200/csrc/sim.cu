@@ -403,6 +403,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         throw Fail(CCW_ERR_CONFIG, "configuration exceeds the exact fp32 screen range (mask*B^2 >= 2^24)");
 
     // ---- device buffers
+    EventTimer tm{ctx, {}, {}, 0};
+    cudaEvent_t ev_sched = tm.get();
+    CCW_CUDA(cudaEventRecord(ev_sched, st));
     Job* d_jobs = ctx->jobs.as<Job>(total_jobs);
     {
         const size_t nstage = static_cast<size_t>(n_real) * nkeys + n_real;
@@ -652,6 +655,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         }
     }
     std::vector<int> hb_par(G, 0);
+    const char* jdump_path = getenv("CCW_TAIL_DUMP");
+    unsigned long long* d_jdump = nullptr;
+    if (jdump_path) {
+        d_jdump = ctx->jdump.as<unsigned long long>(4 * total_jobs);
+        CCW_CUDA(cudaMemsetAsync(d_jdump, 0, sizeof(unsigned long long) * 4 * total_jobs, st));
+        for (int g = 0; g < G; ++g) GP[g].jdump = d_jdump;
+    }
     // per (group, parity) parameter sets
     std::vector<std::array<SimParams, 2>> GPP(G);
     const size_t tm_half = G * maxj * ti->nch * Tc * Tc, w8_half = G * maxj * kpad;
@@ -706,7 +716,6 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const bool skip_prep = skip.find("prep") != std::string::npos;
     const bool skip_ccf = skip.find("ccf") != std::string::npos;
     const bool skip_sel = skip.find("sel") != std::string::npos;
-    EventTimer tm{ctx, {}, {}, 0};
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
@@ -999,6 +1008,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (host_t)
         fprintf(stderr, "host ms: seed %.3f sched %.3f prep %.3f ev0 %.3f launched %.3f\n", t_seed, t_sched, host_prep_ms,
                 t_ev0, host_ms());
+    const double t_launched = host_t ? host_ms() : 0.0;
     CCW_CUDA(cudaEventRecord(ev1, st));
     if (h_out && !stream_out)
         CCW_CUDA(cudaMemcpyAsync(h_dst, fin, out_bytes, cudaMemcpyDeviceToHost, st));
@@ -1022,6 +1032,30 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     CCW_CUDA(cudaStreamSynchronize(st));
     if (sched_err) throw Fail(CCW_ERR_GENERIC, "internal: device schedule disagrees with the host path draws");
+    if (d_jdump) {  // debug: per-job select timing, with each job's group and wave
+        std::vector<unsigned long long> jd(4 * total_jobs);
+        CCW_CUDA(cudaMemcpy(jd.data(), d_jdump, sizeof(unsigned long long) * jd.size(), cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(jdump_path, "wb")) {
+            std::vector<int32_t> gw(2 * total_jobs);
+            for (int g = 0; g < G; ++g)
+                for (int w = 0; w < nkeys; ++w)
+                    for (size_t j = wave_off[g][w]; j < wave_off[g][w + 1]; ++j) {
+                        gw[2 * j] = g;
+                        gw[2 * j + 1] = w;
+                    }
+            const uint64_t tj = total_jobs;
+            fwrite(&tj, sizeof(tj), 1, f);
+            fwrite(jd.data(), sizeof(unsigned long long), jd.size(), f);
+            fwrite(gw.data(), sizeof(int32_t), gw.size(), f);
+            fclose(f);
+        }
+    }
+    if (host_t) {
+        float sms = 0;
+        cudaEventElapsedTime(&sms, ev_sched, ev0);
+        fprintf(stderr, "device schedule (uploads + build_jobs) %.3f ms; host waited %.3f ms after launching\n", sms,
+                host_ms() - t_launched);
+    }
     if (h_out && h_dst != h_out) {  // pinned staging -> the caller's pageable buffer, in parallel
         constexpr size_t kChunk = 4u << 20;
         const int nchunk = static_cast<int>((out_bytes + kChunk - 1) / kChunk);
@@ -1084,6 +1118,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (getenv("CCW_TAIL"))
         fprintf(stderr, "shared rescoring: posts %llu, chunks %llu (own %llu), owner help cycles %llu wait cycles %llu\n",
                 stats[32], stats[33], stats[34], stats[35], stats[36]);
+    if (getenv("CCW_TAIL"))
+        fprintf(stderr, "small groups (g < 8): %llu, rescore+select cycles avg %.0f (items %.0f), scan->group cycles avg %.0f\n",
+                stats[37], stats[37] ? double(stats[38]) / stats[37] : 0.0, stats[37] ? double(stats[40]) / stats[37] : 0.0,
+                stats[37] ? double(stats[39]) / stats[37] : 0.0);
+    if (getenv("CCW_TAIL"))
+        fprintf(stderr, "small-group item (thread 0): loads+products %.0f chain+stores %.0f cycles over %llu\n",
+                stats[43] ? double(stats[41]) / stats[43] : 0.0, stats[43] ? double(stats[42]) / stats[43] : 0.0, stats[43]);
     if (getenv("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
