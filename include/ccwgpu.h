@@ -118,6 +118,7 @@ typedef struct ccw_timing {
     double host_prep_ms;    /* host schedule build (plans + mt19937_64 draws) before launch */
     int64_t bulk_jobs;      /* placements whose tie group went to the bulk (CTA-wide) rescoring */
     int64_t shared_groups;  /* equal-score groups rescored in chunks shared across the launch's CTAs */
+    int64_t d2h_bytes;      /* realization bytes copied device -> host (streamed bands are bit-packed) */
 } ccw_timing;
 
 typedef struct ccw_ctx ccw_ctx;

@@ -44,7 +44,7 @@ class TimingC(C.Structure):
                 ("rescored", C.c_int64), ("screened_jobs", C.c_int64), ("ccf_variant", C.c_int64),
                 ("ccf_mma_flop", C.c_double), ("groups", C.c_int64),
                 ("list_overflows", C.c_int64), ("host_prep_ms", C.c_double),
-                ("bulk_jobs", C.c_int64), ("shared_groups", C.c_int64)]
+                ("bulk_jobs", C.c_int64), ("shared_groups", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 P = C.c_void_p

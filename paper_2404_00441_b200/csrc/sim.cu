@@ -33,6 +33,8 @@
 #include <mutex>
 #include <thread>
 
+#include <immintrin.h>
+
 #include "sim_kernels.cuh"
 
 namespace ccwgpu {
@@ -54,9 +56,9 @@ __device__ __forceinline__ void finalize_region(int r, int y0, int y1, int x0, i
                                                 const int32_t* __restrict__ src, int B, int J, int swc,
                                                 const uint8_t* __restrict__ ti, int ti_w, int wc,
                                                 const uint8_t* __restrict__ hd, int sg_h, int sg_w,
-                                                uint8_t* __restrict__ out, int& local) {
+                                                uint8_t* __restrict__ obase, int opitch, int& local) {
+    // cell (y, x) of the region goes to obase[(y - y0) * opitch + (x - x0)]
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-    uint8_t* o = out + static_cast<size_t>(r) * sg_h * sg_w;
     const uint8_t* hp = hd;
     if constexpr (BT == 0) {
         const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
@@ -80,7 +82,7 @@ __device__ __forceinline__ void finalize_region(int r, int y0, int y1, int x0, i
                     v = h;
                 }
             }
-            o[static_cast<size_t>(y) * sg_w + x] = v;
+            obase[static_cast<size_t>(y - y0) * opitch + (x - x0)] = v;
         }
     } else {
         const int32_t* sm = src + static_cast<size_t>(r) * (wh >> J) * swc;
@@ -113,7 +115,7 @@ __device__ __forceinline__ void finalize_region(int r, int y0, int y1, int x0, i
                             w = h;
                         }
                     }
-                    o[static_cast<size_t>(y) * sg_w + x] = w;
+                    obase[static_cast<size_t>(y - y0) * opitch + (x - x0)] = w;
                 }
             }
         }
@@ -129,8 +131,8 @@ __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww
     pdl_wait();
     const int r = blockIdx.y;
     int local = 0;
-    finalize_region<BT>(r, 0, sg_h, 0, sg_w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w, out,
-                        local);
+    finalize_region<BT>(r, 0, sg_h, 0, sg_w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w,
+                        out + static_cast<size_t>(r) * sg_h * sg_w, sg_w, local);
     if (hd) {
         for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
         if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
@@ -138,12 +140,16 @@ __global__ void finalize_kernel(const uint8_t* __restrict__ work, int wh, int ww
 }
 
 // Progressive finalize: band descriptors (realization, axis, lo, hi) in
-// output coordinates -- axis 0: rows [lo, hi) x every column; axis 1 / 2:
-// every row x columns [lo, hi).  A band is final once every placement
-// covering it is done (run_simulation's checkpoints), so it is rebuilt and
-// copied to the host while later waves still compute.
+// output coordinates -- axis 0: rows [lo, hi) x every column; axis 1: every
+// row x columns [lo, hi).  A band is final once every placement covering it
+// is done (run_simulation's checkpoints), so it is rebuilt and copied to the
+// host while later waves still compute.  With boff the band is written packed
+// at out + boff[band] (axis 0: its rows; axis 1: rows of hi - lo bytes), so a
+// checkpoint's bands leave in one contiguous copy; without, in place in the
+// row-major realizations.
 template <int BT>
-__global__ void finalize_band_kernel(const int4* __restrict__ bands, const uint8_t* __restrict__ work,
+__global__ void finalize_band_kernel(const int4* __restrict__ bands, const long long* __restrict__ boff,
+                                     const uint8_t* __restrict__ work,
                                      int wh, int ww, const int32_t* __restrict__ src, int B, int J,
                                      int swc, const uint8_t* __restrict__ ti, int ti_w, int wc,
                                      const uint8_t* __restrict__ hd, int sg_h, int sg_w,
@@ -153,15 +159,77 @@ __global__ void finalize_band_kernel(const int4* __restrict__ bands, const uint8
     tl_mark(tl, 0);
     const int4 bd = bands[blockIdx.y];
     const int r = bd.x;
+    const size_t rb = static_cast<size_t>(r) * sg_h * sg_w;
     int local = 0;
     if (bd.y == 0)
         finalize_region<BT>(r, bd.z, bd.w, 0, sg_w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w,
-                            out, local);
+                            boff ? out + boff[blockIdx.y] : out + rb + static_cast<size_t>(bd.z) * sg_w, sg_w,
+                            local);
     else
         finalize_region<BT>(r, 0, sg_h, bd.z, bd.w, work, wh, ww, src, B, J, swc, ti, ti_w, wc, hd, sg_h, sg_w,
-                            out, local);
+                            boff ? out + boff[blockIdx.y] : out + rb + bd.z, boff ? bd.w - bd.z : sg_w, local);
     if (hd) {
         for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
+    }
+    tl_mark(tl, 1);
+}
+
+// Streamed bands with few facies: the same cells as finalize_band_kernel
+// (map -> TI cell, hard-data overwrite, mismatch count), written BITS per
+// cell (1, 2 or 4; cell c of a byte in bits [c*BITS, (c+1)*BITS)), each
+// band row padded to whole bytes -- the device->host copy shrinks 8/BITS-fold
+// and the host unpacks while placing the bands.
+template <int BITS>
+__global__ void pack_band_kernel(const int4* __restrict__ bands, const long long* __restrict__ boff,
+                                 const uint8_t* __restrict__ work, int wh, int ww, const int32_t* __restrict__ src,
+                                 int B, int J, int swc, const uint8_t* __restrict__ ti, int ti_w, int wc,
+                                 const uint8_t* __restrict__ hd, int sg_h, int sg_w, uint8_t* __restrict__ out,
+                                 int* mism, unsigned long long* tl) {
+    constexpr int CPB = 8 / BITS;
+    tl_mark(tl, 2);
+    pdl_wait();
+    tl_mark(tl, 0);
+    const int4 bd = bands[blockIdx.y];
+    const int r = bd.x;
+    const int y0 = bd.y == 0 ? bd.z : 0, y1 = bd.y == 0 ? bd.w : sg_h;
+    const int x0 = bd.y == 0 ? 0 : bd.z, x1 = bd.y == 0 ? sg_w : bd.w;
+    const int rowb = (x1 - x0 + CPB - 1) / CPB;
+    const size_t nbytes = static_cast<size_t>(y1 - y0) * rowb;
+    uint8_t* o = out + boff[blockIdx.y];
+    const uint8_t* g = work ? work + static_cast<size_t>(r) * wh * ww : nullptr;
+    const int32_t* sm = src ? src + static_cast<size_t>(r) * (wh >> J) * swc : nullptr;
+    int local = 0;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nbytes;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int y = y0 + static_cast<int>(e / rowb);
+        const int xb = x0 + static_cast<int>(e % rowb) * CPB;
+        unsigned v = 0;
+#pragma unroll
+        for (int c = 0; c < CPB; ++c) {
+            const int x = xb + c;
+            if (x >= x1) break;
+            unsigned cell;
+            if (g) {
+                cell = g[static_cast<size_t>(y) * ww + x];
+            } else {
+                const int b = sm[static_cast<size_t>(y >> J) * swc + (x >> J)];
+                const int by = b / wc, bx = b - by * wc;
+                cell = ti[static_cast<size_t>((by << J) + (y & (B - 1))) * ti_w + (bx << J) + (x & (B - 1))];
+            }
+            if (hd) {
+                const uint8_t h = hd[static_cast<size_t>(y) * ww + x];
+                if (h != kNoDatum) {
+                    local += cell != h;
+                    cell = h;
+                }
+            }
+            v |= cell << (c * BITS);
+        }
+        o[e] = static_cast<uint8_t>(v);
+    }
+    if (hd) {
+        for (int q = 16; q > 0; q >>= 1) local += __shfl_xor_sync(0xffffffffu, local, q);
         if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
     }
     tl_mark(tl, 1);
@@ -216,6 +284,55 @@ int path_variant_of_seed(uint64_t seed) {
     const int origin = static_cast<int>(out(0) % 4);
     const int cm = static_cast<int>(out(1) % 2);
     return origin * 2 + cm;
+}
+
+// A packed band (pack_band_kernel's layout: rows of rowb bytes, CPB cells per
+// byte) -> rows x wdt cells at d with pitch ld.  BMI2 deposits 8 cells per
+// instruction (whole rows are written with non-temporal stores); without
+// BMI2 a byte -> cells table.
+template <int CPB>
+__attribute__((target("bmi2"))) void unpack_band_pdep(uint8_t* d, size_t ld, const uint8_t* sp, size_t rowb,
+                                                      size_t rows, size_t wdt, const uint64_t* lut) {
+    constexpr int kBits = 8 / CPB;  // bits per cell = input bytes per 8 cells
+    constexpr uint64_t kMask = kBits == 1 ? 0x0101010101010101ULL : kBits == 2 ? 0x0303030303030303ULL
+                                                                               : 0x0F0F0F0F0F0F0F0FULL;
+    for (size_t y = 0; y < rows; ++y, d += ld, sp += rowb) {
+        const uint8_t* s = sp;
+        size_t x = 0;
+        if (ld == wdt) {  // whole rows: contiguous, written around the caches
+            for (; x + 8 <= wdt; x += 8, s += kBits) {
+                uint32_t in = 0;
+                std::memcpy(&in, s, kBits);
+                _mm_stream_si64(reinterpret_cast<long long*>(d + x), static_cast<long long>(_pdep_u64(in, kMask)));
+            }
+        } else {  // (non-temporal stores to partial lines are ~10x slower than cached ones)
+            for (; x + 8 <= wdt; x += 8, s += kBits) {
+                uint32_t in = 0;
+                std::memcpy(&in, s, kBits);
+                const uint64_t cells = _pdep_u64(in, kMask);
+                std::memcpy(d + x, &cells, 8);
+            }
+        }
+        for (; x < wdt; ++x) {  // the row's last partial group of 8
+            const size_t c = x & 7;
+            d[x] = static_cast<uint8_t>((s[c / CPB] >> ((c % CPB) * kBits)) & ((1u << kBits) - 1));
+        }
+    }
+    _mm_sfence();
+}
+
+template <int CPB>
+void unpack_band(uint8_t* d, size_t ld, const uint8_t* sp, size_t rowb, size_t rows, size_t wdt,
+                 const uint64_t* lut) {
+    static const bool bmi2 = __builtin_cpu_supports("bmi2");
+    if (bmi2) return unpack_band_pdep<CPB>(d, ld, sp, rowb, rows, wdt, lut);
+    for (size_t y = 0; y < rows; ++y, d += ld, sp += rowb) {
+        const uint8_t* s = sp;
+        for (size_t x = 0; x < wdt; x += CPB, ++s) {
+            const uint64_t cells = lut[*s];
+            std::memcpy(d + x, &cells, std::min<size_t>(CPB, wdt - x));
+        }
+    }
 }
 
 // Mask tables of the fast select (MT_STRIDE int4 per mask variant): the mask
@@ -730,66 +847,111 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // checkpoint waves, overlapping the copy with the remaining waves
     uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
     const size_t out_bytes = static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real;
+    const bool stream_out = h_out && !d_out && !getenv("CCW_NO_STREAM_OUT");
     // device->host copies need page-locked memory to run asynchronously: a
-    // pageable destination gets a pinned staging buffer, copied out at the end
+    // pageable destination without streaming gets a pinned staging buffer,
+    // copied out at the end
     uint8_t* h_dst = h_out;
-    if (h_out) {
+    if (h_out && !stream_out) {
         cudaPointerAttributes pa{};
         const bool pinned = cudaPointerGetAttributes(&pa, h_out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
         if (!pinned) h_dst = static_cast<uint8_t*>(ctx->h_out_stage.get(out_bytes));
     }
-    const bool stream_out = h_out && !getenv("CCW_NO_STREAM_OUT");
-    std::vector<int4> bands;                                   // all checkpoints, in launch order
-    std::vector<std::vector<std::pair<int, std::pair<size_t, size_t>>>> band_at(G);  // per group: (wave, [off, off+n))
+    // Streaming: at each checkpoint wave, every band no remaining placement
+    // covers (rows of a row-major path, columns of a column-major one) is
+    // finalized while later waves compute.  Row bands into a page-locked
+    // caller buffer are contiguous there: finalized in place and copied
+    // directly.  Column bands (and every band of a pageable buffer) are
+    // finalized packed -- pack_bits per cell -- into a device staging area;
+    // a checkpoint's packed bands leave in one contiguous copy into pinned
+    // host staging and host threads unpack them into the caller's buffer.
+    // Checkpoints thicken towards the end, where the last rows / columns
+    // (direct row bands measured slower, r1: one copy per realization band
+    // lengthens the launch loop, and 8-bit rows quadruple the PCIe bytes)
+    const bool direct_rows = getenv("CCW_DIRECT_ROWS") != nullptr;
+    bool h_pinned = false;
     if (stream_out) {
-        int nck = 4;
+        cudaPointerAttributes pa{};
+        h_pinned = cudaPointerGetAttributes(&pa, h_out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+    }
+    struct Checkpoint {
+        int w;
+        size_t b0, bm, b1;  // bands [b0, bm) direct, [bm, b1) packed
+    };
+    std::vector<int4> bands;                                   // all checkpoints, in launch order
+    std::vector<long long> band_off;                           // packed bands: offset in the staging
+    std::vector<std::vector<Checkpoint>> band_at(G);           // per group, in wave order
+    uint8_t* h_stage = nullptr;
+    uint8_t* d_stage = nullptr;
+    // cells per streamed byte: the realizations' codes fit in 1, 2 or 4 bits for F <= 2, 4, 16
+    const int pack_bits = getenv("CCW_NO_PACK") ? 8 : ti->F <= 2 ? 1 : ti->F <= 4 ? 2 : ti->F <= 16 ? 4 : 8;
+    const int pack_cpb = 8 / pack_bits;
+    auto band_rowb = [&](const int4& bd) {  // packed bytes per band row
+        const int wdt = bd.y == 0 ? cfg.sg_width : bd.w - bd.z;
+        return static_cast<size_t>((wdt + pack_cpb - 1) / pack_cpb);
+    };
+    auto band_rows = [&](const int4& bd) { return static_cast<size_t>(bd.y == 0 ? bd.w - bd.z : cfg.sg_height); };
+    if (stream_out) {
+        std::vector<int> cks;
+        // evenly spaced (measured r1: 6 beats both fewer and more, and beats
+        // checkpoints crowded towards the end -- thin column bands cost the
+        // host more per byte than the later landing costs)
+        int nck = 6;
         if (const char* e = getenv("CCW_STREAM_BANDS")) nck = std::max(1, atoi(e));
-        const int delta = std::max(1, (max_key + 1 + nck - 1) / nck);
-        // column-major raster paths free whole columns: strided copies, slower
-        // per byte -- emitted whole at the last wave (CCW_STREAM_COLS=1: every
-        // other checkpoint; measured slower end to end, r1)
-        const char* ce = getenv("CCW_STREAM_COLS");
-        const bool stream_cols = ce && atoi(ce) != 0;  // measured slower (r1): off by default
+        for (int k = 1; k <= nck; ++k) cks.push_back((max_key * k) / nck);
         std::vector<int> done(n_real, 0);  // raster-outer extent already emitted
-        int ck = 0;
+        long long off = 0;
         for (int w = 0; w <= max_key; ++w) {
-            if ((w + 1) % delta != 0 && w != max_key) continue;
-            const bool col_ck = w == max_key || (stream_cols && (ck & 1));
-            ++ck;
+            if (w != max_key && std::find(cks.begin(), cks.end(), w) == cks.end()) continue;
             for (int g = 0; g < G; ++g) {
-                const size_t off = bands.size();
+                const size_t b0 = bands.size();
+                size_t bm = b0;
+                for (int pass = 0; pass < 2; ++pass)  // direct bands first, then packed ones
                 for (int r = 0; r < n_real; ++r) {
                     if (group_of(r) != g) continue;
                     const Plan& p = variants[vid[r]];
-                    // column bands: strided copies at col_ck checkpoints (CCW_STREAM_COLS,
-                    // axis 1), or finalized on the device at every checkpoint and the whole
-                    // realization copied at the last wave (axis 2: the final band, possibly
-                    // empty, carries the copy)
-                    if (p.column_major && stream_cols && !col_ck) continue;
-                    const int axis = !p.column_major ? 0 : (stream_cols ? 1 : 2);
+                    const int axis = p.column_major ? 1 : 0;
+                    const bool direct = axis == 0 && h_pinned && direct_rows;
+                    if (direct != (pass == 0)) continue;
                     const bool asc = axis == 0 ? (p.origin == CCW_TOP_LEFT || p.origin == CCW_TOP_RIGHT)
                                                : (p.origin == CCW_TOP_LEFT || p.origin == CCW_BOTTOM_LEFT);
                     const int extent = axis == 0 ? wh : ww, sg_ext = axis == 0 ? cfg.sg_height : cfg.sg_width;
                     int O = w >= p.n_inner - 1 ? (w - (p.n_inner - 1)) / keymul : -1;
                     O = std::min(O, p.n_outer - 1);
                     const int U = (w == max_key || O == p.n_outer - 1) ? extent : (O + 1) * stride;
-                    const bool carry = axis == 2 && w == max_key;
-                    if (U <= done[r] && !carry) continue;
+                    if (U <= done[r]) continue;
                     int lo = asc ? done[r] : extent - U, hi = asc ? U : extent - done[r];
                     done[r] = std::max(done[r], U);
                     lo = std::max(lo, 0);
                     hi = std::min(hi, sg_ext);
-                    if (hi > lo || carry) bands.push_back(make_int4(r, axis, lo, std::max(lo, hi)));
+                    if (hi <= lo) continue;
+                    bands.push_back(make_int4(r, axis, lo, hi));
+                    if (direct) {
+                        band_off.push_back(-1);
+                        bm = bands.size();
+                    } else {
+                        band_off.push_back(off);
+                        off += static_cast<long long>(band_rows(bands.back()) * band_rowb(bands.back()));
+                    }
                 }
-                if (bands.size() > off) band_at[g].push_back({w, {off, bands.size()}});
+                if (bands.size() > b0) band_at[g].push_back({w, b0, bm, bands.size()});
             }
         }
     }
+    if (stream_out) {
+        h_stage = static_cast<uint8_t*>(ctx->h_out_stage.get(out_bytes));
+        d_stage = ctx->band_stage.as<uint8_t>(out_bytes);
+    }
     int4* d_bands = nullptr;
+    long long* d_boff = nullptr;
     if (!bands.empty()) {
         d_bands = reinterpret_cast<int4*>(ctx->ops_b.get(sizeof(int4) * bands.size()));
         CCW_CUDA(cudaMemcpyAsync(d_bands, bands.data(), sizeof(int4) * bands.size(), cudaMemcpyHostToDevice, st));
+        d_boff = ctx->band_off.as<long long>(band_off.size());
+        CCW_CUDA(cudaMemcpyAsync(d_boff, band_off.data(), sizeof(long long) * band_off.size(),
+                                 cudaMemcpyHostToDevice, st));
     }
     std::vector<size_t> band_next(G, 0);
     struct CopyMark {
@@ -797,6 +959,97 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         cudaEvent_t ev;
     };
     std::vector<CopyMark> copy_marks;
+    struct Arrival {  // one checkpoint's packed bands of one group, landed in h_stage once ev completes
+        size_t b0, b1;
+        cudaEvent_t ev;
+    };
+    auto band_bytes = [&](size_t q) { return band_rows(bands[q]) * band_rowb(bands[q]); };
+    // every packed checkpoint, in landing (band) order, with its event made
+    // up front: a placer thread consumes them while the waves are launched
+    std::vector<Arrival> arrivals;
+    for (int g = 0; g < G; ++g)
+        for (const Checkpoint& ck : band_at[g])
+            if (ck.b1 > ck.bm) arrivals.push_back({ck.bm, ck.b1, tm.get()});
+    std::sort(arrivals.begin(), arrivals.end(), [](const Arrival& a, const Arrival& b) { return a.b0 < b.b0; });
+    std::unique_ptr<std::atomic<int>[]> arr_ready(new std::atomic<int>[arrivals.size() + 1]);
+    for (size_t k = 0; k < arrivals.size(); ++k) arr_ready[k].store(0);
+    auto arrival_index = [&](size_t b0) {
+        return static_cast<size_t>(std::lower_bound(arrivals.begin(), arrivals.end(), b0,
+                                                    [](const Arrival& a, size_t v) { return a.b0 < v; }) -
+                                   arrivals.begin());
+    };
+    uint64_t unpack_lut[256];  // byte -> its pack_cpb cells, one per byte (little endian)
+    for (int b = 0; b < 256; ++b) {
+        uint64_t v = 0;
+        for (int c = 0; c < pack_cpb && pack_bits < 8; ++c)
+            v |= static_cast<uint64_t>((b >> (c * pack_bits)) & ((1 << pack_bits) - 1)) << (8 * c);
+        unpack_lut[b] = v;
+    }
+    std::vector<size_t> packed_q;  // packed bands in landing order, and their arrivals
+    std::vector<int> packed_arrival;
+    for (size_t k = 0; k < arrivals.size(); ++k)
+        for (size_t q = arrivals[k].b0; q < arrivals[k].b1; ++q) {
+            packed_q.push_back(q);
+            packed_arrival.push_back(static_cast<int>(k));
+        }
+    std::atomic<long long> t_wait{0}, t_unpack{0};
+    // Placement: host workers take the packed bands in landing order; each
+    // waits (polling, so the launching thread keeps its core) until the copy
+    // carrying its band has landed, then unpacks it into the caller's buffer.
+    auto place_band = [&](int qi) {
+        const size_t q = packed_q[static_cast<size_t>(qi)];
+        const auto tw0 = std::chrono::steady_clock::now();
+        const size_t k = static_cast<size_t>(packed_arrival[static_cast<size_t>(qi)]);
+        for (int spin = 0;; ++spin) {  // recorded, then landed: short pause-spins, then naps
+            if (arr_ready[k].load(std::memory_order_acquire)) {
+                const cudaError_t e = cudaEventQuery(arrivals[k].ev);
+                if (e == cudaSuccess) break;
+                if (e != cudaErrorNotReady) CCW_CUDA(e);
+            }
+            if (spin < 64)
+                for (int i = 0; i < 64; ++i) _mm_pause();
+            else
+                std::this_thread::sleep_for(std::chrono::microseconds(10));
+        }
+        const auto tw1 = std::chrono::steady_clock::now();
+        t_wait += std::chrono::duration_cast<std::chrono::nanoseconds>(tw1 - tw0).count();
+        const int4 bd = bands[q];
+        const uint8_t* srcp = h_stage + band_off[q];
+        uint8_t* dst = h_out + static_cast<size_t>(bd.x) * cfg.sg_height * cfg.sg_width;
+        const int y0 = bd.y == 0 ? bd.z : 0, x0 = bd.y == 0 ? 0 : bd.z;
+        const size_t wdt = static_cast<size_t>(bd.y == 0 ? cfg.sg_width : bd.w - bd.z);
+        const size_t rowb = band_rowb(bd), rows = band_rows(bd);
+        uint8_t* d = dst + static_cast<size_t>(y0) * cfg.sg_width + x0;
+        if (pack_bits == 8)
+            for (size_t y = 0; y < rows; ++y) std::memcpy(d + y * cfg.sg_width, srcp + y * rowb, wdt);
+        else if (pack_cpb == 8) unpack_band<8>(d, cfg.sg_width, srcp, rowb, rows, wdt, unpack_lut);
+        else if (pack_cpb == 4) unpack_band<4>(d, cfg.sg_width, srcp, rowb, rows, wdt, unpack_lut);
+        else unpack_band<2>(d, cfg.sg_width, srcp, rowb, rows, wdt, unpack_lut);
+        t_unpack += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - tw1).count();
+    };
+    int place_threads = std::max(1, static_cast<int>(std::thread::hardware_concurrency()) - 2);
+    if (const char* e = getenv("CCW_PLACE_THREADS")) place_threads = std::max(1, atoi(e));
+    std::exception_ptr place_err;
+    std::thread placer;
+    if (!packed_q.empty())
+        placer = std::thread([&] {
+            try {
+                ctx->pool.run(static_cast<int>(packed_q.size()), place_band, place_threads);
+            } catch (...) {
+                place_err = std::current_exception();
+            }
+        });
+    struct PlacerJoin {  // the placer never outlives this frame, even on an exception
+        std::thread& t;
+        std::atomic<int>* ready;
+        size_t n;
+        ~PlacerJoin() {
+            if (t.joinable()) {
+                for (size_t k = 0; k < n; ++k) ready[k].store(1);
+                t.join();
+            }
+        }
+    } placer_join{placer, arr_ready.get(), arrivals.size()};
 
     // debug timeline: [resident, past-wait, end] per launch
     const bool want_tl = getenv("CCW_TIMELINE") != nullptr;
@@ -914,61 +1167,68 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     tm.sel.push_back({a, b});
                 }
             }
-            if (band_next[g] < band_at[g].size() && band_at[g][band_next[g]].first == w) {
-                const auto rng = band_at[g][band_next[g]++].second;
-                const int nb = static_cast<int>(rng.second - rng.first);
-                size_t most = 1;  // cells of the largest band: enough CTAs to cover it
-                for (size_t q = rng.first; q < rng.second; ++q)
-                    most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
-                                              (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
-                const int bxb = static_cast<int>(std::min<size_t>((most / fin_cells + 255) / 256 + 1, 1024));
+            if (band_next[g] < band_at[g].size() && band_at[g][band_next[g]].w == w) {
+                const Checkpoint ck = band_at[g][band_next[g]++];
                 // final bands are never written again: rebuild and copy them on the copy
                 // stream, off the group's critical path
                 cudaEvent_t be = tm.get();
                 CCW_CUDA(cudaEventRecord(be, gs));
                 CCW_CUDA(cudaStreamWaitEvent(ctx->copy_streams[g], be, 0));
-                auto band = [&](auto kern) {
-                    launch_pdl(kern, dim3(bxb, nb), dim3(256), 0, ctx->copy_streams[g],
-                               static_cast<const int4*>(d_bands + rng.first), static_cast<const uint8_t*>(d_work),
-                               wh, ww, static_cast<const int32_t*>(d_src), B, J, swc,
-                               static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
-                               static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width, fin, d_mism,
-                               tl_next(w, g, 4));
+                auto launch_bands = [&](size_t q0, size_t q1, bool packed) {
+                    size_t most = 1;  // cells of the largest band: enough CTAs to cover it
+                    for (size_t q = q0; q < q1; ++q)
+                        most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
+                                                  (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
+                    const size_t per_thread = packed && pack_bits < 8 ? static_cast<size_t>(pack_cpb) : fin_cells;
+                    const int bxb = static_cast<int>(std::min<size_t>((most / per_thread + 255) / 256 + 1, 1024));
+                    auto band = [&](auto kern) {
+                        launch_pdl(kern, dim3(bxb, static_cast<unsigned>(q1 - q0)), dim3(256), 0, ctx->copy_streams[g],
+                                   static_cast<const int4*>(d_bands + q0),
+                                   static_cast<const long long*>(packed ? d_boff + q0 : nullptr),
+                                   static_cast<const uint8_t*>(d_work), wh, ww, static_cast<const int32_t*>(d_src), B,
+                                   J, swc, static_cast<const uint8_t*>(ti->d_codes), ti->w, ti->wc,
+                                   static_cast<const uint8_t*>(d_hd), cfg.sg_height, cfg.sg_width,
+                                   packed ? d_stage : fin, d_mism, tl_next(w, g, 4));
+                    };
+                    if (packed && pack_bits == 1) band(pack_band_kernel<1>);
+                    else if (packed && pack_bits == 2) band(pack_band_kernel<2>);
+                    else if (packed && pack_bits == 4) band(pack_band_kernel<4>);
+                    else if (fin_bt == 2) band(finalize_band_kernel<2>);
+                    else if (fin_bt == 4) band(finalize_band_kernel<4>);
+                    else if (fin_bt == 8) band(finalize_band_kernel<8>);
+                    else band(finalize_band_kernel<0>);
+                    ++launches;
                 };
-                if (fin_bt == 2) band(finalize_band_kernel<2>);
-                else if (fin_bt == 4) band(finalize_band_kernel<4>);
-                else if (fin_bt == 8) band(finalize_band_kernel<8>);
-                else band(finalize_band_kernel<0>);
-                ++launches;
-                // copies straight into the caller's buffer; adjacent ranges merged
-                const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
-                size_t o0 = 0, o1 = 0;
-                auto flush = [&] {
-                    if (o1 > o0)
-                        CCW_CUDA(cudaMemcpyAsync(h_dst + o0, fin + o0, o1 - o0, cudaMemcpyDeviceToHost,
-                                                 ctx->copy_streams[g]));
-                    o0 = o1 = 0;
-                };
-                for (size_t q = rng.first; q < rng.second; ++q) {
-                    const int4 bd = bands[q];
-                    const size_t base = static_cast<size_t>(bd.x) * n;
-                    if (bd.y == 2 && w != max_key) continue;  // device-only column band
-                    const bool full = (bd.y == 0 && bd.z == 0 && bd.w == cfg.sg_height) ||
-                                      (bd.y == 1 && bd.z == 0 && bd.w == cfg.sg_width) || bd.y == 2;
-                    if (bd.y == 1 && !full) {  // a column band: one strided copy
-                        flush();
-                        CCW_CUDA(cudaMemcpy2DAsync(h_dst + base + bd.z, cfg.sg_width, fin + base + bd.z,
-                                                   cfg.sg_width, bd.w - bd.z, cfg.sg_height,
-                                                   cudaMemcpyDeviceToHost, ctx->copy_streams[g]));
-                        continue;
+                if (ck.bm > ck.b0) {  // row bands, finalized in place and copied straight to the caller
+                    launch_bands(ck.b0, ck.bm, false);
+                    const size_t n = static_cast<size_t>(cfg.sg_height) * cfg.sg_width;
+                    size_t o0 = 0, o1 = 0;
+                    auto flush = [&] {
+                        if (o1 > o0)
+                            CCW_CUDA(cudaMemcpyAsync(h_out + o0, fin + o0, o1 - o0, cudaMemcpyDeviceToHost,
+                                                     ctx->copy_streams[g]));
+                        o0 = o1 = 0;
+                    };
+                    for (size_t q = ck.b0; q < ck.bm; ++q) {
+                        const int4 bd = bands[q];
+                        const size_t a0 = static_cast<size_t>(bd.x) * n + static_cast<size_t>(bd.z) * cfg.sg_width;
+                        const size_t a1 = static_cast<size_t>(bd.x) * n + static_cast<size_t>(bd.w) * cfg.sg_width;
+                        if (a0 != o1) flush();
+                        if (o1 == 0) o0 = a0;
+                        o1 = a1;
                     }
-                    const size_t a0 = full ? base : base + static_cast<size_t>(bd.z) * cfg.sg_width;
-                    const size_t a1 = full ? base + n : base + static_cast<size_t>(bd.w) * cfg.sg_width;
-                    if (a0 != o1) flush();
-                    if (o1 == 0) o0 = a0;
-                    o1 = a1;
+                    flush();
                 }
-                flush();
+                if (ck.b1 > ck.bm) {  // packed bands: one contiguous copy into the host staging
+                    launch_bands(ck.bm, ck.b1, true);
+                    const size_t p0 = static_cast<size_t>(band_off[ck.bm]);
+                    const size_t p1 = static_cast<size_t>(band_off[ck.b1 - 1]) + band_bytes(ck.b1 - 1);
+                    CCW_CUDA(cudaMemcpyAsync(h_stage + p0, d_stage + p0, p1 - p0, cudaMemcpyDeviceToHost,
+                                             ctx->copy_streams[g]));
+                    const size_t k = arrival_index(ck.bm);
+                    CCW_CUDA(cudaEventRecord(arrivals[k].ev, ctx->copy_streams[g]));
+                    arr_ready[k].store(1, std::memory_order_release);
+                }
                 if (want_tl) {  // debug: copy-stream progress per checkpoint
                     cudaEvent_t ce = tm.get();
                     CCW_CUDA(cudaEventRecord(ce, ctx->copy_streams[g]));
@@ -1010,6 +1270,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 t_ev0, host_ms());
     const double t_launched = host_t ? host_ms() : 0.0;
     CCW_CUDA(cudaEventRecord(ev1, st));
+    if (placer.joinable()) placer.join();
+    if (place_err) std::rethrow_exception(place_err);
+    if (host_t)
+        fprintf(stderr, "host ms: bands placed %.3f (thread-ms waiting %.3f, unpacking %.3f, bands %zu)\n", host_ms(),
+                t_wait * 1e-6, t_unpack * 1e-6, packed_q.size());
     if (h_out && !stream_out)
         CCW_CUDA(cudaMemcpyAsync(h_dst, fin, out_bytes, cudaMemcpyDeviceToHost, st));
     unsigned long long stats[kNumStats] = {0};
@@ -1081,6 +1346,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.host_prep_ms = host_prep_ms;
     ctx->timing.jobs = static_cast<int64_t>(total_jobs);
     ctx->timing.rescored = static_cast<int64_t>(stats[0]);
+    {
+        size_t d2h = h_out && !stream_out ? out_bytes : 0;
+        for (size_t q = 0; q < bands.size(); ++q)
+            d2h += band_off[q] < 0 ? band_rows(bands[q]) * cfg.sg_width : band_bytes(q);
+        ctx->timing.d2h_bytes = static_cast<int64_t>(d2h);
+    }
     for (const CopyMark& cm : copy_marks) {
         float ms = 0;
         cudaEventElapsedTime(&ms, ev0, cm.ev);

@@ -131,6 +131,52 @@ def test_large_tie_groups_bulk_path(oracle, k):
             assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
 
 
+@pytest.mark.parametrize("nf", [2, 3, 5, 17])
+def test_streamed_output_matches_device(nf):
+    """Host results are streamed as bit-packed bands (1/2/4 bits per cell for
+    F <= 2/4/16, bytes above) and unpacked by host threads (sim.cu
+    pack_band_kernel, unpack_band): into pageable and page-locked buffers, with
+    hard data (mismatch counts), they must equal the device-resident results."""
+    import ctypes as C
+    import torch
+    from paper_2404_00441_b200 import _abi, synth
+    rng = np.random.default_rng(100 + nf)
+    ti_a = (synth.channel_ti(152, 172, 5 + nf, scale=4.0).astype(np.int64) * 7 +
+            rng.integers(0, 3, (152, 172))) % nf
+    ti_a = ti_a.astype(np.uint8)
+    ti = cs.CategoricalGrid(152, 172, nf, ti_a)
+    d = dict(sg_height=230, sg_width=190, template_size=24, overlap=8, dwt_level=2, candidates=4)
+    seeds = [cs.mix64(77, i) for i in range(12)]
+    hd = [(int(r), int(c), int(rng.integers(0, nf))) for r, c in zip(rng.integers(0, 230, 40), rng.integers(0, 190, 40))]
+    hd = list({(r, c): (r, c, f) for r, c, f in hd}.values())
+    cfg = to_cfg(d, hd)
+    host = cs.simulate_batch(ti, cfg, seeds)                      # pageable numpy buffer
+    dev = cs.default_device()
+    lib = _abi.lib()
+    h = cs._ti_handle(ti, cfg, None)
+    c = cfg.to_c()
+    n = len(seeds)
+    sa = np.array(seeds, np.uint64)
+    hda = np.array(hd, np.int32).reshape(-1, 3)
+    diags = (_abi.DiagC * n)()
+    d_out = torch.empty(n * 230 * 190, dtype=torch.uint8, device="cuda")
+    dev.check(lib.ccw_simulate_device(dev.handle, h.handle, C.byref(c), sa.ctypes.data_as(_abi.U64P), n,
+                                      hda.ctypes.data_as(_abi.I32P), hda.shape[0], C.c_void_p(d_out.data_ptr()), diags))
+    ref = d_out.cpu().numpy().reshape(n, 230, 190)
+    ref_mism = [diags[r].pre_overwrite_mismatches for r in range(n)]
+    pinned = torch.empty(n * 230 * 190, dtype=torch.uint8).pin_memory()
+    dev.check(lib.ccw_simulate(dev.handle, h.handle, C.byref(c), sa.ctypes.data_as(_abi.U64P), n,
+                               hda.ctypes.data_as(_abi.I32P), hda.shape[0],
+                               C.cast(C.c_void_p(pinned.data_ptr()), _abi.U8P), diags, None))
+    assert dev.last_timing()["d2h_bytes"] < n * 230 * 190 or nf > 16
+    got = pinned.numpy().reshape(n, 230, 190)
+    for r in range(n):
+        assert np.array_equal(host[r].realization.cells, ref[r]), r
+        assert np.array_equal(got[r], ref[r]), r
+        assert host[r].diagnostics.pre_overwrite_mismatches == ref_mism[r]
+        assert diags[r].pre_overwrite_mismatches == ref_mism[r]
+
+
 @pytest.mark.parametrize("hard", [False, True])
 def test_device_schedule_replay(oracle, hard, monkeypatch):
     """The job schedule is drawn on the device (schedule.cu); a draw rejected
