@@ -2,6 +2,7 @@
 """Benchmark: simulated cells/s on BASELINE config 1 (the headline workload).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload config1|single] [--virtual-shards V]
 
 Workload (BASELINE.json configs[1]): TI 500x500 3-facies (channels + levee
 lenses, synth.config1_ti), SG 1000x1000, T=64, OV=16, J=2, K=5 top-k random
@@ -330,6 +331,126 @@ def run_ours(args):
     return 0
 
 
+SINGLE_WORKLOAD = ("config2-single: TI 2000x2000 binary channels, SG 4000x4000, T96 OV24 J3 K1, "
+                   "1% hard data, ONE realization, TI window positions sharded over the ranks "
+                   "(per-wave ncclAllGather of the shards' top-K lists)")
+
+
+def run_single(args):
+    """--workload single: one config-2 realization whose every placement's
+    TI window positions are split across the N ranks; strong
+    scaling.  --virtual-shards V splits each rank's range V ways more."""
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    from paper_2404_00441_b200 import _abi, ccwsim as cs, synth
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _abi.lib()
+    dev = cs.Device(local)
+    uid = None
+    if world > 1 or args.nccl:
+        box = [cs.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            torch.distributed.broadcast_object_list(box, src=0)
+        uid = box[0]
+    dev.set_position_shards(world, rank, uid, args.virtual_shards)
+    stream = torch.cuda.ExternalStream(dev.stream_ptr, device=torch.device("cuda", local))
+    ti_a = synth.config2_ti()
+    hd = synth.config2_hard_data(ti_a)
+    grid = cs.CategoricalGrid(2000, 2000, 2, ti_a)
+    cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1, master_seed=MASTER)
+    tih = cs.TrainingImage(grid, cfg.dwt_level, "indicator", dev)
+    c = cfg.to_c()
+    hd_a = np.ascontiguousarray(hd, np.int32)
+    seeds = np.array([cs.mix64(MASTER, 1)], np.uint64)
+    sg = cfg.sg_height * cfg.sg_width
+    d_out = torch.empty(sg, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    diags = (_abi.DiagC * 1)()
+
+    def step_device():
+        dev.check(lib.ccw_simulate_device(dev.handle, tih.handle, C.byref(c),
+                                          seeds.ctypes.data_as(_abi.U64P), 1,
+                                          hd_a.ctypes.data_as(_abi.I32P), hd_a.shape[0],
+                                          C.c_void_p(d_out.data_ptr()), diags))
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            evs[k][0].record(stream)
+        step_device()
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    timing = dev.last_timing()
+    value = sg * args.steps / (total_ms * 1e-3)
+    # end to end: TI from host bytes, hard data and result through host memory
+    h_out = torch.empty(sg, dtype=torch.uint8).pin_memory()
+    ti_host = np.ascontiguousarray(ti_a)
+
+    def step_e2e():
+        h = C.c_void_p()
+        dev.check(lib.ccw_ti_create(dev.handle, ti_host.ctypes.data_as(_abi.U8P), 2000, 2000, 2,
+                                    cfg.dwt_level, 0, C.byref(h)))
+        dev.check(lib.ccw_simulate(dev.handle, h, C.byref(c), seeds.ctypes.data_as(_abi.U64P), 1,
+                                   hd_a.ctypes.data_as(_abi.I32P), hd_a.shape[0],
+                                   C.cast(C.c_void_p(h_out.data_ptr()), _abi.U8P), diags, None))
+        lib.ccw_ti_destroy(h)
+
+    step_e2e()
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_e2e()
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    d2h = int(dev.last_timing()["d2h_bytes"])
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32(exact-int)+f64",
+                "data": "synthetic",
+                "config": {"workload": SINGLE_WORKLOAD, "position_shards": world * args.virtual_shards,
+                           "exchange": "ncclAllGather" if uid is not None else
+                                       ("device memory (virtual shards)" if args.virtual_shards > 1 else "none"),
+                           "virtual_shards_per_rank": args.virtual_shards,
+                           "l2": "flushed before each timed step (256 MiB write, outside events)",
+                           "timing": "per-step CUDA events on the library stream, max over ranks"},
+                "e2e": {"value": sg * args.steps / e2e_s, "unit": UNIT,
+                        "h2d_bytes_per_step": int(ti_host.nbytes + hd_a.nbytes + seeds.nbytes),
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(timing["launches"]) * args.steps, "clocks": clocks}
+        print(json.dumps(line))
+    dev.set_position_shards(1, 0, None, 1)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,7 +458,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--workload", default="config1", choices=["config1", "single"],
+                    help="config1 (headline) or single: one config-2 realization, positions sharded")
+    ap.add_argument("--virtual-shards", type=int, default=1)
+    ap.add_argument("--nccl", action="store_true",
+                    help="single: exchange through an NCCL communicator even on one rank")
     args = ap.parse_args()
+    if args.impl == "ours" and args.workload == "single":
+        return run_single(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -143,6 +143,30 @@ CCW_API ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops);
  * (kind::i8, M=128, N=256, cta_group::1), measured with an in-library probe. */
 CCW_API ccw_status ccw_measure_i8_peak(ccw_ctx* ctx, double* tops);
 
+/* ------------------------------------------- position sharding --------- */
+/* Candidate-position sharding of one simulation across ranks.
+ * The reference scores every TI window of a placement on one thread
+ * (ccw_score_map_channels, matcher.hpp:147-173, then top_k :177-204).  With
+ * shards, the window positions 0..npos-1 (row-major, as the reference scans
+ * them) are cut into S = nranks * virtual_shards contiguous ranges; shard s
+ * screens and ranks only its range and produces its local top-K under the
+ * reference ranking (fp64 score desc, earlier position on ties).  Per
+ * placement wave the local lists are all-gathered (ncclAllGather over
+ * NVLink/NVSwitch when nranks > 1) and every rank merges the S lists into
+ * the global top-K -- the reference's list, because every global top-K
+ * window is in its own shard's top-K -- then picks and pastes identically.
+ * Every rank must make the same ccw_simulate* calls with the same arguments;
+ * every rank returns the full (identical) realizations.
+ *
+ * nccl_id: the 128-byte ncclUniqueId from ccw_nccl_unique_id on one rank,
+ * broadcast by the caller; may be NULL when nranks == 1.  virtual_shards >= 1
+ * runs that many shards inside this rank, exchanged through device memory
+ * (validation on one GPU).  nranks == 1 && virtual_shards == 1 switches
+ * sharding off.  NCCL is loaded at run time (libnccl.so.2) on first use. */
+CCW_API ccw_status ccw_nccl_unique_id(uint8_t* id128);
+CCW_API ccw_status ccw_ctx_set_position_shards(ccw_ctx* ctx, int nranks, int rank,
+                                               const uint8_t* nccl_id, int virtual_shards);
+
 /* ---------------------------------------------------------- rng -------- */
 /* rng.hpp:11-16 */
 CCW_API uint64_t ccw_mix64(uint64_t seed, uint64_t index);

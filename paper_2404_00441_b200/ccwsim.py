@@ -288,6 +288,17 @@ class SimConfig:
             _raise(rc, buf.value.decode())
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (ccw_nccl_unique_id), to broadcast to the
+    ranks of a position-sharded simulation."""
+    L = _abi.lib()
+    buf = (C.c_uint8 * 128)()
+    rc = L.ccw_nccl_unique_id(C.cast(buf, _abi.U8P))
+    if rc:
+        _raise(rc, L.ccw_last_error(None).decode())
+    return bytes(buf)
+
+
 # ----------------------------------------------------------------- device --
 
 class Device:
@@ -323,6 +334,21 @@ class Device:
     def set_ccf_variant(self, variant: int) -> None:
         """0 auto (tcgen05 int8 when it is exact), 1 fp32 CUDA-core, 2 tcgen05 int8."""
         self.check(self._lib.ccw_ctx_set_ccf_variant(self.handle, int(variant)))
+
+    def set_position_shards(self, nranks: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
+                            virtual_shards: int = 1) -> None:
+        """Candidate-position sharding (include/ccwgpu.h ccw_ctx_set_position_shards):
+        this rank screens and ranks its share of the TI window positions and the
+        shards' top-K lists are all-gathered (NCCL when nccl_id is given) and
+        merged per placement.  nranks = virtual_shards = 1 switches it off."""
+        idp = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("an NCCL unique id has 128 bytes")
+            buf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+            idp = C.cast(buf, _abi.U8P)
+        self.check(self._lib.ccw_ctx_set_position_shards(self.handle, int(nranks), int(rank), idp,
+                                                         int(virtual_shards)))
 
     def measure_fp32_peak(self) -> float:
         """FP32 FFMA peak of this GPU in TFLOP/s (in-library microbenchmark)."""

@@ -268,6 +268,8 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
                               &ctx->ops_b, &ctx->ops_c, &ctx->ops_d, &ctx->ops_e})
         b->release();
     ctx->h_stage.release();
+    ctx->xrec.release();
+    ccwgpu::nccl_comm_destroy(ctx->nccl_comm);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
     for (cudaStream_t s : ctx->copy_streams) cudaStreamDestroy(s);
@@ -297,6 +299,35 @@ ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant) {
         if (variant < 0 || variant > 2)
             throw Fail(CCW_ERR_CONFIG, fmt("ccf variant %d unknown", variant));
         ctx->ccf_variant = variant;
+    });
+}
+
+ccw_status ccw_nccl_unique_id(uint8_t* id128) {
+    if (!id128) {
+        g_err = "ccw_nccl_unique_id: null output pointer";
+        return CCW_ERR_GENERIC;
+    }
+    return guarded(nullptr, [&] { ccwgpu::nccl_unique_id(id128); });
+}
+
+ccw_status ccw_ctx_set_position_shards(ccw_ctx* ctx, int nranks, int rank, const uint8_t* nccl_id,
+                                       int virtual_shards) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            throw Fail(CCW_ERR_CONFIG, fmt("position shards: rank %d of %d is invalid", rank, nranks));
+        if (virtual_shards < 1 || virtual_shards > 64)
+            throw Fail(CCW_ERR_CONFIG, fmt("position shards: %d virtual shards (1-64)", virtual_shards));
+        if (nranks > 1 && !nccl_id)
+            throw Fail(CCW_ERR_CONFIG, "position shards: more than one rank needs an NCCL unique id");
+        CCW_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (cudaStream_t s : ctx->gstreams) CCW_CUDA(cudaStreamSynchronize(s));
+        ccwgpu::nccl_comm_destroy(ctx->nccl_comm);
+        ctx->nccl_comm = nullptr;
+        ctx->shard_nranks = nranks;
+        ctx->shard_rank = rank;
+        ctx->shard_virtual = virtual_shards;
+        if (nccl_id) ctx->nccl_comm = ccwgpu::nccl_comm_init(nranks, rank, nccl_id);
     });
 }
 

@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(CCF_THREADS) ccf_direct_kernel(SimParams P,
     float* wpk = ccf_sm + nscr * SH * SW;
     Rect rc[2];
     const int nr = mask_rects(jb, Tc, P.OVc, rc);
-    const int x0 = blockIdx.y * CCF_TX, y0 = blockIdx.x * CCF_TY;
+    // (position shards: the grid covers the rows of [p0, p0 + npos) only)
+    const int x0 = P.p0 / P.out_w + blockIdx.y * CCF_TX, y0 = blockIdx.x * CCF_TY;
 
     const int tn = nscr * SH * SW;
     for (int e = threadIdx.x; e < tn; e += CCF_THREADS) {
@@ -117,11 +118,12 @@ __global__ void __launch_bounds__(CCF_THREADS) ccf_direct_kernel(SimParams P,
     }
     const int x = x0 + tr;
     if (x < P.out_h) {
-        int32_t* out = P.scores + static_cast<size_t>(slot) * P.sld + static_cast<size_t>(x) * P.out_w;
+        int32_t* out = P.scores + static_cast<size_t>(slot) * P.sld;
 #pragma unroll
         for (int b = 0; b < CCF_RY; ++b) {
             const int y = y0 + tcg + b;
-            if (y < P.out_w) out[y] = __float2int_rn(acc[b]);
+            const int p = x * P.out_w + y - P.p0;  // shard-local position
+            if (y < P.out_w && p >= 0 && p < P.npos) out[p] = __float2int_rn(acc[b]);
         }
     }
 }

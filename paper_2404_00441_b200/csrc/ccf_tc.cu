@@ -498,13 +498,13 @@ TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
 }
 
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* tmax, cudaStream_t st, unsigned long long* tl) {
+                   int32_t* tmax, cudaStream_t st, unsigned long long* tl, int tmax_ld) {
     TcArgs a;
     a.nj = nj;
     a.npos = npos;
     a.sld = sld;
     a.nk = (kpad + kKC - 1) / kKC;
-    a.ntiles = tc_tiles(npos);
+    a.ntiles = tmax_ld >= 0 ? tmax_ld : tc_tiles(npos);  // (row stride of tmax)
     a.scores = scores;
     a.tmax = tmax;
     a.probe = tc_probe_buffer;

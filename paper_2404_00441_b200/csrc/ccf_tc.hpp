@@ -41,6 +41,7 @@ struct TcPlan {
 };
 TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad);
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* tmax, cudaStream_t st, unsigned long long* tl = nullptr);
+                   int32_t* tmax, cudaStream_t st, unsigned long long* tl = nullptr,
+                   int tmax_ld = -1);  // tmax row stride (default: this launch's tile count)
 
 }  // namespace ccwgpu

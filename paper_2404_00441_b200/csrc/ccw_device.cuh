@@ -34,6 +34,17 @@ struct Job {
     int32_t ndep;    //   previous-wave placements this one reads ((o, i-1), (o-1, i+1))
 };
 
+// Candidate-position sharding: one entry of a shard's top-K list (fp64
+// reference score, global row-major window position; pos < 0 = empty slot).
+// valid = 0: the fast select ranked the window by its exact screen score
+// alone (no other local candidate shares it), so key is absent and the merge
+// rescores it -- windows of different shards may share a screen score.
+struct ShardRec {
+    double key;
+    int32_t pos;
+    int32_t valid;
+};
+
 // Parameters shared by every job of one simulate call.
 constexpr int kNumStats = 48;  // device counters per simulation call (SimParams::stats)
 
@@ -110,6 +121,12 @@ struct SimParams {
     int* bulk_sync;          // per job slot: [next position block, finished CTAs]
     double* bulk_keys;       // per job slot x CTA: that CTA's top-K keys
     int* bulk_idx;           //   ... and positions
+    // candidate-position sharding: the select screens window positions
+    // [p0, p0 + npos) (scores / tmax rows are shard-local) and writes its
+    // top-K to xrec[(xshard * xnj + slot) * xk + k] instead of pasting
+    int p0;
+    ShardRec* xrec;          // null: normal select
+    int xnj, xk, xshard;
     // outputs
     int32_t* chosen;         // per job (global job id): fr, fc
     uint8_t* pasted;         // optional trace of pasted patches (global job id * T*T)

@@ -229,6 +229,10 @@ struct ccw_ctx {
     // deferred no placement to the bulk tie select skip its per-wave launch
     // (re-enabled when the warp select reports a would-be deferral)
     std::map<std::tuple<uint64_t, int, int, int, int>, bool> bulk_off;
+    // candidate-position sharding (ccw_ctx_set_position_shards)
+    int shard_nranks = 1, shard_rank = 0, shard_virtual = 1;
+    void* nccl_comm = nullptr;  // ncclComm_t when shard_nranks > 1 (or an explicit id was given)
+    ccwgpu::DevBuf xrec;        // exchange buffer: [S][jobs][K] shard top-K records
 };
 
 struct ccw_ti {
@@ -266,6 +270,12 @@ uint64_t bounded(std::mt19937_64& rng, uint64_t n);
 // plan_raster_path (simulator.hpp:148-190): consumes exactly two draws.
 Plan make_plan(const ccw_sim_config& c, std::mt19937_64& rng);
 Plan make_plan_from(const ccw_sim_config& c, int origin, bool column_major);
+
+// --- NCCL (shard.cpp; libnccl.so.2 loaded on first use) -------------------
+void nccl_unique_id(uint8_t* out128);
+void* nccl_comm_init(int nranks, int rank, const uint8_t* id128);
+void nccl_comm_destroy(void* comm);
+void nccl_all_gather_bytes(void* comm, const void* send, void* recv, size_t bytes, cudaStream_t st);
 
 // --- device entry points (sim.cu / ops.cu / peak.cu) ----------------------
 double measure_ffma_peak(ccw_ctx* ctx);

@@ -210,15 +210,11 @@ __device__ void min_cut_device(const uint8_t* exist, uint8_t* outp, int T, int O
     }
 }
 
-// Rescore the gathered windows and merge them with the running top-K list
-// (K rounds of a block-wide argmax under the reference ranking).
-__device__ void flush_candidates(const SimParams& P, const RunDesc* runs, int R,
-                                 const double* tmpl, int* gidx, double* gkey, int& cnt,
-                                 double* tkey, int* tidx, int& ntop, int K, double* rsum,
-                                 double* rnrm, double* redd, int* redi) {
+// Merge cnt keyed windows (gkey, gidx) with the running top-K list (tkey,
+// tidx, ntop): K rounds of a block-wide argmax under the reference ranking.
+__device__ void merge_top(double* gkey, int* gidx, int& cnt, double* tkey, int* tidx, int& ntop,
+                          int K, double* redd, int* redi) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (P.stats && tid == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
-    rescore_group(P, runs, R, tmpl, gidx, gkey, cnt, rsum, rnrm);
     for (int e = tid; e < ntop; e += SEL_T) {
         gkey[cnt + e] = tkey[e];
         gidx[cnt + e] = tidx[e];
@@ -272,6 +268,94 @@ __device__ void flush_candidates(const SimParams& P, const RunDesc* runs, int R,
     __syncthreads();
 }
 
+// Rescore the gathered windows in fp64 and merge them with the running top-K.
+__device__ void flush_candidates(const SimParams& P, const RunDesc* runs, int R,
+                                 const double* tmpl, int* gidx, double* gkey, int& cnt,
+                                 double* tkey, int* tidx, int& ntop, int K, double* rsum,
+                                 double* rnrm, double* redd, int* redi) {
+    if (P.stats && threadIdx.x == 0) atomicAdd(&P.stats[0], static_cast<unsigned long long>(cnt));
+    rescore_group(P, runs, R, tmpl, gidx, gkey, cnt, rsum, rnrm);
+    merge_top(gkey, gidx, cnt, tkey, tidx, ntop, K, redd, redi);
+}
+
+// select_unconditional / select_conditional (matcher.hpp:207-241) over the
+// ranked list: the job's precomputed draw, or the first candidate whose TI
+// patch matches every hard datum of the footprint (else the fewest
+// mismatches, earliest first).  Returns the chosen window position.
+__device__ int choose_candidate(const SimParams& P, const Job& jb, const int* tidx, int ntop, int* redi) {
+    int pick = jb.pick;
+    if (pick < 0) {
+        int best = 0, best_mis = INT_MAX;
+        pick = -1;
+        const int cell = (jb.top / P.stride) * P.lat_nlc + jb.left / P.stride;
+        const int e0 = P.hd_off[cell], e1 = P.hd_off[cell + 1];
+        for (int c = 0; c < ntop; ++c) {
+            const int pos = tidx[c];
+            const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
+            int mis = 0;
+            for (int e = e0 + threadIdx.x; e < e1; e += SEL_T) {
+                const uint32_t u = P.hd_ent[e];
+                const int rc = static_cast<int>(u >> 8), r = rc / P.T, cc = rc - r * P.T;
+                mis += P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != (u & 255u);
+            }
+            mis = block_reduce(mis, [](int a, int b) { return a + b; }, redi);
+            if (mis == 0) {
+                pick = c;
+                break;
+            }
+            if (mis < best_mis) {
+                best = c;
+                best_mis = mis;
+            }
+        }
+        if (pick < 0) pick = best;
+    }
+    return tidx[pick];
+}
+
+// crop + optional stitch + paste (simulator.hpp:483-493) of the TI patch at
+// fine origin (fr, fc), the source-block map entries and the chosen origin.
+__device__ void paste_placement(const SimParams& P, const Job& jb, int gj, int fr, int fc, uint8_t* exist,
+                                uint8_t* outp, int16_t* from, int* dp, int* seam) {
+    const int tid = threadIdx.x;
+    const int T = P.T;
+    uint8_t* g = P.work ? P.work + static_cast<size_t>(jb.real) * P.wh * P.ww : nullptr;
+    uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
+    if (P.min_cut && jb.shape != kNone) {
+        for (int e = tid; e < T * T; e += SEL_T) {
+            const int r = e / T, c = e - r * T;
+            exist[e] = g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c];
+            outp[e] = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+        }
+        __syncthreads();
+        min_cut_device(exist, outp, T, P.OV, jb.shape, jb.vleft, jb.htop, from, dp, seam);
+        for (int e = tid; e < T * T; e += SEL_T) {
+            const int r = e / T, c = e - r * T;
+            g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = outp[e];
+            if (trace) trace[e] = outp[e];
+        }
+    } else if (P.work || trace) {  // (no work grid: the source-block map is the realization)
+        for (int e = tid; e < T * T; e += SEL_T) {
+            const int r = e / T, c = e - r * T;
+            const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+            if (P.work) g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
+            if (trace) trace[e] = v;
+        }
+    }
+    if (P.src) {
+        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc;
+        for (int e = tid; e < P.Tc * P.Tc; e += SEL_T) {
+            const int a = e / P.Tc, b = e - a * P.Tc;
+            sm[static_cast<size_t>(jb.top / P.B + a) * P.swc + jb.left / P.B + b] =
+                (fr / P.B + a) * P.wc + fc / P.B + b;
+        }
+    }
+    if (tid == 0) {
+        P.chosen[2 * gj] = fr;
+        P.chosen[2 * gj + 1] = fc;
+    }
+}
+
 __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
                                                              const Job* __restrict__ jobs,
                                                              int job0, int use_screen) {
@@ -300,6 +384,7 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
     const Job jb = jobs[gj];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     pdl_wait();
+    if (P.xrec && jb.shape == kNone) return;  // (position shards: the merge places first patches)
     int fr, fc;
     if (jb.shape == kNone) {
         fr = jb.fr;
@@ -342,7 +427,7 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
             // error << 1e-9) can rank in the top-K has R >= R_K (1 - 1e-9),
             // hence key >= the threshold below: a superset, rescored exactly.
             int32_t* scw = P.scores + static_cast<size_t>(blockIdx.x) * P.sld;
-            const int32_t* nn = P.nnmap + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * P.npos;
+            const int32_t* nn = P.nnmap + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * (P.out_h * P.out_w) + P.p0;
             const int cj = P.cjob[blockIdx.x];
             for (int p = tid; p < P.npos; p += SEL_T) {
                 const int n = nn[p];
@@ -376,7 +461,7 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
                     if (w < wid) off += redi[w];
                     tot += redi[w];
                 }
-                if (q) gidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p;
+                if (q) gidx[cnt + off + __popc(bal & ((1u << lane) - 1))] = p + P.p0;
                 cnt += tot;
                 __syncthreads();
                 if (cnt + SEL_T > GCAP)
@@ -387,77 +472,102 @@ __global__ void __launch_bounds__(SEL_T) select_paste_kernel(SimParams P,
         if (cnt > 0)
             flush_candidates(P, runs, R, tmpl, gidx, gkey, cnt, tkey, tidx, ntop, K, rsum, rnrm,
                              redd, redi);
-        // 3. choose (matcher.hpp:207-241)
-        int pick = jb.pick;
-        if (pick < 0) {
-            int best = 0, best_mis = INT_MAX;
-            pick = -1;
-            const int cell = (jb.top / P.stride) * P.lat_nlc + jb.left / P.stride;
-            const int e0 = P.hd_off[cell], e1 = P.hd_off[cell + 1];
-            for (int c = 0; c < ntop; ++c) {
-                const int pos = tidx[c];
-                const int cfr = (pos / P.out_w) << P.J, cfc = (pos % P.out_w) << P.J;
-                int mis = 0;
-                for (int e = e0 + tid; e < e1; e += SEL_T) {
-                    const uint32_t u = P.hd_ent[e];
-                    const int rc = static_cast<int>(u >> 8), r = rc / P.T, cc = rc - r * P.T;
-                    mis += P.ti[static_cast<size_t>(cfr + r) * P.ti_w + cfc + cc] != (u & 255u);
-                }
-                mis = block_reduce(mis, [](int a, int b) { return a + b; }, redi);
-                if (mis == 0) {
-                    pick = c;
-                    break;
-                }
-                if (mis < best_mis) {
-                    best = c;
-                    best_mis = mis;
-                }
-            }
-            if (pick < 0) pick = best;
+        if (P.xrec) {  // position shard: hand the local top-K to the exchange
+            ShardRec* xr = P.xrec + (static_cast<size_t>(P.xshard) * P.xnj + blockIdx.x) * P.xk;
+            for (int k = tid; k < P.xk; k += SEL_T)
+                xr[k] = k < ntop ? ShardRec{tkey[k], tidx[k], 1} : ShardRec{0.0, -1, 0};
+            return;
         }
-        const int pos = tidx[pick];
+        // 3. choose (matcher.hpp:207-241)
+        const int pos = choose_candidate(P, jb, tidx, ntop, redi);
         fr = (pos / P.out_w) << P.J;
         fc = (pos % P.out_w) << P.J;
         __syncthreads();
     }
-
     // 4. crop + optional stitch + paste (simulator.hpp:483-493)
-    const int T = P.T;
-    uint8_t* g = P.work ? P.work + static_cast<size_t>(jb.real) * P.wh * P.ww : nullptr;
-    uint8_t* trace = P.pasted ? P.pasted + static_cast<size_t>(gj) * T * T : nullptr;
-    if (P.min_cut && jb.shape != kNone) {
-        for (int e = tid; e < T * T; e += SEL_T) {
-            const int r = e / T, c = e - r * T;
-            exist[e] = g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c];
-            outp[e] = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
+    paste_placement(P, jb, gj, fr, fc, exist, outp, from, dp, seam);
+}
+
+// Candidate-position sharding, after the exchange: merge the S shard lists
+// of each placement (xrec, [S][nj][xk]) into the reference's top-K, then
+// choose and paste exactly as select_paste_kernel does.  Every rank runs this
+// on identical lists, so every rank pastes the same patch.
+__global__ void __launch_bounds__(SEL_T) shard_merge_kernel(SimParams P, const Job* __restrict__ jobs,
+                                                            int job0, int nshards) {
+    extern __shared__ __align__(16) unsigned char sel_sm[];
+    const SelLayout L = sel_layout(P.K, P.T, P.OV, P.nch, P.Tc, P.scoring == 1);
+    double* redd = reinterpret_cast<double*>(sel_sm + L.redd);
+    int* redi = reinterpret_cast<int*>(sel_sm + L.redi);
+    double* gkey = reinterpret_cast<double*>(sel_sm + L.gkey);
+    int* gidx = reinterpret_cast<int*>(sel_sm + L.gidx);
+    double* tkey = reinterpret_cast<double*>(sel_sm + L.tkey);
+    int* tidx = reinterpret_cast<int*>(sel_sm + L.tidx);
+    uint8_t* exist = sel_sm + L.exist;
+    uint8_t* outp = sel_sm + L.outp;
+    int16_t* from = reinterpret_cast<int16_t*>(sel_sm + L.from);
+    int* dp = reinterpret_cast<int*>(sel_sm + L.dp);
+    int* seam = reinterpret_cast<int*>(sel_sm + L.seam);
+
+    pdl_trigger();
+    const int gj = job0 + blockIdx.x;
+    const Job jb = jobs[gj];
+    const int tid = threadIdx.x;
+    pdl_wait();
+    int fr = jb.fr, fc = jb.fc;
+    if (jb.shape != kNone) {
+        RunDesc* runs = reinterpret_cast<RunDesc*>(sel_sm + L.runs);
+        double* tmpl = reinterpret_cast<double*>(sel_sm + L.tmpl);
+        double* rsum = reinterpret_cast<double*>(sel_sm + L.rsum);
+        double* rnrm = reinterpret_cast<double*>(sel_sm + L.rnrm);
+        const int Tc = P.Tc;
+        // the fp64 template and run list, for keys the fast select left out
+        const double* tm = P.tm64 + static_cast<size_t>(blockIdx.x) * P.nch * Tc * Tc;
+        for (int e = tid; e < P.nch * Tc * Tc; e += SEL_T) tmpl[e] = tm[e];
+        int R = 0;
+        for (int ch = 0; ch < P.nch; ++ch)
+            for (int s = 0; s < Tc; ++s) {
+                int t0, t1;
+                mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+                if (t1 > t0) {
+                    if (tid == 0) runs[R] = {ch, s, t0, t1};
+                    ++R;
+                }
+            }
+        __shared__ int nvalid, nabsent;
+        int ntop = 0, cnt = 0;
+        const int n = nshards * P.xk;
+        for (int e0 = 0; e0 < n; e0 += GCAP) {
+            const int m = min(GCAP, n - e0);
+            if (tid == 0) {
+                nvalid = 0;
+                nabsent = 0;
+            }
+            __syncthreads();
+            for (int e = tid; e < m; e += SEL_T) {
+                const int s = (e0 + e) / P.xk, k = (e0 + e) - s * P.xk;
+                const ShardRec r = P.xrec[(static_cast<size_t>(s) * P.xnj + blockIdx.x) * P.xk + k];
+                if (r.pos >= 0) {  // (empty slots of a short shard list are skipped; the
+                                   //  merge orders by (key, position), so slot order is free)
+                    const int at = atomicAdd(&nvalid, 1);
+                    gkey[at] = r.key;
+                    gidx[at] = r.pos;
+                    if (!r.valid) nabsent = 1;
+                }
+            }
+            __syncthreads();
+            cnt = nvalid;
+            // absent keys: rescore the chunk in the reference's order (the keys
+            // that were present are recomputed bit-identically)
+            if (nabsent) rescore_group(P, runs, R, tmpl, gidx, gkey, cnt, rsum, rnrm);
+            if (cnt > 0) merge_top(gkey, gidx, cnt, tkey, tidx, ntop, P.K, redd, redi);
+            __syncthreads();
         }
+        const int pos = choose_candidate(P, jb, tidx, ntop, redi);
+        fr = (pos / P.out_w) << P.J;
+        fc = (pos % P.out_w) << P.J;
         __syncthreads();
-        min_cut_device(exist, outp, T, P.OV, jb.shape, jb.vleft, jb.htop, from, dp, seam);
-        for (int e = tid; e < T * T; e += SEL_T) {
-            const int r = e / T, c = e - r * T;
-            g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = outp[e];
-            if (trace) trace[e] = outp[e];
-        }
-    } else if (P.work || trace) {  // (no work grid: the source-block map is the realization)
-        for (int e = tid; e < T * T; e += SEL_T) {
-            const int r = e / T, c = e - r * T;
-            const uint8_t v = P.ti[static_cast<size_t>(fr + r) * P.ti_w + fc + c];
-            if (P.work) g[static_cast<size_t>(jb.top + r) * P.ww + jb.left + c] = v;
-            if (trace) trace[e] = v;
-        }
     }
-    if (P.src) {
-        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc;
-        for (int e = tid; e < P.Tc * P.Tc; e += SEL_T) {
-            const int a = e / P.Tc, b = e - a * P.Tc;
-            sm[static_cast<size_t>(jb.top / P.B + a) * P.swc + jb.left / P.B + b] =
-                (fr / P.B + a) * P.wc + fc / P.B + b;
-        }
-    }
-    if (tid == 0) {
-        P.chosen[2 * gj] = fr;
-        P.chosen[2 * gj + 1] = fc;
-    }
+    paste_placement(P, jb, gj, fr, fc, exist, outp, from, dp, seam);
 }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -1275,6 +1385,10 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     if (slot >= nj) return;
     const int gj = job0 + slot;
     const Job jb = jobs[gj];
+    if (P.xrec && jb.shape == kNone) {  // (position shards: the merge places first patches)
+        if (P.defer && tid == 0) P.defer[slot] = INT_MIN;
+        return;
+    }
     const int Tc = P.Tc;
     long long fclk[5] = {clock64(), 0, 0, 0, 0};
 #ifdef CCW_DBG_TAIL
@@ -1364,7 +1478,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         }
         if (P.defer && tid == 0) P.defer[slot] = INT_MIN;
         int picked = -1;  // the chosen position when settled without the ranked list
-        if (n >= 0 && jb.pick >= 0) {
+        if (n >= 0 && jb.pick >= 0 && !P.xrec) {
             // Unconditional pick (matcher.hpp:207-211): only the candidate at rank
             // `pick` of (S desc, fp64 desc, index asc) matters, and windows with
             // different S never swap in fp64 -- so only the equal-S group that
@@ -1492,7 +1606,8 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                 }
                 if (lane < n && rank < K) {
                     S.tidx[rank] = ii;
-                    S.tkey[rank] = ki;
+                    // (position shards: a key that was not computed is marked NaN)
+                    S.tkey[rank] = P.xrec && S.tslot[lane] < 0 ? __longlong_as_double(0x7ff8000000000000ll) : ki;
                 }
             }
             ntop = min(K, n);
@@ -1528,6 +1643,14 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             if (cnt > 0) fast_batch(P, S, tmg, nr, ngrp, cnt, ntop, K);
         }
         fclk[2] = clock64();
+        if (P.xrec) {  // position shard: hand the local top-K to the exchange
+            ShardRec* xr = P.xrec + (static_cast<size_t>(P.xshard) * P.xnj + slot) * P.xk;
+            for (int k = tid; k < P.xk; k += FS_T) {
+                const double key = k < ntop ? S.tkey[k] : 0.0;
+                xr[k] = k < ntop ? ShardRec{key, S.tidx[k], isnan(key) ? 0 : 1} : ShardRec{0.0, -1, 0};
+            }
+            return;
+        }
         // choose (matcher.hpp:207-241)
         if (picked < 0 && wid == 0) {
             const int pos = choose_pick(P, jb, S.tidx, ntop, lane);
@@ -1865,14 +1988,21 @@ __global__ void __launch_bounds__(BK_T, 1)
             __syncwarp();
             ntop = round + 1;
         }
-        const int pos = choose_pick(P, jb, tidx, ntop, lane);
+        if (P.xrec) {  // position shard: the merged list goes to the exchange (every key exact)
+            ShardRec* xr = P.xrec + (static_cast<size_t>(P.xshard) * P.xnj + slot) * P.xk;
+            for (int k = lane; k < P.xk; k += 32)
+                xr[k] = k < ntop ? ShardRec{tkey[k], tidx[k], 1} : ShardRec{0.0, -1, 0};
+        } else {
+            const int pos = choose_pick(P, jb, tidx, ntop, lane);
+            if (lane == 0) shv[3] = pos;
+        }
         if (lane == 0) {
-            shv[3] = pos;
             next[0] = 0;  // reset the placement's counters for the next launch
             next[1] = 0;
             if (P.stats) atomicAdd(&P.stats[3], 1ull);
         }
     }
+    if (P.xrec) return;
     __syncthreads();
     const int pos = shv[3];
     const int fr = (pos / P.out_w) << P.J, fc = (pos % P.out_w) << P.J;

@@ -41,6 +41,18 @@ namespace ccwgpu {
 
 // ----------------------------------------------------------- finalize ----
 
+__global__ void fill_i32_kernel(int32_t* __restrict__ p, size_t n, int32_t v) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+void fill_i32(int32_t* p, size_t n, int32_t v, cudaStream_t st) {
+    if (!p || n == 0) return;
+    fill_i32_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4 * 148)), 256, 0, st>>>(p, n, v);
+    CCW_CUDA(cudaGetLastError());
+}
+
 __global__ void hd_scatter_kernel(const int32_t* __restrict__ hd, int n_hd, uint8_t* plane, int ww) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n_hd) plane[static_cast<size_t>(hd[3 * i]) * ww + hd[3 * i + 1]] = static_cast<uint8_t>(hd[3 * i + 2]);
@@ -473,8 +485,17 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // Realizations are split into G independent groups, each on its own
     // stream, so one group's latency-bound select overlaps another group's
     // tensor-core screen.  Within a group, waves run in order.
+    // candidate-position sharding (ccw_ctx_set_position_shards): S shards of the
+    // window positions, S_virt of them in this rank; one group (the per-wave
+    // exchange is one collective on one stream)
+    const int S_virt = ctx->shard_virtual, S_ranks = ctx->shard_nranks;
+    const int S_all = S_virt * S_ranks;
+    const bool sharded = S_all > 1 || ctx->nccl_comm != nullptr;
+    if (sharded && npos < S_all)
+        throw Fail(CCW_ERR_CONFIG, "position shards: more shards than TI window positions");
     int G = std::max(1, std::min(n_real, 2));
     if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
+    if (sharded) G = 1;
     auto group_of = [&](int r) { return static_cast<int>(static_cast<int64_t>(r) * G / n_real); };
     std::vector<size_t> bucket(static_cast<size_t>(G) * nkeys + 1, 0);
     size_t total_jobs = 0;
@@ -671,9 +692,15 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     P.src = d_src;
     P.swc = swc;
-    const bool warp_select = use_tc && Kp <= kTcQ && !cfg.min_cut && cfg.scoring == 0 &&
-                             ti->nch * Tc <= FS_MAXG && Tc <= PK_MAXTC;
-    if (warp_select) {
+    const bool fast_ok = use_tc && Kp <= kTcQ && !cfg.min_cut && cfg.scoring == 0 &&
+                         ti->nch * Tc <= FS_MAXG && Tc <= PK_MAXTC;
+    // position shards take the fast select when every shard (boundaries at
+    // multiples of one 256-position MMA tile) holds at least K tile maxima of
+    // its own; the other shards' tiles read INT_MIN and are never candidates
+    const bool shard_fast = sharded && fast_ok && !getenv("CCW_SHARD_GENERIC") &&
+                            npos / S_all >= 256 + 128 * Kp;
+    const bool warp_select = !sharded && fast_ok;
+    if (warp_select || shard_fast) {
         const long long key = Tc | (static_cast<long long>(OVc) << 16) | (static_cast<long long>(ti->nch) << 32);
         int4* d_mt = ctx->mtab.as<int4>(static_cast<size_t>(8) * MT_STRIDE);
         if (ctx->mtab_key != key) {
@@ -691,7 +718,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.im2col = d_x;
     // bulk tie select: largest window block whose apex tile fits the shared-memory budget
     size_t bulk_smem = 0;
-    if (warp_select && !getenv("CCW_NOBULK")) {
+    if ((warp_select || shard_fast) && !getenv("CCW_NOBULK")) {
         constexpr size_t kBudget = 200 * 1024;
         for (int by = std::min(out_w, 256); by >= 8 && !bulk_smem; by /= 2) {
             int bx = std::min(out_h, 64);
@@ -816,6 +843,53 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         for (int g = 0; g < G; ++g)
             for (int par = 0; par < 2; ++par)
                 tcplans[g][par] = plan_ccf_tc(GPP[g][par].wts8, static_cast<int>(maxj), d_x, npos, kpad);
+    // position shards of this rank: window ranges, shard-local score rows and
+    // tile maxima, TMA plans over the im2col row slice, the exchange buffer
+    struct ShardPart {
+        int s, p0, n, sld, ntiles;
+        int32_t *scores, *tmax;
+        TcPlan plan;
+    };
+    std::vector<ShardPart> parts;
+    ShardRec* d_xrec = nullptr;
+    if (sharded) {
+        size_t sc_tot = 0, tm_tot = 0;
+        auto cut = [&](int s) {  // shard boundary (256-aligned for the fast select)
+            const int64_t p = static_cast<int64_t>(npos) * s / S_all;
+            return static_cast<int>(shard_fast && s < S_all ? p / 256 * 256 : p);
+        };
+        for (int v = 0; v < S_virt; ++v) {
+            ShardPart sp{};
+            sp.s = ctx->shard_rank * S_virt + v;
+            sp.p0 = cut(sp.s);
+            sp.n = cut(sp.s + 1) - sp.p0;
+            // fast select: full-length rows in global positions, INT_MIN outside the shard
+            sp.sld = shard_fast ? sld : (sp.n + 3) & ~3;
+            sp.ntiles = shard_fast ? ntiles : tc_tiles(sp.n);
+            sc_tot += maxj * sp.sld;
+            tm_tot += maxj * sp.ntiles;
+            parts.push_back(sp);
+        }
+        int32_t* sc = ctx->scores.as<int32_t>(sc_tot);
+        int32_t* tmx = use_tc ? ctx->summary.as<int32_t>(tm_tot) : nullptr;
+        if (shard_fast) {
+            fill_i32(sc, sc_tot, INT_MIN, st);
+            fill_i32(tmx, tm_tot, INT_MIN, st);
+        }
+        for (ShardPart& sp : parts) {
+            sp.scores = sc;
+            sc += maxj * sp.sld;
+            if (tmx) {
+                sp.tmax = tmx;
+                tmx += maxj * sp.ntiles;
+                sp.plan = plan_ccf_tc(GPP[0][0].wts8, static_cast<int>(maxj), d_x + static_cast<size_t>(sp.p0) * kpad,
+                                      sp.n, kpad);
+            }
+        }
+        d_xrec = ctx->xrec.as<ShardRec>(static_cast<size_t>(S_all) * maxj * Kp);
+        CCW_CUDA(cudaFuncSetAttribute(shard_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sel_smem)));
+    }
     // group streams, forked from / joined back to the context stream
     while (static_cast<int>(ctx->copy_streams.size()) < G) {  // one per group: final copies overlap
         cudaStream_t s3;
@@ -1084,6 +1158,96 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             for (size_t j0 = wave_off[g][w]; j0 < wave_off[g][w + 1]; j0 += maxj) {
                 const int nj = static_cast<int>(std::min(maxj, wave_off[g][w + 1] - j0));
                 const bool first_wave = w == 0;  // (wave 0 is every realization's first placement)
+                if (sharded) {
+                    // per shard: screen its window range, local top-K into the
+                    // exchange buffer; all-gather across ranks; merge, pick, paste
+                    if (!first_wave) {
+                        launch_pdl(d_src ? or_prep_src_kernel : or_prep_kernel, dim3(nj), dim3(128), 0, gs, Q,
+                                   static_cast<const Job*>(d_jobs), static_cast<int>(j0));
+                        ++launches;
+                        for (const ShardPart& sp : parts) {
+                            SimParams QV = Q;
+                            if (!shard_fast) {  // (fast: global positions, full-length rows)
+                                QV.p0 = sp.p0;
+                                QV.npos = sp.n;
+                                QV.K = std::min(Kp, sp.n);
+                                QV.sld = sp.sld;
+                                QV.ntiles = sp.ntiles;
+                            }
+                            QV.scores = sp.scores;
+                            QV.tmax = sp.tmax;
+                            QV.xrec = d_xrec;
+                            QV.xnj = nj;
+                            QV.xk = Kp;
+                            QV.xshard = sp.s;
+                            if (any_screen) {
+                                cudaEvent_t a = nullptr, b = nullptr;
+                                if (ctx->profiling) {
+                                    a = tm.get();
+                                    b = tm.get();
+                                    CCW_CUDA(cudaEventRecord(a, gs));
+                                }
+                                if (shard_fast) {
+                                    launch_ccf_tc(sp.plan, sp.n, sp.sld, kpad, nj, sp.scores + sp.p0,
+                                                  sp.tmax + sp.p0 / kTcTile, gs, nullptr, sp.ntiles);
+                                } else if (use_tc) {
+                                    launch_ccf_tc(sp.plan, sp.n, sp.sld, kpad, nj, sp.scores, sp.tmax, gs);
+                                } else {  // fp32 direct screen over the rows holding the shard's range
+                                    const int xr0 = sp.p0 / out_w, xr1 = (sp.p0 + sp.n - 1) / out_w;
+                                    const unsigned gy = static_cast<unsigned>((xr1 - xr0 + CCF_TX) / CCF_TX);
+                                    launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, gy, nj), dim3(CCF_THREADS),
+                                               ccf_smem, gs, QV, static_cast<const Job*>(d_jobs),
+                                               static_cast<int>(j0));
+                                }
+                                if (ctx->profiling) {
+                                    CCW_CUDA(cudaEventRecord(b, gs));
+                                    tm.ccf.push_back({a, b});
+                                }
+                                ++launches;
+                                ++ccf_launches;
+                                if (use_tc) ccf_mma_flop += 2.0 * kpad * static_cast<double>(sp.n) * nj;
+                            }
+                            if (shard_fast) {
+                                launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, QV,
+                                           static_cast<const Job*>(d_jobs), static_cast<int>(j0), nj);
+                                if (QV.defer) {
+                                    launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, QV,
+                                               static_cast<const Job*>(d_jobs), static_cast<int>(j0), nj, bulk_S);
+                                    ++launches;
+                                }
+                            } else {
+                                launch_pdl(select_paste_kernel, dim3(nj), dim3(SEL_T), sel_smem, gs, QV,
+                                           static_cast<const Job*>(d_jobs), static_cast<int>(j0),
+                                           use_screen ? 1 : (norm_screen ? 2 : 0));
+                            }
+                            ++launches;
+                        }
+                        if (any_screen && j0 == wave_off[g][w]) {
+                            double nL = 0, nS = 0, mine = 0;
+                            for (const ShardPart& sp : parts) mine += sp.n;
+                            for (int r = 0; r < n_real; ++r) {
+                                nL += vhistL[vid[r]][w];
+                                nS += vhist[vid[r]][w] - vhistL[vid[r]][w];
+                            }
+                            const double m = nL * mask_cells + nS * static_cast<double>(Tc) * OVc;
+                            ccf_flop += 2.0 * ti->nscr * mine * m;
+                            ccf_flop_ref += 2.0 * ti->nch * mine * m;
+                        }
+                        if (ctx->nccl_comm) {
+                            const size_t chunk = static_cast<size_t>(S_virt) * nj * Kp;
+                            nccl_all_gather_bytes(ctx->nccl_comm, d_xrec + ctx->shard_rank * chunk, d_xrec,
+                                                  chunk * sizeof(ShardRec), gs);
+                        }
+                    }
+                    SimParams QM = Q;
+                    QM.xrec = d_xrec;
+                    QM.xnj = nj;
+                    QM.xk = Kp;
+                    launch_pdl(shard_merge_kernel, dim3(nj), dim3(SEL_T), sel_smem, gs, QM,
+                               static_cast<const Job*>(d_jobs), static_cast<int>(j0), S_all);
+                    ++launches;
+                    continue;
+                }
                 if (!first_wave) {
                     Q.tl = tl_next(w, g, 0);
                     if (!skip_prep && !fuse_prep) {  // (fused: prepared by the previous wave's select)

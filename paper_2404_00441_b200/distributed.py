@@ -1,4 +1,9 @@
-"""Multi-GPU realization sharding (one process per GPU, torch.distributed).
+"""Multi-GPU sharding (one process per GPU, torch.distributed).
+
+Two decompositions:
+
+* realization shards -- below;
+* candidate-position shards of one realization -- simulate_position_sharded.
 
 Realizations are independent -- realization r is a pure function of
 (TI, config, mix64(master, r + 1)) (simulator.hpp:523-566) -- so
@@ -63,3 +68,58 @@ def gather_ensemble(idx: List[int], local: np.ndarray, n_total: int, dst: int = 
         for j, r in enumerate(ids):
             out[r] = arr[j]
     return out
+
+
+# ------------------------------------------------ candidate-position shards --
+#
+# A single realization has no independent units, but every placement's score
+# map does: the reference scores the npos TI windows in row-major order and
+# keeps the K best (matcher.hpp:147-204).  Shard s of S screens the windows
+# [position_range(npos, s, S)) and ranks them locally under the reference's
+# rule (fp64 score descending, earlier position on ties); the global top-K is
+# the merge of the S local top-K lists, because each of its windows is among
+# the K best of its own shard.  On the GPU the lists (16 B per candidate) are
+# all-gathered with ncclAllGather once per placement wave and merged on every
+# rank (libccwgpu.so, shard_merge_kernel); the functions below restate the
+# partition and the merge for host tests.
+
+def position_range(npos: int, shard: int, nshards: int) -> Tuple[int, int]:
+    """[p0, p1) of shard `shard` (the C++ split in sim.cu run_simulation)."""
+    if nshards < 1 or not 0 <= shard < nshards:
+        raise ValueError(f"bad shard {shard} of {nshards}")
+    return npos * shard // nshards, npos * (shard + 1) // nshards
+
+
+def local_top_k(scores: np.ndarray, p0: int, p1: int, k: int) -> List[Tuple[float, int]]:
+    """A shard's top-K (score, global position) under the reference ranking."""
+    flat = np.asarray(scores, np.float64).ravel()
+    pos = np.arange(p0, p1)
+    order = sorted(pos.tolist(), key=lambda p: (-flat[p], p))
+    return [(float(flat[p]), int(p)) for p in order[:min(k, p1 - p0)]]
+
+
+def merge_top_k(lists: Sequence[Sequence[Tuple[float, int]]], k: int) -> List[Tuple[float, int]]:
+    """Global top-K from the shards' lists (shard_merge_kernel's rule)."""
+    allc = [c for lst in lists for c in lst]
+    allc.sort(key=lambda c: (-c[0], c[1]))
+    return allc[:k]
+
+
+def simulate_position_sharded(ti: cs.CategoricalGrid, cfg: cs.SimConfig, seeds: Sequence[int],
+                              device: Optional[cs.Device] = None, group=None,
+                              virtual_shards: int = 1):
+    """Simulate `seeds` with every placement's window positions sharded over
+    the ranks of `group` (torch.distributed, one GPU per rank).  Rank 0 draws
+    the NCCL unique id and broadcasts it; each rank's context joins one NCCL
+    communicator; every rank returns the same SimResult list."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = device or cs.default_device()
+    box = [cs.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    dev.set_position_shards(world, rank, box[0], virtual_shards)
+    try:
+        return cs.simulate_batch(ti, cfg, list(seeds), None, dev)
+    finally:
+        dev.set_position_shards(1, 0, None, 1)
