@@ -311,20 +311,30 @@ __attribute__((target("bmi2"))) void unpack_band_pdep(uint8_t* d, size_t ld, con
     for (size_t y = 0; y < rows; ++y, d += ld, sp += rowb) {
         const uint8_t* s = sp;
         size_t x = 0;
-        if (ld == wdt) {  // whole rows: contiguous, written around the caches
-            for (; x + 8 <= wdt; x += 8, s += kBits) {
-                uint32_t in = 0;
-                std::memcpy(&in, s, kBits);
-                _mm_stream_si64(reinterpret_cast<long long*>(d + x), static_cast<long long>(_pdep_u64(in, kMask)));
-            }
-        } else {  // (non-temporal stores to partial lines are ~10x slower than cached ones)
-            for (; x + 8 <= wdt; x += 8, s += kBits) {
-                uint32_t in = 0;
-                std::memcpy(&in, s, kBits);
-                const uint64_t cells = _pdep_u64(in, kMask);
-                std::memcpy(d + x, &cells, 8);
-            }
+        // Whole 64-byte lines of the destination are written around the caches
+        // (no read-for-ownership); the partial lines at either end of a
+        // column-band row take cached stores (non-temporal stores to partial
+        // lines are ~10x slower than cached ones).  8 cells per input word.
+#define CCW_PUT8(NT)                                                                             \
+    do {                                                                                         \
+        uint32_t in = 0;                                                                         \
+        std::memcpy(&in, s, kBits);                                                              \
+        const uint64_t cells = _pdep_u64(in, kMask);                                             \
+        if (NT)                                                                                  \
+            _mm_stream_si64(reinterpret_cast<long long*>(d + x), static_cast<long long>(cells)); \
+        else                                                                                     \
+            std::memcpy(d + x, &cells, 8);                                                       \
+        x += 8;                                                                                  \
+        s += kBits;                                                                              \
+    } while (0)
+        const size_t head = (64 - (reinterpret_cast<uintptr_t>(d) & 63)) & 63;  // bytes to the first line
+        if ((head & 7) == 0) {
+            while (x < head && x + 8 <= wdt) CCW_PUT8(false);
+            const size_t body = x + (wdt - x) / 64 * 64;
+            while (x < body) CCW_PUT8(true);
         }
+        while (x + 8 <= wdt) CCW_PUT8(false);
+#undef CCW_PUT8
         for (; x < wdt; ++x) {  // the row's last partial group of 8
             const size_t c = x & 7;
             d[x] = static_cast<uint8_t>((s[c / CPB] >> ((c % CPB) * kBits)) & ((1u << kBits) - 1));
@@ -891,14 +901,27 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                       static_cast<int>(sel_smem)));
     }
     // group streams, forked from / joined back to the context stream
+    // Stream priorities (CCW_PRIO = none | copies | waves), default none.
+    // Measured r1 (config 1, end to end): waves first 22.6 G cells/s --
+    // starving the band finalize kernels delays the host's unpacking; copies
+    // first 27.3-28.0 vs none 27.9-29.6, within run-to-run noise.
+    int least = 0, greatest = 0;
+    CCW_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    int wave_prio = least, copy_prio = least;
+    {
+        const char* e = getenv("CCW_PRIO");
+        const std::string pm = e ? e : "none";
+        if (pm == "waves") wave_prio = greatest;
+        if (pm == "copies") copy_prio = greatest;
+    }
     while (static_cast<int>(ctx->copy_streams.size()) < G) {  // one per group: final copies overlap
         cudaStream_t s3;
-        CCW_CUDA(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+        CCW_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, copy_prio));
         ctx->copy_streams.push_back(s3);
     }
     while (static_cast<int>(ctx->gstreams.size()) < G) {
         cudaStream_t s2;
-        CCW_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        CCW_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, wave_prio));
         ctx->gstreams.push_back(s2);
     }
     // timing experiments only (results are wrong when set): skip a kernel class
@@ -944,6 +967,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // (direct row bands measured slower, r1: one copy per realization band
     // lengthens the launch loop, and 8-bit rows quadruple the PCIe bytes)
     const bool direct_rows = getenv("CCW_DIRECT_ROWS") != nullptr;
+    size_t band_cap = 1024;  // CTAs per band of a finalize launch
+    if (const char* e = getenv("CCW_BAND_CTAS")) band_cap = std::max(1, atoi(e));
     bool h_pinned = false;
     if (stream_out) {
         cudaPointerAttributes pa{};
@@ -1344,7 +1369,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
                                                   (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
                     const size_t per_thread = packed && pack_bits < 8 ? static_cast<size_t>(pack_cpb) : fin_cells;
-                    const int bxb = static_cast<int>(std::min<size_t>((most / per_thread + 255) / 256 + 1, 1024));
+                    const int bxb = static_cast<int>(std::min<size_t>((most / per_thread + 255) / 256 + 1, band_cap));
                     auto band = [&](auto kern) {
                         launch_pdl(kern, dim3(bxb, static_cast<unsigned>(q1 - q0)), dim3(256), 0, ctx->copy_streams[g],
                                    static_cast<const int4*>(d_bands + q0),
