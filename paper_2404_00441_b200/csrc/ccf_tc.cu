@@ -216,7 +216,11 @@ __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
     uint64_t* tfull = empty + kStages;   // [2] accumulator ready
     uint64_t* tempty = tfull + 2;        // [2] accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    const uint32_t epi_stage = smem_u32(sm + kStages * kStageBytes + 256);  // 4 KB per epilogue warp
+    // 4 KB per epilogue warp: after the ring when CTAs loop over tiles; in the
+    // ring itself when each CTA drains a single tile (its MMAs have read every
+    // stage before the accumulator is signalled full, and nothing is loaded
+    // after them), which halves the footprint so two CTAs share an SM
+    const uint32_t epi_stage = a.epi_in_ring ? smem_u32(sm) : smem_u32(sm + kStages * kStageBytes + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mt = (a.nj + kM - 1) / kM, n_nt = (a.npos + kN - 1) / kN;
@@ -432,7 +436,10 @@ CUtensorMap make_map(void* base, uint64_t cols_bytes, uint64_t rows, uint32_t bo
 
 }  // namespace
 
-size_t ccf_tc_smem_bytes() { return kStages * kStageBytes + 1024 + 256 + kEpiWarps * 4096; }
+size_t ccf_tc_smem_bytes(bool epi_in_ring) {
+    static_assert(kStages * kStageBytes >= kEpiWarps * 4096, "epilogue staging must fit in the ring");
+    return kStages * kStageBytes + 1024 + 256 + (epi_in_ring ? 0 : kEpiWarps * 4096);
+}
 
 int tc_num_sms() {
     static int sms = 0;
@@ -510,8 +517,11 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     a.probe = tc_probe_buffer;
     a.tl = tl;
     const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
-    dim3 grid(std::min(ntot, tc_num_sms()));
-    launch_pdl(ccf_tc_kernel, grid, dim3(kThreads), ccf_tc_smem_bytes(), st, pl.ma, pl.mb, a);
+    // CTAs resident at once: CCW_TC_MINB per SM when the footprint allows
+    const int slots = tc_num_sms() * CCW_TC_MINB;
+    a.epi_in_ring = ntot <= slots && !getenv("CCW_TC_EPI_SEPARATE");
+    dim3 grid(std::min(ntot, a.epi_in_ring ? slots : tc_num_sms()));
+    launch_pdl(ccf_tc_kernel, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
 }
 
 int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // tile maxima per score row

@@ -23,9 +23,11 @@ struct TcArgs {
     int32_t* tmax;     // [nj][ntiles] maximum score of each tile
     unsigned long long* probe;  // debug phase clocks (null unless CCW_TC_PROBE)
     unsigned long long* tl;     // debug timeline slot (null unless CCW_TIMELINE)
+    int epi_in_ring;            // every CTA drains one tile: the epilogue's transpose
+                                // staging reuses the (then idle) TMA ring
 };
 
-size_t ccf_tc_smem_bytes();
+size_t ccf_tc_smem_bytes(bool epi_in_ring = false);
 extern unsigned long long* tc_probe_buffer;  // debug: ccf phase clocks (CCW_TC_PROBE)
 int tc_kpad(int nscr, int Tc);
 int tc_tiles(int npos);

@@ -1000,6 +1000,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         int nck = 6;
         if (const char* e = getenv("CCW_STREAM_BANDS")) nck = std::max(1, atoi(e));
         for (int k = 1; k <= nck; ++k) cks.push_back((max_key * k) / nck);
+        // extra checkpoints one raster-outer step apart before the end shrink
+        // the bands that can only leave after the last wave
+        int ntail = 0;
+        if (const char* e = getenv("CCW_STREAM_TAIL")) ntail = std::max(0, atoi(e));
+        for (int k = 1; k <= ntail; ++k) cks.push_back(max_key - k * keymul);
         std::vector<int> done(n_real, 0);  // raster-outer extent already emitted
         long long off = 0;
         for (int w = 0; w <= max_key; ++w) {
