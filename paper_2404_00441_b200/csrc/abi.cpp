@@ -443,6 +443,7 @@ void ccw_ti_destroy(ccw_ti* ti) {
     ccwgpu::cache_free(ti->d_scr);
     for (auto& kv : ti->im2col) ccwgpu::cache_free(kv.second);
     for (auto& kv : ti->nnmap) ccwgpu::cache_free(kv.second);
+    for (auto& kv : ti->umap) ccwgpu::cache_free(kv.second);
     delete ti;
 }
 

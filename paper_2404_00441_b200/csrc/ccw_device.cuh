@@ -107,6 +107,9 @@ struct SimParams {
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
     int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)
     const int4* mtab;        // fast select: mask rows and run groups per mask variant
+    const int8_t* umap;      // fast select: [8 mask variants][npos] uniform class of each window --
+                             // the facies every masked coarse block is made of (pure blocks), -1 if
+                             // none; same class => bit-identical fp64 score (null: off)
     const int32_t* nnmap;    // normalized screen: [8 mask variants][npos] sum over mask and
                              // channels of squared TI block counts (null otherwise)
     HelpBoard* hb;           // shared rescoring board of this launch (null: off)

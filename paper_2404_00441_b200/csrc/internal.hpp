@@ -245,6 +245,7 @@ struct ccw_ti {
     float* d_scr = nullptr;      // nscr*hc*wc
     std::map<int, int8_t*> im2col;  // per template size Tc: npos x kpad int8 (tcgen05 screen)
     std::map<std::pair<int, int>, int32_t*> nnmap;  // per (Tc, OVc): normalized-screen norms
+    std::map<std::pair<int, int>, int8_t*> umap;    // per (Tc, OVc): uniform-window classes (8 mask variants)
     uint64_t key = 0;  // content key (hash of cells + shape) for per-context plan memory
 };
 

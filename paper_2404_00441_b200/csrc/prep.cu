@@ -145,4 +145,64 @@ const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
     return m;
 }
 
+// Pure coarse blocks: the facies all B x B fine cells of the block hold, -1 if mixed.
+__global__ void pure_block_kernel(const uint8_t* __restrict__ codes, int w, int hc, int wc, int B,
+                                  int8_t* __restrict__ out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= hc * wc) return;
+    const int br = b / wc, bc = b - br * wc;
+    const uint8_t* c0 = codes + static_cast<size_t>(br) * B * w + static_cast<size_t>(bc) * B;
+    const int f = c0[0];
+    bool pure = f < 16;
+    for (int r = 0; r < B && pure; ++r)
+        for (int c = 0; c < B; ++c) pure &= c0[static_cast<size_t>(r) * w + c] == f;
+    out[b] = pure ? static_cast<int8_t>(f) : static_cast<int8_t>(-1);
+}
+
+// U[v][p]: the facies f when every coarse block of window p under mask
+// variant v is pure f, else -1.  Such windows have the all-f block's apex
+// values on every masked cell in every channel (indicator or raw codes), so
+// their fp64 scores (matcher.hpp:64-81) are bit-identical for any template.
+__global__ void uniform_map_kernel(const int8_t* __restrict__ pure, int wc, int Tc, int OVc, int out_w, int npos,
+                                   int8_t* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int v = blockIdx.y;
+    if (p >= npos) return;
+    const int shape = v < 4 ? kL : (v < 6 ? kVertical : kHorizontal);
+    const int vleft = v < 4 ? (v >> 1) : (v < 6 ? v - 4 : 0);
+    const int htop = v < 4 ? (v & 1) : (v < 6 ? 0 : v - 6);
+    const int x = p / out_w, y = p - x * out_w;
+    int cls = -2;  // (no masked cell seen yet)
+    for (int s = 0; s < Tc && cls != -1; ++s) {
+        int t0, t1;
+        mask_row_run(shape, vleft, htop, Tc, OVc, s, t0, t1);
+        for (int t = t0; t < t1; ++t) {
+            const int f = pure[static_cast<size_t>(x + s) * wc + y + t];
+            if (f < 0 || (cls >= 0 && f != cls)) {
+                cls = -1;
+                break;
+            }
+            cls = f;
+        }
+    }
+    out[static_cast<size_t>(v) * npos + p] = static_cast<int8_t>(cls < 0 ? -1 : cls);
+}
+
+// Uniform-window classes of a TI for template Tc / overlap OVc, cached on the TI.
+const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
+    const auto key = std::make_pair(Tc, OVc);
+    auto it = ti->umap.find(key);
+    if (it != ti->umap.end()) return it->second;
+    const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1, npos = out_h * out_w;
+    const size_t nb = static_cast<size_t>(ti->hc) * ti->wc;
+    int8_t* m = static_cast<int8_t*>(cache_alloc(ti->device, 8 * static_cast<size_t>(npos) + nb));
+    int8_t* pure = m + 8 * static_cast<size_t>(npos);
+    pure_block_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(ti->d_codes, ti->w, ti->hc, ti->wc,
+                                                                              1 << ti->J, pure);
+    uniform_map_kernel<<<dim3((npos + 255) / 256, 8), 256, 0, st>>>(pure, ti->wc, Tc, OVc, out_w, npos, m);
+    CCW_CUDA(cudaGetLastError());
+    ti->umap[key] = m;
+    return m;
+}
+
 }  // namespace ccwgpu

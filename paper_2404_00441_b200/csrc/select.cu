@@ -965,7 +965,54 @@ struct FastSmem {
     int misc[8];
     int tqa[32 * kTM];      // cooperative scan: the tiles whose maximum reaches M_K
     int nq, lcnt, lover;    // their count, the list length, list overflow
+    // uniform-window reduction of a large equal-score group (uniform_reduce)
+    int utmp[SC_LC];
+    signed char ucl[SC_LC], ucl2[SC_LC];
+    int urep[16], urs[16], ucnt[2];
 };
+
+// Large equal-score groups are often windows made entirely of pure blocks of
+// one facies (a background region): their fp64 scores are bit-identical
+// (P.umap), so one representative per facies is rescored.  Reorders S.tie[0,
+// g) so the members to rescore come first and returns their count; the others'
+// keys are copied from their representative by uniform_fill.  The ranking is by
+// (key, position), so the order of S.tie is free.
+constexpr int UD_MIN = 8;
+__device__ CCW_COLD int uniform_reduce(const SimParams& P, FastSmem& S, int g, int var) {
+    const int tid = threadIdx.x;
+    const int8_t* um = P.umap + static_cast<size_t>(var) * P.npos;
+    if (tid < 16) S.urep[tid] = INT_MAX;
+    if (tid < 2) S.ucnt[tid] = 0;
+    __syncthreads();
+    for (int e = tid; e < g; e += FS_T) {
+        const int c = __ldg(um + S.tie[e]);
+        S.ucl[e] = static_cast<signed char>(c);
+        if (c >= 0) atomicMin(&S.urep[c], e);
+    }
+    __syncthreads();
+    for (int e = tid; e < g; e += FS_T) {
+        const int c = S.ucl[e];
+        if (c < 0 || S.urep[c] == e) {
+            const int k = atomicAdd(&S.ucnt[0], 1);
+            S.utmp[k] = S.tie[e];
+            if (c >= 0) S.urs[c] = k;
+        } else {
+            const int d = g - 1 - atomicAdd(&S.ucnt[1], 1);
+            S.utmp[d] = S.tie[e];
+            S.ucl2[d] = static_cast<signed char>(c);
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < g; e += FS_T) S.tie[e] = S.utmp[e];
+    const int gr = S.ucnt[0];
+    __syncthreads();
+    return gr;
+}
+
+__device__ CCW_COLD void uniform_fill(FastSmem& S, int gr, int g) {
+    for (int j = gr + threadIdx.x; j < g; j += FS_T) S.key[j] = S.key[S.urs[S.ucl2[j]]];
+    __syncthreads();
+}
 
 // Cooperative scan (ntiles <= 32 * kTM), step 1 on warp 0: M_K (as scan_job)
 // and the queue of tiles whose maximum reaches it, in tile order.
@@ -1533,9 +1580,11 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
 #ifdef CCW_DBG_TAIL
                 const long long q0 = clock64();
 #endif
-                if (!(P.hb && g >= P.help_min &&
-                      hb_rescore(P, S, slot, g, ngrp, mask_variant(jb.shape, jb.vleft, jb.htop))))
-                    rescore_keys(P, S, tmg, nr, ngrp, S.tie, g, S.key);
+                const int var = mask_variant(jb.shape, jb.vleft, jb.htop);
+                const int gr = P.umap && g >= UD_MIN ? uniform_reduce(P, S, g, var) : g;
+                if (!(P.hb && gr >= P.help_min && hb_rescore(P, S, slot, gr, ngrp, var)))
+                    rescore_keys(P, S, tmg, nr, ngrp, S.tie, gr, S.key);
+                if (gr < g) uniform_fill(S, gr, g);
 #ifdef CCW_DBG_TAIL
                 if (tid == 0 && P.stats && g < 8) {
                     atomicAdd(&P.stats[37], 1ull);

@@ -721,6 +721,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             ctx->mtab_key = key;
         }
         P.mtab = d_mt;
+        if (!getenv("CCW_NO_UNIFORM")) P.umap = ti_umap(ti, Tc, OVc, st);
     }
     P.kpad = kpad;
     P.ntiles = ntiles;

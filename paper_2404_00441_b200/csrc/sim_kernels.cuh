@@ -304,6 +304,7 @@ __global__ void build_jobs_kernel(SchedParams S, Job* __restrict__ jobs);
 __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0);
 __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0);
 const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
+const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 // ccf_direct.cu
 size_t ccf_smem_bytes(int Tc, int nscr);
 __global__ void ccf_direct_kernel(SimParams P, const Job* __restrict__ jobs, int job0);

@@ -205,6 +205,8 @@ def test_shared_rescoring(oracle, help_min, monkeypatch):
     threshold makes most unconditional picks go that way.  Bit-exact."""
     from paper_2404_00441_b200 import synth
     monkeypatch.setenv("CCW_HELP_MIN", str(help_min))
+    # (uniform-window reduction off: it would shrink the groups below help_min)
+    monkeypatch.setenv("CCW_NO_UNIFORM", "1")
     ti_a = synth.channel_ti(200, 200, 31, scale=5.0)
     ti = cs.CategoricalGrid(200, 200, 2, ti_a)
     d = dict(sg_height=260, sg_width=230, template_size=32, overlap=8, dwt_level=2, candidates=5)
@@ -438,3 +440,25 @@ def cfg_dict(cfg):
     return dict(sg_height=c.sg_height, sg_width=c.sg_width, template_size=c.template_size,
                 overlap=c.overlap, dwt_level=c.dwt_level, candidates=c.candidates,
                 scoring=c.scoring, facies_mode=c.facies_mode, min_cut=bool(c.min_cut))
+
+
+def test_uniform_window_groups(oracle):
+    """Large background regions: placements whose overlap is all background
+    tie hundreds of pure-background windows at the top score.  The fast select
+    rescores one representative per uniform facies (their fp64 scores are
+    bit-identical) -- the realizations must still equal the oracle's."""
+    rng = np.random.default_rng(31)
+    ti_a = np.zeros((256, 256), np.uint8)
+    for _ in range(40):  # lenses of facies 1-2 on a background of facies 0
+        r, c = rng.integers(0, 240, 2)
+        h, w = rng.integers(4, 24, 2)
+        ti_a[r:r + h, c:c + w] = rng.integers(1, 3)
+    ti = cs.CategoricalGrid(256, 256, 3, ti_a)
+    for k, mode in ((5, "indicator"), (3, "raw_codes"), (8, "indicator")):
+        d = dict(sg_height=200, sg_width=180, template_size=32, overlap=8, dwt_level=2, candidates=k,
+                 facies_mode=1 if mode == "raw_codes" else 0)
+        cfg = to_cfg(d)
+        seeds = [int(s) for s in rng.integers(0, 2**63, 3)]
+        for s, r in zip(seeds, cs.simulate_batch(ti, cfg, seeds)):
+            o = oracle.simulate_one(ti_a, 3, pyoracle.Cfg(**d), None, seed=s)
+            assert np.array_equal(r.realization.cells, o["realization"]), (k, mode, s)
