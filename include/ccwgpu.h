@@ -142,6 +142,12 @@ CCW_API ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops);
 /* Dense int8 tensor-core rate (TOPS) of the CCF screen's tcgen05 MMA shape
  * (kind::i8, M=128, N=256, cta_group::1), measured with an in-library probe. */
 CCW_API ccw_status ccw_measure_i8_peak(ccw_ctx* ctx, double* tops);
+/* The CCF screen kernel alone (tcgen05 int8 implicit GEMM) on njobs
+ * placements' weights for template_size against the TI's im2col, `iters`
+ * back-to-back launches with no dependency: milliseconds per launch.  The
+ * throughput the kernel reaches when it is not on the wave chain. */
+CCW_API ccw_status ccw_measure_ccf_screen(ccw_ctx* ctx, ccw_ti* ti, int template_size, int njobs,
+                                          int iters, double* ms_per_launch);
 
 /* ------------------------------------------- position sharding --------- */
 /* Candidate-position sharding of one simulation across ranks.

@@ -336,6 +336,18 @@ ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops) {
     return guarded(ctx, [&] { *tflops = ccwgpu::measure_ffma_peak(ctx); });
 }
 
+ccw_status ccw_measure_ccf_screen(ccw_ctx* ctx, ccw_ti* ti, int template_size, int njobs, int iters,
+                                  double* ms_per_launch) {
+    if (!ctx || !ti || !ms_per_launch) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        const int Tc = template_size >> ti->J;
+        if (Tc < 1 || Tc > std::min(ti->hc, ti->wc) || njobs < 1 || iters < 1)
+            throw Fail(CCW_ERR_CONFIG, "ccw_measure_ccf_screen: bad template size, job or iteration count");
+        if (ti->nscr < 1) throw Fail(CCW_ERR_CONFIG, "ccw_measure_ccf_screen: this TI has no screen planes");
+        *ms_per_launch = ccwgpu::measure_ccf_screen(ti, Tc, njobs, iters, ctx->stream);
+    });
+}
+
 ccw_status ccw_measure_i8_peak(ccw_ctx* ctx, double* tops) {
     if (!ctx || !tops) return CCW_ERR_GENERIC;
     return guarded(ctx, [&] { *tops = ccwgpu::measure_i8_peak(ctx->stream); });

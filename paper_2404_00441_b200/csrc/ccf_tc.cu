@@ -495,6 +495,38 @@ double measure_i8_peak(cudaStream_t st) {
     return best;
 }
 
+// Throughput of the screen kernel alone: `njobs` placements' worth of int8
+// weights (all ones) against the TI's im2col, `iters` back-to-back launches
+// with no dependency between them.  Milliseconds per launch.
+double measure_ccf_screen(ccw_ti* ti, int Tc, int njobs, int iters, cudaStream_t st) {
+    const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1, npos = out_h * out_w;
+    const int kpad = tc_kpad(ti->nscr, Tc), sld = (npos + 3) & ~3;
+    const int8_t* X = ti_im2col(ti, Tc, st);
+    int8_t* W = nullptr;
+    int32_t *sc = nullptr, *tmx = nullptr;
+    CCW_CUDA(cudaMalloc(&W, static_cast<size_t>(njobs) * kpad));
+    CCW_CUDA(cudaMalloc(&sc, sizeof(int32_t) * static_cast<size_t>(njobs) * sld));
+    CCW_CUDA(cudaMalloc(&tmx, sizeof(int32_t) * static_cast<size_t>(njobs) * tc_tiles(npos)));
+    CCW_CUDA(cudaMemsetAsync(W, 1, static_cast<size_t>(njobs) * kpad, st));
+    const TcPlan pl = plan_ccf_tc(W, njobs, X, npos, kpad);
+    cudaEvent_t a, b;
+    CCW_CUDA(cudaEventCreate(&a));
+    CCW_CUDA(cudaEventCreate(&b));
+    launch_ccf_tc(pl, npos, sld, kpad, njobs, sc, tmx, st);  // warm-up
+    CCW_CUDA(cudaEventRecord(a, st));
+    for (int i = 0; i < iters; ++i) launch_ccf_tc(pl, npos, sld, kpad, njobs, sc, tmx, st);
+    CCW_CUDA(cudaEventRecord(b, st));
+    CCW_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    CCW_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(W);
+    cudaFree(sc);
+    cudaFree(tmx);
+    return ms / iters;
+}
+
 TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad) {
     TcPlan pl;
     pl.ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);

@@ -36,6 +36,8 @@ int tc_num_sms();
 const int8_t* ti_im2col(ccw_ti* ti, int Tc, cudaStream_t st);
 // Measured dense int8 tcgen05 rate of the screen's MMA shape (TOPS).
 double measure_i8_peak(cudaStream_t st);
+// The screen kernel alone on njobs placements, back-to-back launches (ms per launch).
+double measure_ccf_screen(ccw_ti* ti, int Tc, int njobs, int iters, cudaStream_t st);
 
 // TMA descriptors, built once per simulate call and group.
 struct TcPlan {
