@@ -133,6 +133,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 // One (job tile, half position tile) of accumulators, drained from TMEM:
 // the exact scores and the tile maximum.  stage = this warp's 4 KB of shared
 // memory (32 rows x 128 B, 16-byte chunks swizzled by row) for the transpose.
+template <bool S16>
 __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int m0, int n0,
                                             int warp, int lane, uint32_t stage) {
     const int q = warp & 3;
@@ -189,8 +190,15 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
             const int jr = m0 + q * 32 + row;
             // rows are padded to sld (a multiple of 4) >= npos: a chunk that
             // starts inside the row is stored whole
-            if (jr < a.nj && pos < a.npos)
-                *reinterpret_cast<int4*>(a.scores + static_cast<size_t>(jr) * a.sld + pos) = v;
+            if (jr < a.nj && pos < a.npos) {
+                if (S16) {  // (exact: every score fits int16, checked on the host)
+                    const uint2 h = make_uint2((static_cast<uint32_t>(v.x) & 0xffffu) | (static_cast<uint32_t>(v.y) << 16),
+                                               (static_cast<uint32_t>(v.z) & 0xffffu) | (static_cast<uint32_t>(v.w) << 16));
+                    *reinterpret_cast<uint2*>(reinterpret_cast<int16_t*>(a.scores) + static_cast<size_t>(jr) * a.sld + pos) = h;
+                } else {
+                    *reinterpret_cast<int4*>(a.scores + static_cast<size_t>(jr) * a.sld + pos) = v;
+                }
+            }
         }
         __syncwarp();
     }
@@ -205,6 +213,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
 #ifndef CCW_TC_MINB
 #define CCW_TC_MINB 1
 #endif
+template <bool S16>  // int16 score rows (a separate instance keeps the int32 one unchanged)
 __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
     ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   TcArgs a) {
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
             if (lt == 0 && warp == 2 && lane == 0) probe(4);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int m0 = (t % n_mt) * kM, n0 = (t / n_mt) * kN;
-            tc_epilogue(a, tmem + b * kN, m0, n0, warp, lane, epi_stage + (warp - 2) * 4096);
+            tc_epilogue<S16>(a, tmem + b * kN, m0, n0, warp, lane, epi_stage + (warp - 2) * 4096);
             if (lt == 0 && lane == 0) probe(5);  // summed over the 8 epilogue warps
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -531,19 +540,22 @@ TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
     TcPlan pl;
     pl.ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
     pl.mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
-    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ccf_tc_smem_bytes())));
+    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ccf_tc_smem_bytes())));
     return pl;
 }
 
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* tmax, cudaStream_t st, unsigned long long* tl, int tmax_ld) {
+                   int32_t* tmax, cudaStream_t st, unsigned long long* tl, int tmax_ld, int s16) {
     TcArgs a;
     a.nj = nj;
     a.npos = npos;
     a.sld = sld;
     a.nk = (kpad + kKC - 1) / kKC;
     a.ntiles = tmax_ld >= 0 ? tmax_ld : tc_tiles(npos);  // (row stride of tmax)
+    a.s16 = s16;
     a.scores = scores;
     a.tmax = tmax;
     a.probe = tc_probe_buffer;
@@ -553,7 +565,10 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     const int slots = tc_num_sms() * CCW_TC_MINB;
     a.epi_in_ring = ntot <= slots && !getenv("CCW_TC_EPI_SEPARATE");
     dim3 grid(std::min(ntot, a.epi_in_ring ? slots : tc_num_sms()));
-    launch_pdl(ccf_tc_kernel, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
+    if (s16)
+        launch_pdl(ccf_tc_kernel<true>, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
+    else
+        launch_pdl(ccf_tc_kernel<false>, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
 }
 
 int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // tile maxima per score row

@@ -23,6 +23,7 @@ struct TcArgs {
     int32_t* tmax;     // [nj][ntiles] maximum score of each tile
     unsigned long long* probe;  // debug phase clocks (null unless CCW_TC_PROBE)
     unsigned long long* tl;     // debug timeline slot (null unless CCW_TIMELINE)
+    int s16;                    // score rows as int16 (exact: the host checks |S| < 2^15)
     int epi_in_ring;            // every CTA drains one tile: the epilogue's transpose
                                 // staging reuses the (then idle) TMA ring
 };
@@ -46,6 +47,7 @@ struct TcPlan {
 TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, int kpad);
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
                    int32_t* tmax, cudaStream_t st, unsigned long long* tl = nullptr,
-                   int tmax_ld = -1);  // tmax row stride (default: this launch's tile count)
+                   int tmax_ld = -1,   // tmax row stride (default: this launch's tile count)
+                   int s16 = 0);       // store int16 score rows
 
 }  // namespace ccwgpu

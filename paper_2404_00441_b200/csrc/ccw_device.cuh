@@ -95,6 +95,7 @@ struct SimParams {
     double* tm64;            // nch*Tc*Tc reference-order OR apex values
     int32_t* scores;         // npos screen scores per job, row stride sld (16-byte rows)
     int sld;
+    int s16;                 // fast select: score rows hold int16 (exact when |S| < 2^15, host-checked)
     int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
     // fused OR prep: the select of wave w prepares the placements of wave w+1
     // once both of their wave-w dependencies have pasted (null: separate launch)
@@ -134,6 +135,23 @@ struct SimParams {
     int32_t* chosen;         // per job (global job id): fr, fc
     uint8_t* pasted;         // optional trace of pasted patches (global job id * T*T)
 };
+
+// Screen scores of job slot `slot` (int32 rows, or int16 rows when P.s16):
+// four at p0 (a multiple of 4), or one.
+template <bool S16>
+__device__ __forceinline__ int4 load_score4(const SimParams& P, int slot, int p0) {
+    const size_t o = static_cast<size_t>(slot) * P.sld + p0;
+    if (S16) {
+        const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const int16_t*>(P.scores) + o);
+        return make_int4(static_cast<int16_t>(u.x & 0xffffu), static_cast<int16_t>(u.x >> 16),
+                         static_cast<int16_t>(u.y & 0xffffu), static_cast<int16_t>(u.y >> 16));
+    }
+    return *reinterpret_cast<const int4*>(P.scores + o);
+}
+__device__ __forceinline__ int load_score(const SimParams& P, int slot, size_t p) {
+    const size_t o = static_cast<size_t>(slot) * P.sld + p;
+    return P.s16 ? static_cast<int>(reinterpret_cast<const int16_t*>(P.scores)[o]) : P.scores[o];
+}
 
 // Row-major run of the coarse overlap mask in template row s: [t0, t1).
 // Every simulator mask (strip or L, simulator.hpp:194-215) has at most one

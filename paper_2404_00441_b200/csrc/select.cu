@@ -797,11 +797,11 @@ __device__ __forceinline__ int scan_finish(const SimParams& P, const ScanWarp& W
 // exact K-th score S_K and the candidate positions (>= S_K) into out[].
 // Returns the candidate count, or -1 when the list overflowed (then every
 // window >= mk_out must be rescored -- a superset, still exact).
+template <bool S16>
 __device__ CCW_COLD int scan_job(const SimParams& P, int slot, ScanWarp& W, int* out, int& mk_out,
                                         long long* sclk, int* out_s = nullptr) {
     const int lane = threadIdx.x & 31;
     const int K = P.K;
-    const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
     const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
     // 1. M_K = K-th largest tile maximum (with multiplicity): a lower bound of
     //    the K-th largest screen score S_K (the K best tiles each hold a
@@ -851,7 +851,7 @@ __device__ CCW_COLD int scan_job(const SimParams& P, int slot, ScanWarp& W, int*
 #pragma unroll
             for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
             if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
-                const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
+                const int4 a4 = load_score4<S16>(P, slot, p0);
                 v[u][0] = a4.x;
                 v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
                 v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
@@ -1046,9 +1046,9 @@ __device__ __forceinline__ void coop_head(const SimParams& P, int slot, FastSmem
 // round trip per warp) appended to the shared (score, position) list.  The
 // list order is irrelevant: every later ranking is a total order on (S, fp64
 // key, index).  Overflow iff the list would exceed SC_LC, as in scan_job.
+template <bool S16>
 __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem& S) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
     const int nq = S.nq, mk = S.misc[1];
     for (int q0 = wid * SC_TB; q0 < nq; q0 += (FS_T / 32) * SC_TB) {
         int tl[SC_TB], v[SC_TB][4];
@@ -1060,7 +1060,7 @@ __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem
 #pragma unroll
             for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
             if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
-                const int4 a4 = *reinterpret_cast<const int4*>(sc + p0);
+                const int4 a4 = load_score4<S16>(P, slot, p0);
                 v[u][0] = a4.x;
                 v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
                 v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
@@ -1416,6 +1416,7 @@ __device__ CCW_COLD bool hb_rescore(const SimParams& P, FastSmem& S, int slot, i
 #ifndef CCW_FS_MINB
 #define CCW_FS_MINB 4
 #endif
+template <bool S16>  // int16 score rows (P.s16); one instance each keeps the code lean
 __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     select_fast_kernel(const __grid_constant__ SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
     __shared__ FastSmem S;
@@ -1461,7 +1462,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                 coop_head(P, slot, S);
                 sclk[1] = clock64();
             } else {
-                const int n = scan_job(P, slot, S.sw, S.cidx, mk, sclk, S.cs);
+                const int n = scan_job<S16>(P, slot, S.sw, S.cidx, mk, sclk, S.cs);
                 if (lane == 0) {
                     S.misc[0] = n;
                     S.misc[1] = mk;
@@ -1489,7 +1490,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         }
         __syncthreads();
         if (coop) {
-            coop_list(P, slot, S);
+            coop_list<S16>(P, slot, S);
             __syncthreads();
             if (wid == 0) {
                 sclk[2] = clock64();
@@ -1665,13 +1666,12 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             fast_batch(P, S, tmg, nr, ngrp, n, ntop, K);
         } else {
             // list overflow without the bulk kernel: every window >= M_K, in batches
-            const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
             const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
             int cnt = 0;
             for (int t = 0; t < P.ntiles; ++t) {
                 if (tmx[t] < mk) continue;  // uniform
                 const int p = t * kTcTile + tid;  // FS_T == kTcTile
-                const bool q = p < P.npos && sc[p] >= mk;
+                const bool q = p < P.npos && (S16 ? static_cast<int>(reinterpret_cast<const int16_t*>(P.scores)[static_cast<size_t>(slot) * P.sld + p]) : P.scores[static_cast<size_t>(slot) * P.sld + p]) >= mk;
                 const unsigned bal = __ballot_sync(0xffffffffu, q);
                 if (lane == 0) S.wc[wid] = __popc(bal);
                 __syncthreads();
@@ -1756,6 +1756,9 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     tl_mark(P.tl, 1);
 }
 
+template __global__ void select_fast_kernel<false>(const __grid_constant__ SimParams, const Job* __restrict__, int, int);
+template __global__ void select_fast_kernel<true>(const __grid_constant__ SimParams, const Job* __restrict__, int, int);
+
 __global__ void __launch_bounds__(BK_T, 1)
     select_bulk_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj, int S) {
     extern __shared__ __align__(16) unsigned char bk_sm[];
@@ -1787,7 +1790,6 @@ __global__ void __launch_bounds__(BK_T, 1)
     double* mk = reinterpret_cast<double*>(misc + 320);    // [BK_SMAX * kTcQ] merge keys
     int* mi = reinterpret_cast<int*>(misc + 320 + 8 * BK_SMAX * kTcQ);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int32_t* sc = P.scores + static_cast<size_t>(slot) * P.sld;
     const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
     const double* tm = P.tm64 + static_cast<size_t>(slot) * nch * Tc * Tc;
     long long clk_stage = 0, clk_comp = 0;
@@ -1838,7 +1840,7 @@ __global__ void __launch_bounds__(BK_T, 1)
                 v[i] = INT_MIN;
                 if (e < nb) {
                     const int lx = e / bya, ly = e - lx * bya;
-                    v[i] = sc[(xb + lx) * P.out_w + yb + ly];
+                    v[i] = load_score(P, slot, static_cast<size_t>(xb + lx) * P.out_w + yb + ly);
                 }
             }
             int c = 0;

@@ -723,6 +723,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.mtab = d_mt;
         if (!getenv("CCW_NO_UNIFORM")) P.umap = ti_umap(ti, Tc, OVc, st);
     }
+    // int16 score rows for the fast select when every screen score fits:
+    // |S'| <= mask cells * (largest weight) * (largest block statistic)
+    const bool s16 = warp_select && mask_cells * static_cast<double>(maxv) * maxv < 32767.0 &&
+                     !getenv("CCW_NO_S16");
+    P.s16 = s16 ? 1 : 0;
     P.kpad = kpad;
     P.ntiles = ntiles;
     P.stats = d_stats;
@@ -1239,7 +1244,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                 if (use_tc) ccf_mma_flop += 2.0 * kpad * static_cast<double>(sp.n) * nj;
                             }
                             if (shard_fast) {
-                                launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, QV,
+                                launch_pdl(select_fast_kernel<false>, dim3(nj), dim3(FS_T), 0, gs, QV,
                                            static_cast<const Job*>(d_jobs), static_cast<int>(j0), nj);
                                 if (QV.defer) {
                                     launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, QV,
@@ -1300,7 +1305,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         if (skip_ccf) {
                         } else if (use_tc) {
                             launch_ccf_tc(tcplans[g][par], npos, sld, kpad, nj, Q.scores, Q.tmax, gs,
-                                          tl_next(w, g, 1));
+                                          tl_next(w, g, 1), -1, Q.s16);
                         } else {
                             launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, ccf_grid_xy.y, nj),
                                        dim3(CCF_THREADS), ccf_smem, gs, Q,
@@ -1343,7 +1348,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         Q.hs_reset = d_hslots + (2 * g + (1 - hb_par[g])) * maxj;
                         hb_par[g] ^= 1;
                     }
-                    launch_pdl(select_fast_kernel, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
+                    launch_pdl(Q.s16 ? select_fast_kernel<true> : select_fast_kernel<false>, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
                                static_cast<int>(j0), nj);
                     if (Q.defer && !first_wave) {
                         Q.tl = tl_next(w, g, 5);

@@ -311,6 +311,7 @@ __global__ void ccf_direct_kernel(SimParams P, const Job* __restrict__ jobs, int
 // select.cu
 __global__ void select_paste_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int use_screen);
 __global__ void shard_merge_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nshards);
+template <bool S16>
 __global__ void select_fast_kernel(const __grid_constant__ SimParams P, const Job* __restrict__ jobs, int job0, int nj);
 __global__ void select_bulk_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj, int S);
 
