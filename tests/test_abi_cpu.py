@@ -120,3 +120,22 @@ def test_device_calls_fail_loudly_without_gpu():
         pass
     with pytest.raises(cs.DeviceError):
         cs.Device(0)
+
+
+def test_nccl_unique_id_host_side():
+    """The position-sharding rendezvous (ccw_nccl_unique_id: libnccl.so.2 is
+    dlopen'ed on first use) works without a GPU: 128 bytes, fresh per call."""
+    from paper_2404_00441_b200 import ccwsim as cs
+    a, b = cs.nccl_unique_id(), cs.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
+
+
+def test_position_shard_arguments_validated():
+    """ccw_ctx_set_position_shards rejects bad ranks before touching a device
+    (a null context returns the generic error code, never crashes)."""
+    import ctypes as C
+    from paper_2404_00441_b200 import _abi
+    L = _abi.lib()
+    assert L.ccw_ctx_set_position_shards(None, 2, 0, None, 1) == 7
+    ms = C.c_double()
+    assert L.ccw_measure_ccf_screen(None, None, 64, 1, 1, C.byref(ms)) == 7
