@@ -317,7 +317,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32(exact-int)+f64", "data": "synthetic",
+            "dtype": "i8xi8->i32 screen + f64 rescoring", "data": "synthetic",
             "config": {"workload": WORKLOAD, "realizations_per_gpu": REAL_PER_GPU,
                        "parallelism": f"realization shards x{world}",
                        "l2": "flushed before each timed step (256 MiB write, outside events)",
@@ -457,7 +457,7 @@ def run_single(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32(exact-int)+f64",
+                "scaling": "strong", "vs_baseline": None, "dtype": "i8xi8->i32 screen + f64 rescoring",
                 "data": "synthetic",
                 "config": {"workload": SINGLE_WORKLOAD, "position_shards": world * args.virtual_shards,
                            "exchange": "ncclAllGather" if uid is not None else
