@@ -16,9 +16,19 @@ A step = one batched simulation of those 100 realizations.
   e2e   : the same metric through the public C-ABI call with host buffers:
           ccw_ti_create from host bytes (H2D + pyramid) + ccw_simulate into
           pinned host memory (D2H of every realization), wall clock per step.
+  parity: after the timed region, the first 8 realizations of the last timed
+          call are checked bit for bit against the compiled reference
+          (oracle/_ref, the unmodified reference headers) with the same seeds.
+  config2: at N=1 the same measurements on BASELINE config 2 (TI 2000^2,
+          SG 4000^2, T96 OV24 J3 K1, 1 % hard data, 8 realizations), the
+          largest single-GPU configuration, nested in the same line.
 Rank 0 prints one JSON line.  --impl reference times the reference's own CPU
 implementation (oracle/_ref: the unmodified reference headers) on the host
 cores on a bounded sample of the same workload.
+
+--gpus N without torchrun: bench.py spawns the N ranks itself (one process
+per GPU, NCCL over 127.0.0.1), so `python bench.py --gpus N` and
+`torchrun --nproc-per-node N bench.py --gpus N` measure the same thing.
 """
 from __future__ import annotations
 
@@ -122,20 +132,67 @@ def load_traffic():
     return None
 
 
-def cpu_reference_rate(ti, nf, cfg, n_real, workers):
-    """cells/s of the compiled reference (oracle/_ref) on n_real realizations."""
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_impl():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-    impl, kind = (pyoracle.reference(), "reference") if pyoracle.reference_available() else \
-        (pyoracle.restatement(), "port")
+    if pyoracle.reference_available():
+        return pyoracle, pyoracle.reference(), "reference"
+    return pyoracle, pyoracle.restatement(), "port"
+
+
+def check_parity(got, ti, nf, cfg, seeds, hd=None, n_check=8):
+    """Bit-exact check of benchmarked realizations against the compiled
+    reference (oracle/_ref), same seeds, host threads in parallel."""
+    from concurrent.futures import ThreadPoolExecutor
+    pyoracle, impl, kind = reference_impl()
+    c = pyoracle.Cfg(sg_height=cfg.sg_height, sg_width=cfg.sg_width,
+                     template_size=cfg.template_size, overlap=cfg.overlap,
+                     dwt_level=cfg.dwt_level, candidates=cfg.candidates)
+    idx = list(range(min(n_check, len(seeds))))
+
+    def one(r):
+        o = impl.simulate_one(ti, nf, c, hd, seed=int(seeds[r]))
+        return bool(np.array_equal(got[r], o["realization"]))
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(len(idx), os.cpu_count() or 1)) as ex:
+        ok = list(ex.map(one, idx))
+    return {"checked": len(idx), "equal": all(ok), "mismatched": [r for r, v in zip(idx, ok) if not v],
+            "against": f"oracle/_ref ({kind}: compiled unmodified reference headers)" if kind == "reference"
+                       else "oracle restatement (reference not built)",
+            "what": "realizations 0..%d of the last timed call, same seeds" % (len(idx) - 1),
+            "seconds": round(time.perf_counter() - t0, 2)}
+
+
+def cpu_reference_rate(ti, nf, cfg, n_real, workers, hd=None, master=None):
+    """cells/s of the compiled reference (oracle/_ref) on n_real realizations
+    (simulate_ensemble: seeds mix64(master, r+1)); also returns them."""
+    pyoracle, impl, kind = reference_impl()
     c = pyoracle.Cfg(sg_height=cfg.sg_height, sg_width=cfg.sg_width,
                      template_size=cfg.template_size, overlap=cfg.overlap,
                      dwt_level=cfg.dwt_level, candidates=cfg.candidates,
-                     n_realizations=n_real, master_seed=cfg.master_seed)
+                     n_realizations=n_real, master_seed=cfg.master_seed if master is None else master)
     t0 = time.perf_counter()
-    impl.simulate_ensemble(ti, nf, c, None, workers=workers)
+    out, _ = impl.simulate_ensemble(ti, nf, c, hd, workers=workers)
     dt = time.perf_counter() - t0
-    return n_real * cfg.sg_height * cfg.sg_width / dt, dt, kind
+    return n_real * cfg.sg_height * cfg.sg_width / dt, dt, kind, out
 
 
 def run_reference(args):
@@ -148,11 +205,11 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     sample = max(cores, 4)  # one realization per host thread per step
     for _ in range(args.warmup):
-        cpu_reference_rate(ti, 3, cfg, min(sample, 4), cores)
+        cpu_reference_rate(ti, 3, cfg, min(sample, 4), cores)[:3]
     rates, times = [], []
     kind = "reference"
     for _ in range(args.steps):
-        r, dt, kind = cpu_reference_rate(ti, 3, cfg, sample, cores)
+        r, dt, kind, _ = cpu_reference_rate(ti, 3, cfg, sample, cores)
         rates.append(r)
         times.append(dt)
     value = statistics.median(rates)
@@ -163,6 +220,7 @@ def run_reference(args):
             "impl": "reference",
             "config": {"workload": WORKLOAD, "sample_realizations_per_step": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "cpu_model": cpu_model(),
                              "sample": f"{sample} config-1 realizations per step, "
                                        f"simulate_ensemble(workers={cores})"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -237,13 +295,19 @@ def run_ours(args):
     cells = world * REAL_PER_GPU * sg * args.steps
     value = cells / (total_ms * 1e-3)
 
+    # parity: the last timed call's realizations against the compiled reference
+    got = d_out.view(REAL_PER_GPU, cfg.sg_height, cfg.sg_width).cpu().numpy()
+    parity = check_parity(got, ti_a, nf, cfg, seeds) if rank == 0 else None
+
     # profiling pass (separate from the timed region): per-launch CCF time
     dev.set_profiling(True)
     step_device()
     prof = dev.last_timing()
     dev.set_profiling(False)
     ccf_avg_ms = prof["ccf_ms"] / max(prof["ccf_launches"], 1)
-    flop_per_launch = prof["ccf_flop"] / max(prof["ccf_launches"], 1)
+    # SURVEY 8(d) numerator: 2 x F channels x positions x mask cells per placement
+    flop_per_launch = prof["ccf_flop_ref"] / max(prof["ccf_launches"], 1)
+    screen_per_launch = prof["ccf_flop"] / max(prof["ccf_launches"], 1)
     mma_per_launch = prof["ccf_mma_flop"] / max(prof["ccf_launches"], 1)
     tensor = prof["ccf_variant"] == 2
     peak = dev.measure_i8_peak() if tensor else dev.measure_fp32_peak()
@@ -258,21 +322,12 @@ def run_ours(args):
         dev.check(lib.ccw_measure_ccf_screen(dev.handle, tih.handle, cfg.template_size, nj_sa, 30,
                                              C.byref(sa_ms)))
         sa_s = sa_ms.value * 1e-3
-        sa_bytes = 4.0 * npos_sa * nj_sa + npos_sa * kpad_sa + nj_sa * kpad_sa
-        hbm = None
-        try:
-            hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
-        except Exception:
-            pass
         standalone = {
             "placements_per_launch": nj_sa, "us_per_launch": sa_ms.value * 1e3,
             "mma_tops_issued": 2.0 * kpad_sa * npos_sa * nj_sa / sa_s / 1e12,
-            "algorithmic_tops": 2.0 * 2 * 112 * npos_sa * nj_sa / sa_s / 1e12,
-            "tensor_frac_issued": 2.0 * kpad_sa * npos_sa * nj_sa / sa_s / 1e12 / peak if peak else None,
-            "bytes_per_launch": sa_bytes, "achieved_gbs": sa_bytes / sa_s / 1e9,
-            "hbm_peak_gbs": hbm, "hbm_frac": sa_bytes / sa_s / 1e9 / hbm if hbm else None,
-            "note": "int32 score rows (4 B per window x placement) dominate the bytes; at this batch the "
-                    "kernel is bound by that write stream, in the wave chain by latency"}
+            "algorithmic_tops": 2.0 * nf * 112 * npos_sa * nj_sa / sa_s / 1e12,
+            "frac": 2.0 * nf * 112 * npos_sa * nj_sa / sa_s / 1e12 / peak if peak else None,
+            "note": "same kernel, 1400 L-shaped placements' weights per launch, no wave dependency"}
     # end-to-end through the public API with host buffers
     h_out = torch.empty(REAL_PER_GPU * sg, dtype=torch.uint8).pin_memory()
     ti_host = np.ascontiguousarray(ti_a)
@@ -307,10 +362,14 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.skip_cpu:
         cores = os.cpu_count() or 1
         n = max(cores, 4)
-        rate, dt, kind = cpu_reference_rate(ti_a, nf, cfg, n, cores)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+        rate, dt, kind, _ = cpu_reference_rate(ti_a, nf, cfg, n, cores)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "cpu_model": cpu_model(),
                "sample": f"{n} config-1 realizations, simulate_ensemble(workers={cores}), "
                          f"{dt:.1f} s wall"}
+
+    config2 = None
+    if world == 1 and not args.skip_config2:
+        config2 = measure_config2(dev, lib, local, args, skip_cpu=args.skip_cpu)
 
     if rank == 0:
         line = {
@@ -327,20 +386,25 @@ def run_ours(args):
                          "achieved": achieved, "peak": peak,
                          "unit": "TOPS" if tensor else "TFLOP/s",
                          "frac": achieved / peak if peak else None,
-                         "peak_source": ("in-run tcgen05 kind::i8 probe, same MMA shape (MEASURED_PEAKS.json "
-                                         "has only bf16)") if tensor else
-                                        "in-run FFMA probe (MEASURED_PEAKS.json has no FP32 figure)",
+                         "peak_source": ("measured in this run: tcgen05 kind::i8 MMA probe, the screen's "
+                                         "M=128 N=256 shape, one CTA per SM (ccw_measure_i8_peak; "
+                                         "MEASURED_PEAKS.json has only bf16)") if tensor else
+                                        "measured in this run: FFMA probe (MEASURED_PEAKS.json has no FP32 figure)",
                          "algorithmic_ops_per_launch": flop_per_launch,
-                         "algorithmic_ops_note": "2 x (F-1) screen channels x positions x mask cells per placement "
-                                                 "(the reference's F-channel count is x F/(F-1))",
+                         "algorithmic_ops_note": "SURVEY 8(d): 2 x F channels x TI window positions x coarse "
+                                                 "mask cells per placement, summed over the launch's placements",
+                         "screen_ops_per_launch": screen_per_launch,
+                         "screen_ops_note": "the int8 screen computes F-1 channels (exact: one-hot TI)",
                          "mma_ops_issued_per_launch": mma_per_launch,
                          "avg_launch_ms": ccf_avg_ms,
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "traffic_source": traffic.get("source") if traffic else None,
                          "step_ms_profiled": prof["total_ms"],
                          "ccf_ms_per_step": prof["ccf_ms"], "select_ms_per_step": prof["select_ms"],
                          "fp64_windows_rescored": prof["rescored"],
                          "standalone": standalone},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(ti_host.nbytes + seeds.nbytes),
                     "d2h_bytes_per_step": d2h_bytes,
@@ -348,12 +412,106 @@ def run_ours(args):
                                 "unpacked by host threads into the caller's buffer"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
+            "config2": config2,
         }
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+CONFIG2 = ("config2: TI 2000x2000 binary channels, SG 4000x4000, T96 OV24 J3 K1, 1% hard data "
+           "(160,000 cells from a seeded realization), 8 realizations")
+
+
+def measure_config2(dev, lib, local, args, skip_cpu=False):
+    """BASELINE config 2, the largest single-GPU configuration: device-resident
+    cells/s, e2e through the C-ABI with host buffers, the compiled reference on
+    the host cores on the same 8 seeds (its outputs double as the parity check)."""
+    import torch
+    from paper_2404_00441_b200 import _abi, ccwsim as cs, synth
+    n_real = 8
+    ti_a = synth.config2_ti()
+    hd = synth.config2_hard_data(ti_a)
+    hd_a = np.ascontiguousarray(hd, np.int32)
+    grid = cs.CategoricalGrid(2000, 2000, 2, ti_a)
+    cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1, n_realizations=n_real, master_seed=MASTER)
+    tih = cs.TrainingImage(grid, cfg.dwt_level, "indicator", dev)
+    c = cfg.to_c()
+    seeds = np.array([cs.mix64(MASTER, r + 1) for r in range(n_real)], np.uint64)
+    sg = cfg.sg_height * cfg.sg_width
+    d_out = torch.empty(n_real * sg, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    diags = (_abi.DiagC * n_real)()
+    stream = torch.cuda.ExternalStream(dev.stream_ptr, device=torch.device("cuda", local))
+
+    def step_device():
+        dev.check(lib.ccw_simulate_device(dev.handle, tih.handle, C.byref(c),
+                                          seeds.ctypes.data_as(_abi.U64P), n_real,
+                                          hd_a.ctypes.data_as(_abi.I32P), hd_a.shape[0],
+                                          C.c_void_p(d_out.data_ptr()), diags))
+
+    for _ in range(max(args.warmup, 3)):
+        step_device()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            evs[k][0].record(stream)
+        step_device()
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    timing = dev.last_timing()
+    got = d_out.view(n_real, cfg.sg_height, cfg.sg_width).cpu().numpy()
+    mism = [d.pre_overwrite_mismatches for d in diags]
+    h_out = torch.empty(n_real * sg, dtype=torch.uint8).pin_memory()
+    ti_host = np.ascontiguousarray(ti_a)
+
+    def step_e2e():
+        h = C.c_void_p()
+        dev.check(lib.ccw_ti_create(dev.handle, ti_host.ctypes.data_as(_abi.U8P), 2000, 2000, 2,
+                                    cfg.dwt_level, 0, C.byref(h)))
+        dev.check(lib.ccw_simulate(dev.handle, h, C.byref(c), seeds.ctypes.data_as(_abi.U64P), n_real,
+                                   hd_a.ctypes.data_as(_abi.I32P), hd_a.shape[0],
+                                   C.cast(C.c_void_p(h_out.data_ptr()), _abi.U8P), diags, None))
+        lib.ccw_ti_destroy(h)
+
+    step_e2e()
+    e2e_s = 0.0
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_e2e()
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+    d2h = int(dev.last_timing()["d2h_bytes"])
+    e2e_equal = bool(np.array_equal(h_out.numpy().reshape(n_real, 4000, 4000), got))
+    out = {"workload": CONFIG2, "value": n_real * sg * steps / (total_ms * 1e-3), "unit": UNIT,
+           "ms_per_step": total_ms / steps, "steps": steps,
+           "fp64_windows_rescored": int(timing["rescored"]), "bulk_jobs": int(timing["bulk_jobs"]),
+           "gpu_launches": int(timing["launches"]) * steps,
+           "e2e": {"value": n_real * sg * steps / e2e_s, "unit": UNIT,
+                   "h2d_bytes_per_step": int(ti_host.nbytes + hd_a.nbytes + seeds.nbytes),
+                   "d2h_bytes_per_step": d2h, "equals_device_result": e2e_equal}}
+    if not skip_cpu:
+        cores = os.cpu_count() or 1
+        rate, dt, kind, ref = cpu_reference_rate(ti_a, 2, cfg, n_real, min(cores, n_real), hd, MASTER)
+        ok = [bool(np.array_equal(got[r], ref[r])) for r in range(n_real)]
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": min(cores, n_real), "kind": kind,
+                               "cpu_model": cpu_model(),
+                               "sample": f"the whole config-2 workload ({n_real} realizations), "
+                                         f"simulate_ensemble(workers={min(cores, n_real)}), {dt:.1f} s wall"}
+        out["parity"] = {"checked": n_real, "equal": all(ok),
+                         "mismatched": [r for r, v in enumerate(ok) if not v],
+                         "against": f"oracle/_ref ({kind}), the cpu_baseline run's own outputs, same seeds"}
+    out["pre_overwrite_mismatches"] = mism
+    return out
 
 
 SINGLE_WORKLOAD = ("config2-single: TI 2000x2000 binary channels, SG 4000x4000, T96 OV24 J3 K1, "
@@ -476,6 +634,34 @@ def run_single(args):
     return 0
 
 
+def _rank_main(rank, argv, world, port):
+    """One spawned rank of `bench.py --gpus N` (torchrun's environment)."""
+    os.environ.update({"RANK": str(rank), "LOCAL_RANK": str(rank), "WORLD_SIZE": str(world),
+                       "LOCAL_WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1",
+                       "MASTER_PORT": str(port)})
+    sys.argv = [sys.argv[0]] + list(argv)
+    rc = main()
+    if rc:
+        raise SystemExit(rc)
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: one process per GPU, as torchrun would."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {n} but {have} GPUs visible"}))
+        return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.start_processes(_rank_main, args=(sys.argv[1:], n, port), nprocs=n, join=True,
+                       start_method="spawn")
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -483,12 +669,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-config2", action="store_true",
+                    help="omit the nested config-2 measurement (N=1 only)")
     ap.add_argument("--workload", default="config1", choices=["config1", "single"],
                     help="config1 (headline) or single: one config-2 realization, positions sharded")
     ap.add_argument("--virtual-shards", type=int, default=1)
     ap.add_argument("--nccl", action="store_true",
                     help="single: exchange through an NCCL communicator even on one rank")
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "ours" and args.workload == "single":
         return run_single(args)
     if args.impl == "reference":

@@ -136,6 +136,12 @@ CCW_API ccw_status ccw_ctx_last_timing(ccw_ctx* ctx, ccw_timing* out);
  * counts fit int8, else fp32), 1 = fp32 CUDA-core direct, 2 = tcgen05 int8. */
 CCW_API ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant);
 
+/* Per-context options (all default to the production setting; tests use them
+ * to force rarely taken paths).  Names: groups, sched_replay, norm_screen,
+ * shard_fast, uniform, s16, bulk, help_min, stream_out, pack, stream_bands,
+ * place_threads.  Unknown names or negative values -> CCW_ERR_CONFIG. */
+CCW_API ccw_status ccw_ctx_set_option(ccw_ctx* ctx, const char* name, long long value);
+
 /* FP32 FFMA peak of this GPU (TFLOP/s), measured with an in-library
  * microbenchmark: the roofline denominator of the CUDA-core CCF screen. */
 CCW_API ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops);

@@ -63,6 +63,7 @@ SIGNATURES = {
     "ccw_ctx_set_profiling": (C.c_int, [P, C.c_int]),
     "ccw_ctx_last_timing": (C.c_int, [P, C.POINTER(TimingC)]),
     "ccw_ctx_set_ccf_variant": (C.c_int, [P, C.c_int]),
+    "ccw_ctx_set_option": (C.c_int, [P, C.c_char_p, C.c_longlong]),
     "ccw_nccl_unique_id": (C.c_int, [U8P]),
     "ccw_ctx_set_position_shards": (C.c_int, [P, C.c_int, C.c_int, U8P, C.c_int]),
     "ccw_measure_fp32_peak": (C.c_int, [P, F64P]),

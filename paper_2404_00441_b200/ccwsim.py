@@ -12,6 +12,7 @@ numeric operator and the simulation itself run on the GPU through the C-ABI.
 from __future__ import annotations
 
 import atexit
+import contextlib
 import ctypes as C
 import threading
 import weakref
@@ -331,6 +332,26 @@ class Device:
         self.check(self._lib.ccw_ctx_last_timing(self.handle, C.byref(t)))
         return {k: getattr(t, k) for k, _ in _abi.TimingC._fields_}
 
+    # production defaults of include/ccwgpu.h ccw_ctx_set_option
+    OPTION_DEFAULTS = {"groups": 0, "sched_replay": 0, "norm_screen": 1, "shard_fast": 1,
+                       "uniform": 1, "s16": 1, "bulk": 1, "help_min": 32, "stream_out": 1,
+                       "pack": 1, "stream_bands": 6, "place_threads": 0}
+
+    def set_option(self, name: str, value: int) -> None:
+        """Per-context option (include/ccwgpu.h ccw_ctx_set_option)."""
+        self.check(self._lib.ccw_ctx_set_option(self.handle, name.encode(), int(value)))
+
+    @contextlib.contextmanager
+    def options(self, **kw):
+        """Set options for the duration of a with-block, then restore the defaults."""
+        try:
+            for k, v in kw.items():
+                self.set_option(k, v)
+            yield self
+        finally:
+            for k in kw:
+                self.set_option(k, self.OPTION_DEFAULTS[k])
+
     def set_ccf_variant(self, variant: int) -> None:
         """0 auto (tcgen05 int8 when it is exact), 1 fp32 CUDA-core, 2 tcgen05 int8."""
         self.check(self._lib.ccw_ctx_set_ccf_variant(self.handle, int(variant)))
@@ -364,6 +385,11 @@ class Device:
 
     def close(self) -> None:
         if self.handle:
+            # TI handles cached for this context go with it (the cache keys on
+            # id(self), which a later Device may reuse)
+            for per in list(_ti_cache.values()):
+                for k in [k for k in per if k[1] == id(self)]:
+                    per.pop(k).close()
             self._lib.ccw_ctx_destroy(self.handle)
             self.handle = None
 

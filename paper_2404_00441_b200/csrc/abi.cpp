@@ -60,7 +60,8 @@ void validate_config(const ccw_sim_config& c) {
     if (c.sg_height < 1 || c.sg_width < 1)
         throw Fail(CCW_ERR_CONFIG, "sg_size: dimensions must be positive");
     if (c.dwt_level < 1) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be >= 1");
-    if (c.dwt_level > 10) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be <= 10");
+    // (the reference has no upper bound; 1 << dwt_level must stay an int)
+    if (c.dwt_level > 30) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be <= 30");
     if (c.template_size < 2) throw Fail(CCW_ERR_CONFIG, "template: must be >= 2");
     if (c.overlap < 1 || c.overlap >= c.template_size)
         throw Fail(CCW_ERR_CONFIG, "overlap: must be in [1, template)");
@@ -262,19 +263,14 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (ccwgpu::DevBuf* b : {&ctx->jobs, &ctx->work, &ctx->hd, &ctx->wts, &ctx->wts8,
-                              &ctx->tm64, &ctx->scores, &ctx->summary, &ctx->chosen,
-                              &ctx->pasted, &ctx->mism, &ctx->out, &ctx->stats, &ctx->src, &ctx->ops_a,
-                              &ctx->ops_b, &ctx->ops_c, &ctx->ops_d, &ctx->ops_e})
-        b->release();
-    ctx->h_stage.release();
-    ctx->xrec.release();
+    for (cudaStream_t s : ctx->gstreams) cudaStreamSynchronize(s);
+    for (cudaStream_t s : ctx->copy_streams) cudaStreamSynchronize(s);
     ccwgpu::nccl_comm_destroy(ctx->nccl_comm);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
     for (cudaStream_t s : ctx->copy_streams) cudaStreamDestroy(s);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    delete ctx;  // every DevBuf / HostBuf member frees its memory (RAII)
 }
 
 const char* ccw_last_error(const ccw_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
@@ -322,12 +318,28 @@ ccw_status ccw_ctx_set_position_shards(ccw_ctx* ctx, int nranks, int rank, const
             throw Fail(CCW_ERR_CONFIG, "position shards: more than one rank needs an NCCL unique id");
         CCW_CUDA(cudaStreamSynchronize(ctx->stream));
         for (cudaStream_t s : ctx->gstreams) CCW_CUDA(cudaStreamSynchronize(s));
+        // the old sharding state is dropped first; the new one is committed only
+        // once its communicator exists, so a failed init leaves sharding off
         ccwgpu::nccl_comm_destroy(ctx->nccl_comm);
         ctx->nccl_comm = nullptr;
+        ctx->shard_nranks = 1;
+        ctx->shard_rank = 0;
+        ctx->shard_virtual = 1;
+        void* comm = nccl_id ? ccwgpu::nccl_comm_init(nranks, rank, nccl_id) : nullptr;
+        ctx->nccl_comm = comm;
         ctx->shard_nranks = nranks;
         ctx->shard_rank = rank;
         ctx->shard_virtual = virtual_shards;
-        if (nccl_id) ctx->nccl_comm = ccwgpu::nccl_comm_init(nranks, rank, nccl_id);
+    });
+}
+
+ccw_status ccw_ctx_set_option(ccw_ctx* ctx, const char* name, long long value) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        int* slot = name ? ccwgpu::option_slot(ctx->opt, name) : nullptr;
+        if (!slot) throw Fail(CCW_ERR_CONFIG, fmt("option: unknown name '%s'", name ? name : "(null)"));
+        if (value < 0 || value > (1 << 20)) throw Fail(CCW_ERR_CONFIG, fmt("option %s: value out of range", name));
+        *slot = static_cast<int>(value);
     });
 }
 
@@ -370,7 +382,7 @@ static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device
         if (nf <= 0) throw Fail(CCW_ERR_DIMENSION, "num_facies must be positive");
         if (nf > 255) throw Fail(CCW_ERR_DIMENSION, "num_facies must be <= 255 (uint8 codes)");
         if (levels < 1) throw Fail(CCW_ERR_DIMENSION, "decomposition level must be >= 1");
-        if (levels > 10 || h % (1 << levels) != 0 || w % (1 << levels) != 0)
+        if (levels > 30 || h % (1 << levels) != 0 || w % (1 << levels) != 0)
             throw Fail(CCW_ERR_CONFIG,
                        fmt("training image %dx%d not divisible by 2^dwt_level = %d", h, w,
                            1 << std::min(levels, 30)));

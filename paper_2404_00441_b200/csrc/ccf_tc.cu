@@ -563,7 +563,7 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
     // CTAs resident at once: CCW_TC_MINB per SM when the footprint allows
     const int slots = tc_num_sms() * CCW_TC_MINB;
-    a.epi_in_ring = ntot <= slots && !getenv("CCW_TC_EPI_SEPARATE");
+    a.epi_in_ring = ntot <= slots;
     dim3 grid(std::min(ntot, a.epi_in_ring ? slots : tc_num_sms()));
     if (s16)
         launch_pdl(ccf_tc_kernel<true>, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);

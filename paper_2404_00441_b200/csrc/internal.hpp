@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <exception>
 #include <functional>
 #include <map>
@@ -56,10 +57,14 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     CCW_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
-// Grow-only device buffer owned by a context.
+// Grow-only device buffer owned by a context (freed with it).
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     void* get(size_t bytes) {
         if (bytes > cap) {
             if (p) cudaFree(p);
@@ -81,10 +86,14 @@ struct DevBuf {
     }
 };
 
-// Pinned host staging buffer.
+// Pinned host staging buffer (freed with its owner).
 struct HostBuf {
     void* p = nullptr;
     size_t cap = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { release(); }
     void* get(size_t bytes) {
         if (bytes > cap) {
             if (p) cudaFreeHost(p);
@@ -206,6 +215,51 @@ private:
     std::exception_ptr err_;
 };
 
+// Per-context tuning / test options (ccw_ctx_set_option).  Every default is
+// the production setting; tests flip them to force rarely taken paths.
+struct Options {
+    int groups = 0;            // realization groups on separate streams (0 = auto: 2)
+    int sched_replay = 0;      // 1: every unconditional pick takes the sequential replay (tests)
+    int norm_screen = 1;       // normalized scoring screened on the int8 GEMM
+    int shard_fast = 1;        // position shards may take the fast select
+    int uniform = 1;           // uniform-window reduction of large tie groups
+    int s16 = 1;               // int16 score rows when every screen score fits
+    int bulk = 1;              // bulk (CTA-wide) tie-group rescoring kernel
+    int help_min = 32;         // equal-score groups >= this are rescored by helper CTAs (0 = off)
+    int stream_out = 1;        // progressive band finalize + copy for host results
+    int pack = 1;              // bit-packed streamed bands
+    int stream_bands = 6;      // streaming checkpoints per call
+    int place_threads = 0;     // host unpack threads (0 = auto)
+};
+
+// Known option names (for ccw_ctx_set_option); returns nullptr if unknown.
+inline int* option_slot(Options& o, const std::string& name) {
+    if (name == "groups") return &o.groups;
+    if (name == "sched_replay") return &o.sched_replay;
+    if (name == "norm_screen") return &o.norm_screen;
+    if (name == "shard_fast") return &o.shard_fast;
+    if (name == "uniform") return &o.uniform;
+    if (name == "s16") return &o.s16;
+    if (name == "bulk") return &o.bulk;
+    if (name == "help_min") return &o.help_min;
+    if (name == "stream_out") return &o.stream_out;
+    if (name == "pack") return &o.pack;
+    if (name == "stream_bands") return &o.stream_bands;
+    if (name == "place_threads") return &o.place_threads;
+    return nullptr;
+}
+
+// Diagnostics-only environment switches (timelines, phase clocks): compiled
+// in only with -DCCW_DEBUG_KNOBS; a production build never reads them.
+inline const char* debug_env(const char* name) {
+#ifdef CCW_DEBUG_KNOBS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 }  // namespace ccwgpu
 
 struct ccw_ctx {
@@ -214,6 +268,7 @@ struct ccw_ctx {
     std::string err;
     bool profiling = false;
     int ccf_variant = 0;
+    ccwgpu::Options opt;
     ccw_timing timing{};
     // scratch
     ccwgpu::DevBuf cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,

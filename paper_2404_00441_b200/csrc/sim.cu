@@ -504,7 +504,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (sharded && npos < S_all)
         throw Fail(CCW_ERR_CONFIG, "position shards: more shards than TI window positions");
     int G = std::max(1, std::min(n_real, 2));
-    if (const char* e = getenv("CCW_GROUPS")) G = std::max(1, std::min(n_real, atoi(e)));
+    if (ctx->opt.groups > 0) G = std::max(1, std::min(n_real, ctx->opt.groups));
     if (sharded) G = 1;
     auto group_of = [&](int r) { return static_cast<int>(static_cast<int64_t>(r) * G / n_real); };
     std::vector<size_t> bucket(static_cast<size_t>(G) * nkeys + 1, 0);
@@ -542,13 +542,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // ---- exactness guard for the fp32 screen
     const double maxw = ti->mode == 0 ? B : static_cast<double>(ti->F - 1) * B;
     const double mask_cells = static_cast<double>(Tc) * OVc + static_cast<double>(Tc - OVc) * OVc;
-    const bool use_screen = cfg.scoring == 0 && ti->nscr > 0;
+    bool use_screen = cfg.scoring == 0 && ti->nscr > 0;
     // normalized scoring: screened on the int8 tensor-core GEMM when it applies
     // (otherwise every window is rescored in fp64)
-    bool norm_screen = cfg.scoring == 1 && ti->nscr > 0 && !getenv("CCW_NO_NORM_SCREEN") &&
+    bool norm_screen = cfg.scoring == 1 && ti->nscr > 0 && ctx->opt.norm_screen &&
                        mask_cells * ti->nch * maxw * maxw * maxw * maxw < 2147483647.0;
-    if (use_screen && mask_cells * maxw * maxw * std::max(1, ti->nscr) >= 16777216.0)
-        throw Fail(CCW_ERR_CONFIG, "configuration exceeds the exact fp32 screen range (mask*B^2 >= 2^24)");
 
     // ---- device buffers
     EventTimer tm{ctx, {}, {}, 0};
@@ -586,7 +584,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         SP.thr_fr = (0 - SP.nfr) % SP.nfr;
         SP.thr_fc = (0 - SP.nfc) % SP.nfc;
         SP.thr_k = (0 - static_cast<uint64_t>(Kp)) % static_cast<uint64_t>(Kp);
-        if (getenv("CCW_SCHED_REPLAY")) SP.thr_k = ~0ull;  // tests: every pick "rejected" -> sequential replay
+        if (ctx->opt.sched_replay) SP.thr_k = ~0ull;  // tests: every pick "rejected" -> sequential replay
         SP.nout = 4 + nlr * nlc;  // the path, the first placement's two, one per other placement
         SP.outs = ctx->sched_outs.as<uint64_t>(static_cast<size_t>(n_real) * SP.nout);
         SP.replay = ctx->sched_replay.as<uint64_t>(static_cast<size_t>(n_real) * 313);
@@ -675,6 +673,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (ctx->ccf_variant == 2 && use_screen && !tc_ok)
         throw Fail(CCW_ERR_CONFIG, "tcgen05 int8 screen needs block statistics <= 127");
     const bool use_tc = tc_ok && ctx->ccf_variant != 1;
+    // the fp32 CUDA-core screen is exact only while every partial sum stays
+    // below 2^24; beyond that every window is scored in fp64 (select mode 0)
+    if (use_screen && !use_tc && mask_cells * maxw * maxw * std::max(1, ti->nscr) >= 16777216.0)
+        use_screen = false;
     norm_screen = norm_screen && use_tc;  // the normalized screen rides on the int8 GEMM only
     const bool any_screen = use_screen || norm_screen;
     const int kpad = tc_kpad(ti->nscr, Tc);
@@ -707,7 +709,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // position shards take the fast select when every shard (boundaries at
     // multiples of one 256-position MMA tile) holds at least K tile maxima of
     // its own; the other shards' tiles read INT_MIN and are never candidates
-    const bool shard_fast = sharded && fast_ok && !getenv("CCW_SHARD_GENERIC") &&
+    const bool shard_fast = sharded && fast_ok && ctx->opt.shard_fast &&
                             npos / S_all >= 256 + 128 * Kp;
     const bool warp_select = !sharded && fast_ok;
     if (warp_select || shard_fast) {
@@ -721,12 +723,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             ctx->mtab_key = key;
         }
         P.mtab = d_mt;
-        if (!getenv("CCW_NO_UNIFORM")) P.umap = ti_umap(ti, Tc, OVc, st);
+        if (ctx->opt.uniform) P.umap = ti_umap(ti, Tc, OVc, st);
     }
     // int16 score rows for the fast select when every screen score fits:
     // |S'| <= mask cells * (largest weight) * (largest block statistic)
     const bool s16 = warp_select && mask_cells * static_cast<double>(maxv) * maxv < 32767.0 &&
-                     !getenv("CCW_NO_S16");
+                     ctx->opt.s16;
     P.s16 = s16 ? 1 : 0;
     P.kpad = kpad;
     P.ntiles = ntiles;
@@ -734,7 +736,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.im2col = d_x;
     // bulk tie select: largest window block whose apex tile fits the shared-memory budget
     size_t bulk_smem = 0;
-    if ((warp_select || shard_fast) && !getenv("CCW_NOBULK")) {
+    if ((warp_select || shard_fast) && ctx->opt.bulk) {
         constexpr size_t kBudget = 200 * 1024;
         for (int by = std::min(out_w, 256); by >= 8 && !bulk_smem; by /= 2) {
             int bx = std::min(out_h, 64);
@@ -786,7 +788,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // CTA's preps lengthen the select's critical path by more than the
     // separate, fully parallel prep kernel costs.
     const bool fuse_prep = warp_select && keymul == 2 && max_wave <= maxj && d_src &&
-                           getenv("CCW_FUSE_PREP") != nullptr;
+                           debug_env("CCW_FUSE_PREP") != nullptr;
     int* d_depcnt = nullptr;
     if (fuse_prep) {
         d_depcnt = ctx->depcnt.as<int>(G * maxj);
@@ -797,8 +799,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     HelpBoard* d_boards = nullptr;
     int4* d_hslots = nullptr;
     if (warp_select) {
-        int help_min = 32;
-        if (const char* e = getenv("CCW_HELP_MIN")) help_min = atoi(e);
+        const int help_min = ctx->opt.help_min;
         if (help_min > 0) {
             d_boards = ctx->hboards.as<HelpBoard>(2 * G);
             CCW_CUDA(cudaMemsetAsync(d_boards, 0, sizeof(HelpBoard) * 2 * G, st));
@@ -815,7 +816,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         }
     }
     std::vector<int> hb_par(G, 0);
-    const char* jdump_path = getenv("CCW_TAIL_DUMP");
+    const char* jdump_path = debug_env("CCW_TAIL_DUMP");
     unsigned long long* d_jdump = nullptr;
     if (jdump_path) {
         d_jdump = ctx->jdump.as<unsigned long long>(4 * total_jobs);
@@ -849,7 +850,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                   static_cast<int>(sel_smem)));
 
     unsigned long long* d_probe = nullptr;
-    if (getenv("CCW_TC_PROBE")) {
+    if (debug_env("CCW_TC_PROBE")) {
         d_probe = reinterpret_cast<unsigned long long*>(ctx->ops_d.get(8 * sizeof(unsigned long long)));
         CCW_CUDA(cudaMemsetAsync(d_probe, 0, 8 * sizeof(unsigned long long), st));
     }
@@ -907,19 +908,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                       static_cast<int>(sel_smem)));
     }
     // group streams, forked from / joined back to the context stream
-    // Stream priorities (CCW_PRIO = none | copies | waves), default none.
-    // Measured r1 (config 1, end to end): waves first 22.6 G cells/s --
-    // starving the band finalize kernels delays the host's unpacking; copies
-    // first 27.3-28.0 vs none 27.9-29.6, within run-to-run noise.
+    // (stream priorities measured r1, config 1 end to end: waves first 22.6 G
+    // cells/s -- starving the band finalize kernels delays the host's
+    // unpacking; copies first within noise of none; so none)
     int least = 0, greatest = 0;
     CCW_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    int wave_prio = least, copy_prio = least;
-    {
-        const char* e = getenv("CCW_PRIO");
-        const std::string pm = e ? e : "none";
-        if (pm == "waves") wave_prio = greatest;
-        if (pm == "copies") copy_prio = greatest;
-    }
+    const int wave_prio = least, copy_prio = least;
     while (static_cast<int>(ctx->copy_streams.size()) < G) {  // one per group: final copies overlap
         cudaStream_t s3;
         CCW_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, copy_prio));
@@ -930,16 +924,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, wave_prio));
         ctx->gstreams.push_back(s2);
     }
-    // timing experiments only (results are wrong when set): skip a kernel class
-    const char* skip_env = getenv("CCW_DEBUG_SKIP");
-    const std::string skip = skip_env ? skip_env : "";
-    const bool skip_prep = skip.find("prep") != std::string::npos;
-    const bool skip_ccf = skip.find("ccf") != std::string::npos;
-    const bool skip_sel = skip.find("sel") != std::string::npos;
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
-    const bool host_t = getenv("CCW_HOSTT") != nullptr;
+    const bool host_t = debug_env("CCW_HOSTT") != nullptr;
     auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(); };
     const double t_ev0 = host_t ? host_ms() : 0.0;
     // finalize granularity: one thread per coarse block (B = 2, 4, 8) with the map
@@ -950,7 +938,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // checkpoint waves, overlapping the copy with the remaining waves
     uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real);
     const size_t out_bytes = static_cast<size_t>(cfg.sg_height) * cfg.sg_width * n_real;
-    const bool stream_out = h_out && !d_out && !getenv("CCW_NO_STREAM_OUT");
+    const bool stream_out = h_out && !d_out && ctx->opt.stream_out;
     // device->host copies need page-locked memory to run asynchronously: a
     // pageable destination without streaming gets a pinned staging buffer,
     // copied out at the end
@@ -972,9 +960,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // Checkpoints thicken towards the end, where the last rows / columns
     // (direct row bands measured slower, r1: one copy per realization band
     // lengthens the launch loop, and 8-bit rows quadruple the PCIe bytes)
-    const bool direct_rows = getenv("CCW_DIRECT_ROWS") != nullptr;
-    size_t band_cap = 1024;  // CTAs per band of a finalize launch
-    if (const char* e = getenv("CCW_BAND_CTAS")) band_cap = std::max(1, atoi(e));
+    const bool direct_rows = debug_env("CCW_DIRECT_ROWS") != nullptr;
+    const size_t band_cap = 1024;  // CTAs per band of a finalize launch
     bool h_pinned = false;
     if (stream_out) {
         cudaPointerAttributes pa{};
@@ -991,7 +978,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     uint8_t* h_stage = nullptr;
     uint8_t* d_stage = nullptr;
     // cells per streamed byte: the realizations' codes fit in 1, 2 or 4 bits for F <= 2, 4, 16
-    const int pack_bits = getenv("CCW_NO_PACK") ? 8 : ti->F <= 2 ? 1 : ti->F <= 4 ? 2 : ti->F <= 16 ? 4 : 8;
+    const int pack_bits = !ctx->opt.pack ? 8 : ti->F <= 2 ? 1 : ti->F <= 4 ? 2 : ti->F <= 16 ? 4 : 8;
     const int pack_cpb = 8 / pack_bits;
     auto band_rowb = [&](const int4& bd) {  // packed bytes per band row
         const int wdt = bd.y == 0 ? cfg.sg_width : bd.w - bd.z;
@@ -1003,13 +990,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         // evenly spaced (measured r1: 6 beats both fewer and more, and beats
         // checkpoints crowded towards the end -- thin column bands cost the
         // host more per byte than the later landing costs)
-        int nck = 6;
-        if (const char* e = getenv("CCW_STREAM_BANDS")) nck = std::max(1, atoi(e));
+        const int nck = std::max(1, ctx->opt.stream_bands);
         for (int k = 1; k <= nck; ++k) cks.push_back((max_key * k) / nck);
         // extra checkpoints one raster-outer step apart before the end shrink
         // the bands that can only leave after the last wave
         int ntail = 0;
-        if (const char* e = getenv("CCW_STREAM_TAIL")) ntail = std::max(0, atoi(e));
+        if (const char* e = debug_env("CCW_STREAM_TAIL")) ntail = std::max(0, atoi(e));
         for (int k = 1; k <= ntail; ++k) cks.push_back(max_key - k * keymul);
         std::vector<int> done(n_real, 0);  // raster-outer extent already emitted
         long long off = 0;
@@ -1138,7 +1124,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         t_unpack += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - tw1).count();
     };
     int place_threads = std::max(1, static_cast<int>(std::thread::hardware_concurrency()) - 2);
-    if (const char* e = getenv("CCW_PLACE_THREADS")) place_threads = std::max(1, atoi(e));
+    if (ctx->opt.place_threads > 0) place_threads = ctx->opt.place_threads;
     std::exception_ptr place_err;
     std::thread placer;
     if (!packed_q.empty())
@@ -1162,7 +1148,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     } placer_join{placer, arr_ready.get(), arrivals.size()};
 
     // debug timeline: [resident, past-wait, end] per launch
-    const bool want_tl = getenv("CCW_TIMELINE") != nullptr;
+    const bool want_tl = debug_env("CCW_TIMELINE") != nullptr;
     std::vector<std::array<int, 3>> tl_tag;  // (wave, group, kind 0 prep / 1 ccf / 2 select)
     unsigned long long* d_tl = nullptr;
     const size_t tl_cap = static_cast<size_t>(max_key + 1) * G * 4 * 8;
@@ -1286,7 +1272,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 }
                 if (!first_wave) {
                     Q.tl = tl_next(w, g, 0);
-                    if (!skip_prep && !fuse_prep) {  // (fused: prepared by the previous wave's select)
+                    if (!fuse_prep) {  // (fused: prepared by the previous wave's select)
                         if (d_src)
                             launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
                                        static_cast<const Job*>(d_jobs), static_cast<int>(j0));
@@ -1302,8 +1288,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                             b = tm.get();
                             CCW_CUDA(cudaEventRecord(a, gs));
                         }
-                        if (skip_ccf) {
-                        } else if (use_tc) {
+                        if (use_tc) {
                             launch_ccf_tc(tcplans[g][par], npos, sld, kpad, nj, Q.scores, Q.tmax, gs,
                                           tl_next(w, g, 1), -1, Q.s16);
                         } else {
@@ -1338,8 +1323,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     CCW_CUDA(cudaEventRecord(a, gs));
                 }
                 Q.tl = tl_next(w, g, 2);
-                if (skip_sel && !first_wave) {
-                } else if (warp_select || (first_wave && !cfg.min_cut)) {
+                if (warp_select || (first_wave && !cfg.min_cut)) {
                     const Job* dj = d_jobs;
                     if (d_boards) {
                         Q.hb = d_boards + 2 * g + hb_par[g];
@@ -1579,24 +1563,24 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 pr[2] / n, pr[3] / n, pr[4] / n, pr[5] / (8 * n), pr[6] / n);
         tc_probe_buffer = nullptr;
     }
-    if (getenv("CCW_TAIL"))
+    if (debug_env("CCW_TAIL"))
         fprintf(stderr, "select jobs: ties %llu avg %.0f max %llu cycles | no ties %llu avg %.0f max %llu cycles\n",
                 stats[16], stats[16] ? double(stats[17]) / stats[16] : 0.0, stats[18], stats[19],
                 stats[19] ? double(stats[20]) / stats[19] : 0.0, stats[21]);
-    if (getenv("CCW_TAIL"))
+    if (debug_env("CCW_TAIL"))
         fprintf(stderr, "select cycles histogram <10k %llu <20k %llu <40k %llu <80k %llu >=80k %llu | long jobs: scan+stage %llu batch %llu choose+map %llu candidates %llu\n",
                 stats[22], stats[23], stats[24], stats[25], stats[26], stats[27], stats[28], stats[29], stats[30]);
-    if (getenv("CCW_TAIL"))
+    if (debug_env("CCW_TAIL"))
         fprintf(stderr, "shared rescoring: posts %llu, chunks %llu (own %llu), owner help cycles %llu wait cycles %llu\n",
                 stats[32], stats[33], stats[34], stats[35], stats[36]);
-    if (getenv("CCW_TAIL"))
+    if (debug_env("CCW_TAIL"))
         fprintf(stderr, "small groups (g < 8): %llu, rescore+select cycles avg %.0f (items %.0f), scan->group cycles avg %.0f\n",
                 stats[37], stats[37] ? double(stats[38]) / stats[37] : 0.0, stats[37] ? double(stats[40]) / stats[37] : 0.0,
                 stats[37] ? double(stats[39]) / stats[37] : 0.0);
-    if (getenv("CCW_TAIL"))
+    if (debug_env("CCW_TAIL"))
         fprintf(stderr, "small-group item (thread 0): loads+products %.0f chain+stores %.0f cycles over %llu\n",
                 stats[43] ? double(stats[41]) / stats[43] : 0.0, stats[43] ? double(stats[42]) / stats[43] : 0.0, stats[43]);
-    if (getenv("CCW_PHASES"))
+    if (debug_env("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
                 stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[4], stats[7], stats[14],

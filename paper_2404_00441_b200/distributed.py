@@ -117,9 +117,11 @@ def simulate_position_sharded(ti: cs.CategoricalGrid, cfg: cs.SimConfig, seeds: 
     rank = dist.get_rank(group)
     dev = device or cs.default_device()
     box = [cs.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0, group=group)
-    dev.set_position_shards(world, rank, box[0], virtual_shards)
+    # src is a global rank: group rank 0 of `group` (itself when group is None)
+    src = 0 if group is None else dist.get_global_rank(group, 0)
+    dist.broadcast_object_list(box, src=src, group=group)
     try:
+        dev.set_position_shards(world, rank, box[0], virtual_shards)
         return cs.simulate_batch(ti, cfg, list(seeds), None, dev)
     finally:
         dev.set_position_shards(1, 0, None, 1)

@@ -1,0 +1,192 @@
+"""Parity of the CUDA path against the COMPILED REFERENCE (oracle/_ref: the
+unmodified reference headers, simulator.hpp:418-566) at the BASELINE
+configurations' full sizes, plus the history-dependent launch-plan paths of
+the library (the per-context bulk_off memory, sim.cu run_simulation) and the
+production options forced off.  Every comparison is exact equality."""
+import numpy as np
+import pytest
+
+import pyoracle
+from paper_2404_00441_b200 import ccwsim as cs
+from paper_2404_00441_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg_dict(cfg):
+    c = cfg.to_c()
+    return dict(sg_height=c.sg_height, sg_width=c.sg_width, template_size=c.template_size,
+                overlap=c.overlap, dwt_level=c.dwt_level, candidates=c.candidates,
+                scoring=c.scoring, facies_mode=c.facies_mode, min_cut=bool(c.min_cut))
+
+
+def config0_adjusted():
+    """Config 0': the 250^2 generated TI cropped to its
+    top-left 248^2 (250 is not divisible by 2^J = 4, simulator.hpp:78-81),
+    OV 12 instead of 10 (simulator.hpp:58-60)."""
+    ti_a = np.ascontiguousarray(synth.config0_ti()[:248, :248])
+    cfg = cs.SimConfig(250, 250, 40, 12, 2, 1)
+    return ti_a, cfg
+
+
+def test_config0_adjusted_vs_reference(reference):
+    """Config 0' (TI 248^2 binary channels, SG 250^2, T40, OV12, J2, K1):
+    six realizations bit-identical to the compiled reference, with and
+    without hard data, and through simulate_ensemble (seeds mix64(master, r+1))."""
+    ti_a, cfg = config0_adjusted()
+    ti = cs.CategoricalGrid(248, 248, 2, ti_a)
+    seeds = [cs.mix64(20240441, r + 1) for r in range(6)]
+    res = cs.simulate_batch(ti, cfg, seeds)
+    for s, r in zip(seeds, res):
+        o = reference.simulate_one(ti_a, 2, pyoracle.Cfg(**cfg_dict(cfg)), None, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"]), s
+        assert r.diagnostics.origin == o["diagnostics"]["origin"]
+    # conditional: 1 % hard data drawn from a reference realization
+    hd = synth.hard_data_from(res[0].realization.cells, 0.01, 5)
+    cfg.hard_data = hd
+    for s in seeds[:3]:
+        r = cs.simulate_one(ti, cfg, s)
+        o = reference.simulate_one(ti_a, 2, pyoracle.Cfg(**cfg_dict(cfg)), hd, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"]), s
+        assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+    # simulate_ensemble: worker-count invariance (acceptance.cpp:665-702)
+    cfg.hard_data = cs.HardDataSet()
+    cfg.n_realizations = 4
+    cfg.master_seed = 77
+    ens = cs.simulate_ensemble(ti, cfg, workers=8)
+    ref, _ = reference.simulate_ensemble(ti_a, 2, pyoracle.Cfg(**cfg_dict(cfg), n_realizations=4,
+                                                               master_seed=77), None, workers=1)
+    assert len(ens) == 4
+    for a, b in zip(ens, ref):
+        assert np.array_equal(a.realization.cells, b)
+
+
+@pytest.mark.slow
+def test_config1_full_size_vs_reference(reference):
+    """BASELINE config 1 (TI 500^2 3 facies, SG 1000^2, T64 OV16 J2 K5): the
+    first four of the benchmarked realizations (bench.py: master 20240441,
+    seeds mix64(master, r+1)) bit-identical to the compiled reference."""
+    ti_a = synth.config1_ti()
+    ti = cs.CategoricalGrid(500, 500, 3, ti_a)
+    cfg = cs.SimConfig(1000, 1000, 64, 16, 2, 5)
+    seeds = [cs.mix64(20240441, r + 1) for r in range(100)]
+    res = cs.simulate_batch(ti, cfg, seeds)  # the bench's whole 100-realization call
+    for r in range(4):
+        o = reference.simulate_one(ti_a, 3, pyoracle.Cfg(**cfg_dict(cfg)), None, seed=seeds[r])
+        assert np.array_equal(res[r].realization.cells, o["realization"]), r
+
+
+@pytest.mark.slow
+def test_config2_full_size_vs_reference(reference):
+    """BASELINE config 2 (TI 2000^2, SG 4000^2, T96 OV24 J3 K1, 1 % hard data):
+    one realization of an 8-realization call bit-identical to the compiled
+    reference, hard-data diagnostics included."""
+    ti_a = synth.config2_ti()
+    hd = synth.config2_hard_data(ti_a)
+    ti = cs.CategoricalGrid(2000, 2000, 2, ti_a)
+    cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1)
+    cfg.hard_data = hd
+    seeds = [cs.mix64(20240441, r + 1) for r in range(8)]
+    res = cs.simulate_batch(ti, cfg, seeds)
+    o = reference.simulate_one(ti_a, 2, pyoracle.Cfg(**cfg_dict(cfg)), hd, seed=seeds[3])
+    assert np.array_equal(res[3].realization.cells, o["realization"])
+    assert res[3].diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+
+
+def tie_heavy_case():
+    ti_a = synth.channel_ti(640, 640, 77, scale=6.0)
+    return ti_a, dict(template_size=96, overlap=24, dwt_level=3, candidates=1)
+
+
+def test_learned_bulk_off_then_overflow(oracle):
+    """sim.cu memoizes, per (TI content, Tc, OVc, K, T) on the context, that a
+    call deferred no tie group; the next call then skips the bulk kernel.  A
+    later call that overflows the candidate list on the same TI and shape
+    must take the in-kernel fallback (select.cu) and stay exact; the call
+    after it brings the bulk kernel back."""
+    ti_a, geo = tie_heavy_case()
+    ti = cs.CategoricalGrid(640, 640, 2, ti_a)
+    dev = cs.Device(0)  # a fresh context: no plan memory
+    try:
+        # call 1: one placement (SG = T), nothing screened -> nothing deferred
+        small = dict(sg_height=96, sg_width=96, **geo)
+        cs.simulate_batch(ti, to_cfg(small), [3], device=dev)
+        assert dev.last_timing()["bulk_jobs"] == 0
+        # call 2: the tie-heavy shape, bulk kernel switched off by the memory
+        big = dict(sg_height=600, sg_width=700, **geo)
+        seeds = [cs.mix64(5, 1), cs.mix64(6, 1)]
+        res = cs.simulate_batch(ti, to_cfg(big), seeds, device=dev)
+        t2 = dev.last_timing()
+        assert t2["bulk_jobs"] == 0 and t2["list_overflows"] > 0
+        for s, r in zip(seeds, res):
+            o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**big), None, seed=s)
+            assert np.array_equal(r.realization.cells, o["realization"]), s
+        # call 3: the overflow re-enabled the bulk kernel
+        res3 = cs.simulate_batch(ti, to_cfg(big), seeds, device=dev)
+        assert dev.last_timing()["bulk_jobs"] > 0
+        for a, b in zip(res, res3):
+            assert a.realization == b.realization
+    finally:
+        dev.close()
+
+
+@pytest.mark.parametrize("opts", [dict(bulk=0), dict(uniform=0, s16=0), dict(groups=1),
+                                  dict(groups=3, stream_out=0), dict(pack=0, stream_bands=2)])
+def test_options_forced_paths(oracle, opts):
+    """The production options switched off one by one (include/ccwgpu.h
+    ccw_ctx_set_option): no bulk kernel (every overflow takes the in-kernel
+    fallback), no uniform-class reduction / int32 score rows, other group
+    counts, no streamed or no packed host bands.  Bit-exact."""
+    ti_a, geo = tie_heavy_case()
+    ti = cs.CategoricalGrid(640, 640, 2, ti_a)
+    d = dict(sg_height=500, sg_width=520, **geo)
+    seeds = [cs.mix64(11, 1), cs.mix64(11, 2), cs.mix64(11, 3)]
+    dev = cs.default_device()
+    with dev.options(**opts):
+        res = cs.simulate_batch(ti, to_cfg(d), seeds)
+        if opts.get("bulk") == 0:
+            assert dev.last_timing()["bulk_jobs"] == 0
+    for s, r in zip(seeds, res):
+        o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"]), (opts, s)
+
+
+def test_option_names_validated():
+    dev = cs.default_device()
+    with pytest.raises(cs.ConfigError):
+        dev.set_option("no_such_option", 1)
+    with pytest.raises(cs.ConfigError):
+        dev.set_option("groups", -1)
+
+
+def test_context_create_destroy_frees_device_memory():
+    """ccw_ctx_destroy releases every buffer (DevBuf / HostBuf are RAII): a
+    create / simulate / destroy cycle does not grow the device footprint."""
+    import torch
+    ti_a, cfg = config0_adjusted()
+    ti = cs.CategoricalGrid(248, 248, 2, ti_a)
+
+    def cycle():
+        dev = cs.Device(0)
+        try:
+            cs.simulate_batch(ti, cfg, [1, 2, 3, 4], device=dev)
+        finally:
+            dev.close()
+
+    cycle()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(4):
+        cycle()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 8 << 20, (free0, free1)
+
+
+def to_cfg(d, hd=None):
+    cfg = cs.SimConfig(sg_height=d["sg_height"], sg_width=d["sg_width"],
+                       template_size=d["template_size"], overlap=d["overlap"],
+                       dwt_level=d["dwt_level"], candidates=d["candidates"])
+    if hd:
+        cfg.hard_data = cs.HardDataSet([cs.HardDatum(*p) for p in hd])
+    return cfg

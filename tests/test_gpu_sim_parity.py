@@ -183,7 +183,6 @@ def test_device_schedule_replay(oracle, hard, monkeypatch):
     by bounded() sends the realization to a sequential replay.  Forcing that
     path for every realization must give the same realizations."""
     from paper_2404_00441_b200 import synth
-    monkeypatch.setenv("CCW_SCHED_REPLAY", "1")
     ti_a = synth.channel_ti(160, 160, 41, scale=5.0)
     ti = cs.CategoricalGrid(160, 160, 2, ti_a)
     d = dict(sg_height=150, sg_width=170, template_size=24, overlap=8, dwt_level=2, candidates=3)
@@ -192,7 +191,8 @@ def test_device_schedule_replay(oracle, hard, monkeypatch):
     if hard:
         ref = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=seeds[0])["realization"]
         hd = [tuple(int(v) for v in row) for row in synth.hard_data_from(ref, 0.01, 3)]
-    res = cs.simulate_batch(ti, to_cfg(d, hd), seeds)
+    with cs.default_device().options(sched_replay=1):
+        res = cs.simulate_batch(ti, to_cfg(d, hd), seeds)
     for s, r in zip(seeds, res):
         o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), hd, seed=s)
         assert np.array_equal(r.realization.cells, o["realization"])
@@ -204,16 +204,15 @@ def test_shared_rescoring(oracle, help_min, monkeypatch):
     claimed by the launch's other CTAs (select.cu hb_rescore); a low
     threshold makes most unconditional picks go that way.  Bit-exact."""
     from paper_2404_00441_b200 import synth
-    monkeypatch.setenv("CCW_HELP_MIN", str(help_min))
-    # (uniform-window reduction off: it would shrink the groups below help_min)
-    monkeypatch.setenv("CCW_NO_UNIFORM", "1")
     ti_a = synth.channel_ti(200, 200, 31, scale=5.0)
     ti = cs.CategoricalGrid(200, 200, 2, ti_a)
     d = dict(sg_height=260, sg_width=230, template_size=32, overlap=8, dwt_level=2, candidates=5)
     dev = cs.default_device()
     seeds = [cs.mix64(9, i) for i in range(6)]
-    res = cs.simulate_batch(ti, to_cfg(d, None), seeds)
-    assert dev.last_timing()["shared_groups"] > 0
+    # (uniform-window reduction off: it would shrink the groups below help_min)
+    with dev.options(help_min=help_min, uniform=0):
+        res = cs.simulate_batch(ti, to_cfg(d, None), seeds)
+        assert dev.last_timing()["shared_groups"] > 0
     for s, r in zip(seeds, res):
         o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=s)
         assert np.array_equal(r.realization.cells, o["realization"])
