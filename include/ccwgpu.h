@@ -252,6 +252,69 @@ CCW_API ccw_status ccw_min_cut_stitch(ccw_ctx* ctx, const uint8_t* existing, con
                               int t, int shape, int vertical_on_left, int horizontal_on_top,
                               int overlap, uint8_t* out);
 
+/* ------------------------------------- 3D extension (BASELINE c3, c4) -- */
+/* The reference has no 3D.  The 3D path is the builder's
+ * generalization of simulate_one (simulator.hpp:148-252,418-519) defined in
+ * oracle/ccw3d_oracle.h: 3D grids (axis 2 fastest, axis 0 vertical), 8
+ * corners x 6 axis orders drawn as bounded(rng, 8), bounded(rng, 6),
+ * overlap = the union of the previous-side slabs, EXACT integer scores from
+ * per-facies block counts, ties to the earlier row-major position, K <= 16,
+ * F <= 16.  any_support = 1 is the literal-config extension (overlap not a
+ * multiple of 2^J: a coarse cell is in the mask if any fine overlap cell
+ * falls in its block; the TI is used at floor(d / 2^J) * 2^J). */
+typedef struct ccw_sim3d_config {
+    int32_t sg[3];
+    int32_t template_size;
+    int32_t overlap;
+    int32_t dwt_level;
+    int32_t candidates;
+    int32_t n_realizations;
+    int32_t any_support;
+    int32_t _pad;
+    uint64_t master_seed;
+} ccw_sim3d_config;
+
+typedef struct ccw_diag3d {
+    uint64_t seed;
+    int32_t corner;  /* bit a: axis a walked descending */
+    int32_t order;   /* (outer, middle, inner) axis permutation index */
+    int32_t work[3];
+    int32_t placement_count;
+    int32_t hard_data_count;
+    int32_t pre_overwrite_mismatches;
+    double wall_seconds;
+} ccw_diag3d;
+
+typedef struct ccw_ti3d ccw_ti3d;
+
+/* Uploads a d0 x d1 x d2 TI (codes < num_facies <= 16) and builds its level-J
+ * block counts once on the device. */
+CCW_API ccw_status ccw_ti3d_create(ccw_ctx* ctx, const uint8_t* cells, int d0, int d1, int d2, int num_facies,
+                                   int levels, ccw_ti3d** out);
+CCW_API void ccw_ti3d_destroy(ccw_ti3d* ti);
+/* validate / validate_against in 3D; ti_dims (3 ints) may be NULL.  hd holds
+ * n_hd quadruples (i0, i1, i2, facies) in SG coordinates. */
+CCW_API ccw_status ccw_validate_config3d(const ccw_sim3d_config* cfg, const int32_t* ti_dims, int num_facies,
+                                         const int32_t* hd, int n_hd, char* msg, size_t msg_len);
+/* n_real realizations with explicit seeds; out: n_real * sg0*sg1*sg2 codes
+ * (host memory; _device: device memory).  diag may be NULL.  Position
+ * sharding (ccw_ctx_set_position_shards) applies: shard s screens its range
+ * of window boxes and the per-wave box lists are all-gathered. */
+CCW_API ccw_status ccw_simulate3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg, const uint64_t* seeds,
+                                  int n_real, const int32_t* hd, int n_hd, uint8_t* out, ccw_diag3d* diag);
+CCW_API ccw_status ccw_simulate3d_device(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg,
+                                         const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                                         uint8_t* d_out, ccw_diag3d* diag);
+/* As ccw_simulate3d, plus the provenance trace (SimTrace, simulator.hpp:395-403
+ * in 3D): ti_origins[(r * capacity + p) * 3 + a] = the TI fine origin pasted
+ * at placement p (raster order) of realization r, for p < capacity. */
+CCW_API ccw_status ccw_simulate3d_trace(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg,
+                                        const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                                        uint8_t* out, ccw_diag3d* diag, int32_t* ti_origins, int capacity);
+/* seeds mix64(master, r + 1), r < cfg->n_realizations. */
+CCW_API ccw_status ccw_simulate3d_ensemble(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg,
+                                           const int32_t* hd, int n_hd, uint8_t* out, ccw_diag3d* diag);
+
 /* -------------------------------------------------- host-side helpers -- */
 /* SimConfig::validate / validate_against (simulator.hpp:46-84) incl.
  * validate_hard_data (grid.hpp:151-170); ti_h/ti_w <= 0 skips the TI part. */

@@ -47,6 +47,20 @@ class TimingC(C.Structure):
                 ("bulk_jobs", C.c_int64), ("shared_groups", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
+class Sim3dConfigC(C.Structure):
+    _fields_ = [("sg", C.c_int32 * 3), ("template_size", C.c_int32), ("overlap", C.c_int32),
+                ("dwt_level", C.c_int32), ("candidates", C.c_int32),
+                ("n_realizations", C.c_int32), ("any_support", C.c_int32), ("_pad", C.c_int32),
+                ("master_seed", C.c_uint64)]
+
+
+class Diag3dC(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("corner", C.c_int32), ("order", C.c_int32),
+                ("work", C.c_int32 * 3), ("placement_count", C.c_int32),
+                ("hard_data_count", C.c_int32), ("pre_overwrite_mismatches", C.c_int32),
+                ("wall_seconds", C.c_double)]
+
+
 P = C.c_void_p
 I32P = C.POINTER(C.c_int32)
 U8P = C.POINTER(C.c_uint8)
@@ -92,6 +106,18 @@ SIGNATURES = {
                                          C.c_int, C.c_int, INTP, INTP]),
     "ccw_min_cut_stitch": (C.c_int, [P, U8P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      U8P]),
+    "ccw_ti3d_create": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
+    "ccw_ti3d_destroy": (None, [P]),
+    "ccw_validate_config3d": (C.c_int, [C.POINTER(Sim3dConfigC), I32P, C.c_int, I32P, C.c_int,
+                                        C.c_char_p, C.c_size_t]),
+    "ccw_simulate3d": (C.c_int, [P, P, C.POINTER(Sim3dConfigC), U64P, C.c_int, I32P, C.c_int, U8P,
+                                 C.POINTER(Diag3dC)]),
+    "ccw_simulate3d_trace": (C.c_int, [P, P, C.POINTER(Sim3dConfigC), U64P, C.c_int, I32P, C.c_int, U8P,
+                                       C.POINTER(Diag3dC), I32P, C.c_int]),
+    "ccw_simulate3d_device": (C.c_int, [P, P, C.POINTER(Sim3dConfigC), U64P, C.c_int, I32P, C.c_int,
+                                        P, C.POINTER(Diag3dC)]),
+    "ccw_simulate3d_ensemble": (C.c_int, [P, P, C.POINTER(Sim3dConfigC), I32P, C.c_int, U8P,
+                                          C.POINTER(Diag3dC)]),
     "ccw_validate_config": (C.c_int, [C.POINTER(SimConfigC), C.c_int, C.c_int, C.c_int, I32P,
                                       C.c_int, C.c_char_p, C.c_size_t]),
     "ccw_plan_raster_path": (C.c_int, [C.POINTER(SimConfigC), C.c_int, C.c_int, INTP, INTP, I32P,

@@ -123,6 +123,55 @@ void validate_against(const ccw_sim_config& c, int ti_h, int ti_w, int nf, const
     if (hd) validate_hard_data(hd, n_hd, c.sg_height, c.sg_width, nf);
 }
 
+// 3D extension (oracle/ccw3d_oracle.h: simulator.hpp:46-84 and
+// grid.hpp:151-170 over three axes); same messages as the 2D checks.
+void validate_config3d(const ccw_sim3d_config& c, const int32_t* ti, int nf, const int32_t* hd, int n_hd) {
+    if (c.sg[0] < 1 || c.sg[1] < 1 || c.sg[2] < 1) throw Fail(CCW_ERR_CONFIG, "sg_size: dimensions must be positive");
+    if (c.dwt_level < 1) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be >= 1");
+    if (c.dwt_level > 10) throw Fail(CCW_ERR_CONFIG, "dwt_level: must be <= 10");
+    if (c.template_size < 2) throw Fail(CCW_ERR_CONFIG, "template: must be >= 2");
+    if (c.overlap < 1 || c.overlap >= c.template_size) throw Fail(CCW_ERR_CONFIG, "overlap: must be in [1, template)");
+    const int b = 1 << c.dwt_level;
+    if (c.template_size % b != 0)
+        throw Fail(CCW_ERR_CONFIG, fmt("template: %d not divisible by 2^dwt_level = %d", c.template_size, b));
+    if (!c.any_support && c.overlap % b != 0)
+        throw Fail(CCW_ERR_CONFIG, fmt("overlap: %d not divisible by 2^dwt_level = %d", c.overlap, b));
+    if (c.candidates < 1) throw Fail(CCW_ERR_CONFIG, "candidates: must be >= 1");
+    if (c.n_realizations < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+    for (int a = 0; a < 3; ++a)
+        if (c.template_size > c.sg[a])
+            throw Fail(CCW_ERR_CONFIG, fmt("template: %d exceeds simulation grid %dx%dx%d", c.template_size, c.sg[0],
+                                           c.sg[1], c.sg[2]));
+    if (!ti) return;
+    if (ti[0] < 1 || ti[1] < 1 || ti[2] < 1) throw Fail(CCW_ERR_DIMENSION, "grid dimensions must be positive");
+    if (nf < 1 || nf > 16) throw Fail(CCW_ERR_DIMENSION, "num_facies must be in [1, 16] for the 3D path");
+    for (int a = 0; a < 3; ++a) {
+        const int used = c.any_support ? ti[a] / b * b : ti[a];
+        if (c.template_size > used)
+            throw Fail(CCW_ERR_CONFIG, fmt("template: %d exceeds training image %dx%dx%d", c.template_size, ti[0],
+                                           ti[1], ti[2]));
+    }
+    if (!c.any_support && (ti[0] % b || ti[1] % b || ti[2] % b))
+        throw Fail(CCW_ERR_CONFIG, fmt("training image %dx%dx%d not divisible by 2^dwt_level = %d", ti[0], ti[1],
+                                       ti[2], b));
+    if (n_hd > 0 && !hd) throw Fail(CCW_ERR_GENERIC, "null hard data");
+    std::vector<uint64_t> seen;
+    const size_t n = static_cast<size_t>(c.sg[0]) * c.sg[1] * c.sg[2];
+    if (n_hd > 0) seen.assign((n + 63) / 64, 0);
+    for (int i = 0; i < n_hd; ++i) {
+        const int32_t* d = hd + 4 * i;
+        if (d[0] < 0 || d[0] >= c.sg[0] || d[1] < 0 || d[1] >= c.sg[1] || d[2] < 0 || d[2] >= c.sg[2])
+            throw Fail(CCW_ERR_BOUNDS, fmt("hard datum %d at (%d, %d, %d) outside %dx%dx%d grid", i, d[0], d[1], d[2],
+                                           c.sg[0], c.sg[1], c.sg[2]));
+        if (d[3] < 0 || d[3] >= nf)
+            throw Fail(CCW_ERR_BOUNDS, fmt("hard datum %d has facies %d outside [0, %d)", i, d[3], nf));
+        const size_t cell = (static_cast<size_t>(d[0]) * c.sg[1] + d[1]) * c.sg[2] + d[2];
+        if (seen[cell >> 6] & (1ull << (cell & 63)))
+            throw Fail(CCW_ERR_STRUCTURE, fmt("duplicate hard data at (%d, %d, %d)", d[0], d[1], d[2]));
+        seen[cell >> 6] |= 1ull << (cell & 63);
+    }
+}
+
 uint64_t bounded(std::mt19937_64& rng, uint64_t n) {
     const uint64_t threshold = (0 - n) % n;
     for (;;) {
@@ -636,6 +685,123 @@ ccw_status ccw_min_cut_stitch(ccw_ctx* ctx, const uint8_t* existing, const uint8
         if (shape != CCW_OR_NONE && (overlap < 1 || overlap >= t))
             throw Fail(CCW_ERR_STRUCTURE, "overlap band width out of range");
         ccwgpu::op_min_cut_stitch(ctx, existing, incoming, t, shape, vleft, htop, overlap, out);
+    });
+}
+
+// ------------------------------------------------------------- 3D ----
+
+ccw_status ccw_ti3d_create(ccw_ctx* ctx, const uint8_t* cells, int d0, int d1, int d2, int nf, int levels,
+                           ccw_ti3d** out) {
+    if (!ctx || !out) return CCW_ERR_GENERIC;
+    *out = nullptr;
+    auto* ti = new ccw_ti3d();
+    ccw_status st = guarded(ctx, [&] {
+        if (d0 <= 0 || d1 <= 0 || d2 <= 0) throw Fail(CCW_ERR_DIMENSION, "grid dimensions must be positive");
+        if (nf < 1 || nf > 16) throw Fail(CCW_ERR_DIMENSION, "num_facies must be in [1, 16] for the 3D path");
+        if (levels < 1 || levels > 10) throw Fail(CCW_ERR_DIMENSION, "decomposition level must be in [1, 10]");
+        if (!cells) throw Fail(CCW_ERR_GENERIC, "null cells");
+        const size_t n = static_cast<size_t>(d0) * d1 * d2;
+        for (size_t i = 0; i < n; ++i)
+            if (cells[i] >= nf)
+                throw Fail(CCW_ERR_BOUNDS, fmt("cell %zu holds code %d outside [0, %d)", i, static_cast<int>(cells[i]), nf));
+        const int b = 1 << levels;
+        ti->ctx = ctx;
+        ti->device = ctx->device;
+        ti->d[0] = d0;
+        ti->d[1] = d1;
+        ti->d[2] = d2;
+        for (int a = 0; a < 3; ++a) ti->c[a] = ti->d[a] / b;
+        if (ti->c[0] < 1 || ti->c[1] < 1 || ti->c[2] < 1)
+            throw Fail(CCW_ERR_DIMENSION, "training image smaller than one 2^dwt_level block");
+        ti->F = nf;
+        ti->J = levels;
+        ti->nscr = std::max(nf - 1, 1);
+        ti->mode = (b <= 4 && ti->nscr <= 4) ? 0 : 1;
+        const size_t nc = static_cast<size_t>(ti->c[0]) * ti->c[1] * ti->c[2];
+        ti->d_codes = static_cast<uint8_t*>(ccwgpu::cache_alloc(ti->device, n));
+        ti->d_pk = static_cast<int32_t*>(
+            ccwgpu::cache_alloc(ti->device, sizeof(int32_t) * nc * (ti->mode == 0 ? 1 : ti->nscr)));
+        CCW_CUDA(cudaMemcpyAsync(ti->d_codes, cells, n, cudaMemcpyHostToDevice, ctx->stream));
+        ccwgpu::build_pyramid3d(ti, ctx->stream);
+    });
+    if (st != CCW_OK) {
+        ccw_ti3d_destroy(ti);
+        return st;
+    }
+    *out = ti;
+    return CCW_OK;
+}
+
+void ccw_ti3d_destroy(ccw_ti3d* ti) {
+    if (!ti) return;
+    cudaSetDevice(ti->device);
+    cudaDeviceSynchronize();
+    ccwgpu::cache_free(ti->d_codes);
+    ccwgpu::cache_free(ti->d_pk);
+    delete ti;
+}
+
+ccw_status ccw_validate_config3d(const ccw_sim3d_config* cfg, const int32_t* ti_dims, int nf, const int32_t* hd,
+                                 int n_hd, char* msg, size_t msg_len) {
+    try {
+        if (!cfg) throw Fail(CCW_ERR_GENERIC, "null config");
+        ccwgpu::validate_config3d(*cfg, ti_dims, nf, hd, n_hd);
+        copy_msg(msg, msg_len, "");
+        return CCW_OK;
+    } catch (const Fail& e) {
+        copy_msg(msg, msg_len, e.what());
+        g_err = e.what();
+        return e.code;
+    }
+}
+
+static void check_ti3d(ccw_ti3d* ti, const ccw_sim3d_config* cfg, const int32_t* hd, int n_hd) {
+    if (!cfg) throw Fail(CCW_ERR_GENERIC, "null config");
+    ccwgpu::validate_config3d(*cfg, ti->d, ti->F, hd, n_hd);
+    if (cfg->dwt_level != ti->J)
+        throw Fail(CCW_ERR_CONFIG, fmt("dwt_level: %d does not match the TI pyramid level %d", cfg->dwt_level, ti->J));
+}
+
+ccw_status ccw_simulate3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg, const uint64_t* seeds, int n_real,
+                          const int32_t* hd, int n_hd, uint8_t* out, ccw_diag3d* diag) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti3d(ti, cfg, hd, n_hd);
+        if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+        ccwgpu::run_simulation3d(ctx, ti, *cfg, seeds, n_real, hd, n_hd, nullptr, out, diag);
+    });
+}
+
+ccw_status ccw_simulate3d_trace(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg, const uint64_t* seeds,
+                                int n_real, const int32_t* hd, int n_hd, uint8_t* out, ccw_diag3d* diag,
+                                int32_t* ti_origins, int capacity) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti3d(ti, cfg, hd, n_hd);
+        if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+        if (!ti_origins || capacity < 1) throw Fail(CCW_ERR_GENERIC, "trace: null buffer or zero capacity");
+        ccwgpu::run_simulation3d(ctx, ti, *cfg, seeds, n_real, hd, n_hd, nullptr, out, diag, ti_origins, capacity);
+    });
+}
+
+ccw_status ccw_simulate3d_device(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg, const uint64_t* seeds,
+                                 int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, ccw_diag3d* diag) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti3d(ti, cfg, hd, n_hd);
+        if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+        ccwgpu::run_simulation3d(ctx, ti, *cfg, seeds, n_real, hd, n_hd, d_out, nullptr, diag);
+    });
+}
+
+ccw_status ccw_simulate3d_ensemble(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg, const int32_t* hd,
+                                   int n_hd, uint8_t* out, ccw_diag3d* diag) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti3d(ti, cfg, hd, n_hd);
+        std::vector<uint64_t> seeds(static_cast<size_t>(cfg->n_realizations));
+        for (int r = 0; r < cfg->n_realizations; ++r) seeds[r] = ccw_mix64(cfg->master_seed, static_cast<uint64_t>(r) + 1);
+        ccwgpu::run_simulation3d(ctx, ti, *cfg, seeds.data(), cfg->n_realizations, hd, n_hd, nullptr, out, diag);
     });
 }
 

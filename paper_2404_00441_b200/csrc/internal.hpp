@@ -304,6 +304,18 @@ struct ccw_ti {
     uint64_t key = 0;  // content key (hash of cells + shape) for per-context plan memory
 };
 
+// 3D training image (extension, ccw_ti3d_create): codes and level-J block
+// counts (mode 0: int8x4 packed channels, counts <= 64; mode 1: int32 planes).
+struct ccw_ti3d {
+    ccw_ctx* ctx = nullptr;
+    int device = 0;
+    int d[3] = {0, 0, 0};  // fine extents
+    int c[3] = {0, 0, 0};  // coarse extents (floor(d / 2^J))
+    int F = 0, J = 0, nscr = 0, mode = 0;
+    uint8_t* d_codes = nullptr;
+    int32_t* d_pk = nullptr;
+};
+
 namespace ccwgpu {
 
 // --- host logic shared by the ABI (abi.cpp) ------------------------------
@@ -339,6 +351,12 @@ void build_pyramid(ccw_ti* ti, cudaStream_t s);
 void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
                     int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out,
                     ccw_diag* diag, ccw_trace* traces);
+
+void build_pyramid3d(ccw_ti3d* ti, cudaStream_t s);
+void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, const uint64_t* seeds, int n_real,
+                      const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out, ccw_diag3d* diag,
+                      int32_t* trace = nullptr, int trace_cap = 0);
+void validate_config3d(const ccw_sim3d_config& c, const int32_t* ti_dims, int nf, const int32_t* hd, int n_hd);
 
 void op_dwt2_single(ccw_ctx* ctx, const double* in, int h, int w, double* a, double* dh,
                     double* dv, double* dd);

@@ -1,0 +1,934 @@
+// sim3d.cu -- the 3D CCWSIM extension (BASELINE configs 3 and 4) on sm_100a.
+//
+// The reference has no 3D; oracle/ccw3d_oracle.h is the
+// normative definition: the 2D algorithm of
+// simulator.hpp:148-252,418-519 / matcher.hpp:64-81,177-241 /
+// wavelet.hpp:69-106 generalized to three axes, scored EXACTLY from
+// per-facies block counts (a level-J 3D Haar apex is count / (2 sqrt 2)^J),
+// ranked by (score desc, row-major position asc).
+//
+// Device pipeline per placement wave (waves as in 2D: key
+// (d+1)^2 io + (d+1) im + ii orders every overlapping pair as the raster loop
+// does and lets the rest of a wave run concurrently):
+//
+//   prep3d    overlap block counts of every job from the resident work grid
+//             -> integer weights (n_f - n_{F-1}, the one-hot TI makes the
+//             F-1 channel sum rank exactly like the F channel sum)
+//   screen3d  exact integer CCF of a batch of up to 8 jobs sharing one mask
+//             over a box of TI window positions: the box's TI block counts
+//             staged in shared memory (row pitch padded so a warp's loads hit
+//             32 distinct banks), packed int8x4 channels + dp4a when every
+//             count fits int8 (J <= 2), int32 IMAD per channel otherwise; the
+//             box's top-K packed keys (score << 32 | ~position) per job
+//   [ncclAllGather of the shards' box lists when positions are sharded]
+//   select3d  merge of the box lists -> the job's top-K, conditional /
+//             unconditional pick, T^3 paste into the work grid
+//
+// and finalize3d crops the realizations and forces the hard data.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstring>
+
+#include "ccw_device.cuh"
+#include "internal.hpp"
+
+namespace ccwgpu {
+
+namespace {
+
+constexpr int JB = 8;       // jobs per screen batch (one mask)
+constexpr int KMAX3 = 16;   // candidates per job (3D path)
+constexpr int S3_THREADS = 256;
+
+struct Job3 {
+    int32_t real, place;
+    int32_t P[3];     // footprint origin in the work grid
+    int32_t mask;     // mask id = corner * 8 + shape (shape: bit a = slab on axis a)
+    int32_t pick;     // unconditional draw; -1 conditional; -2 first placement
+    int32_t fr[3];    // first placement's TI origin
+    int32_t lat;      // lattice cell of the footprint (hard-data lists)
+};
+
+struct Batch3 {
+    int32_t j0, n, mask, pad;
+};
+
+struct Geo3 {
+    int c[3];      // TI coarse extents used
+    int o[3];      // window positions per axis
+    int tc, B, J, T, OV, nscr, F;
+    int ti[3];     // TI fine extents (array dims)
+    int W[3];      // work grid extents
+    int sg[3];
+    int any_support;
+    int mode;      // 0: int8x4 counts + dp4a, 1: int32 per channel
+    int aligned4;  // paste may move 4-byte words
+};
+
+// ----------------------------------------------------------- pyramid -----
+// block counts of channels 0..nscr-1 (facies codes); mode 0: int8x4 packed
+// (counts <= 64), mode 1: int32 planes [ch][cell].
+__global__ void pyramid3d_kernel(const uint8_t* __restrict__ ti, int d0, int d1, int d2, int c0, int c1,
+                                 int c2, int B, int nscr, int mode, int32_t* __restrict__ out) {
+    const size_t nc = static_cast<size_t>(c0) * c1 * c2;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < nc;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int q0 = static_cast<int>(e / (static_cast<size_t>(c1) * c2));
+        const int q1 = static_cast<int>((e / c2) % c1), q2 = static_cast<int>(e % c2);
+        int cnt[16] = {0};
+        for (int x0 = 0; x0 < B; ++x0)
+            for (int x1 = 0; x1 < B; ++x1) {
+                const uint8_t* row = ti + (static_cast<size_t>(q0 * B + x0) * d1 + q1 * B + x1) * d2 + q2 * B;
+                for (int x2 = 0; x2 < B; ++x2) {
+                    const int f = row[x2];
+#pragma unroll
+                    for (int ch = 0; ch < 16; ++ch)
+                        if (ch == f) ++cnt[ch];
+                }
+            }
+        if (mode == 0) {
+            uint32_t v = 0;
+            for (int ch = 0; ch < nscr && ch < 4; ++ch) v |= (static_cast<uint32_t>(cnt[ch]) & 0xFFu) << (8 * ch);
+            out[e] = static_cast<int32_t>(v);
+        } else {
+            for (int ch = 0; ch < nscr; ++ch) out[ch * nc + e] = ch < 16 ? cnt[ch] : 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------- prep ------
+// One CTA per job, one warp per mask cell at a time: the overlap's facies
+// counts over the block's supported fine cells (simulator.hpp:225-272 in 3D).
+__global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restrict__ jobs, int j0,
+                                                     const int* __restrict__ mask_off,
+                                                     const int* __restrict__ mask_cells,
+                                                     const uint8_t* __restrict__ work, int32_t* __restrict__ wbuf,
+                                                     int wstride) {
+    pdl_trigger();
+    pdl_wait();
+    const Job3 jb = jobs[j0 + blockIdx.x];
+    const int corner = jb.mask >> 3, shape = jb.mask & 7;
+    const int m_lo = mask_off[jb.mask], nm = mask_off[jb.mask + 1] - m_lo;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int B = g.B, B3 = B * B * B;
+    const uint8_t* wk = work + static_cast<size_t>(jb.real) * g.W[0] * g.W[1] * g.W[2];
+    int32_t* wout = wbuf + static_cast<size_t>(blockIdx.x) * wstride;
+    for (int i = warp; i < nm; i += blockDim.x >> 5) {
+        const int cell = mask_cells[m_lo + i];
+        const int m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
+        int cnt[16] = {0};
+        for (int e = lane; e < B3; e += 32) {
+            const int x0 = m0 * B + e / (B * B), x1 = m1 * B + (e / B) % B, x2 = m2 * B + e % B;
+            const int x[3] = {x0, x1, x2};
+            bool sup = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if ((shape >> a) & 1) {
+                    const bool asc = !((corner >> a) & 1);
+                    sup |= asc ? x[a] < g.OV : x[a] >= g.T - g.OV;
+                }
+            if (!sup) continue;
+            const int f = wk[(static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] + jb.P[2] + x2];
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch)
+                if (ch == f) ++cnt[ch];
+        }
+        int wv[16];
+        const int last = g.F - 1;
+        int nlast = 0;
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+            const int s = __reduce_add_sync(0xffffffffu, cnt[ch]);
+            if (ch == last) nlast = s;
+            wv[ch] = s;
+        }
+#ifdef CCW_DEBUG3D
+        if (lane == 0 && blockIdx.x == 0) printf("prep job %d cell %d (%d,%d,%d) counts %d %d %d %d\n", j0, i, m0, m1, m2, wv[0], wv[1], wv[2], wv[3]);
+#endif
+        if (lane == 0) {
+            if (g.mode == 0) {  // int8x4
+                uint32_t v = 0;
+                for (int ch = 0; ch < g.nscr; ++ch) {
+                    const int w = g.F > 1 ? wv[ch] - nlast : 0;
+                    v |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * ch);
+                }
+                wout[i] = static_cast<int32_t>(v);
+            } else {
+                for (int ch = 0; ch < g.nscr; ++ch) wout[i * g.nscr + ch] = g.F > 1 ? wv[ch] - nlast : 0;
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------- screen ------
+struct Screen3Args {
+    Geo3 g;
+    const Job3* jobs;
+    const Batch3* batches;
+    int bt0;              // first batch of the wave
+    int j0;               // first job of the wave (wbuf / xbuf rows are wave-relative)
+    const int* mask_off;
+    const int* mask_cells;
+    const int32_t* tipk;  // packed TI block counts
+    const int32_t* wbuf;  // [job in wave][wstride]
+    int wstride;
+    int P0, P1, P2, W1;   // box shape (P1 = 4 W1, P0 = 8 / W1, P2 = 8 NP)
+    int nb[3];            // boxes per axis
+    int box0, box1;       // this launch's box range (one shard)
+    int bps;              // boxes per shard slot
+    int shard;            // shard slot of box0
+    int K;
+    int nj;               // jobs in the wave
+    unsigned long long* xbuf;  // [shard][nj][bps][K]
+};
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+    return a > b ? a : b;
+}
+
+__device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = umax64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int MODE, int NP>
+__global__ void __launch_bounds__(S3_THREADS) screen3d_kernel(Screen3Args a) {
+    extern __shared__ __align__(16) int32_t s3[];
+    pdl_trigger();
+    const Geo3& g = a.g;
+    const Batch3 bt = a.batches[a.bt0 + blockIdx.y];
+    const int box = a.box0 + blockIdx.x;
+    const int bx2 = box % a.nb[2], bx1 = (box / a.nb[2]) % a.nb[1], bx0 = box / (a.nb[2] * a.nb[1]);
+    const int B0 = bx0 * a.P0, B1 = bx1 * a.P1, B2 = bx2 * a.P2;
+    const int R0 = a.P0 + g.tc - 1, R1 = a.P1 + g.tc - 1, R2 = a.P2 + g.tc - 1;
+    const int R2p = R2 + ((8 - R2 % 32) + 32) % 32;  // row pitch = 8 mod 32 (conflict-free rows)
+    const int RV = R0 * R1 * R2p;                    // one channel's region
+    const int nch = MODE == 0 ? 1 : g.nscr;
+    const int m_lo = a.mask_off[bt.mask], nm = a.mask_off[bt.mask + 1] - m_lo;
+    int32_t* region = s3;
+    int32_t* moff = region + RV * nch;
+    int32_t* wsm = moff + ((nm + 3) & ~3);  // [nm][nch][JB]
+    const size_t ncell = static_cast<size_t>(g.c[0]) * g.c[1] * g.c[2];
+    // TI block counts of the box's window region (independent of earlier kernels)
+    for (int e = threadIdx.x; e < RV * nch; e += blockDim.x) {
+        const int ch = e / RV, r = e - ch * RV;
+        const int r2 = r % R2p, r1 = (r / R2p) % R1, r0 = r / (R2p * R1);
+        const int q0 = B0 + r0, q1 = B1 + r1, q2 = B2 + r2;
+        int32_t v = 0;
+        if (r2 < R2 && q0 < g.c[0] && q1 < g.c[1] && q2 < g.c[2])
+            v = a.tipk[ch * ncell + (static_cast<size_t>(q0) * g.c[1] + q1) * g.c[2] + q2];
+        region[e] = v;
+    }
+    for (int i = threadIdx.x; i < nm; i += blockDim.x) {
+        const int cell = a.mask_cells[m_lo + i];
+        moff[i] = ((cell >> 16) * R1 + ((cell >> 8) & 0xFF)) * R2p + (cell & 0xFF);
+    }
+    pdl_wait();  // weights (prep3d) ready; the previous select has read xbuf
+    for (int e = threadIdx.x; e < nm * nch * JB; e += blockDim.x) {
+        const int jb = e % JB, ich = e / JB;
+        wsm[e] = jb < bt.n ? a.wbuf[static_cast<size_t>(bt.j0 - a.j0 + jb) * a.wstride + ich] : 0;
+    }
+    __syncthreads();
+#ifdef CCW_DEBUG3D
+    if (threadIdx.x == 0 && blockIdx.x == 0) printf("screen bt j0 %d n %d mask %d nm %d w0 %x region0 %x P %d %d %d\n", bt.j0, bt.n, bt.mask, nm, wsm[0], region[0], a.P0, a.P1, a.P2);
+#endif
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = warp / a.W1, t1 = (warp % a.W1) * 4 + (lane >> 3), l2 = lane & 7;
+    const int base = (t0 * R1 + t1) * R2p + l2;
+    int acc[NP][JB];
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+#pragma unroll
+        for (int j = 0; j < JB; ++j) acc[k][j] = 0;
+    for (int i = 0; i < nm; ++i) {
+        const int o = base + moff[i];
+        if constexpr (MODE == 0) {
+            const int4 w0 = *reinterpret_cast<const int4*>(wsm + i * JB);
+            const int4 w1 = *reinterpret_cast<const int4*>(wsm + i * JB + 4);
+            const int wv[JB] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const int v = region[o + 8 * k];
+#pragma unroll
+                for (int j = 0; j < JB; ++j) acc[k][j] = __dp4a(v, wv[j], acc[k][j]);
+            }
+        } else {
+            for (int ch = 0; ch < nch; ++ch) {
+                const int4 w0 = *reinterpret_cast<const int4*>(wsm + (i * nch + ch) * JB);
+                const int4 w1 = *reinterpret_cast<const int4*>(wsm + (i * nch + ch) * JB + 4);
+                const int wv[JB] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    const int v = region[ch * RV + o + 8 * k];
+#pragma unroll
+                    for (int j = 0; j < JB; ++j) acc[k][j] += v * wv[j];
+                }
+            }
+        }
+    }
+    // packed keys: exact score (biased) above the complemented position, so
+    // the larger key is the better candidate (earlier position on ties)
+    const int p0 = B0 + t0, p1 = B1 + t1;
+    const bool row_ok = p0 < g.o[0] && p1 < g.o[1];
+    __syncthreads();  // (region reused below as the per-warp key lists)
+    unsigned long long* wk = reinterpret_cast<unsigned long long*>(s3);  // [JB][8 warps][K]
+    const int K = a.K;
+#pragma unroll
+    for (int j = 0; j < JB; ++j) {
+        if (j >= bt.n) break;
+        unsigned long long key[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            const int p2 = B2 + l2 + 8 * k;
+            key[k] = 0;
+            if (row_ok && p2 < g.o[2]) {
+                const uint32_t pos = static_cast<uint32_t>((p0 * g.o[1] + p1) * g.o[2] + p2);
+                key[k] = (static_cast<unsigned long long>(static_cast<uint32_t>(acc[k][j]) ^ 0x80000000u) << 32) |
+                         (0xFFFFFFFFu - pos);
+            }
+        }
+        for (int r = 0; r < K; ++r) {
+            unsigned long long m = 0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) m = umax64(m, key[k]);
+            const unsigned long long wm = warp_max64(m);
+#pragma unroll
+            for (int k = 0; k < NP; ++k)
+                if (key[k] == wm) key[k] = 0;  // keys are unique: one lane drops it
+            if (lane == 0) wk[(j * 8 + warp) * K + r] = wm;
+        }
+    }
+    __syncthreads();
+    // warp j merges job j's 8 warp lists
+    if (warp < bt.n) {
+        const int j = warp;
+        const int n = 8 * K;
+        unsigned long long c[(8 * KMAX3 + 31) / 32];
+#pragma unroll
+        for (int q = 0; q < (8 * KMAX3 + 31) / 32; ++q) {
+            const int e = lane + 32 * q;
+            c[q] = e < n ? wk[j * 8 * K + e] : 0;
+        }
+        unsigned long long* dst = a.xbuf + ((static_cast<size_t>(a.shard + (box - a.box0) / a.bps) * a.nj +
+                                             (bt.j0 - a.j0 + j)) * a.bps + (box - a.box0) % a.bps) * K;
+        for (int r = 0; r < K; ++r) {
+            unsigned long long m = 0;
+#pragma unroll
+            for (int q = 0; q < (8 * KMAX3 + 31) / 32; ++q) m = umax64(m, c[q]);
+            const unsigned long long wm = warp_max64(m);
+#pragma unroll
+            for (int q = 0; q < (8 * KMAX3 + 31) / 32; ++q)
+                if (c[q] == wm) c[q] = 0;
+            if (lane == 0) dst[r] = wm;
+        }
+    }
+}
+
+// ----------------------------------------------------------- select ------
+struct Select3Args {
+    Geo3 g;
+    const Job3* jobs;
+    int j0, nj;
+    const unsigned long long* xbuf;  // [S][nj][bps][K]
+    int S, bps, nbox, K, Kp;
+    const int* hd_off;          // CSR per lattice cell (may be null)
+    const uint32_t* hd_ent;     // (x0 << 20 | x1 << 10 | x2) local offset, facies in a second word
+    const uint8_t* hd_fac;
+    const uint8_t* ti;
+    uint8_t* work;
+    int32_t* chosen;            // [job][3]
+};
+
+__device__ __forceinline__ unsigned long long block_max64(unsigned long long v, unsigned long long* red) {
+    v = warp_max64(v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    unsigned long long m = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = umax64(m, red[w]);
+    return m;
+}
+
+__device__ __forceinline__ int block_sum(int v, int* red) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    int s = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
+    return s;
+}
+
+__global__ void __launch_bounds__(128) select3d_kernel(Select3Args a) {
+    __shared__ unsigned long long red[4];
+    __shared__ int redi[4];
+    __shared__ unsigned long long cands[KMAX3];
+    __shared__ int fr_s[3];
+    pdl_trigger();
+    pdl_wait();
+    const Geo3& g = a.g;
+    const int jw = blockIdx.x;
+    const Job3 jb = a.jobs[a.j0 + jw];
+    if (jb.pick == -2) {
+        if (threadIdx.x < 3) fr_s[threadIdx.x] = jb.fr[threadIdx.x];
+    } else {
+        // top-K of the boxes' lists: K rounds of "largest key below the last"
+        const int per = a.bps * a.K;
+        const int total = a.S * per;
+        unsigned long long prev = ~0ull;
+        for (int r = 0; r < a.Kp; ++r) {
+            unsigned long long m = 0;
+            for (int e = threadIdx.x; e < total; e += blockDim.x) {
+                const int s = e / per, rem = e - s * per;
+                if (s * a.bps + rem / a.K >= a.nbox) continue;
+                const unsigned long long v = a.xbuf[(static_cast<size_t>(s) * a.nj + jw) * per + rem];
+                if (v < prev) m = umax64(m, v);
+            }
+            m = block_max64(m, red);
+            if (threadIdx.x == 0) cands[r] = m;
+            prev = m;
+        }
+        __syncthreads();
+#ifdef CCW_DEBUG3D
+        if (threadIdx.x == 0) printf("select job %d cands %llx %llx total %d per %d nbox %d\n", a.j0 + jw, cands[0], a.Kp > 1 ? cands[1] : 0ull, total, per, a.nbox);
+#endif
+        int pick = jb.pick;
+        if (pick < 0) {  // select_conditional (matcher.hpp:222-241)
+            const int h0 = a.hd_off[jb.lat], nh = a.hd_off[jb.lat + 1] - h0;
+            int best = 0, best_m = nh + 1;
+            for (int ci = 0; ci < a.Kp; ++ci) {
+                const uint32_t pos = 0xFFFFFFFFu - static_cast<uint32_t>(cands[ci] & 0xFFFFFFFFull);
+                const int q2 = pos % g.o[2], q1 = (pos / g.o[2]) % g.o[1], q0 = pos / (g.o[2] * g.o[1]);
+                int mm = 0;
+                for (int e = threadIdx.x; e < nh; e += blockDim.x) {
+                    const uint32_t off = a.hd_ent[h0 + e];
+                    const int x0 = off >> 20, x1 = (off >> 10) & 1023, x2 = off & 1023;
+                    const size_t t = (static_cast<size_t>(q0 * g.B + x0) * g.ti[1] + q1 * g.B + x1) * g.ti[2] +
+                                     q2 * g.B + x2;
+                    mm += a.ti[t] != a.hd_fac[h0 + e];
+                }
+                mm = block_sum(mm, redi);
+                if (mm == 0) {
+                    best = ci;
+                    break;
+                }
+                if (mm < best_m) {
+                    best_m = mm;
+                    best = ci;
+                }
+            }
+            pick = best;
+        }
+        if (threadIdx.x == 0) {
+            const uint32_t pos = 0xFFFFFFFFu - static_cast<uint32_t>(cands[pick] & 0xFFFFFFFFull);
+            fr_s[2] = pos % g.o[2] * g.B;
+            fr_s[1] = (pos / g.o[2]) % g.o[1] * g.B;
+            fr_s[0] = pos / (g.o[2] * g.o[1]) * g.B;
+        }
+    }
+    __syncthreads();
+    const int f0 = fr_s[0], f1 = fr_s[1], f2 = fr_s[2];
+    if (threadIdx.x < 3) a.chosen[3 * (a.j0 + jw) + threadIdx.x] = fr_s[threadIdx.x];
+    // crop + paste_into (grid.hpp:172-230): T^3 cells, 4-byte words where aligned
+    uint8_t* wk = a.work + static_cast<size_t>(jb.real) * g.W[0] * g.W[1] * g.W[2];
+    const int T = g.T;
+    const size_t rows = static_cast<size_t>(T) * T;
+    if (g.aligned4) {  // every row start is 4-byte aligned on both sides
+        const int T4 = T >> 2;
+        for (size_t e = threadIdx.x; e < rows * T4; e += blockDim.x) {
+            const int x2 = static_cast<int>(e % T4) * 4;
+            const size_t rr = e / T4;
+            const int x1 = static_cast<int>(rr % T), x0 = static_cast<int>(rr / T);
+            *reinterpret_cast<uint32_t*>(wk + (static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] +
+                                         jb.P[2] + x2) =
+                *reinterpret_cast<const uint32_t*>(a.ti + (static_cast<size_t>(f0 + x0) * g.ti[1] + f1 + x1) * g.ti[2] +
+                                                   f2 + x2);
+        }
+        return;
+    }
+    for (size_t e = threadIdx.x; e < rows * T; e += blockDim.x) {
+        const int x2 = static_cast<int>(e % T);
+        const size_t rr = e / T;
+        const int x1 = static_cast<int>(rr % T), x0 = static_cast<int>(rr / T);
+        wk[(static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] + jb.P[2] + x2] =
+            a.ti[(static_cast<size_t>(f0 + x0) * g.ti[1] + f1 + x1) * g.ti[2] + f2 + x2];
+    }
+}
+
+// --------------------------------------------------------- finalize ------
+__global__ void finalize3d_kernel(const uint8_t* __restrict__ work, int W0, int W1, int W2, int s0, int s1,
+                                  int s2, uint8_t* __restrict__ out) {
+    pdl_wait();
+    const int r = blockIdx.y;
+    const size_t n = static_cast<size_t>(s0) * s1 * s2;
+    const uint8_t* wk = work + static_cast<size_t>(r) * W0 * W1 * W2;
+    uint8_t* o = out + static_cast<size_t>(r) * n;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int x2 = static_cast<int>(e % s2);
+        const size_t rr = e / s2;
+        const int x1 = static_cast<int>(rr % s1), x0 = static_cast<int>(rr / s1);
+        o[e] = wk[(static_cast<size_t>(x0) * W1 + x1) * W2 + x2];
+    }
+}
+
+// hard-data overwrite with the pre-overwrite mismatch count (simulator.hpp:506-513)
+__global__ void hd3d_kernel(const int32_t* __restrict__ hd, int n_hd, int s0, int s1, int s2, uint8_t* out,
+                            int* mism) {
+    const int r = blockIdx.y;
+    const size_t n = static_cast<size_t>(s0) * s1 * s2;
+    int local = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_hd; i += gridDim.x * blockDim.x) {
+        const int* d = hd + 4 * i;
+        uint8_t* c = out + r * n + (static_cast<size_t>(d[0]) * s1 + d[1]) * s2 + d[2];
+        local += *c != d[3];
+        *c = static_cast<uint8_t>(d[3]);
+    }
+    local = __reduce_add_sync(0xffffffffu, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(&mism[r], local);
+}
+
+int padded_extent3(int sg, int t, int stride) {  // simulator.hpp:125-131
+    if (sg == t) return t;
+    return t + (sg - t + stride - 1) / stride * stride;
+}
+
+const int kOrders[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+}  // namespace
+
+// ------------------------------------------------------------ host -------
+
+void build_pyramid3d(ccw_ti3d* ti, cudaStream_t st) {
+    const size_t nc = static_cast<size_t>(ti->c[0]) * ti->c[1] * ti->c[2];
+    const int nb = static_cast<int>(std::min<size_t>((nc + 255) / 256, 4096));
+    pyramid3d_kernel<<<std::max(nb, 1), 256, 0, st>>>(ti->d_codes, ti->d[0], ti->d[1], ti->d[2], ti->c[0], ti->c[1],
+                                                     ti->c[2], 1 << ti->J, ti->nscr, ti->mode,
+                                                     ti->d_pk);
+    CCW_CUDA(cudaGetLastError());
+}
+
+void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, const uint64_t* seeds, int n_real,
+                      const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out, ccw_diag3d* diag,
+                      int32_t* trace, int trace_cap) {
+    const auto wall0 = std::chrono::steady_clock::now();
+    cudaStream_t st = ctx->stream;
+    Geo3 g{};
+    g.J = cfg.dwt_level;
+    g.B = 1 << g.J;
+    g.T = cfg.template_size;
+    g.OV = cfg.overlap;
+    g.tc = g.T >> g.J;
+    g.nscr = ti->nscr;
+    g.F = ti->F;
+    g.any_support = cfg.any_support;
+    g.mode = ti->mode;
+    const int stride = g.T - g.OV;
+    for (int a = 0; a < 3; ++a) {
+        g.c[a] = ti->c[a];
+        g.o[a] = g.c[a] - g.tc + 1;
+        g.ti[a] = ti->d[a];
+        g.sg[a] = cfg.sg[a];
+        g.W[a] = padded_extent3(cfg.sg[a], g.T, stride);
+    }
+    g.aligned4 = (g.W[2] % 4 == 0 && g.ti[2] % 4 == 0 && stride % 4 == 0 && g.B % 4 == 0 && g.T % 4 == 0) ? 1 : 0;
+    const int64_t npos64 = static_cast<int64_t>(g.o[0]) * g.o[1] * g.o[2];
+    if (npos64 >= (int64_t(1) << 31)) throw Fail(CCW_ERR_CONFIG, "3D: too many TI window positions");
+    const int npos = static_cast<int>(npos64);
+    const int Kp = static_cast<int>(std::min<int64_t>(cfg.candidates, npos));
+    if (Kp > KMAX3) throw Fail(CCW_ERR_CONFIG, "candidates: the 3D path supports at most 16 candidates");
+    if (g.tc > 255 || g.T >= 1024) throw Fail(CCW_ERR_CONFIG, "3D: template too large");
+    // exactness of the int32 screen: |S'| <= mask * B^3 * B^3 <= T^3 * B^3
+    if (static_cast<double>(g.T) * g.T * g.T * g.B * g.B * g.B >= 2147483647.0)
+        throw Fail(CCW_ERR_CONFIG, "3D: template^3 * block^3 exceeds the exact int32 screen range");
+    const int n_lat[3] = {(g.W[0] - g.T) / stride + 1, (g.W[1] - g.T) / stride + 1, (g.W[2] - g.T) / stride + 1};
+    const int reach = (g.T + stride - 1) / stride - 1;
+    const int km = reach + 1;
+
+    // ---- host schedule: plans, draws (the whole mt19937_64 sequence is a
+    // function of the geometry: conditional placements draw nothing) ----
+    const size_t nlat = static_cast<size_t>(n_lat[0]) * n_lat[1] * n_lat[2];
+    std::vector<int32_t> hd_off(nlat + 1, 0);
+    std::vector<uint32_t> hd_ent;
+    std::vector<uint8_t> hd_fac;
+    if (hd && n_hd > 0) {
+        auto each = [&](int i, auto&& fn) {
+            const int* d = hd + 4 * i;
+            int lo[3], hi[3];
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::max(0, (d[a] - g.T + 1 + stride - 1) / stride);
+                hi[a] = std::min(n_lat[a] - 1, d[a] / stride);
+            }
+            for (int q0 = lo[0]; q0 <= hi[0]; ++q0)
+                for (int q1 = lo[1]; q1 <= hi[1]; ++q1)
+                    for (int q2 = lo[2]; q2 <= hi[2]; ++q2) {
+                        const int q[3] = {q0, q1, q2};
+                        bool in = true;
+                        for (int a = 0; a < 3; ++a) in &= d[a] >= q[a] * stride && d[a] < q[a] * stride + g.T;
+                        if (in)
+                            fn((static_cast<size_t>(q0) * n_lat[1] + q1) * n_lat[2] + q2, d[0] - q0 * stride,
+                               d[1] - q1 * stride, d[2] - q2 * stride, d[3]);
+                    }
+        };
+        for (int i = 0; i < n_hd; ++i) each(i, [&](size_t q, int, int, int, int) { ++hd_off[q + 1]; });
+        for (size_t q = 0; q < nlat; ++q) hd_off[q + 1] += hd_off[q];
+        hd_ent.resize(hd_off[nlat]);
+        hd_fac.resize(hd_off[nlat]);
+        std::vector<int32_t> fill(hd_off.begin(), hd_off.end() - 1);
+        for (int i = 0; i < n_hd; ++i)
+            each(i, [&](size_t q, int x0, int x1, int x2, int f) {
+                hd_ent[fill[q]] = (static_cast<uint32_t>(x0) << 20) | (static_cast<uint32_t>(x1) << 10) |
+                                  static_cast<uint32_t>(x2);
+                hd_fac[fill[q]++] = static_cast<uint8_t>(f);
+            });
+    }
+    struct Pl {
+        int wave, mask;
+        Job3 j;
+    };
+    std::vector<Pl> pls;
+    std::vector<int> corners(n_real), orders(n_real), counts(n_real);
+    int max_key = 0;
+    std::vector<char> mask_used(64, 0);
+    for (int r = 0; r < n_real; ++r) {
+        std::mt19937_64 rng(seeds[r]);
+        const int corner = static_cast<int>(bounded(rng, 8));
+        const int order = static_cast<int>(bounded(rng, 6));
+        corners[r] = corner;
+        orders[r] = order;
+        const int* ord = kOrders[order];
+        const int n0 = n_lat[ord[0]], n1 = n_lat[ord[1]], n2 = n_lat[ord[2]];
+        counts[r] = n0 * n1 * n2;
+        int place = 0;
+        for (int io = 0; io < n0; ++io)
+            for (int im = 0; im < n1; ++im)
+                for (int ii = 0; ii < n2; ++ii, ++place) {
+                    int idx[3];
+                    idx[ord[0]] = io;
+                    idx[ord[1]] = im;
+                    idx[ord[2]] = ii;
+                    Pl p{};
+                    p.j.real = r;
+                    p.j.place = place;
+                    int sh = 0, lat[3];
+                    for (int a = 0; a < 3; ++a) {
+                        const bool asc = !((corner >> a) & 1);
+                        lat[a] = asc ? idx[a] : n_lat[a] - 1 - idx[a];
+                        p.j.P[a] = lat[a] * stride;
+                        if (idx[a] > 0) sh |= 1 << a;
+                    }
+                    p.j.lat = static_cast<int>((static_cast<size_t>(lat[0]) * n_lat[1] + lat[1]) * n_lat[2] + lat[2]);
+                    p.j.mask = corner * 8 + sh;
+                    p.mask = p.j.mask;
+                    p.wave = km * km * io + km * im + ii;
+                    max_key = std::max(max_key, p.wave);
+                    if (sh == 0) {
+                        p.j.pick = -2;
+                        for (int a = 0; a < 3; ++a)
+                            p.j.fr[a] = static_cast<int>(bounded(rng, static_cast<uint64_t>((ti->c[a] * g.B - g.T) / g.B + 1))) * g.B;
+                    } else {
+                        const bool cond = !hd_off.empty() && hd_off[p.j.lat + 1] > hd_off[p.j.lat];
+                        p.j.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
+                        mask_used[p.j.mask] = 1;
+                    }
+                    pls.push_back(p);
+                }
+    }
+    // mask cell lists (row-major coarse cells of the block-level mask)
+    std::vector<int> mask_off(65, 0), mask_cells;
+    int max_nm = 0;
+    for (int id = 0; id < 64; ++id) {
+        mask_off[id] = static_cast<int>(mask_cells.size());
+        if (mask_used[id]) {
+            const int corner = id >> 3, sh = id & 7;
+            const int tc = g.tc, B = g.B;
+            for (int m0 = 0; m0 < tc; ++m0)
+                for (int m1 = 0; m1 < tc; ++m1)
+                    for (int m2 = 0; m2 < tc; ++m2) {
+                        const int m[3] = {m0, m1, m2};
+                        bool any = false;
+                        for (int a = 0; a < 3; ++a)
+                            if ((sh >> a) & 1) {
+                                const bool asc = !((corner >> a) & 1);
+                                // block [m*B, m*B+B) touches the slab [0, OV) / [T-OV, T)
+                                any |= asc ? m[a] * B < g.OV : m[a] * B + B > g.T - g.OV;
+                            }
+                        if (any) mask_cells.push_back((m0 << 16) | (m1 << 8) | m2);
+                    }
+        }
+        max_nm = std::max(max_nm, static_cast<int>(mask_cells.size()) - mask_off[id]);
+    }
+    mask_off[64] = static_cast<int>(mask_cells.size());
+    // waves -> batches of jobs sharing one mask
+    std::stable_sort(pls.begin(), pls.end(), [](const Pl& x, const Pl& y) {
+        return x.wave != y.wave ? x.wave < y.wave : x.mask < y.mask;
+    });
+    const size_t njobs = pls.size();
+    std::vector<Job3> jobs(njobs);
+    std::vector<Batch3> batches;
+    std::vector<int> wave_j0(max_key + 2, 0), wave_b0(max_key + 2, 0);
+    {
+        size_t k = 0;
+        for (int w = 0; w <= max_key; ++w) {
+            wave_j0[w] = static_cast<int>(k);
+            wave_b0[w] = static_cast<int>(batches.size());
+            while (k < njobs && pls[k].wave == w) {
+                size_t e = k;
+                while (e < njobs && pls[e].wave == w && pls[e].mask == pls[k].mask && e - k < JB) ++e;
+                if (pls[k].j.pick != -2) batches.push_back({static_cast<int>(k), static_cast<int>(e - k), pls[k].mask, 0});
+                k = e;
+            }
+        }
+        wave_j0[max_key + 1] = static_cast<int>(njobs);
+        wave_b0[max_key + 1] = static_cast<int>(batches.size());
+        for (size_t i = 0; i < njobs; ++i) jobs[i] = pls[i].j;
+    }
+    int max_wave = 1;
+    for (int w = 0; w <= max_key; ++w) max_wave = std::max(max_wave, wave_j0[w + 1] - wave_j0[w]);
+
+    // ---- box shape: P2 = 8 NP along axis 2, P1 = 4 W1, P0 = 8 / W1 ----
+    int best_np = 2, best_w1 = 2;
+    double best_v = 1e300;
+    for (int np : {4, 2, 1})
+        for (int w1 : {1, 2, 4, 8}) {
+            const int P[3] = {8 / w1, 4 * w1, 8 * np};
+            double v = 1;
+            for (int a = 0; a < 3; ++a) v *= static_cast<double>((g.o[a] + P[a] - 1) / P[a]) * P[a];
+            v *= 1.0 + 0.02 * (4 - np);  // prefer more positions per thread on ties
+            if (v < best_v) {
+                best_v = v;
+                best_np = np;
+                best_w1 = w1;
+            }
+        }
+    const int P0 = 8 / best_w1, P1 = 4 * best_w1, P2 = 8 * best_np;
+    const int nb[3] = {(g.o[0] + P0 - 1) / P0, (g.o[1] + P1 - 1) / P1, (g.o[2] + P2 - 1) / P2};
+    const int nbox = nb[0] * nb[1] * nb[2];
+    const int mode = ti->mode;
+    const int nch = mode == 0 ? 1 : g.nscr;
+    const int R0 = P0 + g.tc - 1, R1 = P1 + g.tc - 1, R2 = P2 + g.tc - 1;
+    const int R2p = R2 + ((8 - R2 % 32) + 32) % 32;
+    const size_t smem = sizeof(int32_t) * (static_cast<size_t>(R0) * R1 * R2p * nch + ((max_nm + 3) & ~3) +
+                                           static_cast<size_t>(max_nm) * nch * JB);
+    const size_t smem_keys = sizeof(unsigned long long) * JB * 8 * KMAX3;
+    const size_t smem_tot = std::max(smem, smem_keys);
+    if (smem_tot > 227 * 1024) throw Fail(CCW_ERR_CONFIG, "3D: screen tile exceeds the shared-memory budget");
+
+    // ---- position shards (ccw_ctx_set_position_shards) ----
+    const int S_virt = ctx->shard_virtual, S_ranks = ctx->shard_nranks, S = S_virt * S_ranks;
+    if (nbox < S) throw Fail(CCW_ERR_CONFIG, "position shards: more shards than 3D screen boxes");
+    const int bps = (nbox + S - 1) / S;
+
+    // ---- device buffers ----
+    const size_t wvol = static_cast<size_t>(g.W[0]) * g.W[1] * g.W[2];
+    uint8_t* d_work = ctx->work.as<uint8_t>(wvol * n_real);
+    CCW_CUDA(cudaMemsetAsync(d_work, 0, wvol * n_real, st));
+    Job3* d_jobs = reinterpret_cast<Job3*>(ctx->jobs.get(sizeof(Job3) * njobs + 16));
+    CCW_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(Job3) * njobs, cudaMemcpyHostToDevice, st));
+    Batch3* d_bt = reinterpret_cast<Batch3*>(ctx->ops_a.get(sizeof(Batch3) * std::max<size_t>(1, batches.size())));
+    if (!batches.empty())
+        CCW_CUDA(cudaMemcpyAsync(d_bt, batches.data(), sizeof(Batch3) * batches.size(), cudaMemcpyHostToDevice, st));
+    int* d_moff = reinterpret_cast<int*>(ctx->ops_b.get(sizeof(int) * (65 + mask_cells.size() + 1)));
+    int* d_mcells = d_moff + 65;
+    CCW_CUDA(cudaMemcpyAsync(d_moff, mask_off.data(), sizeof(int) * 65, cudaMemcpyHostToDevice, st));
+    if (!mask_cells.empty())
+        CCW_CUDA(cudaMemcpyAsync(d_mcells, mask_cells.data(), sizeof(int) * mask_cells.size(), cudaMemcpyHostToDevice,
+                                 st));
+    const int wstride = std::max(1, max_nm * nch);
+    int32_t* d_w = ctx->wts.as<int32_t>(static_cast<size_t>(max_wave) * wstride);
+    unsigned long long* d_x =
+        ctx->xrec.as<unsigned long long>(static_cast<size_t>(S) * max_wave * bps * std::max(Kp, 1));
+    int32_t* d_chosen = ctx->chosen.as<int32_t>(3 * njobs);
+    int* d_hdoff = nullptr;
+    uint32_t* d_hdent = nullptr;
+    uint8_t* d_hdfac = nullptr;
+    int32_t* d_hd = nullptr;
+    if (hd && n_hd > 0) {
+        d_hdoff = ctx->hdoff.as<int32_t>(hd_off.size());
+        CCW_CUDA(cudaMemcpyAsync(d_hdoff, hd_off.data(), sizeof(int32_t) * hd_off.size(), cudaMemcpyHostToDevice, st));
+        d_hdent = ctx->hdent.as<uint32_t>(std::max<size_t>(1, hd_ent.size()) * 2);
+        d_hdfac = reinterpret_cast<uint8_t*>(d_hdent + std::max<size_t>(1, hd_ent.size()));
+        if (!hd_ent.empty()) {
+            CCW_CUDA(cudaMemcpyAsync(d_hdent, hd_ent.data(), sizeof(uint32_t) * hd_ent.size(), cudaMemcpyHostToDevice,
+                                     st));
+            CCW_CUDA(cudaMemcpyAsync(d_hdfac, hd_fac.data(), hd_fac.size(), cudaMemcpyHostToDevice, st));
+        }
+        d_hd = reinterpret_cast<int32_t*>(ctx->hd.get(sizeof(int32_t) * 4 * n_hd));
+        CCW_CUDA(cudaMemcpyAsync(d_hd, hd, sizeof(int32_t) * 4 * n_hd, cudaMemcpyHostToDevice, st));
+    }
+    int* d_mism = ctx->mism.as<int>(n_real);
+    CCW_CUDA(cudaMemsetAsync(d_mism, 0, sizeof(int) * n_real, st));
+    const size_t sgvol = static_cast<size_t>(cfg.sg[0]) * cfg.sg[1] * cfg.sg[2];
+    uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(sgvol * n_real);
+
+    void (*screen)(Screen3Args) = nullptr;
+    if (mode == 0)
+        screen = best_np == 4 ? screen3d_kernel<0, 4> : best_np == 2 ? screen3d_kernel<0, 2> : screen3d_kernel<0, 1>;
+    else
+        screen = best_np == 4 ? screen3d_kernel<1, 4> : best_np == 2 ? screen3d_kernel<1, 2> : screen3d_kernel<1, 1>;
+    CCW_CUDA(cudaFuncSetAttribute(screen, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_tot)));
+
+    Screen3Args sa{};
+    sa.g = g;
+    sa.jobs = d_jobs;
+    sa.batches = d_bt;
+    sa.mask_off = d_moff;
+    sa.mask_cells = d_mcells;
+    sa.tipk = ti->d_pk;
+    sa.wbuf = d_w;
+    sa.wstride = wstride;
+    sa.P0 = P0;
+    sa.P1 = P1;
+    sa.P2 = P2;
+    sa.W1 = best_w1;
+    for (int a = 0; a < 3; ++a) sa.nb[a] = nb[a];
+    sa.bps = bps;
+    sa.K = std::max(Kp, 1);
+    sa.xbuf = d_x;
+    Select3Args se{};
+    se.g = g;
+    se.jobs = d_jobs;
+    se.xbuf = d_x;
+    se.S = S;
+    se.bps = bps;
+    se.nbox = nbox;
+    se.K = std::max(Kp, 1);
+    se.Kp = Kp;
+    se.hd_off = d_hdoff;
+    se.hd_ent = d_hdent;
+    se.hd_fac = d_hdfac;
+    se.ti = ti->d_codes;
+    se.work = d_work;
+    se.chosen = d_chosen;
+
+    cudaEvent_t ev0, ev1;
+    CCW_CUDA(cudaEventCreate(&ev0));
+    CCW_CUDA(cudaEventCreate(&ev1));
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ccf_ev;
+    CCW_CUDA(cudaEventRecord(ev0, st));
+    int64_t launches = 0, ccf_launches = 0;
+    double ccf_flop = 0;
+    for (int w = 0; w <= max_key; ++w) {
+        const int j0 = wave_j0[w], nj = wave_j0[w + 1] - j0;
+        if (nj == 0) continue;
+        const int b0 = wave_b0[w], nbt = wave_b0[w + 1] - b0;
+        if (nbt > 0) {
+            launch_pdl(prep3d_kernel, dim3(nj), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
+                       static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
+                       static_cast<const uint8_t*>(d_work), d_w, wstride);
+            ++launches;
+            cudaEvent_t ea = nullptr, eb = nullptr;
+            if (ctx->profiling) {
+                CCW_CUDA(cudaEventCreate(&ea));
+                CCW_CUDA(cudaEventCreate(&eb));
+                CCW_CUDA(cudaEventRecord(ea, st));
+            }
+            Screen3Args q = sa;
+            q.bt0 = b0;
+            q.j0 = j0;
+            q.nj = nj;
+            for (int v = 0; v < S_virt; ++v) {
+                const int s = ctx->shard_rank * S_virt + v;
+                q.box0 = std::min(nbox, s * bps);
+                q.box1 = std::min(nbox, (s + 1) * bps);
+                q.shard = s;
+                if (q.box1 <= q.box0) continue;
+                launch_pdl(screen, dim3(q.box1 - q.box0, nbt), dim3(S3_THREADS), smem_tot, st, q);
+                ++launches;
+                ++ccf_launches;
+            }
+            if (ctx->profiling) {
+                CCW_CUDA(cudaEventRecord(eb, st));
+                ccf_ev.push_back({ea, eb});
+            }
+            for (int b = b0; b < b0 + nbt; ++b) {
+                const int nm = mask_off[batches[b].mask + 1] - mask_off[batches[b].mask];
+                ccf_flop += 2.0 * g.F * static_cast<double>(npos) * nm * batches[b].n;
+            }
+            if (ctx->nccl_comm) {
+                const size_t chunk = static_cast<size_t>(S_virt) * nj * bps * sa.K;
+                nccl_all_gather_bytes(ctx->nccl_comm, d_x + ctx->shard_rank * chunk, d_x,
+                                      chunk * sizeof(unsigned long long), st);
+            }
+        }
+        Select3Args q = se;
+        q.j0 = j0;
+        q.nj = nj;
+        launch_pdl(select3d_kernel, dim3(nj), dim3(128), 0, st, q);
+        ++launches;
+    }
+    {
+        const size_t n = sgvol;
+        const int bx = static_cast<int>(std::min<size_t>((n + 255) / 256, 2048));
+        launch_pdl(finalize3d_kernel, dim3(bx, n_real), dim3(256), 0, st, static_cast<const uint8_t*>(d_work), g.W[0],
+                   g.W[1], g.W[2], cfg.sg[0], cfg.sg[1], cfg.sg[2], fin);
+        ++launches;
+        if (d_hd) {
+            hd3d_kernel<<<dim3(std::min((n_hd + 255) / 256, 256), n_real), 256, 0, st>>>(
+                d_hd, n_hd, cfg.sg[0], cfg.sg[1], cfg.sg[2], fin, d_mism);
+            CCW_CUDA(cudaGetLastError());
+            ++launches;
+        }
+    }
+    CCW_CUDA(cudaEventRecord(ev1, st));
+    if (h_out) CCW_CUDA(cudaMemcpyAsync(h_out, fin, sgvol * n_real, cudaMemcpyDeviceToHost, st));
+    std::vector<int> mism(n_real, 0);
+    CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> chosen;
+    if (trace) {
+        chosen.resize(3 * njobs);
+        CCW_CUDA(cudaMemcpyAsync(chosen.data(), d_chosen, sizeof(int32_t) * chosen.size(), cudaMemcpyDeviceToHost, st));
+    }
+    CCW_CUDA(cudaStreamSynchronize(st));
+    if (trace)  // provenance: TI fine origin of every placement, raster order per realization
+        for (size_t k = 0; k < njobs; ++k)
+            if (jobs[k].place < trace_cap)
+                for (int a = 0; a < 3; ++a)
+                    trace[(static_cast<size_t>(jobs[k].real) * trace_cap + jobs[k].place) * 3 + a] = chosen[3 * k + a];
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    double ccf_ms = 0;
+    for (auto& e : ccf_ev) {
+        float m = 0;
+        cudaEventElapsedTime(&m, e.first, e.second);
+        ccf_ms += m;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    ctx->timing = ccw_timing{};
+    ctx->timing.total_ms = ms;
+    ctx->timing.ccf_ms = ccf_ms;
+    ctx->timing.ccf_launches = static_cast<int64_t>(ccf_ev.size());
+    ctx->timing.launches = launches;
+    ctx->timing.ccf_flop = ccf_flop;
+    ctx->timing.ccf_flop_ref = ccf_flop;
+    ctx->timing.waves = max_key + 1;
+    ctx->timing.jobs = static_cast<int64_t>(njobs);
+    ctx->timing.screened_jobs = static_cast<int64_t>(njobs) - n_real;
+    ctx->timing.ccf_variant = mode == 0 ? 3 : 4;
+    ctx->timing.groups = 1;
+    ctx->timing.d2h_bytes = h_out ? static_cast<int64_t>(sgvol * n_real) : 0;
+    (void)ccf_launches;
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    if (diag)
+        for (int r = 0; r < n_real; ++r) {
+            ccw_diag3d& d = diag[r];
+            d.seed = seeds[r];
+            d.corner = corners[r];
+            d.order = orders[r];
+            for (int a = 0; a < 3; ++a) d.work[a] = g.W[a];
+            d.placement_count = counts[r];
+            d.hard_data_count = hd ? n_hd : 0;
+            d.pre_overwrite_mismatches = mism[r];
+            d.wall_seconds = wall;
+        }
+}
+
+}  // namespace ccwgpu

@@ -118,3 +118,141 @@ def config2_hard_data(ti: np.ndarray, realization: np.ndarray | None = None) -> 
         cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1)
         realization = cs.simulate_one(grid, cfg, 777).realization.cells
     return hard_data_from(realization, 0.01, seed=606)
+
+
+# --------------------------------------------------------------- 3D (c3, c4) --
+# Arrays are (d0, d1, d2) = (z, y, x): axis 0 is vertical, so BASELINE's
+# "X x Y x Z" extents appear reversed.
+
+def _ellipsoid(vol: np.ndarray, rng: Mt19937_64, code: int, axes=(5.0, 40.0), flat: float = 0.35,
+               only_on=None) -> None:
+    """One ellipsoidal lens of ``code``: horizontal semi-axes drawn in
+    ``axes``, vertical semi-axis ``flat`` times the smaller one, random
+    azimuth and a small dip; written over ``only_on`` cells (None = any)."""
+    d0, d1, d2 = vol.shape
+    a = _uniform(rng, *axes)
+    b = _uniform(rng, axes[0], a)
+    c = max(1.5, flat * b)
+    z0, y0, x0 = _uniform(rng, 0, d0), _uniform(rng, 0, d1), _uniform(rng, 0, d2)
+    az = _uniform(rng, 0, np.pi)
+    dip = _uniform(rng, -0.15, 0.15)
+    r = int(np.ceil(a)) + 1
+    zs = slice(max(0, int(z0 - c - 2 - r * abs(dip))), min(d0, int(z0 + c + 2 + r * abs(dip)) + 1))
+    ys = slice(max(0, int(y0) - r), min(d1, int(y0) + r + 1))
+    xs = slice(max(0, int(x0) - r), min(d2, int(x0) + r + 1))
+    if zs.start >= zs.stop or ys.start >= ys.stop or xs.start >= xs.stop:
+        return
+    zz, yy, xx = np.meshgrid(np.arange(zs.start, zs.stop, dtype=np.float64) - z0,
+                             np.arange(ys.start, ys.stop, dtype=np.float64) - y0,
+                             np.arange(xs.start, xs.stop, dtype=np.float64) - x0, indexing="ij")
+    u = xx * np.cos(az) + yy * np.sin(az)
+    v = -xx * np.sin(az) + yy * np.cos(az)
+    w = zz - dip * u
+    inside = (u / a) ** 2 + (v / b) ** 2 + (w / c) ** 2 <= 1.0
+    sub = vol[zs, ys, xs]
+    if only_on is not None:
+        inside &= sub == only_on
+    sub[inside] = code
+
+
+def lens_ti3d(shape, seed: int, props=(0.50, 0.25, 0.15, 0.10)) -> np.ndarray:
+    """Config 3: ellipsoidal lenses of facies 1..F-1 (axes 5-40 cells,
+    random orientation) in a background facies 0, added until each facies
+    reaches its proportion."""
+    rng = Mt19937_64(seed)
+    vol = np.zeros(shape, np.uint8)
+    n = vol.size
+    for code in range(1, len(props)):
+        for _ in range(100000):
+            if np.count_nonzero(vol == code) >= props[code] * n:
+                break
+            _ellipsoid(vol, rng, code, only_on=0)
+    return vol
+
+
+def config3_ti() -> np.ndarray:
+    """Config 3: 180 x 150 x 120 (x, y, z) 4-facies lens TI, as a (120, 150, 180)
+    array.  150 is not divisible by 2^J = 4: the adjusted runs use the
+    148-wide crop, the literal runs the any_support extension (same windows)."""
+    return lens_ti3d((120, 150, 180), seed=20240403)
+
+
+def channel_belt_ti3d(shape, seed: int, props=(0.42, 0.26, 0.12, 0.12, 0.08)) -> np.ndarray:
+    """Config 4: sinuous 3D channel belts (facies 1) with levee wings (facies
+    2) along their tops, then ellipsoidal lenses of facies 3 and 4, on a
+    background facies 0."""
+    rng = Mt19937_64(seed)
+    vol = np.zeros(shape, np.uint8)
+    d0, d1, d2 = shape
+    n = vol.size
+    ys = np.arange(d1, dtype=np.float64)[:, None]
+    xs = np.arange(d2, dtype=np.float64)[None, :]
+    for _ in range(100000):
+        if np.count_nonzero(vol == 1) >= props[1] * n:
+            break
+        z0 = _uniform(rng, 0, d0)
+        th = _uniform(rng, 3.0, 10.0)
+        wd = _uniform(rng, 8.0, 30.0)
+        amp = _uniform(rng, 10.0, 60.0)
+        lam = _uniform(rng, 120.0, 400.0)
+        ph = _uniform(rng, 0, 2 * np.pi)
+        base = _uniform(rng, 0, d1)
+        along_x = bounded(rng, 2) == 0
+        if along_x:
+            dist = np.abs(ys - (base + amp * np.sin(2 * np.pi * xs / lam + ph)))
+        else:
+            dist = np.abs(xs - (base * d2 / d1 + amp * np.sin(2 * np.pi * ys / lam + ph)))
+        chan = dist < wd / 2
+        lev = (dist >= wd / 2) & (dist < wd / 2 + _uniform(rng, 3.0, 10.0))
+        for z in range(max(0, int(z0 - th / 2)), min(d0, int(z0 + th / 2) + 1)):
+            sl = vol[z]
+            sl[chan] = 1
+            if z >= z0:  # levees drape the upper half of the belt
+                sl[lev & (sl == 0)] = 2
+    for code in (3, 4):
+        for _ in range(100000):
+            if np.count_nonzero(vol == code) >= props[code] * n:
+                break
+            _ellipsoid(vol, rng, code, axes=(8.0, 40.0), only_on=0)
+    return vol
+
+
+def config4_ti() -> np.ndarray:
+    """Config 4: 400 x 400 x 200 (x, y, z) 5-facies channel-belt TI, as a
+    (200, 400, 400) array."""
+    return channel_belt_ti3d((200, 400, 400), seed=20240404)
+
+
+def hard_data3d_from(realization: np.ndarray, fraction: float, seed: int) -> np.ndarray:
+    """(n, 4) int32 (i0, i1, i2, facies) rows: a seeded partial Fisher-Yates
+    draw of cells read from ``realization``."""
+    shape = realization.shape
+    tot = int(np.prod(shape))
+    n = int(round(fraction * tot))
+    rng = Mt19937_64(seed)
+    chosen = {}
+    out = np.zeros((n, 4), np.int32)
+    for i in range(n):  # sparse partial Fisher-Yates over [0, tot)
+        j = i + bounded(rng, tot - i)
+        vi, vj = chosen.get(i, i), chosen.get(j, j)
+        chosen[i], chosen[j] = vj, vi
+        c = np.unravel_index(vj, shape)
+        out[i] = (c[0], c[1], c[2], realization[c])
+    return out
+
+
+def wells3d_from(realization: np.ndarray, n_wells: int, seed: int) -> np.ndarray:
+    """Vertical wells: ``n_wells`` full columns along axis 0 at seeded
+    distinct (i1, i2) positions, values read from ``realization``."""
+    d0, d1, d2 = realization.shape
+    rng = Mt19937_64(seed)
+    picked = []
+    while len(picked) < n_wells:
+        p = (bounded(rng, d1), bounded(rng, d2))
+        if p not in picked:
+            picked.append(p)
+    rows = []
+    for i1, i2 in picked:
+        for i0 in range(d0):
+            rows.append((i0, i1, i2, int(realization[i0, i1, i2])))
+    return np.array(rows, np.int32)
