@@ -367,9 +367,12 @@ def run_ours(args):
                "sample": f"{n} config-1 realizations, simulate_ensemble(workers={cores}), "
                          f"{dt:.1f} s wall"}
 
-    config2 = None
+    config2 = config3 = config4 = None
     if world == 1 and not args.skip_config2:
         config2 = measure_config2(dev, lib, local, args, skip_cpu=args.skip_cpu)
+    if world == 1 and not args.skip_3d:
+        config3 = measure_3d(3, dev, lib, local, args, skip_cpu=args.skip_cpu)
+        config4 = measure_3d(4, dev, lib, local, args, skip_cpu=args.skip_cpu)
 
     if rank == 0:
         line = {
@@ -413,12 +416,135 @@ def run_ours(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "config2": config2,
+            "config3": config3,
+            "config4": config4,
         }
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def measure_3d(which, dev, lib, local, args, skip_cpu=False):
+    """BASELINE configs 3 / 4 (the 3D extension, oracle/ccw3d_oracle.h):
+    device-resident cells/s, e2e through ccw_ti3d_create + ccw_simulate3d
+    with host buffers, the screen's roofline against the measured integer
+    peak of its inner loop, and the 3D CPU restatement (oracle, "port") on a
+    bounded sample whose outputs double as the parity check."""
+    import torch
+    from paper_2404_00441_b200 import _abi, ccwsim as cs, ccwsim3d as c3, synth
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle3d as P3
+    if which == 3:
+        ti_a = np.ascontiguousarray(synth.config3_ti()[:, :148, :])  # SURVEY H4(i): 180x148x120
+        nf, n_real, wells = 4, 16, None
+        cfg = c3.SimConfig3D(sg=(100, 200, 200), template_size=32, overlap=8, dwt_level=2, candidates=1,
+                             n_realizations=n_real, master_seed=MASTER)
+        label = ("config3: TI 180x148x120 (x,y,z; 150 -> 148 so 2^J divides it, SURVEY H4(i)) 4-facies "
+                 "ellipsoidal lenses, SG 200x200x100, T32 OV8 J2 K1, 16 realizations")
+    else:
+        ti_a = synth.config4_ti()
+        nf, n_real = 5, 1
+        cfg = c3.SimConfig3D(sg=(250, 500, 500), template_size=48, overlap=16, dwt_level=3, candidates=1,
+                             n_realizations=1, master_seed=MASTER)
+        label = ("config4: TI 400x400x200 (x,y,z) 5-facies channel belts + lenses, SG 500x500x250, "
+                 "T48 OV16 (12 -> 16 so 2^J divides it, SURVEY H4(i)) J3 K1, 20 vertical wells, 1 realization")
+    ti = c3.TrainingImage3D(ti_a, nf, cfg.dwt_level, dev)
+    if which == 4:
+        ref_real, _ = c3.simulate3d(ti, cfg, [777])
+        wells = synth.wells3d_from(ref_real[0], 20, 404)
+    hd_a = np.ascontiguousarray(wells, np.int32) if wells is not None else None
+    seeds = np.array([cs.mix64(MASTER, r + 1) for r in range(n_real)], np.uint64)
+    sgv = int(np.prod(cfg.sg))
+    c = cfg.to_c()
+    d_out = torch.empty(n_real * sgv, dtype=torch.uint8, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    diags = (_abi.Diag3dC * n_real)()
+    stream = torch.cuda.ExternalStream(dev.stream_ptr, device=torch.device("cuda", local))
+    hdp = hd_a.ctypes.data_as(_abi.I32P) if hd_a is not None else None
+    nhd = hd_a.shape[0] if hd_a is not None else 0
+
+    def step_device():
+        dev.check(lib.ccw_simulate3d_device(dev.handle, ti.handle, C.byref(c), seeds.ctypes.data_as(_abi.U64P),
+                                            n_real, hdp, nhd, C.c_void_p(d_out.data_ptr()), diags))
+
+    for _ in range(max(args.warmup, 3)):
+        step_device()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            evs[k][0].record(stream)
+        step_device()
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    launches = int(dev.last_timing()["launches"])
+    got = d_out.view(n_real, *cfg.sg).cpu().numpy()
+    dev.set_profiling(True)
+    step_device()
+    prof = dev.last_timing()
+    dev.set_profiling(False)
+    kind = 1 if prof["ccf_variant"] == 3 else 0
+    peak = dev.measure_int_peak(kind)
+    achieved = prof["ccf_flop"] / (prof["ccf_ms"] * 1e-3) / 1e12 if prof["ccf_ms"] else None
+    h_out = np.zeros(n_real * sgv, np.uint8)
+    h_pin = torch.empty(n_real * sgv, dtype=torch.uint8).pin_memory()
+
+    def step_e2e():
+        h = C.c_void_p()
+        d0, d1, d2 = ti_a.shape
+        dev.check(lib.ccw_ti3d_create(dev.handle, ti_a.ctypes.data_as(_abi.U8P), d0, d1, d2, nf, cfg.dwt_level,
+                                      C.byref(h)))
+        dev.check(lib.ccw_simulate3d(dev.handle, h, C.byref(c), seeds.ctypes.data_as(_abi.U64P), n_real, hdp, nhd,
+                                     C.cast(C.c_void_p(h_pin.data_ptr()), _abi.U8P), diags))
+        lib.ccw_ti3d_destroy(h)
+
+    step_e2e()
+    e2e_s = 0.0
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step_e2e()
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+    e2e_equal = bool(np.array_equal(h_pin.numpy().reshape(got.shape), got))
+    out = {"workload": label, "value": n_real * sgv * steps / (total_ms * 1e-3), "unit": UNIT,
+           "ms_per_step": total_ms / steps, "steps": steps, "gpu_launches": launches * steps,
+           "dtype": "int8x4 dp4a -> int32 (exact)" if kind == 1 else "int32 IMAD (exact)",
+           "roofline": {"bound": "int (CUDA cores)",
+                        "kernel": "screen3d_kernel (%s)" % ("dp4a" if kind == 1 else "IMAD"),
+                        "achieved": achieved, "peak": peak, "unit": "TOPS",
+                        "frac": achieved / peak if achieved and peak else None,
+                        "peak_source": "measured in this run: %s probe, 8 chains per thread (ccw_measure_int_peak)"
+                                       % ("dp4a" if kind == 1 else "IMAD"),
+                        "algorithmic_ops_per_step": prof["ccf_flop"],
+                        "algorithmic_ops_note": "SURVEY 8(d): 2 x F channels x window positions x mask cells "
+                                                "per placement",
+                        "screen_ms_per_step": prof["ccf_ms"], "step_ms_profiled": prof["total_ms"]},
+           "e2e": {"value": n_real * sgv * steps / e2e_s, "unit": UNIT,
+                   "h2d_bytes_per_step": int(ti_a.nbytes + seeds.nbytes + (hd_a.nbytes if hd_a is not None else 0)),
+                   "d2h_bytes_per_step": int(n_real * sgv), "equals_device_result": e2e_equal}}
+    if not skip_cpu:
+        o3 = P3.oracle3()
+        cores = os.cpu_count() or 1
+        oc = P3.Cfg3(sg=tuple(cfg.sg), template_size=cfg.template_size, overlap=cfg.overlap,
+                     dwt_level=cfg.dwt_level, candidates=cfg.candidates)
+        t0 = time.perf_counter()
+        o = o3.simulate_one(ti_a, nf, oc, wells, seed=int(seeds[0]), threads=cores)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": sgv / dt, "unit": UNIT, "cores": cores, "kind": "port",
+                               "cpu_model": cpu_model(),
+                               "sample": f"realization 0 of the workload, every score map split over {cores} "
+                                         f"threads, {dt:.1f} s wall (the reference has no 3D: builder's "
+                                         f"exact-integer 3D restatement, oracle/ccw3d_oracle.c)"}
+        out["parity"] = {"checked": 1, "equal": bool(np.array_equal(got[0], o["realization"])),
+                         "against": "oracle/ccw3d_oracle.c (the cpu_baseline run's output), same seed"}
+    return out
 
 
 CONFIG2 = ("config2: TI 2000x2000 binary channels, SG 4000x4000, T96 OV24 J3 K1, 1% hard data "
@@ -671,6 +797,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-config2", action="store_true",
                     help="omit the nested config-2 measurement (N=1 only)")
+    ap.add_argument("--skip-3d", action="store_true",
+                    help="omit the nested config-3 / config-4 (3D) measurements (N=1 only)")
     ap.add_argument("--workload", default="config1", choices=["config1", "single"],
                     help="config1 (headline) or single: one config-2 realization, positions sharded")
     ap.add_argument("--virtual-shards", type=int, default=1)

@@ -145,6 +145,9 @@ CCW_API ccw_status ccw_ctx_set_option(ccw_ctx* ctx, const char* name, long long 
 /* FP32 FFMA peak of this GPU (TFLOP/s), measured with an in-library
  * microbenchmark: the roofline denominator of the CUDA-core CCF screen. */
 CCW_API ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops);
+/* Integer CUDA-core peaks of the 3D screen's inner loops (TOPS, 2 ops per
+ * MAC): kind 0 = IMAD (int32), kind 1 = dp4a (4 int8 MACs per lane). */
+CCW_API ccw_status ccw_measure_int_peak(ccw_ctx* ctx, int kind, double* tops);
 /* Dense int8 tensor-core rate (TOPS) of the CCF screen's tcgen05 MMA shape
  * (kind::i8, M=128, N=256, cta_group::1), measured with an in-library probe. */
 CCW_API ccw_status ccw_measure_i8_peak(ccw_ctx* ctx, double* tops);

@@ -82,6 +82,7 @@ SIGNATURES = {
     "ccw_ctx_set_position_shards": (C.c_int, [P, C.c_int, C.c_int, U8P, C.c_int]),
     "ccw_measure_fp32_peak": (C.c_int, [P, F64P]),
     "ccw_measure_i8_peak": (C.c_int, [P, F64P]),
+    "ccw_measure_int_peak": (C.c_int, [P, C.c_int, F64P]),
     "ccw_measure_ccf_screen": (C.c_int, [P, P, C.c_int, C.c_int, C.c_int, F64P]),
     "ccw_mix64": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ccw_ti_create": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),

@@ -383,6 +383,12 @@ class Device:
         self.check(self._lib.ccw_measure_i8_peak(self.handle, C.byref(v)))
         return v.value
 
+    def measure_int_peak(self, kind: int) -> float:
+        """CUDA-core integer rate (TOPS): kind 0 IMAD, 1 dp4a (the 3D screen's loops)."""
+        v = C.c_double(0)
+        self.check(self._lib.ccw_measure_int_peak(self.handle, int(kind), C.byref(v)))
+        return v.value
+
     def close(self) -> None:
         if self.handle:
             # TI handles cached for this context go with it (the cache keys on

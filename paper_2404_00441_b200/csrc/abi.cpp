@@ -397,6 +397,14 @@ ccw_status ccw_measure_fp32_peak(ccw_ctx* ctx, double* tflops) {
     return guarded(ctx, [&] { *tflops = ccwgpu::measure_ffma_peak(ctx); });
 }
 
+ccw_status ccw_measure_int_peak(ccw_ctx* ctx, int kind, double* tops) {
+    if (!ctx || !tops) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (kind != 0 && kind != 1) throw Fail(CCW_ERR_CONFIG, "int peak: kind must be 0 (IMAD) or 1 (dp4a)");
+        *tops = ccwgpu::measure_int_peak(ctx, kind);
+    });
+}
+
 ccw_status ccw_measure_ccf_screen(ccw_ctx* ctx, ccw_ti* ti, int template_size, int njobs, int iters,
                                   double* ms_per_launch) {
     if (!ctx || !ti || !ms_per_launch) return CCW_ERR_GENERIC;

@@ -347,6 +347,7 @@ void nccl_all_gather_bytes(void* comm, const void* send, void* recv, size_t byte
 
 // --- device entry points (sim.cu / ops.cu / peak.cu) ----------------------
 double measure_ffma_peak(ccw_ctx* ctx);
+double measure_int_peak(ccw_ctx* ctx, int kind);
 void build_pyramid(ccw_ti* ti, cudaStream_t s);
 void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
                     int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out,

@@ -55,4 +55,60 @@ double measure_ffma_peak(ccw_ctx* ctx) {
     return best;
 }
 
+// Integer peaks of the 3D screen's inner loops: IMAD (one int32 MAC per lane)
+// and dp4a (four int8 MACs per lane), 8 independent chains per thread.
+template <int DP4A>
+__global__ void __launch_bounds__(256) int_peak_kernel(int* out, int iters, int seed) {
+    int a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x + k;
+    const int w = 0x01020304 ^ seed;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (DP4A)
+                    a[c] = __dp4a(a[c], w, a[c]);
+                else
+                    a[c] = a[c] * w + c;
+            }
+    }
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345678) out[blockIdx.x] = s;
+}
+
+// ops per second (2 per MAC) in TOPS; kind 0 IMAD, 1 dp4a
+double measure_int_peak(ccw_ctx* ctx, int kind) {
+    int sms = 0;
+    CCW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    int* d = nullptr;
+    const int blocks = sms * 8;
+    CCW_CUDA(cudaMalloc(&d, sizeof(int) * blocks));
+    cudaEvent_t a, b;
+    CCW_CUDA(cudaEventCreate(&a));
+    CCW_CUDA(cudaEventCreate(&b));
+    const int iters = 2048;
+    double best = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+        CCW_CUDA(cudaEventRecord(a, ctx->stream));
+        if (kind == 1)
+            int_peak_kernel<1><<<blocks, 256, 0, ctx->stream>>>(d, iters, 3);
+        else
+            int_peak_kernel<0><<<blocks, 256, 0, ctx->stream>>>(d, iters, 3);
+        CCW_CUDA(cudaEventRecord(b, ctx->stream));
+        CCW_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        CCW_CUDA(cudaEventElapsedTime(&ms, a, b));
+        const double ops = 2.0 * (kind == 1 ? 4 : 1) * 8 * 16 * static_cast<double>(iters) * blocks * 256;
+        if (rep > 0) best = std::max(best, ops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    return best;
+}
+
 }  // namespace ccwgpu

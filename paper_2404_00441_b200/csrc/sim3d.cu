@@ -45,6 +45,7 @@ struct Job3 {
     int32_t real, place;
     int32_t P[3];     // footprint origin in the work grid
     int32_t mask;     // mask id = corner * 8 + shape (shape: bit a = slab on axis a)
+    int32_t bmask;    // the screen batch's mask: corner * 8 + union of its jobs' shapes
     int32_t pick;     // unconditional draw; -1 conditional; -2 first placement
     int32_t fr[3];    // first placement's TI origin
     int32_t lat;      // lattice cell of the footprint (hard-data lists)
@@ -108,13 +109,14 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
     pdl_trigger();
     pdl_wait();
     const Job3 jb = jobs[j0 + blockIdx.x];
-    const int corner = jb.mask >> 3, shape = jb.mask & 7;
-    const int m_lo = mask_off[jb.mask], nm = mask_off[jb.mask + 1] - m_lo;
+    const int corner = jb.mask >> 3, shape = jb.mask & 7;  // the job's own overlap support
+    const int m_lo = mask_off[jb.bmask], nm = mask_off[jb.bmask + 1] - m_lo;  // cells of its batch's mask
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int B = g.B, B3 = B * B * B;
     const uint8_t* wk = work + static_cast<size_t>(jb.real) * g.W[0] * g.W[1] * g.W[2];
     int32_t* wout = wbuf + static_cast<size_t>(blockIdx.x) * wstride;
-    for (int i = warp; i < nm; i += blockDim.x >> 5) {
+    const int nw = blockDim.x >> 5;
+    for (int i = blockIdx.y * nw + warp; i < nm; i += gridDim.y * nw) {
         const int cell = mask_cells[m_lo + i];
         const int m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
         int cnt[16] = {0};
@@ -193,6 +195,98 @@ __device__ __forceinline__ unsigned long long warp_max64(unsigned long long v) {
     return v;
 }
 
+// The CCF of one box for JBT jobs (JBT >= the batch's job count): NP
+// positions per thread strided by 8 along axis 2, JBT accumulators each; then
+// each warp's top-K packed keys per job into wk[j][warp][K].
+template <int MODE, int NP, int JBT>
+__device__ __forceinline__ void screen_body(const Screen3Args& a, const Batch3& bt, const int32_t* region,
+                                            const int32_t* moff, const int32_t* wsm, int nm, int RV, int R1,
+                                            int R2p, int B0, int B1, int B2, int32_t* s3) {
+    const Geo3& g = a.g;
+    const int nch = MODE == 0 ? 1 : g.nscr;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = warp / a.W1, t1 = (warp % a.W1) * 4 + (lane >> 3), l2 = lane & 7;
+    const int base = (t0 * R1 + t1) * R2p + l2;
+    int acc[NP][JBT];
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+#pragma unroll
+        for (int j = 0; j < JBT; ++j) acc[k][j] = 0;
+    auto weights = [&](int row, int (&wv)[JBT]) {
+        const int* w = wsm + row * JB;
+        if constexpr (JBT == 8) {
+            const int4 w0 = *reinterpret_cast<const int4*>(w), w1 = *reinterpret_cast<const int4*>(w + 4);
+            wv[0] = w0.x; wv[1] = w0.y; wv[2] = w0.z; wv[3] = w0.w;
+            wv[4] = w1.x; wv[5] = w1.y; wv[6] = w1.z; wv[7] = w1.w;
+        } else if constexpr (JBT == 4) {
+            const int4 w0 = *reinterpret_cast<const int4*>(w);
+            wv[0] = w0.x; wv[1] = w0.y; wv[2] = w0.z; wv[3] = w0.w;
+        } else if constexpr (JBT == 2) {
+            const int2 w0 = *reinterpret_cast<const int2*>(w);
+            wv[0] = w0.x; wv[1] = w0.y;
+        } else {
+            wv[0] = w[0];
+        }
+    };
+#pragma unroll 2
+    for (int i = 0; i < nm; ++i) {
+        const int o = base + moff[i];
+        if constexpr (MODE == 0) {
+            int wv[JBT];
+            weights(i, wv);
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const int v = region[o + 8 * k];
+#pragma unroll
+                for (int j = 0; j < JBT; ++j) acc[k][j] = __dp4a(v, wv[j], acc[k][j]);
+            }
+        } else {
+            for (int ch = 0; ch < nch; ++ch) {
+                int wv[JBT];
+                weights(i * nch + ch, wv);
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    const int v = region[ch * RV + o + 8 * k];
+#pragma unroll
+                    for (int j = 0; j < JBT; ++j) acc[k][j] += v * wv[j];
+                }
+            }
+        }
+    }
+    // packed keys: exact score (biased) above the complemented position, so
+    // the larger key is the better candidate (earlier position on ties)
+    const int p0 = B0 + t0, p1 = B1 + t1;
+    const bool row_ok = p0 < g.o[0] && p1 < g.o[1];
+    __syncthreads();  // (the region is reused below as the per-warp key lists)
+    unsigned long long* wk = reinterpret_cast<unsigned long long*>(s3);  // [JB][8 warps][K]
+    const int K = a.K;
+#pragma unroll
+    for (int j = 0; j < JBT; ++j) {
+        if (j >= bt.n) break;
+        unsigned long long key[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            const int p2 = B2 + l2 + 8 * k;
+            key[k] = 0;
+            if (row_ok && p2 < g.o[2]) {
+                const uint32_t pos = static_cast<uint32_t>((p0 * g.o[1] + p1) * g.o[2] + p2);
+                key[k] = (static_cast<unsigned long long>(static_cast<uint32_t>(acc[k][j]) ^ 0x80000000u) << 32) |
+                         (0xFFFFFFFFu - pos);
+            }
+        }
+        for (int r = 0; r < K; ++r) {
+            unsigned long long m = 0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) m = umax64(m, key[k]);
+            const unsigned long long wm = warp_max64(m);
+#pragma unroll
+            for (int k = 0; k < NP; ++k)
+                if (key[k] == wm) key[k] = 0;  // keys are unique: one lane drops it
+            if (lane == 0) wk[(j * 8 + warp) * K + r] = wm;
+        }
+    }
+}
+
 template <int MODE, int NP>
 __global__ void __launch_bounds__(S3_THREADS) screen3d_kernel(Screen3Args a) {
     extern __shared__ __align__(16) int32_t s3[];
@@ -236,73 +330,19 @@ __global__ void __launch_bounds__(S3_THREADS) screen3d_kernel(Screen3Args a) {
 #endif
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t0 = warp / a.W1, t1 = (warp % a.W1) * 4 + (lane >> 3), l2 = lane & 7;
-    const int base = (t0 * R1 + t1) * R2p + l2;
-    int acc[NP][JB];
-#pragma unroll
-    for (int k = 0; k < NP; ++k)
-#pragma unroll
-        for (int j = 0; j < JB; ++j) acc[k][j] = 0;
-    for (int i = 0; i < nm; ++i) {
-        const int o = base + moff[i];
-        if constexpr (MODE == 0) {
-            const int4 w0 = *reinterpret_cast<const int4*>(wsm + i * JB);
-            const int4 w1 = *reinterpret_cast<const int4*>(wsm + i * JB + 4);
-            const int wv[JB] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-            for (int k = 0; k < NP; ++k) {
-                const int v = region[o + 8 * k];
-#pragma unroll
-                for (int j = 0; j < JB; ++j) acc[k][j] = __dp4a(v, wv[j], acc[k][j]);
-            }
-        } else {
-            for (int ch = 0; ch < nch; ++ch) {
-                const int4 w0 = *reinterpret_cast<const int4*>(wsm + (i * nch + ch) * JB);
-                const int4 w1 = *reinterpret_cast<const int4*>(wsm + (i * nch + ch) * JB + 4);
-                const int wv[JB] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-                for (int k = 0; k < NP; ++k) {
-                    const int v = region[ch * RV + o + 8 * k];
-#pragma unroll
-                    for (int j = 0; j < JB; ++j) acc[k][j] += v * wv[j];
-                }
-            }
-        }
-    }
-    // packed keys: exact score (biased) above the complemented position, so
-    // the larger key is the better candidate (earlier position on ties)
-    const int p0 = B0 + t0, p1 = B1 + t1;
-    const bool row_ok = p0 < g.o[0] && p1 < g.o[1];
-    __syncthreads();  // (region reused below as the per-warp key lists)
-    unsigned long long* wk = reinterpret_cast<unsigned long long*>(s3);  // [JB][8 warps][K]
-    const int K = a.K;
-#pragma unroll
-    for (int j = 0; j < JB; ++j) {
-        if (j >= bt.n) break;
-        unsigned long long key[NP];
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-            const int p2 = B2 + l2 + 8 * k;
-            key[k] = 0;
-            if (row_ok && p2 < g.o[2]) {
-                const uint32_t pos = static_cast<uint32_t>((p0 * g.o[1] + p1) * g.o[2] + p2);
-                key[k] = (static_cast<unsigned long long>(static_cast<uint32_t>(acc[k][j]) ^ 0x80000000u) << 32) |
-                         (0xFFFFFFFFu - pos);
-            }
-        }
-        for (int r = 0; r < K; ++r) {
-            unsigned long long m = 0;
-#pragma unroll
-            for (int k = 0; k < NP; ++k) m = umax64(m, key[k]);
-            const unsigned long long wm = warp_max64(m);
-#pragma unroll
-            for (int k = 0; k < NP; ++k)
-                if (key[k] == wm) key[k] = 0;  // keys are unique: one lane drops it
-            if (lane == 0) wk[(j * 8 + warp) * K + r] = wm;
-        }
-    }
+    // the batch's job count picks the accumulator width (no MACs on empty slots)
+    if (bt.n > 4)
+        screen_body<MODE, NP, 8>(a, bt, region, moff, wsm, nm, RV, R1, R2p, B0, B1, B2, s3);
+    else if (bt.n > 2)
+        screen_body<MODE, NP, 4>(a, bt, region, moff, wsm, nm, RV, R1, R2p, B0, B1, B2, s3);
+    else if (bt.n > 1)
+        screen_body<MODE, NP, 2>(a, bt, region, moff, wsm, nm, RV, R1, R2p, B0, B1, B2, s3);
+    else
+        screen_body<MODE, NP, 1>(a, bt, region, moff, wsm, nm, RV, R1, R2p, B0, B1, B2, s3);
     __syncthreads();
     // warp j merges job j's 8 warp lists
+    const unsigned long long* wk = reinterpret_cast<const unsigned long long*>(s3);
+    const int K = a.K;
     if (warp < bt.n) {
         const int j = warp;
         const int n = 8 * K;
@@ -433,17 +473,21 @@ __global__ void __launch_bounds__(128) select3d_kernel(Select3Args a) {
     }
     __syncthreads();
     const int f0 = fr_s[0], f1 = fr_s[1], f2 = fr_s[2];
-    if (threadIdx.x < 3) a.chosen[3 * (a.j0 + jw) + threadIdx.x] = fr_s[threadIdx.x];
-    // crop + paste_into (grid.hpp:172-230): T^3 cells, 4-byte words where aligned
+    if (threadIdx.x < 3 && blockIdx.y == 0) a.chosen[3 * (a.j0 + jw) + threadIdx.x] = fr_s[threadIdx.x];
+    // crop + paste_into (grid.hpp:172-230): T^3 cells, 4-byte words where
+    // aligned; the gridDim.y CTAs of a job (each made the same pick) paste
+    // one slab of x0 each
     uint8_t* wk = a.work + static_cast<size_t>(jb.real) * g.W[0] * g.W[1] * g.W[2];
     const int T = g.T;
-    const size_t rows = static_cast<size_t>(T) * T;
+    const int xa = static_cast<int>(static_cast<int64_t>(T) * blockIdx.y / gridDim.y);
+    const int xb = static_cast<int>(static_cast<int64_t>(T) * (blockIdx.y + 1) / gridDim.y);
+    const size_t rows = static_cast<size_t>(xb - xa) * T;
     if (g.aligned4) {  // every row start is 4-byte aligned on both sides
         const int T4 = T >> 2;
         for (size_t e = threadIdx.x; e < rows * T4; e += blockDim.x) {
             const int x2 = static_cast<int>(e % T4) * 4;
             const size_t rr = e / T4;
-            const int x1 = static_cast<int>(rr % T), x0 = static_cast<int>(rr / T);
+            const int x1 = static_cast<int>(rr % T), x0 = xa + static_cast<int>(rr / T);
             *reinterpret_cast<uint32_t*>(wk + (static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] +
                                          jb.P[2] + x2) =
                 *reinterpret_cast<const uint32_t*>(a.ti + (static_cast<size_t>(f0 + x0) * g.ti[1] + f1 + x1) * g.ti[2] +
@@ -454,7 +498,7 @@ __global__ void __launch_bounds__(128) select3d_kernel(Select3Args a) {
     for (size_t e = threadIdx.x; e < rows * T; e += blockDim.x) {
         const int x2 = static_cast<int>(e % T);
         const size_t rr = e / T;
-        const int x1 = static_cast<int>(rr % T), x0 = static_cast<int>(rr / T);
+        const int x1 = static_cast<int>(rr % T), x0 = xa + static_cast<int>(rr / T);
         wk[(static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] + jb.P[2] + x2] =
             a.ti[(static_cast<size_t>(f0 + x0) * g.ti[1] + f1 + x1) * g.ti[2] + f2 + x2];
     }
@@ -634,10 +678,41 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
                     } else {
                         const bool cond = !hd_off.empty() && hd_off[p.j.lat + 1] > hd_off[p.j.lat];
                         p.j.pick = cond ? -1 : static_cast<int>(bounded(rng, static_cast<uint64_t>(Kp)));
-                        mask_used[p.j.mask] = 1;
                     }
                     pls.push_back(p);
                 }
+    }
+    // (wave, corner, shape) order: a batch holds up to JB jobs of one corner,
+    // screened against the union of their overlap masks (a job's weights are
+    // zero on the cells outside its own overlap)
+    std::stable_sort(pls.begin(), pls.end(), [](const Pl& x, const Pl& y) {
+        return x.wave != y.wave ? x.wave < y.wave : x.mask < y.mask;
+    });
+    const size_t njobs = pls.size();
+    std::vector<Job3> jobs(njobs);
+    std::vector<Batch3> batches;
+    std::vector<int> wave_j0(max_key + 2, 0), wave_b0(max_key + 2, 0);
+    {
+        size_t k = 0;
+        for (int w = 0; w <= max_key; ++w) {
+            wave_j0[w] = static_cast<int>(k);
+            wave_b0[w] = static_cast<int>(batches.size());
+            while (k < njobs && pls[k].wave == w) {
+                size_t e = k;
+                while (e < njobs && pls[e].wave == w && (pls[e].mask >> 3) == (pls[k].mask >> 3) && e - k < JB) ++e;
+                int bm = pls[k].mask;
+                for (size_t q = k; q < e; ++q) bm |= pls[q].mask & 7;
+                for (size_t q = k; q < e; ++q) pls[q].j.bmask = bm;
+                if (pls[k].j.pick != -2) {
+                    batches.push_back({static_cast<int>(k), static_cast<int>(e - k), bm, 0});
+                    mask_used[bm] = 1;
+                }
+                k = e;
+            }
+        }
+        wave_j0[max_key + 1] = static_cast<int>(njobs);
+        wave_b0[max_key + 1] = static_cast<int>(batches.size());
+        for (size_t i = 0; i < njobs; ++i) jobs[i] = pls[i].j;
     }
     // mask cell lists (row-major coarse cells of the block-level mask)
     std::vector<int> mask_off(65, 0), mask_cells;
@@ -665,29 +740,6 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     }
     mask_off[64] = static_cast<int>(mask_cells.size());
     // waves -> batches of jobs sharing one mask
-    std::stable_sort(pls.begin(), pls.end(), [](const Pl& x, const Pl& y) {
-        return x.wave != y.wave ? x.wave < y.wave : x.mask < y.mask;
-    });
-    const size_t njobs = pls.size();
-    std::vector<Job3> jobs(njobs);
-    std::vector<Batch3> batches;
-    std::vector<int> wave_j0(max_key + 2, 0), wave_b0(max_key + 2, 0);
-    {
-        size_t k = 0;
-        for (int w = 0; w <= max_key; ++w) {
-            wave_j0[w] = static_cast<int>(k);
-            wave_b0[w] = static_cast<int>(batches.size());
-            while (k < njobs && pls[k].wave == w) {
-                size_t e = k;
-                while (e < njobs && pls[e].wave == w && pls[e].mask == pls[k].mask && e - k < JB) ++e;
-                if (pls[k].j.pick != -2) batches.push_back({static_cast<int>(k), static_cast<int>(e - k), pls[k].mask, 0});
-                k = e;
-            }
-        }
-        wave_j0[max_key + 1] = static_cast<int>(njobs);
-        wave_b0[max_key + 1] = static_cast<int>(batches.size());
-        for (size_t i = 0; i < njobs; ++i) jobs[i] = pls[i].j;
-    }
     int max_wave = 1;
     for (int w = 0; w <= max_key; ++w) max_wave = std::max(max_wave, wave_j0[w + 1] - wave_j0[w]);
 
@@ -699,7 +751,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             const int P[3] = {8 / w1, 4 * w1, 8 * np};
             double v = 1;
             for (int a = 0; a < 3; ++a) v *= static_cast<double>((g.o[a] + P[a] - 1) / P[a]) * P[a];
-            v *= 1.0 + 0.02 * (4 - np);  // prefer more positions per thread on ties
+            v *= (np == 1 ? 1.25 : 1.0) + 0.02 * (4 - np);  // NP = 1 is load-bound; more positions per thread on ties
             if (v < best_v) {
                 best_v = v;
                 best_np = np;
@@ -818,7 +870,8 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         if (nj == 0) continue;
         const int b0 = wave_b0[w], nbt = wave_b0[w + 1] - b0;
         if (nbt > 0) {
-            launch_pdl(prep3d_kernel, dim3(nj), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
+            const int psplit = std::max(1, std::min((max_nm + 7) / 8, (2 * 148 + nj - 1) / nj));
+            launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
                        static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
                        static_cast<const uint8_t*>(d_work), d_w, wstride);
             ++launches;
@@ -859,7 +912,8 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         Select3Args q = se;
         q.j0 = j0;
         q.nj = nj;
-        launch_pdl(select3d_kernel, dim3(nj), dim3(128), 0, st, q);
+        const int ssplit = std::max(1, std::min(g.T / 4, (2 * 148 + nj - 1) / nj));
+        launch_pdl(select3d_kernel, dim3(nj, ssplit), dim3(128), 0, st, q);
         ++launches;
     }
     {

@@ -125,3 +125,29 @@ def simulate_position_sharded(ti: cs.CategoricalGrid, cfg: cs.SimConfig, seeds: 
         return cs.simulate_batch(ti, cfg, list(seeds), None, dev)
     finally:
         dev.set_position_shards(1, 0, None, 1)
+
+
+# ------------------------------------------- 3D candidate-position shards --
+# The 3D screen (csrc/sim3d.cu) scores boxes of TI window positions; shard s
+# of S owns the boxes [s * bps, min((s + 1) * bps, nbox)) with
+# bps = ceil(nbox / S), keeps each box's top-K packed keys and the per-wave
+# box lists are all-gathered (ncclAllGather, rank-major) before every rank
+# merges them (select3d_kernel).  Scores are exact integers, so the packed
+# key alone orders candidates: (score + 2^31) << 32 | (2^32 - 1 - position).
+
+def box_range(nbox: int, shard: int, nshards: int) -> Tuple[int, int]:
+    bps = -(-nbox // nshards)
+    return min(nbox, shard * bps), min(nbox, (shard + 1) * bps)
+
+
+def pack_key3d(score: int, position: int) -> int:
+    return ((int(score) + (1 << 31)) & 0xFFFFFFFF) << 32 | (0xFFFFFFFF - int(position))
+
+
+def unpack_key3d(key: int) -> Tuple[int, int]:
+    return (key >> 32) - (1 << 31), 0xFFFFFFFF - (key & 0xFFFFFFFF)
+
+
+def merge_box_keys(keys: Sequence[int], k: int) -> List[int]:
+    """select3d_kernel's merge: the k largest keys, descending (0 = empty)."""
+    return sorted((int(x) for x in keys if x), reverse=True)[:k]

@@ -136,3 +136,77 @@ def test_position_ranges_partition():
             assert all(p1 > p0 for p0, p1 in rs)
     with pytest.raises(ValueError):
         D.position_range(10, 2, 2)
+
+
+def _worker3d(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+    import torch.distributed as dist
+    import pyoracle3d as P3
+    from paper_2404_00441_b200 import distributed as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o3 = P3.oracle3()
+    rng = np.random.default_rng(11)
+    ti = rng.integers(0, 3, (24, 28, 32)).astype(np.uint8)
+    cnt = o3.block_counts(ti, 3, 1)
+    n = rng.integers(0, 8, (3, 4, 4, 4)).astype(np.int32)
+    mask = np.zeros((4, 4, 4), np.uint8)
+    mask[:2] = 1
+    mask[:, :2] = 1
+    n[:, mask == 0] = 0
+    S = o3.score_map(cnt, n, mask)  # (9, 11, 13) positions
+    K = 4
+    # boxes of 3 x 4 x 8 positions, shard = this rank's box range
+    nb = [-(-S.shape[0] // 3), -(-S.shape[1] // 4), -(-S.shape[2] // 8)]
+    nbox = nb[0] * nb[1] * nb[2]
+    b0, b1 = D.box_range(nbox, rank, world)
+    bps = -(-nbox // world)
+    mine = np.zeros((bps, K), np.uint64)
+    for b in range(b0, b1):
+        q2, q1, q0 = b % nb[2], (b // nb[2]) % nb[1], b // (nb[2] * nb[1])
+        keys = []
+        for p0 in range(q0 * 3, min(S.shape[0], q0 * 3 + 3)):
+            for p1 in range(q1 * 4, min(S.shape[1], q1 * 4 + 4)):
+                for p2 in range(q2 * 8, min(S.shape[2], q2 * 8 + 8)):
+                    pos = (p0 * S.shape[1] + p1) * S.shape[2] + p2
+                    keys.append(D.pack_key3d(int(S[p0, p1, p2]), pos))
+        top = D.merge_box_keys(keys, K)
+        mine[b - b0, :len(top)] = top
+    # ncclAllGather stand-in: gloo all_gather of the rank's box lists
+    t = torch.from_numpy(mine.view(np.int64).copy())
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    allk = np.concatenate([p.numpy().view(np.uint64).ravel() for p in parts])
+    merged = D.merge_box_keys([int(x) for x in allk], K)
+    if rank == 0:
+        np.save(out_path, np.array([D.unpack_key3d(k) for k in merged], np.int64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_3d_position_shards_merge(tmp_path, world):
+    """3D position shards over gloo: per-rank box top-K lists of an exact
+    score map, all-gathered and merged, equal the map's global top-K
+    (score desc, earlier row-major position on ties)."""
+    port = _free_port()
+    out = str(tmp_path / "m3.npy")
+    mp.start_processes(_worker3d, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+    got = np.load(out)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle3d as P3
+    o3 = P3.oracle3()
+    rng = np.random.default_rng(11)
+    ti = rng.integers(0, 3, (24, 28, 32)).astype(np.uint8)
+    cnt = o3.block_counts(ti, 3, 1)
+    n = rng.integers(0, 8, (3, 4, 4, 4)).astype(np.int32)
+    mask = np.zeros((4, 4, 4), np.uint8)
+    mask[:2] = 1
+    mask[:, :2] = 1
+    n[:, mask == 0] = 0
+    flat = o3.score_map(cnt, n, mask).ravel()
+    best = sorted(range(flat.size), key=lambda q: (-flat[q], q))[:4]
+    assert got.tolist() == [[int(flat[q]), q] for q in best]
