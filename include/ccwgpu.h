@@ -69,6 +69,13 @@ typedef struct ccw_sim_config {
     int32_t facies_mode;    /* 0 indicator, 1 raw_codes  (simulator.hpp:25) */
     int32_t min_cut;        /* 0 off, 1 on                                   */
     uint64_t master_seed;
+    /* Literal-config extension (not in the reference; 0 = reference
+     * behaviour): overlap not divisible by 2^J allowed, coarse mask = every
+     * block the fine overlap touches (extract_or zeros the rest of such a
+     * block), TI not divisible by 2^J used at its top-left floor(d/2^J)*2^J
+     * crop.  Semantics: oracle/ccw_oracle.h. */
+    int32_t any_support;
+    int32_t _pad;
 } ccw_sim_config;
 
 /* ccwsim::SimDiagnostics (simulator.hpp:376-392). */

@@ -501,6 +501,9 @@ struct SimConfig {
     FaciesMode facies_mode = FaciesMode::indicator;
     bool min_cut = false;
     std::optional<HardDataSet> hard_data;
+    // extension (not a reference member): the literal-config any-support mask,
+    // include/ccwgpu.h ccw_sim_config::any_support
+    bool any_support = false;
 
     int block() const noexcept { return 1 << dwt_level; }
     int stride() const noexcept { return template_size - overlap; }
@@ -518,6 +521,7 @@ struct SimConfig {
         c.facies_mode = facies_mode == FaciesMode::raw_codes;
         c.min_cut = min_cut;
         c.master_seed = master_seed;
+        c.any_support = any_support;
         return c;
     }
     void validate() const {

@@ -412,7 +412,7 @@ static int validate_cfg(const ccwo_sim_config* c) {
     if (c->template_size % b != 0)
         return fail(CCWO_CONFIG, "template: %d not divisible by 2^dwt_level = %d",
                     c->template_size, b);
-    if (c->overlap % b != 0)
+    if (c->overlap % b != 0 && !c->any_support)
         return fail(CCWO_CONFIG, "overlap: %d not divisible by 2^dwt_level = %d", c->overlap, b);
     if (c->candidates < 1) return fail(CCWO_CONFIG, "candidates: must be >= 1");
     if (c->n_realizations < 1) return fail(CCWO_CONFIG, "realizations: must be >= 1");
@@ -457,11 +457,12 @@ static int validate_against(const ccwo_sim_config* c, int ti_h, int ti_w, int nf
                             const int32_t* hd, int n_hd) {
     int rc = validate_cfg(c);
     if (rc) return rc;
-    if (c->template_size > ti_h || c->template_size > ti_w)
+    const int b = 1 << c->dwt_level;
+    const int uh = c->any_support ? ti_h / b * b : ti_h, uw = c->any_support ? ti_w / b * b : ti_w;
+    if (c->template_size > uh || c->template_size > uw)
         return fail(CCWO_CONFIG, "template: %d exceeds training image %dx%d", c->template_size,
                     ti_h, ti_w);
-    const int b = 1 << c->dwt_level;
-    if (ti_h % b != 0 || ti_w % b != 0)
+    if (!c->any_support && (ti_h % b != 0 || ti_w % b != 0))
         return fail(CCWO_CONFIG, "training image %dx%d not divisible by 2^dwt_level = %d", ti_h,
                     ti_w, b);
     if (hd) return validate_hd(hd, n_hd, c->sg_height, c->sg_width, nf);
@@ -669,15 +670,20 @@ int ccwo_simulate_one(const uint8_t* ti, int ti_h, int ti_w, int nf, const ccwo_
     mt64 rng;
     mt64_seed(&rng, seed);
 
-    /* TI scoring channels at level J (simulator.hpp:429-435) */
+    /* TI scoring channels at level J (simulator.hpp:429-435); with the
+     * literal-config extension over the top-left uh x uw crop */
     const int hc = ti_h >> L, wc = ti_w >> L, tc = t >> L;
-    const size_t tin = (size_t)ti_h * ti_w;
+    const int uh = hc << L, uw = wc << L;
+    const size_t tin = (size_t)uh * uw;
     double* fine = (double*)malloc(sizeof(double) * tin);
     double* ti_c = (double*)malloc(sizeof(double) * (size_t)nch * hc * wc);
     for (int f = 0; f < nch; ++f) {
-        for (size_t i = 0; i < tin; ++i)
-            fine[i] = cfg->facies_mode == 0 ? (ti[i] == f ? 1.0 : 0.0) : (double)ti[i];
-        apex_of(fine, ti_h, ti_w, L, ti_c + (size_t)f * hc * wc);
+        for (int r = 0; r < uh; ++r)
+            for (int c = 0; c < uw; ++c) {
+                const uint8_t v = ti[(size_t)r * ti_w + c];
+                fine[(size_t)r * uw + c] = cfg->facies_mode == 0 ? (v == f ? 1.0 : 0.0) : (double)v;
+            }
+        apex_of(fine, uh, uw, L, ti_c + (size_t)f * hc * wc);
     }
     free(fine);
 
@@ -711,8 +717,8 @@ int ccwo_simulate_one(const uint8_t* ti, int ti_h, int ti_w, int nf, const ccwo_
         int fr = 0, fc = 0;
         if (shape == SH_NONE) {
             /* simulator.hpp:450-453 */
-            fr = (int)bounded(&rng, (uint64_t)((ti_h - t) / b + 1)) * b;
-            fc = (int)bounded(&rng, (uint64_t)((ti_w - t) / b + 1)) * b;
+            fr = (int)bounded(&rng, (uint64_t)((uh - t) / b + 1)) * b;
+            fc = (int)bounded(&rng, (uint64_t)((uw - t) / b + 1)) * b;
         } else {
             /* extract_or (simulator.hpp:225-252) */
             support_mask(shape, plan.origin, t, ov, fmask);
@@ -737,16 +743,21 @@ int ccwo_simulate_one(const uint8_t* ti, int ti_h, int ti_w, int nf, const ccwo_
             if (rc) break;
             for (int f = 0; f < nch; ++f)
                 apex_of(orp + (size_t)f * t * t, t, t, L, orc + (size_t)f * tc * tc);
-            /* coarse_mask_from_fine (simulator.hpp:256-272) */
+            /* coarse_mask_from_fine (simulator.hpp:256-272); the literal-config
+             * extension keeps every block the overlap touches */
             for (int i = 0; i < tc; ++i)
                 for (int j = 0; j < tc; ++j) {
                     const double v = fmask[(i * b) * t + j * b];
+                    double any = 0.0;
                     for (int r = 0; r < b; ++r)
-                        for (int c = 0; c < b; ++c)
-                            if (fmask[(i * b + r) * t + j * b + c] != v)
+                        for (int c = 0; c < b; ++c) {
+                            const double m = fmask[(i * b + r) * t + j * b + c];
+                            if (m == 1.0) any = 1.0;
+                            if (m != v && !cfg->any_support)
                                 rc = fail(CCWO_ERROR,
                                           "internal error: overlap mask not block-aligned");
-                    cmask[i * tc + j] = v;
+                        }
+                    cmask[i * tc + j] = cfg->any_support ? any : v;
                 }
             if (rc) break;
             rc = ccwo_score_map_channels(ti_c, orc, nch, hc, wc, tc, tc, cmask, cfg->scoring,

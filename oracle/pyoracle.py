@@ -40,7 +40,7 @@ class SimConfigC(C.Structure):
                 ("dwt_level", C.c_int32), ("candidates", C.c_int32),
                 ("n_realizations", C.c_int32), ("scoring", C.c_int32),
                 ("facies_mode", C.c_int32), ("min_cut", C.c_int32),
-                ("master_seed", C.c_uint64)]
+                ("master_seed", C.c_uint64), ("any_support", C.c_int32), ("_pad", C.c_int32)]
 
 
 class DiagC(C.Structure):
@@ -67,7 +67,8 @@ def config_struct(cfg) -> SimConfigC:
                       int(cfg.overlap), int(cfg.dwt_level), int(cfg.candidates),
                       int(cfg.n_realizations), mode(cfg.scoring, ["raw", "normalized"]),
                       mode(cfg.facies_mode, ["indicator", "raw_codes"]), int(bool(cfg.min_cut)),
-                      int(cfg.master_seed) & 0xFFFFFFFFFFFFFFFF)
+                      int(cfg.master_seed) & 0xFFFFFFFFFFFFFFFF,
+                      int(bool(getattr(cfg, "any_support", False))), 0)
 
 
 def _p(a, t):
@@ -343,3 +344,4 @@ class Cfg:
     facies_mode: int = 0
     min_cut: bool = False
     master_seed: int = 1234
+    any_support: bool = False  # literal-config extension (ccw_oracle.h)

@@ -74,6 +74,8 @@ ccwsim::CategoricalGrid grid_of(const uint8_t* cells, int h, int w, int nf) {
 }
 
 ccwsim::SimConfig config_of(const ccwo_sim_config* c, const int32_t* hd, int n_hd) {
+    if (c->any_support)  // the literal-config extension is not the reference's behaviour
+        throw ccwsim::ConfigError("any_support: the reference has no literal-config extension");
     ccwsim::SimConfig cfg;
     cfg.sg_height = c->sg_height;
     cfg.sg_width = c->sg_width;

@@ -19,7 +19,7 @@ class SimConfigC(C.Structure):
                 ("dwt_level", C.c_int32), ("candidates", C.c_int32),
                 ("n_realizations", C.c_int32), ("scoring", C.c_int32),
                 ("facies_mode", C.c_int32), ("min_cut", C.c_int32),
-                ("master_seed", C.c_uint64)]
+                ("master_seed", C.c_uint64), ("any_support", C.c_int32), ("_pad", C.c_int32)]
 
 
 class DiagC(C.Structure):

@@ -254,6 +254,9 @@ class SimConfig:
     facies_mode: str = "indicator"  # "indicator" | "raw_codes"
     min_cut: bool = False
     hard_data: Optional[HardDataSet] = None
+    # literal-config extension (not in the reference; include/ccwgpu.h):
+    # overlap / TI extents not divisible by 2^J, any-support coarse mask
+    any_support: bool = False
 
     def block(self) -> int:
         return 1 << self.dwt_level
@@ -268,7 +271,8 @@ class SimConfig:
         mode = fm[self.facies_mode] if isinstance(self.facies_mode, str) else int(self.facies_mode)
         return _abi.SimConfigC(self.sg_height, self.sg_width, self.template_size, self.overlap,
                                self.dwt_level, self.candidates, self.n_realizations, scoring, mode,
-                               int(bool(self.min_cut)), int(self.master_seed) & _M64)
+                               int(bool(self.min_cut)), int(self.master_seed) & _M64,
+                               int(bool(self.any_support)), 0)
 
     def validate(self) -> None:
         c = self.to_c()

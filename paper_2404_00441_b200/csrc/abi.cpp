@@ -69,7 +69,7 @@ void validate_config(const ccw_sim_config& c) {
     if (c.template_size % b != 0)
         throw Fail(CCW_ERR_CONFIG, fmt("template: %d not divisible by 2^dwt_level = %d",
                                        c.template_size, b));
-    if (c.overlap % b != 0)
+    if (c.overlap % b != 0 && !c.any_support)  // (any_support: literal-config extension)
         throw Fail(CCW_ERR_CONFIG,
                    fmt("overlap: %d not divisible by 2^dwt_level = %d", c.overlap, b));
     if (c.candidates < 1) throw Fail(CCW_ERR_CONFIG, "candidates: must be >= 1");
@@ -113,11 +113,14 @@ static void validate_hard_data(const int32_t* hd, int n_hd, int h, int w, int nf
 void validate_against(const ccw_sim_config& c, int ti_h, int ti_w, int nf, const int32_t* hd,
                       int n_hd) {
     validate_config(c);
-    if (c.template_size > ti_h || c.template_size > ti_w)
+    const int b = 1 << c.dwt_level;
+    // any_support (literal-config extension): the TI is used at its top-left
+    // floor(d / 2^J) * 2^J crop, the only cells a block-aligned window reaches
+    const int uh = c.any_support ? ti_h / b * b : ti_h, uw = c.any_support ? ti_w / b * b : ti_w;
+    if (c.template_size > uh || c.template_size > uw)
         throw Fail(CCW_ERR_CONFIG, fmt("template: %d exceeds training image %dx%d",
                                        c.template_size, ti_h, ti_w));
-    const int b = 1 << c.dwt_level;
-    if (ti_h % b != 0 || ti_w % b != 0)
+    if (!c.any_support && (ti_h % b != 0 || ti_w % b != 0))
         throw Fail(CCW_ERR_CONFIG,
                    fmt("training image %dx%d not divisible by 2^dwt_level = %d", ti_h, ti_w, b));
     if (hd) validate_hard_data(hd, n_hd, c.sg_height, c.sg_width, nf);
@@ -439,9 +442,12 @@ static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device
         if (nf <= 0) throw Fail(CCW_ERR_DIMENSION, "num_facies must be positive");
         if (nf > 255) throw Fail(CCW_ERR_DIMENSION, "num_facies must be <= 255 (uint8 codes)");
         if (levels < 1) throw Fail(CCW_ERR_DIMENSION, "decomposition level must be >= 1");
-        if (levels > 30 || h % (1 << levels) != 0 || w % (1 << levels) != 0)
+        // extents 2^J does not divide are kept (the pyramid covers the top-left
+        // floor(d / 2^J) blocks); simulate rejects them unless the config
+        // enables the literal-config extension (validate_against)
+        if (levels > 30 || (h >> levels) < 1 || (w >> levels) < 1)
             throw Fail(CCW_ERR_CONFIG,
-                       fmt("training image %dx%d not divisible by 2^dwt_level = %d", h, w,
+                       fmt("training image %dx%d smaller than one 2^dwt_level = %d block", h, w,
                            1 << std::min(levels, 30)));
         if (mode != 0 && mode != 1) throw Fail(CCW_ERR_CONFIG, "facies_mode: unknown");
         if (!device_ptr) {

@@ -74,6 +74,8 @@ struct SimParams {
     int K;                   // min(candidates, npos)
     int scoring;             // 0 raw, 1 normalized
     int min_cut;
+    int any_support;         // literal-config extension: OV may not be a multiple of B; the
+                             // overlap prep counts only the supported fine cells of a block
     // simulation grid
     uint8_t* work;           // n_real planes of wh*ww
     int wh, ww;
@@ -215,6 +217,61 @@ __device__ __forceinline__ int block_stat(const uint8_t* cells, int ld, int B, i
     int acc = 0;
     for (int r = 0; r < B; ++r)
         for (int c = 0; c < B; ++c) {
+            const int code = cells[r * ld + c];
+            acc += mode == 0 ? (code == f) : code;
+        }
+    return acc;
+}
+
+// Fine-cell overlap support of a template (simulator.hpp:194-215): strips of
+// width OV on the origin's sides.
+__device__ __forceinline__ bool fine_support(int shape, int vleft, int htop, int T, int OV, int r, int c) {
+    const bool vert = shape == kVertical || shape == kL;
+    const bool horz = shape == kHorizontal || shape == kL;
+    return (vert && (vleft ? c < OV : c >= T - OV)) || (horz && (htop ? r < OV : r >= T - OV));
+}
+
+// haar_apex_block / block_stat over only the supported fine cells of a block
+// at template offset (r0, c0): extract_or's zeros stand for the others
+// (simulator.hpp:225-252) -- the literal-config extension's partial blocks.
+__device__ __forceinline__ double haar_apex_block_sup(const uint8_t* cells, int ld, int J, int mode, int f, int r0,
+                                                      int c0, int shape, int vleft, int htop, int T, int OV) {
+    double st[kMaxLevels][4];
+    int cnt[kMaxLevels];
+    for (int l = 0; l < J; ++l) cnt[l] = 0;
+    const int n = 1 << (2 * J);
+    for (int k = 0; k < n; ++k) {
+        int r = 0, c = 0;
+        for (int b = 0; b < J; ++b) {
+            c |= ((k >> (2 * b)) & 1) << b;
+            r |= ((k >> (2 * b + 1)) & 1) << b;
+        }
+        double x = 0.0;
+        if (fine_support(shape, vleft, htop, T, OV, r0 + r, c0 + c)) {
+            const int code = cells[r * ld + c];
+            x = mode == 0 ? (code == f ? 1.0 : 0.0) : (double)code;
+        }
+        int l = 0;
+        st[0][cnt[0]++] = x;
+        while (cnt[l] == 4) {
+            const double lo0 = __dadd_rn(__dmul_rn(kInvSqrt2, st[l][0]), __dmul_rn(kInvSqrt2, st[l][1]));
+            const double lo1 = __dadd_rn(__dmul_rn(kInvSqrt2, st[l][2]), __dmul_rn(kInvSqrt2, st[l][3]));
+            const double a = __dmul_rn(kInvSqrt2, __dadd_rn(lo0, lo1));
+            cnt[l] = 0;
+            ++l;
+            if (l == J) return a;
+            st[l][cnt[l]++] = a;
+        }
+    }
+    return 0.0;
+}
+
+__device__ __forceinline__ int block_stat_sup(const uint8_t* cells, int ld, int B, int mode, int f, int r0, int c0,
+                                              int shape, int vleft, int htop, int T, int OV) {
+    int acc = 0;
+    for (int r = 0; r < B; ++r)
+        for (int c = 0; c < B; ++c) {
+            if (!fine_support(shape, vleft, htop, T, OV, r0 + r, c0 + c)) continue;
             const int code = cells[r * ld + c];
             acc += mode == 0 ? (code == f) : code;
         }

@@ -76,21 +76,32 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
         const bool in = t >= t0 && t < t1;
         const uint8_t* base = grid + static_cast<size_t>(jb.top + s * B) * P.ww + jb.left + t * B;
         int8_t* w8 = P.wts8 ? P.wts8 + static_cast<size_t>(slot) * P.kpad : nullptr;
+        // literal-config extension: blocks the overlap only partly covers
+        // count / transform just their supported cells
+        auto stat = [&](int mode, int f) {
+            return P.any_support ? block_stat_sup(base, P.ww, B, mode, f, s * B, t * B, jb.shape, jb.vleft, jb.htop,
+                                                  P.T, P.OV)
+                                 : block_stat(base, P.ww, B, mode, f);
+        };
         if (P.mode == 0) {
-            const int last = in ? block_stat(base, P.ww, B, 0, P.F - 1) : 0;
+            const int last = in ? stat(0, P.F - 1) : 0;
             csum += last;
             for (int f = 0; f < P.nscr; ++f) {
-                const int v = in ? block_stat(base, P.ww, B, 0, f) - last : 0;
+                const int v = in ? stat(0, f) - last : 0;
                 wts[f * Tc * Tc + c] = v;
                 if (w8) w8[f * Tc * Tc + c] = static_cast<int8_t>(v);
             }
         } else {
-            const int v = in ? block_stat(base, P.ww, B, 1, 0) : 0;
+            const int v = in ? stat(1, 0) : 0;
             wts[c] = v;
             if (w8) w8[c] = static_cast<int8_t>(v);
         }
         for (int ch = 0; ch < P.nch; ++ch)
-            tm[ch * Tc * Tc + c] = in ? haar_apex_block(base, P.ww, P.J, P.mode, ch) : 0.0;
+            tm[ch * Tc * Tc + c] =
+                !in ? 0.0
+                    : P.any_support ? haar_apex_block_sup(base, P.ww, P.J, P.mode, ch, s * B, t * B, jb.shape, jb.vleft,
+                                                          jb.htop, P.T, P.OV)
+                                    : haar_apex_block(base, P.ww, P.J, P.mode, ch);
     }
     if (P.cjob) store_cjob(P.cjob, P.mode, P.B, slot, csum);
 }

@@ -411,7 +411,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     cudaStream_t st = ctx->stream;
     const int T = cfg.template_size, OV = cfg.overlap, J = cfg.dwt_level, B = 1 << J;
     const int stride = T - OV;
-    const int Tc = T >> J, OVc = OV >> J;
+    // literal-config extension (any_support): the coarse mask keeps every block
+    // the fine overlap touches, ceil(OV / B) coarse cells deep
+    const int Tc = T >> J, OVc = cfg.any_support ? (OV + B - 1) >> J : OV >> J;
+    // pastes land on whole TI blocks but, with an overlap 2^J does not
+    // divide, not on whole work-grid blocks: the work grid then holds the
+    // realization (as with min-cut) instead of the source-block map
+    const bool grid_mode = cfg.min_cut || (cfg.any_support && (T - OV) % B != 0);
     const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1;
     const int npos = out_h * out_w;
     const int Kp = std::min(cfg.candidates, npos);
@@ -579,8 +585,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         SP.stride = stride;
         SP.B = B;
         SP.Kp = Kp;
-        SP.nfr = static_cast<uint64_t>((ti->h - T) / B + 1);
-        SP.nfc = static_cast<uint64_t>((ti->w - T) / B + 1);
+        SP.nfr = static_cast<uint64_t>((ti->hc * B - T) / B + 1);  // (the used TI: whole blocks)
+        SP.nfc = static_cast<uint64_t>((ti->wc * B - T) / B + 1);
         SP.thr_fr = (0 - SP.nfr) % SP.nfr;
         SP.thr_fc = (0 - SP.nfc) % SP.nfc;
         SP.thr_k = (0 - static_cast<uint64_t>(Kp)) % static_cast<uint64_t>(Kp);
@@ -595,7 +601,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // the work grid exists only with min-cut (seams read the grid); otherwise
     // the source-block map is the realization until finalize
     uint8_t* d_work = nullptr;
-    if (cfg.min_cut) {
+    if (grid_mode) {
         d_work = ctx->work.as<uint8_t>(plane * n_real);
         CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
     }
@@ -655,6 +661,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     P.K = Kp;
     P.scoring = cfg.scoring;
     P.min_cut = cfg.min_cut;
+    P.any_support = cfg.any_support;
     P.work = d_work;
     P.wh = wh;
     P.ww = ww;
@@ -699,7 +706,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // source-block map (fast or_prep), valid whenever pastes are verbatim TI blocks
     const int swc = ww / B;
     int32_t* d_src = nullptr;
-    if (!cfg.min_cut) {
+    if (!grid_mode) {
         d_src = ctx->src.as<int32_t>(static_cast<size_t>(n_real) * (wh / B) * swc);
     }
     P.src = d_src;
