@@ -325,6 +325,37 @@ CCW_API ccw_status ccw_simulate3d_trace(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_si
 CCW_API ccw_status ccw_simulate3d_ensemble(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config* cfg,
                                            const int32_t* hd, int n_hd, uint8_t* out, ccw_diag3d* diag);
 
+/* ------------------------------------------ validation metrics (f3) ---- */
+/* metrics.hpp:68-311 on the device, over n realizations of h x w codes held
+ * in device memory (on_device = 1: e.g. ccw_simulate_device's output) or in
+ * host memory (copied once).  direction 0 = east_west, 1 = north_south.
+ * Messages as the reference's exceptions. */
+typedef struct ccw_phist ccw_phist;
+/* indicator_variogram (metrics.hpp:68-112): gamma[r * max_lag + h - 1];
+ * present[r] = facies occurs (may be NULL). */
+CCW_API ccw_status ccw_variogram(ccw_ctx* ctx, const uint8_t* grids, int on_device, int n, int h, int w,
+                                 int facies, int direction, int max_lag, double* gamma, int32_t* present);
+/* connectivity_function (metrics.hpp:158-205): prob[r * max_lag + h - 1],
+ * NaN where the lag has no same-facies pair (the reference's unset optional). */
+CCW_API ccw_status ccw_connectivity(ccw_ctx* ctx, const uint8_t* grids, int on_device, int n, int h, int w,
+                                    int facies, int direction, int max_lag, double* prob);
+/* ensemble_average (metrics.hpp:208-227): out h*w doubles. */
+CCW_API ccw_status ccw_ensemble_average(ccw_ctx* ctx, const uint8_t* grids, int on_device, int n, int h, int w,
+                                        int facies, double* out);
+/* downsample_majority (metrics.hpp:288-311): out (h/factor)*(w/factor) codes (host). */
+CCW_API ccw_status ccw_downsample_majority(ccw_ctx* ctx, const uint8_t* grid, int on_device, int h, int w,
+                                           int num_facies, int factor, uint8_t* out);
+/* pattern_histogram (metrics.hpp:230-254), kept on the device: exact keys
+ * (window^2 * ceil(log2 num_facies) <= 128 bits). */
+CCW_API ccw_status ccw_pattern_histogram(ccw_ctx* ctx, const uint8_t* grid, int on_device, int h, int w,
+                                         int num_facies, int window, int stride, ccw_phist** out);
+CCW_API ccw_status ccw_phist_info(const ccw_phist* hist, int64_t* distinct, int64_t* total, int* window);
+/* keys: distinct * window^2 codes (row-major windows), counts: distinct. */
+CCW_API ccw_status ccw_phist_copy(ccw_ctx* ctx, const ccw_phist* hist, uint8_t* keys, uint64_t* counts);
+CCW_API void ccw_phist_destroy(ccw_phist* hist);
+/* js_divergence (metrics.hpp:258-284), base-2, clamped to [0, 1]. */
+CCW_API ccw_status ccw_js_divergence(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* q, double* out);
+
 /* -------------------------------------------------- host-side helpers -- */
 /* SimConfig::validate / validate_against (simulator.hpp:46-84) incl.
  * validate_hard_data (grid.hpp:151-170); ti_h/ti_w <= 0 skips the TI part. */

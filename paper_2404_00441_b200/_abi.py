@@ -119,6 +119,18 @@ SIGNATURES = {
                                         P, C.POINTER(Diag3dC)]),
     "ccw_simulate3d_ensemble": (C.c_int, [P, P, C.POINTER(Sim3dConfigC), I32P, C.c_int, U8P,
                                           C.POINTER(Diag3dC)]),
+    "ccw_variogram": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, F64P,
+                                I32P]),
+    "ccw_connectivity": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   F64P]),
+    "ccw_ensemble_average": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, F64P]),
+    "ccw_downsample_majority": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, U8P]),
+    "ccw_pattern_histogram": (C.c_int, [P, U8P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(P)]),
+    "ccw_phist_info": (C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "ccw_phist_copy": (C.c_int, [P, P, U8P, U64P]),
+    "ccw_phist_destroy": (None, [P]),
+    "ccw_js_divergence": (C.c_int, [P, P, P, F64P]),
     "ccw_validate_config": (C.c_int, [C.POINTER(SimConfigC), C.c_int, C.c_int, C.c_int, I32P,
                                       C.c_int, C.c_char_p, C.c_size_t]),
     "ccw_plan_raster_path": (C.c_int, [C.POINTER(SimConfigC), C.c_int, C.c_int, INTP, INTP, I32P,

@@ -819,6 +819,104 @@ ccw_status ccw_simulate3d_ensemble(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_c
     });
 }
 
+// ------------------------------------------------------- metrics (f3) --
+
+static void check_grids(const uint8_t* g, int n, int h, int w) {
+    if (!g) throw Fail(CCW_ERR_GENERIC, "null grids");
+    if (n < 1) throw Fail(CCW_ERR_EMPTY, "ensemble_average on empty ensemble");
+    if (h < 1 || w < 1) throw Fail(CCW_ERR_DIMENSION, "grid dimensions must be positive");
+}
+
+static void check_lag(int direction, int h, int w, int max_lag) {  // metrics.hpp:70-73
+    if (direction != 0 && direction != 1) throw Fail(CCW_ERR_CONFIG, "direction: must be east_west or north_south");
+    const int extent = direction == 0 ? w : h;
+    if (max_lag < 1 || max_lag >= extent)
+        throw Fail(CCW_ERR_DIMENSION, fmt("max_lag must be in [1, extent) = [1, %d)", extent));
+}
+
+ccw_status ccw_variogram(ccw_ctx* ctx, const uint8_t* grids, int on_device, int n, int h, int w, int facies,
+                         int direction, int max_lag, double* gamma, int32_t* present) {
+    if (!ctx || !gamma) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_grids(grids, n, h, w);
+        check_lag(direction, h, w, max_lag);
+        ccwgpu::metric_variogram(ctx, grids, on_device != 0, n, h, w, facies, direction, max_lag, gamma, present);
+    });
+}
+
+ccw_status ccw_connectivity(ccw_ctx* ctx, const uint8_t* grids, int on_device, int n, int h, int w, int facies,
+                            int direction, int max_lag, double* prob) {
+    if (!ctx || !prob) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_grids(grids, n, h, w);
+        check_lag(direction, h, w, max_lag);
+        if (static_cast<int64_t>(h) * w >= (int64_t(1) << 31)) throw Fail(CCW_ERR_DIMENSION, "grid too large");
+        ccwgpu::metric_connectivity(ctx, grids, on_device != 0, n, h, w, facies, direction, max_lag, prob);
+    });
+}
+
+ccw_status ccw_ensemble_average(ccw_ctx* ctx, const uint8_t* grids, int on_device, int n, int h, int w, int facies,
+                                double* out) {
+    if (!ctx || !out) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (n < 1) throw Fail(CCW_ERR_EMPTY, "ensemble_average on empty ensemble");
+        check_grids(grids, n, h, w);
+        ccwgpu::metric_ensemble_average(ctx, grids, on_device != 0, n, h, w, facies, out);
+    });
+}
+
+ccw_status ccw_downsample_majority(ccw_ctx* ctx, const uint8_t* grid, int on_device, int h, int w, int nf, int factor,
+                                   uint8_t* out) {
+    if (!ctx || !out) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_grids(grid, 1, h, w);
+        if (factor < 1) throw Fail(CCW_ERR_DIMENSION, "downsample factor must be >= 1");  // metrics.hpp:290
+        if (h / factor < 1 || w / factor < 1)
+            throw Fail(CCW_ERR_DIMENSION, fmt("downsample factor %d too large for %dx%d", factor, h, w));
+        if (nf < 1 || nf > 256) throw Fail(CCW_ERR_DIMENSION, "num_facies must be in [1, 256]");
+        ccwgpu::metric_downsample(ctx, grid, on_device != 0, h, w, nf, factor, out, false);
+    });
+}
+
+ccw_status ccw_pattern_histogram(ccw_ctx* ctx, const uint8_t* grid, int on_device, int h, int w, int nf, int window,
+                                 int stride, ccw_phist** out) {
+    if (!ctx || !out) return CCW_ERR_GENERIC;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        check_grids(grid, 1, h, w);
+        if (window < 1 || window > h || window > w)  // metrics.hpp:232-237
+            throw Fail(CCW_ERR_DIMENSION, fmt("window %d does not fit %dx%d grid", window, h, w));
+        if (stride < 1) throw Fail(CCW_ERR_DIMENSION, "stride must be >= 1");
+        if (nf > 256) throw Fail(CCW_ERR_STRUCTURE, "byte pattern keys require num_facies <= 256");
+        *out = ccwgpu::metric_pattern_histogram(ctx, grid, on_device != 0, h, w, std::max(nf, 1), window, stride);
+    });
+}
+
+ccw_status ccw_phist_info(const ccw_phist* hist, int64_t* distinct, int64_t* total, int* window) {
+    if (!hist) return CCW_ERR_GENERIC;
+    if (distinct) *distinct = hist->n;
+    if (total) *total = static_cast<int64_t>(hist->total);
+    if (window) *window = hist->window;
+    return CCW_OK;
+}
+
+ccw_status ccw_phist_copy(ccw_ctx* ctx, const ccw_phist* hist, uint8_t* keys, uint64_t* counts) {
+    if (!ctx || !hist) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] { ccwgpu::metric_phist_copy(ctx, hist, keys, counts); });
+}
+
+void ccw_phist_destroy(ccw_phist* hist) { ccwgpu::metric_phist_destroy(hist); }
+
+ccw_status ccw_js_divergence(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* q, double* out) {
+    if (!ctx || !p || !q || !out) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (p->window != q->window)  // metrics.hpp:259-262
+            throw Fail(CCW_ERR_STRUCTURE, fmt("window sizes disagree: %d vs %d", p->window, q->window));
+        if (p->total == 0 || q->total == 0) throw Fail(CCW_ERR_EMPTY, "js_divergence on empty histogram");
+        *out = ccwgpu::metric_js(ctx, p, q);
+    });
+}
+
 ccw_status ccw_validate_config(const ccw_sim_config* cfg, int ti_h, int ti_w, int nf,
                                const int32_t* hd, int n_hd, char* msg, size_t msg_len) {
     try {

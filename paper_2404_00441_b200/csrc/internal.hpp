@@ -316,6 +316,19 @@ struct ccw_ti3d {
     int32_t* d_pk = nullptr;
 };
 
+// On-device pattern histogram (ccw_pattern_histogram): distinct exact window
+// keys (codes packed bpc bits each, 128 bits as (hi, lo)) in (hi, lo) order
+// with their multiplicities.
+struct ccw_phist {
+    int device = 0;
+    int window = 0, bpc = 0;
+    int64_t n = 0;       // distinct keys
+    uint64_t total = 0;  // windows
+    uint64_t* lo = nullptr;
+    uint64_t* hi = nullptr;
+    uint64_t* cnt = nullptr;
+};
+
 namespace ccwgpu {
 
 // --- host logic shared by the ABI (abi.cpp) ------------------------------
@@ -358,6 +371,21 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
                       const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out, ccw_diag3d* diag,
                       int32_t* trace = nullptr, int trace_cap = 0);
 void validate_config3d(const ccw_sim3d_config& c, const int32_t* ti_dims, int nf, const int32_t* hd, int n_hd);
+
+// metrics.cu (metrics.hpp:68-311 on device)
+void metric_variogram(ccw_ctx* ctx, const uint8_t* grids, bool on_device, int n, int h, int w, int facies,
+                      int direction, int max_lag, double* gamma, int32_t* present);
+void metric_connectivity(ccw_ctx* ctx, const uint8_t* grids, bool on_device, int n, int h, int w, int facies,
+                         int direction, int max_lag, double* prob);
+void metric_ensemble_average(ccw_ctx* ctx, const uint8_t* grids, bool on_device, int n, int h, int w, int facies,
+                             double* out);
+void metric_downsample(ccw_ctx* ctx, const uint8_t* grid, bool on_device, int h, int w, int nf, int factor,
+                       uint8_t* out, bool out_on_device);
+ccw_phist* metric_pattern_histogram(ccw_ctx* ctx, const uint8_t* grid, bool on_device, int h, int w, int nf,
+                                    int win, int stride);
+double metric_js(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* q);
+void metric_phist_copy(ccw_ctx* ctx, const ccw_phist* h, uint8_t* keys, uint64_t* counts);
+void metric_phist_destroy(ccw_phist* h);
 
 void op_dwt2_single(ccw_ctx* ctx, const double* in, int h, int w, double* a, double* dh,
                     double* dv, double* dd);
