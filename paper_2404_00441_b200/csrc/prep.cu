@@ -199,21 +199,52 @@ __global__ void uniform_map_kernel(const int8_t* __restrict__ pure, int wc, int 
     out[static_cast<size_t>(v) * npos + p] = static_cast<int8_t>(cls < 0 ? -1 : cls);
 }
 
-// Uniform-window classes of a TI for template Tc / overlap OVc, cached on the TI.
+// first[f] = the lowest-index pure block of facies f (INT_MAX: none)
+__global__ void first_pure_kernel(const int8_t* __restrict__ pure, int nb, int* __restrict__ first) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb && pure[b] >= 0) atomicMin(&first[pure[b]], b);
+}
+
+// out[f][ch] = the apex of a pure-f block in channel ch: every pure-f block
+// holds the same cells, so the reference-order Haar tree gives one value
+__global__ void pure_apex_kernel(const int* __restrict__ first, const double* __restrict__ ti64, int nb, int nch,
+                                 double* __restrict__ out) {
+    const int f = threadIdx.x / nch, ch = threadIdx.x % nch;
+    if (f >= 16) return;
+    out[f * nch + ch] = first[f] < nb ? ti64[static_cast<size_t>(ch) * nb + first[f]] : 0.0;
+}
+
+// Uniform-window classes of a TI for template Tc / overlap OVc, cached on the
+// TI, followed by the pure blocks and (8-byte aligned) the pure-block apex
+// table [16][nch] (ti_pure_apex).
+static size_t umap_apex_offset(size_t npos, size_t nb) { return (8 * npos + nb + 8 + 7) & ~static_cast<size_t>(7); }
+
 const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
     const auto key = std::make_pair(Tc, OVc);
     auto it = ti->umap.find(key);
     if (it != ti->umap.end()) return it->second;
     const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1, npos = out_h * out_w;
     const size_t nb = static_cast<size_t>(ti->hc) * ti->wc;
-    int8_t* m = static_cast<int8_t*>(cache_alloc(ti->device, 8 * static_cast<size_t>(npos) + nb));
+    const size_t ao = umap_apex_offset(npos, nb);
+    int8_t* m = static_cast<int8_t*>(cache_alloc(ti->device, ao + sizeof(double) * 16 * ti->nch + 16 * sizeof(int)));
     int8_t* pure = m + 8 * static_cast<size_t>(npos);
     pure_block_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(ti->d_codes, ti->w, ti->hc, ti->wc,
                                                                               1 << ti->J, pure);
     uniform_map_kernel<<<dim3((npos + 255) / 256, 8), 256, 0, st>>>(pure, ti->wc, Tc, OVc, out_w, npos, m);
+    double* apex = reinterpret_cast<double*>(m + ao);
+    int* first = reinterpret_cast<int*>(apex + 16 * ti->nch);
+    fill_i32(first, 16, INT_MAX, st);
+    first_pure_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(pure, static_cast<int>(nb), first);
+    pure_apex_kernel<<<1, 16 * ti->nch, 0, st>>>(first, ti->d_ti64, static_cast<int>(nb), ti->nch, apex);
     CCW_CUDA(cudaGetLastError());
     ti->umap[key] = m;
     return m;
+}
+
+const double* ti_pure_apex(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
+    const int8_t* m = ti_umap(ti, Tc, OVc, st);
+    const int npos = (ti->hc - Tc + 1) * (ti->wc - Tc + 1);
+    return reinterpret_cast<const double*>(m + umap_apex_offset(npos, static_cast<size_t>(ti->hc) * ti->wc));
 }
 
 }  // namespace ccwgpu

@@ -1811,6 +1811,41 @@ __global__ void __launch_bounds__(BK_T, 1)
         tk[j] = -INFINITY;
         tix[j] = INT_MAX;
     }
+    auto offer = [&](double ck, int ci) {  // per-thread top-K under the reference ranking
+#pragma unroll
+        for (int j = 0; j < kTcQ; ++j)
+            if (j < K && better(ck, ci, tk[j], tix[j])) {
+                const double t0 = tk[j];
+                const int t1 = tix[j];
+                tk[j] = ck;
+                tix[j] = ci;
+                ck = t0;
+                ci = t1;
+            }
+    };
+    // Uniform-class windows (every masked coarse block pure facies f, P.umap)
+    // carry the all-f block's apex on every masked cell, so their fp64 score is
+    // one value per class: computed once here in the reference's order
+    // (matcher.hpp:72-77, 160-161) and never rescored per window.
+    int* ucand = reinterpret_cast<int*>(bk_sm + L.ucand);
+    double* ukey = reinterpret_cast<double*>(bk_sm + L.ukey);
+    const bool uni = P.umap != nullptr && P.pure_apex != nullptr;
+    const int8_t* um = uni ? P.umap + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * P.npos : nullptr;
+    __syncthreads();  // (template and mask rows staged)
+    if (uni && tid < 16) {
+        double acc = 0.0;
+        for (int ch = 0; ch < nch; ++ch) {
+            const double c = P.pure_apex[tid * nch + ch];
+            const double* tp = tmS + ch * Tc * Tc;
+            for (int r = 0; r < nrows; ++r) {
+                const short4 rw = rows[r];
+                double sum = 0.0;
+                for (int t = rw.y; t < rw.z; ++t) sum = __dadd_rn(sum, __dmul_rn(c, tp[rw.x * Tc + t]));
+                acc = __dadd_rn(acc, sum);
+            }
+        }
+        ukey[tid] = acc;
+    }
     unsigned long long rescored = 0;
     const int nbx = (P.out_h + bx - 1) / bx, nby = (P.out_w + by - 1) / by;
     int* next = P.bulk_sync + 2 * slot;  // [0] next block, [1] finished CTAs
@@ -1830,23 +1865,27 @@ __global__ void __launch_bounds__(BK_T, 1)
         if (!__syncthreads_or(any)) continue;
         // windows of the block at or above the threshold (block-local index)
         const long long c_st = clock64();
-        int cnt = 0;
+        int cnt = 0, ucnt = 0;
         const int nb = bxa * bya;
         for (int e0 = 0; e0 < nb; e0 += BK_T * BK_V) {
-            int v[BK_V];
+            int v[BK_V], u[BK_V];
 #pragma unroll
             for (int i = 0; i < BK_V; ++i) {
                 const int e = e0 + tid * BK_V + i;
                 v[i] = INT_MIN;
+                u[i] = -1;
                 if (e < nb) {
                     const int lx = e / bya, ly = e - lx * bya;
-                    v[i] = load_score(P, slot, static_cast<size_t>(xb + lx) * P.out_w + yb + ly);
+                    const size_t p = static_cast<size_t>(xb + lx) * P.out_w + yb + ly;
+                    v[i] = load_score(P, slot, p);
+                    if (uni && v[i] >= thr) u[i] = um[p];
                 }
             }
+            // counts of rescored (low 16 bits) and uniform-class (high) windows
             int c = 0;
 #pragma unroll
-            for (int i = 0; i < BK_V; ++i) c += v[i] >= thr;
-            int incl = c;  // warp inclusive scan
+            for (int i = 0; i < BK_V; ++i) c += v[i] >= thr ? (u[i] >= 0 ? 0x10000 : 1) : 0;
+            int incl = c;  // warp inclusive scan (both halves at once: < 2^16 each)
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
@@ -1859,12 +1898,23 @@ __global__ void __launch_bounds__(BK_T, 1)
                 off += w < wid ? wcnt[w] : 0;
                 tot += wcnt[w];
             }
-            off += cnt;
+            int offr = cnt + (off & 0xFFFF), offu = ucnt + (off >> 16);
 #pragma unroll
             for (int i = 0; i < BK_V; ++i)
-                if (v[i] >= thr) cand[off++] = e0 + tid * BK_V + i;
-            cnt += tot;
+                if (v[i] >= thr) {
+                    if (u[i] >= 0)
+                        ucand[offu++] = (u[i] << 16) | (e0 + tid * BK_V + i);
+                    else
+                        cand[offr++] = e0 + tid * BK_V + i;
+                }
+            cnt += tot & 0xFFFF;
+            ucnt += tot >> 16;
             __syncthreads();
+        }
+        for (int i = tid; i < ucnt; i += BK_T) {  // uniform classes: the class key
+            const int e = ucand[i] & 0xFFFF;
+            const int lx = e / bya, ly = e - lx * bya;
+            offer(ukey[ucand[i] >> 16], (xb + lx) * P.out_w + yb + ly);
         }
         if (cnt == 0) continue;
         rescored += cnt;
@@ -1921,21 +1971,8 @@ __global__ void __launch_bounds__(BK_T, 1)
                 }
             }
 #pragma unroll
-            for (int k = 0; k < BK_W; ++k) {
-                if (!ok[k]) continue;
-                double ck = acc[k];
-                int ci = pidx[k];
-#pragma unroll
-                for (int j = 0; j < kTcQ; ++j)
-                    if (j < K && better(ck, ci, tk[j], tix[j])) {
-                        const double t0 = tk[j];
-                        const int t1 = tix[j];
-                        tk[j] = ck;
-                        tix[j] = ci;
-                        ck = t0;
-                        ci = t1;
-                    }
-            }
+            for (int k = 0; k < BK_W; ++k)
+                if (ok[k]) offer(acc[k], pidx[k]);
         }
         clk_comp += clock64() - c_cp;
     }

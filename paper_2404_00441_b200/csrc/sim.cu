@@ -730,7 +730,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
             ctx->mtab_key = key;
         }
         P.mtab = d_mt;
-        if (ctx->opt.uniform) P.umap = ti_umap(ti, Tc, OVc, st);
+        if (ctx->opt.uniform) {
+            P.umap = ti_umap(ti, Tc, OVc, st);
+            P.pure_apex = ti_pure_apex(ti, Tc, OVc, st);
+        }
     }
     // int16 score rows for the fast select when every screen score fits:
     // |S'| <= mask cells * (largest weight) * (largest block statistic)
