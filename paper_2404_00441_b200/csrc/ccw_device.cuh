@@ -111,6 +111,7 @@ struct SimParams {
     int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)
     const int4* mtab;        // fast select: mask rows and run groups per mask variant
     const double* pure_apex; // [16][nch] apex values of a pure block of facies f (any: they are equal)
+    const int* ufirst;       // [8 variants][16 classes][kTcQ] lowest window positions of each uniform class
     const int8_t* umap;      // fast select: [8 mask variants][npos] uniform class of each window --
                              // the facies every masked coarse block is made of (pure blocks), -1 if
                              // none; same class => bit-identical fp64 score (null: off)

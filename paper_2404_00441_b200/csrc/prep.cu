@@ -214,9 +214,35 @@ __global__ void pure_apex_kernel(const int* __restrict__ first, const double* __
     out[f * nch + ch] = first[f] < nb ? ti64[static_cast<size_t>(ch) * nb + first[f]] : 0.0;
 }
 
+// first[v][f][0, kTcQ): the kTcQ lowest window positions of uniform class f
+// under mask variant v (INT_MAX pads).  One CTA per (f, v): each thread keeps
+// the first matches of its contiguous chunk, chunks are merged in order.
+__global__ void __launch_bounds__(256) uniform_first_kernel(const int8_t* __restrict__ umap, int npos,
+                                                            int* __restrict__ first) {
+    const int f = blockIdx.x, v = blockIdx.y;
+    __shared__ int loc[256][kTcQ];
+    __shared__ int nloc[256];
+    const int8_t* u = umap + static_cast<size_t>(v) * npos;
+    const int chunk = (npos + blockDim.x - 1) / blockDim.x;
+    const int p0 = threadIdx.x * chunk, p1 = min(npos, p0 + chunk);
+    int n = 0;
+    for (int p = p0; p < p1 && n < kTcQ; ++p)
+        if (u[p] == f) loc[threadIdx.x][n++] = p;
+    nloc[threadIdx.x] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int* out = first + (static_cast<size_t>(v) * 16 + f) * kTcQ;
+        int k = 0;
+        for (int t = 0; t < static_cast<int>(blockDim.x) && k < kTcQ; ++t)
+            for (int i = 0; i < nloc[t] && k < kTcQ; ++i) out[k++] = loc[t][i];
+        for (; k < kTcQ; ++k) out[k] = INT_MAX;
+    }
+}
+
 // Uniform-window classes of a TI for template Tc / overlap OVc, cached on the
-// TI, followed by the pure blocks and (8-byte aligned) the pure-block apex
-// table [16][nch] (ti_pure_apex).
+// TI, followed by the pure blocks, (8-byte aligned) the pure-block apex table
+// [16][nch] (ti_pure_apex) and the first positions of every class
+// [8][16][kTcQ] (ti_uniform_first).
 static size_t umap_apex_offset(size_t npos, size_t nb) { return (8 * npos + nb + 8 + 7) & ~static_cast<size_t>(7); }
 
 const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
@@ -226,7 +252,8 @@ const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
     const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1, npos = out_h * out_w;
     const size_t nb = static_cast<size_t>(ti->hc) * ti->wc;
     const size_t ao = umap_apex_offset(npos, nb);
-    int8_t* m = static_cast<int8_t*>(cache_alloc(ti->device, ao + sizeof(double) * 16 * ti->nch + 16 * sizeof(int)));
+    int8_t* m = static_cast<int8_t*>(cache_alloc(ti->device, ao + sizeof(double) * 16 * ti->nch + 16 * sizeof(int) +
+                                                              sizeof(int) * 8 * 16 * kTcQ));
     int8_t* pure = m + 8 * static_cast<size_t>(npos);
     pure_block_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(ti->d_codes, ti->w, ti->hc, ti->wc,
                                                                               1 << ti->J, pure);
@@ -236,9 +263,15 @@ const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
     fill_i32(first, 16, INT_MAX, st);
     first_pure_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(pure, static_cast<int>(nb), first);
     pure_apex_kernel<<<1, 16 * ti->nch, 0, st>>>(first, ti->d_ti64, static_cast<int>(nb), ti->nch, apex);
+    uniform_first_kernel<<<dim3(16, 8), 256, 0, st>>>(m, npos, first + 16);
     CCW_CUDA(cudaGetLastError());
     ti->umap[key] = m;
     return m;
+}
+
+const int* ti_uniform_first(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
+    const double* apex = ti_pure_apex(ti, Tc, OVc, st);
+    return reinterpret_cast<const int*>(apex + 16 * ti->nch) + 16;
 }
 
 const double* ti_pure_apex(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {

@@ -840,6 +840,17 @@ __device__ CCW_COLD int scan_job(const SimParams& P, int slot, ScanWarp& W, int*
     //    32-tile groups and loaded SC_TB per round trip.
     int nl = 0, ntl = 0;
     bool over = false;
+    {  // more qualifying tiles than list slots: an overflow before any score is read
+        int nq = 0;
+        if (regs) {
+#pragma unroll
+            for (int i = 0; i < kTM; ++i) nq += __popc(__ballot_sync(0xffffffffu, tv[i] != INT_MIN && tv[i] >= mk));
+        } else {
+            for (int t0 = 0; t0 < P.ntiles; t0 += 32)
+                nq += __popc(__ballot_sync(0xffffffffu, t0 + lane < P.ntiles && tmx[t0 + lane] >= mk));
+        }
+        over = nq > SC_LC;
+    }
     auto flush_tiles = [&]() {
         __syncwarp();
         int tl[SC_TB], v[SC_TB][4];
@@ -1038,7 +1049,9 @@ __device__ __forceinline__ void coop_head(const SimParams& P, int slot, FastSmem
         S.misc[1] = mk;
         S.nq = nq;
         S.lcnt = 0;
-        S.lover = 0;
+        // every queued tile holds a window >= M_K: more tiles than list slots
+        // is an overflow before a single score is read
+        S.lover = nq > SC_LC ? 1 : 0;
     }
 }
 
@@ -1050,6 +1063,7 @@ template <bool S16>
 __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem& S) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nq = S.nq, mk = S.misc[1];
+    if (S.lover) return;  // (coop_head: the list cannot fit)
     for (int q0 = wid * SC_TB; q0 < nq; q0 += (FS_T / 32) * SC_TB) {
         int tl[SC_TB], v[SC_TB][4];
 #pragma unroll
@@ -1827,10 +1841,10 @@ __global__ void __launch_bounds__(BK_T, 1)
     // carry the all-f block's apex on every masked cell, so their fp64 score is
     // one value per class: computed once here in the reference's order
     // (matcher.hpp:72-77, 160-161) and never rescored per window.
-    int* ucand = reinterpret_cast<int*>(bk_sm + L.ucand);
     double* ukey = reinterpret_cast<double*>(bk_sm + L.ukey);
-    const bool uni = P.umap != nullptr && P.pure_apex != nullptr;
-    const int8_t* um = uni ? P.umap + static_cast<size_t>(mask_variant(jb.shape, jb.vleft, jb.htop)) * P.npos : nullptr;
+    const bool uni = P.umap != nullptr && P.pure_apex != nullptr && P.ufirst != nullptr;
+    const int var = mask_variant(jb.shape, jb.vleft, jb.htop);
+    const int8_t* um = uni ? P.umap + static_cast<size_t>(var) * P.npos : nullptr;
     __syncthreads();  // (template and mask rows staged)
     if (uni && tid < 16) {
         double acc = 0.0;
@@ -1845,6 +1859,13 @@ __global__ void __launch_bounds__(BK_T, 1)
             }
         }
         ukey[tid] = acc;
+        // every member of a class shares its score and key, so the class's
+        // candidates are its K lowest positions -- offered once per placement
+        // (by CTA 0), when the class reaches the threshold
+        const int* fp = P.ufirst + (static_cast<size_t>(var) * 16 + tid) * kTcQ;
+        if (part == 0 && fp[0] != INT_MAX && load_score(P, slot, fp[0]) >= thr)
+            for (int j = 0; j < K; ++j)
+                if (fp[j] != INT_MAX) offer(acc, fp[j]);
     }
     unsigned long long rescored = 0;
     const int nbx = (P.out_h + bx - 1) / bx, nby = (P.out_w + by - 1) / by;
@@ -1865,27 +1886,25 @@ __global__ void __launch_bounds__(BK_T, 1)
         if (!__syncthreads_or(any)) continue;
         // windows of the block at or above the threshold (block-local index)
         const long long c_st = clock64();
-        int cnt = 0, ucnt = 0;
+        int cnt = 0;
         const int nb = bxa * bya;
         for (int e0 = 0; e0 < nb; e0 += BK_T * BK_V) {
-            int v[BK_V], u[BK_V];
+            int v[BK_V];
 #pragma unroll
             for (int i = 0; i < BK_V; ++i) {
                 const int e = e0 + tid * BK_V + i;
                 v[i] = INT_MIN;
-                u[i] = -1;
                 if (e < nb) {
                     const int lx = e / bya, ly = e - lx * bya;
                     const size_t p = static_cast<size_t>(xb + lx) * P.out_w + yb + ly;
-                    v[i] = load_score(P, slot, p);
-                    if (uni && v[i] >= thr) u[i] = um[p];
+                    // (uniform-class windows were offered per class above)
+                    if (!uni || um[p] < 0) v[i] = load_score(P, slot, p);
                 }
             }
-            // counts of rescored (low 16 bits) and uniform-class (high) windows
             int c = 0;
 #pragma unroll
-            for (int i = 0; i < BK_V; ++i) c += v[i] >= thr ? (u[i] >= 0 ? 0x10000 : 1) : 0;
-            int incl = c;  // warp inclusive scan (both halves at once: < 2^16 each)
+            for (int i = 0; i < BK_V; ++i) c += v[i] >= thr;
+            int incl = c;  // warp inclusive scan
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
@@ -1898,23 +1917,12 @@ __global__ void __launch_bounds__(BK_T, 1)
                 off += w < wid ? wcnt[w] : 0;
                 tot += wcnt[w];
             }
-            int offr = cnt + (off & 0xFFFF), offu = ucnt + (off >> 16);
+            off += cnt;
 #pragma unroll
             for (int i = 0; i < BK_V; ++i)
-                if (v[i] >= thr) {
-                    if (u[i] >= 0)
-                        ucand[offu++] = (u[i] << 16) | (e0 + tid * BK_V + i);
-                    else
-                        cand[offr++] = e0 + tid * BK_V + i;
-                }
-            cnt += tot & 0xFFFF;
-            ucnt += tot >> 16;
+                if (v[i] >= thr) cand[off++] = e0 + tid * BK_V + i;
+            cnt += tot;
             __syncthreads();
-        }
-        for (int i = tid; i < ucnt; i += BK_T) {  // uniform classes: the class key
-            const int e = ucand[i] & 0xFFFF;
-            const int lx = e / bya, ly = e - lx * bya;
-            offer(ukey[ucand[i] >> 16], (xb + lx) * P.out_w + yb + ly);
         }
         if (cnt == 0) continue;
         rescored += cnt;

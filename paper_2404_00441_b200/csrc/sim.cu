@@ -733,6 +733,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         if (ctx->opt.uniform) {
             P.umap = ti_umap(ti, Tc, OVc, st);
             P.pure_apex = ti_pure_apex(ti, Tc, OVc, st);
+            P.ufirst = ti_uniform_first(ti, Tc, OVc, st);
         }
     }
     // int16 score rows for the fast select when every screen score fits:

@@ -254,7 +254,7 @@ constexpr int BK_V = 8;      // positions per thread per scan pass
 constexpr int BK_SMAX = 8;   // CTAs per placement (upper bound)
 
 struct BulkLayout {
-    size_t stage, tm, rows, cand, ucand, ukey, misc, total;
+    size_t stage, tm, rows, cand, ukey, misc, total;
     int sh, sw;
 };
 
@@ -272,8 +272,6 @@ __host__ __device__ inline BulkLayout bulk_layout(int nch, int Tc, int bx, int b
     L.rows = o;
     o += static_cast<size_t>(Tc) * sizeof(short4);
     L.cand = o;
-    o += (static_cast<size_t>(bx) * by + BK_T) * sizeof(int);
-    L.ucand = o;  // uniform-class windows: (class << 16) | block-local index
     o += (static_cast<size_t>(bx) * by + BK_T) * sizeof(int);
     o = (o + 15) & ~static_cast<size_t>(15);
     L.ukey = o;   // fp64 key of each uniform class for this placement
@@ -310,6 +308,7 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
 const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 const double* ti_pure_apex(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
+const int* ti_uniform_first(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 void fill_i32(int32_t* p, size_t n, int32_t v, cudaStream_t st);
 // ccf_direct.cu
 size_t ccf_smem_bytes(int Tc, int nscr);
