@@ -133,7 +133,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 // One (job tile, half position tile) of accumulators, drained from TMEM:
 // the exact scores and the tile maximum.  stage = this warp's 4 KB of shared
 // memory (32 rows x 128 B, 16-byte chunks swizzled by row) for the transpose.
-template <bool S16>
+template <bool S16, bool NU>
 __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int m0, int n0,
                                             int warp, int lane, uint32_t stage) {
     const int q = warp & 3;
@@ -142,7 +142,10 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
     const uint32_t trow = tbuf + (static_cast<uint32_t>(q * 32) << 16) + half * (kN / 2);
     const int pbase = n0 + half * (kN / 2);
     const int ntile = (n0 / kN) * 2 + half;
-    int mx = INT_MIN;
+    int mx = INT_MIN, mxn = INT_MIN;
+    const bool nu = NU && job < a.nj;
+    uint4 ub = make_uint4(0, 0, 0, 0);  // this job's non-uniform bits of the 128 positions (tmax_nu)
+    if (NU && nu) ub = *reinterpret_cast<const uint4*>(a.ubits + static_cast<size_t>(a.jvar[job]) * (a.ustride / 32) + pbase / 32);
     // store phase: lane -> (row r0 + 4 i, 16-byte chunk lane & 7)
     const int srow = lane >> 3, schunk = lane & 7;
 #ifndef CCW_TC_LDTM1  // (measured r1: two chunks per wait is ~2% faster end to end)
@@ -151,6 +154,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
 #ifdef CCW_TC_LDTM2
     uint32_t rr[2][32];  // two 32-column chunks per TMEM round trip (more registers)
 #endif
+#pragma unroll
     for (int c = 0; c < kN / 64; ++c) {
 #ifdef CCW_TC_LDTM2
         if ((c & 1) == 0) {
@@ -169,6 +173,12 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
 #pragma unroll
         for (int i = 0; i < 32; ++i)
             if (i < lim) mx = max(mx, static_cast<int>(r[i]));
+        if (NU && nu) {  // (the bits are 0 past npos: ustride covers whole tiles)
+            const uint32_t bm = c == 0 ? ub.x : c == 1 ? ub.y : c == 2 ? ub.z : ub.w;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if ((bm >> i) & 1u) mxn = max(mxn, static_cast<int>(r[i]));
+        }
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
             const uint32_t addr = stage + lane * 128 + ((v ^ (lane & 7)) << 4);
@@ -203,6 +213,7 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
         __syncwarp();
     }
     if (job < a.nj) a.tmax[static_cast<size_t>(job) * a.ntiles + ntile] = mx;
+    if (NU && nu) a.tmax_nu[static_cast<size_t>(job) * a.ntiles + ntile] = mxn;
 }
 
 // Persistent implicit GEMM: one CTA per SM loops over (job tile, position
@@ -213,7 +224,9 @@ __device__ __forceinline__ void tc_epilogue(const TcArgs& a, uint32_t tbuf, int 
 #ifndef CCW_TC_MINB
 #define CCW_TC_MINB 1
 #endif
-template <bool S16>  // int16 score rows (a separate instance keeps the int32 one unchanged)
+// S16: int16 score rows; NU: per-tile non-uniform maxima too (tie-storm TIs)
+// -- separate instances keep the common one's registers unchanged
+template <bool S16, bool NU>
 __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
     ccf_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   TcArgs a) {
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, CCW_TC_MINB)
             if (lt == 0 && warp == 2 && lane == 0) probe(4);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int m0 = (t % n_mt) * kM, n0 = (t / n_mt) * kN;
-            tc_epilogue<S16>(a, tmem + b * kN, m0, n0, warp, lane, epi_stage + (warp - 2) * 4096);
+            tc_epilogue<S16, NU>(a, tmem + b * kN, m0, n0, warp, lane, epi_stage + (warp - 2) * 4096);
             if (lt == 0 && lane == 0) probe(5);  // summed over the 8 epilogue warps
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -540,16 +553,21 @@ TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
     TcPlan pl;
     pl.ma = make_map(const_cast<int8_t*>(d_w8), kpad, maxj, kM);
     pl.mb = make_map(const_cast<int8_t*>(d_x), kpad, npos, kN);
-    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(ccf_tc_smem_bytes())));
-    CCW_CUDA(cudaFuncSetAttribute(ccf_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(ccf_tc_smem_bytes())));
+    for (auto k : {ccf_tc_kernel<false, false>, ccf_tc_kernel<true, false>, ccf_tc_kernel<false, true>,
+                   ccf_tc_kernel<true, true>})
+        CCW_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ccf_tc_smem_bytes())));
     return pl;
 }
 
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
-                   int32_t* tmax, cudaStream_t st, unsigned long long* tl, int tmax_ld, int s16) {
-    TcArgs a;
+                   int32_t* tmax, cudaStream_t st, unsigned long long* tl, int tmax_ld, int s16, int32_t* tmax_nu,
+                   const uint32_t* ubits, int ustride, const int8_t* jvar) {
+    TcArgs a{};
+    a.tmax_nu = tmax_nu;
+    a.ubits = ubits;
+    a.ustride = ustride;
+    a.jvar = jvar;
     a.nj = nj;
     a.npos = npos;
     a.sld = sld;
@@ -565,10 +583,9 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     const int slots = tc_num_sms() * CCW_TC_MINB;
     a.epi_in_ring = ntot <= slots;
     dim3 grid(std::min(ntot, a.epi_in_ring ? slots : tc_num_sms()));
-    if (s16)
-        launch_pdl(ccf_tc_kernel<true>, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
-    else
-        launch_pdl(ccf_tc_kernel<false>, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
+    auto k = s16 ? (tmax_nu ? ccf_tc_kernel<true, true> : ccf_tc_kernel<true, false>)
+                 : (tmax_nu ? ccf_tc_kernel<false, true> : ccf_tc_kernel<false, false>);
+    launch_pdl(k, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);
 }
 
 int tc_tiles(int npos) { return 2 * ((npos + kN - 1) / kN); }  // tile maxima per score row

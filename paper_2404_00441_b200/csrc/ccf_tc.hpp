@@ -26,6 +26,12 @@ struct TcArgs {
     int s16;                    // score rows as int16 (exact: the host checks |S| < 2^15)
     int epi_in_ring;            // every CTA drains one tile: the epilogue's transpose
                                 // staging reuses the (then idle) TMA ring
+    // optional: per tile the maximum over NON-uniform windows (tie-storm
+    // placements skip the uniform classes, whose scores are class constants)
+    int32_t* tmax_nu;           // [nj][ntiles] (null: off)
+    const uint32_t* ubits;      // [8][ustride / 32] non-uniform windows as bits
+    int ustride;
+    const int8_t* jvar;         // [nj] mask variant of each job
 };
 
 size_t ccf_tc_smem_bytes(bool epi_in_ring = false);
@@ -48,6 +54,7 @@ TcPlan plan_ccf_tc(const int8_t* d_w8, int maxj, const int8_t* d_x, int npos, in
 void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_t* scores,
                    int32_t* tmax, cudaStream_t st, unsigned long long* tl = nullptr,
                    int tmax_ld = -1,   // tmax row stride (default: this launch's tile count)
-                   int s16 = 0);       // store int16 score rows
+                   int s16 = 0, int32_t* tmax_nu = nullptr, const uint32_t* ubits = nullptr, int ustride = 0,
+                   const int8_t* jvar = nullptr);       // store int16 score rows
 
 }  // namespace ccwgpu

@@ -99,6 +99,9 @@ struct SimParams {
     int sld;
     int s16;                 // fast select: score rows hold int16 (exact when |S| < 2^15, host-checked)
     int* defer;              // per job slot: threshold handed to select_bulk_kernel, INT_MIN = none
+    int* defer_list;         // deferred job slots of this launch (appended by the fast select)
+    int* defer_cnt;          //   ... their count (two counters alternate by launch parity:
+    int* defer_cnt_next;     //   the bulk launch zeroes the next launch's)
     // fused OR prep: the select of wave w prepares the placements of wave w+1
     // once both of their wave-w dependencies have pasted (null: separate launch)
     int* depcnt;             // per next-wave slot: dependencies that have pasted
@@ -110,6 +113,9 @@ struct SimParams {
     int bulk_bx, bulk_by;    // select_bulk_kernel window block (positions per shared-memory tile)
     int32_t* cjob;           // normalized screen: per job slot, S = S' + cjob (null otherwise)
     const int4* mtab;        // fast select: mask rows and run groups per mask variant
+    int ustride;             // row stride of umap (a multiple of 256 >= npos)
+    int8_t* jvar;            // per job slot: mask variant (written by the OR prep; null: unused)
+    int32_t* tmax_nu;        // per job slot: per tile the max score over non-uniform windows (null: off)
     const double* pure_apex; // [16][nch] apex values of a pure block of facies f (any: they are equal)
     const int* ufirst;       // [8 variants][16 classes][kTcQ] lowest window positions of each uniform class
     const int8_t* umap;      // fast select: [8 mask variants][npos] uniform class of each window --

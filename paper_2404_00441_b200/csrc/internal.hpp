@@ -272,7 +272,7 @@ struct ccw_ctx {
     ccw_timing timing{};
     // scratch
     ccwgpu::DevBuf cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
-        stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, ops_a, ops_b, ops_c, ops_d, ops_e;
+        stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, tmaxnu, jvar, ops_a, ops_b, ops_c, ops_d, ops_e;
     long long mtab_key = -1;  // (Tc, OVc, nch) of the mask tables in mtab
     ccwgpu::HostBuf h_stage;
     ccwgpu::HostBuf h_out_stage;  // pinned landing zone when the caller's result buffer is pageable
@@ -284,6 +284,9 @@ struct ccw_ctx {
     // deferred no placement to the bulk tie select skip its per-wave launch
     // (re-enabled when the warp select reports a would-be deferral)
     std::map<std::tuple<uint64_t, int, int, int, int>, bool> bulk_off;
+    // ... and whose last call deferred many placements (a tie storm: the
+    // screen then also keeps per-tile non-uniform maxima for the bulk kernel)
+    std::map<std::tuple<uint64_t, int, int, int, int>, bool> tie_storm;
     // candidate-position sharding (ccw_ctx_set_position_shards)
     int shard_nranks = 1, shard_rank = 0, shard_virtual = 1;
     void* nccl_comm = nullptr;  // ncclComm_t when shard_nranks > 1 (or an explicit id was given)

@@ -49,6 +49,7 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
     pdl_trigger();
     const int slot = blockIdx.x;
     const Job jb = jobs[job0 + slot];
+    if (P.jvar && threadIdx.x == 0) P.jvar[slot] = static_cast<int8_t>(mask_variant(jb.shape, jb.vleft, jb.htop));
     tl_mark(P.tl, 2);
     pdl_wait();
     tl_mark(P.tl, 0);
@@ -61,6 +62,7 @@ __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int jo
     const int slot = blockIdx.x;
     const Job jb = jobs[job0 + slot];
     pdl_wait();
+    if (P.jvar && threadIdx.x == 0) P.jvar[slot] = static_cast<int8_t>(mask_variant(jb.shape, jb.vleft, jb.htop));
     const int Tc = P.Tc, B = P.B;
     const uint8_t* grid = P.work + static_cast<size_t>(jb.real) * P.wh * P.ww;
     int32_t* wts = P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
@@ -175,7 +177,7 @@ __global__ void pure_block_kernel(const uint8_t* __restrict__ codes, int w, int 
 // values on every masked cell in every channel (indicator or raw codes), so
 // their fp64 scores (matcher.hpp:64-81) are bit-identical for any template.
 __global__ void uniform_map_kernel(const int8_t* __restrict__ pure, int wc, int Tc, int OVc, int out_w, int npos,
-                                   int8_t* __restrict__ out) {
+                                   int ustride, int8_t* __restrict__ out) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int v = blockIdx.y;
     if (p >= npos) return;
@@ -196,7 +198,7 @@ __global__ void uniform_map_kernel(const int8_t* __restrict__ pure, int wc, int 
             cls = f;
         }
     }
-    out[static_cast<size_t>(v) * npos + p] = static_cast<int8_t>(cls < 0 ? -1 : cls);
+    out[static_cast<size_t>(v) * ustride + p] = static_cast<int8_t>(cls < 0 ? -1 : cls);
 }
 
 // first[f] = the lowest-index pure block of facies f (INT_MAX: none)
@@ -217,12 +219,12 @@ __global__ void pure_apex_kernel(const int* __restrict__ first, const double* __
 // first[v][f][0, kTcQ): the kTcQ lowest window positions of uniform class f
 // under mask variant v (INT_MAX pads).  One CTA per (f, v): each thread keeps
 // the first matches of its contiguous chunk, chunks are merged in order.
-__global__ void __launch_bounds__(256) uniform_first_kernel(const int8_t* __restrict__ umap, int npos,
+__global__ void __launch_bounds__(256) uniform_first_kernel(const int8_t* __restrict__ umap, int npos, int ustride,
                                                             int* __restrict__ first) {
     const int f = blockIdx.x, v = blockIdx.y;
     __shared__ int loc[256][kTcQ];
     __shared__ int nloc[256];
-    const int8_t* u = umap + static_cast<size_t>(v) * npos;
+    const int8_t* u = umap + static_cast<size_t>(v) * ustride;
     const int chunk = (npos + blockDim.x - 1) / blockDim.x;
     const int p0 = threadIdx.x * chunk, p1 = min(npos, p0 + chunk);
     int n = 0;
@@ -239,11 +241,32 @@ __global__ void __launch_bounds__(256) uniform_first_kernel(const int8_t* __rest
     }
 }
 
+// Non-uniform windows as bits: [8][ustride / 32] words, bit i of word k set
+// when window 32 k + i of the variant is non-uniform (the screen's tmax_nu).
+__global__ void uniform_bits_kernel(const int8_t* __restrict__ umap, int npos, int ustride, uint32_t* __restrict__ bits) {
+    const int nw = ustride / 32;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= 8 * nw) return;
+    const int v = e / nw, k = e - v * nw;
+    const int8_t* u = umap + static_cast<size_t>(v) * ustride + 32 * k;
+    uint32_t b = 0;
+    for (int i = 0; i < 32; ++i) b |= static_cast<uint32_t>(32 * k + i < npos && u[i] < 0) << i;
+    bits[e] = b;
+}
+
 // Uniform-window classes of a TI for template Tc / overlap OVc, cached on the
 // TI, followed by the pure blocks, (8-byte aligned) the pure-block apex table
 // [16][nch] (ti_pure_apex) and the first positions of every class
 // [8][16][kTcQ] (ti_uniform_first).
-static size_t umap_apex_offset(size_t npos, size_t nb) { return (8 * npos + nb + 8 + 7) & ~static_cast<size_t>(7); }
+template <typename T>
+static T* align16(T* p) {  // (the screen epilogue reads the bits as uint4)
+    return reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(p) + 15) & ~static_cast<uintptr_t>(15));
+}
+
+int umap_stride(int npos) { return (npos + 255) & ~255; }  // (whole 256-position screen tiles)
+static size_t umap_apex_offset(size_t npos, size_t nb) {
+    return (8 * static_cast<size_t>(umap_stride(static_cast<int>(npos))) + nb + 8 + 7) & ~static_cast<size_t>(7);
+}
 
 const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
     const auto key = std::make_pair(Tc, OVc);
@@ -253,20 +276,29 @@ const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
     const size_t nb = static_cast<size_t>(ti->hc) * ti->wc;
     const size_t ao = umap_apex_offset(npos, nb);
     int8_t* m = static_cast<int8_t*>(cache_alloc(ti->device, ao + sizeof(double) * 16 * ti->nch + 16 * sizeof(int) +
-                                                              sizeof(int) * 8 * 16 * kTcQ));
-    int8_t* pure = m + 8 * static_cast<size_t>(npos);
+                                                              sizeof(int) * 8 * 16 * kTcQ +
+                                                              sizeof(uint32_t) * 8 * (umap_stride(npos) / 32) + 16));
+    const int us = umap_stride(npos);
+    int8_t* pure = m + 8 * static_cast<size_t>(us);
+    CCW_CUDA(cudaMemsetAsync(m, 0xFF, 8 * static_cast<size_t>(us), st));  // (padding: non-uniform)
     pure_block_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(ti->d_codes, ti->w, ti->hc, ti->wc,
                                                                               1 << ti->J, pure);
-    uniform_map_kernel<<<dim3((npos + 255) / 256, 8), 256, 0, st>>>(pure, ti->wc, Tc, OVc, out_w, npos, m);
+    uniform_map_kernel<<<dim3((npos + 255) / 256, 8), 256, 0, st>>>(pure, ti->wc, Tc, OVc, out_w, npos, us, m);
     double* apex = reinterpret_cast<double*>(m + ao);
     int* first = reinterpret_cast<int*>(apex + 16 * ti->nch);
     fill_i32(first, 16, INT_MAX, st);
     first_pure_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(pure, static_cast<int>(nb), first);
     pure_apex_kernel<<<1, 16 * ti->nch, 0, st>>>(first, ti->d_ti64, static_cast<int>(nb), ti->nch, apex);
-    uniform_first_kernel<<<dim3(16, 8), 256, 0, st>>>(m, npos, first + 16);
+    uniform_first_kernel<<<dim3(16, 8), 256, 0, st>>>(m, npos, us, first + 16);
+    uint32_t* ubits = align16(reinterpret_cast<uint32_t*>(first + 16 + 8 * 16 * kTcQ));
+    uniform_bits_kernel<<<(8 * (us / 32) + 255) / 256, 256, 0, st>>>(m, npos, us, ubits);
     CCW_CUDA(cudaGetLastError());
     ti->umap[key] = m;
     return m;
+}
+
+const uint32_t* ti_uniform_bits(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {
+    return align16(reinterpret_cast<const uint32_t*>(ti_uniform_first(ti, Tc, OVc, st) + 8 * 16 * kTcQ));
 }
 
 const int* ti_uniform_first(ccw_ti* ti, int Tc, int OVc, cudaStream_t st) {

@@ -991,7 +991,7 @@ struct FastSmem {
 constexpr int UD_MIN = 8;
 __device__ CCW_COLD int uniform_reduce(const SimParams& P, FastSmem& S, int g, int var) {
     const int tid = threadIdx.x;
-    const int8_t* um = P.umap + static_cast<size_t>(var) * P.npos;
+    const int8_t* um = P.umap + static_cast<size_t>(var) * P.ustride;
     if (tid < 16) S.urep[tid] = INT_MAX;
     if (tid < 2) S.ucnt[tid] = 0;
     __syncthreads();
@@ -1535,7 +1535,10 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         mk = S.misc[1];
         int ntop = 0;
         if (n < 0 && P.defer) {  // a large tie group: the bulk kernel rescores every window >= M_K
-            if (tid == 0) P.defer[slot] = max(mk, INT_MIN + 1);  // (INT_MIN marks "not deferred")
+            if (tid == 0) {
+                P.defer[slot] = max(mk, INT_MIN + 1);  // (INT_MIN marks "not deferred")
+                if (P.defer_list) P.defer_list[atomicAdd(P.defer_cnt, 1)] = slot;
+            }
             return;
         }
         if (P.defer && tid == 0) P.defer[slot] = INT_MIN;
@@ -1773,15 +1776,9 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
 template __global__ void select_fast_kernel<false>(const __grid_constant__ SimParams, const Job* __restrict__, int, int);
 template __global__ void select_fast_kernel<true>(const __grid_constant__ SimParams, const Job* __restrict__, int, int);
 
-__global__ void __launch_bounds__(BK_T, 1)
-    select_bulk_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj, int S) {
-    extern __shared__ __align__(16) unsigned char bk_sm[];
-    pdl_trigger();
-    tl_mark(P.tl, 2);
-    pdl_wait();
-    tl_mark(P.tl, 0);
-    const int slot = blockIdx.y, part = blockIdx.x;
-    if (slot >= nj) return;
+// One CTA's share (part of S) of one deferred placement.
+__device__ __forceinline__ void bulk_part(const SimParams& P, const Job* __restrict__ jobs, int job0, int slot,
+                                          int part, int S, unsigned char* bk_sm) {
     const int thr = P.defer[slot];
     if (thr == INT_MIN) return;  // handled by the warp select
     const int gj = job0 + slot;
@@ -1844,7 +1841,7 @@ __global__ void __launch_bounds__(BK_T, 1)
     double* ukey = reinterpret_cast<double*>(bk_sm + L.ukey);
     const bool uni = P.umap != nullptr && P.pure_apex != nullptr && P.ufirst != nullptr;
     const int var = mask_variant(jb.shape, jb.vleft, jb.htop);
-    const int8_t* um = uni ? P.umap + static_cast<size_t>(var) * P.npos : nullptr;
+    const int8_t* um = uni ? P.umap + static_cast<size_t>(var) * P.ustride : nullptr;
     __syncthreads();  // (template and mask rows staged)
     if (uni && tid < 16) {
         double acc = 0.0;
@@ -1868,9 +1865,51 @@ __global__ void __launch_bounds__(BK_T, 1)
                 if (fp[j] != INT_MAX) offer(acc, fp[j]);
     }
     unsigned long long rescored = 0;
+#ifdef CCW_DEBUG_KNOBS
+    const long long dbg_c0 = clock64();
+#endif
     const int nbx = (P.out_h + bx - 1) / bx, nby = (P.out_w + by - 1) / by;
     int* next = P.bulk_sync + 2 * slot;  // [0] next block, [1] finished CTAs
+    if (P.tmax_nu && uni) {
+        // Only a tile whose maximum over NON-uniform windows reaches the
+        // threshold can hold a candidate the class keys do not cover: this
+        // CTA's share (tiles part, part + S, ...) is filtered on the screen's
+        // tmax_nu, and each qualifying tile's windows are checked by one
+        // thread each and rescored straight from L2 (reference order).
+        const int32_t* tn = P.tmax_nu + static_cast<size_t>(slot) * P.ntiles;
+        int* tq = cand;
+        if (tid == 0) wcnt[0] = 0;
+        __syncthreads();
+        for (int t = part + S * tid; t < P.ntiles; t += S * BK_T)
+            if (tn[t] >= thr) tq[atomicAdd(&wcnt[0], 1)] = t;
+        __syncthreads();
+        const int nq = wcnt[0];
+        constexpr int kTpp = BK_T / kTcTile;  // tiles per pass
+        for (int q0 = 0; q0 < nq; q0 += kTpp) {
+            const int qi = q0 + tid / kTcTile;
+            if (qi >= nq) continue;
+            const int p = tq[qi] * kTcTile + tid % kTcTile;
+            if (p >= P.npos || um[p] >= 0 || load_score(P, slot, p) < thr) continue;
+            const int x = p / P.out_w, y = p - x * P.out_w;
+            double acc = 0.0;
+            for (int ch = 0; ch < nch; ++ch) {
+                const double* sp = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc + static_cast<size_t>(x) * P.wc + y;
+                const double* tp = tmS + ch * Tc * Tc;
+                for (int r = 0; r < nrows; ++r) {
+                    const short4 rw = rows[r];
+                    const double* a = sp + rw.x * P.wc + rw.y;
+                    const double* b = tp + rw.x * Tc + rw.y;
+                    double sum = 0.0;  // sum += ti*or left to right (matcher.hpp:72-76)
+                    for (int t = 0; t < rw.z - rw.y; ++t) sum = __dadd_rn(sum, __dmul_rn(__ldg(a + t), b[t]));
+                    acc = __dadd_rn(acc, sum);
+                }
+            }
+            offer(acc, p);
+            if (P.stats) atomicAdd(&P.stats[0], 1ull);
+        }
+    }
     for (;;) {
+        if (P.tmax_nu && uni) break;  // (the tile path above covered this placement)
         __syncthreads();  // previous block's stage / candidates consumed
         if (tid == 0) shv[0] = atomicAdd(next, 1);
         __syncthreads();
@@ -1889,18 +1928,26 @@ __global__ void __launch_bounds__(BK_T, 1)
         int cnt = 0;
         const int nb = bxa * bya;
         for (int e0 = 0; e0 < nb; e0 += BK_T * BK_V) {
+            // every load of the pass in flight at once (score and class are
+            // independent: one round trip per pass)
             int v[BK_V];
+            int8_t u[BK_V];
 #pragma unroll
             for (int i = 0; i < BK_V; ++i) {
                 const int e = e0 + tid * BK_V + i;
                 v[i] = INT_MIN;
+                u[i] = -1;
                 if (e < nb) {
                     const int lx = e / bya, ly = e - lx * bya;
                     const size_t p = static_cast<size_t>(xb + lx) * P.out_w + yb + ly;
-                    // (uniform-class windows were offered per class above)
-                    if (!uni || um[p] < 0) v[i] = load_score(P, slot, p);
+                    v[i] = load_score(P, slot, p);
+                    if (uni) u[i] = um[p];
                 }
             }
+            // (uniform-class windows were offered per class above)
+#pragma unroll
+            for (int i = 0; i < BK_V; ++i)
+                if (u[i] >= 0) v[i] = INT_MIN;
             int c = 0;
 #pragma unroll
             for (int i = 0; i < BK_V; ++i) c += v[i] >= thr;
@@ -1926,19 +1973,24 @@ __global__ void __launch_bounds__(BK_T, 1)
         }
         if (cnt == 0) continue;
         rescored += cnt;
-        // stage the apex tile the block's windows read
-        const int sha = bxa + Tc - 1, swa = bya + Tc - 1;
-        for (int ch = 0; ch < nch; ++ch) {
-            const double* src = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
-                                static_cast<size_t>(xb) * P.wc + yb;
-            double* dst = stg + static_cast<size_t>(ch) * L.sh * L.sw;
-            for (int e = tid; e < sha * swa; e += BK_T) {
-                const int r = e / swa, c = e - r * swa;
-                cp_async8(dst + r * L.sw + c, src + static_cast<size_t>(r) * P.wc + c);
+        // stage the apex tile the block's windows read -- worth it only for
+        // many windows; a few are rescored straight from L2
+        const bool staged = cnt >= BK_STAGE_MIN;
+        const int pitch = staged ? L.sw : P.wc;
+        if (staged) {
+            const int sha = bxa + Tc - 1, swa = bya + Tc - 1;
+            for (int ch = 0; ch < nch; ++ch) {
+                const double* src = P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
+                                    static_cast<size_t>(xb) * P.wc + yb;
+                double* dst = stg + static_cast<size_t>(ch) * L.sh * L.sw;
+                for (int e = tid; e < sha * swa; e += BK_T) {
+                    const int r = e / swa, c = e - r * swa;
+                    cp_async8(dst + r * L.sw + c, src + static_cast<size_t>(r) * P.wc + c);
+                }
             }
+            cp_async_wait_all();
+            __syncthreads();
         }
-        cp_async_wait_all();
-        __syncthreads();
         const long long c_cp = clock64();
         clk_stage += c_cp - c_st;
         for (int i0 = tid; i0 < cnt; i0 += BK_T * BK_W) {
@@ -1950,18 +2002,20 @@ __global__ void __launch_bounds__(BK_T, 1)
                 ok[k] = i < cnt;
                 const int e = cand[ok[k] ? i : i0];
                 const int lx = e / bya, ly = e - lx * bya;
-                base[k] = lx * L.sw + ly;
+                base[k] = lx * pitch + ly;
                 pidx[k] = (xb + lx) * P.out_w + yb + ly;
             }
             double acc[BK_W];
 #pragma unroll
             for (int k = 0; k < BK_W; ++k) acc[k] = 0.0;
             for (int ch = 0; ch < nch; ++ch) {
-                const double* sp = stg + static_cast<size_t>(ch) * L.sh * L.sw;
+                const double* sp = staged ? stg + static_cast<size_t>(ch) * L.sh * L.sw
+                                          : P.ti64 + static_cast<size_t>(ch) * P.hc * P.wc +
+                                                static_cast<size_t>(xb) * P.wc + yb;
                 const double* tp = tmS + ch * Tc * Tc;
                 for (int r = 0; r < nrows; ++r) {
                     const short4 rw = rows[r];
-                    const double* a = sp + rw.x * L.sw + rw.y;
+                    const double* a = sp + rw.x * pitch + rw.y;
                     const double* b = tp + rw.x * Tc + rw.y;
                     const int len = rw.z - rw.y;
                     double sum[BK_W];
@@ -1984,6 +2038,14 @@ __global__ void __launch_bounds__(BK_T, 1)
         }
         clk_comp += clock64() - c_cp;
     }
+#ifdef CCW_DEBUG_KNOBS
+    const long long dbg_c1 = clock64();
+    if (tid == 0 && P.stats) {
+        atomicAdd(&P.stats[44], static_cast<unsigned long long>(dbg_c0 - clk_start));
+        atomicAdd(&P.stats[45], static_cast<unsigned long long>(dbg_c1 - dbg_c0));
+        atomicMax(&P.stats[46], static_cast<unsigned long long>(dbg_c1 - clk_start));
+    }
+#endif
     // this CTA's top-K: K rounds of a block-wide arg-best over the per-thread lists
     double* lk = stg;
     int* li = reinterpret_cast<int*>(stg + BK_T * kTcQ);
@@ -2045,6 +2107,9 @@ __global__ void __launch_bounds__(BK_T, 1)
     }
     __syncthreads();
     if (shv[2] != S - 1) return;  // not the last CTA of this placement
+#ifdef CCW_DEBUG_KNOBS
+    const long long dbg_c2 = clock64();
+#endif
     // last CTA: merge the S lists (reference ranking), choose, paste
     __threadfence();
     const int nm = S * K;
@@ -2107,6 +2172,39 @@ __global__ void __launch_bounds__(BK_T, 1)
     if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
+#ifdef CCW_DEBUG_KNOBS
+        if (P.stats) atomicAdd(&P.stats[47], static_cast<unsigned long long>(clock64() - dbg_c2));
+#endif
+    }
+}
+
+// Persistent over the launch's deferred placements (the fast select lists
+// them): CTA b takes work items b, b + gridDim.x, ... = (placement, part).
+// Without a list (defer_list null) the grid is (S, nj) as one item per CTA.
+__global__ void __launch_bounds__(BK_T, 1)
+    select_bulk_kernel(SimParams P, const Job* __restrict__ jobs, int job0, int nj, int S) {
+    extern __shared__ __align__(16) unsigned char bk_sm[];
+    pdl_trigger();
+    tl_mark(P.tl, 2);
+    pdl_wait();
+    tl_mark(P.tl, 0);
+    if (!P.defer_list) {
+        if (static_cast<int>(blockIdx.y) < nj) bulk_part(P, jobs, job0, blockIdx.y, blockIdx.x, S, bk_sm);
+        tl_mark(P.tl, 1);
+        return;
+    }
+    const int ndef = __ldcg(P.defer_cnt);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.defer_cnt_next = 0;  // (the next launch's list)
+    // as many CTAs per deferred placement as the grid covers (the same S in
+    // every CTA: each placement's last CTA is its (S-1)-th finisher)
+#ifndef CCW_BK_CAP
+#define CCW_BK_CAP 8
+#endif
+    const int Sd = max(1, min(CCW_BK_CAP, static_cast<int>(gridDim.x) / max(ndef, 1)));
+    (void)S;
+    for (int w = blockIdx.x; w < ndef * Sd; w += gridDim.x) {
+        __syncthreads();  // (the previous item's shared memory is consumed)
+        bulk_part(P, jobs, job0, __ldcg(P.defer_list + w / Sd), w % Sd, Sd, bk_sm);
     }
     tl_mark(P.tl, 1);
 }

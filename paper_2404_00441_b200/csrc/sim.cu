@@ -732,6 +732,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.mtab = d_mt;
         if (ctx->opt.uniform) {
             P.umap = ti_umap(ti, Tc, OVc, st);
+            P.ustride = umap_stride(npos);
             P.pure_apex = ti_pure_apex(ti, Tc, OVc, st);
             P.ufirst = ti_uniform_first(ti, Tc, OVc, st);
         }
@@ -748,9 +749,15 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // bulk tie select: largest window block whose apex tile fits the shared-memory budget
     size_t bulk_smem = 0;
     if ((warp_select || shard_fast) && ctx->opt.bulk) {
+        // (measured r2, config 2: blocks of up to 64 x 256 windows beat 32 x 64
+        // ones, 19.0 vs 25.0 ms -- every block costs a tile-max round trip)
         constexpr size_t kBudget = 200 * 1024;
-        for (int by = std::min(out_w, 256); by >= 8 && !bulk_smem; by /= 2) {
-            int bx = std::min(out_h, 64);
+#ifndef CCW_BK_BY
+#define CCW_BK_BY 256
+#define CCW_BK_BX 64
+#endif
+        for (int by = std::min(out_w, CCW_BK_BY); by >= 8 && !bulk_smem; by /= 2) {
+            int bx = std::min(out_h, CCW_BK_BX);
             while (bx > 1 && bulk_layout(ti->nch, Tc, bx, by).total > kBudget) --bx;
             if (bulk_layout(ti->nch, Tc, bx, by).total <= kBudget && (bx >= 4 || bx == out_h)) {
                 P.bulk_bx = bx;
@@ -761,7 +768,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     const auto bulk_key = std::make_tuple(ti->key, Tc, OVc, Kp, T);
     const bool bulk_launch = bulk_smem && !ctx->bulk_off.count(bulk_key);
-    int* d_defer = bulk_launch ? ctx->defer.as<int>(G * maxj) : nullptr;
+    // thresholds [G][maxj], deferred-slot lists [G][maxj], list counters [G][2]
+    int* d_defer = bulk_launch ? ctx->defer.as<int>(2 * G * maxj + 2 * G) : nullptr;
+    int* d_dcnt = d_defer ? d_defer + 2 * G * maxj : nullptr;
+    if (d_dcnt) CCW_CUDA(cudaMemsetAsync(d_dcnt, 0, sizeof(int) * 2 * G, st));
+    std::vector<int> dpar(G, 0);  // per group: which list counter the next select / bulk pair uses
     int bulk_S = 1;
     if (bulk_launch) {
         // CTAs per deferred placement: enough to cover the SMs when a wave
@@ -773,6 +784,17 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         P.bulk_keys = ctx->bulk_keys.as<double>(G * maxj * BK_SMAX * kTcQ);
         P.bulk_idx = ctx->bulk_idx.as<int>(G * maxj * BK_SMAX * kTcQ);
     }
+    // tie-storm placements: the screen also keeps per-tile maxima over the
+    // non-uniform windows, so the bulk kernel reads only the tiles that can
+    // hold a non-uniform candidate (the uniform classes are class constants)
+    int32_t* d_tmaxnu = nullptr;
+    int8_t* d_jvar = nullptr;
+    const uint32_t* d_ubits = nullptr;
+    if (bulk_launch && warp_select && P.umap && P.ufirst && use_tc && ctx->tie_storm.count(bulk_key)) {
+        d_ubits = ti_uniform_bits(ti, Tc, OVc, st);
+        d_tmaxnu = ctx->tmaxnu.as<int32_t>(G * maxj * ntiles);
+        d_jvar = ctx->jvar.as<int8_t>(G * maxj);
+    }
     if (bulk_smem)
         CCW_CUDA(cudaFuncSetAttribute(select_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(bulk_smem)));
@@ -783,8 +805,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         GP[g].tm64 = d_tm + g * maxj * ti->nch * Tc * Tc;
         GP[g].wts8 = d_w8 ? d_w8 + g * maxj * kpad : nullptr;
         GP[g].tmax = d_tmax ? d_tmax + g * maxj * ntiles : nullptr;
+        GP[g].tmax_nu = d_tmaxnu ? d_tmaxnu + g * maxj * ntiles : nullptr;
+        GP[g].jvar = d_jvar ? d_jvar + g * maxj : nullptr;
         GP[g].cjob = d_cjob ? d_cjob + g * maxj : nullptr;
         GP[g].defer = d_defer ? d_defer + g * maxj : nullptr;
+        GP[g].defer_list = d_defer ? d_defer + G * maxj + g * maxj : nullptr;
         if (d_defer) {
             GP[g].bulk_sync = P.bulk_sync + 2 * g * maxj;
             GP[g].bulk_keys = P.bulk_keys + g * maxj * BK_SMAX * kTcQ;
@@ -1241,11 +1266,17 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                 if (use_tc) ccf_mma_flop += 2.0 * kpad * static_cast<double>(sp.n) * nj;
                             }
                             if (shard_fast) {
+                                if (QV.defer) {
+                                    QV.defer_cnt = d_dcnt + 2 * g + dpar[g];
+                                    QV.defer_cnt_next = d_dcnt + 2 * g + (1 - dpar[g]);
+                                    dpar[g] ^= 1;
+                                }
                                 launch_pdl(select_fast_kernel<false>, dim3(nj), dim3(FS_T), 0, gs, QV,
                                            static_cast<const Job*>(d_jobs), static_cast<int>(j0), nj);
                                 if (QV.defer) {
-                                    launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, QV,
-                                               static_cast<const Job*>(d_jobs), static_cast<int>(j0), nj, bulk_S);
+                                    launch_pdl(select_bulk_kernel, dim3(tc_num_sms()), dim3(BK_T),
+                                               bulk_smem, gs, QV, static_cast<const Job*>(d_jobs), static_cast<int>(j0),
+                                               nj, bulk_S);
                                     ++launches;
                                 }
                             } else {
@@ -1301,7 +1332,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         }
                         if (use_tc) {
                             launch_ccf_tc(tcplans[g][par], npos, sld, kpad, nj, Q.scores, Q.tmax, gs,
-                                          tl_next(w, g, 1), -1, Q.s16);
+                                          tl_next(w, g, 1), -1, Q.s16, Q.tmax_nu, d_ubits, P.ustride, Q.jvar);
                         } else {
                             launch_pdl(ccf_direct_kernel, dim3(ccf_grid_xy.x, ccf_grid_xy.y, nj),
                                        dim3(CCF_THREADS), ccf_smem, gs, Q,
@@ -1343,12 +1374,17 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         Q.hs_reset = d_hslots + (2 * g + (1 - hb_par[g])) * maxj;
                         hb_par[g] ^= 1;
                     }
+                    if (Q.defer && !first_wave) {
+                        Q.defer_cnt = d_dcnt + 2 * g + dpar[g];
+                        Q.defer_cnt_next = d_dcnt + 2 * g + (1 - dpar[g]);
+                        dpar[g] ^= 1;
+                    }
                     launch_pdl(Q.s16 ? select_fast_kernel<true> : select_fast_kernel<false>, dim3(nj), dim3(FS_T), 0, gs, Q, dj,
                                static_cast<int>(j0), nj);
                     if (Q.defer && !first_wave) {
                         Q.tl = tl_next(w, g, 5);
-                        launch_pdl(select_bulk_kernel, dim3(bulk_S, nj), dim3(BK_T), bulk_smem, gs, Q, dj,
-                                   static_cast<int>(j0), nj, bulk_S);
+                        launch_pdl(select_bulk_kernel, dim3(tc_num_sms()), dim3(BK_T), bulk_smem,
+                                   gs, Q, dj, static_cast<int>(j0), nj, bulk_S);
                         ++launches;
                     }
                 }
@@ -1592,6 +1628,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         fprintf(stderr, "small-group item (thread 0): loads+products %.0f chain+stores %.0f cycles over %llu\n",
                 stats[43] ? double(stats[41]) / stats[43] : 0.0, stats[43] ? double(stats[42]) / stats[43] : 0.0, stats[43]);
     if (debug_env("CCW_PHASES"))
+        fprintf(stderr, "bulk CTA phases: setup %llu loop %llu (max CTA %llu) last-CTA merge+paste %llu cycles\n",
+                stats[44], stats[45], stats[46], stats[47]);
+    if (debug_env("CCW_PHASES"))
         fprintf(stderr, "phase clocks: scan[M_K %llu list %llu S_K %llu cand %llu] fast[scan+stage %llu batch %llu choose+map %llu]"
                 " | bulk total %llu stage %llu compute %llu | tiles>=M_K %llu list %llu\n",
                 stats[8], stats[9], stats[10], stats[11], stats[12], stats[13], stats[4], stats[7], stats[14],
@@ -1600,6 +1639,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.list_overflows = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
     ctx->timing.shared_groups = static_cast<int64_t>(stats[32]);
+    if (bulk_launch && stats[1] > 0 && stats[3] * 50 > stats[1])  // > 2 % of the screened placements
+        ctx->tie_storm[bulk_key] = true;
+    else
+        ctx->tie_storm.erase(bulk_key);
     if (bulk_launch && stats[3] == 0)
         ctx->bulk_off[bulk_key] = true;
     else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back

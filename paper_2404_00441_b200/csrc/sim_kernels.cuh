@@ -250,8 +250,9 @@ constexpr int FS_RS = CCW_FS_RS;    // (window, run) partial sums per batch
 #endif
 constexpr int BK_T = CCW_BK_T;
 constexpr int BK_W = CCW_BK_W;
-constexpr int BK_V = 8;      // positions per thread per scan pass
-constexpr int BK_SMAX = 8;   // CTAs per placement (upper bound)
+constexpr int BK_V = 16;     // positions per thread per scan pass
+constexpr int BK_SMAX = 32;  // CTAs per placement (upper bound)
+constexpr int BK_STAGE_MIN = 512;  // windows of a block worth staging its apex tile for
 
 struct BulkLayout {
     size_t stage, tm, rows, cand, ukey, misc, total;
@@ -307,8 +308,10 @@ __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, in
 __global__ void or_prep_kernel(SimParams P, const Job* __restrict__ jobs, int job0);
 const int32_t* ti_nnmap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 const int8_t* ti_umap(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
+int umap_stride(int npos);
 const double* ti_pure_apex(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 const int* ti_uniform_first(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
+const uint32_t* ti_uniform_bits(ccw_ti* ti, int Tc, int OVc, cudaStream_t st);
 void fill_i32(int32_t* p, size_t n, int32_t v, cudaStream_t st);
 // ccf_direct.cu
 size_t ccf_smem_bytes(int Tc, int nscr);
