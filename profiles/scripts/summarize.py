@@ -54,8 +54,10 @@ def ncu_summary(tag, rep, kernel):
     det = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     out = io.StringIO()
-    out.write(f"# {tag} {kernel}: ncu --set full --clock-control none --import-source on -k regex:{kernel} "
-              "-s 200 -c 1 (python bench.py --steps 1 --warmup 1 --skip-cpu, config 1)\n")
+    src = {"s3d": "profiles/scripts/config3_run.py (WHICH=3)", "s4d": "profiles/scripts/config3_run.py (WHICH=4)",
+           "bulk": "profiles/scripts/config2_run.py"}.get(rep, "python bench.py --steps 1 --warmup 1 --skip-cpu, config 1")
+    out.write(f"# {tag} {kernel}: one launch, ncu --set full --clock-control none --import-source on ({src}); "
+              "see profiles/scripts/evidence_run.sh\n")
     r = list(csv.reader(io.StringIO(det)))
     h = r[0]
     si, mi, ui, vi = h.index("Section Name"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
@@ -76,3 +78,7 @@ if __name__ == "__main__":
     launch_shares(tag)
     ncu_summary(tag, "ccf", "ccf_tc_kernel")
     ncu_summary(tag, "sel", "select_fast_kernel")
+    for rep, kern in (("s3d", "screen3d_kernel (config 3)"), ("s4d", "screen3d_kernel (config 4)"),
+                      ("bulk", "select_bulk_kernel (config 2)")):
+        if os.path.exists(os.path.join(OUT, rep + ".ncu-rep")):
+            ncu_summary(tag, rep, kern)
