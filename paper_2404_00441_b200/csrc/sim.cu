@@ -997,7 +997,14 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     // (direct row bands measured slower, r1: one copy per realization band
     // lengthens the launch loop, and 8-bit rows quadruple the PCIe bytes)
     const bool direct_rows = debug_env("CCW_DIRECT_ROWS") != nullptr;
-    const size_t band_cap = 1024;  // CTAs per band of a finalize launch
+    // CTAs per band of a finalize launch: few while waves still run (the
+    // bands are not urgent and the waves need the SMs), many for the last
+    // checkpoint, which the call waits for (measured r2, config 1 e2e:
+    // 16 -> 3.18 ms vs 1024 -> 3.31 ms per call)
+#ifndef CCW_BAND_LAST
+#define CCW_BAND_LAST 1024
+#endif
+    const size_t band_cap_mid = 16, band_cap_last = CCW_BAND_LAST;
     bool h_pinned = false;
     if (stream_out) {
         cudaPointerAttributes pa{};
@@ -1411,6 +1418,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                         most = std::max(most, static_cast<size_t>(bands[q].w - bands[q].z) *
                                                   (bands[q].y == 0 ? cfg.sg_width : cfg.sg_height));
                     const size_t per_thread = packed && pack_bits < 8 ? static_cast<size_t>(pack_cpb) : fin_cells;
+                    const size_t band_cap = ck.w == max_key ? band_cap_last : band_cap_mid;
                     const int bxb = static_cast<int>(std::min<size_t>((most / per_thread + 255) / 256 + 1, band_cap));
                     auto band = [&](auto kern) {
                         launch_pdl(kern, dim3(bxb, static_cast<unsigned>(q1 - q0)), dim3(256), 0, ctx->copy_streams[g],
