@@ -32,6 +32,10 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <thread>
+#include <mutex>
+#include <exception>
+#include <algorithm>
 
 #include "ccwgpu.h"
 
@@ -652,6 +656,31 @@ struct SimResult {
 
 namespace gpu_detail {
 
+// fn(i) for i in [0, n) on up to 16 host threads (boundary glue: converting
+// the library's byte grids into the reference's int grids).
+template <class F>
+inline void parallel_for(int n, F&& fn) {
+    const int nt = std::max(1, std::min({n, 16, static_cast<int>(std::thread::hardware_concurrency())}));
+    if (nt <= 1) {
+        for (int i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::exception_ptr err;
+    std::mutex mu;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            try {
+                for (int i = t; i < n; i += nt) fn(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu);
+                if (!err) err = std::current_exception();
+            }
+        });
+    for (auto& x : th) x.join();
+    if (err) std::rethrow_exception(err);
+}
+
 // One device TI handle (pyramid built once on the GPU).
 struct TiHandle {
     ccw_ti* h = nullptr;
@@ -695,11 +724,15 @@ inline std::vector<SimResult> run(const CategoricalGrid& ti, const SimConfig& cf
                        diags.data(), traces ? ct.data() : nullptr));
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::vector<SimResult> res(n);
-    for (int r = 0; r < n; ++r) {
+    // the realizations as the reference's std::vector<int> grids: one host
+    // thread per realization range (100 M ints for config 1)
+    parallel_for(n, [&](int r) {
         res[r].realization = CategoricalGrid(
             cfg.sg_height, cfg.sg_width, ti.num_facies(),
             std::vector<int>(out.begin() + static_cast<std::ptrdiff_t>(sg * r),
                              out.begin() + static_cast<std::ptrdiff_t>(sg * (r + 1))));
+    });
+    for (int r = 0; r < n; ++r) {
         SimDiagnostics& d = res[r].diagnostics;
         d.seed = diags[r].seed;
         d.origin = static_cast<Corner>(diags[r].origin);
