@@ -48,6 +48,7 @@ enum {
     CCW_ERR_EMPTY = 5,      /* ccwsim::EmptyInputError  (errors.hpp:38) */
     CCW_ERR_IO = 6,         /* ccwsim::IoError          (errors.hpp:50) */
     CCW_ERR_GENERIC = 7,    /* ccwsim::Error            (errors.hpp:9)  */
+    CCW_ERR_DEGENERACY = 8, /* ccwsim::DegeneracyError  (errors.hpp:44) */
     CCW_ERR_CUDA = 100
 };
 
@@ -355,6 +356,16 @@ CCW_API ccw_status ccw_phist_copy(ccw_ctx* ctx, const ccw_phist* hist, uint8_t* 
 CCW_API void ccw_phist_destroy(ccw_phist* hist);
 /* js_divergence (metrics.hpp:258-284), base-2, clamped to [0, 1]. */
 CCW_API ccw_status ccw_js_divergence(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* q, double* out);
+/* anodi (metrics.hpp:318-384; the MDS step, which needs Eigen, excluded):
+ * ensembles A (n_a grids) and B (n_b) of h x w codes (on_device as above),
+ * the TI in host memory; per level p the grids are majority-downsampled by
+ * 2^(p-1), histogrammed with `window`, and every pairwise JS divergence runs
+ * on the device.  weights: levels values or NULL (uniform).  out: levels x 8
+ * doubles (between_a, between_b, within_a, within_b, d_between, d_within,
+ * ratio, weight). */
+CCW_API ccw_status ccw_anodi(ccw_ctx* ctx, const uint8_t* grids_a, int n_a, const uint8_t* grids_b, int n_b,
+                             int on_device, int h, int w, const uint8_t* ti, int ti_h, int ti_w, int num_facies,
+                             int levels, int window, const double* weights, double* out, double* aggregate);
 
 /* -------------------------------------------------- host-side helpers -- */
 /* SimConfig::validate / validate_against (simulator.hpp:46-84) incl.

@@ -185,3 +185,95 @@ void ccwm_downsample_majority(const uint8_t* g, int h, int w, int nf, int factor
         }
     free(cnt);
 }
+
+/* metrics.hpp:318-384 (ANODI without the MDS step).  out: levels x 8
+ * doubles (between_a, between_b, within_a, within_b, d_between, d_within,
+ * ratio, weight).  Returns 0, 5 (EmptyInput), 2 (Dimension), 3 (Structure)
+ * or 8 (Degeneracy). */
+typedef struct {
+    uint8_t* keys;
+    uint64_t* counts;
+    int n;
+    uint64_t total;
+} hist_t;
+
+static hist_t make_hist(const uint8_t* g, int h, int w, int nf, int factor, int win) {
+    const int oh = h / factor, ow = w / factor;
+    uint8_t* d = malloc((size_t)oh * ow);
+    if (factor == 1)
+        memcpy(d, g, (size_t)h * w);
+    else
+        ccwm_downsample_majority(g, h, w, nf, factor, d);
+    const long nwin = (long)(oh - win + 1) * (ow - win + 1);
+    hist_t r;
+    r.keys = malloc((size_t)(nwin > 0 ? nwin : 1) * win * win);
+    r.counts = malloc(sizeof(uint64_t) * (size_t)(nwin > 0 ? nwin : 1));
+    r.n = nwin > 0 ? ccwm_pattern_histogram(d, oh, ow, win, 1, r.keys, r.counts, &r.total) : 0;
+    if (nwin <= 0) r.total = 0;
+    free(d);
+    return r;
+}
+
+int ccwm_anodi(const uint8_t* ga, int na, const uint8_t* gb, int nb, int h, int w, const uint8_t* ti, int th,
+               int tw, int nf, int levels, int win, const double* weights, double* out, double* aggregate) {
+    if (na < 2 || nb < 2) return 5;
+    if (levels < 1) return 2;
+    const int kw = win * win;
+    *aggregate = 0.0;
+    for (int p = 1; p <= levels; ++p) {
+        const int factor = 1 << (p - 1);
+        hist_t* ha = malloc(sizeof(hist_t) * na);
+        hist_t* hb = malloc(sizeof(hist_t) * nb);
+        for (int i = 0; i < na; ++i) ha[i] = make_hist(ga + (size_t)i * h * w, h, w, nf, factor, win);
+        for (int i = 0; i < nb; ++i) hb[i] = make_hist(gb + (size_t)i * h * w, h, w, nf, factor, win);
+        hist_t ht = make_hist(ti, th, tw, nf, factor, win);
+        double s = 0.0;
+        size_t pairs = 0;
+        for (int i = 0; i < na; ++i)
+            for (int j = i + 1; j < na; ++j, ++pairs)
+                s += ccwm_js_divergence(ha[i].keys, ha[i].counts, ha[i].n, ha[i].total, ha[j].keys, ha[j].counts,
+                                        ha[j].n, ha[j].total, kw);
+        const double between_a = s / (double)pairs;
+        s = 0.0;
+        pairs = 0;
+        for (int i = 0; i < nb; ++i)
+            for (int j = i + 1; j < nb; ++j, ++pairs)
+                s += ccwm_js_divergence(hb[i].keys, hb[i].counts, hb[i].n, hb[i].total, hb[j].keys, hb[j].counts,
+                                        hb[j].n, hb[j].total, kw);
+        const double between_b = s / (double)pairs;
+        s = 0.0;
+        for (int i = 0; i < na; ++i)
+            s += ccwm_js_divergence(ha[i].keys, ha[i].counts, ha[i].n, ha[i].total, ht.keys, ht.counts, ht.n, ht.total,
+                                    kw);
+        const double within_a = s / (double)na;
+        s = 0.0;
+        for (int i = 0; i < nb; ++i)
+            s += ccwm_js_divergence(hb[i].keys, hb[i].counts, hb[i].n, hb[i].total, ht.keys, ht.counts, ht.n, ht.total,
+                                    kw);
+        const double within_b = s / (double)nb;
+        for (int i = 0; i < na; ++i) {
+            free(ha[i].keys);
+            free(ha[i].counts);
+        }
+        for (int i = 0; i < nb; ++i) {
+            free(hb[i].keys);
+            free(hb[i].counts);
+        }
+        free(ha);
+        free(hb);
+        free(ht.keys);
+        free(ht.counts);
+        double* o = out + (size_t)(p - 1) * 8;
+        o[0] = between_a;
+        o[1] = between_b;
+        o[2] = within_a;
+        o[3] = within_b;
+        o[7] = weights ? weights[p - 1] : 1.0 / levels;
+        if (within_a == 0.0 || within_b == 0.0 || between_b == 0.0) return 8;
+        o[4] = between_a / between_b;
+        o[5] = within_a / within_b;
+        o[6] = o[4] / o[5];
+        *aggregate += o[7] * o[6];
+    }
+    return 0;
+}

@@ -79,3 +79,20 @@ def downsample_majority(g, nf, factor):
     _lib().ccwm_downsample_majority(_p(g, C.c_uint8), g.shape[0], g.shape[1], int(nf), int(factor),
                                     _p(out, C.c_uint8))
     return out
+
+
+def anodi(ens_a, ens_b, ti, nf, levels, window, weights=None):
+    """metrics.hpp:318-384 (no MDS): (levels x 8 array, aggregate); raises
+    RuntimeError with the reference's error class name on failure."""
+    a = np.ascontiguousarray(ens_a, np.uint8)
+    b = np.ascontiguousarray(ens_b, np.uint8)
+    t = np.ascontiguousarray(ti, np.uint8)
+    out = np.zeros((max(levels, 1), 8), np.float64)
+    agg = C.c_double()
+    w = np.ascontiguousarray(weights, np.float64) if weights is not None else None
+    rc = _lib().ccwm_anodi(_p(a, C.c_uint8), a.shape[0], _p(b, C.c_uint8), b.shape[0], a.shape[1], a.shape[2],
+                           _p(t, C.c_uint8), t.shape[0], t.shape[1], int(nf), int(levels), int(window),
+                           _p(w, C.c_double) if w is not None else None, _p(out, C.c_double), C.byref(agg))
+    if rc:
+        raise RuntimeError({5: "EmptyInputError", 2: "DimensionError", 8: "DegeneracyError"}.get(rc, str(rc)))
+    return out[:levels], agg.value

@@ -131,6 +131,8 @@ SIGNATURES = {
     "ccw_phist_copy": (C.c_int, [P, P, U8P, U64P]),
     "ccw_phist_destroy": (None, [P]),
     "ccw_js_divergence": (C.c_int, [P, P, P, F64P]),
+    "ccw_anodi": (C.c_int, [P, U8P, C.c_int, U8P, C.c_int, C.c_int, C.c_int, C.c_int, U8P, C.c_int, C.c_int,
+                            C.c_int, C.c_int, C.c_int, F64P, F64P, F64P]),
     "ccw_validate_config": (C.c_int, [C.POINTER(SimConfigC), C.c_int, C.c_int, C.c_int, I32P,
                                       C.c_int, C.c_char_p, C.c_size_t]),
     "ccw_plan_raster_path": (C.c_int, [C.POINTER(SimConfigC), C.c_int, C.c_int, INTP, INTP, I32P,

@@ -68,12 +68,16 @@ class ParseError(Error):
         self.line = line
 
 
+class DegeneracyError(Error):
+    """errors.hpp:44-47 (ANODI on degenerate ensembles)."""
+
+
 class DeviceError(Error):
     """CUDA failure inside libccwgpu.so (status >= 100)."""
 
 
 _ERRORS = {1: BoundsError, 2: DimensionError, 3: StructureError, 4: ConfigError,
-           5: EmptyInputError, 6: IoError, 7: Error}
+           5: EmptyInputError, 6: IoError, 7: Error, 8: DegeneracyError}
 
 
 def _raise(code: int, msg: str):

@@ -917,6 +917,22 @@ ccw_status ccw_js_divergence(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* 
     });
 }
 
+ccw_status ccw_anodi(ccw_ctx* ctx, const uint8_t* ga, int na, const uint8_t* gb, int nb, int on_device, int h, int w,
+                     const uint8_t* ti, int th, int tw, int nf, int levels, int window, const double* weights,
+                     double* out, double* aggregate) {
+    if (!ctx || !out || !aggregate) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        if (na < 2 || nb < 2) throw Fail(CCW_ERR_EMPTY, "anodi requires at least 2 realizations per ensemble");
+        if (levels < 1) throw Fail(CCW_ERR_DIMENSION, "anodi requires levels >= 1");
+        if (!ga || !gb || !ti) throw Fail(CCW_ERR_GENERIC, "null grids");
+        if (h < 1 || w < 1 || th < 1 || tw < 1) throw Fail(CCW_ERR_DIMENSION, "grid dimensions must be positive");
+        if (window < 1) throw Fail(CCW_ERR_DIMENSION, "window must be >= 1");
+        if (nf < 1 || nf > 256) throw Fail(CCW_ERR_DIMENSION, "num_facies must be in [1, 256]");
+        ccwgpu::metric_anodi(ctx, ga, na, gb, nb, on_device != 0, h, w, ti, th, tw, nf, levels, window, weights, out,
+                             aggregate);
+    });
+}
+
 ccw_status ccw_validate_config(const ccw_sim_config* cfg, int ti_h, int ti_w, int nf,
                                const int32_t* hd, int n_hd, char* msg, size_t msg_len) {
     try {

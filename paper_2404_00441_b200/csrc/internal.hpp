@@ -389,6 +389,9 @@ ccw_phist* metric_pattern_histogram(ccw_ctx* ctx, const uint8_t* grid, bool on_d
 double metric_js(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* q);
 void metric_phist_copy(ccw_ctx* ctx, const ccw_phist* h, uint8_t* keys, uint64_t* counts);
 void metric_phist_destroy(ccw_phist* h);
+void metric_anodi(ccw_ctx* ctx, const uint8_t* ga, int na, const uint8_t* gb, int nb, bool on_device, int h, int w,
+                  const uint8_t* ti, int th, int tw, int nf, int levels, int win, const double* weights, double* out,
+                  double* aggregate);
 
 void op_dwt2_single(ccw_ctx* ctx, const double* in, int h, int w, double* a, double* dh,
                     double* dv, double* dd);

@@ -356,6 +356,51 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int n, double*
     }
 }
 
+// One histogram of a batch (ANODI): device arrays + counts.
+struct HistDesc {
+    const uint64_t* lo;
+    const uint64_t* hi;
+    const uint64_t* cnt;
+    int64_t n;
+    double total;
+};
+
+// JS divergence of every listed histogram pair, one CTA per pair: the terms of
+// js_terms_kernel, reduced per CTA in a fixed order.
+__global__ void js_pairs_kernel(const HistDesc* __restrict__ hd, const int2* __restrict__ pairs,
+                                double* __restrict__ out) {
+    const int2 pr = pairs[blockIdx.x];
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int side = 0; side < 2; ++side) {
+        const HistDesc a = hd[side ? pr.y : pr.x], b = hd[side ? pr.x : pr.y];
+        for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+            const uint64_t kh = a.hi[i], kl = a.lo[i];
+            int64_t lo = 0, hi = b.n;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                const bool less = b.hi[mid] < kh || (b.hi[mid] == kh && b.lo[mid] < kl);
+                if (less)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            const double pp = static_cast<double>(a.cnt[i]) / a.total;
+            const double qq = (lo < b.n && b.hi[lo] == kh && b.lo[lo] == kl) ? static_cast<double>(b.cnt[lo]) / b.total
+                                                                             : 0.0;
+            s += 0.5 * pp * log2(2.0 * pp / (pp + qq));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) t += red[k];
+        out[blockIdx.x] = fmin(fmax(t, 0.0), 1.0);  // metrics.hpp:283
+    }
+}
+
 int grid_for(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)); }
 
 }  // namespace
@@ -516,6 +561,108 @@ double metric_js(ccw_ctx* ctx, const ccw_phist* p, const ccw_phist* q) {
     CCW_CUDA(cudaMemcpyAsync(&s, part.p + bp + bq, sizeof(double), cudaMemcpyDeviceToHost, st));
     CCW_CUDA(cudaStreamSynchronize(st));
     return std::clamp(s, 0.0, 1.0);  // metrics.hpp:283
+}
+
+// anodi (metrics.hpp:318-384, without MDS).  out: levels x 8 doubles.
+void metric_anodi(ccw_ctx* ctx, const uint8_t* ga, int na, const uint8_t* gb, int nb, bool on_device, int h, int w,
+                  const uint8_t* ti, int th, int tw, int nf, int levels, int win, const double* weights, double* out,
+                  double* aggregate) {
+    cudaStream_t st = ctx->stream;
+    const size_t cells = static_cast<size_t>(h) * w;
+    GridInput ia(ga, on_device, na * cells, st), ib(gb, on_device, nb * cells, st);
+    GridInput it(ti, false, static_cast<size_t>(th) * tw, st);
+    *aggregate = 0.0;
+    for (int p = 1; p <= levels; ++p) {
+        const int factor = 1 << (p - 1);
+        const int oh = h / factor, ow = w / factor, toh = th / factor, tow = tw / factor;
+        if (oh < win || ow < win || toh < win || tow < win)
+            throw Fail(CCW_ERR_DIMENSION, "window does not fit the level-" + std::to_string(p) + " grids");
+        Scratch<uint8_t> da(factor > 1 ? static_cast<size_t>(na) * oh * ow : 0, st),
+            db(factor > 1 ? static_cast<size_t>(nb) * oh * ow : 0, st), dt(static_cast<size_t>(toh) * tow, st);
+        // downsample_majority of every grid (the level-1 grids are used as they are)
+        auto down = [&](const uint8_t* src, int hh, int ww, uint8_t* dst) {
+            metric_downsample(ctx, src, true, hh, ww, nf, factor, dst, true);
+        };
+        std::vector<const uint8_t*> pa(na), pb(nb);
+        for (int r = 0; r < na; ++r) {
+            if (factor > 1) down(ia.d + r * cells, h, w, da.p + static_cast<size_t>(r) * oh * ow);
+            pa[r] = factor > 1 ? da.p + static_cast<size_t>(r) * oh * ow : ia.d + r * cells;
+        }
+        for (int r = 0; r < nb; ++r) {
+            if (factor > 1) down(ib.d + r * cells, h, w, db.p + static_cast<size_t>(r) * oh * ow);
+            pb[r] = factor > 1 ? db.p + static_cast<size_t>(r) * oh * ow : ib.d + r * cells;
+        }
+        if (factor > 1)
+            down(it.d, th, tw, dt.p);
+        else
+            CCW_CUDA(cudaMemcpyAsync(dt.p, it.d, static_cast<size_t>(th) * tw, cudaMemcpyDeviceToDevice, st));
+        // pattern histograms: [A..., B..., TI]
+        std::vector<ccw_phist*> hs;
+        struct Free {
+            std::vector<ccw_phist*>& v;
+            ~Free() {
+                for (ccw_phist* x : v) metric_phist_destroy(x);
+            }
+        } free_hs{hs};
+        for (int r = 0; r < na; ++r) hs.push_back(metric_pattern_histogram(ctx, pa[r], true, oh, ow, nf, win, 1));
+        for (int r = 0; r < nb; ++r) hs.push_back(metric_pattern_histogram(ctx, pb[r], true, oh, ow, nf, win, 1));
+        hs.push_back(metric_pattern_histogram(ctx, dt.p, true, toh, tow, nf, win, 1));
+        std::vector<HistDesc> desc;
+        for (ccw_phist* x : hs) desc.push_back({x->lo, x->hi, x->cnt, x->n, static_cast<double>(x->total)});
+        // pairs in the reference's order: A pairs, B pairs, A vs TI, B vs TI
+        std::vector<int2> pairs;
+        for (int i = 0; i < na; ++i)
+            for (int j = i + 1; j < na; ++j) pairs.push_back(make_int2(i, j));
+        for (int i = 0; i < nb; ++i)
+            for (int j = i + 1; j < nb; ++j) pairs.push_back(make_int2(na + i, na + j));
+        const int tix = na + nb;
+        for (int i = 0; i < na; ++i) pairs.push_back(make_int2(i, tix));
+        for (int i = 0; i < nb; ++i) pairs.push_back(make_int2(na + i, tix));
+        Scratch<HistDesc> ddesc(desc.size(), st);
+        Scratch<int2> dpairs(pairs.size(), st);
+        Scratch<double> djs(pairs.size(), st);
+        CCW_CUDA(cudaMemcpyAsync(ddesc.p, desc.data(), sizeof(HistDesc) * desc.size(), cudaMemcpyHostToDevice, st));
+        CCW_CUDA(cudaMemcpyAsync(dpairs.p, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice, st));
+        js_pairs_kernel<<<static_cast<unsigned>(pairs.size()), 256, 0, st>>>(ddesc.p, dpairs.p, djs.p);
+        CCW_CUDA(cudaGetLastError());
+        std::vector<double> js(pairs.size());
+        CCW_CUDA(cudaMemcpyAsync(js.data(), djs.p, sizeof(double) * js.size(), cudaMemcpyDeviceToHost, st));
+        CCW_CUDA(cudaStreamSynchronize(st));
+        // means in the reference's summation order (metrics.hpp:340-356)
+        size_t k = 0;
+        double s = 0.0;
+        const size_t npa = static_cast<size_t>(na) * (na - 1) / 2, npb = static_cast<size_t>(nb) * (nb - 1) / 2;
+        for (size_t q = 0; q < npa; ++q) s += js[k++];
+        const double between_a = s / static_cast<double>(npa);
+        s = 0.0;
+        for (size_t q = 0; q < npb; ++q) s += js[k++];
+        const double between_b = s / static_cast<double>(npb);
+        s = 0.0;
+        for (int q = 0; q < na; ++q) s += js[k++];
+        const double within_a = s / na;
+        s = 0.0;
+        for (int q = 0; q < nb; ++q) s += js[k++];
+        const double within_b = s / nb;
+        double* o = out + static_cast<size_t>(p - 1) * 8;
+        o[0] = between_a;
+        o[1] = between_b;
+        o[2] = within_a;
+        o[3] = within_b;
+        o[7] = weights ? weights[p - 1] : 1.0 / levels;
+        if (within_a == 0.0 || within_b == 0.0)
+            throw Fail(CCW_ERR_DEGENERACY, "realizations identical to TI at level " + std::to_string(p));
+        if (between_b == 0.0)
+            throw Fail(CCW_ERR_DEGENERACY,
+                       "ensemble B has zero between-realization variability at level " + std::to_string(p));
+        o[4] = between_a / between_b;
+        o[5] = within_a / within_b;
+        o[6] = o[4] / o[5];
+        *aggregate += o[7] * o[6];
+    }
+    ia.release(st);
+    ib.release(st);
+    it.release(st);
+    CCW_CUDA(cudaStreamSynchronize(st));
 }
 
 void metric_phist_copy(ccw_ctx* ctx, const ccw_phist* h, uint8_t* keys, uint64_t* counts) {

@@ -176,3 +176,49 @@ def js_divergence(p: PatternHistogram, q: PatternHistogram) -> float:
     v = C.c_double()
     p.device.check(p.device._lib.ccw_js_divergence(p.device.handle, p.handle, q.handle, C.byref(v)))
     return v.value
+
+
+@dataclass
+class AnodiLevel:
+    between_a: float
+    between_b: float
+    within_a: float
+    within_b: float
+    d_between: float
+    d_within: float
+    ratio: float
+    weight: float
+
+
+@dataclass
+class AnodiResult:
+    levels: List[AnodiLevel]
+    aggregate: float
+
+
+def anodi(ensemble_a, ensemble_b, ti, levels: int, window: int, weights: Optional[Sequence[float]] = None,
+          num_facies: Optional[int] = None, device: Optional[Device] = None) -> AnodiResult:
+    """metrics.hpp:318-384 (the MDS step needs Eigen and is not included):
+    ensembles as lists of grids, (n, h, w) arrays or CUDA tensors."""
+    dev = device or default_device()
+    pa, ona, na, h, w, ka = _grids(ensemble_a)
+    pb, onb, nb, hb, wb, kb = _grids(ensemble_b)
+    if ona != onb:
+        raise ValueError("both ensembles must be on the device or both on the host")
+    if (hb, wb) != (h, w):
+        from .ccwsim import StructureError
+        raise StructureError("ensembles differ in grid size")
+    t = np.ascontiguousarray(ti.cells if isinstance(ti, CategoricalGrid) else ti, np.uint8)
+    nf = num_facies if num_facies is not None else (ti.num_facies if isinstance(ti, CategoricalGrid)
+                                                    else int(t.max()) + 1)
+    out = np.zeros((max(levels, 1), 8), np.float64)
+    agg = C.c_double()
+    wts = np.ascontiguousarray(weights, np.float64) if weights is not None else None
+    if wts is not None and len(wts) != levels:
+        from .ccwsim import StructureError
+        raise StructureError("weight count does not match level count")
+    dev.check(dev._lib.ccw_anodi(dev.handle, pa, na, pb, nb, ona, h, w, t.ctypes.data_as(_abi.U8P), t.shape[0],
+                                 t.shape[1], int(nf), int(levels), int(window),
+                                 wts.ctypes.data_as(_abi.F64P) if wts is not None else None,
+                                 out.ctypes.data_as(_abi.F64P), C.byref(agg)))
+    return AnodiResult([AnodiLevel(*[float(v) for v in row]) for row in out[:levels]], agg.value)

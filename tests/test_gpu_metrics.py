@@ -118,3 +118,24 @@ def test_downsample_exact():
         g = cs.CategoricalGrid(grids.shape[1], grids.shape[2], 3, grids[0])
         d = G.downsample_majority(g, factor)
         assert np.array_equal(d.cells, M.downsample_majority(grids[0], 3, factor))
+
+
+def test_anodi_matches_restatement():
+    grids, ti_a = ensemble(n=8)
+    ga, gb = grids[:4], grids[4:]
+    for levels, win, wts in ((3, 3, None), (2, 4, [0.75, 0.25])):
+        res = G.anodi(ga, gb, ti_a, levels, win, wts, num_facies=3)
+        exp, agg = M.anodi(ga, gb, ti_a, 3, levels, win, wts)
+        got = np.array([[l.between_a, l.between_b, l.within_a, l.within_b, l.d_between, l.d_within, l.ratio,
+                         l.weight] for l in res.levels])
+        assert np.allclose(got, exp, rtol=0, atol=1e-9), (got, exp)
+        assert abs(res.aggregate - agg) < 1e-9
+    # identical ensembles: r = 1 (test_metrics.cpp:449-459); on-device input
+    import torch
+    d = torch.from_numpy(ga).cuda()
+    res = G.anodi(d, d, ti_a, 2, 3, num_facies=3)
+    assert abs(res.aggregate - 1.0) < 1e-9
+    with pytest.raises(cs.DegeneracyError):
+        G.anodi([ti_a[:96, :130]] * 2, [ti_a[:96, :130]] * 2, ti_a[:96, :130], 2, 3, num_facies=3)
+    with pytest.raises(cs.EmptyInputError):
+        G.anodi(ga[:1], gb, ti_a, 2, 3, num_facies=3)

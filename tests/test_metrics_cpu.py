@@ -112,3 +112,56 @@ def test_pattern_histogram_and_js():
     assert M.js_divergence(p, p, 1) == 0.0
     disj = M.js_divergence(([(b"a", 2), (b"b", 2)], 4), ([(b"c", 1), (b"d", 3)], 4), 1)
     assert abs(disj - 1.0) < 1e-12
+
+
+def _anodi_case(seed=49):
+    rng = np.random.default_rng(seed)
+    ti = np.zeros((32, 32), np.uint8)
+    ti[8:12, :] = 1
+    ti[20:23, 3:29] = 1
+    a = rng.integers(0, 2, (3, 32, 32)).astype(np.uint8)
+    b = rng.integers(0, 2, (3, 32, 32)).astype(np.uint8)
+    return a, b, ti
+
+
+def test_anodi_known_answers():
+    # test_metrics.cpp:440-523, acceptance.cpp:610-630
+    a, b, ti = _anodi_case()
+    lv, agg = M.anodi(a, a, ti, 2, 3, 4)
+    assert lv.shape == (3, 8)
+    for row in lv:
+        assert abs(row[4] - 1) < 1e-12 and abs(row[5] - 1) < 1e-12 and abs(row[6] - 1) < 1e-12
+        assert abs(row[7] - 1 / 3) < 1e-12
+    assert abs(agg - 1) < 1e-9
+    lv, agg = M.anodi(a, b, ti, 2, 2, 4)
+    assert abs(agg - float((lv[:, 7] * lv[:, 6]).sum())) < 1e-12
+    lv, agg = M.anodi(a, b, ti, 2, 2, 4, [0.75, 0.25])
+    assert lv[0, 7] == 0.75 and lv[1, 7] == 0.25
+    assert abs(agg - (0.75 * lv[0, 6] + 0.25 * lv[1, 6])) < 1e-12
+    with pytest.raises(RuntimeError, match="DegeneracyError"):
+        M.anodi(np.stack([ti, ti]), np.stack([ti, ti]), ti, 2, 2, 4)
+    with pytest.raises(RuntimeError, match="EmptyInputError"):
+        M.anodi(a[:1], b, ti, 2, 2, 4)
+
+
+def test_anodi_matches_from_scratch_evaluation():
+    # test_metrics.cpp:474-513: every level statistic from downsample + histogram + JS
+    a, b, ti = _anodi_case(7)
+    win = 4
+    lv, _ = M.anodi(a, b, ti, 2, 2, win)
+    for level in (1, 2):
+        f = 1 << (level - 1)
+        hist = lambda g: M.pattern_histogram(M.downsample_majority(g, 2, f) if f > 1 else g, win)
+        th = hist(ti)
+
+        def pairwise(e):
+            v = [M.js_divergence(hist(e[i]), hist(e[j]), win) for i in range(len(e)) for j in range(i + 1, len(e))]
+            return sum(v) / len(v)
+
+        def vs_ti(e):
+            return sum(M.js_divergence(hist(g), th, win) for g in e) / len(e)
+
+        row = lv[level - 1]
+        assert abs(row[0] - pairwise(a)) < 1e-9 and abs(row[1] - pairwise(b)) < 1e-9
+        assert abs(row[2] - vs_ti(a)) < 1e-9 and abs(row[3] - vs_ti(b)) < 1e-9
+        assert abs(row[6] - (row[0] / row[1]) / (row[2] / row[3])) < 1e-9
