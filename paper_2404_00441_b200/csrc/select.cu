@@ -726,70 +726,73 @@ struct ScanWarp {
 
 constexpr int kTM = 16;  // tile maxima per lane in registers (512 tiles per placement)
 
-// K-th largest (with multiplicity) of the warp's register-held values.
-__device__ __forceinline__ int regs_kth(const int (&tv)[kTM], int K) {
+// K-th largest (with multiplicity) of the warp's register-held values (NT
+// per lane; rounds of warp max and count, each reduced as a tree so a round's
+// dependent chain is log2(NT) deep).
+template <int NT>
+__device__ __forceinline__ int regs_kth(const int (&tv)[NT], int K) {
     int cur = INT_MAX, acc = 0, mk = INT_MIN;
     for (int round = 0; round < K; ++round) {
-        int m = INT_MIN;
+        int m[NT], c[NT];
 #pragma unroll
-        for (int i = 0; i < kTM; ++i)
-            if (tv[i] < cur) m = max(m, tv[i]);
-        m = __reduce_max_sync(0xffffffffu, m);
-        int c = 0;
+        for (int i = 0; i < NT; ++i) m[i] = tv[i] < cur ? tv[i] : INT_MIN;
 #pragma unroll
-        for (int i = 0; i < kTM; ++i) c += tv[i] == m;
-        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
-        mk = m;
-        if (acc >= K || m == INT_MIN) break;
-        cur = m;
+        for (int w = NT / 2; w > 0; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) m[i] = max(m[i], m[i + w]);
+        const int mx = __reduce_max_sync(0xffffffffu, m[0]);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) c[i] = tv[i] == mx;
+#pragma unroll
+        for (int w = NT / 2; w > 0; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) c[i] += c[i + w];
+        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c[0])));
+        mk = mx;
+        if (acc >= K || mx == INT_MIN) break;
+        cur = mx;
     }
     return mk;
 }
 
 // Steps 3-4 of the scan (one warp): the exact K-th score S_K of the list
-// W.lv[0, nl) and the candidate positions (>= S_K) into out[].
-__device__ __forceinline__ int scan_finish(const SimParams& P, const ScanWarp& W, int nl, int mk, int* out,
-                                           long long* sclk, int* out_s) {
+// W.lv[0, nl) and the candidate positions (>= S_K) into out[].  NV list
+// values per lane (NV * 32 >= nl).
+template <int NV>
+__device__ __forceinline__ int scan_finish_nv(const SimParams& P, const ScanWarp& W, int nl, int mk, int* out,
+                                              long long* sclk, int* out_s, int K) {
     const int lane = threadIdx.x & 31;
-    const int K = P.K;
     // 3. exact S_K from the list (rounds of warp max with multiplicity)
-    int lvr[SC_LC / 32];
+    int lvr[NV];
 #pragma unroll
-    for (int j2 = 0; j2 < SC_LC / 32; ++j2) {
+    for (int j2 = 0; j2 < NV; ++j2) {
         const int e = j2 * 32 + lane;
         lvr[j2] = e < nl ? W.lv[e] : INT_MIN;
     }
-    int thr = mk, cur = INT_MAX, acc = 0;
-    for (int round = 0; round < K; ++round) {
-        int m = INT_MIN;
-#pragma unroll
-        for (int j2 = 0; j2 < SC_LC / 32; ++j2)
-            if (lvr[j2] < cur) m = max(m, lvr[j2]);
-        m = __reduce_max_sync(0xffffffffu, m);
-        int c = 0;
-#pragma unroll
-        for (int j2 = 0; j2 < SC_LC / 32; ++j2) c += lvr[j2] == m;
-        acc += static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
-        thr = m;
-        if (acc >= K || m == INT_MIN) break;
-        cur = m;
-    }
+    const int thr = nl > 0 ? regs_kth<NV>(lvr, K) : mk;
     sclk[3] = clock64();
     // 4. the candidates: every listed window >= S_K
     int* cd = out;
     int cnt = 0;
-    for (int e0 = 0; e0 < nl; e0 += 32) {
-        const int e = e0 + lane;
-        const bool q = e < nl && W.lv[e] >= thr;
+#pragma unroll
+    for (int j2 = 0; j2 < NV; ++j2) {
+        const int e = j2 * 32 + lane;
+        const bool q = e < nl && lvr[j2] >= thr;
         const unsigned bal = __ballot_sync(0xffffffffu, q);
         if (q) {
             const int o = cnt + __popc(bal & ((1u << lane) - 1));
             cd[o] = W.lp[e];
-            if (out_s) out_s[o] = W.lv[e];
+            if (out_s) out_s[o] = lvr[j2];
         }
         cnt += __popc(bal);
     }
     return cnt;
+}
+
+__device__ __forceinline__ int scan_finish(const SimParams& P, const ScanWarp& W, int nl, int mk, int* out,
+                                           long long* sclk, int* out_s, int K) {
+    return nl <= 32 ? scan_finish_nv<1>(P, W, nl, mk, out, sclk, out_s, K)
+                    : scan_finish_nv<SC_LC / 32>(P, W, nl, mk, out, sclk, out_s, K);
 }
 
 // Warp-level scan of one placement (every lane of the warp calls it): the
@@ -832,7 +835,7 @@ __device__ CCW_COLD int scan_job(const SimParams& P, int slot, ScanWarp& W, int*
         }
         mk = warp_kth(top, K, lane);
     } else {
-        mk = regs_kth(tv, K);
+        mk = regs_kth<kTM>(tv, K);
     }
     sclk[1] = clock64();
     // 2. every window scoring >= M_K, from the tiles whose maximum reaches it,
@@ -928,7 +931,7 @@ __device__ CCW_COLD int scan_job(const SimParams& P, int slot, ScanWarp& W, int*
         if (lane == 0 && P.stats) atomicAdd(&P.stats[2], 1ull);
         return -1;
     }
-    return scan_finish(P, W, nl, mk, out, sclk, out_s);
+    return scan_finish(P, W, nl, mk, out, sclk, out_s, K);
 }
 
 // Fused OR prep (select epilogue): after this placement's source-block map
@@ -976,10 +979,14 @@ struct FastSmem {
     int misc[8];
     int tqa[32 * kTM];      // cooperative scan: the tiles whose maximum reaches M_K
     int nq, lcnt, lover;    // their count, the list length, list overflow
+    int lean;               // lean_scan: 0 not taken, 1 list done, 2 group settled too
     // uniform-window reduction of a large equal-score group (uniform_reduce)
     int utmp[SC_LC];
     signed char ucl[SC_LC], ucl2[SC_LC];
     int urep[16], urs[16], ucnt[2];
+#ifdef CCW_DBG_TAIL
+    long long dbg[8];
+#endif
 };
 
 // Large equal-score groups are often windows made entirely of pure blocks of
@@ -1027,19 +1034,32 @@ __device__ CCW_COLD void uniform_fill(FastSmem& S, int gr, int g) {
 
 // Cooperative scan (ntiles <= 32 * kTM), step 1 on warp 0: M_K (as scan_job)
 // and the queue of tiles whose maximum reaches it, in tile order.
-__device__ __forceinline__ void coop_head(const SimParams& P, int slot, FastSmem& S) {
+template <int NT>
+__device__ __forceinline__ void coop_head_nt(const SimParams& P, int slot, FastSmem& S, int K) {
     const int lane = threadIdx.x & 31;
     const int32_t* tmx = P.tmax + static_cast<size_t>(slot) * P.ntiles;
-    int tv[kTM];
+    int tv[NT];
 #pragma unroll
-    for (int i = 0; i < kTM; ++i) {
+    for (int i = 0; i < NT; ++i) {
         const int e = i * 32 + lane;
         tv[i] = e < P.ntiles ? tmx[e] : INT_MIN;
     }
-    const int mk = regs_kth(tv, P.K);
+#ifdef CCW_DBG_TAIL
+    {
+        int sdbg = 0;
+#pragma unroll
+        for (int i = 0; i < NT; ++i) sdbg ^= tv[i];
+        const long long c = clock64();
+        if (lane == 0) S.dbg[0] = c + (sdbg == 0x12345 ? 1 : 0);
+    }
+#endif
+    const int mk = regs_kth<NT>(tv, K);
+#ifdef CCW_DBG_TAIL
+    if (lane == 0) S.dbg[1] = clock64();
+#endif
     int nq = 0;
 #pragma unroll
-    for (int i = 0; i < kTM; ++i) {
+    for (int i = 0; i < NT; ++i) {
         const bool q = tv[i] != INT_MIN && tv[i] >= mk;
         const unsigned bal = __ballot_sync(0xffffffffu, q);
         if (q) S.tqa[nq + __popc(bal & ((1u << lane) - 1))] = i * 32 + lane;
@@ -1055,6 +1075,13 @@ __device__ __forceinline__ void coop_head(const SimParams& P, int slot, FastSmem
     }
 }
 
+__device__ __forceinline__ void coop_head(const SimParams& P, int slot, FastSmem& S, int K) {
+    if (P.ntiles <= 32 * 4)
+        coop_head_nt<4>(P, slot, S, K);
+    else
+        coop_head_nt<kTM>(P, slot, S, K);
+}
+
 // Step 2 on every warp: the windows >= M_K of the queued tiles (SC_TB tiles per
 // round trip per warp) appended to the shared (score, position) list.  The
 // list order is irrelevant: every later ranking is a total order on (S, fp64
@@ -1068,6 +1095,9 @@ __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem
         int tl[SC_TB], v[SC_TB][4];
 #pragma unroll
         for (int u = 0; u < SC_TB; ++u) tl[u] = q0 + u < nq ? S.tqa[q0 + u] : -1;
+#ifdef CCW_DBG_TAIL
+        if (q0 == 0 && lane == 0) S.dbg[5] = clock64() + (tl[0] == 0x7fffffff);
+#endif
 #pragma unroll
         for (int u = 0; u < SC_TB; ++u) {
             const int p0 = tl[u] * kTcTile + lane * 4;
@@ -1081,6 +1111,15 @@ __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem
                 v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
             }
         }
+#ifdef CCW_DBG_TAIL
+        if (q0 == 0) {
+            int sdbg = 0;
+#pragma unroll
+            for (int u = 0; u < SC_TB; ++u) sdbg ^= v[u][0];
+            const long long cl = clock64();
+            if (lane == 0) S.dbg[2] = cl + (sdbg == 0x12345 ? 1 : 0);
+        }
+#endif
         int c = 0;
 #pragma unroll
         for (int u = 0; u < SC_TB; ++u)
@@ -1097,6 +1136,9 @@ __device__ __forceinline__ void coop_list(const SimParams& P, int slot, FastSmem
         int base = 0;
         if (lane == 0) base = atomicAdd(&S.lcnt, tot);
         base = __shfl_sync(0xffffffffu, base, 0);
+#ifdef CCW_DBG_TAIL
+        if (q0 == 0 && lane == 0) S.dbg[6] = clock64() + (base == 0x7fffffff);
+#endif
         if (base + tot > SC_LC) {
             if (lane == 0) S.lover = 1;
             continue;
@@ -1177,7 +1219,7 @@ __device__ __forceinline__ void rescore_items(const SimParams& P, FastSmem& S, T
             }
         }
 #ifdef CCW_DBG_TAIL
-        if (threadIdx.x == 0 && P.stats && ng < 8) {
+        if (threadIdx.x == 0 && P.stats && ng < 8 && cidx != S.utmp) {
             const long long z2 = clock64();
             atomicAdd(&P.stats[41], static_cast<unsigned long long>(z1 - z0));
             atomicAdd(&P.stats[42], static_cast<unsigned long long>(z2 - z1));
@@ -1206,6 +1248,9 @@ __device__ CCW_COLD void rescore_keys(const SimParams& P, FastSmem& S, const dou
         rescore_items(P, S, tm_smem ? static_cast<const double*>(S.tm) : tmg, nr, ngrp, cidx, e0, ng, R);
         __syncthreads();
 #ifdef CCW_DBG_TAIL
+        if (tid == 0 && e0 == 0) S.dbg[5] = clock64();
+#endif
+#ifdef CCW_DBG_TAIL
         if (tid == 0 && P.stats && cnt < 8) {
             atomicAdd(&P.stats[40], static_cast<unsigned long long>(clock64() - r0));
             r0 = clock64();
@@ -1227,6 +1272,9 @@ __device__ CCW_COLD void rescore_keys(const SimParams& P, FastSmem& S, const dou
             keys[e0 + e] = acc;
         }
         __syncthreads();
+#ifdef CCW_DBG_TAIL
+        if (tid == 0 && e0 == 0) S.dbg[6] = clock64();
+#endif
     }
 }
 
@@ -1430,13 +1478,192 @@ __device__ CCW_COLD bool hb_rescore(const SimParams& P, FastSmem& S, int slot, i
 #ifndef CCW_FS_MINB
 #define CCW_FS_MINB 4
 #endif
+// Lean scan of an unconditional pick (warp 0; every lane calls it), after
+// coop_head queued the nq tiles whose maximum reaches mk: when they fit one
+// round trip (nq <= SC_TB) the warp reads their rows itself -- no other warp,
+// no shared-memory atomics, no block barrier -- and, when the list of windows
+// >= mk fits one per lane, settles the equal-score group holding rank `pick`
+// in the same rounds that find S_{pick+1} (pick_group's outputs, S.lean =
+// 2).  Returns false (nothing written) when the queue is too long for it.
+template <bool S16>
+__device__ __forceinline__ bool lean_scan(const SimParams& P, int slot, FastSmem& S, int pick, int K,
+                                          long long* sclk) {
+    const int lane = threadIdx.x & 31;
+    const int nq = S.nq, mk = S.misc[1];
+    if (nq > SC_TB || S.lover) return false;
+    int tl[SC_TB], v[SC_TB][4];
+#pragma unroll
+    for (int u = 0; u < SC_TB; ++u) tl[u] = u < nq ? S.tqa[u] : -1;
+#pragma unroll
+    for (int u = 0; u < SC_TB; ++u) {
+        const int p0 = tl[u] * kTcTile + lane * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[u][i] = INT_MIN;
+        if (tl[u] >= 0 && p0 < P.npos) {  // rows are padded to a multiple of 4
+            const int4 a4 = load_score4<S16>(P, slot, p0);
+            v[u][0] = a4.x;
+            v[u][1] = p0 + 1 < P.npos ? a4.y : INT_MIN;
+            v[u][2] = p0 + 2 < P.npos ? a4.z : INT_MIN;
+            v[u][3] = p0 + 3 < P.npos ? a4.w : INT_MIN;
+        }
+    }
+#ifdef CCW_DBG_TAIL
+    {
+        int sdbg = 0;
+#pragma unroll
+        for (int u = 0; u < SC_TB; ++u) sdbg ^= v[u][0];
+        const long long cl = clock64();
+        if (lane == 0) S.dbg[2] = cl + (sdbg == 0x12345 ? 1 : 0);
+    }
+#endif
+    // the (score, position) list of windows >= mk, in lane order
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < SC_TB; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c += v[u][i] != INT_MIN && v[u][i] >= mk;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int nl = __shfl_sync(0xffffffffu, incl, 31);
+    if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+    if (nl > SC_LC) {  // (the general path's overflow: deferred with threshold mk)
+        if (lane == 0) {
+            S.misc[0] = -1;
+            S.lean = 1;
+            if (P.stats) atomicAdd(&P.stats[2], 1ull);
+        }
+        return true;
+    }
+    int o = incl - c;
+#pragma unroll
+    for (int u = 0; u < SC_TB; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (v[u][i] != INT_MIN && v[u][i] >= mk) {
+                S.sw.lv[o] = v[u][i];
+                S.sw.lp[o] = tl[u] * kTcTile + lane * 4 + i;
+                ++o;
+            }
+    __syncwarp();
+    sclk[2] = clock64();
+    if (nl > 32) {  // the general finish over the list
+        const int n = scan_finish(P, S.sw, nl, mk, S.cidx, sclk, S.cs, K);
+        if (lane == 0) {
+            S.misc[0] = n;
+            S.lean = 1;
+        }
+        return true;
+    }
+    // one window per lane: rounds of (max, count) down to the group holding
+    // rank `pick`; its score is S_{pick+1}, the candidates are the windows >= it
+    const int lv = lane < nl ? S.sw.lv[lane] : INT_MIN;
+    const int lp = lane < nl ? S.sw.lp[lane] : -1;
+    int cur = INT_MAX, acc = 0, sp = INT_MIN, above = 0;
+    for (int round = 0; round <= pick && round < nl; ++round) {
+        const int m = __reduce_max_sync(0xffffffffu, lv < cur ? lv : INT_MIN);
+        const int cn = __popc(__ballot_sync(0xffffffffu, lane < nl && lv == m));
+        sp = m;
+        above = acc;
+        if (acc + cn > pick) break;
+        acc += cn;
+        cur = m;
+    }
+    sclk[3] = clock64();
+    const bool cand = lane < nl && lv >= sp;
+    const unsigned cb = __ballot_sync(0xffffffffu, cand);
+    if (cand) {
+        const int e = __popc(cb & ((1u << lane) - 1));
+        S.cidx[e] = lp;
+        S.cs[e] = lv;
+    }
+    const bool q = lane < nl && lv == sp;
+    const unsigned gb = __ballot_sync(0xffffffffu, q);
+    if (q) S.tie[__popc(gb & ((1u << lane) - 1))] = lp;
+    if (lane == 0) {
+        S.misc[0] = __popc(cb);
+        S.misc[6] = __popc(gb);
+        S.misc[5] = pick - above;  // rank inside the group
+        S.lean = 2;
+    }
+    return true;
+}
+
+// Unconditional pick (one warp): the equal-score group of the candidates
+// S.cs/S.cidx[0, n) that holds rank `pick` of (S desc, ...) into S.tie, its
+// size into S.misc[6] and the rank inside it into S.misc[5].  KV candidates
+// per lane (KV * 32 >= n).
+template <int KV>
+__device__ __forceinline__ void pick_group(FastSmem& S, int n, int pick, int lane) {
+    int v[KV];
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+        const int e = j * 32 + lane;
+        v[j] = e < n ? S.cs[e] : INT_MIN;
+    }
+    int cur = INT_MAX, acc = 0, sp = INT_MIN, above = 0;
+    for (int round = 0; round <= pick && round < n; ++round) {
+        int m = INT_MIN;
+#pragma unroll
+        for (int j = 0; j < KV; ++j)
+            if (v[j] < cur) m = max(m, v[j]);
+        m = __reduce_max_sync(0xffffffffu, m);
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < KV; ++j) c += v[j] == m;
+        c = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+        sp = m;
+        above = acc;
+        if (acc + c > pick) break;
+        acc += c;
+        cur = m;
+    }
+    int g = 0;
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+        const int e = j * 32 + lane;
+        const bool q = e < n && v[j] == sp;
+        const unsigned bal = __ballot_sync(0xffffffffu, q);
+        if (q) S.tie[g + __popc(bal & ((1u << lane) - 1))] = S.cidx[e];
+        g += __popc(bal);
+    }
+    if (lane == 0) {
+        S.misc[6] = g;
+        S.misc[5] = pick - above;  // rank inside the group
+    }
+}
+
 template <bool S16>  // int16 score rows (P.s16); one instance each keeps the code lean
 __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     select_fast_kernel(const __grid_constant__ SimParams P, const Job* __restrict__ jobs, int job0, int nj) {
     __shared__ FastSmem S;
     const int slot = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#ifdef CCW_DBG_TAIL
+    if (tid < 8) S.dbg[tid] = 0;
+#endif
     pdl_trigger();
     tl_mark(P.tl, 2);
+#ifdef CCW_TI_PREFETCH
+    // keep the fp64 TI apex planes (the tie rescoring's operands, rarely read)
+    // in L2: each CTA of the launch touches its slice, before the wait
+    if (wid == 1 && P.ti64) {
+        const size_t lines = (static_cast<size_t>(P.nch) * P.hc * P.wc * sizeof(double) + 127) / 128;
+        const size_t l0 = lines * slot / gridDim.x, l1 = lines * (slot + 1) / gridDim.x;
+        for (size_t l = l0 + lane; l < l1; l += 32)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const char*>(P.ti64) + l * 128));
+    }
+#endif
+#ifdef CCW_DBG_TLB  // experiment: touch this slot's score row before the wait (translation only)
+    if (wid == 1 && slot < nj) {
+        const char* r = reinterpret_cast<const char*>(P.scores) + static_cast<size_t>(slot) * P.sld * (P.s16 ? 2 : 4);
+        unsigned x;
+        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(x) : "l"(r + lane * 768));
+        if (x == 0x12345677u) S.misc[0] = 0;
+    }
+#endif
     pdl_wait();
     tl_mark(P.tl, 0);
     if (P.hb_reset && slot == 0) {  // the next launch's board (the last launch that used it is complete)
@@ -1456,6 +1683,10 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
 #ifdef CCW_DBG_TAIL
     const unsigned long long dbg_t0 = gtimer();
     int dbg_n = -2, dbg_g = 0;
+    long long pc[8] = {clock64(), 0, 0, 0, 0, 0, 0, 0};  // head, list, finish, resolve, choose, paste, deps
+#define PCLK(i) pc[i] = clock64()
+#else
+#define PCLK(i)
 #endif
     int fr, fc;
     if (jb.shape == kNone) {
@@ -1469,12 +1700,23 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         // the scan: warp 0 alone (scan_job), or with the list step spread over
         // every warp when the tile maxima fit in registers
         const bool coop = CCW_COOP_SCAN && P.ntiles <= 32 * kTM;
+        // An unconditional pick (matcher.hpp:207-211) needs only the top
+        // pick + 1 windows in rank order: every window at or above rank `pick`
+        // scores >= the (pick+1)-th largest score S_{pick+1} >= the (pick+1)-th
+        // largest tile maximum, so the scan runs with K' = pick + 1 -- fewer
+        // rounds, fewer qualifying tiles, and the list (and a deferral's
+        // threshold) is still a superset of the ranks that matter.
+        const bool upick = jb.pick >= 0 && !P.xrec;
+        const int Ks = upick ? min(jb.pick + 1, K) : K;
         long long sclk[5];
         if (wid == 0) {
             sclk[0] = clock64();
             if (coop) {
-                coop_head(P, slot, S);
+                coop_head(P, slot, S, Ks);
                 sclk[1] = clock64();
+                PCLK(1);
+                __syncwarp();
+                if (!(upick && lean_scan<S16>(P, slot, S, jb.pick, Ks, sclk)) && lane == 0) S.lean = 0;
             } else {
                 const int n = scan_job<S16>(P, slot, S.sw, S.cidx, mk, sclk, S.cs);
                 if (lane == 0) {
@@ -1501,11 +1743,19 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                 S.misc[7] = info.z;
             }
             cp_async_wait_all();
+#ifdef CCW_DBG_TAIL
+            if (tid == 32) S.dbg[3] = clock64();
+#endif
         }
         __syncthreads();
-        if (coop) {
+#ifdef CCW_DBG_TAIL
+        if (tid == 0) S.dbg[4] = clock64();
+#endif
+        const int lean = coop ? S.lean : 0;
+        if (coop && !lean) {
             coop_list<S16>(P, slot, S);
             __syncthreads();
+            PCLK(2);
             if (wid == 0) {
                 sclk[2] = clock64();
                 const int nl = S.lcnt, mk0 = S.misc[1];
@@ -1514,7 +1764,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                 if (S.lover) {
                     if (P.stats && lane == 0) atomicAdd(&P.stats[2], 1ull);
                 } else {
-                    n = scan_finish(P, S.sw, nl, mk0, S.cidx, sclk, S.cs);
+                    n = scan_finish(P, S.sw, nl, mk0, S.cidx, sclk, S.cs, Ks);
                 }
                 if (lane == 0) {
                     S.misc[0] = n;
@@ -1528,6 +1778,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             __syncthreads();
         }
         fclk[1] = clock64();
+        PCLK(3);
         const int n = S.misc[0], nr = S.misc[2], ngrp = S.misc[3];
 #ifdef CCW_DBG_TAIL
         dbg_n = n;
@@ -1548,46 +1799,13 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             // `pick` of (S desc, fp64 desc, index asc) matters, and windows with
             // different S never swap in fp64 -- so only the equal-S group that
             // holds rank `pick` can need fp64 keys, and none when it is a single window.
-            if (wid == 0) {
-                constexpr int kV = SC_LC / 32;
-                int v[kV];
-#pragma unroll
-                for (int j = 0; j < kV; ++j) {
-                    const int e = j * 32 + lane;
-                    v[j] = e < n ? S.cs[e] : INT_MIN;
-                }
-                int cur = INT_MAX, acc = 0, sp = INT_MIN, above = 0;
-                for (int round = 0; round <= jb.pick && round < n; ++round) {
-                    int m = INT_MIN;
-#pragma unroll
-                    for (int j = 0; j < kV; ++j)
-                        if (v[j] < cur) m = max(m, v[j]);
-                    m = __reduce_max_sync(0xffffffffu, m);
-                    int c = 0;
-#pragma unroll
-                    for (int j = 0; j < kV; ++j) c += v[j] == m;
-                    c = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
-                    sp = m;
-                    above = acc;
-                    if (acc + c > jb.pick) break;
-                    acc += c;
-                    cur = m;
-                }
-                int g = 0;
-#pragma unroll
-                for (int j = 0; j < kV; ++j) {
-                    const int e = j * 32 + lane;
-                    const bool q = e < n && v[j] == sp;
-                    const unsigned bal = __ballot_sync(0xffffffffu, q);
-                    if (q) S.tie[g + __popc(bal & ((1u << lane) - 1))] = S.cidx[e];
-                    g += __popc(bal);
-                }
-                if (lane == 0) {
-                    S.misc[6] = g;
-                    S.misc[5] = jb.pick - above;  // rank inside the group
-                }
+            if (wid == 0 && lean != 2) {
+                if (n <= 32)
+                    pick_group<1>(S, n, jb.pick, lane);
+                else
+                    pick_group<SC_LC / 32>(S, n, jb.pick, lane);
             }
-            __syncthreads();
+            if (lean != 2) __syncthreads();
             const int g = S.misc[6], rk = S.misc[5];
 #ifdef CCW_DBG_TAIL
             dbg_g = g;
@@ -1599,6 +1817,17 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                 const long long q0 = clock64();
 #endif
                 const int var = mask_variant(jb.shape, jb.vleft, jb.htop);
+#ifdef CCW_DBG_TAIL
+                if (tid == 0) S.dbg[3] = clock64();
+#endif
+#ifdef CCW_DBG_WARM  // experiment: a dry run on other windows first (warm code, cold data)
+                if (g < 8) {
+                    for (int e = tid; e < g; e += FS_T) S.utmp[e] = (S.tie[e] + 7919) % P.npos;
+                    __syncthreads();
+                    rescore_keys(P, S, tmg, nr, ngrp, S.utmp, g, S.key + 64);
+                    if (tid == 0 && P.stats) atomicAdd(&P.stats[39], static_cast<unsigned long long>(clock64() - q0));
+                }
+#endif
                 const int gr = P.umap && g >= UD_MIN ? uniform_reduce(P, S, g, var) : g;
                 if (!(P.hb && gr >= P.help_min && hb_rescore(P, S, slot, gr, ngrp, var)))
                     rescore_keys(P, S, tmg, nr, ngrp, S.tie, gr, S.key);
@@ -1610,7 +1839,15 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                     atomicAdd(&P.stats[39], static_cast<unsigned long long>(q0 - fclk[1]));
                 }
 #endif
-                if (wid == 0) {  // the rk-th best of the group by (fp64 desc, index asc)
+                if (g <= FS_T) {  // the rk-th best of the group by (fp64 desc, index asc): direct ranks
+                    if (tid < g) {
+                        const double ke = S.key[tid];
+                        const int ie = S.tie[tid];
+                        int rank = 0;
+                        for (int j = 0; j < g; ++j) rank += better(S.key[j], S.tie[j], ke, ie);
+                        if (rank == rk) S.misc[4] = ie;
+                    }
+                } else if (wid == 0) {
                     for (int round = 0; round <= rk; ++round) {
                         double bk = 0.0;
                         int bi = INT_MAX, bp = -1;
@@ -1641,6 +1878,9 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
                     }
                 }
                 __syncthreads();
+#ifdef CCW_DBG_TAIL
+                if (tid == 0) S.dbg[7] = clock64();
+#endif
                 picked = S.misc[4];
             }
         } else if (n >= 0 && n <= 32) {
@@ -1709,6 +1949,7 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
             if (cnt > 0) fast_batch(P, S, tmg, nr, ngrp, cnt, ntop, K);
         }
         fclk[2] = clock64();
+        PCLK(4);
         if (P.xrec) {  // position shard: hand the local top-K to the exchange
             ShardRec* xr = P.xrec + (static_cast<size_t>(P.xshard) * P.xnj + slot) * P.xk;
             for (int k = tid; k < P.xk; k += FS_T) {
@@ -1724,12 +1965,15 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
         }
         __syncthreads();
         fclk[3] = clock64();
+        PCLK(5);
         const int pos = picked >= 0 ? picked : S.misc[4];
         fr = (pos / P.out_w) << P.J;
         fc = (pos % P.out_w) << P.J;
     }
     paste_job<FS_T>(P, jb, gj, fr, fc, tid);
+    PCLK(6);
     prep_dependents(P, jobs, jb, &S.misc[5]);
+    PCLK(7);
     if (tid == 0) {
         P.chosen[2 * gj] = fr;
         P.chosen[2 * gj + 1] = fc;
@@ -1762,15 +2006,24 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     if (P.hb) hb_help(P, S);  // rescore posted chunks of this launch's large groups
 #ifdef CCW_DBG_TAIL
     if (P.jdump && tid == 0) {
-        unsigned long long* d = P.jdump + 4 * static_cast<size_t>(gj);
+        unsigned long long* d = P.jdump + 8 * static_cast<size_t>(gj);
         d[0] = dbg_t0;
         d[1] = dbg_t1;
         d[2] = gtimer();
         d[3] = static_cast<unsigned long long>(static_cast<unsigned>(dbg_n)) |
                (static_cast<unsigned long long>(dbg_g) << 32);
+        for (int q = 1; q < 8; ++q) {  // cycle deltas from the start, 16 bits each (saturated)
+            const long long dv = pc[q] ? min(pc[q] - pc[0], 65535ll) : 0;
+            d[4 + (q >> 2)] |= static_cast<unsigned long long>(dv) << (16 * (q & 3));
+        }
+        for (int q = 0; q < 8; ++q) {  // 0 tmax loaded, 1 M_K, 2 rows loaded, 3 staging done, 4 sync, 5 tl read, 6 atomic
+            const long long dv = S.dbg[q] > pc[0] ? min(S.dbg[q] - pc[0], 65535ll) : 0;
+            d[6 + (q >> 2)] |= static_cast<unsigned long long>(dv) << (16 * (q & 3));
+        }
     }
 #endif
     tl_mark(P.tl, 1);
+#undef PCLK
 }
 
 template __global__ void select_fast_kernel<false>(const __grid_constant__ SimParams, const Job* __restrict__, int, int);

@@ -855,8 +855,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     const char* jdump_path = debug_env("CCW_TAIL_DUMP");
     unsigned long long* d_jdump = nullptr;
     if (jdump_path) {
-        d_jdump = ctx->jdump.as<unsigned long long>(4 * total_jobs);
-        CCW_CUDA(cudaMemsetAsync(d_jdump, 0, sizeof(unsigned long long) * 4 * total_jobs, st));
+        d_jdump = ctx->jdump.as<unsigned long long>(8 * total_jobs);
+        CCW_CUDA(cudaMemsetAsync(d_jdump, 0, sizeof(unsigned long long) * 8 * total_jobs, st));
         for (int g = 0; g < G; ++g) GP[g].jdump = d_jdump;
     }
     // per (group, parity) parameter sets
@@ -1537,7 +1537,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     CCW_CUDA(cudaStreamSynchronize(st));
     if (sched_err) throw Fail(CCW_ERR_GENERIC, "internal: device schedule disagrees with the host path draws");
     if (d_jdump) {  // debug: per-job select timing, with each job's group and wave
-        std::vector<unsigned long long> jd(4 * total_jobs);
+        std::vector<unsigned long long> jd(8 * total_jobs);
         CCW_CUDA(cudaMemcpy(jd.data(), d_jdump, sizeof(unsigned long long) * jd.size(), cudaMemcpyDeviceToHost));
         if (FILE* f = fopen(jdump_path, "wb")) {
             std::vector<int32_t> gw(2 * total_jobs);
