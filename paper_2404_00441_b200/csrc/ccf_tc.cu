@@ -581,8 +581,10 @@ void launch_ccf_tc(const TcPlan& pl, int npos, int sld, int kpad, int nj, int32_
     const int ntot = ((npos + kN - 1) / kN) * ((nj + kM - 1) / kM);
     // CTAs resident at once: CCW_TC_MINB per SM when the footprint allows
     const int slots = tc_num_sms() * CCW_TC_MINB;
-    a.epi_in_ring = ntot <= slots;
-    dim3 grid(std::min(ntot, a.epi_in_ring ? slots : tc_num_sms()));
+    int cap = slots;
+    if (const char* e = debug_env("CCW_TC_GRID")) cap = std::max(1, std::min(slots, atoi(e)));
+    a.epi_in_ring = ntot <= cap;
+    dim3 grid(std::min(ntot, cap));
     auto k = s16 ? (tmax_nu ? ccf_tc_kernel<true, true> : ccf_tc_kernel<true, false>)
                  : (tmax_nu ? ccf_tc_kernel<false, true> : ccf_tc_kernel<false, false>);
     launch_pdl(k, grid, dim3(kThreads), ccf_tc_smem_bytes(a.epi_in_ring), st, pl.ma, pl.mb, a);

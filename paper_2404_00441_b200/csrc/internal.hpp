@@ -230,6 +230,8 @@ struct Options {
     int pack = 1;              // bit-packed streamed bands
     int stream_bands = 6;      // streaming checkpoints per call
     int place_threads = 0;     // host unpack threads (0 = auto)
+    int wave = 0;              // fused wave kernel (wave.cu) where it applies (experimental)
+    int wave_cs = 0;           // its CTAs per cluster (0 = auto)
 };
 
 // Known option names (for ccw_ctx_set_option); returns nullptr if unknown.
@@ -246,6 +248,8 @@ inline int* option_slot(Options& o, const std::string& name) {
     if (name == "pack") return &o.pack;
     if (name == "stream_bands") return &o.stream_bands;
     if (name == "place_threads") return &o.place_threads;
+    if (name == "wave") return &o.wave;
+    if (name == "wave_cs") return &o.wave_cs;
     return nullptr;
 }
 

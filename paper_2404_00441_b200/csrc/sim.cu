@@ -795,6 +795,18 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         d_tmaxnu = ctx->tmaxnu.as<int32_t>(G * maxj * ntiles);
         d_jvar = ctx->jvar.as<int8_t>(G * maxj);
     }
+    // fused wave kernel (wave.cu): one launch per wave for the source-block-map
+    // path with the int8 screen; TIs whose last call was a tie storm keep the
+    // select + bulk kernels (the wave kernel's fallback is exact but slow)
+    const bool use_wave = !sharded && use_tc && use_screen && d_src && !cfg.min_cut && cfg.scoring == 0 &&
+                          ctx->opt.wave && wave_supported(ti->nscr, Tc, ti->nch, Kp, T, OV) &&
+                          !ctx->tie_storm.count(bulk_key);
+    const int8_t* d_strips = nullptr;
+    int wave_nmb = 1;
+    if (use_wave) {
+        d_strips = ti_strips(ti, Tc, st, &wave_nmb);
+        wave_prepare(P);
+    }
     if (bulk_smem)
         CCW_CUDA(cudaFuncSetAttribute(select_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(bulk_smem)));
@@ -1319,6 +1331,39 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     ++launches;
                     continue;
                 }
+                if (use_wave && !first_wave) {
+                    cudaEvent_t a = nullptr, b = nullptr;
+                    if (ctx->profiling) {
+                        a = tm.get();
+                        b = tm.get();
+                        CCW_CUDA(cudaEventRecord(a, gs));
+                    }
+                    SimParams QW = Q;
+                    QW.tl = tl_next(w, g, 1);
+                    const int cs = wave_pick_cs(QW, nj, ctx->opt.wave_cs);
+                    launch_wave(QW, d_jobs, static_cast<int>(j0), nj, d_strips, wave_nmb, cs, gs);
+                    if (ctx->profiling) {
+                        CCW_CUDA(cudaEventRecord(b, gs));
+                        tm.ccf.push_back({a, b});
+                    }
+                    ++launches;
+                    ++ccf_launches;
+                    const int jps = wave_jobs_per_set();
+                    ccf_mma_flop += 2.0 * ((nj + jps - 1) / jps) * jps * (128.0 * wave_nmb * out_w) *
+                                    (ti->nscr * ((Tc + 1) & ~1) * 16.0);
+                    if (j0 == wave_off[g][w]) {
+                        double nL = 0, nS = 0;
+                        for (int r = 0; r < n_real; ++r)
+                            if (group_of(r) == g) {
+                                nL += vhistL[vid[r]][w];
+                                nS += vhist[vid[r]][w] - vhistL[vid[r]][w];
+                            }
+                        const double m = nL * mask_cells + nS * static_cast<double>(Tc) * OVc;
+                        ccf_flop += 2.0 * ti->nscr * npos * m;
+                        ccf_flop_ref += 2.0 * ti->nch * npos * m;
+                    }
+                    continue;
+                }
                 if (!first_wave) {
                     Q.tl = tl_next(w, g, 0);
                     if (!fuse_prep) {  // (fused: prepared by the previous wave's select)
@@ -1635,6 +1680,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (debug_env("CCW_TAIL"))
         fprintf(stderr, "small-group item (thread 0): loads+products %.0f chain+stores %.0f cycles over %llu\n",
                 stats[43] ? double(stats[41]) / stats[43] : 0.0, stats[43] ? double(stats[42]) / stats[43] : 0.0, stats[43]);
+    if (debug_env("CCW_PHASES") && use_wave && stats[14])
+        fprintf(stderr, "wave CTA phases (mean cycles from CTA start over %llu CTAs): dep-wait %.0f prep %.0f screen %.0f "
+                "lists-sync %.0f post+sync %.0f end %.0f\n", stats[14], stats[8] / double(stats[14]),
+                stats[9] / double(stats[14]), stats[10] / double(stats[14]), stats[11] / double(stats[14]),
+                stats[12] / double(stats[14]), stats[13] / double(stats[14]));
+    if (debug_env("CCW_PHASES") && use_wave && stats[14])
+        fprintf(stderr, "wave screen per CTA: mma waits acc %.0f full %.0f issue %.0f | epilogue(q0) waits %.0f work %.0f (ldtm %.0f) | "
+                "compactions per tile %.3f | tiles per CTA %.1f\n", stats[16] / double(stats[14]), stats[17] / double(stats[14]),
+                stats[22] / double(stats[14]), stats[18] / double(stats[14]), stats[19] / double(stats[14]), stats[23] / double(stats[14]), stats[20] / double(std::max(1ull, stats[21])),
+                stats[21] / double(stats[14]));
     if (debug_env("CCW_PHASES"))
         fprintf(stderr, "bulk CTA phases: setup %llu loop %llu (max CTA %llu) last-CTA merge+paste %llu cycles\n",
                 stats[44], stats[45], stats[46], stats[47]);
@@ -1647,7 +1702,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.list_overflows = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
     ctx->timing.shared_groups = static_cast<int64_t>(stats[32]);
-    if (bulk_launch && stats[1] > 0 && stats[3] * 50 > stats[1])  // > 2 % of the screened placements
+    if (use_wave) {
+        if (stats[1] > 0 && stats[2] * 50 > stats[1]) ctx->tie_storm[bulk_key] = true;
+    } else if (bulk_launch && stats[1] > 0 && stats[3] * 50 > stats[1])  // > 2 % of the screened placements
         ctx->tie_storm[bulk_key] = true;
     else
         ctx->tie_storm.erase(bulk_key);
