@@ -275,7 +275,7 @@ struct ccw_ctx {
     ccwgpu::Options opt;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf wave_w, cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, tmaxnu, jvar, ops_a, ops_b, ops_c, ops_d, ops_e;
     long long mtab_key = -1;  // (Tc, OVc, nch) of the mask tables in mtab
     ccwgpu::HostBuf h_stage;

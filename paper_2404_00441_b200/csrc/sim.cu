@@ -802,9 +802,13 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                           ctx->opt.wave && wave_supported(ti->nscr, Tc, ti->nch, Kp, T, OV) &&
                           !ctx->tie_storm.count(bulk_key);
     const int8_t* d_strips = nullptr;
-    int wave_nmb = 1;
+    int wave_nmb = 1, wave_nb = 16;
+    int8_t* d_wave_w = nullptr;
+    size_t wave_w_per_group = 0;
     if (use_wave) {
-        d_strips = ti_strips(ti, Tc, st, &wave_nmb);
+        d_strips = ti_strips(ti, Tc, st, &wave_nmb, &wave_nb);
+        wave_w_per_group = wave_wglob_bytes(P, static_cast<int>(maxj));
+        d_wave_w = ctx->wave_w.as<int8_t>(G * wave_w_per_group);
         wave_prepare(P);
     }
     if (bulk_smem)
@@ -1341,7 +1345,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     SimParams QW = Q;
                     QW.tl = tl_next(w, g, 1);
                     const int cs = wave_pick_cs(QW, nj, ctx->opt.wave_cs);
-                    launch_wave(QW, d_jobs, static_cast<int>(j0), nj, d_strips, wave_nmb, cs, gs);
+                    launch_wave(QW, d_jobs, static_cast<int>(j0), nj, d_strips, wave_nmb, wave_nb, cs, d_wave_w + g * wave_w_per_group, gs);
                     if (ctx->profiling) {
                         CCW_CUDA(cudaEventRecord(b, gs));
                         tm.ccf.push_back({a, b});
@@ -1349,7 +1353,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                     ++launches;
                     ++ccf_launches;
                     const int jps = wave_jobs_per_set();
-                    ccf_mma_flop += 2.0 * ((nj + jps - 1) / jps) * jps * (128.0 * wave_nmb * out_w) *
+                    ccf_mma_flop += 2.0 * ((nj + jps - 1) / jps) * jps * (static_cast<double>(wave_nb) * wave_nmb * out_w) *
                                     (ti->nscr * ((Tc + 1) & ~1) * 16.0);
                     if (j0 == wave_off[g][w]) {
                         double nL = 0, nS = 0;
@@ -1681,8 +1685,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         fprintf(stderr, "small-group item (thread 0): loads+products %.0f chain+stores %.0f cycles over %llu\n",
                 stats[43] ? double(stats[41]) / stats[43] : 0.0, stats[43] ? double(stats[42]) / stats[43] : 0.0, stats[43]);
     if (debug_env("CCW_PHASES") && use_wave && stats[14])
-        fprintf(stderr, "wave CTA phases (mean cycles from CTA start over %llu CTAs): dep-wait %.0f prep %.0f screen %.0f "
-                "lists-sync %.0f post+sync %.0f end %.0f\n", stats[14], stats[8] / double(stats[14]),
+        fprintf(stderr, "wave CTA phases (mean cycles from CTA start over %llu CTAs): dep-wait %.0f prep-own %.0f prep+sync %.0f screen %.0f "
+                "lists-sync %.0f post+sync %.0f end %.0f\n", stats[14], stats[8] / double(stats[14]), stats[24] / double(stats[14]),
                 stats[9] / double(stats[14]), stats[10] / double(stats[14]), stats[11] / double(stats[14]),
                 stats[12] / double(stats[14]), stats[13] / double(stats[14]));
     if (debug_env("CCW_PHASES") && use_wave && stats[14])
@@ -1690,6 +1694,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 "compactions per tile %.3f | tiles per CTA %.1f\n", stats[16] / double(stats[14]), stats[17] / double(stats[14]),
                 stats[22] / double(stats[14]), stats[18] / double(stats[14]), stats[19] / double(stats[14]), stats[23] / double(stats[14]), stats[20] / double(std::max(1ull, stats[21])),
                 stats[21] / double(stats[14]));
+    if (debug_env("CCW_PHASES") && use_wave && stats[14])
+        fprintf(stderr, "wave epilogue(q0) split per CTA: ldtm %.0f first-tile insert %.0f filter %.0f list %.0f bound-read %.0f "
+                "bound-publish %.0f\n", stats[25] / double(stats[14]), stats[26] / double(stats[14]), stats[27] / double(stats[14]),
+                stats[28] / double(stats[14]), stats[29] / double(stats[14]), stats[30] / double(stats[14]));
     if (debug_env("CCW_PHASES"))
         fprintf(stderr, "bulk CTA phases: setup %llu loop %llu (max CTA %llu) last-CTA merge+paste %llu cycles\n",
                 stats[44], stats[45], stats[46], stats[47]);
@@ -1712,7 +1720,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         ctx->bulk_off[bulk_key] = true;
     else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back
         ctx->bulk_off.erase(bulk_key);
-    ctx->timing.ccf_variant = any_screen ? (use_tc ? 2 : 1) : 0;
+    ctx->timing.ccf_variant = any_screen ? (use_wave ? 5 : (use_tc ? 2 : 1)) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();

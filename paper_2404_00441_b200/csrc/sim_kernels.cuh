@@ -290,16 +290,19 @@ __host__ __device__ inline BulkLayout bulk_layout(int nch, int Tc, int bx, int b
 // launch per wave (source-block-map path, raw scoring, K <= 16, Tc <= 16).
 struct WaveArgs {
     const int8_t* strips;  // ti_strips: [out_w][nmb][nscr][144][16] int8
-    int nmb;               // 128-row position blocks per column
+    int nmb;               // position blocks per column
+    int nb;                // positions per block (a multiple of 16, <= 128)
+    int8_t* wglob;         // per set: the A operand (screen weights) staged in global memory
     int dbg;               // debug builds only (CCW_WAVE_DBG): 1 no prep loads, 2 no list work, 4 no MMA
 };
 bool wave_supported(int nscr, int Tc, int nch, int K, int T, int OV);
-const int8_t* ti_strips(ccw_ti* ti, int Tc, cudaStream_t st, int* nmb_out);
+const int8_t* ti_strips(ccw_ti* ti, int Tc, cudaStream_t st, int* nmb_out, int* nb_out);
 int wave_pick_cs(const SimParams& P, int nj, int want);
 int wave_jobs_per_set();
 void wave_prepare(const SimParams& P);
-void launch_wave(const SimParams& P, const Job* jobs, int job0, int nj, const int8_t* strips, int nmb, int cs,
-                 cudaStream_t st);
+void launch_wave(const SimParams& P, const Job* jobs, int job0, int nj, const int8_t* strips, int nmb, int nb, int cs,
+                 int8_t* wglob, cudaStream_t st);
+size_t wave_wglob_bytes(const SimParams& P, int nj);
 
 // ---------------------------------------------------------- kernels -----
 

@@ -45,16 +45,18 @@ namespace ccwgpu {
 
 namespace {
 
-constexpr int WV_NJ = 16;     // placements per cluster (the MMA's N)
+constexpr int WV_M = 128;     // placements per cluster (the MMA's M, one TMEM lane each)
 constexpr int WV_T = 256;     // threads per CTA (= SEL_T for the fallback)
-constexpr int WV_SR = 144;    // strip rows: 128 positions + up to 16 template rows
-constexpr int WV_CAP = 64;    // list capacity per (epilogue warp, placement)
-constexpr int WV_ST = 6;      // strip ring stages
-constexpr int WV_NACC = 4;    // TMEM accumulators (16 columns each)
+constexpr int WV_NB = 128;    // positions per strip block (the MMA's N <= 128)
+constexpr int WV_SR = WV_NB + 16;  // strip rows: a block of positions + up to 16 template rows
+constexpr int WV_LC = 32;     // list capacity per placement and CTA
+constexpr int WV_LS = WV_LC + 1;  // list row stride (int2): spreads the lanes' rows over the banks
+constexpr int WV_ST = 4;      // strip ring stages
+constexpr int WV_NACC = 4;    // TMEM accumulators (WV_NB columns each)
 constexpr int WV_GCAP = 128;  // equal-score group members rescored per warp
 constexpr int WV_RS = 256;    // (member, run) partial sums per chunk
-constexpr int WV_MAXCS = 4;   // CTAs per cluster (position column ranges)
-constexpr int WV_KMAX = 16;   // largest K (and K') this path takes
+constexpr int WV_MAXCS = 16;  // CTAs per cluster (position column ranges)
+constexpr int WV_KMAX = 8;    // largest K (and K') this path takes
 #ifndef CCW_WV_MINB
 #define CCW_WV_MINB 1
 #endif
@@ -124,10 +126,11 @@ struct WvWarp {
 };
 
 struct WvLayout {
-    int stage_bytes, tsp;
-    size_t u, b, lists, cnt, thr, ov, sthr, kq, fb, jobs, bar, total;
+    int stage_bytes, tsp, nb;
+    size_t u, a, lists, cnt, drop, gthr, fb, jobs, bar, total;
 };
 
+// nb: positions per strip block (a multiple of 16, <= WV_NB)
 __host__ __device__ inline WvLayout wv_layout(int nscr, int Tc, int nch, int K, int T, int OV) {
     WvLayout L{};
     L.tsp = (Tc + 1) & ~1;
@@ -139,67 +142,25 @@ __host__ __device__ inline WvLayout wv_layout(int nscr, int Tc, int nch, int K, 
     size_t o = 0;
     L.u = o;
     o += (u + 1023) & ~static_cast<size_t>(1023);
-    L.b = o;  // B operand: [nscr * tsp core-matrix columns][16 placements][16 bytes]
-    o += static_cast<size_t>(nscr) * L.tsp * WV_NJ * 16;
-    L.lists = o;  // [4 quarters][16 placements][WV_CAP] (score, position)
-    o += static_cast<size_t>(4) * WV_NJ * WV_CAP * sizeof(int2);
-    L.cnt = o;  // [4][16] list lengths
-    o += 4 * WV_NJ * sizeof(int);
-    L.thr = o;  // [4][16] list thresholds
-    o += 4 * WV_NJ * sizeof(int);
-    L.ov = o;  // [4][16] largest value dropped from a list (INT_MIN: none)
-    o += 4 * WV_NJ * sizeof(int);
-    L.sthr = o;  // [16] shared lower bound of S_K' (max of the quarters' K'-th largest)
-    o += WV_NJ * sizeof(int);
-    L.kq = o;  // [16] K' per placement
-    o += WV_NJ * sizeof(int);
+    L.a = o;  // A operand (weights): [nscr * tsp core-matrix columns][128 placements][16 bytes]
+    o += static_cast<size_t>(nscr) * L.tsp * WV_M * 16;
+    L.lists = o;  // [128 placements][WV_LS] (score, position)
+    o += static_cast<size_t>(WV_M) * WV_LS * sizeof(int2);
+    L.cnt = o;  // [128] list lengths
+    o += WV_M * sizeof(int);
+    L.drop = o;  // [128] largest value dropped from the list (INT_MIN: none)
+    o += WV_M * sizeof(int);
+    L.gthr = o;  // [128] (rank 0) the cluster's shared lower bound of S_K'
+    o += WV_M * sizeof(int);
     L.fb = o;  // fallback bits of the placements this CTA owns
     o += 4 * sizeof(int);
-    L.jobs = o;
-    o += WV_NJ * sizeof(Job);
+    L.jobs = o;  // the placements this CTA owns (j = rank + CS * i)
+    o += (WV_M / 2) * sizeof(Job);
     o = (o + 15) & ~static_cast<size_t>(15);
     L.bar = o;  // full[ST], empty[ST], tfull[NACC], tempty[NACC], tmem slot
-    o += (2 * WV_ST + 2 * WV_NACC) * sizeof(uint64_t) + 16;
+    o += (2 * WV_ST + 2 * WV_NACC + 1) * sizeof(uint64_t) + 16;
     L.total = o + 1024;  // (base alignment slack)
     return L;
-}
-
-// Raise a list's threshold to its K'-th largest score (or the shared bound,
-// whichever is higher) and keep the entries at or above it (warp-wide).  When
-// the entries tying at the threshold do not fit, they are dropped and the
-// threshold moves past them: the returned .z is the dropped value (INT_MIN
-// if none) -- a lower bound of S_K', so the post-scan knows the lists are
-// complete above it.  Returns (length, threshold, dropped value).
-__device__ __forceinline__ int4 wv_compact(int2* L, int cnt, int kq, int thr) {
-    const int lane = threadIdx.x & 31;
-    const int2 e0 = lane < cnt ? L[lane] : make_int2(INT_MIN, -1);
-    const int2 e1 = lane + 32 < cnt ? L[lane + 32] : make_int2(INT_MIN, -1);
-    int cur = INT_MAX, acc = 0, m = INT_MIN;
-    for (int r = 0; r < kq; ++r) {
-        const int a = max(e0.y >= 0 && e0.x < cur ? e0.x : INT_MIN, e1.y >= 0 && e1.x < cur ? e1.x : INT_MIN);
-        m = __reduce_max_sync(0xffffffffu, a);
-        if (m == INT_MIN) break;
-        acc += __popc(__ballot_sync(0xffffffffu, e0.y >= 0 && e0.x == m)) +
-               __popc(__ballot_sync(0xffffffffu, e1.y >= 0 && e1.x == m));
-        if (acc >= kq) break;
-        cur = m;
-    }
-    if (acc >= kq) thr = max(thr, m);
-    bool k0 = e0.y >= 0 && e0.x >= thr, k1 = e1.y >= 0 && e1.x >= thr;
-    int dropped = INT_MIN;
-    if (__popc(__ballot_sync(0xffffffffu, k0)) + __popc(__ballot_sync(0xffffffffu, k1)) > WV_CAP - 32) {
-        dropped = thr;  // (thr is a lower bound of S_K': a local K'-th largest or the shared bound)
-        k0 = k0 && e0.x > thr;
-        k1 = k1 && e1.x > thr;
-        thr = thr + 1;
-    }
-    const unsigned b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
-    const unsigned lt = (1u << lane) - 1;
-    __syncwarp();
-    if (k0) L[__popc(b0 & lt)] = e0;
-    if (k1) L[__popc(b0) + __popc(b1 & lt)] = e1;
-    __syncwarp();
-    return make_int4(__popc(b0) + __popc(b1), thr, dropped, 0);
 }
 
 // fp64 reference scores (matcher.hpp:64-81, 158-161) of the windows
@@ -246,38 +207,34 @@ __device__ __noinline__ void wv_rescore(const SimParams& P, const Job& jb, WvWar
 }
 
 // The post-scan of placement j (one warp): the union of the cluster's lists,
-// S_K', the ranked candidates up to rank `need`, the pick, the paste.
+// the ranking up to rank K' (matcher.hpp:177-204), the pick, the paste.
 // Returns false when the placement needs the fallback.
 template <int CS>
-__device__ __noinline__ bool wv_post(const SimParams& P, const Job& jb, int gj, int j, int kq, const int2* lists,
-                        const int* cnts, const int* ovs, WvWarp& W) {
+__device__ __noinline__ bool wv_post(const SimParams& P, const Job& jb, int gj, int j, const int2* lists,
+                                     const int* cnts, const int* drops, WvWarp& W) {
     const int lane = threadIdx.x & 31;
     cg::cluster_group cl = cg::this_cluster();
-    constexpr int NL = 4 * CS;
-    int v[NL], p[NL];
+    int v[CS], p[CS];
     int dmax = INT_MIN;  // largest value any list dropped: the lists are complete above it
 #pragma unroll
-    for (int li = 0; li < NL; ++li) {
-        const int r = li >> 2, q = li & 3;
-        const int2* rl = cl.map_shared_rank(lists, r) + (q * WV_NJ + j) * WV_CAP;
-        const int n = *(cl.map_shared_rank(cnts, r) + q * WV_NJ + j);
-        dmax = max(dmax, *(cl.map_shared_rank(ovs, r) + q * WV_NJ + j));
+    for (int r = 0; r < CS; ++r) {
+        const int2* rl = cl.map_shared_rank(lists, r) + j * WV_LS;
+        const int n = *(cl.map_shared_rank(cnts, r) + j);
+        dmax = max(dmax, *(cl.map_shared_rank(drops, r) + j));
         const int2 e = lane < n ? rl[lane] : make_int2(INT_MIN, -1);
-        v[li] = e.x;
-        p[li] = e.y;
+        v[r] = e.x;
+        p[r] = e.y;
     }
-    // the ranking up to rank `need` (matcher.hpp:177-204): equal-S groups in
-    // descending S; a group of one needs no fp64 key
     const int pick = jb.pick;
-    const int need = kq;
+    const int need = pick >= 0 ? min(pick + 1, P.K) : P.K;
     int R = 0;
     int above = 0, cur = INT_MAX;
     bool runs_ready = false;
     while (above < need) {
         int a = INT_MIN;
 #pragma unroll
-        for (int li = 0; li < NL; ++li)
-            if (p[li] >= 0 && v[li] < cur) a = max(a, v[li]);
+        for (int r = 0; r < CS; ++r)
+            if (p[r] >= 0 && v[r] < cur) a = max(a, v[r]);
         const int m = __reduce_max_sync(0xffffffffu, a);
         if (m == INT_MIN) {  // fewer listed windows than `need`
             if (dmax != INT_MIN) return false;
@@ -286,7 +243,7 @@ __device__ __noinline__ bool wv_post(const SimParams& P, const Job& jb, int gj, 
         if (m <= dmax) return false;  // windows of this score may have been dropped: the generic select
         int g = 0;
 #pragma unroll
-        for (int li = 0; li < NL; ++li) g += __popc(__ballot_sync(0xffffffffu, p[li] >= 0 && v[li] == m));
+        for (int r = 0; r < CS; ++r) g += __popc(__ballot_sync(0xffffffffu, p[r] >= 0 && v[r] == m));
         cur = m;
         if (pick >= 0 && above + g <= pick) {  // ranks before the pick: order irrelevant
             above += g;
@@ -294,8 +251,8 @@ __device__ __noinline__ bool wv_post(const SimParams& P, const Job& jb, int gj, 
         }
         if (g == 1) {
 #pragma unroll
-            for (int li = 0; li < NL; ++li)
-                if (p[li] >= 0 && v[li] == m) W.tidx[above] = p[li];
+            for (int r = 0; r < CS; ++r)
+                if (p[r] >= 0 && v[r] == m) W.tidx[above] = p[r];
             above += 1;
             __syncwarp();
             continue;
@@ -303,9 +260,9 @@ __device__ __noinline__ bool wv_post(const SimParams& P, const Job& jb, int gj, 
         if (g > WV_GCAP) return false;  // a tie storm: the generic select
         int o = 0;
 #pragma unroll
-        for (int li = 0; li < NL; ++li) {
-            const unsigned bl = __ballot_sync(0xffffffffu, p[li] >= 0 && v[li] == m);
-            if (bl & (1u << lane)) W.gpos[o + __popc(bl & ((1u << lane) - 1))] = p[li];
+        for (int r = 0; r < CS; ++r) {
+            const unsigned bl = __ballot_sync(0xffffffffu, p[r] >= 0 && v[r] == m);
+            if (bl & (1u << lane)) W.gpos[o + __popc(bl & ((1u << lane) - 1))] = p[r];
             o += __popc(bl);
         }
         if (!runs_ready) {  // the mask's runs in reference order (channel-major, rows ascending)
@@ -356,100 +313,244 @@ __device__ __noinline__ bool wv_post(const SimParams& P, const Job& jb, int gj, 
     return true;
 }
 
-// The epilogue of one TMEM lane quarter q (one warp): every tile's 16
-// placement scores of 32 positions; a placement's list takes the windows at or
-// above its threshold.  Kept compact (thresholds and lengths in shared memory,
-// a loop over the placements a tile actually lists): the common tile is a
-// TMEM load, 16 compares and one warp reduction.
-__device__ __noinline__ void wv_epilogue(const SimParams& P, const WaveArgs& A, const WvLayout& L, uint32_t tmem, int q,
-                                         int c0, int ntile, int2* lists, int* cnts, int* thrs, int* ovs, int* sthr,
-                                         const int* kqs, uint64_t* tfull, uint64_t* tempty) {
-    const int lane = threadIdx.x & 31;
-    int* wthr = thrs + q * WV_NJ;
-    int* wcnt = cnts + q * WV_NJ;
-    if (lane < WV_NJ) {
-        wthr[lane] = kqs[lane] > 0 ? INT_MIN : INT_MAX;  // (absent placements never list)
-        wcnt[lane] = 0;
+// OR prep of the placements this CTA owns (j = rank + CS * i): their int8
+// screen weights (prep_src_job's arithmetic), one (placement, template row)
+// per thread, as 16-byte rows of the set's A operand in global memory
+// (A.wglob, the shared-memory layout); every CTA of the cluster then bulk-loads
+// the whole operand.  Rows past Tc and absent placements are written as zeros,
+// so every row is written exactly once.
+template <int CS>
+__device__ __noinline__ void wv_prep(const SimParams& P, const WaveArgs& A, const Job* js, int njs, int rank,
+                                     int8_t* wg, int tsp) {
+    const int Tc = P.Tc, B = P.B;
+    const size_t nc = static_cast<size_t>(P.hc) * P.wc;
+    constexpr int NOWN = WV_M / CS;
+    for (int it = threadIdx.x; it < NOWN * tsp; it += WV_T) {
+        const int i = it / tsp, s = it - i * tsp;
+        const int j = rank + CS * i;
+        int w[4][16];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int t = 0; t < 16; ++t) w[f][t] = 0;
+        if (j < njs && s < Tc) {
+            const Job& jb = js[i];
+            int t0, t1;
+            mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+            const int32_t* srow = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc +
+                                  static_cast<size_t>(jb.top / B + s) * P.swc + jb.left / B;
+            int sb[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) sb[t] = t >= t0 && t < t1 && !(A.dbg & 1) ? srow[t] : -1;
+            float n[4][16];
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int t = 0; t < 16; ++t) n[f][t] = f < P.nscr && sb[t] >= 0 ? P.tiscr[f * nc + sb[t]] : 0.f;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                if (t < t0 || t >= t1) continue;
+                int last = B * B;
+#pragma unroll
+                for (int f = 0; f < 4; ++f)
+                    if (f < P.nscr) last -= static_cast<int>(n[f][t]);
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    const int c = static_cast<int>(n[f][t]);
+                    w[f][t] = P.mode == 0 ? c - last : c;
+                }
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+            if (f >= P.nscr) break;
+            int4 row;
+            row.x = (w[f][0] & 255) | ((w[f][1] & 255) << 8) | ((w[f][2] & 255) << 16) | (w[f][3] << 24);
+            row.y = (w[f][4] & 255) | ((w[f][5] & 255) << 8) | ((w[f][6] & 255) << 16) | (w[f][7] << 24);
+            row.z = (w[f][8] & 255) | ((w[f][9] & 255) << 8) | ((w[f][10] & 255) << 16) | (w[f][11] << 24);
+            row.w = (w[f][12] & 255) | ((w[f][13] & 255) << 8) | ((w[f][14] & 255) << 16) | (w[f][15] << 24);
+            *reinterpret_cast<int4*>(wg + (static_cast<size_t>(f * tsp + s) * WV_M + j) * 16) = row;
+        }
     }
-    __syncwarp();
-    int2* myl = lists + q * WV_NJ * WV_CAP;
-    long long e_wait = 0, e_work = 0, ncomp = 0, e_ld = 0;
-    const unsigned lt = (1u << lane) - 1;
+}
+
+// The epilogue of one TMEM lane quarter (one warp, one placement per thread):
+// every tile's scores of its placement, a running top-K' of the values seen
+// (sorted, in registers) whose K'-th entry is the list threshold, and the
+// list of (score, position) at or above it in shared memory.  The cluster
+// shares the thresholds (gthr at rank 0: the max over CTAs of their K'-th
+// largest, still a lower bound of S_K'), so after a CTA's first tile a
+// 16-value chunk is almost always dismissed by its maximum alone.
+__device__ __forceinline__ void wv_insert(int val, int (&top)[WV_KMAX], int kq) {
+    int x = val;
+#pragma unroll
+    for (int k = 0; k < WV_KMAX; ++k)
+        if (k < kq && x > top[k]) {
+            const int y = top[k];
+            top[k] = x;
+            x = y;
+        }
+}
+
+// A full list: the K'-th largest of its windows (top rebuilt from them)
+// raises the threshold; a tie group at it that still does not fit is dropped
+// and the threshold moves past it (the post-scan checks the dropped value).
+// Returns (length, threshold, dropped value).
+__device__ __noinline__ int4 wv_make_room(int2* my, int cnt, int kq, int thr, int drop) {
+    // K'-th largest (with multiplicity) of the listed scores: rounds of "largest
+    // below the previous round", each one pass over the list
+    int cur = INT_MAX, acc = 0, kth = INT_MIN;
+    for (int r = 0; r < kq; ++r) {
+        int m = INT_MIN, c = 0;
+        for (int e = 0; e < cnt; ++e) {
+            const int x = my[e].x;
+            if (x < cur && x > m) {
+                m = x;
+                c = 1;
+            } else if (x == m) {
+                ++c;
+            }
+        }
+        if (m == INT_MIN) break;
+        acc += c;
+        if (acc >= kq) {
+            kth = m;
+            break;
+        }
+        cur = m;
+    }
+    thr = max(thr, kth);
+    int n2 = 0;
+    for (int e = 0; e < cnt; ++e) {
+        const int2 x = my[e];
+        if (x.x >= thr) my[n2++] = x;
+    }
+    if (n2 > WV_LC - 16) {  // a tie group at the threshold leaves no room: drop it
+        drop = max(drop, thr);
+        int n3 = 0;
+        for (int e = 0; e < n2; ++e) {
+            const int2 x = my[e];
+            if (x.x > thr) my[n3++] = x;
+        }
+        n2 = n3;
+        thr = thr + 1;
+    }
+    return make_int4(n2, thr, drop, kth);
+}
+
+__device__ __noinline__ void wv_epilogue(const SimParams& P, const WaveArgs& A, const WvLayout& L, uint32_t tmem, int q,
+                                         int c0, int ntile, int njs, const Job* __restrict__ jobs, int gj0, int2* lists,
+                                         int* cnts, int* drops, int* gthr, uint64_t* tfull, uint64_t* tempty) {
+    const int lane = threadIdx.x & 31;
+    const int j = q * 32 + lane;
+    cg::cluster_group cl = cg::this_cluster();
+    int* gt = cl.map_shared_rank(gthr, 0) + j;  // the cluster's shared bound for this placement
+    int kq = 0;
+    if (j < njs) {
+        const int pick = jobs[gj0 + j].pick;
+        kq = pick >= 0 ? min(pick + 1, P.K) : P.K;
+    }
+    int top[WV_KMAX];
+#pragma unroll
+    for (int k = 0; k < WV_KMAX; ++k) top[k] = INT_MIN;
+    // thr: windows below it are never listed; a lower bound of S_K' (this
+    // CTA's K'-th largest so far, the cluster's bound, or past a dropped tie)
+    int thr = kq > 0 ? INT_MIN : INT_MAX, drop = INT_MIN, cnt = 0, kpub = INT_MIN;
+    int2* my = lists + j * WV_LS;
+    long long e_wait = 0, e_work = 0, ncomp = 0, t_ld = 0, t_ins = 0, t_flt = 0, t_st = 0, t_gt = 0, t_pub = 0;
+    auto kth_of = [&]() {
+        int t = INT_MIN;
+#pragma unroll
+        for (int k = 0; k < WV_KMAX; ++k)
+            if (k == kq - 1) t = top[k];
+        return t;
+    };
     for (int i = 0; i < ntile; ++i) {
         const int b = i % WV_NACC;
         const long long k0 = clock64();
         mbar_wait(su(&tfull[b]), (i / WV_NACC) & 1);
         const long long k1 = clock64();
         e_wait += k1 - k0;
+        long long q0 = clock64();
+        if (i > 0 && kq > 0 && !(A.dbg & 8)) thr = max(thr, *gt);  // the other CTAs' bounds
+        t_gt += clock64() - q0;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t v[16];
-        ldtm16(tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 16, v);
-        e_ld += clock64() - k1;
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(su(&tempty[b]));
         const int c = c0 + i / A.nmb, mb = i - (i / A.nmb) * A.nmb;
-        const int r = mb * 128 + q * 32 + lane;
-        const bool valid = r < P.out_h && !(A.dbg & 2);
-        const int pos = r * P.out_w + c;
-        unsigned hit = 0;
-        const int4* t4 = reinterpret_cast<const int4*>(wthr);
+        const int r0 = mb * A.nb;
+        const uint32_t tb = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * WV_NB;
+        for (int ch = 0; ch < A.nb; ch += 16) {
+            uint32_t vv[16];
+            long long q1 = clock64();
+            ldtm16(tb + ch, vv);
+            t_ld += clock64() - q1;
+            q1 = clock64();
+            if (ch + 16 >= A.nb) {  // the accumulator is drained: the MMA may reuse it
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(su(&tempty[b]));
+            }
+            const int nv = min(16, P.out_h - (r0 + ch));  // valid rows of the chunk
+            int cm0 = INT_MIN, cm1 = INT_MIN, cm2 = INT_MIN, cm3 = INT_MIN;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const int4 t = t4[g];
-            hit |= (static_cast<int>(v[4 * g]) >= t.x ? 1u : 0u) << (4 * g);
-            hit |= (static_cast<int>(v[4 * g + 1]) >= t.y ? 1u : 0u) << (4 * g + 1);
-            hit |= (static_cast<int>(v[4 * g + 2]) >= t.z ? 1u : 0u) << (4 * g + 2);
-            hit |= (static_cast<int>(v[4 * g + 3]) >= t.w ? 1u : 0u) << (4 * g + 3);
-        }
-        if (!valid) hit = 0;
-        unsigned jobs_hit = __reduce_or_sync(0xffffffffu, hit);
-        if (jobs_hit == 0) {
-            e_work += clock64() - k1;
-            continue;
-        }
-        int val[WV_NJ];  // (dynamic pick below: a select chain, not local memory)
+            for (int u = 0; u < 16; u += 4) {
+                cm0 = max(cm0, u < nv ? static_cast<int>(vv[u]) : INT_MIN);
+                cm1 = max(cm1, u + 1 < nv ? static_cast<int>(vv[u + 1]) : INT_MIN);
+                cm2 = max(cm2, u + 2 < nv ? static_cast<int>(vv[u + 2]) : INT_MIN);
+                cm3 = max(cm3, u + 3 < nv ? static_cast<int>(vv[u + 3]) : INT_MIN);
+            }
+            const int cm = max(max(cm0, cm1), max(cm2, cm3));
+            const bool anyc = __any_sync(0xffffffffu, cm >= thr);
+            t_flt += clock64() - q1;
+            if (!anyc) continue;
+            const long long q2 = clock64();
+            // list the chunk's windows at or above the threshold
+            unsigned m = 0;
 #pragma unroll
-        for (int j = 0; j < WV_NJ; ++j) val[j] = static_cast<int>(v[j]);
-        while (jobs_hit) {
-            const int j = __ffs(jobs_hit) - 1;
-            jobs_hit &= jobs_hit - 1;
-            int vj = val[0];
-#pragma unroll
-            for (int k = 1; k < WV_NJ; ++k) vj = k == j ? val[k] : vj;
-            const bool pr = (hit >> j) & 1u;
-            const unsigned bal = __ballot_sync(0xffffffffu, pr);
-            int cnt = wcnt[j];
-            if (pr) myl[j * WV_CAP + cnt + __popc(bal & lt)] = make_int2(vj, pos);
-            cnt += __popc(bal);
-            __syncwarp();
-            if (cnt > WV_CAP - 32) {
+            for (int u = 0; u < 16; ++u) m |= (u < nv && static_cast<int>(vv[u]) >= thr ? 1u : 0u) << u;
+            if (m && cnt + __popc(m) > WV_LC) {
                 ++ncomp;
-                const int4 rr = wv_compact(myl + j * WV_CAP, cnt, kqs[j], max(wthr[j], sthr[j]));
-                cnt = rr.x;
-                if (lane == 0) {
-                    wthr[j] = rr.y;
-                    if (rr.z != INT_MIN) {
-                        ovs[q * WV_NJ + j] = max(ovs[q * WV_NJ + j], rr.z);
-                        atomicMax(&sthr[j], rr.z);
-                    } else if (rr.y != INT_MIN) {
-                        atomicMax(&sthr[j], rr.y);
-                    }
+                const int4 st = wv_make_room(my, cnt, kq, thr, drop);
+                cnt = st.x;
+                thr = st.y;
+                drop = st.z;
+                kpub = max(kpub, st.w);
+                m = 0;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) m |= (u < nv && static_cast<int>(vv[u]) >= thr ? 1u : 0u) << u;
+                if (cnt + __popc(m) > WV_LC) {  // ties at the raised threshold still do not fit
+                    drop = max(drop, thr);
+                    thr = thr + 1;
+                    m = 0;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) m |= (u < nv && static_cast<int>(vv[u]) >= thr ? 1u : 0u) << u;
                 }
             }
-            if (lane == 0) wcnt[j] = cnt;
-            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if ((m >> u) & 1u) my[cnt + __popc(m & ((1u << u) - 1))] = make_int2(static_cast<int>(vv[u]), (r0 + ch + u) * P.out_w + c);
+            cnt += __popc(m);
+            t_st += clock64() - q2;
         }
-        if ((i & 7) == 7 && lane < WV_NJ) wthr[lane] = max(wthr[lane], sthr[lane]);  // the other quarters' bounds
-        __syncwarp();
+        const long long q3 = clock64();
+        if (kq > 0 && !(A.dbg & 8)) {  // publish this CTA's bound (a K'-th largest it has seen)
+            if (kpub != INT_MIN) atomicMax(gt, kpub);
+        }
+        t_pub += clock64() - q3;
         e_work += clock64() - k1;
     }
+    cnts[j] = cnt;
+    drops[j] = drop;
     if (P.tl && P.stats && lane == 0 && q == 0) {
         atomicAdd(&P.stats[18], static_cast<unsigned long long>(e_wait));
         atomicAdd(&P.stats[19], static_cast<unsigned long long>(e_work));
         atomicAdd(&P.stats[20], static_cast<unsigned long long>(ncomp));
         atomicAdd(&P.stats[21], static_cast<unsigned long long>(ntile));
-        atomicAdd(&P.stats[23], static_cast<unsigned long long>(e_ld));
+        atomicAdd(&P.stats[25], static_cast<unsigned long long>(t_ld));
+        atomicAdd(&P.stats[26], static_cast<unsigned long long>(t_ins));
+        atomicAdd(&P.stats[27], static_cast<unsigned long long>(t_flt));
+        atomicAdd(&P.stats[28], static_cast<unsigned long long>(t_st));
+        atomicAdd(&P.stats[29], static_cast<unsigned long long>(t_gt));
+        atomicAdd(&P.stats[30], static_cast<unsigned long long>(t_pub));
     }
 }
 
@@ -461,41 +562,41 @@ __device__ __noinline__ void wv_fallback(const SimParams& Q, const Job* __restri
 }
 
 template <int CS>
-__global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
+__global__ void __launch_bounds__(WV_T, 1)
     wave_kernel(const __grid_constant__ SimParams P, const Job* __restrict__ jobs, int job0, int nj, WaveArgs A) {
     extern __shared__ __align__(1024) uint8_t wv_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(wv_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const WvLayout L = wv_layout(P.nscr, P.Tc, P.nch, P.K, P.T, P.OV);
     uint8_t* ring = sm + L.u;
-    int8_t* Bs = reinterpret_cast<int8_t*>(sm + L.b);
+    int8_t* Abuf = reinterpret_cast<int8_t*>(sm + L.a);
     int2* lists = reinterpret_cast<int2*>(sm + L.lists);
     int* cnts = reinterpret_cast<int*>(sm + L.cnt);
-    int* thrs = reinterpret_cast<int*>(sm + L.thr);
-    int* ovs = reinterpret_cast<int*>(sm + L.ov);
-    int* sthr = reinterpret_cast<int*>(sm + L.sthr);
-    int* kqs = reinterpret_cast<int*>(sm + L.kq);
+    int* drops = reinterpret_cast<int*>(sm + L.drop);
+    int* gthr = reinterpret_cast<int*>(sm + L.gthr);
     int* fbm = reinterpret_cast<int*>(sm + L.fb);
     Job* js = reinterpret_cast<Job*>(sm + L.jobs);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.bar);
     uint64_t* empty = full + WV_ST;
     uint64_t* tfull = empty + WV_ST;
     uint64_t* tempty = tfull + WV_NACC;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + WV_NACC);
+    uint64_t* abar = tempty + WV_NACC;  // the A operand landed
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(abar + 1);
 
     cg::cluster_group cl = cg::this_cluster();
     const int rank = static_cast<int>(cl.block_rank());
     const int set = static_cast<int>(blockIdx.x) / CS;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int js0 = set * WV_NJ;                     // first job slot of the set
-    const int njs = min(WV_NJ, nj - js0);            // placements of this set
+    const int js0 = set * WV_M;                      // first job slot of the set
+    const int njs = min(WV_M, nj - js0);             // placements of this set
     const int cpc = (P.out_w + CS - 1) / CS;         // columns per CTA
     const int c0 = min(P.out_w, rank * cpc), c1 = min(P.out_w, c0 + cpc);
     const int ntile = (c1 - c0) * A.nmb;
-    const int tsp = L.tsp, nk = P.nscr * (tsp / 2);  // MMAs per tile (K = 32 bytes each)
+    const int tsp = L.tsp;
+    constexpr int NOWN = WV_M / CS;
 
     const long long pc0 = clock64();
     auto phase = [&](int k) {  // debug timeline runs only: cycles from CTA start per phase, summed
-        if (P.tl && P.stats && tid == 0) atomicAdd(&P.stats[8 + k], static_cast<unsigned long long>(clock64() - pc0));
+        if (P.tl && P.stats && tid == 0) atomicAdd(&P.stats[k < 6 ? 8 + k : 24], static_cast<unsigned long long>(clock64() - pc0));
     };
     pdl_trigger();
     if (tid == 0) {
@@ -507,20 +608,19 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
             mbar_init(su(&tfull[b]), 1);
             mbar_init(su(&tempty[b]), 4);
         }
+        mbar_init(su(abar), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su(tslot)), "n"(WV_NACC * 16));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su(tslot)), "n"(WV_NACC * WV_NB));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    for (int e = tid; e < P.nscr * tsp * WV_NJ; e += WV_T)  // zero B (K padding, absent placements)
-        reinterpret_cast<int4*>(Bs)[e] = make_int4(0, 0, 0, 0);
-    if (tid < 4 * WV_NJ) ovs[tid] = INT_MIN;
-    if (tid < WV_NJ) {
-        sthr[tid] = INT_MIN;
-        if (tid < njs) js[tid] = jobs[job0 + js0 + tid];
+    if (tid < NOWN) {
+        const int j = rank + CS * tid;
+        if (j < njs) js[tid] = jobs[job0 + js0 + j];
     }
     if (tid < 4) fbm[tid] = 0;
+    if (tid < WV_M) gthr[tid] = INT_MIN;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -539,65 +639,18 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
     tl_mark(P.tl, 0);
     phase(0);
 
-    // ---- OR prep: int8 screen weights of the set's placements into B ----------
-    // (prep_src_job's arithmetic; thread = template cell, every placement's map
-    //  entry then every screen plane in flight at once)
-    {
-        const int Tc = P.Tc, B = P.B;
-        const size_t nc = static_cast<size_t>(P.hc) * P.wc;
-        const int c = tid, s = c / Tc, t = c - s * Tc;
-        if (c < Tc * Tc) {
-            int sb[WV_NJ];
-            unsigned inm = 0;
-#pragma unroll
-            for (int j = 0; j < WV_NJ; ++j) {
-                sb[j] = 0;
-                if (j < njs) {
-                    const Job& jb = js[j];
-                    int t0, t1;
-                    mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
-                    if (t >= t0 && t < t1) {
-                        inm |= 1u << j;
-                        if (!(A.dbg & 1))
-                            sb[j] = P.src[static_cast<size_t>(jb.real) * (P.wh / B) * P.swc +
-                                          static_cast<size_t>(jb.top / B + s) * P.swc + jb.left / B + t];
-                    }
-                }
-            }
-            for (int f0 = 0; f0 < P.nscr; f0 += 2) {  // two screen planes per round trip
-                float n[WV_NJ][2];
-#pragma unroll
-                for (int j = 0; j < WV_NJ; ++j)
-#pragma unroll
-                    for (int u = 0; u < 2; ++u)
-                        n[j][u] = ((inm >> j) & 1u) && f0 + u < P.nscr && !(A.dbg & 1) ? P.tiscr[(f0 + u) * nc + sb[j]] : 0.f;
-#pragma unroll
-                for (int j = 0; j < WV_NJ; ++j) {
-                    if (!((inm >> j) & 1u)) continue;
-                    int last = B * B;
-                    if (P.mode == 0)  // the last facies' count: every cell holds one facies
-                        for (int f = 0; f < P.nscr; ++f)
-                            last -= static_cast<int>(f >= f0 && f < f0 + 2 ? n[j][f - f0] : P.tiscr[f * nc + sb[j]]);
-#pragma unroll
-                    for (int u = 0; u < 2; ++u)
-                        if (f0 + u < P.nscr) {
-                            const int v = static_cast<int>(n[j][u]);
-                            Bs[(((f0 + u) * tsp + s) * WV_NJ + j) * 16 + t] = static_cast<int8_t>(P.mode == 0 ? v - last : v);
-                        }
-                }
-            }
-        }
-        if (tid < WV_NJ) {
-            int kq = 0;
-            if (tid < njs) {
-                const Job& jb = js[tid];
-                kq = jb.pick >= 0 ? min(jb.pick + 1, P.K) : P.K;
-            }
-            kqs[tid] = kq;
-        }
+    const int abytes = P.nscr * tsp * WV_M * 16;
+    int8_t* wg = A.wglob + static_cast<size_t>(set) * abytes;
+    wv_prep<CS>(P, A, js, njs, rank, wg, tsp);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // (generic writes -> the bulk copy's async proxy)
+    phase(6);
+    cl.sync();  // every row of the set's A operand is in global memory (gthr initialised too)
+    if (tid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_expect_tx(su(abar), abytes);
+        for (int o = 0; o < abytes; o += 32768)
+            bulk_load(su(Abuf + o), wg + o, min(32768, abytes - o), su(abar));
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B: generic writes -> the MMA's async proxy
-    __syncthreads();
     phase(1);
 
     // ---- screen: strips -> tcgen05 -> exact top-K' lists ----------------------
@@ -612,18 +665,20 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
                           A.strips + (static_cast<size_t>(c) * A.nmb + mb) * L.stage_bytes, L.stage_bytes, su(&full[s]));
             }
     } else if (warp == 1) {
-        if (lane == 0) {  // single-thread MMA issuer
-            constexpr uint32_t idesc = wv_idesc(128, WV_NJ);
-            constexpr int KM = 32;  // MMAs per tile: nscr * tsp / 2 <= 4 * 8
-            uint64_t ad0[KM], bd[KM];
-            const uint32_t abase = su(ring), bbase = su(Bs);
+        if (lane == 0) {  // single-thread MMA issuer: D[placement][position] += W[placement][k] * strip[position][k]
+            const uint32_t idesc = wv_idesc(WV_M, A.nb);
+            constexpr int KM = 16;  // MMAs per tile: nscr * tsp / 2 (<= 16: K <= 512 bytes)
+            uint64_t ad[KM], bd0[KM];
+            const uint32_t abase = su(Abuf), bbase = su(ring);
+            const int hs = tsp / 2;
 #pragma unroll
             for (int k = 0; k < KM; ++k) {
-                const int ch = k / 8, sp = k % 8;  // (tsp / 2 <= 8: s pairs padded to 8 per channel)
-                ad0[k] = ns_desc(abase + ch * (WV_SR * 16) + sp * 32, 16, 128);
-                bd[k] = ns_desc(bbase + (ch * tsp + 2 * sp) * (WV_NJ * 16), WV_NJ * 16, 128);
+                const int ch = k / hs, sp = k - ch * hs;
+                ad[k] = ns_desc(abase + (ch * tsp + 2 * sp) * (WV_M * 16), WV_M * 16, 128);
+                bd0[k] = ns_desc(bbase + ch * (WV_SR * 16) + sp * 32, 16, 128);
             }
-            const int hs = tsp / 2;
+            const int nk = P.nscr * hs;
+            mbar_wait(su(abar), 0);
             long long w_acc = 0, w_full = 0, w_iss = 0;
             for (int i = 0; i < ntile; ++i) {
                 const int s = i % WV_ST, b = i % WV_NACC;
@@ -635,11 +690,11 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
                 const long long k2 = clock64();
                 w_full += k2 - k1;
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t aoff = static_cast<uint64_t>((s * L.stage_bytes) >> 4);
-                const uint32_t d = tmem + b * 16;
+                const uint64_t boff = static_cast<uint64_t>((s * L.stage_bytes) >> 4);
+                const uint32_t d = tmem + b * WV_NB;
 #pragma unroll
                 for (int k = 0; k < KM; ++k)
-                    if ((k / 8) < P.nscr && (k % 8) < hs) mma_i8(d, ad0[k] + aoff, bd[k], idesc, k == 0 ? 0u : 1u);
+                    if (k < nk) mma_i8(d, ad[k], bd0[k] + boff, idesc, k == 0 ? 0u : 1u);
                 mma_commit(su(&empty[s]));
                 mma_commit(su(&tfull[b]));
                 w_iss += clock64() - k2;
@@ -650,8 +705,8 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
                 atomicAdd(&P.stats[17], static_cast<unsigned long long>(w_full));
             }
         }
-    } else if (warp < 6) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) ..
-        wv_epilogue(P, A, L, tmem, warp & 3, c0, ntile, lists, cnts, thrs, ovs, sthr, kqs, tfull, tempty);
+    } else if (warp < 6) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. = placements
+        wv_epilogue(P, A, L, tmem, warp & 3, c0, ntile, njs, jobs, job0 + js0, lists, cnts, drops, gthr, tfull, tempty);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -661,64 +716,72 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
 
     // ---- post-scan: the placements this CTA owns, one warp each --------------
     WvWarp& W = reinterpret_cast<WvWarp*>(ring)[warp];
-    for (int j = rank + CS * warp; j < njs && !(A.dbg & 2); j += CS * 8) {
-        const bool ok = wv_post<CS>(P, js[j], job0 + js0 + j, j, kqs[j], lists, cnts, ovs, W);
-        if (!ok && lane == 0) atomicOr(&fbm[0], 1 << j);
+    for (int i = warp; i < NOWN && !(A.dbg & 2); i += 8) {
+        const int j = rank + CS * i;
+        if (j >= njs) break;
+        const bool ok = wv_post<CS>(P, js[i], job0 + js0 + j, j, lists, cnts, drops, W);
+        if (!ok && lane == 0) atomicOr(&fbm[i >> 5], 1 << (i & 31));
     }
     __syncthreads();
     cl.sync();  // remote list reads done; fallback bits published
-    int fb = 0;
+    int fb[CS];
+    bool anyfb = false;
 #pragma unroll
-    for (int r = 0; r < CS; ++r) fb |= *cl.map_shared_rank(fbm, r);
+    for (int r = 0; r < CS; ++r) {
+        fb[r] = *cl.map_shared_rank(fbm, r);
+        anyfb |= fb[r] != 0;
+    }
     cl.sync();  // no CTA leaves while another reads its shared memory
     phase(4);
 
     // ---- fallback (tie storms): full score rows, then the generic select -----
-    if (fb) {
+    if (anyfb) {
+        mbar_wait(su(abar), 0);
         const int Tc = P.Tc;
         const size_t nc = static_cast<size_t>(P.hc) * P.wc;
-        for (int j = 0; j < njs; ++j) {
-            if (!((fb >> j) & 1)) continue;
-            const int slot = js0 + j;
-            int32_t* row = P.scores + static_cast<size_t>(slot) * P.sld;
-            for (int e = tid; e < (c1 - c0) * P.out_h; e += WV_T) {
-                const int c = c0 + e / P.out_h, r = e - (e / P.out_h) * P.out_h;
-                const int mb = r >> 7, rl = r & 127;
-                const int8_t* st = A.strips + (static_cast<size_t>(c) * A.nmb + mb) * L.stage_bytes;
-                int acc = 0;
-                for (int f = 0; f < P.nscr; ++f)
-                    for (int s = 0; s < tsp; ++s) {
-                        const int4 a = *reinterpret_cast<const int4*>(st + (f * WV_SR + rl + s) * 16);
-                        const int4 w = *reinterpret_cast<const int4*>(Bs + ((f * tsp + s) * WV_NJ + j) * 16);
-                        acc = __dp4a(a.x, w.x, acc);
-                        acc = __dp4a(a.y, w.y, acc);
-                        acc = __dp4a(a.z, w.z, acc);
-                        acc = __dp4a(a.w, w.w, acc);
+        for (int r = 0; r < CS; ++r)
+            for (int i = 0; i < NOWN; ++i) {
+                if (!((fb[r] >> i) & 1)) continue;
+                const int j = r + CS * i, slot = js0 + j;
+                int32_t* row = P.scores + static_cast<size_t>(slot) * P.sld;
+                for (int e = tid; e < (c1 - c0) * P.out_h; e += WV_T) {
+                    const int c = c0 + e / P.out_h, rr = e - (e / P.out_h) * P.out_h;
+                    const int mb = rr / A.nb, rl = rr - mb * A.nb;
+                    const int8_t* st = A.strips + (static_cast<size_t>(c) * A.nmb + mb) * L.stage_bytes;
+                    int acc = 0;
+                    for (int f = 0; f < P.nscr; ++f)
+                        for (int s = 0; s < tsp; ++s) {
+                            const int4 a = *reinterpret_cast<const int4*>(st + (f * WV_SR + rl + s) * 16);
+                            const int4 w = *reinterpret_cast<const int4*>(Abuf + (static_cast<size_t>(f * tsp + s) * WV_M + j) * 16);
+                            acc = __dp4a(a.x, w.x, acc);
+                            acc = __dp4a(a.y, w.y, acc);
+                            acc = __dp4a(a.z, w.z, acc);
+                            acc = __dp4a(a.w, w.w, acc);
+                        }
+                    row[rr * P.out_w + c] = acc;
+                }
+                if (r == rank) {  // the owner stages the placement's fp64 template
+                    const Job& jb = js[i];
+                    const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc;
+                    double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
+                    for (int cc = tid; cc < Tc * Tc; cc += WV_T) {
+                        const int s = cc / Tc, t = cc - s * Tc;
+                        int t0, t1;
+                        mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
+                        const bool in = t >= t0 && t < t1;
+                        const int sb = in ? src[static_cast<size_t>(jb.top / P.B + s) * P.swc + jb.left / P.B + t] : 0;
+                        for (int chn = 0; chn < P.nch; ++chn) tm[chn * Tc * Tc + cc] = in ? P.ti64[chn * nc + sb] : 0.0;
                     }
-                row[r * P.out_w + c] = acc;
-            }
-            if (j % CS == rank) {  // the owner stages the placement's fp64 template
-                const Job& jb = js[j];
-                const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc;
-                double* tm = P.tm64 + static_cast<size_t>(slot) * P.nch * Tc * Tc;
-                for (int c = tid; c < Tc * Tc; c += WV_T) {
-                    const int s = c / Tc, t = c - s * Tc;
-                    int t0, t1;
-                    mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
-                    const bool in = t >= t0 && t < t1;
-                    const int sb = in ? src[static_cast<size_t>(jb.top / P.B + s) * P.swc + jb.left / P.B + t] : 0;
-                    for (int ch = 0; ch < P.nch; ++ch) tm[ch * Tc * Tc + c] = in ? P.ti64[ch * nc + sb] : 0.0;
                 }
             }
-        }
         __threadfence();
         cl.sync();  // every column range of the rows is written
         SimParams Q = P;
         Q.tmax = nullptr;
-        for (int j = rank; j < njs; j += CS)
-            if ((fb >> j) & 1) {
+        for (int i = 0; i < NOWN; ++i)
+            if ((fb[rank] >> i) & 1) {
                 __syncthreads();
-                wv_fallback(Q, jobs, job0, js0 + j, ring);
+                wv_fallback(Q, jobs, job0, js0 + rank + CS * i, ring);
                 if (tid == 0 && P.stats) atomicAdd(&P.stats[2], 1ull);
             }
     }
@@ -726,12 +789,12 @@ __global__ void __launch_bounds__(WV_T, CCW_WV_MINB)
     phase(5);
     if (P.tl && P.stats && tid == 0) atomicAdd(&P.stats[14], 1ull);
     tl_mark(P.tl, 1);
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(WV_NACC * 16));
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(WV_NACC * WV_NB));
 }
 
-__global__ void strips_kernel(const float* __restrict__ scr, int nscr, int hc, int wc, int out_w, int nmb,
+__global__ void strips_kernel(const float* __restrict__ scr, int nscr, int hc, int wc, int out_w, int nmb, int nb,
                               int8_t* __restrict__ out) {
-    // out[c][mb][ch][WV_SR][16] = plane[ch][mb * 128 + row][c + t], 0 outside
+    // out[c][mb][ch][WV_SR][16] = plane[ch][mb * nb + row][c + t], 0 outside
     const size_t per = static_cast<size_t>(nscr) * WV_SR * 16;
     const size_t total = static_cast<size_t>(out_w) * nmb * per;
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
@@ -739,7 +802,7 @@ __global__ void strips_kernel(const float* __restrict__ scr, int nscr, int hc, i
         const size_t cm = i / per, rem = i - cm * per;
         const int c = static_cast<int>(cm / nmb), mb = static_cast<int>(cm - static_cast<size_t>(c) * nmb);
         const int ch = static_cast<int>(rem / (WV_SR * 16)), rr = static_cast<int>(rem % (WV_SR * 16));
-        const int row = mb * 128 + rr / 16, col = c + rr % 16;
+        const int row = mb * nb + rr / 16, col = c + rr % 16;
         int8_t v = 0;
         if (row < hc && col < wc) v = static_cast<int8_t>(__float2int_rn(scr[(static_cast<size_t>(ch) * hc + row) * wc + col]));
         out[i] = v;
@@ -748,56 +811,72 @@ __global__ void strips_kernel(const float* __restrict__ scr, int nscr, int hc, i
 
 }  // namespace
 
-int wave_max_cs() { return WV_MAXCS; }
-int wave_jobs_per_set() { return WV_NJ; }
+int wave_jobs_per_set() { return WV_M; }
 
 bool wave_supported(int nscr, int Tc, int nch, int K, int T, int OV) {
-    if (nscr < 1 || nscr > 4 || Tc > 16 || Tc < 1 || K > WV_KMAX || K < 1 || nch * Tc > 64) return false;
+    const int tsp = (Tc + 1) & ~1;
+    if (nscr < 1 || nscr > 4 || nscr * tsp > 32 || Tc > 16 || Tc < 1 || K > WV_KMAX || K < 1 || nch * Tc > 64)
+        return false;
     return wv_layout(nscr, Tc, nch, K, T, OV).total <= 227 * 1024;
 }
 
-const int8_t* ti_strips(ccw_ti* ti, int Tc, cudaStream_t st, int* nmb_out) {
+// Position blocks of a column: nb positions (a multiple of 16, <= 128) each.
+static void wave_blocks(int out_h, int* nmb, int* nb) {
+    *nmb = (out_h + WV_NB - 1) / WV_NB;
+    const int per = (out_h + *nmb - 1) / *nmb;
+    *nb = (per + 15) & ~15;
+}
+
+const int8_t* ti_strips(ccw_ti* ti, int Tc, cudaStream_t st, int* nmb_out, int* nb_out) {
     const int out_h = ti->hc - Tc + 1, out_w = ti->wc - Tc + 1;
-    const int nmb = (out_h + 127) / 128;
+    int nmb, nb;
+    wave_blocks(out_h, &nmb, &nb);
     *nmb_out = nmb;
+    *nb_out = nb;
     const int key = -1000 - Tc;  // (shares the per-TI cache map with the im2col, keyed apart)
     auto it = ti->im2col.find(key);
     if (it != ti->im2col.end()) return it->second;
     const size_t bytes = static_cast<size_t>(out_w) * nmb * ti->nscr * WV_SR * 16;
     int8_t* X = static_cast<int8_t*>(cache_alloc(ti->device, bytes));
     strips_kernel<<<static_cast<unsigned>(std::min<size_t>((bytes + 255) / 256, 148 * 8)), 256, 0, st>>>(
-        ti->d_scr, ti->nscr, ti->hc, ti->wc, out_w, nmb, X);
+        ti->d_scr, ti->nscr, ti->hc, ti->wc, out_w, nmb, nb, X);
     CCW_CUDA(cudaGetLastError());
     ti->im2col[key] = X;
     return X;
 }
 
 int wave_pick_cs(const SimParams& P, int nj, int want) {
-    const int sets = (nj + WV_NJ - 1) / WV_NJ;
-    if (want > 0) return std::max(1, std::min(WV_MAXCS, want));
-    int cs = WV_MAXCS;
-    while (cs > 1 && sets * cs > 148) --cs;
+    const int sets = (nj + WV_M - 1) / WV_M;
+    if (want == 4 || want == 8 || want == 16) return want;
     (void)P;
-    return cs;
+    return sets * 16 <= 148 ? 16 : (sets * 8 <= 148 ? 8 : 4);
 }
 
-// Once per simulate call: the kernels' dynamic shared-memory ceiling.
+// Once per simulate call: the kernels' dynamic shared-memory ceiling and
+// (cluster size 16) the non-portable cluster permission.
 void wave_prepare(const SimParams& P) {
     const int bytes = static_cast<int>(wv_layout(P.nscr, P.Tc, P.nch, P.K, P.T, P.OV).total);
-    CCW_CUDA(cudaFuncSetAttribute(wave_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    CCW_CUDA(cudaFuncSetAttribute(wave_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    CCW_CUDA(cudaFuncSetAttribute(wave_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CCW_CUDA(cudaFuncSetAttribute(wave_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CCW_CUDA(cudaFuncSetAttribute(wave_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CCW_CUDA(cudaFuncSetAttribute(wave_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CCW_CUDA(cudaFuncSetAttribute(wave_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
-void launch_wave(const SimParams& P, const Job* jobs, int job0, int nj, const int8_t* strips, int nmb, int cs,
-                 cudaStream_t st) {
+size_t wave_wglob_bytes(const SimParams& P, int nj) {
+    const int tsp = (P.Tc + 1) & ~1;
+    return static_cast<size_t>((nj + WV_M - 1) / WV_M) * P.nscr * tsp * WV_M * 16;
+}
+
+void launch_wave(const SimParams& P, const Job* jobs, int job0, int nj, const int8_t* strips, int nmb, int nb, int cs,
+                 int8_t* wglob, cudaStream_t st) {
     const WvLayout L = wv_layout(P.nscr, P.Tc, P.nch, P.K, P.T, P.OV);
     WaveArgs A{};
     A.strips = strips;
     A.nmb = nmb;
+    A.nb = nb;
+    A.wglob = wglob;
     if (const char* e = debug_env("CCW_WAVE_DBG")) A.dbg = atoi(e);
-    const int sets = (nj + WV_NJ - 1) / WV_NJ;
+    const int sets = (nj + WV_M - 1) / WV_M;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(sets * cs));
     cfg.blockDim = dim3(WV_T);
@@ -818,10 +897,9 @@ void launch_wave(const SimParams& P, const Job* jobs, int job0, int nj, const in
     }
     auto go = [&](auto kern) { CCW_CUDA(cudaLaunchKernelEx(&cfg, kern, P, jobs, job0, nj, A)); };
     switch (cs) {
-        case 1: go(wave_kernel<1>); break;
-        case 2: go(wave_kernel<2>); break;
-        case 3: go(wave_kernel<3>); break;
-        default: go(wave_kernel<4>); break;
+        case 4: go(wave_kernel<4>); break;
+        case 8: go(wave_kernel<8>); break;
+        default: go(wave_kernel<16>); break;
     }
 }
 

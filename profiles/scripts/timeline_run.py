@@ -11,6 +11,8 @@ seeds = np.array([cs.mix64(20240441, r + 1) for r in range(100)], np.uint64)
 c = cfg.to_c(); d_out = torch.empty(100 * 10**6, dtype=torch.uint8, device="cuda:0")
 diags = (_abi.DiagC * 100)()
 if os.environ.get("GROUPS"): dev.set_option("groups", int(os.environ["GROUPS"]))
+for _k in ("wave", "wave_cs"):
+    if os.environ.get(_k.upper()): dev.set_option(_k, int(os.environ[_k.upper()]))
 for i in range(int(os.environ.get("REPS", "4"))):
     dev.check(lib.ccw_simulate_device(dev.handle, tih.handle, C.byref(c), seeds.ctypes.data_as(_abi.U64P), 100, None, 0, C.c_void_p(d_out.data_ptr()), diags))
     torch.cuda.synchronize()

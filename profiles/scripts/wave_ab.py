@@ -12,7 +12,7 @@ seeds = np.array([cs.mix64(20240441, r + 1) for r in range(NR)], np.uint64)
 c = cfg.to_c(); d_out = torch.empty(NR * 10**6, dtype=torch.uint8, device="cuda:0")
 diags = (_abi.DiagC * NR)()
 outs = {}
-for wave in [0, 1] + [1] * 0:
+for wave in [0, 1]:
     dev.set_option("wave", wave)
     for cs_ in ([0] if wave == 0 else [int(x) for x in os.environ.get("CS", "0").split(",")]):
         dev.set_option("wave_cs", cs_)

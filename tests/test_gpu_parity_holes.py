@@ -190,3 +190,47 @@ def to_cfg(d, hd=None):
     if hd:
         cfg.hard_data = cs.HardDataSet([cs.HardDatum(*p) for p in hd])
     return cfg
+
+
+@pytest.mark.parametrize("cs_", [4, 8, 16])
+def test_wave_kernel_paths(oracle, cs_):
+    """The fused wave kernel (csrc/wave.cu, option `wave`): OR prep, the
+    implicit-im2col tcgen05 screen, the epilogue's top-K' lists, fp64 tie
+    ranking, conditional and unconditional picks and the in-kernel tie-storm
+    fallback, for every cluster size.  Bit-exact against the restatement."""
+    dev = cs.Device(0)  # a fresh context: no tie-storm memory
+    try:
+        with dev.options(wave=1, wave_cs=cs_):
+            # tie-heavy binary channels, J3, K1: list drops and the generic fallback
+            ti_a, geo = tie_heavy_case()
+            ti = cs.CategoricalGrid(640, 640, 2, ti_a)
+            d = dict(sg_height=500, sg_width=520, **geo)
+            seeds = [cs.mix64(13, 1), cs.mix64(13, 2)]
+            res = cs.simulate_batch(ti, to_cfg(d), seeds, device=dev)
+            assert dev.last_timing()["ccf_variant"] == 5  # the wave kernel ran
+            for s, r in zip(seeds, res):
+                o = oracle.simulate_one(ti_a, 2, pyoracle.Cfg(**d), None, seed=s)
+                assert np.array_equal(r.realization.cells, o["realization"]), ("ties", cs_, s)
+            # three facies, K5 unconditional picks (config-1 shape, smaller grid)
+            ti3 = synth.config1_ti()
+            g3 = cs.CategoricalGrid(500, 500, 3, ti3)
+            d3 = dict(sg_height=400, sg_width=352, template_size=64, overlap=16, dwt_level=2, candidates=5)
+            seeds3 = [cs.mix64(17, r + 1) for r in range(3)]
+            res3 = cs.simulate_batch(g3, to_cfg(d3), seeds3, device=dev)
+            assert dev.last_timing()["ccf_variant"] == 5
+            for s, r in zip(seeds3, res3):
+                o = oracle.simulate_one(ti3, 3, pyoracle.Cfg(**d3), None, seed=s)
+                assert np.array_equal(r.realization.cells, o["realization"]), ("k5", cs_, s)
+            # conditional picks: config 0' with 1 % hard data
+            ti0, cfg0 = config0_adjusted()
+            g0 = cs.CategoricalGrid(248, 248, 2, ti0)
+            base = cs.simulate_one(g0, cfg0, 5, device=dev).realization.cells
+            hd = synth.hard_data_from(base, 0.01, 5)
+            cfg0.hard_data = hd
+            for s in [cs.mix64(19, 1), cs.mix64(19, 2)]:
+                r = cs.simulate_one(g0, cfg0, s, device=dev)
+                o = oracle.simulate_one(ti0, 2, pyoracle.Cfg(**cfg_dict(cfg0)), hd, seed=s)
+                assert np.array_equal(r.realization.cells, o["realization"]), ("cond", cs_, s)
+                assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
+    finally:
+        dev.close()
