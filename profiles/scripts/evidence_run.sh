@@ -19,3 +19,7 @@ WHICH=4 REPS=1 ncu --set full --clock-control none --import-source on -k regex:s
 REPS=1 ncu --set full --clock-control none --import-source on -k regex:select_bulk -s 120 -c 1 \
     -o gpurun_out/bulk python profiles/scripts/config2_run.py > gpurun_out/ncu_bulk.log 2>&1
 tail -c 400 gpurun_out/b.log; tail -c 300 gpurun_out/bref.log
+# the experimental fused wave kernel (option wave=1, off by default): one launch, config 1
+WAVE=1 WAVE_CS=16 REPS=1 ncu --set full --clock-control none --import-source on -k regex:wave_kernel -s 20 -c 1 \
+    -o gpurun_out/wave python profiles/scripts/timeline_run.py > gpurun_out/ncu_wave.log 2>&1
+CS=4,8,16 python profiles/scripts/wave_ab.py > gpurun_out/wave_ab.log 2>&1

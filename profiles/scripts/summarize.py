@@ -55,7 +55,8 @@ def ncu_summary(tag, rep, kernel):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     out = io.StringIO()
     src = {"s3d": "profiles/scripts/config3_run.py (WHICH=3)", "s4d": "profiles/scripts/config3_run.py (WHICH=4)",
-           "bulk": "profiles/scripts/config2_run.py"}.get(rep, "python bench.py --steps 1 --warmup 1 --skip-cpu, config 1")
+           "bulk": "profiles/scripts/config2_run.py",
+           "wave": "WAVE=1 WAVE_CS=16 profiles/scripts/timeline_run.py (the experimental fused wave kernel, config 1)"}.get(rep, "python bench.py --steps 1 --warmup 1 --skip-cpu, config 1")
     out.write(f"# {tag} {kernel}: one launch, ncu --set full --clock-control none --import-source on ({src}); "
               "see profiles/scripts/evidence_run.sh\n")
     r = list(csv.reader(io.StringIO(det)))
@@ -79,6 +80,6 @@ if __name__ == "__main__":
     ncu_summary(tag, "ccf", "ccf_tc_kernel")
     ncu_summary(tag, "sel", "select_fast_kernel")
     for rep, kern in (("s3d", "screen3d_kernel (config 3)"), ("s4d", "screen3d_kernel (config 4)"),
-                      ("bulk", "select_bulk_kernel (config 2)")):
+                      ("bulk", "select_bulk_kernel (config 2)"), ("wave", "wave_kernel<16> (experimental)")):
         if os.path.exists(os.path.join(OUT, rep + ".ncu-rep")):
             ncu_summary(tag, rep, kern)
