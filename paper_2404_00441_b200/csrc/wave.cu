@@ -35,7 +35,6 @@
 
 #include <algorithm>
 #include <climits>
-#include <map>
 
 #include "select_common.cuh"
 
@@ -57,9 +56,6 @@ constexpr int WV_GCAP = 128;  // equal-score group members rescored per warp
 constexpr int WV_RS = 256;    // (member, run) partial sums per chunk
 constexpr int WV_MAXCS = 16;  // CTAs per cluster (position column ranges)
 constexpr int WV_KMAX = 8;    // largest K (and K') this path takes
-#ifndef CCW_WV_MINB
-#define CCW_WV_MINB 1
-#endif
 
 static_assert(WV_T == SEL_T, "the fallback runs the generic select with every thread");
 

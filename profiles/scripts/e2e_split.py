@@ -16,7 +16,8 @@ for _k in ("stream_bands", "place_threads", "groups", "pack"):
 def sim(h):
     dev.check(lib.ccw_simulate(dev.handle, h, C.byref(c), seeds.ctypes.data_as(_abi.U64P), 100, None, 0,
                                C.cast(C.c_void_p(h_out.data_ptr()), _abi.U8P), diags, None))
-for rep in range(4):
+res_t = []
+for rep in range(int(os.environ.get("REPS", "4"))):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     h = C.c_void_p()
     dev.check(lib.ccw_ti_create(dev.handle, ti_a.ctypes.data_as(_abi.U8P), 500, 500, 3, 2, 0, C.byref(h)))
@@ -29,5 +30,8 @@ for rep in range(4):
     t_b = dev.last_timing()
     lib.ccw_ti_destroy(h)
     torch.cuda.synchronize(); t4 = time.perf_counter()
+    res_t.append((t4 - t0) * 1e3)
+    if os.environ.get("QUIET"): continue
     print("ti_create %.3f ms | simulate(first on handle) %.3f ms (device %.3f, host_prep %.3f) | simulate(kept handle) %.3f ms (device %.3f) | destroy %.3f ms | d2h %d B" % (
         (t1 - t0) * 1e3, (t2 - t1) * 1e3, t["total_ms"], t["host_prep_ms"], (t3 - t2) * 1e3, t_b["total_ms"], (t4 - t3) * 1e3, t["d2h_bytes"]), flush=True)
+print("e2e step ms: median %.3f min %.3f (%s)" % (sorted(res_t)[len(res_t) // 2], min(res_t), " ".join(f"{k}={os.environ[k]}" for k in ("STREAM_BANDS", "PLACE_THREADS", "CCW_STREAM_TAIL") if k in os.environ)))
