@@ -58,6 +58,87 @@ __global__ void hd_scatter_kernel(const int32_t* __restrict__ hd, int n_hd, uint
     if (i < n_hd) plane[static_cast<size_t>(hd[3 * i]) * ww + hd[3 * i + 1]] = static_cast<uint8_t>(hd[3 * i + 2]);
 }
 
+// Hard-data CSR per stride-lattice cell (a placement's footprint origin):
+// entries (footprint cell r * T + c) << 8 | facies.  Count, scan, fill; the
+// order inside a cell is free (the conditional choice sums mismatches).
+__device__ __forceinline__ void hd_cells(const int32_t* hd, int i, int T, int stride, int nlr, int nlc, int& qr0,
+                                         int& qr1, int& qc0, int& qc1) {
+    const int r = hd[3 * i], c = hd[3 * i + 1];
+    qr0 = max(0, (r - T + 1 + stride - 1) / stride);
+    qc0 = max(0, (c - T + 1 + stride - 1) / stride);
+    qr1 = min(nlr - 1, r / stride);
+    qc1 = min(nlc - 1, c / stride);
+}
+
+__global__ void hd_count_kernel(const int32_t* __restrict__ hd, int n, int T, int stride, int nlr, int nlc,
+                                int32_t* __restrict__ cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int qr0, qr1, qc0, qc1;
+    hd_cells(hd, i, T, stride, nlr, nlc, qr0, qr1, qc0, qc1);
+    const int r = hd[3 * i], c = hd[3 * i + 1];
+    for (int qr = qr0; qr <= qr1; ++qr)
+        for (int qc = qc0; qc <= qc1; ++qc)
+            if (r >= qr * stride && r < qr * stride + T && c >= qc * stride && c < qc * stride + T)
+                atomicAdd(&cnt[static_cast<size_t>(qr) * nlc + qc], 1);
+}
+
+// One CTA: off[0..ncell] (off[q + 1] holds cell q's count on entry) becomes the
+// exclusive scan; cursors = a copy of the starts; lattice[q] = cell q holds data.
+__global__ void hd_scan_kernel(int32_t* __restrict__ off, int ncell, int32_t* __restrict__ cursors,
+                               uint8_t* __restrict__ lattice) {
+    __shared__ int part[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < ncell; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        const int v = q < ncell ? off[q + 1] : 0;
+        if (q < ncell) lattice[q] = v > 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) part[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int p = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, p, o);
+                if (lane >= o) p += y;
+            }
+            part[lane] = p;
+        }
+        __syncthreads();
+        const int incl = x + (wid > 0 ? part[wid - 1] : 0) + carry;
+        if (q < ncell) {
+            off[q + 1] = incl;
+            cursors[q] = incl - v;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) off[0] = 0;
+}
+
+__global__ void hd_fill_kernel(const int32_t* __restrict__ hd, int n, int T, int stride, int nlr, int nlc,
+                               int32_t* __restrict__ cursors, uint32_t* __restrict__ ent) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int qr0, qr1, qc0, qc1;
+    hd_cells(hd, i, T, stride, nlr, nlc, qr0, qr1, qc0, qc1);
+    const int r = hd[3 * i], c = hd[3 * i + 1], v = hd[3 * i + 2];
+    for (int qr = qr0; qr <= qr1; ++qr)
+        for (int qc = qc0; qc <= qc1; ++qc)
+            if (r >= qr * stride && r < qr * stride + T && c >= qc * stride && c < qc * stride + T) {
+                const int at = atomicAdd(&cursors[static_cast<size_t>(qr) * nlc + qc], 1);
+                ent[at] = (static_cast<uint32_t>((r - qr * stride) * T + (c - qc * stride)) << 8) | static_cast<uint32_t>(v);
+            }
+}
+
 // Rebuild (and hard-data overwrite) the output cells of rows [y0, y1) x columns
 // [x0, x1) of realization r.  With the source-block map, one thread per
 // coarse block: one map entry, then the B x B TI patch (BT = B for 2/4/8; 0 =
@@ -451,36 +532,9 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     // hard data per lattice cell (placements sit on the stride lattice for
     // every raster path): CSR lists of (cell in footprint, facies), so the
-    // conditional choice reads only the cells that hold data
-    std::vector<uint8_t> lattice_hd;
-    std::vector<int32_t> hd_off;
-    std::vector<uint32_t> hd_ent;
-    if (hd && n_hd > 0) {
-        const size_t ncell = static_cast<size_t>(nlr) * nlc;
-        lattice_hd.assign(ncell, 0);
-        hd_off.assign(ncell + 1, 0);
-        auto each_cell = [&](int i, auto&& fn) {
-            const int r = hd[3 * i], c = hd[3 * i + 1];
-            const int qr0 = std::max(0, (r - T + 1 + stride - 1) / stride);
-            const int qc0 = std::max(0, (c - T + 1 + stride - 1) / stride);
-            for (int qr = qr0; qr <= std::min(nlr - 1, r / stride); ++qr)
-                for (int qc = qc0; qc <= std::min(nlc - 1, c / stride); ++qc)
-                    if (r >= qr * stride && r < qr * stride + T && c >= qc * stride && c < qc * stride + T)
-                        fn(static_cast<size_t>(qr) * nlc + qc, r - qr * stride, c - qc * stride, hd[3 * i + 2]);
-        };
-        for (int i = 0; i < n_hd; ++i)
-            each_cell(i, [&](size_t q, int, int, int) { ++hd_off[q + 1]; });
-        for (size_t q = 0; q < ncell; ++q) {
-            lattice_hd[q] = hd_off[q + 1] > 0;
-            hd_off[q + 1] += hd_off[q];
-        }
-        hd_ent.resize(hd_off[ncell]);
-        std::vector<int32_t> fill(hd_off.begin(), hd_off.end() - 1);
-        for (int i = 0; i < n_hd; ++i)
-            each_cell(i, [&](size_t q, int lr, int lc, int v) {
-                hd_ent[fill[q]++] = (static_cast<uint32_t>(lr * T + lc) << 8) | static_cast<uint32_t>(v);
-            });
-    }
+    // conditional choice reads only the cells that hold data -- built on the
+    // device (hd_count / hd_scan / hd_fill kernels below)
+    const bool have_hd = hd && n_hd > 0;
     int max_key = 0;
     for (int v = 0; v < 8; ++v)
         if (have[v]) max_key = std::max(max_key, keymul * (variants[v].n_outer - 1) + variants[v].n_inner - 1);
@@ -558,6 +612,27 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     EventTimer tm{ctx, {}, {}, 0};
     cudaEvent_t ev_sched = tm.get();
     CCW_CUDA(cudaEventRecord(ev_sched, st));
+    int32_t* d_hdl = nullptr;
+    uint8_t* d_lat = nullptr;
+    const int32_t* P_hd_off = nullptr;
+    const uint32_t* P_hd_ent = nullptr;
+    if (have_hd) {
+        const size_t ncell = static_cast<size_t>(nlr) * nlc;
+        const int cover = (T + stride - 1) / stride;  // lattice positions per axis covering one cell
+        d_hdl = reinterpret_cast<int32_t*>(ctx->ops_e.get(sizeof(int32_t) * 3 * n_hd));
+        CCW_CUDA(cudaMemcpyAsync(d_hdl, hd, sizeof(int32_t) * 3 * n_hd, cudaMemcpyHostToDevice, st));
+        int32_t* d_off = ctx->hdoff.as<int32_t>(2 * (ncell + 1));  // offsets, then the fill cursors
+        uint32_t* d_ent = ctx->hdent.as<uint32_t>(std::max<size_t>(1, static_cast<size_t>(n_hd) * cover * cover));
+        d_lat = ctx->lattice.as<uint8_t>(ncell);
+        CCW_CUDA(cudaMemsetAsync(d_off, 0, sizeof(int32_t) * 2 * (ncell + 1), st));
+        const unsigned nb = static_cast<unsigned>((n_hd + 255) / 256);
+        hd_count_kernel<<<nb, 256, 0, st>>>(d_hdl, n_hd, T, stride, nlr, nlc, d_off + 1);
+        hd_scan_kernel<<<1, 1024, 0, st>>>(d_off, static_cast<int>(ncell), d_off + ncell + 1, d_lat);
+        hd_fill_kernel<<<nb, 256, 0, st>>>(d_hdl, n_hd, T, stride, nlr, nlc, d_off + ncell + 1, d_ent);
+        CCW_CUDA(cudaGetLastError());
+        P_hd_off = d_off;
+        P_hd_ent = d_ent;
+    }
     Job* d_jobs = ctx->jobs.as<Job>(total_jobs);
     {
         const size_t nstage = static_cast<size_t>(n_real) * nkeys + n_real;
@@ -571,11 +646,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                                  cudaMemcpyHostToDevice, st));
         SP.vid = d_roff + static_cast<size_t>(n_real) * nkeys;
         SP.roff = d_roff;
-        if (!lattice_hd.empty()) {
-            uint8_t* d_lat = ctx->lattice.as<uint8_t>(lattice_hd.size());
-            CCW_CUDA(cudaMemcpyAsync(d_lat, lattice_hd.data(), lattice_hd.size(), cudaMemcpyHostToDevice, st));
-            SP.lattice_hd = d_lat;
-        }
+        if (d_lat) SP.lattice_hd = d_lat;
         SP.err = d_err;
         SP.n_real = n_real;
         SP.nkeys = nkeys;
@@ -606,23 +677,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         CCW_CUDA(cudaMemsetAsync(d_work, 0, plane * n_real, st));
     }
     uint8_t* d_hd = nullptr;
-    const int32_t* P_hd_off = nullptr;
-    const uint32_t* P_hd_ent = nullptr;
-    if (hd && n_hd > 0) {
+    if (have_hd) {
         d_hd = ctx->hd.as<uint8_t>(plane);
         CCW_CUDA(cudaMemsetAsync(d_hd, kNoDatum, plane, st));
-        int32_t* d_hdl = reinterpret_cast<int32_t*>(ctx->ops_e.get(sizeof(int32_t) * 3 * n_hd));
-        CCW_CUDA(cudaMemcpyAsync(d_hdl, hd, sizeof(int32_t) * 3 * n_hd, cudaMemcpyHostToDevice, st));
         hd_scatter_kernel<<<(n_hd + 255) / 256, 256, 0, st>>>(d_hdl, n_hd, d_hd, ww);
         CCW_CUDA(cudaGetLastError());
-        int32_t* d_off = ctx->hdoff.as<int32_t>(hd_off.size());
-        uint32_t* d_ent = ctx->hdent.as<uint32_t>(std::max<size_t>(1, hd_ent.size()));
-        CCW_CUDA(cudaMemcpyAsync(d_off, hd_off.data(), sizeof(int32_t) * hd_off.size(), cudaMemcpyHostToDevice, st));
-        if (!hd_ent.empty())
-            CCW_CUDA(cudaMemcpyAsync(d_ent, hd_ent.data(), sizeof(uint32_t) * hd_ent.size(),
-                                     cudaMemcpyHostToDevice, st));
-        P_hd_off = d_off;
-        P_hd_ent = d_ent;
     }
     const int sld = (npos + 3) & ~3;  // (score rows exist only for the block-select path)
     const size_t score_budget = (static_cast<size_t>(512) << 20) / G;

@@ -11,10 +11,17 @@ cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1, n_realizations=n, master_seed=20240
 seeds = np.array([cs.mix64(20240441, r + 1) for r in range(n)], np.uint64)
 c = cfg.to_c(); d_out = torch.empty(n * 16 * 10**6, dtype=torch.uint8, device="cuda:0")
 diags = (_abi.DiagC * n)()
-dev.set_profiling(True)
+for _k in ("groups", "wave", "wave_cs"):
+    if os.environ.get(_k.upper()): dev.set_option(_k, int(os.environ[_k.upper()]))
+dev.set_profiling(os.environ.get("PROF", "1") == "1")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
+stream = torch.cuda.ExternalStream(dev.stream_ptr, device=torch.device("cuda", 0))
 for i in range(int(os.environ.get("REPS", "3"))):
+    if os.environ.get("FLUSH"):
+        with torch.cuda.stream(stream):
+            flush.zero_()
     dev.check(lib.ccw_simulate_device(dev.handle, tih.handle, C.byref(c), seeds.ctypes.data_as(_abi.U64P), n,
                                       hd.ctypes.data_as(_abi.I32P), hd.shape[0], C.c_void_p(d_out.data_ptr()), diags))
     torch.cuda.synchronize()
     t = dev.last_timing()
-    print("total_ms %.2f rescored %d bulk_jobs %d" % (t["total_ms"], t["rescored"], t["bulk_jobs"]))
+    print("total_ms %.2f rescored %d bulk_jobs %d ccf_ms %.2f select_ms %.2f launches %d" % (t["total_ms"], t["rescored"], t["bulk_jobs"], t["ccf_ms"], t["select_ms"], t["launches"]))
