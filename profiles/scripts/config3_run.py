@@ -15,7 +15,7 @@ else:
     nf = 5
 dev = cs.default_device()
 ti = c3.TrainingImage3D(ti_a, nf, cfg.dwt_level, dev)
-dev.set_profiling(True)
+dev.set_profiling(os.environ.get("PROF", "1") == "1")
 for i in range(int(os.environ.get("REPS", "2"))):
     c3.simulate3d_ensemble(ti, cfg)
     t = dev.last_timing()
