@@ -105,6 +105,8 @@ struct SimParams {
     // fused OR prep: the select of wave w prepares the placements of wave w+1
     // once both of their wave-w dependencies have pasted (null: separate launch)
     int* depcnt;             // per next-wave slot: dependencies that have pasted
+    int* depflag;            // dependency flags (option flagprep): per flat job, the previous-wave
+                             // placements it reads that have pasted (select -> OR prep of the next wave)
     int next_j0;             // flat index of the next wave's first job (this group)
     int8_t* n_wts8;          // next wave's prep outputs (the other parity buffers)
     double* n_tm64;

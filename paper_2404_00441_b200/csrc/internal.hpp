@@ -232,6 +232,7 @@ struct Options {
     int place_threads = 0;     // host unpack threads (0 = auto)
     int wave = 0;              // fused wave kernel (wave.cu) where it applies (experimental)
     int wave_cs = 0;           // its CTAs per cluster (0 = auto)
+    int flagprep = 1;          // OR prep waits on per-placement dependency flags, not the whole select
 };
 
 // Known option names (for ccw_ctx_set_option); returns nullptr if unknown.
@@ -250,6 +251,7 @@ inline int* option_slot(Options& o, const std::string& name) {
     if (name == "place_threads") return &o.place_threads;
     if (name == "wave") return &o.wave;
     if (name == "wave_cs") return &o.wave_cs;
+    if (name == "flagprep") return &o.flagprep;
     return nullptr;
 }
 
@@ -275,7 +277,7 @@ struct ccw_ctx {
     ccwgpu::Options opt;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf wave_w, cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf wave_w, depflag, cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, tmaxnu, jvar, ops_a, ops_b, ops_c, ops_d, ops_e;
     long long mtab_key = -1;  // (Tc, OVc, nch) of the mask tables in mtab
     ccwgpu::HostBuf h_stage;

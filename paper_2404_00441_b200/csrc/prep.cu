@@ -45,13 +45,43 @@ void build_pyramid(ccw_ti* ti, cudaStream_t s) {
     CCW_CUDA(cudaGetLastError());
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Dependency flags (P.depflag, option flagprep): a placement's prep starts as
+// soon as the previous-wave placements it reads have pasted (their select
+// CTAs count them here after the map writes), not when the whole previous
+// launch has ended -- the prep overlaps the select's tail.  The launch has
+// one extra CTA that waits for the previous launch in full, so this
+// launch's completion still implies it (the screen that follows rewrites
+// the score rows that launch reads).
 __global__ void or_prep_src_kernel(SimParams P, const Job* __restrict__ jobs, int job0) {
     pdl_trigger();
     const int slot = blockIdx.x;
+    if (P.depflag && slot == static_cast<int>(gridDim.x) - 1) {
+        pdl_wait();
+        return;
+    }
     const Job jb = jobs[job0 + slot];
     if (P.jvar && threadIdx.x == 0) P.jvar[slot] = static_cast<int8_t>(mask_variant(jb.shape, jb.vleft, jb.htop));
     tl_mark(P.tl, 2);
-    pdl_wait();
+    if (P.depflag && jb.ndep > 0) {
+        if (threadIdx.x == 0) {
+            const int* f = P.depflag + job0 + slot;
+            long long spins = 0;
+            while (ld_acquire(f) < jb.ndep) {
+                __nanosleep(32);
+                if (++spins > (1ll << 27)) __trap();  // (a missing signal is a bug: fail, do not hang)
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    } else {
+        pdl_wait();
+    }
     tl_mark(P.tl, 0);
     prep_src_job(P, jb, slot, P.wts8, P.tm64, P.cjob);
     tl_mark(P.tl, 1);

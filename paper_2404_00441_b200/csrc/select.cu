@@ -1374,6 +1374,14 @@ __global__ void __launch_bounds__(FS_T, CCW_FS_MINB)
     paste_job<FS_T>(P, jb, gj, fr, fc, tid);
     PCLK(6);
     prep_dependents(P, jobs, jb, &S.misc[5]);
+    if (P.depflag) {  // the next wave's OR prep of each dependent waits for these map writes
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            if (jb.dep0 >= 0) atomicAdd(&P.depflag[jb.dep0], 1);
+            if (jb.dep1 >= 0) atomicAdd(&P.depflag[jb.dep1], 1);
+        }
+    }
     PCLK(7);
     if (tid == 0) {
         P.chosen[2 * gj] = fr;

@@ -873,6 +873,16 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     if (bulk_smem)
         CCW_CUDA(cudaFuncSetAttribute(select_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(bulk_smem)));
+    // dependency flags between a wave's select and the next wave's OR prep
+    // (option flagprep; or_prep_src_kernel): needs every paste in the select
+    // (no bulk deferrals), the raster neighbours of keymul 2 and the map path
+    const bool flag_prep = ctx->opt.flagprep && warp_select && keymul == 2 && d_src && !bulk_launch && !use_wave &&
+                           debug_env("CCW_FUSE_PREP") == nullptr;
+    if (flag_prep) {
+        int* d_depflag = ctx->depflag.as<int>(total_jobs);
+        CCW_CUDA(cudaMemsetAsync(d_depflag, 0, sizeof(int) * total_jobs, st));
+        P.depflag = d_depflag;
+    }
     std::vector<SimParams> GP(G, P);
     for (int g = 0; g < G; ++g) {
         GP[g].scores = d_scores + g * maxj * sld;
@@ -1430,8 +1440,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 if (!first_wave) {
                     Q.tl = tl_next(w, g, 0);
                     if (!fuse_prep) {  // (fused: prepared by the previous wave's select)
-                        if (d_src)
-                            launch_pdl(or_prep_src_kernel, dim3(nj), dim3(128), 0, gs, Q,
+                        if (d_src)  // (+1 CTA with flag_prep: it waits for the previous launch in full)
+                            launch_pdl(or_prep_src_kernel, dim3(nj + (flag_prep ? 1 : 0)), dim3(128), 0, gs, Q,
                                        static_cast<const Job*>(d_jobs), static_cast<int>(j0));
                         else
                             launch_pdl(or_prep_kernel, dim3(nj), dim3(128), 0, gs, Q,
