@@ -3,6 +3,8 @@
 // plan and the mt19937_64 draw schedule.  Messages match the reference's
 // exception texts (tests match substrings such as "overlap" / "template").
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -319,6 +321,7 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
     for (cudaStream_t s : ctx->copy_streams) cudaStreamSynchronize(s);
     ccwgpu::nccl_comm_destroy(ctx->nccl_comm);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->upload_done) cudaEventDestroy(ctx->upload_done);
     for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
     for (cudaStream_t s : ctx->copy_streams) cudaStreamDestroy(s);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -432,6 +435,45 @@ uint64_t ccw_mix64(uint64_t seed, uint64_t index) {  // rng.hpp:11-16
     return z ^ (z >> 31);
 }
 
+// A large host upload: the context's host threads copy chunks into pinned
+// staging and each chunk leaves with its own async copy as soon as it is
+// staged (a pageable cudaMemcpy goes through the driver's bounce buffer one
+// chunk at a time, ~4x slower for a 32 MB 3D training image).  The staging
+// buffer is reused by the next upload only after these copies complete.
+static void upload_host(ccw_ctx* ctx, void* d, const void* h, size_t n) {
+    constexpr size_t kSmall = 1u << 20, kChunk = 2u << 20;
+    if (n < kSmall) {
+        CCW_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, ctx->stream));
+        return;
+    }
+    if (ctx->upload_done) CCW_CUDA(cudaEventSynchronize(ctx->upload_done));
+    uint8_t* stage = static_cast<uint8_t*>(ctx->h_upload.get(n));
+    const int nchunk = static_cast<int>((n + kChunk - 1) / kChunk);
+    // chunks are staged in parallel; copies are issued in chunk order on the
+    // context stream as each one is ready
+    std::vector<std::atomic<int>> ready(nchunk);
+    for (auto& r : ready) r.store(0);
+    const int device = ctx->device;
+    std::thread issuer([&] {
+        cudaSetDevice(device);
+        for (int i = 0; i < nchunk; ++i) {
+            while (!ready[i].load(std::memory_order_acquire)) std::this_thread::yield();
+            const size_t o = static_cast<size_t>(i) * kChunk;
+            cudaMemcpyAsync(static_cast<uint8_t*>(d) + o, stage + o, std::min(kChunk, n - o),
+                            cudaMemcpyHostToDevice, ctx->stream);
+        }
+    });
+    ctx->pool.run(nchunk, [&](int i) {
+        const size_t o = static_cast<size_t>(i) * kChunk;
+        std::memcpy(stage + o, static_cast<const uint8_t*>(h) + o, std::min(kChunk, n - o));
+        ready[i].store(1, std::memory_order_release);
+    });
+    issuer.join();
+    if (!ctx->upload_done) CCW_CUDA(cudaEventCreateWithFlags(&ctx->upload_done, cudaEventDisableTiming));
+    CCW_CUDA(cudaEventRecord(ctx->upload_done, ctx->stream));
+    CCW_CUDA(cudaGetLastError());
+}
+
 static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device_ptr, int h,
                                  int w, int nf, int levels, int mode, ccw_ti** out) {
     if (!ctx || !out) return CCW_ERR_GENERIC;
@@ -450,13 +492,6 @@ static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device
                        fmt("training image %dx%d smaller than one 2^dwt_level = %d block", h, w,
                            1 << std::min(levels, 30)));
         if (mode != 0 && mode != 1) throw Fail(CCW_ERR_CONFIG, "facies_mode: unknown");
-        if (!device_ptr) {
-            // grid.hpp:36-40 code-range check (the device path trusts its caller)
-            for (size_t i = 0; i < static_cast<size_t>(h) * w; ++i)
-                if (cells[i] >= nf)
-                    throw Fail(CCW_ERR_BOUNDS, fmt("cell %zu holds code %d outside [0, %d)", i,
-                                                   static_cast<int>(cells[i]), nf));
-        }
         ti->ctx = ctx;
         ti->device = ctx->device;
         ti->h = h;
@@ -496,9 +531,16 @@ static ccw_status ti_create_impl(ccw_ctx* ctx, const uint8_t* cells, bool device
             key = ccwgpu::mix_key(key ^ (next_id.fetch_add(1) << 1 | 1));
         }
         ti->key = key;
-        CCW_CUDA(cudaMemcpyAsync(ti->d_codes, cells, n,
-                                 device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                 ctx->stream));
+        if (device_ptr) {
+            CCW_CUDA(cudaMemcpyAsync(ti->d_codes, cells, n, cudaMemcpyDeviceToDevice, ctx->stream));
+        } else {
+            upload_host(ctx, ti->d_codes, cells, n);
+            // grid.hpp:36-40 code-range check, on the device (the device-pointer path trusts its caller)
+            const size_t bad = ccwgpu::first_bad_code(ti->d_codes, n, nf, ctx->stream, ctx->chk.as<unsigned long long>(1));
+            if (bad < n)
+                throw Fail(CCW_ERR_BOUNDS, fmt("cell %zu holds code %d outside [0, %d)", bad,
+                                               static_cast<int>(cells[bad]), nf));
+        }
         ccwgpu::build_pyramid(ti, ctx->stream);
     });
     if (st != CCW_OK) {
@@ -715,9 +757,6 @@ ccw_status ccw_ti3d_create(ccw_ctx* ctx, const uint8_t* cells, int d0, int d1, i
         if (levels < 1 || levels > 10) throw Fail(CCW_ERR_DIMENSION, "decomposition level must be in [1, 10]");
         if (!cells) throw Fail(CCW_ERR_GENERIC, "null cells");
         const size_t n = static_cast<size_t>(d0) * d1 * d2;
-        for (size_t i = 0; i < n; ++i)
-            if (cells[i] >= nf)
-                throw Fail(CCW_ERR_BOUNDS, fmt("cell %zu holds code %d outside [0, %d)", i, static_cast<int>(cells[i]), nf));
         const int b = 1 << levels;
         ti->ctx = ctx;
         ti->device = ctx->device;
@@ -735,7 +774,10 @@ ccw_status ccw_ti3d_create(ccw_ctx* ctx, const uint8_t* cells, int d0, int d1, i
         ti->d_codes = static_cast<uint8_t*>(ccwgpu::cache_alloc(ti->device, n));
         ti->d_pk = static_cast<int32_t*>(
             ccwgpu::cache_alloc(ti->device, sizeof(int32_t) * nc * (ti->mode == 0 ? 1 : ti->nscr)));
-        CCW_CUDA(cudaMemcpyAsync(ti->d_codes, cells, n, cudaMemcpyHostToDevice, ctx->stream));
+        upload_host(ctx, ti->d_codes, cells, n);
+        const size_t bad = ccwgpu::first_bad_code(ti->d_codes, n, nf, ctx->stream, ctx->chk.as<unsigned long long>(1));  // (grid.hpp:36-40)
+        if (bad < n)
+            throw Fail(CCW_ERR_BOUNDS, fmt("cell %zu holds code %d outside [0, %d)", bad, static_cast<int>(cells[bad]), nf));
         ccwgpu::build_pyramid3d(ti, ctx->stream);
     });
     if (st != CCW_OK) {

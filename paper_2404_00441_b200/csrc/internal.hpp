@@ -122,6 +122,8 @@ inline uint64_t mix_key(uint64_t z) {
 // training-image buffers come and go with every ccw_ti; returning them to
 // the driver (cudaFree) would unmap memory and stall on every destroy.
 void* cache_alloc(int device, size_t bytes);
+// device code-range check of an uploaded grid: the first index holding a code >= nf, n if none (ops.cu)
+size_t first_bad_code(const uint8_t* d, size_t n, int nf, cudaStream_t st, unsigned long long* d_scratch);
 void cache_free(void* p);
 
 // Persistent host worker pool (one per context): run(n, fn) calls fn(i) for
@@ -277,11 +279,13 @@ struct ccw_ctx {
     ccwgpu::Options opt;
     ccw_timing timing{};
     // scratch
-    ccwgpu::DevBuf wave_w, depflag, cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
+    ccwgpu::DevBuf wave_w, depflag, chk, cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
         stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, tmaxnu, jvar, ops_a, ops_b, ops_c, ops_d, ops_e;
     long long mtab_key = -1;  // (Tc, OVc, nch) of the mask tables in mtab
     ccwgpu::HostBuf h_stage;
     ccwgpu::HostBuf h_out_stage;  // pinned landing zone when the caller's result buffer is pageable
+    ccwgpu::HostBuf h_upload;     // pinned staging of large host uploads (upload_host, abi.cpp)
+    cudaEvent_t upload_done = nullptr;  // the last staged upload's copies
     ccwgpu::HostPool pool;
     std::vector<cudaEvent_t> ev_pool;
     std::vector<cudaStream_t> gstreams;  // realization-group streams

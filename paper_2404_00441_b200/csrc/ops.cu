@@ -356,4 +356,43 @@ void op_select_conditional(ccw_ctx* ctx, const int32_t* rows, const int32_t* col
     *mismatches = o[1];
 }
 
+// First cell whose code is >= nf (n if none): the code-range check of an
+// uploaded grid (grid.hpp:36-40), on the device.
+__global__ void first_bad_code_kernel(const uint8_t* __restrict__ c, size_t n, int nf,
+                                      unsigned long long* __restrict__ first) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x * 16;
+    for (size_t i0 = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; i0 < n; i0 += stride) {
+        if (i0 + 16 <= n && (reinterpret_cast<uintptr_t>(c + i0) & 15) == 0) {
+            const uint4 v = *reinterpret_cast<const uint4*>(c + i0);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (static_cast<int>((w[k >> 2] >> (8 * (k & 3))) & 255u) >= nf) {
+                    atomicMin(first, static_cast<unsigned long long>(i0 + k));
+                    break;
+                }
+        } else {
+            for (size_t i = i0; i < n && i < i0 + 16; ++i)
+                if (c[i] >= nf) {
+                    atomicMin(first, static_cast<unsigned long long>(i));
+                    break;
+                }
+        }
+    }
+}
+
+size_t first_bad_code(const uint8_t* d, size_t n, int nf, cudaStream_t st, unsigned long long* d_first) {
+    if (nf >= 256 || n == 0) return n;
+    const unsigned long long init = n;
+    CCW_CUDA(cudaMemcpyAsync(d_first, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const size_t threads = (n + 15) / 16;
+    const unsigned nb = static_cast<unsigned>(std::min<size_t>((threads + 255) / 256, 148 * 16));
+    first_bad_code_kernel<<<nb, 256, 0, st>>>(d, n, nf, d_first);
+    CCW_CUDA(cudaGetLastError());
+    unsigned long long got = n;
+    CCW_CUDA(cudaMemcpyAsync(&got, d_first, sizeof(got), cudaMemcpyDeviceToHost, st));
+    CCW_CUDA(cudaStreamSynchronize(st));
+    return static_cast<size_t>(got);
+}
+
 }  // namespace ccwgpu
