@@ -284,6 +284,8 @@ def run_ours(args):
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
+    if os.environ.get("CCW_BENCH_STEPS"):  # diagnostics: every timed step's device time
+        print("step ms: " + " ".join(f"{t:.3f}" for t in step_ms), file=sys.stderr)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device=f"cuda:{local}")
