@@ -234,3 +234,47 @@ def test_wave_kernel_paths(oracle, cs_):
                 assert r.diagnostics.pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
     finally:
         dev.close()
+
+
+def test_flagprep_off_equals_on(oracle):
+    """The dependency-flag OR prep (option flagprep, default on: a prep CTA
+    waits only on the two previous-wave placements it reads) and the whole-
+    launch wait give the same realizations, equal to the restatement."""
+    ti_a = synth.config1_ti()
+    ti = cs.CategoricalGrid(500, 500, 3, ti_a)
+    d = dict(sg_height=520, sg_width=616, template_size=64, overlap=16, dwt_level=2, candidates=5)
+    seeds = [cs.mix64(23, r + 1) for r in range(6)]
+    dev = cs.default_device()
+    cs.simulate_batch(ti, to_cfg(d), seeds[:1])  # (the bulk-off plan memory: flag prep needs it)
+    res_on = cs.simulate_batch(ti, to_cfg(d), seeds)
+    with dev.options(flagprep=0):
+        res_off = cs.simulate_batch(ti, to_cfg(d), seeds)
+    for s, a, b in zip(seeds, res_on, res_off):
+        assert np.array_equal(a.realization.cells, b.realization.cells), s
+    for s, r in zip(seeds[:2], res_on[:2]):
+        o = oracle.simulate_one(ti_a, 3, pyoracle.Cfg(**d), None, seed=s)
+        assert np.array_equal(r.realization.cells, o["realization"]), s
+
+
+def test_ti_upload_code_range_checked_on_device():
+    """Large training images go through the staged upload and the device
+    code-range check (grid.hpp:36-40): the first bad cell and its code are
+    reported exactly as the host check did."""
+    import ctypes as C
+    from paper_2404_00441_b200 import _abi
+    dev = cs.default_device()
+    lib = _abi.lib()
+    a = np.zeros((1500, 1500), np.uint8)
+    a[700, 1234] = 7
+    a[900, 3] = 5
+    h = C.c_void_p()
+    with pytest.raises(cs.BoundsError, match=r"cell 1051234 holds code 7 outside \[0, 3\)"):
+        dev.check(lib.ccw_ti_create(dev.handle, a.ctypes.data_as(_abi.U8P), 1500, 1500, 3, 2, 0, C.byref(h)))
+    b = np.zeros((64, 96, 200), np.uint8)
+    b[10, 20, 30] = 9
+    with pytest.raises(cs.BoundsError, match=r"cell 196030 holds code 9 outside \[0, 4\)"):
+        dev.check(lib.ccw_ti3d_create(dev.handle, b.ctypes.data_as(_abi.U8P), 64, 96, 200, 4, 2, C.byref(h)))
+    # a valid large TI through the same path simulates like the small-TI path
+    a[:] = (np.arange(1500 * 1500).reshape(1500, 1500) // 37 % 3).astype(np.uint8)
+    dev.check(lib.ccw_ti_create(dev.handle, a.ctypes.data_as(_abi.U8P), 1500, 1500, 3, 2, 0, C.byref(h)))
+    lib.ccw_ti_destroy(h)
