@@ -454,13 +454,15 @@ static void upload_host(ccw_ctx* ctx, void* d, const void* h, size_t n) {
     std::vector<std::atomic<int>> ready(nchunk);
     for (auto& r : ready) r.store(0);
     const int device = ctx->device;
+    cudaError_t issue_err = cudaSuccess;  // (the issuer's first error, rethrown by the caller)
     std::thread issuer([&] {
         cudaSetDevice(device);
         for (int i = 0; i < nchunk; ++i) {
             while (!ready[i].load(std::memory_order_acquire)) std::this_thread::yield();
             const size_t o = static_cast<size_t>(i) * kChunk;
-            cudaMemcpyAsync(static_cast<uint8_t*>(d) + o, stage + o, std::min(kChunk, n - o),
-                            cudaMemcpyHostToDevice, ctx->stream);
+            const cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(d) + o, stage + o, std::min(kChunk, n - o),
+                                                  cudaMemcpyHostToDevice, ctx->stream);
+            if (e != cudaSuccess && issue_err == cudaSuccess) issue_err = e;
         }
     });
     ctx->pool.run(nchunk, [&](int i) {
@@ -469,6 +471,8 @@ static void upload_host(ccw_ctx* ctx, void* d, const void* h, size_t n) {
         ready[i].store(1, std::memory_order_release);
     });
     issuer.join();
+    if (issue_err != cudaSuccess)
+        throw Fail(CCW_ERR_CUDA, std::string("cudaMemcpyAsync (staged upload): ") + cudaGetErrorString(issue_err));
     if (!ctx->upload_done) CCW_CUDA(cudaEventCreateWithFlags(&ctx->upload_done, cudaEventDisableTiming));
     CCW_CUDA(cudaEventRecord(ctx->upload_done, ctx->stream));
     CCW_CUDA(cudaGetLastError());
