@@ -776,6 +776,9 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     if (nbox < S) throw Fail(CCW_ERR_CONFIG, "position shards: more shards than 3D screen boxes");
     const int bps = (nbox + S - 1) / S;
 
+    const bool host_t = debug_env("CCW_HOSTT") != nullptr;
+    auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(); };
+    const double t_plan = host_t ? host_ms() : 0.0;
     // ---- device buffers ----
     const size_t wvol = static_cast<size_t>(g.W[0]) * g.W[1] * g.W[2];
     uint8_t* d_work = ctx->work.as<uint8_t>(wvol * n_real);
@@ -863,6 +866,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     CCW_CUDA(cudaEventCreate(&ev1));
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ccf_ev;
     CCW_CUDA(cudaEventRecord(ev0, st));
+    const double t_ev0 = host_t ? host_ms() : 0.0;
     int64_t launches = 0, ccf_launches = 0;
     double ccf_flop = 0;
     for (int w = 0; w <= max_key; ++w) {
@@ -930,6 +934,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         }
     }
     CCW_CUDA(cudaEventRecord(ev1, st));
+    if (host_t) fprintf(stderr, "3D host ms: plan %.3f ev0 %.3f launched %.3f\n", t_plan, t_ev0, host_ms());
     if (h_out) CCW_CUDA(cudaMemcpyAsync(h_out, fin, sgvol * n_real, cudaMemcpyDeviceToHost, st));
     std::vector<int> mism(n_real, 0);
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
