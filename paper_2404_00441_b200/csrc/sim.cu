@@ -1302,7 +1302,10 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     for (int w = 0; w <= max_key; ++w) {
         for (int g = 0; g < G; ++g) {
             cudaStream_t gs = ctx->gstreams[g];
-            const int par = fuse_prep ? (w & 1) : 0;
+            // parity halves of the prep outputs: with the fused prep or the flag
+            // prep, wave w+1's prep runs while wave w's select may still read its
+            // fp64 templates (rescoring, helpers), so the waves alternate halves
+            const int par = (fuse_prep || flag_prep) ? (w & 1) : 0;
             SimParams Q = GPP[g][par];
             Q.next_j0 = static_cast<int>(wave_off[g][std::min(w + 1, nkeys)]);
             for (size_t j0 = wave_off[g][w]; j0 < wave_off[g][w + 1]; j0 += maxj) {
