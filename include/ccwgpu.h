@@ -221,6 +221,18 @@ CCW_API ccw_status ccw_simulate(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* 
 CCW_API ccw_status ccw_simulate_device(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
                                const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
                                uint8_t* d_out, ccw_diag* diag);
+
+/* Asynchronous ccw_simulate_device, without diagnostics: returns once the
+ * call is enqueued on the context's stream, so consecutive calls overlap one
+ * call's host-side planning with the previous call's device work.  d_out is
+ * complete, ccw_ctx_last_timing covers the call, and an error the device
+ * detects is returned, after ccw_ctx_synchronize (or any later synchronous
+ * call).  Page-locked seeds / hard-data arrays must stay valid until then. */
+CCW_API ccw_status ccw_simulate_device_async(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                                             const uint64_t* seeds, int n_real, const int32_t* hd,
+                                             int n_hd, uint8_t* d_out);
+/* Wait for the context's asynchronous calls and report their errors. */
+CCW_API ccw_status ccw_ctx_synchronize(ccw_ctx* ctx);
 /* simulate_ensemble (simulator.hpp:523-566): seeds mix64(master, r+1), all
  * cfg->n_realizations in one batched call (the reference's `workers` knob is
  * meaningless here and is ignored by the C++ shim, which the reference's

@@ -94,6 +94,8 @@ SIGNATURES = {
                                C.POINTER(DiagC), C.POINTER(TraceC)]),
     "ccw_simulate_device": (C.c_int, [P, P, C.POINTER(SimConfigC), U64P, C.c_int, I32P, C.c_int,
                                       P, C.POINTER(DiagC)]),
+    "ccw_simulate_device_async": (C.c_int, [P, P, C.POINTER(SimConfigC), U64P, C.c_int, I32P, C.c_int, C.c_void_p]),
+    "ccw_ctx_synchronize": (C.c_int, [P]),
     "ccw_simulate_ensemble": (C.c_int, [P, P, C.POINTER(SimConfigC), I32P, C.c_int, U8P,
                                         C.POINTER(DiagC)]),
     "ccw_dwt2_single_f64": (C.c_int, [P, F64P, C.c_int, C.c_int, F64P, F64P, F64P, F64P]),

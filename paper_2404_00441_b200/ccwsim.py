@@ -335,6 +335,11 @@ class Device:
     def set_profiling(self, on: bool) -> None:
         self.check(self._lib.ccw_ctx_set_profiling(self.handle, int(bool(on))))
 
+    def synchronize(self) -> None:
+        """Wait for this context's asynchronous calls (ccw_ctx_synchronize) and raise
+        the first error one of them reported."""
+        self.check(self._lib.ccw_ctx_synchronize(self.handle))
+
     def last_timing(self) -> dict:
         t = _abi.TimingC()
         self.check(self._lib.ccw_ctx_last_timing(self.handle, C.byref(t)))

@@ -322,6 +322,11 @@ void ccw_ctx_destroy(ccw_ctx* ctx) {
     ccwgpu::nccl_comm_destroy(ctx->nccl_comm);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->upload_done) cudaEventDestroy(ctx->upload_done);
+    for (auto& sl : ctx->aslot)
+        for (cudaEvent_t e : {sl.done, sl.t0, sl.t1})
+            if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->stage_ev)
+        if (e) cudaEventDestroy(e);
     for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
     for (cudaStream_t s : ctx->copy_streams) cudaStreamDestroy(s);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -340,8 +345,10 @@ ccw_status ccw_ctx_set_profiling(ccw_ctx* ctx, int enabled) {
 
 ccw_status ccw_ctx_last_timing(ccw_ctx* ctx, ccw_timing* out) {
     if (!ctx || !out) return CCW_ERR_GENERIC;
-    *out = ctx->timing;
-    return CCW_OK;
+    return guarded(ctx, [&] {
+        ccwgpu::async_settle(ctx, true);  // (an asynchronous call's counters)
+        *out = ctx->timing;
+    });
 }
 
 ccw_status ccw_ctx_set_ccf_variant(ccw_ctx* ctx, int variant) {
@@ -621,6 +628,31 @@ ccw_status ccw_simulate_device(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* c
         if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
         ccwgpu::run_simulation(ctx, ti, *cfg, seeds, n_real, hd, n_hd, d_out, nullptr, diag,
                                nullptr);
+    });
+}
+
+ccw_status ccw_simulate_device_async(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config* cfg,
+                                     const uint64_t* seeds, int n_real, const int32_t* hd, int n_hd,
+                                     uint8_t* d_out) {
+    if (!ctx || !ti) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        check_ti_cfg(ti, cfg, hd, n_hd);
+        if (n_real < 1) throw Fail(CCW_ERR_CONFIG, "realizations: must be >= 1");
+        if (!d_out) throw Fail(CCW_ERR_GENERIC, "null output");
+        ccwgpu::run_simulation(ctx, ti, *cfg, seeds, n_real, hd, n_hd, d_out, nullptr, nullptr, nullptr, true);
+    });
+}
+
+ccw_status ccw_ctx_synchronize(ccw_ctx* ctx) {
+    if (!ctx) return CCW_ERR_GENERIC;
+    return guarded(ctx, [&] {
+        CCW_CUDA(cudaStreamSynchronize(ctx->stream));
+        ccwgpu::async_settle(ctx, true);
+        if (!ctx->async_err.empty()) {
+            const std::string e = ctx->async_err;
+            ctx->async_err.clear();
+            throw Fail(CCW_ERR_GENERIC, e);
+        }
     });
 }
 

@@ -297,6 +297,21 @@ struct ccw_ctx {
     // ... and whose last call deferred many placements (a tie storm: the
     // screen then also keeps per-tile non-uniform maxima for the bulk kernel)
     std::map<std::tuple<uint64_t, int, int, int, int>, bool> tie_storm;
+    // asynchronous device calls (ccw_simulate_device_async): two result slots
+    // alternate by call parity; a slot's counters land in pinned memory and are
+    // folded into the timing and the plan memory later (ccwgpu::async_settle)
+    struct AsyncSlot {
+        bool valid = false;
+        cudaEvent_t done = nullptr, t0 = nullptr, t1 = nullptr;
+        ccwgpu::HostBuf res;  // [kNumStats] stats, then the schedule error flag
+        ccw_timing timing{};  // every field but the counters read back
+        std::tuple<uint64_t, int, int, int, int> key{};
+        bool use_wave = false, bulk_launch = false;
+    } aslot[2];
+    int async_par = 0;
+    std::string async_err;     // the first device-side error an async call reported
+    ccwgpu::HostBuf h_stage2;  // second roff staging half (calls alternate)
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};  // the staging half's upload completed
     // candidate-position sharding (ccw_ctx_set_position_shards)
     int shard_nranks = 1, shard_rank = 0, shard_virtual = 1;
     void* nccl_comm = nullptr;  // ncclComm_t when shard_nranks > 1 (or an explicit id was given)
@@ -375,9 +390,10 @@ void nccl_all_gather_bytes(void* comm, const void* send, void* recv, size_t byte
 double measure_ffma_peak(ccw_ctx* ctx);
 double measure_int_peak(ccw_ctx* ctx, int kind);
 void build_pyramid(ccw_ti* ti, cudaStream_t s);
+void async_settle(ccw_ctx* ctx, bool block);
 void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
                     int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out,
-                    ccw_diag* diag, ccw_trace* traces);
+                    ccw_diag* diag, ccw_trace* traces, bool async_call = false);
 
 void build_pyramid3d(ccw_ti3d* ti, cudaStream_t s);
 void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, const uint64_t* seeds, int n_real,

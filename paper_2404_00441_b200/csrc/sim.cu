@@ -485,10 +485,66 @@ void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
 
 }  // namespace
 
+// The per-context plan memory (sim.cu run_simulation): after a call, whether
+// its TI/shape deferred tie groups (bulk kernel on/off) or stormed (keep the
+// select + bulk kernels instead of the wave kernel).
+static void learn_plan(ccw_ctx* ctx, const std::tuple<uint64_t, int, int, int, int>& key, bool use_wave,
+                       bool bulk_launch, const unsigned long long* stats) {
+    if (use_wave) {
+        if (stats[1] > 0 && stats[2] * 50 > stats[1]) ctx->tie_storm[key] = true;
+    } else if (bulk_launch && stats[1] > 0 && stats[3] * 50 > stats[1])  // > 2 % of the screened placements
+        ctx->tie_storm[key] = true;
+    else
+        ctx->tie_storm.erase(key);
+    if (bulk_launch && stats[3] == 0)
+        ctx->bulk_off[key] = true;
+    else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back
+        ctx->bulk_off.erase(key);
+}
+
+// Fold finished asynchronous calls into the context: timing, plan memory and
+// device-side errors (oldest first; block = wait for them).
+void async_settle(ccw_ctx* ctx, bool block) {
+    for (int k = 0; k < 2; ++k) {
+        ccw_ctx::AsyncSlot& sl = ctx->aslot[k == 0 ? ctx->async_par : 1 - ctx->async_par];
+        if (!sl.valid) continue;
+        if (block) {
+            CCW_CUDA(cudaEventSynchronize(sl.done));
+        } else if (cudaEventQuery(sl.done) != cudaSuccess) {
+            cudaGetLastError();
+            break;  // (the newer slot cannot be done before the older one)
+        }
+        const unsigned long long* st = static_cast<const unsigned long long*>(sl.res.p);
+        ccw_timing t = sl.timing;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, sl.t0, sl.t1);
+        t.total_ms = ms;
+        t.rescored = static_cast<int64_t>(st[0]);
+        t.screened_jobs = static_cast<int64_t>(st[1]);
+        t.list_overflows = static_cast<int64_t>(st[2]);
+        t.bulk_jobs = static_cast<int64_t>(st[3]);
+        t.shared_groups = static_cast<int64_t>(st[32]);
+        ctx->timing = t;
+        learn_plan(ctx, sl.key, sl.use_wave, sl.bulk_launch, st);
+        if (st[kNumStats] != 0 && ctx->async_err.empty())
+            ctx->async_err = "internal: device schedule disagrees with the host path draws";
+        sl.valid = false;
+    }
+}
+
 void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const uint64_t* seeds,
                     int n_real, const int32_t* hd, int n_hd, uint8_t* d_out, uint8_t* h_out,
-                    ccw_diag* diag, ccw_trace* traces) {
+                    ccw_diag* diag, ccw_trace* traces, bool async_call) {
     const auto wall0 = std::chrono::steady_clock::now();
+    // earlier asynchronous calls: a synchronous call settles them all; an
+    // asynchronous one settles what has finished (its own slot was used two
+    // calls ago and is normally done)
+    async_settle(ctx, !async_call);
+    if (async_call && ctx->aslot[ctx->async_par].valid) {
+        CCW_CUDA(cudaEventSynchronize(ctx->aslot[ctx->async_par].done));
+        async_settle(ctx, false);
+    }
+    const int apar = ctx->async_par;
     cudaStream_t st = ctx->stream;
     const int T = cfg.template_size, OV = cfg.overlap, J = cfg.dwt_level, B = 1 << J;
     const int stride = T - OV;
@@ -582,7 +638,11 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         for (int k = 0; k < nkeys; ++k) max_wave = std::max(max_wave, wave_off[g][k + 1] - wave_off[g][k]);
     }
     // each realization's first slot in every wave bucket (uploaded for the device schedule)
-    int32_t* roff = static_cast<int32_t*>(ctx->h_stage.get(sizeof(int32_t) * (static_cast<size_t>(n_real) * nkeys + n_real)));
+    // (pinned staging halves alternate by call: the previous call's upload from
+    // the other half may still be queued behind its predecessor)
+    ccwgpu::HostBuf& hstage = apar == 0 ? ctx->h_stage : ctx->h_stage2;
+    if (ctx->stage_ev[apar]) CCW_CUDA(cudaEventSynchronize(ctx->stage_ev[apar]));
+    int32_t* roff = static_cast<int32_t*>(hstage.get(sizeof(int32_t) * (static_cast<size_t>(n_real) * nkeys + n_real)));
     int32_t* vid_stage = roff + static_cast<size_t>(n_real) * nkeys;
     std::copy(vid.begin(), vid.end(), vid_stage);
     {
@@ -638,6 +698,8 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
         const size_t nstage = static_cast<size_t>(n_real) * nkeys + n_real;
         int32_t* d_roff = ctx->roff.as<int32_t>(nstage);
         CCW_CUDA(cudaMemcpyAsync(d_roff, roff, sizeof(int32_t) * nstage, cudaMemcpyHostToDevice, st));
+        if (!ctx->stage_ev[apar]) CCW_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[apar], cudaEventDisableTiming));
+        CCW_CUDA(cudaEventRecord(ctx->stage_ev[apar], st));
         int* d_err = ctx->sched_err.as<int>(1);
         CCW_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), st));
         SchedParams SP{};
@@ -1047,6 +1109,12 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     }
     cudaEvent_t ev0 = tm.get(), ev1 = tm.get();
     CCW_CUDA(cudaEventRecord(ev0, st));
+    if (async_call) {  // (this call's span on events the next call does not reuse)
+        ccw_ctx::AsyncSlot& sl = ctx->aslot[apar];
+        for (cudaEvent_t* e : {&sl.done, &sl.t0, &sl.t1})
+            if (!*e) CCW_CUDA(cudaEventCreate(e));
+        CCW_CUDA(cudaEventRecord(sl.t0, st));
+    }
     for (int g = 0; g < G; ++g) CCW_CUDA(cudaStreamWaitEvent(ctx->gstreams[g], ev0, 0));
     const bool host_t = debug_env("CCW_HOSTT") != nullptr;
     auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(); };
@@ -1630,6 +1698,34 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
                 t_ev0, host_ms());
     const double t_launched = host_t ? host_ms() : 0.0;
     CCW_CUDA(cudaEventRecord(ev1, st));
+    if (async_call) {
+        // device output, no diagnostics: the counters go to this call's pinned
+        // slot and are folded in by a later call or ccw_ctx_synchronize
+        ccw_ctx::AsyncSlot& sl = ctx->aslot[apar];
+        CCW_CUDA(cudaEventRecord(sl.t1, st));
+        unsigned long long* res = static_cast<unsigned long long*>(sl.res.get(sizeof(unsigned long long) * (kNumStats + 1)));
+        res[kNumStats] = 0;
+        CCW_CUDA(cudaMemcpyAsync(res, d_stats, sizeof(unsigned long long) * kNumStats, cudaMemcpyDeviceToHost, st));
+        CCW_CUDA(cudaMemcpyAsync(res + kNumStats, ctx->sched_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CCW_CUDA(cudaEventRecord(sl.done, st));
+        sl.timing = ccw_timing{};
+        sl.timing.ccf_launches = ccf_launches;
+        sl.timing.launches = launches + (d_hd ? 1 : 0);
+        sl.timing.ccf_flop = ccf_flop;
+        sl.timing.ccf_flop_ref = ccf_flop_ref;
+        sl.timing.waves = static_cast<int64_t>(max_key + 1);
+        sl.timing.groups = G;
+        sl.timing.host_prep_ms = host_prep_ms;
+        sl.timing.jobs = static_cast<int64_t>(total_jobs);
+        sl.timing.ccf_variant = any_screen ? (use_wave ? 5 : (use_tc ? 2 : 1)) : 0;
+        sl.timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
+        sl.key = bulk_key;
+        sl.use_wave = use_wave;
+        sl.bulk_launch = bulk_launch;
+        sl.valid = true;
+        ctx->async_par = 1 - apar;
+        return;
+    }
     if (placer.joinable()) placer.join();
     if (place_err) std::rethrow_exception(place_err);
     if (host_t)
@@ -1782,16 +1878,7 @@ void run_simulation(ccw_ctx* ctx, ccw_ti* ti, const ccw_sim_config& cfg, const u
     ctx->timing.list_overflows = static_cast<int64_t>(stats[2]);
     ctx->timing.bulk_jobs = static_cast<int64_t>(stats[3]);
     ctx->timing.shared_groups = static_cast<int64_t>(stats[32]);
-    if (use_wave) {
-        if (stats[1] > 0 && stats[2] * 50 > stats[1]) ctx->tie_storm[bulk_key] = true;
-    } else if (bulk_launch && stats[1] > 0 && stats[3] * 50 > stats[1])  // > 2 % of the screened placements
-        ctx->tie_storm[bulk_key] = true;
-    else
-        ctx->tie_storm.erase(bulk_key);
-    if (bulk_launch && stats[3] == 0)
-        ctx->bulk_off[bulk_key] = true;
-    else if (!bulk_launch && stats[2] > 0)  // a list overflowed: bring the bulk kernel back
-        ctx->bulk_off.erase(bulk_key);
+    learn_plan(ctx, bulk_key, use_wave, bulk_launch, stats);
     ctx->timing.ccf_variant = any_screen ? (use_wave ? 5 : (use_tc ? 2 : 1)) : 0;
     ctx->timing.ccf_mma_flop = use_tc ? ccf_mma_flop : 0.0;
 

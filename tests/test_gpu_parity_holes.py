@@ -278,3 +278,42 @@ def test_ti_upload_code_range_checked_on_device():
     a[:] = (np.arange(1500 * 1500).reshape(1500, 1500) // 37 % 3).astype(np.uint8)
     dev.check(lib.ccw_ti_create(dev.handle, a.ctypes.data_as(_abi.U8P), 1500, 1500, 3, 2, 0, C.byref(h)))
     lib.ccw_ti_destroy(h)
+
+
+def test_async_device_calls_equal_sync():
+    """ccw_simulate_device_async: back-to-back calls (each one's host planning
+    overlapping the previous one's device work, alternating staging halves and
+    result slots) produce the synchronous call's realizations; the timing and
+    the plan memory are settled by ccw_ctx_synchronize."""
+    import ctypes as C
+    import torch
+    from paper_2404_00441_b200 import _abi
+    ti_a = synth.config1_ti()
+    grid = cs.CategoricalGrid(500, 500, 3, ti_a)
+    cfg = cs.SimConfig(440, 392, 64, 16, 2, 5, n_realizations=12, master_seed=31)
+    dev = cs.Device(0)
+    lib = _abi.lib()
+    try:
+        tih = cs.TrainingImage(grid, 2, "indicator", dev)
+        c = cfg.to_c()
+        n = 12
+        sg = 440 * 392
+        outs = [torch.zeros(n * sg, dtype=torch.uint8, device="cuda:0") for _ in range(5)]
+        ref = torch.zeros(n * sg, dtype=torch.uint8, device="cuda:0")
+        seed_sets = [np.array([cs.mix64(31 + k % 2, r + 1) for r in range(n)], np.uint64) for k in range(5)]
+        diags = (_abi.DiagC * n)()
+        for k in range(5):
+            dev.check(lib.ccw_simulate_device_async(dev.handle, tih.handle, C.byref(c),
+                                                    seed_sets[k].ctypes.data_as(_abi.U64P), n, None, 0,
+                                                    C.c_void_p(outs[k].data_ptr())))
+        dev.synchronize()
+        t = dev.last_timing()
+        assert t["total_ms"] > 0 and t["jobs"] > 0
+        for k in range(5):
+            dev.check(lib.ccw_simulate_device(dev.handle, tih.handle, C.byref(c),
+                                              seed_sets[k].ctypes.data_as(_abi.U64P), n, None, 0,
+                                              C.c_void_p(ref.data_ptr()), diags))
+            torch.cuda.synchronize()
+            assert torch.equal(outs[k], ref), k
+    finally:
+        dev.close()
