@@ -11,7 +11,7 @@ cfg = cs.SimConfig(4000, 4000, 96, 24, 3, 1, n_realizations=n, master_seed=20240
 seeds = np.array([cs.mix64(20240441, r + 1) for r in range(n)], np.uint64)
 c = cfg.to_c(); d_out = torch.empty(n * 16 * 10**6, dtype=torch.uint8, device="cuda:0")
 diags = (_abi.DiagC * n)()
-for _k in ("groups", "wave", "wave_cs"):
+for _k in ("groups", "wave", "wave_cs", "help_min"):
     if os.environ.get(_k.upper()): dev.set_option(_k, int(os.environ[_k.upper()]))
 dev.set_profiling(os.environ.get("PROF", "1") == "1")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")

@@ -12,6 +12,7 @@ seeds = np.array([cs.mix64(20240441, r + 1) for r in range(100)], np.uint64)
 c = cfg.to_c(); d_out = torch.empty(100 * 10**6, dtype=torch.uint8, device="cuda:0")
 diags = (_abi.DiagC * 100)()
 ref = None
+if os.environ.get("HELP_MIN"): dev.set_option("help_min", int(os.environ["HELP_MIN"]))
 if os.environ.get("FLAGPREP"): dev.set_option("flagprep", int(os.environ["FLAGPREP"]))
 for G in [int(g) for g in os.environ.get("GROUPS", "1,2,3,4").split(",")]:
     dev.set_option("groups", G)
