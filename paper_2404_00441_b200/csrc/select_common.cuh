@@ -608,11 +608,16 @@ __device__ __forceinline__ void paste_job(const SimParams& P, const Job& jb, int
     // from the map at finalize: only the map (and a requested trace) is written.
     if (P.work || P.pasted) paste_copy<JT>(P, jb, gj, fr, fc, jt);
     if (P.src) {  // Tc x Tc map entries spread over every thread
-        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc +
-                      static_cast<size_t>(jb.top / P.B) * P.swc + jb.left / P.B;
-        const int s0 = (fr / P.B) * P.wc + fc / P.B;
+        // (B = 2^J: shifts, not integer divisions -- this is on every
+        //  placement's critical path; a power-of-two Tc splits e by shifts too)
+        const int J = P.J;
+        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh >> J) * P.swc +
+                      static_cast<size_t>(jb.top >> J) * P.swc + (jb.left >> J);
+        const int s0 = (fr >> J) * P.wc + (fc >> J);
+        const bool pow2 = (Tc & (Tc - 1)) == 0;
+        const int lt = __ffs(Tc) - 1;
         for (int e = jt; e < Tc * Tc; e += JT) {
-            const int a = e / Tc, b = e - a * Tc;
+            const int a = pow2 ? e >> lt : e / Tc, b = e - a * Tc;
             sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
         }
     }

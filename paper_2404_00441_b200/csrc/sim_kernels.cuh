@@ -45,7 +45,11 @@ __device__ __forceinline__ void store_cjob(int32_t* cjob, int mode, int B, int s
 __device__ __forceinline__ void prep_src_job(const SimParams& P, const Job& jb, int slot, int8_t* w8base,
                                              double* tmbase, int32_t* cjobbase) {
     const int Tc = P.Tc, B = P.B, nc = P.hc * P.wc;
-    const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh / B) * P.swc;
+    const int J = P.J;  // (B = 2^J: block coordinates by shifts)
+    const int32_t* src = P.src + static_cast<size_t>(jb.real) * (P.wh >> J) * P.swc +
+                         static_cast<size_t>(jb.top >> J) * P.swc + (jb.left >> J);
+    const bool tc_pow2 = (Tc & (Tc - 1)) == 0;
+    const int tc_log = __ffs(Tc) - 1;
     int32_t* wts = w8base ? nullptr : P.wts + static_cast<size_t>(slot) * P.nscr * Tc * Tc;
     double* tm = tmbase ? tmbase + static_cast<size_t>(slot) * P.nch * Tc * Tc : nullptr;
     int8_t* w8 = w8base ? w8base + static_cast<size_t>(slot) * P.kpad : nullptr;
@@ -62,11 +66,11 @@ __device__ __forceinline__ void prep_src_job(const SimParams& P, const Job& jb, 
 #pragma unroll
             for (int u = 0; u < kCpt; ++u) {
                 const int c = c0 + u * blockDim.x;
-                const int s = c / Tc, t = c - s * Tc;
+                const int s = tc_pow2 ? c >> tc_log : c / Tc, t = c - s * Tc;
                 int t0 = 0, t1 = 0;
                 if (c < Tc * Tc) mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
                 in[u] = c < Tc * Tc && t >= t0 && t < t1;
-                sb[u] = in[u] ? src[static_cast<size_t>(jb.top / B + s) * P.swc + jb.left / B + t] : 0;
+                sb[u] = in[u] ? src[static_cast<size_t>(s) * P.swc + t] : 0;
             }
             float n[kCpt][kCh];
             double a[kCpt][kCh];
@@ -106,11 +110,11 @@ __device__ __forceinline__ void prep_src_job(const SimParams& P, const Job& jb, 
         return;
     }
     for (int c = threadIdx.x; c < Tc * Tc; c += blockDim.x) {
-        const int s = c / Tc, t = c - s * Tc;
+        const int s = tc_pow2 ? c >> tc_log : c / Tc, t = c - s * Tc;
         int t0, t1;
         mask_row_run(jb.shape, jb.vleft, jb.htop, Tc, P.OVc, s, t0, t1);
         const bool in = t >= t0 && t < t1;
-        const int sb = in ? src[static_cast<size_t>(jb.top / B + s) * P.swc + jb.left / B + t] : 0;
+        const int sb = in ? src[static_cast<size_t>(s) * P.swc + t] : 0;
         int last = B * B;
         if (P.mode == 0)
             for (int f = 0; f < P.nscr; ++f) last -= static_cast<int>(P.tiscr[static_cast<size_t>(f) * nc + sb]);
