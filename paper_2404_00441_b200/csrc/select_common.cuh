@@ -325,12 +325,14 @@ static __device__ void paste_placement(const SimParams& P, const Job& jb, int gj
             if (trace) trace[e] = v;
         }
     }
-    if (P.src) {
-        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh / P.B) * P.swc;
-        for (int e = tid; e < P.Tc * P.Tc; e += SEL_T) {
-            const int a = e / P.Tc, b = e - a * P.Tc;
-            sm[static_cast<size_t>(jb.top / P.B + a) * P.swc + jb.left / P.B + b] =
-                (fr / P.B + a) * P.wc + fc / P.B + b;
+    if (P.src) {  // (block coordinates by shifts: B = 2^J)
+        const int J = P.J, Tc = P.Tc;
+        int32_t* sm = P.src + static_cast<size_t>(jb.real) * (P.wh >> J) * P.swc +
+                      static_cast<size_t>(jb.top >> J) * P.swc + (jb.left >> J);
+        const int s0 = (fr >> J) * P.wc + (fc >> J);
+        for (int e = tid; e < Tc * Tc; e += SEL_T) {
+            const int a = e / Tc, b = e - a * Tc;
+            sm[static_cast<size_t>(a) * P.swc + b] = s0 + a * P.wc + b;
         }
     }
     if (tid == 0) {
