@@ -349,7 +349,7 @@ class Device:
     OPTION_DEFAULTS = {"groups": 0, "sched_replay": 0, "norm_screen": 1, "shard_fast": 1,
                        "uniform": 1, "s16": 1, "bulk": 1, "help_min": 32, "stream_out": 1,
                        "pack": 1, "stream_bands": 6, "place_threads": 0,
-                       "wave": 0, "wave_cs": 0, "flagprep": 1}
+                       "wave": 0, "wave_cs": 0, "flagprep": 1, "tc3d": 1}
 
     def set_option(self, name: str, value: int) -> None:
         """Per-context option (include/ccwgpu.h ccw_ctx_set_option)."""

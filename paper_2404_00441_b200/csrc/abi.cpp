@@ -830,6 +830,7 @@ void ccw_ti3d_destroy(ccw_ti3d* ti) {
     cudaDeviceSynchronize();
     ccwgpu::cache_free(ti->d_codes);
     ccwgpu::cache_free(ti->d_pk);
+    for (auto& kv : ti->im2col) ccwgpu::cache_free(kv.second);
     delete ti;
 }
 

@@ -235,6 +235,7 @@ struct Options {
     int wave = 0;              // fused wave kernel (wave.cu) where it applies (experimental)
     int wave_cs = 0;           // its CTAs per cluster (0 = auto)
     int flagprep = 1;          // OR prep waits on per-placement dependency flags, not the whole select
+    int tc3d = 1;              // 3D: tcgen05 int8 screen where the block counts fit int8 (sim3d.cu)
 };
 
 // Known option names (for ccw_ctx_set_option); returns nullptr if unknown.
@@ -254,6 +255,7 @@ inline int* option_slot(Options& o, const std::string& name) {
     if (name == "wave") return &o.wave;
     if (name == "wave_cs") return &o.wave_cs;
     if (name == "flagprep") return &o.flagprep;
+    if (name == "tc3d") return &o.tc3d;
     return nullptr;
 }
 
@@ -280,7 +282,7 @@ struct ccw_ctx {
     ccw_timing timing{};
     // scratch
     ccwgpu::DevBuf wave_w, depflag, chk, cjob, depcnt, defer, bulk_sync, bulk_keys, bulk_idx, hdoff, hdent, jobs, work, hd, wts, wts8, tm64, scores, summary, chosen, pasted, mism, out,
-        stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, tmaxnu, jvar, ops_a, ops_b, ops_c, ops_d, ops_e;
+        stats, src, mtab, roff, seeds, lattice, sched_err, sched_outs, sched_replay, jdump, band_off, band_stage, hboards, hpos, hkeys, hdone, tmaxnu, jvar, ops_a, ops_b, ops_c, ops_d, ops_e, tc3_w, tc3_sc, tc3_tm;
     long long mtab_key = -1;  // (Tc, OVc, nch) of the mask tables in mtab
     ccwgpu::HostBuf h_stage;
     ccwgpu::HostBuf h_out_stage;  // pinned landing zone when the caller's result buffer is pageable
@@ -342,6 +344,9 @@ struct ccw_ti3d {
     int F = 0, J = 0, nscr = 0, mode = 0;
     uint8_t* d_codes = nullptr;
     int32_t* d_pk = nullptr;
+    // im2col of the packed counts for the tcgen05 screen, keyed by the coarse
+    // template size (sim3d.cu ti3d_im2col); freed with the TI
+    std::map<int, int8_t*> im2col;
 };
 
 // On-device pattern histogram (ccw_pattern_histogram): distinct exact window

@@ -30,6 +30,7 @@
 #include <climits>
 #include <cstring>
 
+#include "ccf_tc.hpp"
 #include "ccw_device.cuh"
 #include "internal.hpp"
 
@@ -367,6 +368,106 @@ __global__ void __launch_bounds__(S3_THREADS) screen3d_kernel(Screen3Args a) {
     }
 }
 
+// ------------------------------------------- tcgen05 screen (mode 0) ------
+// Where the block counts fit int8 (mode 0: B <= 4, <= 4 screen channels) the
+// 3D CCF is the same implicit GEMM as the 2D screen (ccf_tc.cu): placements x
+// window positions over K = tc^3 cells x 4 packed channel bytes.  The window
+// matrix is an explicit im2col of the packed TI counts, built once per TI and
+// coarse template size; the weights are the prep's packed words scattered to
+// their window cells (zero off the mask, so the full-window product equals
+// the masked sum of screen3d_kernel bit for bit).
+__global__ void im2col3d_kernel(const int32_t* __restrict__ tipk, int c1, int c2, int o1, int o2, int tc,
+                                int npos, int kwords, int32_t* __restrict__ X) {
+    const int tc3 = tc * tc * tc;
+    const size_t total = static_cast<size_t>(npos) * kwords;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int pos = static_cast<int>(e / kwords), cell = static_cast<int>(e - static_cast<size_t>(pos) * kwords);
+        int32_t v = 0;
+        if (cell < tc3) {
+            const int m2 = cell % tc, m1 = (cell / tc) % tc, m0 = cell / (tc * tc);
+            const int p2 = pos % o2, p1 = (pos / o2) % o1, p0 = pos / (o2 * o1);
+            v = tipk[(static_cast<size_t>(p0 + m0) * c1 + p1 + m1) * c2 + p2 + m2];
+        }
+        X[e] = v;
+    }
+}
+
+// One CTA per job of the wave: its row of the weight matrix.
+__global__ void __launch_bounds__(128) w8_scatter3d_kernel(const Job3* __restrict__ jobs, int j0,
+                                                           const int* __restrict__ mask_off,
+                                                           const int* __restrict__ mask_cells,
+                                                           const int32_t* __restrict__ wbuf, int wstride, int tc,
+                                                           int kwords, int32_t* __restrict__ W) {
+    pdl_trigger();
+    pdl_wait();
+    const Job3 jb = jobs[j0 + blockIdx.x];
+    int32_t* row = W + static_cast<size_t>(blockIdx.x) * kwords;
+    for (int i = threadIdx.x; i < kwords; i += blockDim.x) row[i] = 0;
+    __syncthreads();
+    const int m_lo = mask_off[jb.bmask], nm = mask_off[jb.bmask + 1] - m_lo;
+    const int32_t* w = wbuf + static_cast<size_t>(blockIdx.x) * wstride;
+    for (int i = threadIdx.x; i < nm; i += blockDim.x) {
+        const int cell = mask_cells[m_lo + i];
+        row[((cell >> 16) * tc + ((cell >> 8) & 0xFF)) * tc + (cell & 0xFF)] = w[i];
+    }
+}
+
+// One CTA per job: the K best packed keys (score desc, position asc) of its
+// score row, written as the single "box" list select3d merges.  Only tiles
+// whose maximum reaches the K-th largest tile maximum can hold a top-K window.
+__global__ void __launch_bounds__(128) keys3d_kernel(const int32_t* __restrict__ scores,
+                                                     const int32_t* __restrict__ tmax, int sld, int tld,
+                                                     int npos, int K, unsigned long long* __restrict__ xbuf) {
+    __shared__ unsigned long long red[4];
+    pdl_trigger();
+    pdl_wait();
+    const int j = blockIdx.x, tid = threadIdx.x;
+    const int32_t* tm = tmax + static_cast<size_t>(j) * tld;
+    const int32_t* sc = scores + static_cast<size_t>(j) * sld;
+    const int nt = (npos + kTcTile - 1) / kTcTile;
+    auto block_max = [&](unsigned long long v) {
+        v = warp_max64(v);
+        __syncthreads();
+        if ((tid & 31) == 0) red[tid >> 5] = v;
+        __syncthreads();
+        return umax64(umax64(red[0], red[1]), umax64(red[2], red[3]));
+    };
+    int thr = INT_MIN;
+    if (nt > K) {
+        unsigned long long prev = ~0ull, m = 0;
+        for (int r = 0; r < K; ++r) {
+            m = 0;
+            for (int t = tid; t < nt; t += 128) {
+                const unsigned long long key =
+                    (static_cast<unsigned long long>(static_cast<uint32_t>(tm[t]) ^ 0x80000000u) << 32) |
+                    (0xFFFFFFFFu - static_cast<uint32_t>(t));
+                if (key < prev) m = umax64(m, key);
+            }
+            m = block_max(m);
+            prev = m;
+        }
+        thr = static_cast<int>(static_cast<uint32_t>(m >> 32) ^ 0x80000000u);
+    }
+    unsigned long long prev = ~0ull;
+    for (int r = 0; r < K; ++r) {
+        unsigned long long m = 0;
+        for (int t = 0; t < nt; ++t) {
+            if (tm[t] < thr) continue;
+            const int p = t * kTcTile + tid;
+            if (p < npos) {
+                const unsigned long long key =
+                    (static_cast<unsigned long long>(static_cast<uint32_t>(sc[p]) ^ 0x80000000u) << 32) |
+                    (0xFFFFFFFFu - static_cast<uint32_t>(p));
+                if (key < prev) m = umax64(m, key);
+            }
+        }
+        m = block_max(m);
+        if (tid == 0) xbuf[static_cast<size_t>(j) * K + r] = m;
+        prev = m;
+    }
+}
+
 // ----------------------------------------------------------- select ------
 struct Select3Args {
     Geo3 g;
@@ -555,6 +656,20 @@ void build_pyramid3d(ccw_ti3d* ti, cudaStream_t st) {
                                                      ti->c[2], 1 << ti->J, ti->nscr, ti->mode,
                                                      ti->d_pk);
     CCW_CUDA(cudaGetLastError());
+}
+
+// im2col of the packed TI counts for the tcgen05 screen (cached on the TI):
+// [npos][kwords] words, window cell (m0, m1, m2) at word (m0 tc + m1) tc + m2.
+static const int8_t* ti3d_im2col(ccw_ti3d* ti, const Geo3& g, int npos, int kwords, cudaStream_t st) {
+    auto it = ti->im2col.find(g.tc);
+    if (it != ti->im2col.end()) return it->second;
+    const size_t total = static_cast<size_t>(npos) * kwords;
+    int32_t* X = static_cast<int32_t*>(cache_alloc(ti->device, total * sizeof(int32_t)));
+    const unsigned nb = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 32));
+    im2col3d_kernel<<<std::max(nb, 1u), 256, 0, st>>>(ti->d_pk, g.c[1], g.c[2], g.o[1], g.o[2], g.tc, npos, kwords, X);
+    CCW_CUDA(cudaGetLastError());
+    ti->im2col[g.tc] = reinterpret_cast<int8_t*>(X);
+    return reinterpret_cast<int8_t*>(X);
 }
 
 void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, const uint64_t* seeds, int n_real,
@@ -775,6 +890,14 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     const int S_virt = ctx->shard_virtual, S_ranks = ctx->shard_nranks, S = S_virt * S_ranks;
     if (nbox < S) throw Fail(CCW_ERR_CONFIG, "position shards: more shards than 3D screen boxes");
     const int bps = (nbox + S - 1) / S;
+    // ---- tcgen05 screen (option tc3d): int8 block counts, unsharded ----
+    const int tc3 = g.tc * g.tc * g.tc;
+    const int kwords = ((tc3 + 31) / 32) * 32;  // K = 4 kwords bytes, whole 128-byte stages
+    const int sld = (npos + 3) & ~3;
+    const int tld = tc_tiles(npos);
+    const bool use_tc = ctx->opt.tc3d && mode == 0 && S == 1 && !ctx->nccl_comm && Kp >= 1 &&
+                        static_cast<size_t>(npos) * kwords * 4 <= (size_t(4) << 30) &&
+                        static_cast<size_t>(max_wave) * sld * 4 <= (size_t(2) << 30);
 
     const bool host_t = debug_env("CCW_HOSTT") != nullptr;
     auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(); };
@@ -821,6 +944,18 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     const size_t sgvol = static_cast<size_t>(cfg.sg[0]) * cfg.sg[1] * cfg.sg[2];
     uint8_t* fin = d_out ? d_out : ctx->out.as<uint8_t>(sgvol * n_real);
 
+    TcPlan tcplan{};
+    int32_t* d_w8 = nullptr;
+    int32_t* d_sc = nullptr;
+    int32_t* d_tm = nullptr;
+    if (use_tc) {
+        const int maxj = ((max_wave + 127) / 128) * 128;
+        d_w8 = ctx->tc3_w.as<int32_t>(static_cast<size_t>(maxj) * kwords);
+        d_sc = ctx->tc3_sc.as<int32_t>(static_cast<size_t>(max_wave) * sld);
+        d_tm = ctx->tc3_tm.as<int32_t>(static_cast<size_t>(max_wave) * tld);
+        const int8_t* X = ti3d_im2col(ti, g, npos, kwords, st);
+        tcplan = plan_ccf_tc(reinterpret_cast<const int8_t*>(d_w8), maxj, X, npos, kwords * 4);
+    }
     void (*screen)(Screen3Args) = nullptr;
     if (mode == 0)
         screen = best_np == 4 ? screen3d_kernel<0, 4> : best_np == 2 ? screen3d_kernel<0, 2> : screen3d_kernel<0, 1>;
@@ -889,7 +1024,17 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             q.bt0 = b0;
             q.j0 = j0;
             q.nj = nj;
-            for (int v = 0; v < S_virt; ++v) {
+            if (use_tc) {
+                launch_pdl(w8_scatter3d_kernel, dim3(nj), dim3(128), 0, st, static_cast<const Job3*>(d_jobs), j0,
+                           static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
+                           static_cast<const int32_t*>(d_w), wstride, g.tc, kwords, d_w8);
+                launch_ccf_tc(tcplan, npos, sld, kwords * 4, nj, d_sc, d_tm, st);
+                launch_pdl(keys3d_kernel, dim3(nj), dim3(128), 0, st, static_cast<const int32_t*>(d_sc),
+                           static_cast<const int32_t*>(d_tm), sld, tld, npos, sa.K, d_x);
+                launches += 3;
+                ++ccf_launches;
+            }
+            for (int v = 0; v < (use_tc ? 0 : S_virt); ++v) {
                 const int s = ctx->shard_rank * S_virt + v;
                 q.box0 = std::min(nbox, s * bps);
                 q.box1 = std::min(nbox, (s + 1) * bps);
@@ -916,6 +1061,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         Select3Args q = se;
         q.j0 = j0;
         q.nj = nj;
+        if (use_tc) q.S = q.bps = q.nbox = 1;  // keys3d_kernel's single list per job
         const int ssplit = std::max(1, std::min(g.T / 4, (2 * 148 + nj - 1) / nj));
         launch_pdl(select3d_kernel, dim3(nj, ssplit), dim3(128), 0, st, q);
         ++launches;
@@ -971,7 +1117,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     ctx->timing.waves = max_key + 1;
     ctx->timing.jobs = static_cast<int64_t>(njobs);
     ctx->timing.screened_jobs = static_cast<int64_t>(njobs) - n_real;
-    ctx->timing.ccf_variant = mode == 0 ? 3 : 4;
+    ctx->timing.ccf_variant = use_tc ? 6 : mode == 0 ? 3 : 4;
     ctx->timing.groups = 1;
     ctx->timing.d2h_bytes = h_out ? static_cast<int64_t>(sgvol * n_real) : 0;
     (void)ccf_launches;

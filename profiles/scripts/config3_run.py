@@ -1,4 +1,4 @@
-# BASELINE configs 3 / 4 (3D) on the device: REPS calls (WHICH=3 or 4), for ncu captures of screen3d_kernel.
+# BASELINE configs 3 / 4 (3D) on the device: REPS calls (WHICH=3 or 4), for ncu captures of screen3d_kernel (TC3D=0) or the tcgen05 3D screen (TC3D=1, default).
 import os, sys, ctypes as C, numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2404_00441_b200 import ccwsim as cs, ccwsim3d as c3, synth
@@ -15,6 +15,7 @@ else:
     nf = 5
 dev = cs.default_device()
 ti = c3.TrainingImage3D(ti_a, nf, cfg.dwt_level, dev)
+dev.set_option("tc3d", int(os.environ.get("TC3D", "1")))
 dev.set_profiling(os.environ.get("PROF", "1") == "1")
 for i in range(int(os.environ.get("REPS", "2"))):
     c3.simulate3d_ensemble(ti, cfg)

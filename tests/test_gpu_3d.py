@@ -50,11 +50,22 @@ def random_case(rng, trial):
     return ti, nf, cfg
 
 
+@pytest.mark.parametrize("tc3d", [1, 0])
 @pytest.mark.parametrize("block", range(4))
-def test_randomized_corpus_vs_oracle(o3, block):
+def test_randomized_corpus_vs_oracle(o3, block, tc3d):
     """J 1-3, F 1-5, K 1-8, overlap shapes of every corner / axis order,
-    the literal-config extension on every third case, hard data on half."""
+    the literal-config extension on every third case, hard data on half;
+    with the tcgen05 screen (int8 block counts: J <= 2, F <= 5) and without."""
     rng = np.random.default_rng(1000 + block)
+    dev = cs.default_device()
+    dev.set_option("tc3d", tc3d)
+    try:
+        _corpus(o3, block, tc3d, rng, dev)
+    finally:
+        dev.set_option("tc3d", 1)
+
+
+def _corpus(o3, block, tc3d, rng, dev):
     for trial in range(8):
         ti_a, nf, cfg = random_case(rng, trial)
         seeds = [int(s) for s in rng.integers(0, 2**63, 4)]
@@ -70,6 +81,8 @@ def test_randomized_corpus_vs_oracle(o3, block):
             assert diags[r].pre_overwrite_mismatches == o["diagnostics"]["pre_overwrite_mismatches"]
             assert diags[r].corner == o["diagnostics"]["corner"]
             assert diags[r].order == o["diagnostics"]["order"]
+        int8_counts = cfg.dwt_level <= 2 and nf <= 5
+        assert dev.last_timing()["ccf_variant"] == (6 if tc3d and int8_counts else 3 if int8_counts else 4)
         ti.close()
 
 
