@@ -106,20 +106,38 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
                                                      const int* __restrict__ mask_off,
                                                      const int* __restrict__ mask_cells,
                                                      const uint8_t* __restrict__ work, int32_t* __restrict__ wbuf,
-                                                     int wstride) {
+                                                     int wstride, int tcrow) {
+    // tcrow > 0 (tcgen05 screen): wbuf rows are the GEMM's weight rows, one
+    // packed word per WINDOW cell (row stride tcrow words, zero off the job's
+    // own overlap support); else one entry per cell of the batch's mask.
     pdl_trigger();
     pdl_wait();
     const Job3 jb = jobs[j0 + blockIdx.x];
     const int corner = jb.mask >> 3, shape = jb.mask & 7;  // the job's own overlap support
-    const int m_lo = mask_off[jb.bmask], nm = mask_off[jb.bmask + 1] - m_lo;  // cells of its batch's mask
+    const int m_lo = mask_off[jb.bmask];
+    const int nm = tcrow > 0 ? tcrow : mask_off[jb.bmask + 1] - m_lo;  // cells of its batch's mask
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int B = g.B, B3 = B * B * B;
     const uint8_t* wk = work + static_cast<size_t>(jb.real) * g.W[0] * g.W[1] * g.W[2];
     int32_t* wout = wbuf + static_cast<size_t>(blockIdx.x) * wstride;
     const int nw = blockDim.x >> 5;
     for (int i = blockIdx.y * nw + warp; i < nm; i += gridDim.y * nw) {
-        const int cell = mask_cells[m_lo + i];
-        const int m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
+        int m0, m1, m2;
+        if (tcrow > 0) {
+            m2 = i % g.tc, m1 = (i / g.tc) % g.tc, m0 = i / (g.tc * g.tc);
+            const int m[3] = {m0, m1, m2};
+            bool any = false;  // does the block touch one of the job's slabs at all?
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if ((shape >> a) & 1) any |= !((corner >> a) & 1) ? m[a] * B < g.OV : m[a] * B + B > g.T - g.OV;
+            if (!any || m0 >= g.tc) {
+                if (lane == 0) wout[i] = 0;
+                continue;
+            }
+        } else {
+            const int cell = mask_cells[m_lo + i];
+            m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
+        }
         int cnt[16] = {0};
         for (int e = lane; e < B3; e += 32) {
             const int x0 = m0 * B + e / (B * B), x1 = m1 * B + (e / B) % B, x2 = m2 * B + e % B;
@@ -142,7 +160,7 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
         int nlast = 0;
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch) {
-            const int s = __reduce_add_sync(0xffffffffu, cnt[ch]);
+            const int s = ch < g.F ? __reduce_add_sync(0xffffffffu, cnt[ch]) : 0;  // (uniform: F is a launch constant)
             if (ch == last) nlast = s;
             wv[ch] = s;
         }
@@ -373,9 +391,9 @@ __global__ void __launch_bounds__(S3_THREADS) screen3d_kernel(Screen3Args a) {
 // 3D CCF is the same implicit GEMM as the 2D screen (ccf_tc.cu): placements x
 // window positions over K = tc^3 cells x 4 packed channel bytes.  The window
 // matrix is an explicit im2col of the packed TI counts, built once per TI and
-// coarse template size; the weights are the prep's packed words scattered to
-// their window cells (zero off the mask, so the full-window product equals
-// the masked sum of screen3d_kernel bit for bit).
+// coarse template size; the prep writes one packed weight word per window cell
+// (zero off the job's overlap support, so the full-window product equals the
+// masked sum of screen3d_kernel bit for bit).
 __global__ void im2col3d_kernel(const int32_t* __restrict__ tipk, int c1, int c2, int o1, int o2, int tc,
                                 int npos, int kwords, int32_t* __restrict__ X) {
     const int tc3 = tc * tc * tc;
@@ -393,81 +411,6 @@ __global__ void im2col3d_kernel(const int32_t* __restrict__ tipk, int c1, int c2
     }
 }
 
-// One CTA per job of the wave: its row of the weight matrix.
-__global__ void __launch_bounds__(128) w8_scatter3d_kernel(const Job3* __restrict__ jobs, int j0,
-                                                           const int* __restrict__ mask_off,
-                                                           const int* __restrict__ mask_cells,
-                                                           const int32_t* __restrict__ wbuf, int wstride, int tc,
-                                                           int kwords, int32_t* __restrict__ W) {
-    pdl_trigger();
-    pdl_wait();
-    const Job3 jb = jobs[j0 + blockIdx.x];
-    int32_t* row = W + static_cast<size_t>(blockIdx.x) * kwords;
-    for (int i = threadIdx.x; i < kwords; i += blockDim.x) row[i] = 0;
-    __syncthreads();
-    const int m_lo = mask_off[jb.bmask], nm = mask_off[jb.bmask + 1] - m_lo;
-    const int32_t* w = wbuf + static_cast<size_t>(blockIdx.x) * wstride;
-    for (int i = threadIdx.x; i < nm; i += blockDim.x) {
-        const int cell = mask_cells[m_lo + i];
-        row[((cell >> 16) * tc + ((cell >> 8) & 0xFF)) * tc + (cell & 0xFF)] = w[i];
-    }
-}
-
-// One CTA per job: the K best packed keys (score desc, position asc) of its
-// score row, written as the single "box" list select3d merges.  Only tiles
-// whose maximum reaches the K-th largest tile maximum can hold a top-K window.
-__global__ void __launch_bounds__(128) keys3d_kernel(const int32_t* __restrict__ scores,
-                                                     const int32_t* __restrict__ tmax, int sld, int tld,
-                                                     int npos, int K, unsigned long long* __restrict__ xbuf) {
-    __shared__ unsigned long long red[4];
-    pdl_trigger();
-    pdl_wait();
-    const int j = blockIdx.x, tid = threadIdx.x;
-    const int32_t* tm = tmax + static_cast<size_t>(j) * tld;
-    const int32_t* sc = scores + static_cast<size_t>(j) * sld;
-    const int nt = (npos + kTcTile - 1) / kTcTile;
-    auto block_max = [&](unsigned long long v) {
-        v = warp_max64(v);
-        __syncthreads();
-        if ((tid & 31) == 0) red[tid >> 5] = v;
-        __syncthreads();
-        return umax64(umax64(red[0], red[1]), umax64(red[2], red[3]));
-    };
-    int thr = INT_MIN;
-    if (nt > K) {
-        unsigned long long prev = ~0ull, m = 0;
-        for (int r = 0; r < K; ++r) {
-            m = 0;
-            for (int t = tid; t < nt; t += 128) {
-                const unsigned long long key =
-                    (static_cast<unsigned long long>(static_cast<uint32_t>(tm[t]) ^ 0x80000000u) << 32) |
-                    (0xFFFFFFFFu - static_cast<uint32_t>(t));
-                if (key < prev) m = umax64(m, key);
-            }
-            m = block_max(m);
-            prev = m;
-        }
-        thr = static_cast<int>(static_cast<uint32_t>(m >> 32) ^ 0x80000000u);
-    }
-    unsigned long long prev = ~0ull;
-    for (int r = 0; r < K; ++r) {
-        unsigned long long m = 0;
-        for (int t = 0; t < nt; ++t) {
-            if (tm[t] < thr) continue;
-            const int p = t * kTcTile + tid;
-            if (p < npos) {
-                const unsigned long long key =
-                    (static_cast<unsigned long long>(static_cast<uint32_t>(sc[p]) ^ 0x80000000u) << 32) |
-                    (0xFFFFFFFFu - static_cast<uint32_t>(p));
-                if (key < prev) m = umax64(m, key);
-            }
-        }
-        m = block_max(m);
-        if (tid == 0) xbuf[static_cast<size_t>(j) * K + r] = m;
-        prev = m;
-    }
-}
-
 // ----------------------------------------------------------- select ------
 struct Select3Args {
     Geo3 g;
@@ -475,6 +418,11 @@ struct Select3Args {
     int j0, nj;
     const unsigned long long* xbuf;  // [S][nj][bps][K]
     int S, bps, nbox, K, Kp;
+    // tcgen05 screen: exact score rows and their 128-position tile maxima
+    // instead of the boxes' key lists (null: off)
+    const int32_t* sc;  // [nj][sld]
+    const int32_t* tm;  // [nj][tld]
+    int sld, tld, npos;
     const int* hd_off;          // CSR per lattice cell (may be null)
     const uint32_t* hd_ent;     // (x0 << 20 | x1 << 10 | x2) local offset, facies in a second word
     const uint8_t* hd_fac;
@@ -505,11 +453,70 @@ __device__ __forceinline__ int block_sum(int v, int* red) {
     return s;
 }
 
+__device__ __forceinline__ unsigned long long key64(int score, uint32_t idx) {
+    return (static_cast<unsigned long long>(static_cast<uint32_t>(score) ^ 0x80000000u) << 32) | (0xFFFFFFFFu - idx);
+}
+
+// The K best packed keys (score desc, position asc) of one score row of the
+// tcgen05 screen.  Only tiles whose maximum reaches the K-th largest tile
+// maximum can hold a top-K window: those tiles are listed, then K rounds of
+// "largest key below the last" over the listed tiles' positions.
+constexpr int TLCAP = 128;
+__device__ void row_top_keys(const int32_t* __restrict__ sc, const int32_t* __restrict__ tm, int npos, int K,
+                             unsigned long long* cands, unsigned long long* red, int* tl, int* ntl) {
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int nt = (npos + kTcTile - 1) / kTcTile;
+    int thr = INT_MIN;
+    if (nt > K) {
+        unsigned long long prev = ~0ull, m = 0;
+        for (int r = 0; r < K; ++r) {
+            m = 0;
+            for (int t = tid; t < nt; t += nth) {
+                const unsigned long long key = key64(tm[t], static_cast<uint32_t>(t));
+                if (key < prev) m = umax64(m, key);
+            }
+            m = block_max64(m, red);
+            prev = m;
+        }
+        thr = static_cast<int>(static_cast<uint32_t>(m >> 32) ^ 0x80000000u);
+    }
+    if (tid == 0) *ntl = 0;
+    __syncthreads();
+    for (int t = tid; t < nt; t += nth)
+        if (tm[t] >= thr) {
+            const int q = atomicAdd(ntl, 1);
+            if (q < TLCAP) tl[q] = t;
+        }
+    __syncthreads();
+    const int n = *ntl;
+    unsigned long long prev = ~0ull;
+    for (int r = 0; r < K; ++r) {
+        unsigned long long m = 0;
+        auto tile = [&](int t) {
+            for (int p = t * kTcTile + tid; p < min(npos, (t + 1) * kTcTile); p += nth) {
+                const unsigned long long key = key64(sc[p], static_cast<uint32_t>(p));
+                if (key < prev) m = umax64(m, key);
+            }
+        };
+        if (n <= TLCAP) {
+            for (int q = 0; q < n; ++q) tile(tl[q]);
+        } else {  // a tie storm over many tiles: every qualifying tile, unlisted
+            for (int t = 0; t < nt; ++t)
+                if (tm[t] >= thr) tile(t);
+        }
+        m = block_max64(m, red);
+        if (tid == 0) cands[r] = m;
+        prev = m;
+    }
+}
+
 __global__ void __launch_bounds__(128) select3d_kernel(Select3Args a) {
     __shared__ unsigned long long red[4];
     __shared__ int redi[4];
     __shared__ unsigned long long cands[KMAX3];
     __shared__ int fr_s[3];
+    __shared__ int tl_s[TLCAP];
+    __shared__ int ntl_s;
     pdl_trigger();
     pdl_wait();
     const Geo3& g = a.g;
@@ -522,7 +529,10 @@ __global__ void __launch_bounds__(128) select3d_kernel(Select3Args a) {
         const int per = a.bps * a.K;
         const int total = a.S * per;
         unsigned long long prev = ~0ull;
-        for (int r = 0; r < a.Kp; ++r) {
+        if (a.sc)  // (tcgen05 screen: straight from the score row)
+            row_top_keys(a.sc + static_cast<size_t>(jw) * a.sld, a.tm + static_cast<size_t>(jw) * a.tld, a.npos,
+                         a.Kp, cands, red, tl_s, &ntl_s);
+        for (int r = 0; r < (a.sc ? 0 : a.Kp); ++r) {
             unsigned long long m = 0;
             for (int e = threadIdx.x; e < total; e += blockDim.x) {
                 const int s = e / per, rem = e - s * per;
@@ -1009,10 +1019,17 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         if (nj == 0) continue;
         const int b0 = wave_b0[w], nbt = wave_b0[w + 1] - b0;
         if (nbt > 0) {
-            const int psplit = std::max(1, std::min((max_nm + 7) / 8, (2 * 148 + nj - 1) / nj));
-            launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
-                       static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
-                       static_cast<const uint8_t*>(d_work), d_w, wstride);
+            // (latency-bound: one or two cells per warp, up to 16 CTAs per SM)
+            const int pcells = use_tc ? kwords : max_nm;
+            const int psplit = std::max(1, std::min((pcells + 7) / 8, (16 * 148 + nj - 1) / nj));
+            if (use_tc)  // weight rows of the GEMM, written in place
+                launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
+                           static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
+                           static_cast<const uint8_t*>(d_work), d_w8, kwords, kwords);
+            else
+                launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
+                           static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
+                           static_cast<const uint8_t*>(d_work), d_w, wstride, 0);
             ++launches;
             cudaEvent_t ea = nullptr, eb = nullptr;
             if (ctx->profiling) {
@@ -1025,13 +1042,8 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             q.j0 = j0;
             q.nj = nj;
             if (use_tc) {
-                launch_pdl(w8_scatter3d_kernel, dim3(nj), dim3(128), 0, st, static_cast<const Job3*>(d_jobs), j0,
-                           static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
-                           static_cast<const int32_t*>(d_w), wstride, g.tc, kwords, d_w8);
                 launch_ccf_tc(tcplan, npos, sld, kwords * 4, nj, d_sc, d_tm, st);
-                launch_pdl(keys3d_kernel, dim3(nj), dim3(128), 0, st, static_cast<const int32_t*>(d_sc),
-                           static_cast<const int32_t*>(d_tm), sld, tld, npos, sa.K, d_x);
-                launches += 3;
+                launches += 1;
                 ++ccf_launches;
             }
             for (int v = 0; v < (use_tc ? 0 : S_virt); ++v) {
@@ -1061,8 +1073,14 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         Select3Args q = se;
         q.j0 = j0;
         q.nj = nj;
-        if (use_tc) q.S = q.bps = q.nbox = 1;  // keys3d_kernel's single list per job
-        const int ssplit = std::max(1, std::min(g.T / 4, (2 * 148 + nj - 1) / nj));
+        if (use_tc) {  // the score rows and tile maxima instead of key lists
+            q.sc = d_sc;
+            q.tm = d_tm;
+            q.sld = sld;
+            q.tld = tld;
+            q.npos = npos;
+        }
+        const int ssplit = std::max(1, std::min(g.T / 4, (8 * 148 + nj - 1) / nj));
         launch_pdl(select3d_kernel, dim3(nj, ssplit), dim3(128), 0, st, q);
         ++launches;
     }
