@@ -138,31 +138,70 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
             const int cell = mask_cells[m_lo + i];
             m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
         }
-        int cnt[16] = {0};
-        for (int e = lane; e < B3; e += 32) {
-            const int x0 = m0 * B + e / (B * B), x1 = m1 * B + (e / B) % B, x2 = m2 * B + e % B;
-            const int x[3] = {x0, x1, x2};
-            bool sup = false;
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-                if ((shape >> a) & 1) {
-                    const bool asc = !((corner >> a) & 1);
-                    sup |= asc ? x[a] < g.OV : x[a] >= g.T - g.OV;
-                }
-            if (!sup) continue;
-            const int f = wk[(static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] + jb.P[2] + x2];
-#pragma unroll
-            for (int ch = 0; ch < 16; ++ch)
-                if (ch == f) ++cnt[ch];
-        }
         int wv[16];
         const int last = g.F - 1;
         int nlast = 0;
+        if (B3 <= 4096) {
+            // byte counters, four facies per word (a lane sees <= 128 cells),
+            // summed over the warp as 16-bit halves (<= 4096); B = 2^J: shifts
+            uint32_t c4[4] = {0, 0, 0, 0};
+            const int J = g.J, bm = B - 1;
+            for (int e = lane; e < B3; e += 32) {
+                const int x0 = m0 * B + (e >> (2 * J)), x1 = m1 * B + ((e >> J) & bm), x2 = m2 * B + (e & bm);
+                const int x[3] = {x0, x1, x2};
+                bool sup = false;
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
-            const int s = ch < g.F ? __reduce_add_sync(0xffffffffu, cnt[ch]) : 0;  // (uniform: F is a launch constant)
-            if (ch == last) nlast = s;
-            wv[ch] = s;
+                for (int a = 0; a < 3; ++a)
+                    if ((shape >> a) & 1) {
+                        const bool asc = !((corner >> a) & 1);
+                        sup |= asc ? x[a] < g.OV : x[a] >= g.T - g.OV;
+                    }
+                if (!sup) continue;
+                const int f = wk[(static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] + jb.P[2] + x2];
+                const uint32_t inc = 1u << ((f & 3) * 8);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if ((f >> 2) == q) c4[q] += inc;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t lo = 0, hi = 0;
+                if (4 * q < g.F) {  // (uniform: F is a launch constant)
+                    lo = __reduce_add_sync(0xffffffffu, c4[q] & 0x00FF00FFu);
+                    hi = __reduce_add_sync(0xffffffffu, (c4[q] >> 8) & 0x00FF00FFu);
+                }
+                wv[4 * q] = lo & 0xFFFF;
+                wv[4 * q + 1] = hi & 0xFFFF;
+                wv[4 * q + 2] = lo >> 16;
+                wv[4 * q + 3] = hi >> 16;
+            }
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch)
+                if (ch == last) nlast = wv[ch];
+        } else {
+            int cnt[16] = {0};
+            for (int e = lane; e < B3; e += 32) {
+                const int x0 = m0 * B + e / (B * B), x1 = m1 * B + (e / B) % B, x2 = m2 * B + e % B;
+                const int x[3] = {x0, x1, x2};
+                bool sup = false;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    if ((shape >> a) & 1) {
+                        const bool asc = !((corner >> a) & 1);
+                        sup |= asc ? x[a] < g.OV : x[a] >= g.T - g.OV;
+                    }
+                if (!sup) continue;
+                const int f = wk[(static_cast<size_t>(jb.P[0] + x0) * g.W[1] + jb.P[1] + x1) * g.W[2] + jb.P[2] + x2];
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch)
+                    if (ch == f) ++cnt[ch];
+            }
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+                const int s = ch < g.F ? __reduce_add_sync(0xffffffffu, cnt[ch]) : 0;  // (uniform)
+                if (ch == last) nlast = s;
+                wv[ch] = s;
+            }
         }
 #ifdef CCW_DEBUG3D
         if (lane == 0 && blockIdx.x == 0) printf("prep job %d cell %d (%d,%d,%d) counts %d %d %d %d\n", j0, i, m0, m1, m2, wv[0], wv[1], wv[2], wv[3]);
@@ -170,15 +209,134 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
         if (lane == 0) {
             if (g.mode == 0) {  // int8x4
                 uint32_t v = 0;
-                for (int ch = 0; ch < g.nscr; ++ch) {
-                    const int w = g.F > 1 ? wv[ch] - nlast : 0;
-                    v |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * ch);
-                }
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch)
+                    if (ch < g.nscr) {
+                        const int w = g.F > 1 ? wv[ch] - nlast : 0;
+                        v |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * ch);
+                    }
                 wout[i] = static_cast<int32_t>(v);
             } else {
-                for (int ch = 0; ch < g.nscr; ++ch) wout[i * g.nscr + ch] = g.F > 1 ? wv[ch] - nlast : 0;
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch)
+                    if (ch < g.nscr) wout[i * g.nscr + ch] = g.F > 1 ? wv[ch] - nlast : 0;
             }
         }
+    }
+}
+
+// The same weights for B <= 4 with B threads per coarse cell (one x0 plane of
+// the block each, <= 4 rows of <= 4 facies bytes): every row is loaded before
+// anything is counted (independent loads, always inside the work grid), a
+// facies' cells are counted as byte-equality masks (__vcmpeq4 + popc) under
+// the row's support mask, and the planes are summed with shuffles on byte
+// counters (a block has <= 64 cells).  The warp-per-cell kernel above is
+// instruction- and latency-bound at these block sizes.  W4: aligned 4-byte rows.
+template <int B, bool W4>
+__global__ void __launch_bounds__(128) prep3d_cell_kernel(Geo3 g, const Job3* __restrict__ jobs, int j0,
+                                                          const int* __restrict__ mask_off,
+                                                          const int* __restrict__ mask_cells,
+                                                          const uint8_t* __restrict__ work,
+                                                          int32_t* __restrict__ wbuf, int wstride, int tcrow) {
+    pdl_trigger();
+    pdl_wait();
+    const Job3 jb = jobs[j0 + blockIdx.x];
+    const int corner = jb.mask >> 3, shape = jb.mask & 7;
+    const int m_lo = mask_off[jb.bmask];
+    const int nm = tcrow > 0 ? tcrow : mask_off[jb.bmask + 1] - m_lo;
+    const int gi = blockIdx.y * blockDim.x + threadIdx.x;
+    const int i = gi / B, x0 = gi % B;  // (a cell's B threads share a warp)
+    int32_t* wout = wbuf + static_cast<size_t>(blockIdx.x) * wstride;
+    int m0 = 0, m1 = 0, m2 = 0;
+    bool live = i < nm;
+    if (live) {
+        if (tcrow > 0) {
+            m2 = i % g.tc, m1 = (i / g.tc) % g.tc, m0 = i / (g.tc * g.tc);
+            live = m0 < g.tc;  // (else row padding: weight 0)
+        } else {
+            const int cell = mask_cells[m_lo + i];
+            m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
+        }
+    }
+    // per axis: fine coordinates [lo, hi) of the template lie in the job's slab
+    int lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const bool on = (shape >> a) & 1, asc = !((corner >> a) & 1);
+        lo[a] = !on ? 1 : asc ? 0 : g.T - g.OV;
+        hi[a] = !on ? 0 : asc ? g.OV : g.T;
+    }
+    uint32_t rw[B];  // this plane's rows, B facies bytes each
+    uint32_t sm[B];  // 0xFF in the bytes of supported cells
+#pragma unroll
+    for (int x1 = 0; x1 < B; ++x1) rw[x1] = sm[x1] = 0;
+    if (live) {
+        const uint8_t* wk = work + static_cast<size_t>(jb.real) * g.W[0] * g.W[1] * g.W[2];
+        const uint8_t* base = wk + (static_cast<size_t>(jb.P[0] + m0 * B + x0) * g.W[1] + jb.P[1] + m1 * B) * g.W[2] +
+                              jb.P[2] + m2 * B;
+#pragma unroll
+        for (int x1 = 0; x1 < B; ++x1) {
+            const uint8_t* row = base + static_cast<size_t>(x1) * g.W[2];
+            if constexpr (W4) {
+                rw[x1] = *reinterpret_cast<const uint32_t*>(row);
+            } else {
+                uint32_t w = 0;
+#pragma unroll
+                for (int x2 = 0; x2 < B; ++x2) w |= static_cast<uint32_t>(row[x2]) << (8 * x2);
+                rw[x1] = w;
+            }
+        }
+        const int X0 = m0 * B + x0;
+        const bool s0 = X0 >= lo[0] && X0 < hi[0];
+        uint32_t m2mask = 0, all = 0;
+#pragma unroll
+        for (int x2 = 0; x2 < B; ++x2) {
+            const int X2 = m2 * B + x2;
+            all |= 0xFFu << (8 * x2);
+            if (X2 >= lo[2] && X2 < hi[2]) m2mask |= 0xFFu << (8 * x2);
+        }
+#pragma unroll
+        for (int x1 = 0; x1 < B; ++x1) {
+            const int X1 = m1 * B + x1;
+            sm[x1] = (s0 || (X1 >= lo[1] && X1 < hi[1])) ? all : m2mask;
+        }
+    }
+    uint32_t c4[4] = {0, 0, 0, 0};  // byte counters, four facies per word
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch)
+        if (ch < g.F) {  // (uniform: F is a launch constant)
+            int n = 0;
+#pragma unroll
+            for (int x1 = 0; x1 < B; ++x1) n += __popc(__vcmpeq4(rw[x1], 0x01010101u * ch) & sm[x1]);
+            c4[ch >> 2] += static_cast<uint32_t>(n >> 3) << (8 * (ch & 3));
+        }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (4 * q < g.F) {
+#pragma unroll
+            for (int o = 1; o < B; o <<= 1) c4[q] += __shfl_xor_sync(0xffffffffu, c4[q], o);
+        }
+    if (x0 != 0 || i >= nm) return;
+    int wv[16];
+    int nlast = 0;
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch) {
+        wv[ch] = (c4[ch >> 2] >> (8 * (ch & 3))) & 0xFF;
+        if (ch == g.F - 1) nlast = wv[ch];
+    }
+    if (g.mode == 0) {  // int8x4
+        uint32_t v = 0;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+            if (ch < g.nscr) {
+                const int w = g.F > 1 ? wv[ch] - nlast : 0;
+                v |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * ch);
+            }
+        wout[i] = static_cast<int32_t>(v);
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch)
+            if (ch < g.nscr) wout[i * g.nscr + ch] = g.F > 1 ? wv[ch] - nlast : 0;
     }
 }
 
@@ -1022,7 +1180,15 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             // (latency-bound: one or two cells per warp, up to 16 CTAs per SM)
             const int pcells = use_tc ? kwords : max_nm;
             const int psplit = std::max(1, std::min((pcells + 7) / 8, (16 * 148 + nj - 1) / nj));
-            if (use_tc)  // weight rows of the GEMM, written in place
+            if (g.B <= 4) {  // one thread per coarse cell
+                const int py = (pcells * g.B + 127) / 128;
+                auto pk = g.B == 4 ? (g.aligned4 ? prep3d_cell_kernel<4, true> : prep3d_cell_kernel<4, false>)
+                                   : prep3d_cell_kernel<2, false>;
+                launch_pdl(pk, dim3(nj, py), dim3(128), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
+                           static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
+                           static_cast<const uint8_t*>(d_work), use_tc ? d_w8 : d_w, use_tc ? kwords : wstride,
+                           use_tc ? kwords : 0);
+            } else if (use_tc)  // weight rows of the GEMM, written in place
                 launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
                            static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
                            static_cast<const uint8_t*>(d_work), d_w8, kwords, kwords);
