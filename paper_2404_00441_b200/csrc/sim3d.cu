@@ -637,6 +637,16 @@ __device__ void row_top_keys(const int32_t* __restrict__ sc, const int32_t* __re
             prev = m;
         }
         thr = static_cast<int>(static_cast<uint32_t>(m >> 32) ^ 0x80000000u);
+        if (K == 1) {
+            // the best window is in the first tile that holds the row maximum
+            const int t = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(m & 0xFFFFFFFFull));
+            unsigned long long b = 0;
+            for (int p = t * kTcTile + tid; p < min(npos, (t + 1) * kTcTile); p += nth)
+                b = umax64(b, key64(sc[p], static_cast<uint32_t>(p)));
+            b = block_max64(b, red);
+            if (tid == 0) cands[0] = b;
+            return;
+        }
     }
     if (tid == 0) *ntl = 0;
     __syncthreads();
@@ -781,6 +791,19 @@ __global__ void finalize3d_kernel(const uint8_t* __restrict__ work, int W0, int 
     const size_t n = static_cast<size_t>(s0) * s1 * s2;
     const uint8_t* wk = work + static_cast<size_t>(r) * W0 * W1 * W2;
     uint8_t* o = out + static_cast<size_t>(r) * n;
+    if (s2 % 4 == 0 && W2 % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(work) & 3) == 0) {  // 4-byte words: every row start is aligned on both sides
+        const int q2 = s2 >> 2;
+        for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n / 4;
+             e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const int x2 = static_cast<int>(e % q2) * 4;
+            const size_t rr = e / q2;
+            const int x1 = static_cast<int>(rr % s1), x0 = static_cast<int>(rr / s1);
+            *reinterpret_cast<uint32_t*>(o + 4 * e) =
+                *reinterpret_cast<const uint32_t*>(wk + (static_cast<size_t>(x0) * W1 + x1) * W2 + x2);
+        }
+        return;
+    }
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int x2 = static_cast<int>(e % s2);
