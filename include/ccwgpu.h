@@ -119,7 +119,7 @@ typedef struct ccw_timing {
     int64_t jobs;
     int64_t rescored;       /* windows rescored in fp64 (the exact-score tie groups)   */
     int64_t screened_jobs;  /* placements that went through the CCF screen            */
-    int64_t ccf_variant;    /* 0 none (normalized / F=1), 1 fp32 direct, 2 tcgen05 int8, 5 fused wave kernel; 3D: 3 / 4 by block-count width */
+    int64_t ccf_variant;    /* 0 none (normalized / F=1), 1 fp32 direct, 2 tcgen05 int8, 5 fused wave kernel; 3D: 3 / 4 by block-count width (dp4a / IMAD), 6 tcgen05 int8 over the 3D im2col */
     double ccf_mma_flop;    /* tensor-core MMA FLOP issued (full Tc x Tc window, padded K) */
     int64_t groups;         /* realization groups run concurrently on separate streams */
     int64_t list_overflows; /* placements with more than 256 windows at or above the tile bound */

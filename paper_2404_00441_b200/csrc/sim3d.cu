@@ -107,9 +107,11 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
                                                      const int* __restrict__ mask_cells,
                                                      const uint8_t* __restrict__ work, int32_t* __restrict__ wbuf,
                                                      int wstride, int tcrow) {
-    // tcrow > 0 (tcgen05 screen): wbuf rows are the GEMM's weight rows, one
-    // packed word per WINDOW cell (row stride tcrow words, zero off the job's
-    // own overlap support); else one entry per cell of the batch's mask.
+    // tcrow > 0 (tcgen05 screen of 9-bit counts, see im2col3d_digits_kernel):
+    // wbuf holds THREE int8 GEMM rows per job (row stride wstride * 4 / 3
+    // bytes), two digit bytes per (window cell, channel) over all tcrow = tc^3
+    // window cells (zero off the job's own overlap support); else one int32
+    // entry per cell of the batch's mask and channel.
     pdl_trigger();
     pdl_wait();
     const Job3 jb = jobs[j0 + blockIdx.x];
@@ -123,17 +125,15 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
     const int nw = blockDim.x >> 5;
     for (int i = blockIdx.y * nw + warp; i < nm; i += gridDim.y * nw) {
         int m0, m1, m2;
+        int B3e = B3;  // (0: the block touches none of the job's slabs, nothing to count)
         if (tcrow > 0) {
             m2 = i % g.tc, m1 = (i / g.tc) % g.tc, m0 = i / (g.tc * g.tc);
             const int m[3] = {m0, m1, m2};
-            bool any = false;  // does the block touch one of the job's slabs at all?
+            bool any = false;
 #pragma unroll
             for (int a = 0; a < 3; ++a)
                 if ((shape >> a) & 1) any |= !((corner >> a) & 1) ? m[a] * B < g.OV : m[a] * B + B > g.T - g.OV;
-            if (!any || m0 >= g.tc) {
-                if (lane == 0) wout[i] = 0;
-                continue;
-            }
+            if (!any) B3e = 0;
         } else {
             const int cell = mask_cells[m_lo + i];
             m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
             // summed over the warp as 16-bit halves (<= 4096); B = 2^J: shifts
             uint32_t c4[4] = {0, 0, 0, 0};
             const int J = g.J, bm = B - 1;
-            for (int e = lane; e < B3; e += 32) {
+            for (int e = lane; e < B3e; e += 32) {
                 const int x0 = m0 * B + (e >> (2 * J)), x1 = m1 * B + ((e >> J) & bm), x2 = m2 * B + (e & bm);
                 const int x[3] = {x0, x1, x2};
                 bool sup = false;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
                 if (ch == last) nlast = wv[ch];
         } else {
             int cnt[16] = {0};
-            for (int e = lane; e < B3; e += 32) {
+            for (int e = lane; e < B3e; e += 32) {
                 const int x0 = m0 * B + e / (B * B), x1 = m1 * B + (e / B) % B, x2 = m2 * B + e % B;
                 const int x[3] = {x0, x1, x2};
                 bool sup = false;
@@ -207,7 +207,22 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
         if (lane == 0 && blockIdx.x == 0) printf("prep job %d cell %d (%d,%d,%d) counts %d %d %d %d\n", j0, i, m0, m1, m2, wv[0], wv[1], wv[2], wv[3]);
 #endif
         if (lane == 0) {
-            if (g.mode == 0) {  // int8x4
+            if (tcrow > 0) {
+                // w = 32 hi + lo, lo in [0, 32), |hi| <= 16; against x = 32 xh + xl:
+                // row 1 . X = sum hi xh, row 2 . X = sum (lo xh + hi xl), row 3 . X = sum lo xl
+                const int kbytes = wstride * 4 / 3;
+                int8_t* r1 = reinterpret_cast<int8_t*>(wout);
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch)
+                    if (ch < g.nscr) {
+                        const int w = g.F > 1 ? wv[ch] - nlast : 0;
+                        const uint32_t wl = static_cast<uint32_t>(w & 31), wh = static_cast<uint32_t>(w >> 5) & 0xFFu;
+                        const int off = (i * g.nscr + ch) * 2;
+                        *reinterpret_cast<uint16_t*>(r1 + off) = static_cast<uint16_t>(wh);
+                        *reinterpret_cast<uint16_t*>(r1 + kbytes + off) = static_cast<uint16_t>(wl | (wh << 8));
+                        *reinterpret_cast<uint16_t*>(r1 + 2 * kbytes + off) = static_cast<uint16_t>(wl << 8);
+                    }
+            } else if (g.mode == 0) {  // int8x4
                 uint32_t v = 0;
 #pragma unroll
                 for (int ch = 0; ch < 4; ++ch)
@@ -566,6 +581,61 @@ __global__ void im2col3d_kernel(const int32_t* __restrict__ tipk, int c1, int c2
             v = tipk[(static_cast<size_t>(p0 + m0) * c1 + p1 + m1) * c2 + p2 + m2];
         }
         X[e] = v;
+    }
+}
+
+// Counts up to 512 (J = 3: mode 1) as two int8 digits, x = 32 xh + xl: per
+// (window cell, channel) the bytes (xh, xl), K = 2 nscr tc^3 bytes.  With the
+// prep's three weight rows per job the exact score is
+// 1024 row1 + 32 row2 + row3 (keys3d_digits_kernel).
+__global__ void im2col3d_digits_kernel(const int32_t* __restrict__ tipk, size_t ncell, int c1, int c2, int o1,
+                                       int o2, int tc, int nscr, int npos, int kbytes, int8_t* __restrict__ X) {
+    const int per = tc * tc * tc * nscr;
+    const size_t total = static_cast<size_t>(npos) * per;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int pos = static_cast<int>(e / per), k = static_cast<int>(e - static_cast<size_t>(pos) * per);
+        const int ch = k % nscr, cell = k / nscr;
+        const int m2 = cell % tc, m1 = (cell / tc) % tc, m0 = cell / (tc * tc);
+        const int p2 = pos % o2, p1 = (pos / o2) % o1, p0 = pos / (o2 * o1);
+        const int x = tipk[ch * ncell + (static_cast<size_t>(p0 + m0) * c1 + p1 + m1) * c2 + p2 + m2];
+        *reinterpret_cast<uint16_t*>(X + static_cast<size_t>(pos) * kbytes + 2 * k) =
+            static_cast<uint16_t>((x >> 5) | ((x & 31) << 8));
+    }
+}
+
+// Per job and position chunk: the K best packed keys of the combined score
+// 1024 row1 + 32 row2 + row3, as one "box" list of select3d's merge.
+__global__ void __launch_bounds__(256) keys3d_digits_kernel(const int32_t* __restrict__ sc, int sld, int npos,
+                                                            int K, unsigned long long* __restrict__ xbuf) {
+    __shared__ unsigned long long red[8];
+    pdl_trigger();
+    pdl_wait();
+    const int j = blockIdx.x, ns = gridDim.y, s = blockIdx.y, tid = threadIdx.x;
+    const int32_t* r1 = sc + static_cast<size_t>(3 * j) * sld;
+    const int32_t* r2 = r1 + sld;
+    const int32_t* r3 = r2 + sld;
+    const int chunk = (npos + ns - 1) / ns;
+    const int p_lo = s * chunk, p_hi = min(npos, p_lo + chunk);
+    unsigned long long prev = ~0ull;
+    for (int r = 0; r < K; ++r) {
+        unsigned long long m = 0;
+        for (int p = p_lo + tid; p < p_hi; p += 256) {
+            const int S = 1024 * r1[p] + 32 * r2[p] + r3[p];
+            const unsigned long long key =
+                (static_cast<unsigned long long>(static_cast<uint32_t>(S) ^ 0x80000000u) << 32) |
+                (0xFFFFFFFFu - static_cast<uint32_t>(p));
+            if (key < prev) m = umax64(m, key);
+        }
+        m = warp_max64(m);
+        __syncthreads();
+        if ((tid & 31) == 0) red[tid >> 5] = m;
+        __syncthreads();
+        m = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) m = umax64(m, red[w]);
+        if (tid == 0) xbuf[(static_cast<size_t>(j) * ns + s) * K + r] = m;
+        prev = m;
     }
 }
 
@@ -1089,6 +1159,13 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     const bool use_tc = ctx->opt.tc3d && mode == 0 && S == 1 && !ctx->nccl_comm && Kp >= 1 &&
                         static_cast<size_t>(npos) * kwords * 4 <= (size_t(4) << 30) &&
                         static_cast<size_t>(max_wave) * sld * 4 <= (size_t(2) << 30);
+    // ... and 9-bit counts (mode 1, B^3 <= 512: config 4) as two int8 digits,
+    // three GEMM rows per job (im2col3d_digits_kernel)
+    const int kdig = ((2 * g.nscr * tc3 + 127) / 128) * 128;  // K bytes
+    const int nsplit = 8;                                      // position chunks per job (keys3d_digits_kernel)
+    const bool use_dig = ctx->opt.tc3d && mode == 1 && g.B * g.B * g.B <= 512 && S == 1 && !ctx->nccl_comm &&
+                         Kp >= 1 && static_cast<size_t>(npos) * kdig <= (size_t(4) << 30) &&
+                         static_cast<size_t>(max_wave) * 3 * sld * 4 <= (size_t(2) << 30);
 
     const bool host_t = debug_env("CCW_HOSTT") != nullptr;
     auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(); };
@@ -1146,6 +1223,29 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         d_tm = ctx->tc3_tm.as<int32_t>(static_cast<size_t>(max_wave) * tld);
         const int8_t* X = ti3d_im2col(ti, g, npos, kwords, st);
         tcplan = plan_ccf_tc(reinterpret_cast<const int8_t*>(d_w8), maxj, X, npos, kwords * 4);
+    }
+    if (use_dig) {
+        const int maxj = ((3 * max_wave + 127) / 128) * 128;
+        d_w8 = ctx->tc3_w.as<int32_t>(static_cast<size_t>(maxj) * kdig / 4);
+        CCW_CUDA(cudaMemsetAsync(d_w8, 0, static_cast<size_t>(maxj) * kdig, st));  // (K padding stays zero)
+        d_sc = ctx->tc3_sc.as<int32_t>(static_cast<size_t>(3 * max_wave) * sld);
+        d_tm = ctx->tc3_tm.as<int32_t>(static_cast<size_t>(3 * max_wave) * tld);
+        auto it = ti->im2col.find(-g.tc);  // (digit layout: keyed by -tc)
+        int8_t* X = it != ti->im2col.end() ? it->second : nullptr;
+        if (!X) {
+            const size_t bytes = static_cast<size_t>(npos) * kdig;
+            X = static_cast<int8_t*>(cache_alloc(ti->device, bytes));
+            CCW_CUDA(cudaMemsetAsync(X, 0, bytes, st));
+            const size_t total = static_cast<size_t>(npos) * tc3 * g.nscr;
+            im2col3d_digits_kernel<<<static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, st>>>(
+                ti->d_pk, static_cast<size_t>(g.c[0]) * g.c[1] * g.c[2], g.c[1], g.c[2], g.o[1], g.o[2], g.tc, g.nscr,
+                npos, kdig, X);
+            CCW_CUDA(cudaGetLastError());
+            ti->im2col[-g.tc] = X;
+        }
+        tcplan = plan_ccf_tc(reinterpret_cast<const int8_t*>(d_w8), maxj, X, npos, kdig);
+        d_x = ctx->xrec.as<unsigned long long>(
+            std::max(static_cast<size_t>(S) * max_wave * bps, static_cast<size_t>(max_wave) * nsplit) * std::max(Kp, 1));
     }
     void (*screen)(Screen3Args) = nullptr;
     if (mode == 0)
@@ -1211,11 +1311,12 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
                            static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
                            static_cast<const uint8_t*>(d_work), use_tc ? d_w8 : d_w, use_tc ? kwords : wstride,
                            use_tc ? kwords : 0);
-            } else if (use_tc)  // weight rows of the GEMM, written in place
-                launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
+            } else if (use_dig) {  // three digit rows per job, written in place
+                const int ps = std::max(1, std::min((tc3 + 7) / 8, (16 * 148 + nj - 1) / nj));
+                launch_pdl(prep3d_kernel, dim3(nj, ps), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
                            static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
-                           static_cast<const uint8_t*>(d_work), d_w8, kwords, kwords);
-            else
+                           static_cast<const uint8_t*>(d_work), d_w8, 3 * kdig / 4, tc3);
+            } else
                 launch_pdl(prep3d_kernel, dim3(nj, psplit), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
                            static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
                            static_cast<const uint8_t*>(d_work), d_w, wstride, 0);
@@ -1235,7 +1336,14 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
                 launches += 1;
                 ++ccf_launches;
             }
-            for (int v = 0; v < (use_tc ? 0 : S_virt); ++v) {
+            if (use_dig) {
+                launch_ccf_tc(tcplan, npos, sld, kdig, 3 * nj, d_sc, d_tm, st);
+                launch_pdl(keys3d_digits_kernel, dim3(nj, nsplit), dim3(256), 0, st, static_cast<const int32_t*>(d_sc),
+                           sld, npos, sa.K, d_x);
+                launches += 2;
+                ++ccf_launches;
+            }
+            for (int v = 0; v < (use_tc || use_dig ? 0 : S_virt); ++v) {
                 const int s = ctx->shard_rank * S_virt + v;
                 q.box0 = std::min(nbox, s * bps);
                 q.box1 = std::min(nbox, (s + 1) * bps);
@@ -1268,6 +1376,10 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             q.sld = sld;
             q.tld = tld;
             q.npos = npos;
+        }
+        if (use_dig) {  // keys3d_digits_kernel's chunk lists
+            q.S = 1;
+            q.bps = q.nbox = nsplit;
         }
         const int ssplit = std::max(1, std::min(g.T / 4, (8 * 148 + nj - 1) / nj));
         launch_pdl(select3d_kernel, dim3(nj, ssplit), dim3(128), 0, st, q);
@@ -1324,7 +1436,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     ctx->timing.waves = max_key + 1;
     ctx->timing.jobs = static_cast<int64_t>(njobs);
     ctx->timing.screened_jobs = static_cast<int64_t>(njobs) - n_real;
-    ctx->timing.ccf_variant = use_tc ? 6 : mode == 0 ? 3 : 4;
+    ctx->timing.ccf_variant = use_tc ? 6 : use_dig ? 7 : mode == 0 ? 3 : 4;
     ctx->timing.groups = 1;
     ctx->timing.d2h_bytes = h_out ? static_cast<int64_t>(sgvol * n_real) : 0;
     (void)ccf_launches;

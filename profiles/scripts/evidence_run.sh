@@ -12,8 +12,11 @@ ncu --set full --clock-control none --import-source on -k regex:ccf_tc_kernel -s
     -o gpurun_out/ccf python $B1 > gpurun_out/ncu_ccf.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:select_fast_kernel -s 200 -c 1 \
     -o gpurun_out/sel python $B1 > gpurun_out/ncu_sel.log 2>&1
-WHICH=3 REPS=1 ncu --set full --clock-control none --import-source on -k regex:screen3d -s 40 -c 1 \
+# config 3 screens on the tensor cores (option tc3d, default on): the 2D ccf_tc_kernel over the 3D im2col
+WHICH=3 REPS=1 ncu --set full --clock-control none --import-source on -k regex:ccf_tc -s 20 -c 1 \
     -o gpurun_out/s3d python profiles/scripts/config3_run.py > gpurun_out/ncu_s3d.log 2>&1
+WHICH=3 REPS=1 PROF=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches3d.csv \
+    python profiles/scripts/config3_run.py > gpurun_out/ncu_list3d.log 2>&1
 WHICH=4 REPS=1 ncu --set full --clock-control none --import-source on -k regex:screen3d -s 40 -c 1 \
     -o gpurun_out/s4d python profiles/scripts/config3_run.py > gpurun_out/ncu_s4d.log 2>&1
 REPS=1 ncu --set full --clock-control none --import-source on -k regex:select_bulk -s 120 -c 1 \
