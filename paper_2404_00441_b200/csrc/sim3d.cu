@@ -146,7 +146,46 @@ __global__ void __launch_bounds__(256) prep3d_kernel(Geo3 g, const Job3* __restr
             // summed over the warp as 16-bit halves (<= 4096); B = 2^J: shifts
             uint32_t c4[4] = {0, 0, 0, 0};
             const int J = g.J, bm = B - 1;
-            for (int e = lane; e < B3e; e += 32) {
+            const bool fast8 = B == 8 && g.aligned4;
+            if (fast8 && B3e) {
+                // B = 8, aligned rows: the block is 64 rows of two 4-byte words; a
+                // lane loads its four words up front (independent, inside the
+                // work grid) and counts a facies as byte-equality masks under
+                // the word's support mask (as prep3d_cell_kernel)
+                int lo3[3], hi3[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const bool on = (shape >> a) & 1, asc = !((corner >> a) & 1);
+                    lo3[a] = !on ? 1 : asc ? 0 : g.T - g.OV;
+                    hi3[a] = !on ? 0 : asc ? g.OV : g.T;
+                }
+                uint32_t wd[4], sm[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int wi = lane + 32 * k, row = wi >> 1, half = wi & 1;
+                    const int X0 = m0 * 8 + (row >> 3), X1 = m1 * 8 + (row & 7), X2 = m2 * 8 + half * 4;
+                    wd[k] = *reinterpret_cast<const uint32_t*>(
+                        wk + (static_cast<size_t>(jb.P[0] + X0) * g.W[1] + jb.P[1] + X1) * g.W[2] + jb.P[2] + X2);
+                    uint32_t m = 0;
+                    if ((X0 >= lo3[0] && X0 < hi3[0]) || (X1 >= lo3[1] && X1 < hi3[1])) {
+                        m = 0xFFFFFFFFu;
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if (X2 + b >= lo3[2] && X2 + b < hi3[2]) m |= 0xFFu << (8 * b);
+                    }
+                    sm[k] = m;
+                }
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch)
+                    if (ch < g.F) {  // (uniform)
+                        int n = 0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) n += __popc(__vcmpeq4(wd[k], 0x01010101u * ch) & sm[k]);
+                        c4[ch >> 2] += static_cast<uint32_t>(n >> 3) << (8 * (ch & 3));
+                    }
+            }
+            for (int e = lane; e < (fast8 ? 0 : B3e); e += 32) {
                 const int x0 = m0 * B + (e >> (2 * J)), x1 = m1 * B + ((e >> J) & bm), x2 = m2 * B + (e & bm);
                 const int x[3] = {x0, x1, x2};
                 bool sup = false;
