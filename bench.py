@@ -507,7 +507,9 @@ def measure_3d(which, dev, lib, local, args, skip_cpu=False):
     step_device()
     prof = dev.last_timing()
     dev.set_profiling(False)
-    tc3 = prof["ccf_variant"] == 6  # tcgen05 int8 screen over the 3D im2col (option tc3d)
+    # tcgen05 int8 screen over the 3D im2col (option tc3d): 6 int8 counts, 7 9-bit counts as two digits
+    tc3 = prof["ccf_variant"] in (6, 7)
+    digits = prof["ccf_variant"] == 7
     kind = 1 if prof["ccf_variant"] == 3 else 0
     peak = dev.measure_i8_peak() if tc3 else dev.measure_int_peak(kind)
     achieved = prof["ccf_flop"] / (prof["ccf_ms"] * 1e-3) / 1e12 if prof["ccf_ms"] else None
@@ -534,11 +536,13 @@ def measure_3d(which, dev, lib, local, args, skip_cpu=False):
     e2e_equal = bool(np.array_equal(h_pin.numpy().reshape(got.shape), got))
     out = {"workload": label, "value": n_real * sgv * steps / (total_ms * 1e-3), "unit": UNIT,
            "ms_per_step": total_ms / steps, "steps": steps, "gpu_launches": launches * steps,
-           "dtype": "i8xi8->i32 tcgen05 (exact)" if tc3 else
+           "dtype": ("i8xi8->i32 tcgen05, 9-bit counts as two int8 digits (exact)" if digits else
+                     "i8xi8->i32 tcgen05 (exact)") if tc3 else
                     "int8x4 dp4a -> int32 (exact)" if kind == 1 else "int32 IMAD (exact)",
            "roofline": {"bound": "tensor" if tc3 else "int (CUDA cores)",
-                        "kernel": "w8_scatter3d + ccf_tc_kernel (tcgen05 kind::i8 over the 3D im2col) + keys3d"
-                                  if tc3 else "screen3d_kernel (%s)" % ("dp4a" if kind == 1 else "IMAD"),
+                        "kernel": ("ccf_tc_kernel (tcgen05 kind::i8 over the two-digit 3D im2col, three rows per "
+                                   "placement) + keys3d_digits_kernel" if digits else
+                                   "ccf_tc_kernel (tcgen05 kind::i8 over the 3D im2col)") if tc3 else "screen3d_kernel (%s)" % ("dp4a" if kind == 1 else "IMAD"),
                         "achieved": achieved, "peak": peak, "unit": "TOPS",
                         "frac": achieved / peak if achieved and peak else None,
                         "peak_source": "measured in this run: tcgen05 kind::i8 MMA probe (ccw_measure_i8_peak)"

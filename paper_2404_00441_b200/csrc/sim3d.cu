@@ -1420,7 +1420,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             q.S = 1;
             q.bps = q.nbox = nsplit;
         }
-        const int ssplit = std::max(1, std::min(g.T / 4, (8 * 148 + nj - 1) / nj));
+        const int ssplit = std::max(1, std::min(g.T, (16 * 148 + nj - 1) / nj));
         launch_pdl(select3d_kernel, dim3(nj, ssplit), dim3(128), 0, st, q);
         ++launches;
     }

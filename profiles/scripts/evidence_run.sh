@@ -17,8 +17,10 @@ WHICH=3 REPS=1 ncu --set full --clock-control none --import-source on -k regex:c
     -o gpurun_out/s3d python profiles/scripts/config3_run.py > gpurun_out/ncu_s3d.log 2>&1
 WHICH=3 REPS=1 PROF=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches3d.csv \
     python profiles/scripts/config3_run.py > gpurun_out/ncu_list3d.log 2>&1
-WHICH=4 REPS=1 ncu --set full --clock-control none --import-source on -k regex:screen3d -s 40 -c 1 \
+WHICH=4 REPS=1 ncu --set full --clock-control none --import-source on -k regex:ccf_tc -s 20 -c 1 \
     -o gpurun_out/s4d python profiles/scripts/config3_run.py > gpurun_out/ncu_s4d.log 2>&1
+WHICH=4 REPS=1 PROF=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches4d.csv \
+    python profiles/scripts/config3_run.py > gpurun_out/ncu_list4d.log 2>&1
 REPS=1 ncu --set full --clock-control none --import-source on -k regex:select_bulk -s 120 -c 1 \
     -o gpurun_out/bulk python profiles/scripts/config2_run.py > gpurun_out/ncu_bulk.log 2>&1
 tail -c 400 gpurun_out/b.log; tail -c 300 gpurun_out/bref.log

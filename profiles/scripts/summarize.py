@@ -79,7 +79,7 @@ if __name__ == "__main__":
     launch_shares(tag)
     ncu_summary(tag, "ccf", "ccf_tc_kernel")
     ncu_summary(tag, "sel", "select_fast_kernel")
-    for rep, kern in (("s3d", "ccf_tc_kernel over the 3D im2col (config 3, option tc3d)"), ("s4d", "screen3d_kernel (config 4)"),
+    for rep, kern in (("s3d", "ccf_tc_kernel over the 3D im2col (config 3, option tc3d)"), ("s4d", "ccf_tc_kernel over the two-digit 3D im2col (config 4, option tc3d)"),
                       ("bulk", "select_bulk_kernel (config 2)"), ("wave", "wave_kernel<16> (experimental)")):
         if os.path.exists(os.path.join(OUT, rep + ".ncu-rep")):
             ncu_summary(tag, rep, kern)
