@@ -306,7 +306,6 @@ __global__ void __launch_bounds__(128) prep3d_cell_kernel(Geo3 g, const Job3* __
     if (live) {
         if (tcrow > 0) {
             m2 = i % g.tc, m1 = (i / g.tc) % g.tc, m0 = i / (g.tc * g.tc);
-            live = m0 < g.tc;  // (else row padding: weight 0)
         } else {
             const int cell = mask_cells[m_lo + i];
             m0 = cell >> 16, m1 = (cell >> 8) & 0xFF, m2 = cell & 0xFF;
@@ -386,7 +385,15 @@ __global__ void __launch_bounds__(128) prep3d_cell_kernel(Geo3 g, const Job3* __
                 const int w = g.F > 1 ? wv[ch] - nlast : 0;
                 v |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * ch);
             }
-        wout[i] = static_cast<int32_t>(v);
+        if (tcrow > 0) {  // GEMM row: max(nscr, 1) channel bytes per window cell
+            const int bpc = max(g.nscr, 1);
+            int8_t* r8 = reinterpret_cast<int8_t*>(wout) + i * bpc;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+                if (ch < bpc) r8[ch] = static_cast<int8_t>((v >> (8 * ch)) & 0xFFu);
+        } else {
+            wout[i] = static_cast<int32_t>(v);
+        }
     } else {
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch)
@@ -607,19 +614,20 @@ __global__ void __launch_bounds__(S3_THREADS) screen3d_kernel(Screen3Args a) {
 // (zero off the job's overlap support, so the full-window product equals the
 // masked sum of screen3d_kernel bit for bit).
 __global__ void im2col3d_kernel(const int32_t* __restrict__ tipk, int c1, int c2, int o1, int o2, int tc,
-                                int npos, int kwords, int32_t* __restrict__ X) {
+                                int npos, int bpc, int kbytes, int8_t* __restrict__ X) {
+    // bpc = screen channels (1..4): byte cell * bpc + ch of a position's row is
+    // channel ch's count of window cell (m0, m1, m2), cell = (m0 tc + m1) tc + m2;
+    // the row padding up to kbytes was zeroed by the caller
     const int tc3 = tc * tc * tc;
-    const size_t total = static_cast<size_t>(npos) * kwords;
+    const size_t total = static_cast<size_t>(npos) * tc3;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int pos = static_cast<int>(e / kwords), cell = static_cast<int>(e - static_cast<size_t>(pos) * kwords);
-        int32_t v = 0;
-        if (cell < tc3) {
-            const int m2 = cell % tc, m1 = (cell / tc) % tc, m0 = cell / (tc * tc);
-            const int p2 = pos % o2, p1 = (pos / o2) % o1, p0 = pos / (o2 * o1);
-            v = tipk[(static_cast<size_t>(p0 + m0) * c1 + p1 + m1) * c2 + p2 + m2];
-        }
-        X[e] = v;
+        const int pos = static_cast<int>(e / tc3), cell = static_cast<int>(e - static_cast<size_t>(pos) * tc3);
+        const int m2 = cell % tc, m1 = (cell / tc) % tc, m0 = cell / (tc * tc);
+        const int p2 = pos % o2, p1 = (pos / o2) % o1, p0 = pos / (o2 * o1);
+        const uint32_t v = static_cast<uint32_t>(tipk[(static_cast<size_t>(p0 + m0) * c1 + p1 + m1) * c2 + p2 + m2]);
+        int8_t* x = X + static_cast<size_t>(pos) * kbytes + cell * bpc;
+        for (int ch = 0; ch < bpc; ++ch) x[ch] = static_cast<int8_t>((v >> (8 * ch)) & 0xFFu);
     }
 }
 
@@ -959,17 +967,19 @@ void build_pyramid3d(ccw_ti3d* ti, cudaStream_t st) {
 }
 
 // im2col of the packed TI counts for the tcgen05 screen (cached on the TI):
-// [npos][kwords] words, window cell (m0, m1, m2) at word (m0 tc + m1) tc + m2.
-static const int8_t* ti3d_im2col(ccw_ti3d* ti, const Geo3& g, int npos, int kwords, cudaStream_t st) {
+// [npos][kbytes] int8, bpc channel bytes per window cell.
+static const int8_t* ti3d_im2col(ccw_ti3d* ti, const Geo3& g, int npos, int bpc, int kbytes, cudaStream_t st) {
     auto it = ti->im2col.find(g.tc);
     if (it != ti->im2col.end()) return it->second;
-    const size_t total = static_cast<size_t>(npos) * kwords;
-    int32_t* X = static_cast<int32_t*>(cache_alloc(ti->device, total * sizeof(int32_t)));
+    const size_t bytes = static_cast<size_t>(npos) * kbytes;
+    int8_t* X = static_cast<int8_t*>(cache_alloc(ti->device, bytes));
+    CCW_CUDA(cudaMemsetAsync(X, 0, bytes, st));
+    const size_t total = static_cast<size_t>(npos) * g.tc * g.tc * g.tc;
     const unsigned nb = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 32));
-    im2col3d_kernel<<<std::max(nb, 1u), 256, 0, st>>>(ti->d_pk, g.c[1], g.c[2], g.o[1], g.o[2], g.tc, npos, kwords, X);
+    im2col3d_kernel<<<std::max(nb, 1u), 256, 0, st>>>(ti->d_pk, g.c[1], g.c[2], g.o[1], g.o[2], g.tc, npos, bpc, kbytes, X);
     CCW_CUDA(cudaGetLastError());
-    ti->im2col[g.tc] = reinterpret_cast<int8_t*>(X);
-    return reinterpret_cast<int8_t*>(X);
+    ti->im2col[g.tc] = X;
+    return X;
 }
 
 void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, const uint64_t* seeds, int n_real,
@@ -1192,11 +1202,12 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     const int bps = (nbox + S - 1) / S;
     // ---- tcgen05 screen (option tc3d): int8 block counts, unsharded ----
     const int tc3 = g.tc * g.tc * g.tc;
-    const int kwords = ((tc3 + 31) / 32) * 32;  // K = 4 kwords bytes, whole 128-byte stages
+    const int bpc = std::max(g.nscr, 1);                  // channel bytes per window cell
+    const int kbytes = ((tc3 * bpc + 127) / 128) * 128;  // K, whole 128-byte stages
     const int sld = (npos + 3) & ~3;
     const int tld = tc_tiles(npos);
     const bool use_tc = ctx->opt.tc3d && mode == 0 && S == 1 && !ctx->nccl_comm && Kp >= 1 &&
-                        static_cast<size_t>(npos) * kwords * 4 <= (size_t(4) << 30) &&
+                        static_cast<size_t>(npos) * kbytes <= (size_t(4) << 30) &&
                         static_cast<size_t>(max_wave) * sld * 4 <= (size_t(2) << 30);
     // ... and 9-bit counts (mode 1, B^3 <= 512: config 4) as two int8 digits,
     // three GEMM rows per job (im2col3d_digits_kernel)
@@ -1257,11 +1268,12 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     int32_t* d_tm = nullptr;
     if (use_tc) {
         const int maxj = ((max_wave + 127) / 128) * 128;
-        d_w8 = ctx->tc3_w.as<int32_t>(static_cast<size_t>(maxj) * kwords);
+        d_w8 = ctx->tc3_w.as<int32_t>(static_cast<size_t>(maxj) * kbytes / 4);
+        CCW_CUDA(cudaMemsetAsync(d_w8, 0, static_cast<size_t>(maxj) * kbytes, st));  // (K padding stays zero)
         d_sc = ctx->tc3_sc.as<int32_t>(static_cast<size_t>(max_wave) * sld);
         d_tm = ctx->tc3_tm.as<int32_t>(static_cast<size_t>(max_wave) * tld);
-        const int8_t* X = ti3d_im2col(ti, g, npos, kwords, st);
-        tcplan = plan_ccf_tc(reinterpret_cast<const int8_t*>(d_w8), maxj, X, npos, kwords * 4);
+        const int8_t* X = ti3d_im2col(ti, g, npos, bpc, kbytes, st);
+        tcplan = plan_ccf_tc(reinterpret_cast<const int8_t*>(d_w8), maxj, X, npos, kbytes);
     }
     if (use_dig) {
         const int maxj = ((3 * max_wave + 127) / 128) * 128;
@@ -1340,7 +1352,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
         const int b0 = wave_b0[w], nbt = wave_b0[w + 1] - b0;
         if (nbt > 0) {
             // (latency-bound: one or two cells per warp, up to 16 CTAs per SM)
-            const int pcells = use_tc ? kwords : max_nm;
+            const int pcells = use_tc ? tc3 : max_nm;
             const int psplit = std::max(1, std::min((pcells + 7) / 8, (16 * 148 + nj - 1) / nj));
             if (g.B <= 4) {  // one thread per coarse cell
                 const int py = (pcells * g.B + 127) / 128;
@@ -1348,8 +1360,8 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
                                    : prep3d_cell_kernel<2, false>;
                 launch_pdl(pk, dim3(nj, py), dim3(128), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
                            static_cast<const int*>(d_moff), static_cast<const int*>(d_mcells),
-                           static_cast<const uint8_t*>(d_work), use_tc ? d_w8 : d_w, use_tc ? kwords : wstride,
-                           use_tc ? kwords : 0);
+                           static_cast<const uint8_t*>(d_work), use_tc ? d_w8 : d_w, use_tc ? kbytes / 4 : wstride,
+                           use_tc ? tc3 : 0);
             } else if (use_dig) {  // three digit rows per job, written in place
                 const int ps = std::max(1, std::min((tc3 + 7) / 8, (16 * 148 + nj - 1) / nj));
                 launch_pdl(prep3d_kernel, dim3(nj, ps), dim3(256), 0, st, g, static_cast<const Job3*>(d_jobs), j0,
@@ -1371,7 +1383,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
             q.j0 = j0;
             q.nj = nj;
             if (use_tc) {
-                launch_ccf_tc(tcplan, npos, sld, kwords * 4, nj, d_sc, d_tm, st);
+                launch_ccf_tc(tcplan, npos, sld, kbytes, nj, d_sc, d_tm, st);
                 launches += 1;
                 ++ccf_launches;
             }
