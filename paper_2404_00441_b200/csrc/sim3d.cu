@@ -1212,7 +1212,7 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     // ... and 9-bit counts (mode 1, B^3 <= 512: config 4) as two int8 digits,
     // three GEMM rows per job (im2col3d_digits_kernel)
     const int kdig = ((2 * g.nscr * tc3 + 127) / 128) * 128;  // K bytes
-    const int nsplit = 8;                                      // position chunks per job (keys3d_digits_kernel)
+    const int nsplit = 32;                                     // position chunks per job (keys3d_digits_kernel)
     const bool use_dig = ctx->opt.tc3d && mode == 1 && g.B * g.B * g.B <= 512 && S == 1 && !ctx->nccl_comm &&
                          Kp >= 1 && static_cast<size_t>(npos) * kdig <= (size_t(4) << 30) &&
                          static_cast<size_t>(max_wave) * 3 * sld * 4 <= (size_t(2) << 30);
