@@ -555,7 +555,8 @@ def measure_3d(which, dev, lib, local, args, skip_cpu=False):
                         "screen_ms_per_step": prof["ccf_ms"], "step_ms_profiled": prof["total_ms"]},
            "e2e": {"value": n_real * sgv * steps / e2e_s, "unit": UNIT,
                    "h2d_bytes_per_step": int(ti_a.nbytes + seeds.nbytes + (hd_a.nbytes if hd_a is not None else 0)),
-                   "d2h_bytes_per_step": int(n_real * sgv), "equals_device_result": e2e_equal}}
+                   "d2h_bytes_per_step": int(dev.last_timing()["d2h_bytes"]),
+                   "equals_device_result": e2e_equal}}
     if not skip_cpu:
         o3 = P3.oracle3()
         cores = os.cpu_count() or 1

@@ -125,6 +125,8 @@ void* cache_alloc(int device, size_t bytes);
 // device code-range check of an uploaded grid: the first index holding a code >= nf, n if none (ops.cu)
 size_t first_bad_code(const uint8_t* d, size_t n, int nf, cudaStream_t st, unsigned long long* d_scratch);
 void cache_free(void* p);
+// packed cells (1, 2 or 4 bits each, first cell in the low bits) -> bytes (sim.cu)
+void unpack_cells(uint8_t* d, const uint8_t* s, size_t n, int bits);
 
 // Persistent host worker pool (one per context): run(n, fn) calls fn(i) for
 // every i in [0, n) on the workers and the calling thread, then rethrows the

@@ -485,6 +485,29 @@ void build_mask_tables(int Tc, int OVc, int nch, std::vector<int4>& tab) {
 
 }  // namespace
 
+// n cells packed `bits` per cell (1, 2 or 4; 8 / bits cells per byte, first
+// cell in the low bits) -> one byte per cell at d (the 3D result path).
+void unpack_cells(uint8_t* d, const uint8_t* s, size_t n, int bits) {
+    static uint64_t lut[3][256];
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (int k = 0; k < 3; ++k) {
+            const int b = 1 << k, cpb = 8 / b;
+            for (int v = 0; v < 256; ++v) {
+                uint64_t o = 0;
+                for (int c = 0; c < cpb; ++c) o |= static_cast<uint64_t>((v >> (c * b)) & ((1 << b) - 1)) << (8 * c);
+                lut[k][v] = o;
+            }
+        }
+    });
+    if (bits == 1) unpack_band<8>(d, 0, s, 0, 1, n, lut[0]);
+    else if (bits == 2) unpack_band<4>(d, 0, s, 0, 1, n, lut[1]);
+    else unpack_band<2>(d, 0, s, 0, 1, n, lut[2]);
+}
+
+namespace {
+}  // namespace
+
 // The per-context plan memory (sim.cu run_simulation): after a call, whether
 // its TI/shape deferred tie groups (bulk kernel on/off) or stormed (keep the
 // select + bulk kernels instead of the wave kernel).

@@ -930,6 +930,30 @@ __global__ void finalize3d_kernel(const uint8_t* __restrict__ work, int W0, int 
     }
 }
 
+// Result codes packed `bits` per cell (8 / bits cells per byte, first cell in
+// the low bits) for the device -> host copy; the host unpacks (unpack_cells).
+template <int BITS>
+__global__ void pack3d_kernel(const uint8_t* __restrict__ in, size_t n, uint8_t* __restrict__ out) {
+    constexpr int CPB = 8 / BITS;
+    const size_t nb = (n + CPB - 1) / CPB;
+    for (size_t b = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; b < nb;
+         b += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t c0 = b * CPB;
+        uint32_t v = 0;
+        if (c0 + CPB <= n && (reinterpret_cast<uintptr_t>(in) & 7) == 0) {
+            uint64_t w;  // CPB aligned cells in one load
+            if constexpr (CPB == 8) w = *reinterpret_cast<const uint64_t*>(in + c0);
+            else if constexpr (CPB == 4) w = *reinterpret_cast<const uint32_t*>(in + c0);
+            else w = *reinterpret_cast<const uint16_t*>(in + c0);
+#pragma unroll
+            for (int c = 0; c < CPB; ++c) v |= static_cast<uint32_t>((w >> (8 * c)) & ((1u << BITS) - 1)) << (c * BITS);
+        } else {
+            for (int c = 0; c < CPB && c0 + c < n; ++c) v |= static_cast<uint32_t>(in[c0 + c] & ((1u << BITS) - 1)) << (c * BITS);
+        }
+        out[b] = static_cast<uint8_t>(v);
+    }
+}
+
 // hard-data overwrite with the pre-overwrite mismatch count (simulator.hpp:506-513)
 __global__ void hd3d_kernel(const int32_t* __restrict__ hd, int n_hd, int s0, int s1, int s2, uint8_t* out,
                             int* mism) {
@@ -1209,11 +1233,12 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     const bool use_tc = ctx->opt.tc3d && mode == 0 && S == 1 && !ctx->nccl_comm && Kp >= 1 &&
                         static_cast<size_t>(npos) * kbytes <= (size_t(4) << 30) &&
                         static_cast<size_t>(max_wave) * sld * 4 <= (size_t(2) << 30);
-    // ... and 9-bit counts (mode 1, B^3 <= 512: config 4) as two int8 digits,
+    // ... and 9-bit counts (mode 1 at B = 8: config 4; B <= 4 with more than 4
+    // screen channels keeps the CUDA-core screen) as two int8 digits,
     // three GEMM rows per job (im2col3d_digits_kernel)
     const int kdig = ((2 * g.nscr * tc3 + 127) / 128) * 128;  // K bytes
     const int nsplit = 32;                                     // position chunks per job (keys3d_digits_kernel)
-    const bool use_dig = ctx->opt.tc3d && mode == 1 && g.B * g.B * g.B <= 512 && S == 1 && !ctx->nccl_comm &&
+    const bool use_dig = ctx->opt.tc3d && mode == 1 && g.B == 8 && S == 1 && !ctx->nccl_comm &&
                          Kp >= 1 && static_cast<size_t>(npos) * kdig <= (size_t(4) << 30) &&
                          static_cast<size_t>(max_wave) * 3 * sld * 4 <= (size_t(2) << 30);
 
@@ -1451,13 +1476,56 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     }
     CCW_CUDA(cudaEventRecord(ev1, st));
     if (host_t) fprintf(stderr, "3D host ms: plan %.3f ev0 %.3f launched %.3f\n", t_plan, t_ev0, host_ms());
-    if (h_out) CCW_CUDA(cudaMemcpyAsync(h_out, fin, sgvol * n_real, cudaMemcpyDeviceToHost, st));
+    // Host result, opt-in (option `pack` = 2): codes packed 1 / 2 / 4 bits per
+    // cell on the device, copied in chunks to pinned staging and unpacked into
+    // the caller's buffer by the context's host threads as the chunks land.
+    // Off by default: with a pinned result buffer the plain copy is faster on
+    // the 16-core bench hosts (config 3 e2e 17.2 vs 13.2 G cells/s packed).
+    const size_t out_cells = sgvol * n_real;
+    const int pbits = g.F <= 2 ? 1 : g.F <= 4 ? 2 : 4;
+    const bool packed_out = h_out && ctx->opt.pack >= 2 && g.F <= 16 && out_cells >= (size_t(1) << 16);
+    std::vector<cudaEvent_t> pk_ev;
+    uint8_t* h_pk = nullptr;
+    size_t pk_chunk = 0;  // cells per chunk (a multiple of 64 cells and of whole bytes)
+    if (packed_out) {
+        const int cpb = 8 / pbits;
+        const size_t pbytes = (out_cells + cpb - 1) / cpb;
+        uint8_t* d_pk = ctx->band_stage.as<uint8_t>(pbytes);
+        h_pk = static_cast<uint8_t*>(ctx->h_out_stage.get(pbytes));
+        const unsigned nb = static_cast<unsigned>(std::min<size_t>((pbytes + 255) / 256, 148 * 16));
+        if (pbits == 1) pack3d_kernel<1><<<nb, 256, 0, st>>>(fin, out_cells, d_pk);
+        else if (pbits == 2) pack3d_kernel<2><<<nb, 256, 0, st>>>(fin, out_cells, d_pk);
+        else pack3d_kernel<4><<<nb, 256, 0, st>>>(fin, out_cells, d_pk);
+        CCW_CUDA(cudaGetLastError());
+        ++launches;
+        const int nchunk = 32;
+        pk_chunk = ((out_cells + nchunk - 1) / nchunk + 511) / 512 * 512;
+        for (size_t c0 = 0; c0 < out_cells; c0 += pk_chunk) {
+            const size_t c1 = std::min(out_cells, c0 + pk_chunk);
+            CCW_CUDA(cudaMemcpyAsync(h_pk + c0 / cpb, d_pk + c0 / cpb, (c1 - c0 + cpb - 1) / cpb, cudaMemcpyDeviceToHost, st));
+            cudaEvent_t e;
+            CCW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CCW_CUDA(cudaEventRecord(e, st));
+            pk_ev.push_back(e);
+        }
+    } else if (h_out) {
+        CCW_CUDA(cudaMemcpyAsync(h_out, fin, out_cells, cudaMemcpyDeviceToHost, st));
+    }
     std::vector<int> mism(n_real, 0);
     CCW_CUDA(cudaMemcpyAsync(mism.data(), d_mism, sizeof(int) * n_real, cudaMemcpyDeviceToHost, st));
     std::vector<int32_t> chosen;
     if (trace) {
         chosen.resize(3 * njobs);
         CCW_CUDA(cudaMemcpyAsync(chosen.data(), d_chosen, sizeof(int32_t) * chosen.size(), cudaMemcpyDeviceToHost, st));
+    }
+    if (packed_out) {
+        const int cpb = 8 / pbits;
+        ctx->pool.run(static_cast<int>(pk_ev.size()), [&](int c) {
+            CCW_CUDA(cudaEventSynchronize(pk_ev[c]));
+            const size_t c0 = static_cast<size_t>(c) * pk_chunk, c1 = std::min(out_cells, c0 + pk_chunk);
+            unpack_cells(h_out + c0, h_pk + c0 / cpb, c1 - c0, pbits);
+        });
+        for (auto e : pk_ev) cudaEventDestroy(e);
     }
     CCW_CUDA(cudaStreamSynchronize(st));
     if (trace)  // provenance: TI fine origin of every placement, raster order per realization
@@ -1489,7 +1557,8 @@ void run_simulation3d(ccw_ctx* ctx, ccw_ti3d* ti, const ccw_sim3d_config& cfg, c
     ctx->timing.screened_jobs = static_cast<int64_t>(njobs) - n_real;
     ctx->timing.ccf_variant = use_tc ? 6 : use_dig ? 7 : mode == 0 ? 3 : 4;
     ctx->timing.groups = 1;
-    ctx->timing.d2h_bytes = h_out ? static_cast<int64_t>(sgvol * n_real) : 0;
+    ctx->timing.d2h_bytes = !h_out ? 0 : packed_out ? static_cast<int64_t>((out_cells + 8 / pbits - 1) / (8 / pbits))
+                                                    : static_cast<int64_t>(out_cells);
     (void)ccf_launches;
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     if (diag)

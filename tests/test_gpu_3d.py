@@ -102,6 +102,47 @@ def test_all_corners_and_orders(o3):
         assert np.array_equal(got[r], o["realization"]), r
 
 
+@pytest.mark.parametrize("nf", [2, 4, 7])
+def test_packed_host_result(o3, nf):
+    """Option pack = 2: result codes packed 1 / 2 / 4 bits per cell for the
+    device -> host copy and unpacked by host threads; same realizations."""
+    rng = np.random.default_rng(40 + nf)
+    ti_a = blocky(rng, (40, 36, 44), nf, cell=2)
+    cfg = c3.SimConfig3D(sg=(41, 50, 37), template_size=8, overlap=4, dwt_level=1, candidates=2)
+    seeds = [3, 4, 5]
+    ti = c3.TrainingImage3D(ti_a, nf, 1)
+    dev = cs.default_device()
+    ref, _ = c3.simulate3d(ti, cfg, seeds)
+    with dev.options(pack=2):
+        got, _ = c3.simulate3d(ti, cfg, seeds)
+        assert dev.last_timing()["d2h_bytes"] < ref.size
+    assert np.array_equal(got, ref)
+    o = o3.simulate_one(ti_a, nf, to_o(cfg), None, seed=seeds[1])
+    assert np.array_equal(got[1], o["realization"])
+    with dev.options(tc3d=0):
+        alt, _ = c3.simulate3d(ti, cfg, seeds)
+    assert np.array_equal(alt, ref)
+    ti.close()
+
+
+@pytest.mark.parametrize("nf,J", [(6, 1), (7, 2), (9, 2), (6, 3), (8, 3)])
+def test_many_facies(o3, nf, J):
+    """More than 5 facies (more than 4 screen channels: int32 counts at B <= 4,
+    two-digit tensor screen at B = 8)."""
+    rng = np.random.default_rng(70 + nf + J)
+    B = 1 << J
+    T = 2 * B if J == 3 else 4 * B
+    ti_a = blocky(rng, (5 * T // 2 + B, 3 * T, 2 * T + 2 * B), nf, cell=2)
+    cfg = c3.SimConfig3D(sg=(2 * T + 3, 2 * T, 3 * T - 1), template_size=T, overlap=B, dwt_level=J, candidates=3)
+    ti = c3.TrainingImage3D(ti_a, nf, J)
+    seeds = [11, 12]
+    got, _ = c3.simulate3d(ti, cfg, seeds)
+    for r, s in enumerate(seeds):
+        o = o3.simulate_one(ti_a, nf, to_o(cfg), None, seed=s)
+        assert np.array_equal(got[r], o["realization"]), (nf, J, r)
+    ti.close()
+
+
 def test_ensemble_seeds(o3):
     rng = np.random.default_rng(9)
     ti_a = blocky(rng, (24, 32, 28), 2)
